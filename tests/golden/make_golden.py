@@ -1,0 +1,393 @@
+"""Generate the golden fixtures under tests/golden/ by running the REFERENCE.
+
+Test infrastructure only.  Runs in the build container, where the reference
+package `trackfront` is importable from /root/reference/pkg/src; the GPU box
+has no /root/reference, so the outputs are committed as compressed .npz files
+and the tests read those.
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONPATH=/root/reference/pkg/src \
+        python tests/golden/make_golden.py
+
+Every fixture stores the exact inputs handed to the reference stage functions
+and the reference outputs (numba CPU path, ExecutionEngine("seq")).  Recipes
+follow SURVEY.md §8(d):
+
+* cfg1  rendered 752x480 pinhole pair -> extract_features (ORB, 1200 kps, 8
+        levels) -> match_pinhole_phase1 -> refine_match_phase2 -> reject_outliers
+        (reference stereo.py:77-188, kernels.py:300-428)
+* cfg2  feature-bundle frame (seed 3) + 5k-point local map (rng 7) ->
+        phase1 + matches_from_candidates + reject_outliers, run_phase_a,
+        resolve_conflicts, search_by_projection (plain / rotation-checked /
+        skip-masked), search_local_points (projection.py:118-221,
+        localmap.py:79-122)
+* cfg3  TUM-VI-shaped fisheye pair (seed 5) -> bruteforce_match_kernel,
+        match_fisheye (with the reference's triangulation), fisheye
+        search_local_points on a 3050-point map (rng 9)
+* small known-answer / edge cases: ties,
+        duplicates, empty inputs, single candidates.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+OUT = Path(__file__).resolve().parent
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+if REF_SRC not in sys.path:
+    sys.path.insert(0, REF_SRC)
+
+from trackfront import kernels  # noqa: E402
+from trackfront.cameras import FisheyeCamera, PinholeCamera  # noqa: E402
+from trackfront.descriptors import random_descriptors  # noqa: E402
+from trackfront.engine import ExecutionEngine  # noqa: E402
+from trackfront.extraction import ExtractionConfig, extract_features  # noqa: E402
+from trackfront.geometry import Pose, so3_exp  # noqa: E402
+from trackfront.localmap import LocalMap, search_local_points  # noqa: E402
+from trackfront.mapping import (Frame, FrameGrid, MapPointSoA, NO_POINT)  # noqa: E402
+from trackfront.projection import (ProjectionSearchConfig, resolve_conflicts,  # noqa: E402
+                                   run_phase_a, search_by_projection)
+from trackfront.stereo import (StereoMatchConfig, match_fisheye,  # noqa: E402
+                               match_pinhole_phase1, matches_from_candidates,
+                               refine_match_phase2, reject_outliers)
+from trackfront.synthetic import (SyntheticSceneConfig, _octave_from_distance,  # noqa: E402
+                                  default_pinhole, generate_synthetic)
+
+ENGINE = ExecutionEngine("seq")
+
+
+def feats_dict(prefix: str, f) -> dict:
+    return {
+        f"{prefix}_u": np.ascontiguousarray(f.u, dtype=np.float64),
+        f"{prefix}_v": np.ascontiguousarray(f.v, dtype=np.float64),
+        f"{prefix}_octave": np.ascontiguousarray(f.octave, dtype=np.int32),
+        f"{prefix}_angle": np.ascontiguousarray(f.angle, dtype=np.float64),
+        f"{prefix}_response": np.ascontiguousarray(f.response, dtype=np.float32),
+        f"{prefix}_desc": np.ascontiguousarray(f.descriptors, dtype=np.uint64),
+    }
+
+
+def soa_dict(prefix: str, s: MapPointSoA) -> dict:
+    return {
+        f"{prefix}_positions": np.ascontiguousarray(s.positions),
+        f"{prefix}_descriptors": np.ascontiguousarray(s.descriptors),
+        f"{prefix}_normals": np.ascontiguousarray(s.normals),
+        f"{prefix}_min_d": np.ascontiguousarray(s.min_distances),
+        f"{prefix}_max_d": np.ascontiguousarray(s.max_distances),
+        f"{prefix}_ids": np.ascontiguousarray(s.point_ids),
+    }
+
+
+def matches_dict(prefix: str, m) -> dict:
+    return {
+        f"{prefix}_right_idx": m.right_idx.copy(),
+        f"{prefix}_distance": m.distance.copy(),
+        f"{prefix}_disparity": m.disparity.copy(),
+        f"{prefix}_refined_u": m.refined_u.copy(),
+        f"{prefix}_depth": m.depth.copy(),
+        f"{prefix}_sad": m.sad.copy(),
+    }
+
+
+def corr_dict(prefix: str, c) -> dict:
+    return {
+        f"{prefix}_point_idx": c.point_idx.copy(),
+        f"{prefix}_keypoint_idx": c.keypoint_idx.copy(),
+        f"{prefix}_distance": c.distance.copy(),
+        f"{prefix}_octave": c.octave.copy(),
+    }
+
+
+def flip_bits(desc: np.ndarray, rng: np.random.Generator, nflip: int) -> np.ndarray:
+    out = desc.copy()
+    for i in range(len(out)):
+        bits = rng.choice(256, size=nflip, replace=False)
+        for b in bits:
+            out[i, b >> 6] ^= np.uint64(1) << np.uint64(b & 63)
+    return out
+
+
+def build_local_map(seq, frame_idx: int, cam, total: int, rng, scfg) -> MapPointSoA:
+    """All landmarks visible in the left view plus uniformly drawn others
+    (SURVEY.md §8(d) cfg2 recipe)."""
+    visible = seq.frames[frame_idx].landmark_ids_left
+    others = np.setdiff1d(np.arange(len(seq.landmarks)), visible)
+    extra = total - len(visible)
+    if extra > 0:
+        pick = rng.choice(others, size=min(extra, len(others)), replace=False)
+        ids = np.sort(np.concatenate([visible, pick]))
+    else:
+        ids = np.sort(visible)
+    pose_wc = seq.gt_poses[frame_idx]
+    center = pose_wc.translation
+    pos = seq.landmarks[ids]
+    d = np.linalg.norm(pos - center, axis=1)
+    normals = (pos - center) / d[:, None]
+    octs = _octave_from_distance(d, scfg).astype(np.float64)
+    max_d = d * (scfg.scale ** octs)
+    min_d = max_d / (scfg.scale ** (scfg.levels - 1))
+    desc = flip_bits(seq.landmark_desc[ids], rng, 8)
+    return MapPointSoA(positions=pos.copy(), descriptors=desc, normals=normals,
+                       min_distances=min_d, max_distances=max_d,
+                       point_ids=ids.astype(np.int64))
+
+
+def perturbed_pose(seq, frame_idx: int) -> Pose:
+    gt = seq.pose_cw(frame_idx)
+    rot = so3_exp(np.array([0.002, -0.001, 0.001])) @ gt.rotation
+    return Pose(rot, gt.translation + np.array([0.01, 0.0, -0.01]))
+
+
+def make_frame(fid, left, right, cam, pose, cell_px=48) -> Frame:
+    grid = FrameGrid(left.u, left.v, cam.width, cam.height, cell_px)
+    return Frame(fid, 0.0, left, right, np.full(len(left), -1.0),
+                 np.full(len(left), NO_POINT, dtype=np.int64), pose, grid)
+
+
+def pose_dict(prefix: str, p: Pose) -> dict:
+    return {f"{prefix}_rot": p.rotation.copy(), f"{prefix}_trans": p.translation.copy()}
+
+
+# ---------------------------------------------------------------------------
+
+def gen_hamming() -> None:
+    rng = np.random.default_rng(12345)
+    n = 1024
+    a = random_descriptors(rng, n)
+    b = random_descriptors(rng, n)
+    b[:64] = a[:64]            # distance 0
+    b[64:128] = ~a[64:128]     # distance 256
+    out = np.empty(n, dtype=np.int64)
+    kernels.hamming_pairs_kernel(a, b, out, 0, n)
+    np.savez_compressed(OUT / "hamming.npz", a=a, b=b, out=out)
+
+
+def gen_cfg1() -> dict:
+    scfg = SyntheticSceneConfig(landmark_count=8000, n_frames=2, trajectory="line")
+    seq = generate_synthetic(scfg, seed=11)
+    img_l, img_r = seq.render_pair(0)
+    ecfg = ExtractionConfig()
+    left, pyr_l = extract_features(img_l, ecfg, ENGINE)
+    right, pyr_r = extract_features(img_r, ecfg, ENGINE)
+    cam = seq.cam
+    scfg_st = StereoMatchConfig()
+    scale_pow = ecfg.scale_powers()
+    idx, dist = match_pinhole_phase1(left, right, cam.height, scale_pow, scfg_st, ENGINE)
+    m2 = refine_match_phase2(pyr_l, pyr_r, left, right, idx, dist, cam, scfg_st, ENGINE)
+    pre = matches_dict("p2", m2)
+    m3 = reject_outliers(m2, scfg_st)
+    d = {}
+    d.update(feats_dict("left", left))
+    d.update(feats_dict("right", right))
+    d.update(pyr_l_data=pyr_l.data.copy(), pyr_l_offsets=pyr_l.offsets.copy(),
+             pyr_l_widths=pyr_l.widths.copy(), pyr_l_heights=pyr_l.heights.copy(),
+             pyr_r_data=pyr_r.data.copy(), pyr_r_offsets=pyr_r.offsets.copy(),
+             pyr_r_widths=pyr_r.widths.copy(), pyr_r_heights=pyr_r.heights.copy(),
+             scale_pow=scale_pow, p1_idx=idx.copy(), p1_dist=dist.copy())
+    d.update(pre)
+    d.update(matches_dict("final", m3))
+    np.savez_compressed(OUT / "cfg1_stereo.npz", **d)
+    return {"cfg1": {"n_left": len(left), "n_right": len(right),
+                     "p1_candidates": int((idx >= 0).sum()),
+                     "final_matches": int((m3.right_idx >= 0).sum())}}
+
+
+def gen_cfg2() -> dict:
+    scfg = SyntheticSceneConfig(landmark_count=12000, n_frames=2, trajectory="line",
+                                keypoint_noise_px=0.5)
+    seq = generate_synthetic(scfg, seed=3)
+    cam = seq.cam
+    fr = seq.frames[0]
+    left, right = fr.left, fr.right
+    scfg_st = StereoMatchConfig()
+    scale_pow = scfg.scale ** np.arange(scfg.levels, dtype=np.float64)
+    idx, dist = match_pinhole_phase1(left, right, cam.height, scale_pow, scfg_st, ENGINE)
+    m = matches_from_candidates(idx, dist, left, right, cam, scfg_st)
+    pre = matches_dict("fc", m)
+    m = reject_outliers(m, scfg_st)
+    rng = np.random.default_rng(7)
+    soa = build_local_map(seq, 0, cam, 5000, rng, scfg)
+    pose = perturbed_pose(seq, 0)
+    pcfg = ProjectionSearchConfig()
+    frame = make_frame(0, left, right, cam, pose)
+    kp, kd, ko = run_phase_a(soa, frame, pose, cam, pcfg, scfg.scale, scfg.levels, ENGINE)
+    kp, kd, ko = kp.copy(), kd.copy(), ko.copy()
+    corr = resolve_conflicts(kp, kd, ko)
+    # rotation-checked, prev-frame style search (window 15, u_offset +1)
+    ref_angles = np.random.default_rng(17).uniform(0.0, 2 * math.pi, len(soa))
+    # bias: most points keep their true angle so the histogram is peaked
+    lm_angle = seq.landmark_angle[soa.point_ids]
+    keep = np.random.default_rng(18).uniform(size=len(soa)) < 0.8
+    ref_angles = np.where(keep, lm_angle, ref_angles)
+    corr_rot = search_by_projection(soa, frame, pose, cam, pcfg, scfg.scale, scfg.levels,
+                                    ENGINE, ref_angles=ref_angles, rotation_check=True,
+                                    window_px=pcfg.window_prev_px, u_offset=1.0)
+    # skip-masked variant
+    skip = (np.random.default_rng(19).uniform(size=len(soa)) < 0.3).astype(np.uint8)
+    corr_skip = search_by_projection(soa, frame, pose, cam, pcfg, scfg.scale, scfg.levels,
+                                     ENGINE, skip_mask=skip)
+    # search_local_points on a fresh frame
+    local = LocalMap((0,), soa.point_ids.copy(), soa)
+    frame_a = make_frame(0, left, right, cam, pose)
+    count_a = search_local_points(local, frame_a, cam, pcfg, scfg.scale, scfg.levels, ENGINE)
+    # ... and on a frame with pre-filled slots (skip mask + "only if empty")
+    frame_b = make_frame(0, left, right, cam, pose)
+    prng = np.random.default_rng(23)
+    pre_k = prng.choice(len(left), size=200, replace=False)
+    pre_ids = prng.choice(soa.point_ids, size=200, replace=False)
+    frame_b.slots[pre_k] = pre_ids
+    slots_b_in = frame_b.slots.copy()
+    count_b = search_local_points(local, frame_b, cam, pcfg, scfg.scale, scfg.levels, ENGINE)
+    d = {}
+    d.update(feats_dict("left", left))
+    d.update(feats_dict("right", right))
+    d.update(soa_dict("map", soa))
+    d.update(pose_dict("pose", pose))
+    d.update(scale_pow=scale_pow, p1_idx=idx.copy(), p1_dist=dist.copy())
+    d.update(pre)
+    d.update(matches_dict("final", m))
+    d.update(pa_kp=kp, pa_dist=kd, pa_oct=ko, ref_angles=ref_angles, skip=skip)
+    d.update(corr_dict("corr", corr))
+    d.update(corr_dict("corr_rot", corr_rot))
+    d.update(corr_dict("corr_skip", corr_skip))
+    d.update(slots_a=frame_a.slots.copy(), count_a=np.int64(count_a),
+             slots_b_in=slots_b_in, slots_b=frame_b.slots.copy(), count_b=np.int64(count_b),
+             grid_start=frame.grid.start.copy(), grid_indices=frame.grid.indices.copy())
+    np.savez_compressed(OUT / "cfg2_frame_map.npz", **d)
+    return {"cfg2": {"n_left": len(left), "n_right": len(right), "map": len(soa),
+                     "claims": int((kp >= 0).sum()), "corr": len(corr),
+                     "corr_rot": len(corr_rot), "corr_skip": len(corr_skip),
+                     "count_a": int(count_a), "count_b": int(count_b),
+                     "stereo_matches": int((m.right_idx >= 0).sum())}}
+
+
+def fisheye_cam() -> FisheyeCamera:
+    return FisheyeCamera(fx=190.0, fy=190.0, cx=256.0, cy=256.0,
+                         k1=0.003, k2=-0.002, k3=0.001, k4=-0.0005,
+                         width=512, height=512,
+                         right_extrinsic=Pose(np.eye(3), np.array([-0.1, 0.0, 0.0])))
+
+
+def gen_cfg3() -> dict:
+    cam = fisheye_cam()
+    scfg = SyntheticSceneConfig(landmark_count=3050, n_frames=2, trajectory="line",
+                                keypoint_noise_px=0.3)
+    seq = generate_synthetic(scfg, seed=5, cam=cam)
+    fr = seq.frames[0]
+    left, right = fr.left, fr.right
+    scfg_st = StereoMatchConfig()
+    idx = np.empty(len(left), dtype=np.int64)
+    dist = np.empty(len(left), dtype=np.int64)
+    kernels.bruteforce_match_kernel(left.descriptors, right.descriptors, scfg_st.t_match,
+                                    scfg_st.ratio, 0, len(left), idx, dist)
+    lidx, ridx, pts, dists = match_fisheye(left, right, cam, scfg_st, ENGINE)
+    rng = np.random.default_rng(9)
+    soa = build_local_map(seq, 0, cam, 3050, rng, scfg)
+    pose = perturbed_pose(seq, 0)
+    pcfg = ProjectionSearchConfig()
+    frame = make_frame(0, left, right, cam, pose)
+    kp, kd, ko = run_phase_a(soa, frame, pose, cam, pcfg, scfg.scale, scfg.levels, ENGINE)
+    kp, kd, ko = kp.copy(), kd.copy(), ko.copy()
+    corr = resolve_conflicts(kp, kd, ko)
+    local = LocalMap((0,), soa.point_ids.copy(), soa)
+    frame_a = make_frame(0, left, right, cam, pose)
+    count_a = search_local_points(local, frame_a, cam, pcfg, scfg.scale, scfg.levels, ENGINE)
+    d = {}
+    d.update(feats_dict("left", left))
+    d.update(feats_dict("right", right))
+    d.update(soa_dict("map", soa))
+    d.update(pose_dict("pose", pose))
+    d.update(bf_idx=idx, bf_dist=dist, mf_lidx=lidx, mf_ridx=ridx, mf_pts=pts, mf_dists=dists)
+    d.update(pa_kp=kp, pa_dist=kd, pa_oct=ko)
+    d.update(corr_dict("corr", corr))
+    d.update(slots_a=frame_a.slots.copy(), count_a=np.int64(count_a))
+    np.savez_compressed(OUT / "cfg3_fisheye.npz", **d)
+    return {"cfg3": {"n_left": len(left), "n_right": len(right), "map": len(soa),
+                     "bf_accepted": int((idx >= 0).sum()), "mf_accepted": len(lidx),
+                     "claims": int((kp >= 0).sum()), "corr": len(corr),
+                     "count_a": int(count_a)}}
+
+
+def gen_edge() -> dict:
+    """Tie / multiplicity / duplicate cases run through the reference kernels."""
+    rng = np.random.default_rng(99)
+    out = {}
+    # brute force with heavy duplication: right set has repeated descriptors
+    base = random_descriptors(rng, 40)
+    left = base[rng.integers(0, 40, size=300)]
+    right = base[rng.integers(0, 40, size=257)]
+    right[::7] = ~right[::7]
+    idx = np.empty(len(left), dtype=np.int64)
+    dist = np.empty(len(left), dtype=np.int64)
+    kernels.bruteforce_match_kernel(left, right, 100, 0.8, 0, len(left), idx, dist)
+    out.update(dup_left=left, dup_right=right, dup_idx=idx, dup_dist=dist)
+    # single right candidate (second stays at 100000)
+    one_r = base[:1]
+    idx1 = np.empty(len(left), dtype=np.int64)
+    dist1 = np.empty(len(left), dtype=np.int64)
+    kernels.bruteforce_match_kernel(left, one_r, 100, 0.8, 0, len(left), idx1, dist1)
+    out.update(one_right=one_r, one_idx=idx1, one_dist=dist1)
+    # phase 1 with coarse rows, many equal distances (low-entropy descriptors)
+    n = 500
+    small = random_descriptors(rng, 6)
+    lu = rng.uniform(50, 700, n)
+    lv = np.round(rng.uniform(0, 479, n) * 2) / 2  # half-integer rows: rounding ties
+    ru = lu - rng.uniform(-5, 60, n)
+    rv = lv + rng.normal(0, 1.0, n)
+    rv[::5] = lv[::5]
+    loct = rng.integers(0, 8, n).astype(np.int32)
+    roct = np.clip(loct + rng.integers(-2, 3, n), 0, 7).astype(np.int32)
+    ld = small[rng.integers(0, 6, n)]
+    rd = small[rng.integers(0, 6, n)]
+    from trackfront.mapping import FeatureSet
+    lf = FeatureSet(lu, lv, loct, np.zeros(n), np.zeros(n, np.float32), ld)
+    rf = FeatureSet(ru, rv, roct, np.zeros(n), np.zeros(n, np.float32), rd)
+    sp = 1.2 ** np.arange(8, dtype=np.float64)
+    p_idx, p_dist = match_pinhole_phase1(lf, rf, 480, sp, StereoMatchConfig(), ENGINE)
+    out.update(tie_lu=lu, tie_lv=lv, tie_ru=ru, tie_rv=rv, tie_loct=loct, tie_roct=roct,
+               tie_ld=ld, tie_rd=rd, tie_idx=p_idx.copy(), tie_dist=p_dist.copy())
+    # reject_outliers median on even / odd counts
+    from trackfront.stereo import StereoMatches
+    sads = []
+    for cnt in (1, 2, 7, 8, 101, 1000):
+        s = rng.integers(0, 5000, cnt).astype(np.int64)
+        s[: max(1, cnt // 10)] *= 7
+        k = np.arange(cnt)
+        mm = StereoMatches(right_idx=k.copy(), distance=np.full(cnt, 5, np.int64),
+                           disparity=np.full(cnt, 3.0), refined_u=np.full(cnt, 1.0),
+                           depth=np.full(cnt, 2.0), sad=s.copy())
+        mm.right_idx[::9] = -1
+        rin = mm.right_idx.copy()
+        reject_outliers(mm, StereoMatchConfig())
+        out[f"med{cnt}_sad"] = s
+        out[f"med{cnt}_rin"] = rin
+        out[f"med{cnt}_rout"] = mm.right_idx.copy()
+        out[f"med{cnt}_sadout"] = mm.sad.copy()
+        sads.append(cnt)
+    np.savez_compressed(OUT / "edge_cases.npz", **out)
+    return {"edge": {"dup_accepted": int((idx >= 0).sum()), "tie_matched": int((p_idx >= 0).sum()),
+                     "median_counts": sads}}
+
+
+def main() -> None:
+    kernels.warmup()
+    summary = {}
+    gen_hamming()
+    summary.update(gen_edge())
+    summary.update(gen_cfg2())
+    summary.update(gen_cfg3())
+    summary.update(gen_cfg1())
+    summary["generator"] = "tests/golden/make_golden.py (reference trackfront, seq engine)"
+    (OUT / "summary.json").write_text(json.dumps(summary, indent=1))
+    print(json.dumps(summary, indent=1))
+
+
+if __name__ == "__main__":
+    main()
