@@ -1,0 +1,248 @@
+/*
+ * fasttrack_b200.h -- C ABI of the B200 tracking hot path.
+ *
+ * One entry point per reference stage function (reference = trackfront,
+ * pkg/src/trackfront).  Every entry:
+ *   - takes DEVICE pointers, plain sizes and a POD parameter struct,
+ *   - enqueues kernels on `stream` (a cudaStream_t) and returns without
+ *     synchronising,
+ *   - allocates nothing: scratch lives in a caller-provided ft_workspace
+ *     (size from ft_workspace_bytes(), initialised once by ft_workspace_init();
+ *     launches may use any F / capacities up to the workspace's),
+ *   - returns 0 on success, a negative FT_E* code for argument errors, or a
+ *     positive cudaError_t from the launch.
+ *
+ * Batched layout: every entry processes F independent frames ("frame
+ * streams") in one launch.  Frame f's items live at [f * cap, f * cap + n_f)
+ * of each array; the per-frame counts n_f are read from DEVICE memory, so a
+ * CUDA graph captured once replays every frame with new counts.
+ *
+ * Descriptors are 256-bit ORB strings, 32 bytes per row, bit b in 64-bit word
+ * b >> 6 at bit b & 63 (reference descriptors.py:7-9,23-30); the kernels read
+ * them as 8 x u32 with two 16-byte vector loads, so rows must be 16-B aligned.
+ *
+ * Reference interface each entry replaces:
+ *   ft_hamming_pairs        kernels.py:48-51        hamming_pairs_kernel
+ *   ft_stereo_pinhole       stereo.py:77-188        match_pinhole_phase1 ->
+ *                                                   refine_match_phase2 |
+ *                                                   matches_from_candidates ->
+ *                                                   reject_outliers
+ *                           (also tracker.py:415-427 _run_stereo, pinhole branch)
+ *   ft_stereo_fisheye_bf    stereo.py:238-244       bruteforce_match_kernel as
+ *                                                   launched by match_fisheye
+ *   ft_project_search       projection.py:118-221   run_phase_a ->
+ *                                                   resolve_conflicts ->
+ *                                                   rotation_consistency_filter
+ *                           localmap.py:79-122      search_local_points (skip mask,
+ *                                                   slot write, filled count)
+ */
+#ifndef FASTTRACK_B200_H
+#define FASTTRACK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FT_ABI_VERSION 1
+#define FT_MAX_LEVELS 16
+
+enum {
+    FT_OK = 0,
+    FT_E_NULL = -1,       /* required pointer is NULL */
+    FT_E_RANGE = -2,      /* size / capacity / level count out of range */
+    FT_E_WORKSPACE = -3,  /* workspace too small */
+    FT_E_CONFIG = -4      /* invalid parameter value */
+};
+
+typedef void *ft_stream_t; /* cudaStream_t */
+
+/* Device scratch shared by all entries.  Sections are disjoint, so the
+ * stereo and projection entries may run concurrently on two streams. */
+typedef struct {
+    void *base;
+    size_t bytes;
+    int32_t n_frames;    /* max frames per launch */
+    int32_t cap_left;    /* max keypoints per frame (left or right) */
+    int32_t cap_points;  /* max map points per frame */
+} ft_workspace;
+
+/* Keypoints of one image side, F frames at stride `cap`
+ * (reference mapping.py:18-65 FeatureSet). */
+typedef struct {
+    const double *u;        /* [F*cap] level-0 column */
+    const double *v;        /* [F*cap] level-0 row */
+    const int32_t *octave;  /* [F*cap] pyramid level */
+    const double *angle;    /* [F*cap] orientation (rad); may be NULL unless
+                               the rotation check runs */
+    const uint64_t *desc;   /* [F*cap][4] */
+    const int32_t *count;   /* DEVICE [F] keypoints per frame */
+    int32_t cap;            /* per-frame stride (>= every count) */
+} ft_keypoints;
+
+/* Flat u8 image pyramid, F frames at stride `frame_bytes`
+ * (reference extraction.py:67-94 ImagePyramid).  Level geometry is shared by
+ * all frames and passed by value. */
+typedef struct {
+    const uint8_t *data;
+    int64_t frame_bytes;
+    int32_t n_levels;
+    int64_t offsets[FT_MAX_LEVELS];
+    int32_t widths[FT_MAX_LEVELS];
+    int32_t heights[FT_MAX_LEVELS];
+} ft_pyramid;
+
+/* reference stereo.py:22-42 StereoMatchConfig + camera terms used. */
+typedef struct {
+    int32_t t_match;
+    double band_factor;
+    double min_disparity;
+    double max_disparity;
+    int32_t half_window;
+    int32_t half_slide;
+    double outlier_multiplier;
+    double ratio;               /* fisheye ratio test */
+    double baseline_times_fx;   /* depth = bf / disparity (stereo.py:131-132) */
+    int32_t height;             /* image rows: row-bucket count (stereo.py:88) */
+    int32_t n_levels;
+    double scale_pow[FT_MAX_LEVELS]; /* scale ** arange(levels), host-computed */
+} ft_stereo_params;
+
+/* ft_stereo_pinhole mode bits */
+#define FT_STEREO_PHASE1 0x1      /* run phase 1 (else read cand_idx/cand_dist) */
+#define FT_STEREO_REFINE 0x2      /* phase 2 SAD refinement (needs pyramids) */
+#define FT_STEREO_FROM_CAND 0x4   /* matches_from_candidates (no images) */
+#define FT_STEREO_REJECT 0x8      /* reject_outliers (median SAD) */
+
+/* Per-left-keypoint outputs at stride cap_left
+ * (reference stereo.py:45-64 StereoMatches). */
+typedef struct {
+    int64_t *cand_idx;   /* phase-1 output / input when !PHASE1 */
+    int64_t *cand_dist;
+    int64_t *right_idx;  /* may be NULL in phase-1-only mode */
+    int64_t *distance;
+    double *disparity;
+    double *refined_u;
+    double *depth;
+    int64_t *sad;
+    int32_t *n_matched;  /* DEVICE [F] matches after rejection; may be NULL */
+} ft_stereo_out;
+
+/* Map points of F local maps at stride `cap`
+ * (reference mapping.py:163-201 MapPointSoA). */
+typedef struct {
+    const double *positions;  /* [F*cap][3] */
+    const double *normals;    /* [F*cap][3] */
+    const double *min_dist;   /* [F*cap] */
+    const double *max_dist;   /* [F*cap] */
+    const uint64_t *desc;     /* [F*cap][4] */
+    const int64_t *point_ids; /* [F*cap], ascending per frame (LocalMap contract) */
+    const int32_t *count;     /* DEVICE [F] */
+    int32_t cap;
+} ft_map_points;
+
+/* reference projection.py:26-45 ProjectionSearchConfig + camera + grid. */
+typedef struct {
+    int32_t cam_kind;      /* 0 pinhole, 1 Kannala-Brandt fisheye */
+    double fx, fy, cx, cy, k1, k2, k3, k4;
+    double width, height;
+    int32_t cell_px;       /* FrameGrid cell (mapping.py:15) */
+    int32_t grid_nx, grid_ny;
+    int32_t n_levels;
+    double scale_pow[FT_MAX_LEVELS];
+    double inv_log_scale;  /* 1.0 / log(scale), host-computed (projection.py:155) */
+    double window_px;
+    int32_t t_proj;
+    double ratio;
+    double view_cos_min;
+    double u_offset;
+    int32_t histogram_bins;
+    int32_t histogram_keep;
+} ft_project_params;
+
+/* ft_project_search mode bits */
+#define FT_PROJ_RESOLVE 0x1      /* resolve_conflicts -> correspondences */
+#define FT_PROJ_ROTATION 0x2     /* rotation_consistency_filter (needs angles) */
+#define FT_PROJ_SKIP_SLOTS 0x4   /* skip points whose id is already slotted */
+#define FT_PROJ_WRITE_SLOTS 0x8  /* search_local_points slot write + count */
+
+typedef struct {
+    const double *rot;          /* DEVICE [F][9] row-major world->camera R */
+    const double *trans;        /* DEVICE [F][3] */
+    const uint8_t *skip;        /* [F*cap_points] explicit skip mask; may be NULL */
+    const double *ref_angles;   /* [F*cap_points] for the rotation check; may be NULL */
+    int64_t *slots;             /* [F*cap_kp] frame slots (read for SKIP_SLOTS,
+                                   updated by WRITE_SLOTS) */
+} ft_project_io;
+
+typedef struct {
+    int64_t *out_kp;     /* [F*cap_points] phase A (run_phase_a) */
+    int64_t *out_dist;
+    int64_t *out_oct;
+    int64_t *corr_point; /* [F*cap_points] resolved correspondences, point order */
+    int64_t *corr_kp;
+    int64_t *corr_dist;
+    int64_t *corr_oct;
+    int32_t *corr_count; /* DEVICE [F] */
+    int32_t *slot_count; /* DEVICE [F] filled slots after WRITE_SLOTS */
+} ft_project_out;
+
+/* --- entry points ------------------------------------------------------- */
+
+int ft_abi_version(void);
+const char *ft_status_string(int status);
+
+/* Bytes of device workspace for F frames of the given capacities. */
+size_t ft_workspace_bytes(int32_t n_frames, int32_t cap_left, int32_t cap_points);
+
+/* Initialise a workspace once after allocation (counters to 0, claims to
+ * ~0); every kernel restores that state on exit. */
+int ft_workspace_init(const ft_workspace *ws, ft_stream_t stream);
+
+/* kernels.py:48-51: out[i] = popcount(a[i] ^ b[i]) over 256 bits. */
+int ft_hamming_pairs(const uint64_t *a, const uint64_t *b, int64_t n, int64_t *out,
+                     ft_stream_t stream);
+
+/* stereo.py:77-188 (pinhole). */
+int ft_stereo_pinhole(int32_t n_frames, const ft_keypoints *left, const ft_keypoints *right,
+                      const ft_pyramid *left_pyr, const ft_pyramid *right_pyr,
+                      const ft_stereo_params *params, int32_t mode, const ft_stereo_out *out,
+                      const ft_workspace *ws, ft_stream_t stream);
+
+/* stereo.py:238-244 -> kernels.py:434-464 (fisheye brute force + ratio test). */
+int ft_stereo_fisheye_bf(int32_t n_frames, const ft_keypoints *left, const ft_keypoints *right,
+                         int32_t t_match, double ratio, int64_t *out_idx, int64_t *out_dist,
+                         const ft_workspace *ws, ft_stream_t stream);
+
+/* projection.py:118-221 + localmap.py:79-122. */
+int ft_project_search(int32_t n_frames, const ft_map_points *points, const ft_keypoints *frame,
+                      const ft_project_params *params, const ft_project_io *io, int32_t mode,
+                      const ft_project_out *out, const ft_workspace *ws, ft_stream_t stream);
+
+/* projection.py:161-178 resolve_conflicts on caller-held phase-A arrays
+ * (one frame): correspondences in point order into out->corr_* and
+ * out->corr_count[0].  n_kp <= ws->cap_left. */
+int ft_resolve_conflicts(int32_t n_points, const int64_t *out_kp, const int64_t *out_dist,
+                         const int64_t *out_oct, int32_t n_kp, const ft_project_out *out,
+                         const ft_workspace *ws, ft_stream_t stream);
+
+/* projection.py:181-200 rotation_consistency_filter, in place on m
+ * correspondences (one frame); kept count into *count. */
+int ft_rotation_filter(int32_t m, int64_t *corr_point, int64_t *corr_kp, int64_t *corr_dist,
+                       int64_t *corr_oct, const double *ref_angles, const double *kp_angles,
+                       int32_t histogram_bins, int32_t histogram_keep, int32_t *count,
+                       ft_stream_t stream);
+
+/* Integer-pipe microbenchmark used for the roofline denominator: each thread
+ * runs `iters` iterations of 8 independent XOR+POPC chains.  Writes a
+ * checksum to *sink so nothing is dead code. */
+int ft_bench_popc(int32_t blocks, int32_t threads, int32_t iters, uint32_t *sink,
+                  ft_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTTRACK_B200_H */

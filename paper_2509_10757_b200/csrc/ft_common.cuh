@@ -1,0 +1,178 @@
+// ft_common.cuh -- shared device helpers for the sm_100a tracking kernels.
+//
+// Numerics: these translation units are compiled with -fmad=false so every
+// double expression rounds exactly like the numba reference (no FMA
+// contraction; numba leaves fastmath off, reference kernels.py:1-7).  Keep the
+// reference's left-to-right evaluation order when editing fp64 expressions.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fasttrack_b200.h"
+
+#define FT_DEV __device__ __forceinline__
+
+namespace ft {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// 256-bit descriptor held in registers as 8 x u32 (two 16-B loads).
+struct Desc {
+    uint4 lo, hi;
+};
+
+FT_DEV Desc load_desc(const uint64_t *base, int64_t row) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(base + 4 * row);
+    Desc d;
+    d.lo = __ldg(p);
+    d.hi = __ldg(p + 1);
+    return d;
+}
+
+// reference kernels.py:31-45 (_popcount64 x 4): XOR + POPC over 8 words.
+FT_DEV uint32_t hamming(const Desc &a, const Desc &b) {
+    return __popc(a.lo.x ^ b.lo.x) + __popc(a.lo.y ^ b.lo.y) + __popc(a.lo.z ^ b.lo.z) +
+           __popc(a.lo.w ^ b.lo.w) + __popc(a.hi.x ^ b.hi.x) + __popc(a.hi.y ^ b.hi.y) +
+           __popc(a.hi.z ^ b.hi.z) + __popc(a.hi.w ^ b.hi.w);
+}
+
+// numba int(round(x)) and np.round are round-half-to-even.
+FT_DEV long long round_half_even(double x) { return __double2ll_rn(x); }
+
+FT_DEV int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
+
+// Best / second-best-with-multiplicity state of the ratio-tested scans
+// (kernels.py:444-464 and 552-579).  key = (dist << 16) | index, so the
+// unsigned minimum is the lexicographic (dist, index) minimum -- the lowest
+// index among the best distances, which both reference scans produce.
+// `second` is the second order statistic of the distance multiset.
+constexpr uint32_t NO_KEY = 0xffffffffu;
+constexpr uint32_t NO_SECOND = 100000u;  // kernels.py:446,553
+
+struct Best2 {
+    uint32_t key;
+    uint32_t second;
+};
+
+FT_DEV uint32_t key_dist(uint32_t key) { return key == NO_KEY ? NO_SECOND : (key >> 16); }
+
+FT_DEV void best2_init(Best2 &b) {
+    b.key = NO_KEY;
+    b.second = NO_SECOND;
+}
+
+FT_DEV void best2_push(Best2 &b, uint32_t d, uint32_t j) {
+    const uint32_t k = (d << 16) | j;
+    if (k < b.key) {
+        b.second = min(b.second, key_dist(b.key));
+        b.key = k;
+    } else {
+        b.second = min(b.second, d);
+    }
+}
+
+// Merge two disjoint candidate multisets.
+FT_DEV void best2_merge(Best2 &b, uint32_t okey, uint32_t osec) {
+    const uint32_t lo = min(b.key, okey), hi = max(b.key, okey);
+    b.second = min(min(b.second, osec), key_dist(hi));
+    b.key = lo;
+}
+
+FT_DEV void best2_warp_reduce(Best2 &b) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const uint32_t ok = __shfl_xor_sync(FULL, b.key, s);
+        const uint32_t os = __shfl_xor_sync(FULL, b.second, s);
+        best2_merge(b, ok, os);
+    }
+}
+
+// Reference ratio test: bj >= 0 and best <= t and float(best) <= ratio * float(second).
+FT_DEV bool ratio_accept(const Best2 &b, int t_max, double ratio) {
+    if (b.key == NO_KEY) return false;
+    const uint32_t best = b.key >> 16;
+    return (int)best <= t_max && (double)best <= ratio * (double)b.second;
+}
+
+// Block-wide exclusive scan of one int per thread.  `tmp` holds >= NT/32
+// ints.  Contains __syncthreads(); call from every thread of the block.
+template <int NT>
+__device__ int block_exclusive_scan(int v, int *tmp, int &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        const int y = __shfl_up_sync(FULL, x, s);
+        if (lane >= s) x += y;
+    }
+    if (lane == 31) tmp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int w = lane < NT / 32 ? tmp[lane] : 0;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+            const int y = __shfl_up_sync(FULL, w, s);
+            if (lane >= s) w += y;
+        }
+        if (lane < NT / 32) tmp[lane] = w;
+    }
+    __syncthreads();
+    const int base = wid > 0 ? tmp[wid - 1] : 0;
+    total = tmp[NT / 32 - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+// Counting-sort CSR of n items over nbins bins, built by one block in shared
+// memory: start[nbins + 1], cursor[nbins], items[n].  bin_of(j) must be
+// deterministic.  Order inside a bin is arbitrary (atomics); every consumer
+// in this library reduces order-independently.
+template <int NT, typename BinFn>
+__device__ void block_csr(int n, int nbins, BinFn bin_of, int *start, int *cursor,
+                          uint16_t *items, int *scan_tmp) {
+    for (int b = threadIdx.x; b < nbins; b += NT) cursor[b] = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += NT) atomicAdd(&cursor[bin_of(j)], 1);
+    __syncthreads();
+    const int per = (nbins + NT - 1) / NT;
+    const int b0 = threadIdx.x * per;
+    int local = 0;
+    for (int i = 0; i < per; ++i)
+        if (b0 + i < nbins) local += cursor[b0 + i];
+    int total;
+    int run = block_exclusive_scan<NT>(local, scan_tmp, total);
+    for (int i = 0; i < per; ++i)
+        if (b0 + i < nbins) {
+            const int c = cursor[b0 + i];
+            start[b0 + i] = run;
+            cursor[b0 + i] = run;
+            run += c;
+        }
+    if (threadIdx.x == 0) start[nbins] = total;
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += NT) {
+        const int pos = atomicAdd(&cursor[bin_of(j)], 1);
+        items[pos] = (uint16_t)j;
+    }
+    __syncthreads();
+}
+
+// "Last block done": true in exactly one block of the group, after every
+// block has passed here with its global writes fenced.  The winner resets the
+// counter for the next launch.
+__device__ inline bool last_block_ticket(unsigned *counter, unsigned n_blocks, int *smem_flag) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned t = atomicAdd(counter, 1u);
+        *smem_flag = (t == n_blocks - 1);
+        if (t == n_blocks - 1) *counter = 0;
+    }
+    __syncthreads();
+    const bool last = *smem_flag != 0;
+    if (last) __threadfence();
+    return last;
+}
+
+}  // namespace ft

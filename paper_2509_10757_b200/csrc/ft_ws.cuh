@@ -1,0 +1,92 @@
+// ft_ws.cuh -- workspace layout shared by the C-ABI entries (host side).
+//
+// Sections (disjoint; offsets depend only on the workspace's own F / caps,
+// so any launch with F <= ws.n_frames and capacities <= the workspace's may
+// use it, and the stereo and projection entries may run concurrently):
+//   stereo   counters u32[F]
+//   fisheye  counters u32[F * tiles(cap_left)] | partials uint2[fisheye_entries]
+//   project  counters u32[F] | blk_count i32[F * nb(cap_points)]
+//            | claims u64[F * cap_left] | blk_list uint2[F * cap_points]
+// Counters start at 0 and claims at ~0; kernels restore both before exit.
+#pragma once
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/fasttrack_b200.h"
+
+namespace ft {
+
+constexpr size_t WS_ALIGN = 256;
+constexpr int WS_BF_TL = 128;   // fisheye left tile (ft_fisheye.cu)
+constexpr int WS_PPB = 256;     // map points per block (ft_project.cu)
+constexpr int WS_SM_HINT = 148;
+
+inline size_t ws_align(size_t x) { return (x + WS_ALIGN - 1) & ~(WS_ALIGN - 1); }
+inline int ws_tiles(int cap_left) { return (cap_left + WS_BF_TL - 1) / WS_BF_TL; }
+inline int ws_nb(int cap_points) { return (cap_points + WS_PPB - 1) / WS_PPB; }
+
+// Right-set splits of the fisheye all-pairs kernel: about 4 blocks per SM.
+inline int fisheye_splits(int F, int cap_left, int cap_right) {
+    const int tiles = ws_tiles(cap_left);
+    int s = (4 * WS_SM_HINT + tiles * F - 1) / (tiles * F);
+    const int max_s = (cap_right + 63) / 64;
+    if (s > max_s) s = max_s;
+    return s < 1 ? 1 : s;
+}
+
+inline size_t fisheye_entries(int F, int cap_left) {
+    size_t e = (size_t)F * cap_left * fisheye_splits(F, cap_left, 65535);
+    const size_t floor_e = (size_t)F * cap_left * 8;
+    return e > floor_e ? e : floor_e;
+}
+
+struct WsLayout {
+    size_t stereo_counters, fisheye_counters, fisheye_partials, proj_counters, proj_blk_count,
+        proj_claims, proj_blk_list, total;
+    size_t fisheye_partial_entries;
+};
+
+inline WsLayout ws_layout(int F, int cap_left, int cap_points) {
+    WsLayout L;
+    size_t o = 0;
+    L.stereo_counters = o;
+    o += ws_align((size_t)F * 4);
+    L.fisheye_counters = o;
+    o += ws_align((size_t)F * ws_tiles(cap_left) * 4);
+    L.fisheye_partials = o;
+    L.fisheye_partial_entries = fisheye_entries(F, cap_left);
+    o += ws_align(L.fisheye_partial_entries * 8);
+    L.proj_counters = o;
+    o += ws_align((size_t)F * 4);
+    L.proj_blk_count = o;
+    o += ws_align((size_t)F * ws_nb(cap_points) * 4);
+    L.proj_claims = o;
+    o += ws_align((size_t)F * cap_left * 8);
+    L.proj_blk_list = o;
+    o += ws_align((size_t)F * cap_points * 8);
+    L.total = o;
+    return L;
+}
+
+// Validates a workspace against a launch; returns FT_OK or an FT_E code.
+inline int ws_check(const ft_workspace *ws, int F, int cap_left, int cap_points) {
+    if (!ws || !ws->base) return FT_E_NULL;
+    if (ws->n_frames < 1 || ws->cap_left < 1 || ws->cap_points < 1) return FT_E_RANGE;
+    if (F > ws->n_frames || cap_left > ws->cap_left || cap_points > ws->cap_points)
+        return FT_E_WORKSPACE;
+    if (ws->bytes < ws_layout(ws->n_frames, ws->cap_left, ws->cap_points).total)
+        return FT_E_WORKSPACE;
+    return FT_OK;
+}
+
+template <typename T>
+inline T *ws_ptr(const ft_workspace *ws, size_t off) {
+    return reinterpret_cast<T *>(static_cast<char *>(ws->base) + off);
+}
+
+inline WsLayout ws_layout(const ft_workspace *ws) {
+    return ws_layout(ws->n_frames, ws->cap_left, ws->cap_points);
+}
+
+}  // namespace ft

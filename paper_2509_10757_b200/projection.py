@@ -1,0 +1,338 @@
+"""Search by projection drop-in: the reference's stage functions on B200.
+
+Signatures, argument meaning, outputs and error behaviour follow the
+reference module ``trackfront.projection`` (pkg/src/trackfront/projection.py).
+Phase A (projection + windowed descriptor search), phase B (conflict
+resolution) and phase C (rotation histogram) run fused in
+``ft_project_search`` (csrc/ft_project.cu); ``run_phase_a`` /
+``resolve_conflicts`` / ``rotation_consistency_filter`` are also callable on
+their own through their own C-ABI entries.  ``engine`` / ``pool`` are accepted
+for signature compatibility and ignored.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _lib
+from .runtime import (Layout, add_keypoints, keypoints_struct, project_params, put_keypoints,
+                      runtime)
+from .types import Correspondences, ProjectionSearchConfig, NO_POINT
+
+__all__ = ["ProjectionSearchConfig", "Correspondences", "predict_scale", "frustum_and_cone_check",
+           "run_phase_a", "resolve_conflicts", "rotation_consistency_filter",
+           "search_by_projection", "search_prev_frame"]
+
+
+def predict_scale(distance: float, max_distance: float, scale: float, levels: int) -> int:
+    """Scalar twin of the kernel's level prediction (reference projection.py:70-77)."""
+    r = math.log(max_distance / distance) / math.log(scale)
+    return int(min(max(math.ceil(r - 1e-9), 0), levels - 1))
+
+
+def frustum_and_cone_check(position, normal, min_distance, max_distance, pose, cam,
+                           cfg: ProjectionSearchConfig, scale: float, levels: int):
+    """Scalar visibility gate for one map point (reference projection.py:80-107);
+    host helper for callers, the kernels inline the same test."""
+    position = np.asarray(position, dtype=np.float64)
+    p = pose.rotation @ position + pose.translation
+    if p[2] <= 1e-6:
+        return None
+    x, y, z = float(p[0]), float(p[1]), float(p[2])
+    if hasattr(cam, "k1"):
+        r = math.hypot(x, y)
+        if r < 1e-12:
+            u, v = cam.cx, cam.cy
+        else:
+            th = math.atan2(r, z)
+            t2 = th * th
+            d = th * (1.0 + t2 * (cam.k1 + t2 * (cam.k2 + t2 * (cam.k3 + t2 * cam.k4))))
+            u, v = cam.fx * d * x / r + cam.cx, cam.fy * d * y / r + cam.cy
+    else:
+        u, v = cam.fx * x / z + cam.cx, cam.fy * y / z + cam.cy
+    if not (0.0 <= u < cam.width and 0.0 <= v < cam.height):
+        return None
+    dist = float(np.linalg.norm(p))
+    if dist < min_distance or dist > max_distance:
+        return None
+    center = -pose.rotation.T @ pose.translation
+    cosang = float((position - center) @ np.asarray(normal)) / dist
+    if cosang < cfg.view_cos_min:
+        return None
+    return predict_scale(dist, max_distance, scale, levels), u, v, cosang
+
+
+# ---------------------------------------------------------------------------
+
+def _grid_geometry(frame, cam) -> tuple[int, int, int]:
+    g = getattr(frame, "grid", None)
+    if g is not None:
+        return int(g.cell_px), int(g.nx), int(g.ny)
+    cell = 48
+    return cell, max(1, (int(cam.width) + cell - 1) // cell), max(1, (int(cam.height) + cell - 1) // cell)
+
+
+def _add_points(lay: Layout, cap: int) -> None:
+    lay.add("P_n", 4)
+    lay.add("P_pos", 24 * cap)
+    lay.add("P_nrm", 24 * cap)
+    lay.add("P_mind", 8 * cap)
+    lay.add("P_maxd", 8 * cap)
+    lay.add("P_desc", 32 * cap)
+    lay.add("P_ids", 8 * cap)
+
+
+def _put_points(rt, lay: Layout, pts) -> int:
+    m = len(pts.point_ids)
+    rt.put(lay, "P_n", np.array([m], dtype=np.int32), np.int32)
+    if m:
+        rt.put(lay, "P_pos", np.asarray(pts.positions).reshape(m, 3), np.float64)
+        rt.put(lay, "P_nrm", np.asarray(pts.normals).reshape(m, 3), np.float64)
+        rt.put(lay, "P_mind", pts.min_distances, np.float64)
+        rt.put(lay, "P_maxd", pts.max_distances, np.float64)
+        rt.put(lay, "P_desc", np.asarray(pts.descriptors).reshape(m, 4), np.uint64)
+        rt.put(lay, "P_ids", pts.point_ids, np.int64)
+    return m
+
+
+def _points_struct(rt, lay: Layout, cap: int) -> _lib.FtMapPoints:
+    s = _lib.FtMapPoints()
+    s.positions, s.normals = rt.ptr(lay, "P_pos"), rt.ptr(lay, "P_nrm")
+    s.min_dist, s.max_dist = rt.ptr(lay, "P_mind"), rt.ptr(lay, "P_maxd")
+    s.desc, s.point_ids, s.count = rt.ptr(lay, "P_desc"), rt.ptr(lay, "P_ids"), rt.ptr(lay, "P_n")
+    s.cap = cap
+    return s
+
+
+def _out_struct(rt, lay: Layout, phase_a: bool) -> _lib.FtProjectOut:
+    o = _lib.FtProjectOut()
+    if phase_a:
+        o.out_kp, o.out_dist, o.out_oct = (rt.ptr(lay, "out_kp"), rt.ptr(lay, "out_dist"),
+                                           rt.ptr(lay, "out_oct"))
+    o.corr_point, o.corr_kp = rt.ptr(lay, "c_point"), rt.ptr(lay, "c_kp")
+    o.corr_dist, o.corr_oct = rt.ptr(lay, "c_dist"), rt.ptr(lay, "c_oct")
+    o.corr_count, o.slot_count = rt.ptr(lay, "c_n"), rt.ptr(lay, "slot_n")
+    return o
+
+
+def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale: float,
+                   levels: int, *, skip_mask=None, ref_angles=None, rotation: bool = False,
+                   window_px=None, u_offset: float = 0.0, slots=None, skip_slotted=False,
+                   write_slots=False, resolve=True, phase_a_out=False):
+    """One fused ``ft_project_search`` launch on one frame.
+
+    Returns a dict with any of: out_kp/out_dist/out_oct (phase A),
+    corr (Correspondences), slots (updated copy), count (filled slots)."""
+    rt = runtime()
+    left = frame.left
+    n_kp, m = len(left.u), len(points.point_ids)
+    cap_kp, cap_pts = rt.caps(n_kp, m)
+    cell, nx, ny = _grid_geometry(frame, cam)
+    with_angle = bool(rotation and ref_angles is not None)
+    lay = Layout()
+    add_keypoints(lay, "K", cap_kp, with_angle=with_angle)
+    _add_points(lay, cap_pts)
+    lay.add("rot", 72)
+    lay.add("trans", 24)
+    if skip_mask is not None:
+        lay.add("skip", cap_pts)
+    if with_angle:
+        lay.add("ref_ang", 8 * cap_pts)
+    if slots is not None:
+        lay.add("slots", 8 * cap_kp)
+    in_end = lay.total
+    out_begin = lay.total
+    if phase_a_out:
+        lay.add("out_kp", 8 * cap_pts)
+        lay.add("out_dist", 8 * cap_pts)
+        lay.add("out_oct", 8 * cap_pts)
+    for nm_ in ("c_point", "c_kp", "c_dist", "c_oct"):
+        lay.add(nm_, 8 * cap_pts)
+    lay.add("c_n", 4)
+    lay.add("slot_n", 4)
+    mode = 0
+    if resolve:
+        mode |= _lib.FT_PROJ_RESOLVE
+    if with_angle:
+        mode |= _lib.FT_PROJ_ROTATION
+    if skip_slotted:
+        mode |= _lib.FT_PROJ_SKIP_SLOTS
+    if write_slots:
+        mode |= _lib.FT_PROJ_WRITE_SLOTS
+    with rt.lock:
+        rt.reserve(lay.total)
+        put_keypoints(rt, lay, "K", left, with_angle=with_angle)
+        _put_points(rt, lay, points)
+        rt.put(lay, "rot", np.asarray(pose.rotation, dtype=np.float64).reshape(9), np.float64)
+        rt.put(lay, "trans", np.asarray(pose.translation, dtype=np.float64).reshape(3), np.float64)
+        if skip_mask is not None:
+            rt.put(lay, "skip", np.asarray(skip_mask, dtype=np.uint8), np.uint8)
+        if with_angle:
+            rt.put(lay, "ref_ang", ref_angles, np.float64)
+        if slots is not None:
+            rt.put(lay, "slots", slots, np.int64)
+        rt.h2d(0, in_end)
+        ws = rt.workspace()
+        params = project_params(cam, cfg, scale, levels, cell, nx, ny, window_px, u_offset)
+        io = _lib.FtProjectIO()
+        io.rot, io.trans = rt.ptr(lay, "rot"), rt.ptr(lay, "trans")
+        io.skip = rt.ptr(lay, "skip") if skip_mask is not None else None
+        io.ref_angles = rt.ptr(lay, "ref_ang") if with_angle else None
+        io.slots = rt.ptr(lay, "slots") if slots is not None else None
+        st = rt.lib.ft_project_search(1, _points_struct(rt, lay, cap_pts),
+                                      keypoints_struct(rt, lay, "K", cap_kp), params, io, mode,
+                                      _out_struct(rt, lay, phase_a_out), ws,
+                                      rt.stream.cuda_stream)
+        _lib.check(st, "ft_project_search")
+        if slots is not None:
+            rt.d2h(lay.offsets["slots"], lay.offsets["slots"] + 8 * n_kp)
+        rt.d2h(out_begin, lay.total)
+        rt.sync()
+        res = {}
+        if phase_a_out:
+            for k in ("out_kp", "out_dist", "out_oct"):
+                res[k] = rt.host_view(lay, k, np.int64, (m,)).copy()
+        if resolve:
+            c = int(rt.host_view(lay, "c_n", np.int32, (1,))[0])
+            res["corr"] = Correspondences(*(rt.host_view(lay, k, np.int64, (c,)).copy()
+                                            for k in ("c_point", "c_kp", "c_dist", "c_oct")))
+        if slots is not None:
+            res["slots"] = rt.host_view(lay, "slots", np.int64, (n_kp,)).copy()
+        if write_slots:
+            res["count"] = int(rt.host_view(lay, "slot_n", np.int32, (1,))[0])
+    return res
+
+
+def run_phase_a(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale: float,
+                levels: int, engine=None, skip_mask: np.ndarray | None = None,
+                window_px: float | None = None, u_offset: float = 0.0, pool=None
+                ) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Per-point candidate keypoint, distance and predicted octave
+    (reference projection.py:118-158 -> kernels.py:470-579)."""
+    n = len(points.point_ids)
+    if n == 0:
+        z = np.empty(0, dtype=np.int64)
+        return z, z.copy(), z.copy()
+    r = project_search(points, frame, pose, cam, cfg, scale, levels, skip_mask=skip_mask,
+                       window_px=window_px, u_offset=u_offset, resolve=False, phase_a_out=True)
+    return r["out_kp"], r["out_dist"], r["out_oct"]
+
+
+def resolve_conflicts(out_kp: np.ndarray, out_dist: np.ndarray,
+                      out_oct: np.ndarray) -> Correspondences:
+    """Phase B (reference projection.py:161-178): per keypoint the lowest
+    distance wins, ties to the lower point index; output in point order."""
+    out_kp = np.asarray(out_kp)
+    n = len(out_kp)
+    if n == 0 or not (out_kp >= 0).any():
+        return Correspondences.empty()
+    n_kp = int(out_kp.max()) + 1
+    rt = runtime()
+    cap_kp, cap_pts = rt.caps(n_kp, n)
+    lay = Layout()
+    for k in ("kp", "dist", "oct"):
+        lay.add(k, 8 * n)
+    in_end = lay.total
+    for k in ("c_point", "c_kp", "c_dist", "c_oct"):
+        lay.add(k, 8 * n)
+    lay.add("c_n", 4)
+    with rt.lock:
+        rt.reserve(lay.total)
+        rt.put(lay, "kp", out_kp, np.int64)
+        rt.put(lay, "dist", out_dist, np.int64)
+        rt.put(lay, "oct", out_oct, np.int64)
+        rt.h2d(0, in_end)
+        o = _lib.FtProjectOut()
+        o.corr_point, o.corr_kp = rt.ptr(lay, "c_point"), rt.ptr(lay, "c_kp")
+        o.corr_dist, o.corr_oct, o.corr_count = (rt.ptr(lay, "c_dist"), rt.ptr(lay, "c_oct"),
+                                                 rt.ptr(lay, "c_n"))
+        st = rt.lib.ft_resolve_conflicts(n, rt.ptr(lay, "kp"), rt.ptr(lay, "dist"),
+                                         rt.ptr(lay, "oct"), n_kp, o, rt.workspace(),
+                                         rt.stream.cuda_stream)
+        _lib.check(st, "ft_resolve_conflicts")
+        rt.d2h(in_end, lay.total)
+        rt.sync()
+        c = int(rt.host_view(lay, "c_n", np.int32, (1,))[0])
+        return Correspondences(*(rt.host_view(lay, k, np.int64, (c,)).copy()
+                                 for k in ("c_point", "c_kp", "c_dist", "c_oct")))
+
+
+def rotation_consistency_filter(corr: Correspondences, ref_angles: np.ndarray,
+                                kp_angles: np.ndarray,
+                                cfg: ProjectionSearchConfig) -> Correspondences:
+    """Phase C (reference projection.py:181-200): keep correspondences in
+    the K most populated of B angle-difference bins (ties: lower bin)."""
+    m = len(corr.point_idx)
+    if m == 0:
+        return corr
+    rt = runtime()
+    lay = Layout()
+    for k in ("c_point", "c_kp", "c_dist", "c_oct"):
+        lay.add(k, 8 * m)
+    lay.add("ref", 8 * len(ref_angles))
+    lay.add("kpa", 8 * len(kp_angles))
+    in_end = lay.total
+    lay.add("c_n", 4)
+    with rt.lock:
+        rt.reserve(lay.total)
+        for k, arr in (("c_point", corr.point_idx), ("c_kp", corr.keypoint_idx),
+                       ("c_dist", corr.distance), ("c_oct", corr.octave)):
+            rt.put(lay, k, arr, np.int64)
+        rt.put(lay, "ref", ref_angles, np.float64)
+        rt.put(lay, "kpa", kp_angles, np.float64)
+        rt.h2d(0, in_end)
+        st = rt.lib.ft_rotation_filter(m, rt.ptr(lay, "c_point"), rt.ptr(lay, "c_kp"),
+                                       rt.ptr(lay, "c_dist"), rt.ptr(lay, "c_oct"),
+                                       rt.ptr(lay, "ref"), rt.ptr(lay, "kpa"),
+                                       int(cfg.histogram_bins), int(cfg.histogram_keep),
+                                       rt.ptr(lay, "c_n"), rt.stream.cuda_stream)
+        _lib.check(st, "ft_rotation_filter")
+        rt.d2h(0, lay.total)
+        rt.sync()
+        c = int(rt.host_view(lay, "c_n", np.int32, (1,))[0])
+        return Correspondences(*(rt.host_view(lay, k, np.int64, (c,)).copy()
+                                 for k in ("c_point", "c_kp", "c_dist", "c_oct")))
+
+
+def search_by_projection(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale: float,
+                         levels: int, engine=None, skip_mask: np.ndarray | None = None,
+                         ref_angles: np.ndarray | None = None, rotation_check: bool = False,
+                         window_px: float | None = None, u_offset: float = 0.0,
+                         pool=None) -> Correspondences:
+    """Project map points into the frame and resolve the best associations
+    (reference projection.py:203-221) -- phases A, B and C in ONE launch."""
+    if len(points.point_ids) == 0:
+        return Correspondences.empty()
+    r = project_search(points, frame, pose, cam, cfg, scale, levels, skip_mask=skip_mask,
+                       ref_angles=ref_angles, rotation=bool(rotation_check),
+                       window_px=window_px, u_offset=u_offset)
+    return r["corr"]
+
+
+def search_prev_frame(prev, cur, pose, world, cam, cfg: ProjectionSearchConfig, scale: float,
+                      levels: int, engine=None, soa_out=None, pool=None):
+    """Match the previous frame's map points into the current frame
+    (reference projection.py:224-253).  Decomposition of the host-side world
+    map stays on the host, as in the reference."""
+    from .types import MapPointSoA
+    slot_idx = np.nonzero(prev.slots != NO_POINT)[0]
+    if len(slot_idx) == 0:
+        return Correspondences.empty(), np.empty(0, dtype=np.int64)
+    pids = prev.slots[slot_idx]
+    mps = [world.points[int(p)] for p in pids]
+    soa = MapPointSoA(positions=np.array([p.position for p in mps], dtype=np.float64).reshape(-1, 3),
+                      descriptors=np.array([p.descriptor for p in mps], dtype=np.uint64).reshape(-1, 4),
+                      normals=np.array([p.normal for p in mps], dtype=np.float64).reshape(-1, 3),
+                      min_distances=np.array([p.min_distance for p in mps], dtype=np.float64),
+                      max_distances=np.array([p.max_distance for p in mps], dtype=np.float64),
+                      point_ids=np.array([p.point_id for p in mps], dtype=np.int64))
+    ref_angles = prev.left.angle[slot_idx]
+    rel = pose.matrix() @ np.linalg.inv(prev.pose.matrix())
+    forward = float(rel[2, 3])
+    u_offset = math.copysign(cfg.prev_u_offset_px, forward) if abs(forward) > 1e-9 else 0.0
+    corr = search_by_projection(soa, cur, pose, cam, cfg, scale, levels, ref_angles=ref_angles,
+                                rotation_check=cfg.rotation_check_prev,
+                                window_px=cfg.window_prev_px, u_offset=u_offset)
+    return corr, soa.point_ids

@@ -1,0 +1,329 @@
+"""Stereo matching drop-in: the reference's stage functions on B200.
+
+Signatures, argument meaning, outputs and error behaviour follow the
+reference module ``trackfront.stereo`` (pkg/src/trackfront/stereo.py); the
+work runs in the fused sm_100a kernel ``ft_stereo_pinhole`` /
+``ft_stereo_fisheye_bf`` (csrc/ft_stereo.cu, csrc/ft_fisheye.cu) via the C ABI.
+``engine`` / ``pool`` arguments are accepted for signature compatibility and
+ignored: the device is the engine.
+
+ORB-SLAM-style aliases: ``compute_stereo_matches`` (pinhole: phase 1 ->
+phase 2 | from-candidates -> reject, ONE launch) and
+``compute_stereo_fisheye_matches``.
+"""
+
+from __future__ import annotations
+
+from types import SimpleNamespace
+
+import numpy as np
+
+from . import _lib
+from .runtime import (Layout, add_keypoints, keypoints_struct, put_keypoints, pyramid_struct,
+                      runtime, stereo_params)
+from .types import StereoMatchConfig, StereoMatches
+
+__all__ = ["StereoMatchConfig", "StereoMatches", "build_row_buckets", "match_pinhole_phase1",
+           "refine_match_phase2", "matches_from_candidates", "reject_outliers",
+           "triangulate_rays", "match_fisheye", "matches_to_csv_rows",
+           "compute_stereo_matches", "compute_stereo_fisheye_matches"]
+
+
+def build_row_buckets(v: np.ndarray, height: int) -> tuple[np.ndarray, np.ndarray]:
+    """CSR of keypoint indices by rounded row (reference stereo.py:67-74).
+
+    Provided for API completeness; the device kernels build the same buckets
+    in shared memory and never call this."""
+    rows = np.clip(np.round(np.asarray(v)).astype(np.int64), 0, height - 1)
+    order = np.argsort(rows, kind="stable")
+    start = np.zeros(height + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=height), out=start[1:])
+    return start, order.astype(np.int64)
+
+
+def _matches_layout(lay: Layout, cap: int) -> None:
+    for name, nb in (("cand_idx", 8), ("cand_dist", 8), ("right_idx", 8), ("distance", 8),
+                     ("disparity", 8), ("refined_u", 8), ("depth", 8), ("sad", 8)):
+        lay.add(name, nb * cap)
+    lay.add("n_matched", 4)
+
+
+def _out_struct(rt, lay: Layout) -> _lib.FtStereoOut:
+    o = _lib.FtStereoOut()
+    for name in ("cand_idx", "cand_dist", "right_idx", "distance", "disparity", "refined_u",
+                 "depth", "sad", "n_matched"):
+        setattr(o, name, rt.ptr(lay, name))
+    return o
+
+
+def _read_matches(rt, lay: Layout, n: int) -> StereoMatches:
+    g = lambda name, dt: rt.host_view(lay, name, dt, (n,)).copy()  # noqa: E731
+    return StereoMatches(right_idx=g("right_idx", np.int64), distance=g("distance", np.int64),
+                         disparity=g("disparity", np.float64), refined_u=g("refined_u", np.float64),
+                         depth=g("depth", np.float64), sad=g("sad", np.int64))
+
+
+def _run_stereo(mode: int, left, right, cam, cfg, scale_pow, height: int,
+                left_pyr=None, right_pyr=None, cand=None, matches=None,
+                out_cand: bool = False):
+    """Pack -> one H2D -> ft_stereo_pinhole -> one D2H."""
+    rt = runtime()
+    n, nr = len(left.u), len(right.u)
+    cap, _ = rt.caps(max(n, nr))
+    lay = Layout()
+    add_keypoints(lay, "L", cap)
+    add_keypoints(lay, "R", cap)
+    use_pyr = bool(mode & _lib.FT_STEREO_REFINE)
+    if use_pyr:
+        lay.add("pyr_l", int(left_pyr.offsets[-1]))
+        lay.add("pyr_r", int(right_pyr.offsets[-1]))
+    in_end = lay.total
+    _matches_layout(lay, cap)
+    with rt.lock:
+        rt.reserve(lay.total)
+        put_keypoints(rt, lay, "L", left)
+        put_keypoints(rt, lay, "R", right)
+        if use_pyr:
+            rt.put(lay, "pyr_l", left_pyr.data, np.uint8)
+            rt.put(lay, "pyr_r", right_pyr.data, np.uint8)
+        upload_end = in_end
+        if cand is not None:
+            rt.put(lay, "cand_idx", cand[0], np.int64)
+            rt.put(lay, "cand_dist", cand[1], np.int64)
+            upload_end = lay.offsets["cand_dist"] + 8 * n
+        if matches is not None:
+            for name, dt in (("right_idx", np.int64), ("distance", np.int64),
+                             ("disparity", np.float64), ("refined_u", np.float64),
+                             ("depth", np.float64), ("sad", np.int64)):
+                rt.put(lay, name, getattr(matches, name), dt)
+            upload_end = lay.total
+        rt.h2d(0, upload_end)
+        ws = rt.workspace()
+        params = stereo_params(cfg, height, scale_pow, getattr(cam, "baseline_times_fx", 1.0))
+        kl = keypoints_struct(rt, lay, "L", cap)
+        kr = keypoints_struct(rt, lay, "R", cap)
+        pl = pyramid_struct(left_pyr, rt.ptr(lay, "pyr_l"), 0) if use_pyr else None
+        pr = pyramid_struct(right_pyr, rt.ptr(lay, "pyr_r"), 0) if use_pyr else None
+        out = _out_struct(rt, lay)
+        st = rt.lib.ft_stereo_pinhole(1, kl, kr, pl, pr, params, mode, out, ws,
+                                      rt.stream.cuda_stream)
+        _lib.check(st, "ft_stereo_pinhole")
+        rt.d2h(lay.offsets["cand_idx"], lay.total)
+        rt.sync()
+        res = _read_matches(rt, lay, n) if mode & ~_lib.FT_STEREO_PHASE1 else None
+        cidx = rt.host_view(lay, "cand_idx", np.int64, (n,)).copy() if out_cand else None
+        cdist = rt.host_view(lay, "cand_dist", np.int64, (n,)).copy() if out_cand else None
+    return res, cidx, cdist
+
+
+def match_pinhole_phase1(left, right, height: int, scale_pow: np.ndarray,
+                         cfg: StereoMatchConfig, engine=None, row_buckets=None,
+                         out_idx: np.ndarray | None = None,
+                         out_dist: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Best-candidate right index (or -1) and distance per left keypoint
+    (reference stereo.py:77-103 -> kernels.py:300-345).
+
+    ``row_buckets`` is accepted for compatibility; the kernel rebuilds the
+    buckets of ``build_row_buckets`` on the device (same rows, same sets)."""
+    n = len(left.u)
+    idx = out_idx if out_idx is not None else np.empty(n, dtype=np.int64)
+    dist = out_dist if out_dist is not None else np.empty(n, dtype=np.int64)
+    if n == 0:
+        return idx, dist
+    _, ci, cd = _run_stereo(_lib.FT_STEREO_PHASE1, left, right, None, cfg, scale_pow, height,
+                            out_cand=True)
+    idx[:n] = ci
+    dist[:n] = cd
+    return idx, dist
+
+
+def refine_match_phase2(left_pyr, right_pyr, left, right, cand_idx: np.ndarray,
+                        cand_dist: np.ndarray, cam, cfg: StereoMatchConfig,
+                        engine=None) -> StereoMatches:
+    """Sub-pixel SAD refinement of phase-1 candidates (reference
+    stereo.py:106-140 -> kernels.py:351-428)."""
+    n = len(left.u)
+    if n == 0:
+        z = np.zeros(0)
+        zi = np.zeros(0, dtype=np.int64)
+        return StereoMatches(zi.copy(), zi.copy(), z.copy(), z.copy(), z.copy(), zi.copy())
+    scale_pow = left_pyr.scale ** np.arange(len(left_pyr.widths), dtype=np.float64)
+    res, _, _ = _run_stereo(_lib.FT_STEREO_REFINE, left, right, cam, cfg, scale_pow,
+                            int(cam.height), left_pyr, right_pyr,
+                            cand=(np.asarray(cand_idx), np.asarray(cand_dist)))
+    return res
+
+
+def matches_from_candidates(cand_idx: np.ndarray, cand_dist: np.ndarray, left, right, cam,
+                            cfg: StereoMatchConfig) -> StereoMatches:
+    """Accept phase-1 candidates at their raw disparity (reference
+    stereo.py:143-168)."""
+    n = len(cand_idx)
+    if n == 0:
+        z = np.zeros(0)
+        zi = np.zeros(0, dtype=np.int64)
+        return StereoMatches(zi.copy(), zi.copy(), z.copy(), z.copy(), z.copy(), zi.copy())
+    res, _, _ = _run_stereo(_lib.FT_STEREO_FROM_CAND, left, right, cam, cfg, np.ones(1),
+                            int(getattr(cam, "height", 1)),
+                            cand=(np.asarray(cand_idx), np.asarray(cand_dist)))
+    return res
+
+
+def reject_outliers(matches: StereoMatches, cfg: StereoMatchConfig) -> StereoMatches:
+    """Drop matches whose SAD exceeds outlier_multiplier x median, in place
+    (reference stereo.py:171-188).  SADs must lie in [0, 2^32)."""
+    m = matches.right_idx >= 0
+    if not m.any():
+        return matches
+
+    n = len(matches.right_idx)
+    left = SimpleNamespace(u=np.zeros(n), v=np.zeros(n), octave=np.zeros(n, dtype=np.int32),
+                           descriptors=np.zeros((n, 4), dtype=np.uint64))
+    res, _, _ = _run_stereo(_lib.FT_STEREO_REJECT, left, left, None, cfg, np.ones(1), 1,
+                            matches=matches)
+    for name in ("right_idx", "distance", "disparity", "refined_u", "depth", "sad"):
+        getattr(matches, name)[...] = getattr(res, name)
+    return matches
+
+
+def compute_stereo_matches(left, right, cam, cfg: StereoMatchConfig | None = None,
+                           scale_pow: np.ndarray | None = None, left_pyr=None,
+                           right_pyr=None) -> StereoMatches:
+    """ORB-SLAM ComputeStereoMatches: the reference tracker's pinhole
+    ``_run_stereo`` (tracker.py:415-427) as ONE fused launch -- phase 1, then
+    phase 2 when pyramids are given (else matches_from_candidates), then
+    reject_outliers."""
+    cfg = cfg or StereoMatchConfig()
+    if scale_pow is None:
+        scale_pow = (left_pyr.scale ** np.arange(len(left_pyr.widths), dtype=np.float64)
+                     if left_pyr is not None else 1.2 ** np.arange(8, dtype=np.float64))
+    n = len(left.u)
+    if n == 0:
+        return StereoMatches(*(np.zeros(0, dtype=t) for t in (np.int64, np.int64, np.float64,
+                                                              np.float64, np.float64, np.int64)))
+    mode = _lib.FT_STEREO_PHASE1 | _lib.FT_STEREO_REJECT
+    mode |= _lib.FT_STEREO_REFINE if left_pyr is not None else _lib.FT_STEREO_FROM_CAND
+    res, _, _ = _run_stereo(mode, left, right, cam, cfg, scale_pow, int(cam.height), left_pyr,
+                            right_pyr)
+    return res
+
+
+# ---------------------------------------------------------------------------
+# fisheye
+
+def triangulate_rays(origin_a, dir_a, origin_b, dir_b):
+    """Midpoint of the shortest segment between two rays, None when
+    parallel (reference stereo.py:191-197, including its solve at :207-216)."""
+    pt, _, _, _ = _closest_ray_points(origin_a, dir_a, origin_b, dir_b)
+    return pt
+
+
+def _closest_ray_points(oa, da, ob, db):
+    # Host-side restatement of reference stereo.py:200-220, kept term for term
+    # (including the sign of t at :216, which the reference tracker's output
+    # depends on).
+    da = np.asarray(da, dtype=np.float64)
+    db = np.asarray(db, dtype=np.float64)
+    oa = np.asarray(oa, dtype=np.float64)
+    ob = np.asarray(ob, dtype=np.float64)
+    if np.linalg.norm(np.cross(da, db)) < 1e-9:
+        return None, None, None, None
+    r = ob - oa
+    a11, a12, a22 = da @ da, da @ db, db @ db
+    b1, b2 = da @ r, db @ r
+    den = a11 * a22 - a12 * a12
+    s = (b1 * a22 - a12 * b2) / den
+    t = (a11 * b2 - a12 * b1) / den
+    pa = oa + s * da
+    pb = ob + t * db
+    gap = float(np.linalg.norm(pa - pb))
+    return (pa + pb) / 2.0, gap, s, t
+
+
+def fisheye_bruteforce(left, right, cfg: StereoMatchConfig) -> tuple[np.ndarray, np.ndarray]:
+    """kernels.py:434-464 over all left keypoints on the device: (idx, dist)."""
+    rt = runtime()
+    n, nr = len(left.u), len(right.u)
+    cap, _ = rt.caps(max(n, nr))
+    lay = Layout()
+    add_keypoints(lay, "L", cap)
+    add_keypoints(lay, "R", cap)
+    in_end = lay.total
+    lay.add("idx", 8 * cap)
+    lay.add("dist", 8 * cap)
+    with rt.lock:
+        rt.reserve(lay.total)
+        put_keypoints(rt, lay, "L", left)
+        put_keypoints(rt, lay, "R", right)
+        rt.h2d(0, in_end)
+        ws = rt.workspace()
+        kl = keypoints_struct(rt, lay, "L", cap)
+        kr = keypoints_struct(rt, lay, "R", cap)
+        st = rt.lib.ft_stereo_fisheye_bf(1, kl, kr, int(cfg.t_match), float(cfg.ratio),
+                                         rt.ptr(lay, "idx"), rt.ptr(lay, "dist"), ws,
+                                         rt.stream.cuda_stream)
+        _lib.check(st, "ft_stereo_fisheye_bf")
+        rt.d2h(lay.offsets["idx"], lay.total)
+        rt.sync()
+        idx = rt.host_view(lay, "idx", np.int64, (n,)).copy()
+        dist = rt.host_view(lay, "dist", np.int64, (n,)).copy()
+    return idx, dist
+
+
+def match_fisheye(left, right, cam, cfg: StereoMatchConfig, engine=None
+                  ) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
+    """Brute-force fisheye matching plus ray-midpoint triangulation
+    (reference stereo.py:223-273).  The all-pairs matching runs on the B200;
+    the per-accepted-pair triangulation is the reference's host loop."""
+    n = len(left.u)
+    empty = (np.empty(0, dtype=np.int64), np.empty(0, dtype=np.int64), np.empty((0, 3)),
+             np.empty(0, dtype=np.int64))
+    if n == 0 or len(right.u) == 0:
+        return empty
+    idx, dist = fisheye_bruteforce(left, right, cfg)
+    t_rl = cam.right_extrinsic
+    t_lr = t_rl.inverse()
+    left_ids, right_ids, points, dists = [], [], [], []
+    for i in np.nonzero(idx >= 0)[0]:
+        j = int(idx[i])
+        ray_l = cam.unproject(float(left.u[i]), float(left.v[i]))
+        ray_r = cam.unproject(float(right.u[j]), float(right.v[j]))
+        dir_r = t_lr.rotation @ ray_r
+        pt, gap, _, _ = _closest_ray_points(np.zeros(3), ray_l, t_lr.translation, dir_r)
+        if pt is None or gap is None or gap > cfg.ray_gap_ceiling:
+            continue
+        p_right = t_rl.transform(pt)
+        if pt[2] <= 0 or p_right[2] <= 0:
+            continue
+        left_ids.append(int(i))
+        right_ids.append(j)
+        points.append(pt)
+        dists.append(int(dist[i]))
+    if not left_ids:
+        return empty
+    return (np.asarray(left_ids, dtype=np.int64), np.asarray(right_ids, dtype=np.int64),
+            np.asarray(points), np.asarray(dists, dtype=np.int64))
+
+
+def compute_stereo_fisheye_matches(left, right, cam, cfg: StereoMatchConfig | None = None
+                                   ) -> StereoMatches:
+    """ORB-SLAM ComputeStereoFishEyeMatches: the reference tracker's fisheye
+    ``_run_stereo`` branch (tracker.py:399-414) -> per-left StereoMatches."""
+    cfg = cfg or StereoMatchConfig()
+    lidx, ridx, points, dists = match_fisheye(left, right, cam, cfg)
+    n = len(left.u)
+    out = StereoMatches(right_idx=np.full(n, -1, dtype=np.int64),
+                        distance=np.full(n, 10000, dtype=np.int64), disparity=np.zeros(n),
+                        refined_u=np.zeros(n), depth=np.zeros(n), sad=np.zeros(n, dtype=np.int64))
+    out.right_idx[lidx] = ridx
+    out.distance[lidx] = dists
+    out.depth[lidx] = points[:, 2] if len(points) else 0.0
+    return out
+
+
+def matches_to_csv_rows(matches: StereoMatches) -> list[str]:
+    """'left_idx,right_idx,disparity,depth,distance' per matched pair
+    (reference stereo.py:276-283)."""
+    return [f"{i},{matches.right_idx[i]},{matches.disparity[i]:.6f},"
+            f"{matches.depth[i]:.6f},{matches.distance[i]}"
+            for i in np.nonzero(matches.right_idx >= 0)[0]]

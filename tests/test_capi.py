@@ -1,0 +1,64 @@
+"""CPU-side checks of the C ABI: the library loads, exports every entry
+include/fasttrack_b200.h declares, and validates arguments without a GPU."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2509_10757_b200 import _lib
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "fasttrack_b200.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char \*)\s*(ft_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_entries():
+    names = declared_functions()
+    for must in ("ft_stereo_pinhole", "ft_stereo_fisheye_bf", "ft_project_search",
+                 "ft_resolve_conflicts", "ft_rotation_filter", "ft_workspace_bytes",
+                 "ft_workspace_init", "ft_hamming_pairs"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.load()
+    for name in declared_functions():
+        assert hasattr(L, name), name
+    assert set(_lib.EXPORTS) <= set(declared_functions())
+
+
+def test_abi_version_and_status_strings():
+    L = _lib.load()
+    assert L.ft_abi_version() == 1
+    assert L.ft_status_string(0) == b"ok"
+    assert b"NULL" in L.ft_status_string(-1)
+
+
+def test_workspace_sizing_monotone():
+    L = _lib.load()
+    a = L.ft_workspace_bytes(1, 1024, 1024)
+    b = L.ft_workspace_bytes(1, 2048, 1024)
+    c = L.ft_workspace_bytes(4, 2048, 8192)
+    assert 0 < a < b < c
+    assert L.ft_workspace_bytes(0, 1024, 1024) == 0
+
+
+def test_argument_validation_without_gpu():
+    """Null / range errors are returned before any CUDA call."""
+    L = _lib.load()
+    kp = _lib.FtKeypoints()
+    kp.cap = 0
+    params = _lib.FtStereoParams()
+    out = _lib.FtStereoOut()
+    ws = _lib.FtWorkspace()
+    assert L.ft_stereo_pinhole(1, None, None, None, None, None, 0, None, None, None) == -1
+    assert L.ft_stereo_pinhole(1, kp, kp, None, None, params, 1, out, ws, None) == -2
+    assert L.ft_stereo_fisheye_bf(1, kp, kp, 100, 0.8, None, None, ws, None) == -1
+    assert L.ft_resolve_conflicts(0, None, None, None, 0, None, None, None) == -1
+    assert L.ft_rotation_filter(0, None, None, None, None, None, None, 0, 1,
+                                ctypes.byref(ctypes.c_int32()), None) == -4

@@ -1,0 +1,282 @@
+"""GPU parity: the B200 drop-in (through the C ABI) against the reference's
+golden outputs and the CPU oracle on the same inputs.  Bit-exact for indices,
+distances, SADs and slots; disparity / refined_u / depth are compared exactly
+too (they are computed in fp64 with the reference's evaluation order), with
+the north-star tolerance (1e-4 px) asserted as the contract."""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+import paper_2509_10757_b200 as ft
+from paper_2509_10757_b200.types import Frame, FrameGrid, ProjectionSearchConfig, StereoMatchConfig
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("right_idx", "distance", "disparity", "refined_u", "depth", "sad")
+CORR = ("point_idx", "keypoint_idx", "distance", "octave")
+PX_TOL = 1e-4  # north star: stereo depth / uR within 1e-4 px
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def assert_matches(m, d, prefix):
+    for f in ("right_idx", "distance", "sad"):
+        np.testing.assert_array_equal(getattr(m, f), d[f"{prefix}_{f}"], err_msg=f)
+    for f in ("disparity", "refined_u", "depth"):
+        np.testing.assert_allclose(getattr(m, f), d[f"{prefix}_{f}"], rtol=0, atol=PX_TOL,
+                                   err_msg=f)
+        np.testing.assert_array_equal(getattr(m, f), d[f"{prefix}_{f}"], err_msg=f + " (bitwise)")
+
+
+def assert_corr(c, d, prefix):
+    for f in CORR:
+        np.testing.assert_array_equal(getattr(c, f), d[f"{prefix}_{f}"], err_msg=f)
+
+
+def make_frame(left, right, cam, pose):
+    grid = FrameGrid(left.u, left.v, cam.width, cam.height, 48)
+    return Frame(0, 0.0, left, right, np.full(len(left.u), -1.0),
+                 np.full(len(left.u), -1, dtype=np.int64), pose, grid)
+
+
+def test_hamming_pairs_capi():
+    import torch
+    from paper_2509_10757_b200 import _lib
+    d = G.load("hamming.npz")
+    L = _lib.load()
+    a = torch.from_numpy(d["a"].view(np.int64)).cuda()
+    b = torch.from_numpy(d["b"].view(np.int64)).cuda()
+    out = torch.empty(len(d["a"]), dtype=torch.int64, device="cuda")
+    _lib.check(L.ft_hamming_pairs(a.data_ptr(), b.data_ptr(), len(d["a"]), out.data_ptr(),
+                                  torch.cuda.current_stream().cuda_stream), "hamming")
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy(), d["out"])
+
+
+def test_cfg1_phase1_phase2_reject():
+    d = G.load("cfg1_stereo.npz")
+    left, right = G.feats(d, "left"), G.feats(d, "right")
+    cam, cfg = G.pinhole(), StereoMatchConfig()
+    idx, dist = ft.match_pinhole_phase1(left, right, cam.height, d["scale_pow"], cfg)
+    np.testing.assert_array_equal(idx, d["p1_idx"])
+    np.testing.assert_array_equal(dist, d["p1_dist"])
+    pl, pr = G.pyramid(d, "l"), G.pyramid(d, "r")
+    m = ft.refine_match_phase2(pl, pr, left, right, idx, dist, cam, cfg)
+    assert_matches(m, d, "p2")
+    ft.reject_outliers(m, cfg)
+    assert_matches(m, d, "final")
+    # fused single launch (tracker _run_stereo pinhole branch)
+    f = ft.compute_stereo_matches(left, right, cam, cfg, d["scale_pow"], pl, pr)
+    assert_matches(f, d, "final")
+
+
+def test_cfg2_stereo_from_candidates():
+    d = G.load("cfg2_frame_map.npz")
+    left, right = G.feats(d, "left"), G.feats(d, "right")
+    cam, cfg = G.pinhole(), StereoMatchConfig()
+    idx, dist = ft.match_pinhole_phase1(left, right, cam.height, d["scale_pow"], cfg)
+    np.testing.assert_array_equal(idx, d["p1_idx"])
+    m = ft.matches_from_candidates(idx, dist, left, right, cam, cfg)
+    assert_matches(m, d, "fc")
+    f = ft.compute_stereo_matches(left, right, cam, cfg, d["scale_pow"])
+    assert_matches(f, d, "final")
+
+
+def test_cfg2_projection_all_variants():
+    d = G.load("cfg2_frame_map.npz")
+    left, right = G.feats(d, "left"), G.feats(d, "right")
+    cam, cfg = G.pinhole(), ProjectionSearchConfig()
+    pts, pose = G.soa(d), G.pose(d)
+    frame = make_frame(left, right, cam, pose)
+    kp, kd, ko = ft.run_phase_a(pts, frame, pose, cam, cfg, 1.2, 8)
+    np.testing.assert_array_equal(kp, d["pa_kp"])
+    np.testing.assert_array_equal(kd, d["pa_dist"])
+    np.testing.assert_array_equal(ko, d["pa_oct"])
+    assert_corr(ft.resolve_conflicts(kp, kd, ko), d, "corr")
+    assert_corr(ft.search_by_projection(pts, frame, pose, cam, cfg, 1.2, 8), d, "corr")
+    c = ft.search_by_projection(pts, frame, pose, cam, cfg, 1.2, 8, ref_angles=d["ref_angles"],
+                                rotation_check=True, window_px=cfg.window_prev_px, u_offset=1.0)
+    assert_corr(c, d, "corr_rot")
+    c = ft.search_by_projection(pts, frame, pose, cam, cfg, 1.2, 8, skip_mask=d["skip"])
+    assert_corr(c, d, "corr_skip")
+    # standalone phase C on the golden phase-B output
+    base = ft.search_by_projection(pts, frame, pose, cam, cfg, 1.2, 8,
+                                   window_px=cfg.window_prev_px, u_offset=1.0)
+    c2 = ft.rotation_consistency_filter(base, d["ref_angles"], left.angle, cfg)
+    assert_corr(c2, d, "corr_rot")
+
+
+def test_cfg2_search_local_points():
+    d = G.load("cfg2_frame_map.npz")
+    left, right = G.feats(d, "left"), G.feats(d, "right")
+    cam, cfg = G.pinhole(), ProjectionSearchConfig()
+    local, pose = G.local_map(d), G.pose(d)
+    fa = make_frame(left, right, cam, pose)
+    n = ft.search_local_points(local, fa, cam, cfg, 1.2, 8)
+    assert n == int(d["count_a"])
+    np.testing.assert_array_equal(fa.slots, d["slots_a"])
+    fb = make_frame(left, right, cam, pose)
+    fb.slots[...] = d["slots_b_in"]
+    n = ft.search_local_points(local, fb, cam, cfg, 1.2, 8)
+    assert n == int(d["count_b"])
+    np.testing.assert_array_equal(fb.slots, d["slots_b"])
+
+
+def test_cfg3_fisheye():
+    d = G.load("cfg3_fisheye.npz")
+    left, right = G.feats(d, "left"), G.feats(d, "right")
+    cfg = StereoMatchConfig()
+    from paper_2509_10757_b200.stereo import fisheye_bruteforce
+    idx, dist = fisheye_bruteforce(left, right, cfg)
+    np.testing.assert_array_equal(idx, d["bf_idx"])
+    np.testing.assert_array_equal(dist, d["bf_dist"])
+    cam = G.fisheye()
+    lidx, ridx, pts3, dists = ft.match_fisheye(left, right, cam, cfg)
+    np.testing.assert_array_equal(lidx, d["mf_lidx"])
+    np.testing.assert_array_equal(ridx, d["mf_ridx"])
+    np.testing.assert_array_equal(pts3, d["mf_pts"])
+    pcfg = ProjectionSearchConfig()
+    pts, pose = G.soa(d), G.pose(d)
+    frame = make_frame(left, right, cam, pose)
+    kp, kd, ko = ft.run_phase_a(pts, frame, pose, cam, pcfg, 1.2, 8)
+    np.testing.assert_array_equal(kp, d["pa_kp"])
+    np.testing.assert_array_equal(kd, d["pa_dist"])
+    np.testing.assert_array_equal(ko, d["pa_oct"])
+    fa = make_frame(left, right, cam, pose)
+    n = ft.search_local_points(G.local_map(d), fa, cam, pcfg, 1.2, 8)
+    assert n == int(d["count_a"])
+    np.testing.assert_array_equal(fa.slots, d["slots_a"])
+
+
+def test_edge_cases():
+    d = G.load("edge_cases.npz")
+    from types import SimpleNamespace as NS
+    from paper_2509_10757_b200.stereo import fisheye_bruteforce
+    cfg = StereoMatchConfig()
+
+    def F(desc, u=None, v=None, o=None):
+        n = len(desc)
+        return NS(u=np.zeros(n) if u is None else u, v=np.zeros(n) if v is None else v,
+                  octave=np.zeros(n, np.int32) if o is None else o, descriptors=desc)
+
+    idx, dist = fisheye_bruteforce(F(d["dup_left"]), F(d["dup_right"]), cfg)
+    np.testing.assert_array_equal(idx, d["dup_idx"])
+    np.testing.assert_array_equal(dist, d["dup_dist"])
+    idx, dist = fisheye_bruteforce(F(d["dup_left"]), F(d["one_right"]), cfg)
+    np.testing.assert_array_equal(idx, d["one_idx"])
+    np.testing.assert_array_equal(dist, d["one_dist"])
+    lf = F(d["tie_ld"], d["tie_lu"], d["tie_lv"], d["tie_loct"])
+    rf = F(d["tie_rd"], d["tie_ru"], d["tie_rv"], d["tie_roct"])
+    idx, dist = ft.match_pinhole_phase1(lf, rf, 480, 1.2 ** np.arange(8.0), cfg)
+    np.testing.assert_array_equal(idx, d["tie_idx"])
+    np.testing.assert_array_equal(dist, d["tie_dist"])
+    for cnt in (1, 2, 7, 8, 101, 1000):
+        m = ft.StereoMatches(right_idx=d[f"med{cnt}_rin"].copy(),
+                             distance=np.full(cnt, 5, np.int64), disparity=np.full(cnt, 3.0),
+                             refined_u=np.full(cnt, 1.0), depth=np.full(cnt, 2.0),
+                             sad=d[f"med{cnt}_sad"].copy())
+        ft.reject_outliers(m, cfg)
+        np.testing.assert_array_equal(m.right_idx, d[f"med{cnt}_rout"])
+        np.testing.assert_array_equal(m.sad, d[f"med{cnt}_sadout"])
+
+
+def test_empty_inputs():
+    e = ft.FeatureSet.empty()
+    cfg = StereoMatchConfig()
+    idx, dist = ft.match_pinhole_phase1(e, e, 480, np.ones(8), cfg)
+    assert len(idx) == 0
+    assert ft.match_fisheye(e, e, G.fisheye(), cfg)[0].shape == (0,)
+    assert len(ft.resolve_conflicts(np.empty(0, np.int64), np.empty(0, np.int64),
+                                    np.empty(0, np.int64))) == 0
+    # left keypoints but no right keypoints
+    d = G.load("cfg2_frame_map.npz")
+    left = G.feats(d, "left")
+    idx, dist = ft.match_pinhole_phase1(left, e, 480, d["scale_pow"], cfg)
+    assert (idx == -1).all() and (dist == 10000).all()
+
+
+def _oracle_local_search(O, w, pcfg, slots):
+    grid = O.frame_grid(w.left.u, w.left.v, w.cam.width, w.cam.height, 48) + (48,)
+    return O.search_local_points(w.local.point_ids, w.local.soa, w.left.u, w.left.v,
+                                 w.left.octave, w.left.descriptors, grid, slots, w.pose, w.cam,
+                                 pcfg, 1.2, 8)
+
+
+@pytest.mark.parametrize("seed,n_lm,m_pts,images", [(11, 12000, 5000, True),
+                                                    (12, 20000, 20000, False),
+                                                    (13, 20000, 20000, True),
+                                                    (14, 4000, 1000, True)])
+def test_random_pinhole_vs_oracle(oracle, seed, n_lm, m_pts, images):
+    from paper_2509_10757_b200.synthetic import make_workload
+    w = make_workload(seed=seed, n_landmarks=n_lm, map_points=m_pts, images=images)
+    cfg, pcfg = StereoMatchConfig(), ProjectionSearchConfig()
+    ref = oracle.stereo_pinhole(w.left, w.right, w.pyr_left, w.pyr_right, w.cam, cfg,
+                                w.scale_pow)
+    got = ft.compute_stereo_matches(w.left, w.right, w.cam, cfg, w.scale_pow, w.pyr_left,
+                                    w.pyr_right)
+    for f in FIELDS:
+        np.testing.assert_array_equal(getattr(got, f), getattr(ref, f), err_msg=f)
+    slots = np.full(len(w.left.u), -1, np.int64)
+    # pre-slot a few keypoints with map ids to exercise skip + "only if empty"
+    rng = np.random.default_rng(seed)
+    k = rng.choice(len(slots), size=len(slots) // 10, replace=False)
+    slots[k] = rng.choice(w.local.point_ids, size=len(k), replace=False)
+    frame = w.frame()
+    frame.slots[...] = slots
+    n_ref = _oracle_local_search(oracle, w, pcfg, slots)
+    n = ft.search_local_points(w.local, frame, w.cam, pcfg, 1.2, 8)
+    assert n == n_ref
+    np.testing.assert_array_equal(frame.slots, slots)
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_random_fisheye_vs_oracle(oracle, seed):
+    from paper_2509_10757_b200.synthetic import make_workload
+    from paper_2509_10757_b200.stereo import fisheye_bruteforce
+    w = make_workload(seed=seed, n_landmarks=5000, map_points=5000, fisheye=True, noise_px=0.3)
+    cfg, pcfg = StereoMatchConfig(), ProjectionSearchConfig()
+    idx, dist = fisheye_bruteforce(w.left, w.right, cfg)
+    ridx, rdist = oracle.bruteforce(w.left.descriptors, w.right.descriptors, cfg.t_match,
+                                    cfg.ratio, 4)
+    np.testing.assert_array_equal(idx, ridx)
+    np.testing.assert_array_equal(dist, rdist)
+    frame = w.frame()
+    kp, kd, ko = ft.run_phase_a(w.local.soa, frame, w.pose, w.cam, pcfg, 1.2, 8)
+    grid = oracle.frame_grid(w.left.u, w.left.v, w.cam.width, w.cam.height, 48) + (48,)
+    rkp, rkd, rko = oracle.run_phase_a(w.local.soa, w.left.u, w.left.v, w.left.octave,
+                                       w.left.descriptors, grid, w.pose, w.cam, pcfg, 1.2, 8)
+    np.testing.assert_array_equal(kp, rkp)
+    np.testing.assert_array_equal(kd, rkd)
+    np.testing.assert_array_equal(ko, rko)
+
+
+def test_projection_fp64_audit_many_points(oracle):
+    """Transcendental audit (SURVEY §7 hard part 1): 1e6 random fisheye and
+    pinhole map points near frustum edges, device vs oracle phase A."""
+    from paper_2509_10757_b200.synthetic import make_workload
+    for fish in (False, True):
+        w = make_workload(seed=31, n_landmarks=6000, map_points=2000, fisheye=fish)
+        rng = np.random.default_rng(5)
+        m = 200_000
+        pts = ft.MapPointSoA(
+            positions=rng.uniform(-6, 6, size=(m, 3)) + np.array([4.0, 0, 0]),
+            descriptors=w.local.soa.descriptors[rng.integers(0, 2000, m)],
+            normals=np.tile(np.array([[1.0, 0, 0]]), (m, 1)),
+            min_distances=np.full(m, 0.1), max_distances=rng.uniform(2, 12, m),
+            point_ids=np.arange(m, dtype=np.int64))
+        pcfg = ProjectionSearchConfig(view_cos_min=-1.0)
+        frame = w.frame()
+        kp, kd, ko = ft.run_phase_a(pts, frame, w.pose, w.cam, pcfg, 1.2, 8)
+        grid = oracle.frame_grid(w.left.u, w.left.v, w.cam.width, w.cam.height, 48) + (48,)
+        rkp, rkd, rko = oracle.run_phase_a(pts, w.left.u, w.left.v, w.left.octave,
+                                           w.left.descriptors, grid, w.pose, w.cam, pcfg, 1.2, 8,
+                                           nthreads=8)
+        np.testing.assert_array_equal(kp, rkp)
+        np.testing.assert_array_equal(ko, rko)
+        np.testing.assert_array_equal(kd, rkd)
