@@ -1,0 +1,468 @@
+"""Benchmark: stereo + local-map tracking at EuRoC shape on B200.
+
+Metric (BASELINE.json): "stereo+local-map tracking ms/frame and frames/s at
+EuRoC shape, 1/2/4/8 B200".  Workload = BASELINE configs[1] (cfg2): one
+EuRoC-shaped stereo frame (752x480, ~1270 keypoints per image, 8 levels,
+scale 1.2, rendered textured images so stereo phase 2 runs on real pyramids)
+plus a 5000-point local map; a step is one frame per stream through
+
+    stereo:  phase 1 -> SAD phase 2 -> median-SAD rejection   (ft_stereo_pinhole)
+    map:     skip slotted -> project -> window search -> resolve -> slot write
+                                                               (ft_project_search)
+
+Default: 1 stream per GPU (single-stream latency = ms_per_step).  Under
+torchrun each rank drives its own GPU with independent streams (weak scaling,
+no collective on the data path; NCCL only for the barrier and max-time).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--streams S]
+    python bench.py --impl reference ...    # CPU oracle arm (host cores)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0
+
+
+def parse() -> argparse.Namespace:
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--streams", type=int, default=1, help="frame streams per GPU")
+    p.add_argument("--frames", type=int, default=8, help="distinct frames cycled per stream")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-images", action="store_true", help="feature bundles only (no phase 2)")
+    p.add_argument("--batched-streams", type=int, default=64,
+                   help="extra batched measurement (0 disables)")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--quick", action="store_true", help="skip cpu baseline / batched (profiling)")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+def make_frames(n: int, seed0: int, images: bool):
+    from paper_2509_10757_b200.synthetic import make_workload
+    return [make_workload(seed=seed0 + i, n_landmarks=12000, map_points=5000, images=images,
+                          offset=0.05 * i) for i in range(n)]
+
+
+def algorithmic_units(w) -> dict:
+    """Per-frame work the reference algorithm performs:
+    phase-1 Hamming evaluations (pairs passing the octave/band/disparity
+    predicates), SAD candidates, projection-window Hamming evaluations, and
+    unique bytes (stereo: keypoints 64 B/kp/side + both pyramids; map: 104 B
+    per point + 64 B per keypoint)."""
+    from paper_2509_10757_b200.types import StereoMatchConfig
+    cfg = StereoMatchConfig()
+    L, R = w.left, w.right
+    band = cfg.band_factor * w.scale_pow[L.octave]
+    dv = np.abs(R.v[None, :] - L.v[:, None])
+    disp = L.u[:, None] - R.u[None, :]
+    rows = np.clip(np.round(R.v), 0, w.cam.height - 1)
+    r0 = np.maximum(np.floor(L.v - band), 0)
+    r1 = np.minimum(np.ceil(L.v + band), w.cam.height - 1)
+    in_rows = (rows[None, :] >= r0[:, None]) & (rows[None, :] <= r1[:, None])
+    ok = (in_rows & (np.abs(R.octave[None, :] - L.octave[:, None]) <= 1) & (dv <= band[:, None])
+          & (disp >= cfg.min_disparity) & (disp <= cfg.max_disparity))
+    ham_p1 = int(ok.sum())
+    cand = int((ok.any(axis=1)).sum())
+    n_l, n_r = len(L.u), len(R.u)
+    pyr_bytes = 2 * int(w.pyr_left.offsets[-1]) if w.pyr_left is not None else 0
+    m = len(w.local.point_ids)
+    return {"hamming_phase1": ham_p1, "sad_candidates": cand,
+            "sad_absdiff": cand * 11 * 121,
+            "stereo_bytes": (n_l + n_r) * 64 + pyr_bytes,
+            "map_bytes": m * 104 + n_l * 64}
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+class ClockSampler:
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self) -> dict:
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline (oracle port on host cores)
+
+def cpu_frame(w, nthreads: int) -> int:
+    """One frame through the oracle: stereo (phase 1 -> phase 2 | from-cand ->
+    reject), FrameGrid, search_local_points.  Returns the filled slots."""
+    from oracle import oracle as O
+    from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
+    O.stereo_pinhole(w.left, w.right, w.pyr_left, w.pyr_right, w.cam, StereoMatchConfig(),
+                     w.scale_pow, nthreads)
+    grid = O.frame_grid(w.left.u, w.left.v, w.cam.width, w.cam.height, 48) + (48,)
+    slots = np.full(len(w.left.u), -1, np.int64)
+    return O.search_local_points(w.local.point_ids, w.local.soa, w.left.u, w.left.v,
+                                 w.left.octave, w.left.descriptors, grid, slots, w.pose, w.cam,
+                                 ProjectionSearchConfig(), 1.2, 8, nthreads)
+
+
+def cpu_frames_per_s(frames, seconds: float, nthreads: int) -> tuple[float, int]:
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        cpu_frame(frames[done % len(frames)], nthreads)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= seconds and done >= 3:
+            return done / el, done
+
+
+def cpu_baseline(frames, seconds: float) -> dict:
+    from oracle import oracle as O
+    O.lib()
+    nmax = max(1, O.max_threads())
+    best = None
+    for nt in sorted({1, nmax}):
+        fps, n = cpu_frames_per_s(frames, seconds / 2, nt)
+        if best is None or fps > best[0]:
+            best = (fps, n, nt)
+    return {"value": best[0], "unit": "frames/s", "cores": best[2], "kind": "port",
+            "sample": f"{best[1]} cfg2 frames (stereo phase1+phase2+reject, FrameGrid, "
+                      f"search_local_points) in ~{seconds / 2:.0f} s, oracle/ft_oracle.c "
+                      f"OpenMP over items, best of 1 and {nmax} threads"}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    frames = make_frames(min(args.frames, 4), 1000, not args.no_images)
+    from oracle import oracle as O
+    O.lib()
+    nt = max(1, O.max_threads())
+    for k in range(args.warmup):
+        cpu_frame(frames[k % len(frames)], nt)
+    per_step = []
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        for s in range(args.streams):
+            cpu_frame(frames[(k + s) % len(frames)], nt)
+        per_step.append(time.perf_counter() - t0)
+    total = sum(per_step)
+    value = args.streams * args.steps / total
+    line = {"metric": "stereo+local-map tracking frames/s at EuRoC shape", "impl": "reference",
+            "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32",
+            "data": "synthetic", "config": config_dict(args),
+            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": nt, "kind": "port",
+                             "sample": f"{args.streams * args.steps} cfg2 frames through "
+                                       "oracle/ft_oracle.c (C port of the reference numba "
+                                       "kernels), OpenMP over items"},
+            "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def config_dict(args) -> dict:
+    return {"workload": "cfg2: EuRoC-shaped stereo frame 752x480 (~1270 kps/image, 8 levels, "
+                        "scale 1.2" + (", rendered pyramids -> SAD phase 2" if not args.no_images
+                                       else ", feature bundle") +
+                        ") + 5000-point local map; stereo + SearchLocalPoints per frame",
+            "streams_per_gpu": args.streams, "frames_cycled": args.frames,
+            "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": f"independent frame streams x {args.gpus} GPU (no collective)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def main() -> None:
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2509_10757_b200 import _lib
+    from paper_2509_10757_b200.pipeline import FramePipeline
+
+    images = not args.no_images
+    frames = make_frames(args.frames, 1000 + 97 * rank, images)
+    w0 = frames[0]
+    cap_kp = int(max(max(len(f.left.u), len(f.right.u)) for f in frames) + 31) // 32 * 32
+    cap_pts = int(max(len(f.local.point_ids) for f in frames) + 255) // 256 * 256
+    S = args.streams
+    pipe = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
+                         pyramid_geometry=w0.pyr_left if images else None)
+
+    def load(step: int) -> None:
+        for s in range(S):
+            f = frames[(step + s) % len(frames)]
+            pipe.load_frame(s, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def l2_flush():
+        with torch.cuda.stream(pipe.stream):
+            flush.fill_(1)
+
+    load(0)
+    pipe.capture()
+    # correctness spot check of the resident pipeline against the oracle (rank 0, stream 0)
+    pipe.replay(copies=True)
+    pipe.synchronize()
+    check = spot_check(pipe, frames[0]) if rank == 0 else None
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    # ---- value: inputs resident in HBM, compute graph only -----------------
+    for k in range(args.warmup):
+        load(k)
+        pipe.replay(copies=True)
+    pipe.synchronize()
+    comp_ms = []
+    with ClockSampler(local_rank) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            load(k)
+            with torch.cuda.stream(pipe.stream):
+                pipe.dev[:pipe.in_end].copy_(pipe.host[:pipe.in_end], non_blocking=True)
+            l2_flush()
+            a, b = ev(), ev()
+            a.record(pipe.stream)
+            pipe.replay(copies=False)
+            b.record(pipe.stream)
+            pipe.synchronize()
+            comp_ms.append(a.elapsed_time(b))
+        torch.cuda.synchronize()
+        # ---- e2e: pinned host inputs -> H2D -> compute -> D2H, host wall clock
+        e2e_ms, e2e_ev_ms = [], []
+        for k in range(args.steps):
+            load(k)
+            l2_flush()
+            pipe.synchronize()
+            a, b = ev(), ev()
+            t0 = time.perf_counter()
+            a.record(pipe.stream)
+            pipe.replay(copies=True)
+            b.record(pipe.stream)
+            pipe.synchronize()
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+            e2e_ev_ms.append(a.elapsed_time(b))
+        if dist:
+            dist.barrier()
+    clocks = clk.summary()
+
+    # ---- per-kernel timing for the roofline (eager, on the launching stream)
+    kern = {"stereo": [], "project": []}
+    for k in range(max(10, args.steps // 2)):
+        load(k)
+        with torch.cuda.stream(pipe.stream):
+            pipe.dev[:pipe.in_end].copy_(pipe.host[:pipe.in_end], non_blocking=True)
+        for name, fn in (("stereo", pipe.launch_stereo), ("project", pipe.launch_project)):
+            l2_flush()
+            a, b = ev(), ev()
+            a.record(pipe.stream)
+            fn(pipe.stream)
+            b.record(pipe.stream)
+            pipe.synchronize()
+            kern[name].append(a.elapsed_time(b))
+    stereo_ms, project_ms = float(np.median(kern["stereo"])), float(np.median(kern["project"]))
+
+    tot_comp = sum(comp_ms)
+    tot_e2e = sum(e2e_ms)
+    if dist:
+        t = torch.tensor([tot_comp, tot_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_comp, tot_e2e = float(t[0]), float(t[1])
+    frames_total = world * S * args.steps
+    value = frames_total / (tot_comp / 1e3)
+    e2e_value = frames_total / (tot_e2e / 1e3)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    units = algorithmic_units(w0)
+    peaks = json.loads(PEAKS_FILE.read_text()) if PEAKS_FILE.exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM))
+    dominant = "stereo" if stereo_ms >= project_ms else "project"
+    dom_ms = max(stereo_ms, project_ms)
+    dom_bytes = S * (units["stereo_bytes"] if dominant == "stereo" else units["map_bytes"])
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    popc = popc_peak(torch, _lib)
+    ham = S * units["hamming_phase1"]
+    roofline = {"bound": "hbm", "kernel": f"ft_{dominant}", "achieved": achieved,
+                "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": None, "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+                "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": dom_ms,
+                "note": "single-frame launches are latency-bound (~10 us of work per kernel); "
+                        "see roofline_int and batched for the pipe-bound view"}
+    line = {"metric": "stereo+local-map tracking frames/s at EuRoC shape", "value": value,
+            "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_comp / args.steps, "latency_ms_per_frame": tot_comp / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64+u32", "data": "synthetic", "config": config_dict(args),
+            "e2e": {"value": e2e_value, "unit": "frames/s",
+                    "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes(),
+                    "ms_per_step_wall": tot_e2e / args.steps,
+                    "ms_per_step_events": float(np.sum(e2e_ev_ms)) / args.steps},
+            "roofline": roofline,
+            "roofline_int": {"bound": "popc", "kernel": "ft_stereo (phase 1)",
+                             "hamming_per_launch": ham, "popc_per_launch": 8 * ham,
+                             "achieved_gpopc_s": 8 * ham / (stereo_ms / 1e3) / 1e9,
+                             "peak_gpopc_s": popc, "frac": (8 * ham / (stereo_ms / 1e3) / 1e9) / popc
+                             if popc else None},
+            "kernels_ms": {"ft_stereo_pinhole": stereo_ms, "ft_project_search": project_ms},
+            "work_per_frame": units, "clocks": clocks,
+            "gpu_launches": 4 * args.steps, "parity_spot_check": check}
+    if not args.quick:
+        if args.batched_streams > 0 and world == 1:
+            line["batched"] = batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts,
+                                          images, flush)
+        line["cpu_baseline"] = cpu_baseline(frames[:2], args.cpu_seconds)
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def spot_check(pipe, w) -> bool:
+    from oracle import oracle as O
+    from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
+    r = pipe.result(0, len(w.left.u))
+    ref = O.stereo_pinhole(w.left, w.right, w.pyr_left, w.pyr_right, w.cam, StereoMatchConfig(),
+                           w.scale_pow)
+    ok = all(np.array_equal(getattr(r.matches, f), getattr(ref, f))
+             for f in ("right_idx", "distance", "disparity", "refined_u", "depth", "sad"))
+    grid = O.frame_grid(w.left.u, w.left.v, w.cam.width, w.cam.height, 48) + (48,)
+    slots = np.full(len(w.left.u), -1, np.int64)
+    n = O.search_local_points(w.local.point_ids, w.local.soa, w.left.u, w.left.v, w.left.octave,
+                              w.left.descriptors, grid, slots, w.pose, w.cam,
+                              ProjectionSearchConfig(), 1.2, 8)
+    ok = ok and n == r.n_slots and np.array_equal(slots, r.slots)
+    if not ok:
+        raise SystemExit("bench spot check FAILED: pipeline output differs from the oracle")
+    return ok
+
+
+def popc_peak(torch, _lib) -> float | None:
+    """Measured POPC throughput (G popc/s) of ft_bench_popc at full occupancy."""
+    L = _lib.load()
+    sink = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, threads, iters = sms * 8, 256, 4096
+    s = torch.cuda.current_stream()
+    for _ in range(2):
+        _lib.check(L.ft_bench_popc(blocks, threads, iters, sink.data_ptr(), s.cuda_stream), "popc")
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    _lib.check(L.ft_bench_popc(blocks, threads, iters, sink.data_ptr(), s.cuda_stream), "popc")
+    b.record(s)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    return blocks * threads * iters * 8 / (ms / 1e3) / 1e9
+
+
+def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flush) -> dict:
+    S = args.batched_streams
+    w0 = frames[0]
+    pipe = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
+                         pyramid_geometry=w0.pyr_left if images else None)
+    for s in range(S):
+        f = frames[s % len(frames)]
+        pipe.load_frame(s, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
+    pipe.capture()
+    steps = max(5, args.steps // 5)
+    for _ in range(3):
+        pipe.replay(copies=True)
+    pipe.synchronize()
+    comp, e2e = [], []
+    for _ in range(steps):
+        with torch.cuda.stream(pipe.stream):
+            flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(pipe.stream)
+        pipe.replay(copies=False)
+        b.record(pipe.stream)
+        pipe.synchronize()
+        comp.append(a.elapsed_time(b))
+        with torch.cuda.stream(pipe.stream):
+            flush.fill_(1)
+        pipe.synchronize()
+        t0 = time.perf_counter()
+        pipe.replay(copies=True)
+        pipe.synchronize()
+        e2e.append(1e3 * (time.perf_counter() - t0))
+    return {"streams": S, "steps": steps, "ms_per_step": float(np.mean(comp)),
+            "frames_per_s": S * steps / (sum(comp) / 1e3),
+            "e2e_frames_per_s": S * steps / (sum(e2e) / 1e3),
+            "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes()}
+
+
+if __name__ == "__main__":
+    main()

@@ -173,8 +173,10 @@ typedef struct {
     const double *trans;        /* DEVICE [F][3] */
     const uint8_t *skip;        /* [F*cap_points] explicit skip mask; may be NULL */
     const double *ref_angles;   /* [F*cap_points] for the rotation check; may be NULL */
-    int64_t *slots;             /* [F*cap_kp] frame slots (read for SKIP_SLOTS,
-                                   updated by WRITE_SLOTS) */
+    const int64_t *slots_in;    /* [F*cap_kp] frame slots before the search (read by
+                                   SKIP_SLOTS and by the "only if empty" rule) */
+    int64_t *slots_out;         /* [F*cap_kp] slots after WRITE_SLOTS; may equal
+                                   slots_in (in place) */
 } ft_project_io;
 
 typedef struct {

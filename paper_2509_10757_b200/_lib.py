@@ -74,7 +74,8 @@ class FtProjectParams(ctypes.Structure):
 
 
 class FtProjectIO(ctypes.Structure):
-    _fields_ = [("rot", vp), ("trans", vp), ("skip", vp), ("ref_angles", vp), ("slots", vp)]
+    _fields_ = [("rot", vp), ("trans", vp), ("skip", vp), ("ref_angles", vp), ("slots_in", vp),
+                ("slots_out", vp)]
 
 
 class FtProjectOut(ctypes.Structure):

@@ -279,20 +279,26 @@ __device__ void resolve_frame(const ProjArgs &a, int f, int n_pts, int n_kp, int
     }
     if (threadIdx.x == 0 && a.o.corr_count) a.o.corr_count[f] = n_final;
     if (a.mode & FT_PROJ_WRITE_SLOTS) {
-        // localmap.py:113-121: write only empty slots; each keypoint appears
-        // at most once among the winners, so the writes never race.
+        // localmap.py:113-121: write only slots that were empty before the
+        // search; each keypoint appears at most once among the winners, so
+        // the writes never race.
+        if (a.io.slots_out != a.io.slots_in) {
+            for (int k = threadIdx.x; k < n_kp; k += PS_THREADS)
+                a.io.slots_out[kbase + k] = a.io.slots_in[kbase + k];
+            __syncthreads();
+        }
         for (int c = threadIdx.x; c < n_final; c += PS_THREADS) {
             const long long kp = __ldcg(a.o.corr_kp + pbase + c);
             const long long pi = __ldcg(a.o.corr_point + pbase + c);
-            int64_t *slot = a.io.slots + kbase + kp;
-            if (*slot == NO_POINT_ID) *slot = a.P.point_ids[pbase + pi];
+            if (a.io.slots_in[kbase + kp] == NO_POINT_ID)
+                a.io.slots_out[kbase + kp] = a.P.point_ids[pbase + pi];
         }
         __syncthreads();
         if (threadIdx.x == 0) misc[1] = 0;
         __syncthreads();
         int filled = 0;
         for (int k = threadIdx.x; k < n_kp; k += PS_THREADS)
-            filled += __ldcg(a.io.slots + kbase + k) != NO_POINT_ID;
+            filled += __ldcg(a.io.slots_out + kbase + k) != NO_POINT_ID;
         atomicAdd(&misc[1], filled);
         __syncthreads();
         if (threadIdx.x == 0 && a.o.slot_count) a.o.slot_count[f] = misc[1];
@@ -354,7 +360,7 @@ __global__ void __launch_bounds__(PS_THREADS) project_search_kernel(const ProjAr
             for (int h = threadIdx.x; h < (1 << a.hash_bits); h += PS_THREADS) htab[h] = HASH_EMPTY;
             __syncthreads();
             for (int k = threadIdx.x; k < n_kp; k += PS_THREADS) {
-                const long long id = a.io.slots[kbase + k];
+                const long long id = a.io.slots_in[kbase + k];
                 if (id != NO_POINT_ID) hash_insert(htab, a.hash_bits, id);
             }
         }
@@ -464,7 +470,8 @@ extern "C" int ft_project_search(int32_t n_frames, const ft_map_points *points,
         return FT_E_RANGE;
     if (params->histogram_bins < 1 || params->histogram_bins > MAX_BINS) return FT_E_CONFIG;
     if (!io->rot || !io->trans) return FT_E_NULL;
-    if ((mode & (FT_PROJ_SKIP_SLOTS | FT_PROJ_WRITE_SLOTS)) && !io->slots) return FT_E_NULL;
+    if ((mode & (FT_PROJ_SKIP_SLOTS | FT_PROJ_WRITE_SLOTS)) && !io->slots_in) return FT_E_NULL;
+    if ((mode & FT_PROJ_WRITE_SLOTS) && !io->slots_out) return FT_E_NULL;
     if ((mode & FT_PROJ_WRITE_SLOTS) && !(mode & FT_PROJ_RESOLVE)) return FT_E_CONFIG;
     if ((mode & FT_PROJ_RESOLVE) &&
         (!out->corr_point || !out->corr_kp || !out->corr_dist || !out->corr_oct))

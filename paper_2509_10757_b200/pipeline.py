@@ -1,0 +1,263 @@
+"""Resident, graph-captured per-frame hot path for S independent frame
+streams on one B200 (BASELINE cfg 2/4/5).
+
+One step processes one frame of every stream:
+
+    pinned staging --(1 H2D)--> device inputs
+        stream A: ft_stereo_pinhole   phase 1 -> phase 2 | from-candidates -> reject
+        stream B: ft_project_search   skip-slotted -> phase A -> resolve -> slot write
+    device results --(1 D2H)--> pinned results
+
+Stereo and the local-map search are independent within a frame (the
+reference runs them in sequence only because it is single-threaded,
+tracker.py:268-358), so they run concurrently on two streams.  The whole step
+is captured ONCE as a CUDA graph; per-frame counts live in device memory, so
+replays need no re-capture.  Layout: every per-frame array is at a fixed
+stride (capacity) per stream, inputs packed first (one contiguous H2D range),
+outputs last (one contiguous D2H range).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .runtime import Layout, make_workspace, project_params, pyramid_struct, stereo_params
+from .types import ProjectionSearchConfig, StereoMatchConfig, StereoMatches
+
+
+@dataclass
+class StreamResult:
+    matches: StereoMatches
+    slots: np.ndarray
+    n_slots: int
+    n_matched: int
+
+
+class FramePipeline:
+    def __init__(self, cam, n_streams: int = 1, cap_kp: int = 2048, cap_points: int = 8192,
+                 pyramid_geometry=None, stereo_cfg: StereoMatchConfig | None = None,
+                 proj_cfg: ProjectionSearchConfig | None = None, scale: float = 1.2,
+                 levels: int = 8, grid_cell_px: int = 48, device: int | None = None):
+        if not torch.cuda.is_available():
+            raise _lib.FtError("FramePipeline needs a CUDA device (no CPU fallback)")
+        self.lib = _lib.load()
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.cam = cam
+        self.S = int(n_streams)
+        self.cap_kp = int(cap_kp)
+        self.cap_pts = int(cap_points)
+        self.scfg = stereo_cfg or StereoMatchConfig()
+        self.pcfg = proj_cfg or ProjectionSearchConfig()
+        self.scale, self.levels = float(scale), int(levels)
+        self.scale_pow = self.scale ** np.arange(self.levels, dtype=np.float64)
+        self.pyr = pyramid_geometry  # object with widths / heights / offsets, or None
+        self.cell = int(grid_cell_px)
+        self.nx = max(1, (int(cam.width) + self.cell - 1) // self.cell)
+        self.ny = max(1, (int(cam.height) + self.cell - 1) // self.cell)
+
+        S, ck, cp = self.S, self.cap_kp, self.cap_pts
+        lay = Layout()
+        for side in ("L", "R"):
+            lay.add(f"{side}_n", 4 * S)
+            lay.add(f"{side}_u", 8 * S * ck)
+            lay.add(f"{side}_v", 8 * S * ck)
+            lay.add(f"{side}_oct", 4 * S * ck)
+            lay.add(f"{side}_desc", 32 * S * ck)
+        self.pyr_bytes = int(self.pyr.offsets[-1]) if self.pyr is not None else 0
+        if self.pyr is not None:
+            lay.add("pyr_l", S * self.pyr_bytes)
+            lay.add("pyr_r", S * self.pyr_bytes)
+        lay.add("P_n", 4 * S)
+        lay.add("P_pos", 24 * S * cp)
+        lay.add("P_nrm", 24 * S * cp)
+        lay.add("P_mind", 8 * S * cp)
+        lay.add("P_maxd", 8 * S * cp)
+        lay.add("P_desc", 32 * S * cp)
+        lay.add("P_ids", 8 * S * cp)
+        lay.add("rot", 72 * S)
+        lay.add("trans", 24 * S)
+        lay.add("slots_in", 8 * S * ck)
+        self.in_end = lay.total
+        self.out_begin = lay.total
+        lay.add("slots", 8 * S * ck)   # updated slots (output)
+        for name in ("right_idx", "distance", "disparity", "refined_u", "depth", "sad"):
+            lay.add(name, 8 * S * ck)
+        lay.add("n_matched", 4 * S)
+        lay.add("slot_n", 4 * S)
+        lay.add("c_n", 4 * S)
+        self.out_end = lay.total
+        # device-only scratch (not copied)
+        lay.add("cand_idx", 8 * S * ck)
+        lay.add("cand_dist", 8 * S * ck)
+        for name in ("c_point", "c_kp", "c_dist", "c_oct"):
+            lay.add(name, 8 * S * cp)
+        self.lay = lay
+        self.dev = torch.zeros(lay.total, dtype=torch.uint8, device=self.device)
+        self.host = torch.zeros(lay.total, dtype=torch.uint8).pin_memory()
+        self.hnp = self.host.numpy()
+        self.stream = torch.cuda.Stream(self.device)
+        self.stream_b = torch.cuda.Stream(self.device)
+        self.ws = make_workspace(self.lib, self.device, self.stream, S, ck, cp)
+        self._build_structs()
+        self.graph = None
+        self.graph_compute = None
+
+    # -- host views ------------------------------------------------------------
+
+    def _h(self, name: str, dtype, shape) -> np.ndarray:
+        off = self.lay.offsets[name]
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        return self.hnp[off:off + n].view(dtype).reshape(shape)
+
+    def _d(self, name: str) -> int:
+        return self.dev.data_ptr() + self.lay.offsets[name]
+
+    def load_frame(self, s: int, left, right, local, pose, pyr_left=None, pyr_right=None,
+                   slots=None) -> None:
+        """Copy stream s's frame inputs into the pinned staging area."""
+        S, ck, cp = self.S, self.cap_kp, self.cap_pts
+        for side, fs in (("L", left), ("R", right)):
+            n = len(fs.u)
+            if n > ck:
+                raise ValueError(f"{n} keypoints exceed capacity {ck}")
+            self._h(f"{side}_n", np.int32, (S,))[s] = n
+            self._h(f"{side}_u", np.float64, (S, ck))[s, :n] = fs.u
+            self._h(f"{side}_v", np.float64, (S, ck))[s, :n] = fs.v
+            self._h(f"{side}_oct", np.int32, (S, ck))[s, :n] = fs.octave
+            self._h(f"{side}_desc", np.uint64, (S, ck, 4))[s, :n] = np.asarray(fs.descriptors).reshape(n, 4)
+        if self.pyr is not None:
+            if pyr_left is None or pyr_right is None:
+                raise ValueError("pipeline was built with pyramids: pass pyr_left / pyr_right")
+            pb = self.pyr_bytes
+            self._h("pyr_l", np.uint8, (S, pb))[s] = pyr_left.data
+            self._h("pyr_r", np.uint8, (S, pb))[s] = pyr_right.data
+        soa = local.soa
+        m = len(local.point_ids)
+        if m > cp:
+            raise ValueError(f"{m} map points exceed capacity {cp}")
+        self._h("P_n", np.int32, (S,))[s] = m
+        self._h("P_pos", np.float64, (S, cp, 3))[s, :m] = np.asarray(soa.positions).reshape(m, 3)
+        self._h("P_nrm", np.float64, (S, cp, 3))[s, :m] = np.asarray(soa.normals).reshape(m, 3)
+        self._h("P_mind", np.float64, (S, cp))[s, :m] = soa.min_distances
+        self._h("P_maxd", np.float64, (S, cp))[s, :m] = soa.max_distances
+        self._h("P_desc", np.uint64, (S, cp, 4))[s, :m] = np.asarray(soa.descriptors).reshape(m, 4)
+        self._h("P_ids", np.int64, (S, cp))[s, :m] = soa.point_ids
+        self._h("rot", np.float64, (S, 9))[s] = np.asarray(pose.rotation).reshape(9)
+        self._h("trans", np.float64, (S, 3))[s] = np.asarray(pose.translation).reshape(3)
+        sl = self._h("slots_in", np.int64, (S, ck))
+        sl[s] = -1
+        if slots is not None:
+            sl[s, :len(left.u)] = slots
+
+    def h2d_bytes(self) -> int:
+        return self.in_end
+
+    def d2h_bytes(self) -> int:
+        return self.out_end - self.out_begin
+
+    # -- launch ----------------------------------------------------------------
+
+    def _build_structs(self) -> None:
+        S, ck, cp = self.S, self.cap_kp, self.cap_pts
+        kps = {}
+        for side in ("L", "R"):
+            k = _lib.FtKeypoints()
+            k.u, k.v = self._d(f"{side}_u"), self._d(f"{side}_v")
+            k.octave, k.desc = self._d(f"{side}_oct"), self._d(f"{side}_desc")
+            k.angle, k.count, k.cap = None, self._d(f"{side}_n"), ck
+            kps[side] = k
+        self.kl, self.kr = kps["L"], kps["R"]
+        self.pl = pyramid_struct(self.pyr, self._d("pyr_l"), self.pyr_bytes) if self.pyr is not None else None
+        self.pr = pyramid_struct(self.pyr, self._d("pyr_r"), self.pyr_bytes) if self.pyr is not None else None
+        self.sparams = stereo_params(self.scfg, int(self.cam.height), self.scale_pow,
+                                     float(self.cam.baseline_times_fx))
+        self.smode = _lib.FT_STEREO_PHASE1 | _lib.FT_STEREO_REJECT | (
+            _lib.FT_STEREO_REFINE if self.pyr is not None else _lib.FT_STEREO_FROM_CAND)
+        o = _lib.FtStereoOut()
+        for name in ("cand_idx", "cand_dist", "right_idx", "distance", "disparity", "refined_u",
+                     "depth", "sad", "n_matched"):
+            setattr(o, name, self._d(name))
+        self.sout = o
+        P = _lib.FtMapPoints()
+        P.positions, P.normals = self._d("P_pos"), self._d("P_nrm")
+        P.min_dist, P.max_dist = self._d("P_mind"), self._d("P_maxd")
+        P.desc, P.point_ids, P.count, P.cap = self._d("P_desc"), self._d("P_ids"), self._d("P_n"), cp
+        self.points = P
+        self.pparams = project_params(self.cam, self.pcfg, self.scale, self.levels, self.cell,
+                                      self.nx, self.ny, None, 0.0)
+        io = _lib.FtProjectIO()
+        io.rot, io.trans, io.skip, io.ref_angles = self._d("rot"), self._d("trans"), None, None
+        io.slots_in, io.slots_out = self._d("slots_in"), self._d("slots")
+        self.pio = io
+        po = _lib.FtProjectOut()
+        po.corr_point, po.corr_kp = self._d("c_point"), self._d("c_kp")
+        po.corr_dist, po.corr_oct = self._d("c_dist"), self._d("c_oct")
+        po.corr_count, po.slot_count = self._d("c_n"), self._d("slot_n")
+        self.pout = po
+        self.pmode = (_lib.FT_PROJ_RESOLVE | _lib.FT_PROJ_SKIP_SLOTS | _lib.FT_PROJ_WRITE_SLOTS)
+
+    def launch_stereo(self, stream) -> None:
+        _lib.check(self.lib.ft_stereo_pinhole(self.S, self.kl, self.kr, self.pl, self.pr,
+                                              self.sparams, self.smode, self.sout, self.ws,
+                                              stream.cuda_stream), "ft_stereo_pinhole")
+
+    def launch_project(self, stream) -> None:
+        _lib.check(self.lib.ft_project_search(self.S, self.points, self.kl, self.pparams,
+                                              self.pio, self.pmode, self.pout, self.ws,
+                                              stream.cuda_stream), "ft_project_search")
+
+    def _step(self, copies: bool) -> None:
+        a, b = self.stream, self.stream_b
+        if copies:
+            with torch.cuda.stream(a):
+                self.dev[:self.in_end].copy_(self.host[:self.in_end], non_blocking=True)
+        b.wait_stream(a)
+        self.launch_stereo(a)
+        self.launch_project(b)
+        a.wait_stream(b)
+        if copies:
+            with torch.cuda.stream(a):
+                self.host[self.out_begin:self.out_end].copy_(
+                    self.dev[self.out_begin:self.out_end], non_blocking=True)
+
+    def run_eager(self, copies: bool = True) -> None:
+        self._step(copies)
+
+    def capture(self) -> None:
+        """Capture the full step (with copies) and the compute-only step."""
+        self.run_eager(True)  # warm: sets kernel attributes, loads modules
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self._step(True)
+        self.graph_compute = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph_compute, stream=self.stream):
+            self._step(False)
+        self.stream.synchronize()
+
+    def replay(self, copies: bool = True) -> None:
+        if self.graph is None:
+            self.capture()
+        # CUDAGraph.replay() launches on torch's current stream
+        with torch.cuda.stream(self.stream):
+            (self.graph if copies else self.graph_compute).replay()
+
+    def synchronize(self) -> None:
+        self.stream.synchronize()
+
+    # -- results ---------------------------------------------------------------
+
+    def result(self, s: int, n_left: int) -> StreamResult:
+        S, ck = self.S, self.cap_kp
+        g = lambda name, dt: self._h(name, dt, (S, ck))[s, :n_left].copy()  # noqa: E731
+        m = StereoMatches(right_idx=g("right_idx", np.int64), distance=g("distance", np.int64),
+                          disparity=g("disparity", np.float64),
+                          refined_u=g("refined_u", np.float64), depth=g("depth", np.float64),
+                          sad=g("sad", np.int64))
+        return StreamResult(matches=m, slots=g("slots", np.int64),
+                            n_slots=int(self._h("slot_n", np.int32, (S,))[s]),
+                            n_matched=int(self._h("n_matched", np.int32, (S,))[s]))

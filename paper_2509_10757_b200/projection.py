@@ -180,7 +180,7 @@ def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale:
         io.rot, io.trans = rt.ptr(lay, "rot"), rt.ptr(lay, "trans")
         io.skip = rt.ptr(lay, "skip") if skip_mask is not None else None
         io.ref_angles = rt.ptr(lay, "ref_ang") if with_angle else None
-        io.slots = rt.ptr(lay, "slots") if slots is not None else None
+        io.slots_in = io.slots_out = rt.ptr(lay, "slots") if slots is not None else None
         st = rt.lib.ft_project_search(1, _points_struct(rt, lay, cap_pts),
                                       keypoints_struct(rt, lay, "K", cap_kp), params, io, mode,
                                       _out_struct(rt, lay, phase_a_out), ws,
