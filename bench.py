@@ -86,7 +86,13 @@ def algorithmic_units(w) -> dict:
     n_l, n_r = len(L.u), len(R.u)
     pyr_bytes = 2 * int(w.pyr_left.offsets[-1]) if w.pyr_left is not None else 0
     m = len(w.local.point_ids)
-    return {"hamming_phase1": ham_p1, "sad_candidates": cand,
+    from oracle import oracle as O
+    from paper_2509_10757_b200.types import ProjectionSearchConfig
+    grid = O.frame_grid(L.u, L.v, w.cam.width, w.cam.height, 48) + (48,)
+    hc: list = []
+    O.run_phase_a(w.local.soa, L.u, L.v, L.octave, L.descriptors, grid, w.pose, w.cam,
+                  ProjectionSearchConfig(), 1.2, 8, ham_count=hc)
+    return {"hamming_phase1": ham_p1, "hamming_projection": hc[0], "sad_candidates": cand,
             "sad_absdiff": cand * 11 * 121,
             "stereo_bytes": (n_l + n_r) * 64 + pyr_bytes,
             "map_bytes": m * 104 + n_l * 64}
@@ -318,12 +324,13 @@ def main() -> None:
     clocks = clk.summary()
 
     # ---- per-kernel timing for the roofline (eager, on the launching stream)
-    kern = {"stereo": [], "project": []}
+    kern = {"track": [], "stereo_only": [], "map_only": []}
     for k in range(max(10, args.steps // 2)):
         load(k)
         with torch.cuda.stream(pipe.stream):
             pipe.dev[:pipe.in_end].copy_(pipe.host[:pipe.in_end], non_blocking=True)
-        for name, fn in (("stereo", pipe.launch_stereo), ("project", pipe.launch_project)):
+        for name, fn in (("track", pipe.launch_track), ("stereo_only", pipe.launch_stereo),
+                         ("map_only", pipe.launch_project)):
             l2_flush()
             a, b = ev(), ev()
             a.record(pipe.stream)
@@ -331,7 +338,7 @@ def main() -> None:
             b.record(pipe.stream)
             pipe.synchronize()
             kern[name].append(a.elapsed_time(b))
-    stereo_ms, project_ms = float(np.median(kern["stereo"])), float(np.median(kern["project"]))
+    track_ms = float(np.median(kern["track"]))
 
     tot_comp = sum(comp_ms)
     tot_e2e = sum(e2e_ms)
@@ -351,18 +358,16 @@ def main() -> None:
     units = algorithmic_units(w0)
     peaks = json.loads(PEAKS_FILE.read_text()) if PEAKS_FILE.exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM))
-    dominant = "stereo" if stereo_ms >= project_ms else "project"
-    dom_ms = max(stereo_ms, project_ms)
-    dom_bytes = S * (units["stereo_bytes"] if dominant == "stereo" else units["map_bytes"])
-    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    dom_bytes = S * (units["stereo_bytes"] + units["map_bytes"])
+    achieved = dom_bytes / (track_ms / 1e3) / 1e9
     popc = popc_peak(torch, _lib)
-    ham = S * units["hamming_phase1"]
-    roofline = {"bound": "hbm", "kernel": f"ft_{dominant}", "achieved": achieved,
+    ham = S * (units["hamming_phase1"] + units["hamming_projection"])
+    roofline = {"bound": "hbm", "kernel": "ft_track_frames", "achieved": achieved,
                 "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "traffic": None, "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
-                "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": dom_ms,
-                "note": "single-frame launches are latency-bound (~10 us of work per kernel); "
-                        "see roofline_int and batched for the pipe-bound view"}
+                "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": track_ms,
+                "note": "one frame per launch is latency-bound (dependent L2/HBM round trips "
+                        "and group barriers); see roofline_int and batched"}
     line = {"metric": "stereo+local-map tracking frames/s at EuRoC shape", "value": value,
             "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_comp / args.steps, "latency_ms_per_frame": tot_comp / args.steps,
@@ -373,14 +378,16 @@ def main() -> None:
                     "ms_per_step_wall": tot_e2e / args.steps,
                     "ms_per_step_events": float(np.sum(e2e_ev_ms)) / args.steps},
             "roofline": roofline,
-            "roofline_int": {"bound": "popc", "kernel": "ft_stereo (phase 1)",
+            "roofline_int": {"bound": "popc", "kernel": "ft_track_frames",
                              "hamming_per_launch": ham, "popc_per_launch": 8 * ham,
-                             "achieved_gpopc_s": 8 * ham / (stereo_ms / 1e3) / 1e9,
-                             "peak_gpopc_s": popc, "frac": (8 * ham / (stereo_ms / 1e3) / 1e9) / popc
-                             if popc else None},
-            "kernels_ms": {"ft_stereo_pinhole": stereo_ms, "ft_project_search": project_ms},
+                             "achieved_gpopc_s": 8 * ham / (track_ms / 1e3) / 1e9,
+                             "peak_gpopc_s": popc, "peak_source": "ft_bench_popc (measured)",
+                             "frac": (8 * ham / (track_ms / 1e3) / 1e9) / popc if popc else None},
+            "kernels_ms": {"ft_track_frames": track_ms,
+                           "stereo_only": float(np.median(kern["stereo_only"])),
+                           "map_only": float(np.median(kern["map_only"]))},
             "work_per_frame": units, "clocks": clocks,
-            "gpu_launches": 4 * args.steps, "parity_spot_check": check}
+            "gpu_launches": 2 * args.steps, "parity_spot_check": check}
     if not args.quick:
         if args.batched_streams > 0 and world == 1:
             line["batched"] = batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts,

@@ -30,6 +30,7 @@
  *                           (also tracker.py:415-427 _run_stereo, pinhole branch)
  *   ft_stereo_fisheye_bf    stereo.py:238-244       bruteforce_match_kernel as
  *                                                   launched by match_fisheye
+ *   ft_track_frames         tracker.py:279 + :354   stereo + SearchLocalPoints fused
  *   ft_project_search       projection.py:118-221   run_phase_a ->
  *                                                   resolve_conflicts ->
  *                                                   rotation_consistency_filter
@@ -222,6 +223,19 @@ int ft_stereo_fisheye_bf(int32_t n_frames, const ft_keypoints *left, const ft_ke
 int ft_project_search(int32_t n_frames, const ft_map_points *points, const ft_keypoints *frame,
                       const ft_project_params *params, const ft_project_io *io, int32_t mode,
                       const ft_project_out *out, const ft_workspace *ws, ft_stream_t stream);
+
+/* The whole per-frame hot path in ONE cooperative launch: pinhole stereo
+ * (ft_stereo_pinhole semantics, `smode`) on left/right and search by
+ * projection / SearchLocalPoints (ft_project_search semantics, `pmode`) of
+ * `points` into the LEFT keypoints, side by side in block groups.  Mirrors
+ * the reference tracker's per-frame calls tracker.py:279 (_run_stereo) and
+ * tracker.py:354 (search_local_points). */
+int ft_track_frames(int32_t n_frames, const ft_keypoints *left, const ft_keypoints *right,
+                    const ft_pyramid *left_pyr, const ft_pyramid *right_pyr,
+                    const ft_stereo_params *sparams, int32_t smode, const ft_stereo_out *sout,
+                    const ft_map_points *points, const ft_project_params *pparams,
+                    const ft_project_io *io, int32_t pmode, const ft_project_out *pout,
+                    const ft_workspace *ws, ft_stream_t stream);
 
 /* projection.py:161-178 resolve_conflicts on caller-held phase-A arrays
  * (one frame): correspondences in point order into out->corr_* and

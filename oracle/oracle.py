@@ -66,7 +66,7 @@ def lib():
             [c_dp, c_dp, c_dp, c_dp, c_u64p, c_u8p, I64, c_dp, c_dp, I64]
             + [F64] * 10
             + [c_dp, c_dp, c_i32p, c_u64p, c_i64p, c_i64p, I64, I64, I64, c_dp, I64, F64, F64,
-               I64, F64, F64, F64, c_i64p, c_i64p, c_i64p, INT])
+               I64, F64, F64, F64, c_i64p, c_i64p, c_i64p, INT, c_i64p])
         L.fto_resolve_conflicts.argtypes = [c_i64p, c_i64p, c_i64p, I64, I64, c_i64p, c_i64p,
                                             c_i64p, c_i64p]
         L.fto_resolve_conflicts.restype = I64
@@ -288,9 +288,10 @@ def camera_args(cam) -> tuple:
 
 def run_phase_a(points, kp_u, kp_v, kp_oct, kp_desc, grid, pose, cam, cfg, scale: float,
                 levels: int, skip_mask=None, window_px=None, u_offset: float = 0.0,
-                nthreads: int = 1):
+                nthreads: int = 1, ham_count: list | None = None):
     """projection.py:118-158 -> kernels.py:470-579.  ``grid`` is
-    (start, indices, nx, ny, cell_px)."""
+    (start, indices, nx, ny, cell_px).  ``ham_count`` (a list) receives the
+    number of Hamming evaluations performed (work accounting for bench.py)."""
     n = len(points.point_ids)
     out_kp = np.empty(n, dtype=np.int64)
     out_dist = np.empty(n, dtype=np.int64)
@@ -308,6 +309,7 @@ def run_phase_a(points, kp_u, kp_v, kp_oct, kp_desc, grid, pose, cam, cfg, scale
     rot, tr = _f64(pose.rotation), _f64(pose.translation)
     ku, kv, ko, kd = _f64(kp_u), _f64(kp_v), _i32(kp_oct), _u64(kp_desc)
     gs, gi = _i64(grid[0]), _i64(grid[1])
+    hc = ctypes.c_int64(0)
     lib().fto_project_search(
         _p(pos, c_dp), _p(nor, c_dp), _p(mind, c_dp), _p(maxd, c_dp), _p(pdesc, c_u64p),
         _p(skip, c_u8p), n, _p(rot, c_dp), _p(tr, c_dp), int(ca[0]),
@@ -316,7 +318,10 @@ def run_phase_a(points, kp_u, kp_v, kp_oct, kp_desc, grid, pose, cam, cfg, scale
         _p(gi, c_i64p), int(grid[2]), int(grid[3]), int(grid[4]), _p(scale_pow, c_dp),
         int(levels), 1.0 / math.log(scale), float(window), int(cfg.t_proj), float(cfg.ratio),
         float(cfg.view_cos_min), float(u_offset),
-        _p(out_kp, c_i64p), _p(out_dist, c_i64p), _p(out_oct, c_i64p), nthreads)
+        _p(out_kp, c_i64p), _p(out_dist, c_i64p), _p(out_oct, c_i64p), nthreads,
+        ctypes.byref(hc))
+    if ham_count is not None:
+        ham_count.append(int(hc.value))
     return out_kp, out_dist, out_oct
 
 

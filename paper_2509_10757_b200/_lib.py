@@ -92,7 +92,7 @@ _lib = None
 
 EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_workspace_init",
            "ft_hamming_pairs", "ft_stereo_pinhole", "ft_stereo_fisheye_bf", "ft_project_search",
-           "ft_resolve_conflicts", "ft_rotation_filter", "ft_bench_popc")
+           "ft_track_frames", "ft_resolve_conflicts", "ft_rotation_filter", "ft_bench_popc")
 
 
 def build(force: bool = False) -> Path:
@@ -126,6 +126,10 @@ def load() -> ctypes.CDLL:
                                        W, vp]
     L.ft_project_search.argtypes = [i32, P(FtMapPoints), P(FtKeypoints), P(FtProjectParams),
                                     P(FtProjectIO), i32, P(FtProjectOut), W, vp]
+    L.ft_track_frames.argtypes = [i32, P(FtKeypoints), P(FtKeypoints), P(FtPyramid),
+                                  P(FtPyramid), P(FtStereoParams), i32, P(FtStereoOut),
+                                  P(FtMapPoints), P(FtProjectParams), P(FtProjectIO), i32,
+                                  P(FtProjectOut), W, vp]
     L.ft_resolve_conflicts.argtypes = [i32, vp, vp, vp, i32, P(FtProjectOut), W, vp]
     L.ft_rotation_filter.argtypes = [i32, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp]
     L.ft_bench_popc.argtypes = [i32, i32, i32, vp, vp]

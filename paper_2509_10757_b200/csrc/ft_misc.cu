@@ -1,0 +1,188 @@
+// ft_misc.cu -- small C-ABI entries: the Hamming self-test kernel and the
+// standalone phase B / phase C kernels for callers that hold phase-A arrays.
+#include "ft_common.cuh"
+#include "ft_ws.cuh"
+
+namespace ft {
+
+constexpr unsigned long long NO_CLAIM = ~0ull;
+constexpr int MAX_BINS = 256;
+
+FT_DEV double py_mod_m(double a, double b) {  // numpy float remainder
+    double r = fmod(a, b);
+    if (r != 0.0 && ((b < 0.0) != (r < 0.0))) r += b;
+    return r;
+}
+
+// reference kernels.py:48-51
+__global__ void hamming_pairs_kernel(const uint64_t *a, const uint64_t *b, int64_t n,
+                                     int64_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = hamming(load_desc(a, i), load_desc(b, i));
+}
+
+}  // namespace ft
+
+using namespace ft;
+
+extern "C" int ft_hamming_pairs(const uint64_t *a, const uint64_t *b, int64_t n, int64_t *out,
+                                ft_stream_t stream) {
+    if (n < 0) return FT_E_RANGE;
+    if (n == 0) return FT_OK;
+    if (!a || !b || !out) return FT_E_NULL;
+    const int threads = 256;
+    int64_t blocks = (n + threads - 1) / threads;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    hamming_pairs_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(a, b, n, out);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Standalone phase B / phase C for callers that hold phase-A arrays
+// (reference projection.py:161-178 resolve_conflicts and :181-200
+// rotation_consistency_filter called on their own).  One frame.
+
+namespace ft {
+
+constexpr int RS_THREADS = 1024;
+
+__global__ void claim_kernel(const int64_t *out_kp, const int64_t *out_dist, int n, int n_kp,
+                             unsigned long long *claims) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const long long kp = out_kp[i];
+        if (kp < 0 || kp >= n_kp) continue;
+        atomicMin(claims + kp, ((unsigned long long)out_dist[i] << 32) | (unsigned)i);
+    }
+}
+
+__global__ void __launch_bounds__(RS_THREADS)
+compact_winners_kernel(const int64_t *out_kp, const int64_t *out_dist, const int64_t *out_oct,
+                       int n, int n_kp, unsigned long long *claims, int64_t *cp, int64_t *ck,
+                       int64_t *cd, int64_t *co, int32_t *count) {
+    __shared__ int scan_tmp[32];
+    int n_win = 0;
+    for (int r0 = 0; r0 < n; r0 += RS_THREADS) {
+        const int i = r0 + threadIdx.x;
+        int win = 0;
+        long long kp = -1;
+        if (i < n) {
+            kp = out_kp[i];
+            if (kp >= 0 && kp < n_kp)
+                win = claims[kp] == (((unsigned long long)out_dist[i] << 32) | (unsigned)i);
+        }
+        int total;
+        const int pos = n_win + block_exclusive_scan<RS_THREADS>(win, scan_tmp, total);
+        if (win) {
+            cp[pos] = i;
+            ck[pos] = kp;
+            cd[pos] = out_dist[i];
+            co[pos] = out_oct[i];
+        }
+        n_win += total;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += RS_THREADS) {
+        const long long kp = out_kp[i];
+        if (kp >= 0 && kp < n_kp) claims[kp] = NO_CLAIM;
+    }
+    if (threadIdx.x == 0) *count = n_win;
+}
+
+__global__ void __launch_bounds__(RS_THREADS)
+rotation_filter_kernel(int64_t *cp, int64_t *ck, int64_t *cd, int64_t *co, int m,
+                       const double *ref_angles, const double *kp_angles, int nbins, int keep_k,
+                       int32_t *count) {
+    __shared__ int scan_tmp[32];
+    __shared__ int hist[MAX_BINS];
+    __shared__ int keepw[MAX_BINS / 32];
+    const double two_pi = 2.0 * 3.141592653589793;
+    for (int b = threadIdx.x; b < nbins; b += RS_THREADS) hist[b] = 0;
+    __syncthreads();
+    auto bin_of = [&](int c) {
+        const double diff = py_mod_m(kp_angles[ck[c]] - ref_angles[cp[c]], two_pi);
+        long long b = (long long)floor(diff / two_pi * (double)nbins);
+        return (int)(b < 0 ? 0 : (b > nbins - 1 ? nbins - 1 : b));
+    };
+    for (int c = threadIdx.x; c < m; c += RS_THREADS) atomicAdd(&hist[bin_of(c)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < MAX_BINS / 32; ++w) keepw[w] = 0;
+        for (int t = 0; t < keep_k && t < nbins; ++t) {
+            int sel = -1;
+            for (int b = 0; b < nbins; ++b) {
+                if (keepw[b >> 5] & (1 << (b & 31))) continue;
+                if (sel < 0 || hist[b] > hist[sel]) sel = b;
+            }
+            if (sel >= 0) keepw[sel >> 5] |= 1 << (sel & 31);
+        }
+    }
+    __syncthreads();
+    int n_keep = 0;
+    for (int r0 = 0; r0 < m; r0 += RS_THREADS) {
+        const int c = r0 + threadIdx.x;
+        int keep = 0;
+        long long p = 0, k = 0, d = 0, o = 0;
+        if (c < m) {
+            const int b = bin_of(c);
+            keep = (keepw[b >> 5] >> (b & 31)) & 1;
+            p = cp[c];
+            k = ck[c];
+            d = cd[c];
+            o = co[c];
+        }
+        int total;
+        const int pos = n_keep + block_exclusive_scan<RS_THREADS>(keep, scan_tmp, total);
+        if (keep) {
+            cp[pos] = p;
+            ck[pos] = k;
+            cd[pos] = d;
+            co[pos] = o;
+        }
+        n_keep += total;
+    }
+    if (threadIdx.x == 0) *count = n_keep;
+}
+
+}  // namespace ft
+
+extern "C" int ft_resolve_conflicts(int32_t n_points, const int64_t *out_kp,
+                                    const int64_t *out_dist, const int64_t *out_oct, int32_t n_kp,
+                                    const ft_project_out *out, const ft_workspace *ws,
+                                    ft_stream_t stream) {
+    if (!out || !ws || !out->corr_count) return FT_E_NULL;
+    if (n_points < 0 || n_kp < 0 || n_kp > 65535) return FT_E_RANGE;
+    if (n_points > 0 && (!out_kp || !out_dist || !out_oct || !out->corr_point || !out->corr_kp ||
+                         !out->corr_dist || !out->corr_oct))
+        return FT_E_NULL;
+    const int wst = ws_check(ws, 1, n_kp > 0 ? n_kp : 1, 1);
+    if (wst != FT_OK) return wst;
+    unsigned long long *claims = ws_ptr<unsigned long long>(ws, ws_layout(ws).proj_claims);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_points > 0) {
+        const int blocks = (n_points + 255) / 256 < 1184 ? (n_points + 255) / 256 : 1184;
+        claim_kernel<<<blocks, 256, 0, s>>>(out_kp, out_dist, n_points, n_kp, claims);
+    }
+    compact_winners_kernel<<<1, RS_THREADS, 0, s>>>(out_kp, out_dist, out_oct, n_points, n_kp,
+                                                    claims, out->corr_point, out->corr_kp,
+                                                    out->corr_dist, out->corr_oct,
+                                                    out->corr_count);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int ft_rotation_filter(int32_t m, int64_t *corr_point, int64_t *corr_kp,
+                                  int64_t *corr_dist, int64_t *corr_oct, const double *ref_angles,
+                                  const double *kp_angles, int32_t histogram_bins,
+                                  int32_t histogram_keep, int32_t *count, ft_stream_t stream) {
+    if (!count) return FT_E_NULL;
+    if (m < 0) return FT_E_RANGE;
+    if (histogram_bins < 1 || histogram_bins > MAX_BINS || histogram_keep < 1 ||
+        histogram_keep > histogram_bins)
+        return FT_E_CONFIG;
+    if (m > 0 && (!corr_point || !corr_kp || !corr_dist || !corr_oct || !ref_angles || !kp_angles))
+        return FT_E_NULL;
+    rotation_filter_kernel<<<1, RS_THREADS, 0, (cudaStream_t)stream>>>(
+        corr_point, corr_kp, corr_dist, corr_oct, m, ref_angles, kp_angles, histogram_bins,
+        histogram_keep, count);
+    return (int)cudaGetLastError();
+}

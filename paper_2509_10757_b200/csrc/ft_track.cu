@@ -1,0 +1,1192 @@
+// ft_track.cu -- the per-frame tracking hot path as ONE cooperative sm_100a
+// kernel: pinhole stereo matching and search-by-projection / SearchLocalPoints
+// run side by side in block groups, with in-kernel group barriers replacing
+// the reference's host round trips.
+//
+// Reference semantics (trackfront, pkg/src/trackfront):
+//   stereo phase 1   kernels.py:300-345 stereo_phase1_kernel; stereo.py:67-103
+//   stereo phase 2   kernels.py:351-428 stereo_phase2_kernel; stereo.py:106-140
+//   no-image accept  stereo.py:143-168 matches_from_candidates
+//   reject           stereo.py:171-188 reject_outliers (np.median semantics)
+//   phase A          kernels.py:470-579 project_search_kernel; projection.py:118-158
+//   grid             mapping.py:68-100 FrameGrid (truncate, clip)
+//   phase B          projection.py:161-178 resolve_conflicts
+//   phase C          projection.py:181-200 rotation_consistency_filter
+//   local search     localmap.py:79-122 search_local_points
+//
+// Launch geometry (host picks it, see track_launch):
+//   grid = W group slots x (Gs stereo blocks + Gm map blocks), 512 threads,
+//   launched cooperatively so every block is resident.  Slot w processes
+//   frames w, w+W, w+2W, ... ; within a frame the Gs stereo blocks split the
+//   left keypoints and the Gm map blocks split the map points.
+//
+// Stereo block: stage the right keypoint table (u, v, octave, descriptor) in
+//   shared memory with coalesced loads and build the row-bucket CSR there;
+//   one warp per left keypoint: phase 1 over the contiguous CSR range of rows
+//   [r0, r1] with a redux.sync min of (dist << 16 | j) (= the reference's
+//   lexicographic (dist, j) order), then phase 2 with the 11x11 / 11x21
+//   patches staged per warp in shared memory.  REJECT: group barrier, then
+//   every stereo block radix-selects the same median over the frame's
+//   accepted SADs and resets its own rejected matches (no serial tail).
+// Map block: stage the frame's keypoint table + cell-grid CSR (+ a hash set
+//   of slotted point ids) in shared memory; thread-per-point fp64 projection
+//   in the reference's evaluation order; warp per visible point over the
+//   window's cell rows with a shuffle merge of (best key, second);
+//   claims are 64-bit atomicMin keys (~epoch << 32 | dist << 23 | point) so
+//   the minimum is the reference's (lowest dist, lowest point) winner and
+//   stale claims from earlier launches always lose (no reset pass).  After a
+//   group barrier each block resolves its own points; ordered outputs use
+//   one more barrier for the cross-block prefix.
+#include <cstring>
+
+#include "ft_common.cuh"
+#include "ft_ws.cuh"
+
+namespace ft {
+
+constexpr int TK_THREADS = 512;
+constexpr int TK_WARPS = TK_THREADS / 32;
+constexpr int TK_MAX_BINS = 256;
+constexpr long long NO_PID = -1;  // mapping.py:13 NO_POINT
+constexpr long long HASH_EMPTY = (long long)0x8000000000000000ull;
+
+struct TrackArgs {
+    int32_t F, W, Gs, Gm;
+    // stereo
+    int32_t smode;
+    ft_keypoints L, R;
+    ft_pyramid PL, PR;
+    ft_stereo_params sp;
+    ft_stereo_out so;
+    int32_t patch_ints;
+    // map
+    int32_t pmode;
+    ft_map_points P;
+    ft_keypoints K;
+    ft_project_params pp;
+    ft_project_io io;
+    ft_project_out po;
+    int32_t hash_bits;
+    int32_t map_chunk_cap;  // max points per map block (smem sizing)
+    // workspace
+    unsigned long long *bar_s;   // [W]
+    unsigned long long *bar_m;   // [W]
+    unsigned long long *ep_m;    // [W]
+    unsigned long long *claims;  // [F][cap_kp]
+    int *blk_counts;             // [F][Gm]
+    int *hist;                   // [F][TK_MAX_BINS]
+};
+
+// ---------------------------------------------------------------------------
+// group barrier among the G blocks of one role in one slot.  The counter only
+// grows; the generation is the arrival ticket / G, so no reset is needed.
+
+FT_DEV unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ void group_barrier(unsigned long long *ctr, int G) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long t = atomicAdd(ctr, 1ull);
+        const unsigned long long target = (t / G + 1) * (unsigned long long)G;
+        while (ld_acquire_u64(ctr) < target) __nanosleep(32);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// k-th smallest (0-based) of vals[0..n) by 8-bit radix select, skipping the
+// all-zero high digits (SAD values are < 2^16 for the default 11x11 window).
+
+__device__ uint32_t block_select(const uint32_t *vals, int n, int k, int *hist, int *scan_tmp,
+                                 int *misc) {
+    uint32_t mx = 0;
+    for (int i = threadIdx.x; i < n; i += TK_THREADS) mx = max(mx, vals[i]);
+    mx = __reduce_max_sync(FULL, mx);
+    if (threadIdx.x == 0) misc[0] = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned *>(misc), mx);
+    __syncthreads();
+    mx = (uint32_t)misc[0];
+    int top = 24;
+    while (top > 0 && (mx >> top) == 0) top -= 8;
+    uint32_t prefix = 0, mask = 0;
+    for (int sh = top; sh >= 0; sh -= 8) {
+        if (threadIdx.x < 256) hist[threadIdx.x] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += TK_THREADS) {
+            const uint32_t x = vals[i];
+            if ((x & mask) == prefix) atomicAdd(&hist[(x >> sh) & 0xffu], 1);
+        }
+        __syncthreads();
+        const int c = threadIdx.x < 256 ? hist[threadIdx.x] : 0;
+        int total;
+        const int run = block_exclusive_scan<TK_THREADS>(c, scan_tmp, total);
+        if (threadIdx.x < 256 && k >= run && k < run + c) {
+            misc[1] = threadIdx.x;
+            misc[2] = k - run;
+        }
+        __syncthreads();
+        prefix |= (uint32_t)misc[1] << sh;
+        mask |= 0xffu << sh;
+        k = misc[2];
+        __syncthreads();
+    }
+    return prefix;
+}
+
+// ---------------------------------------------------------------------------
+// stereo role
+
+struct StereoSmem {
+    double *ru, *rv;
+    uint4 *rd;        // [2*cap]
+    int *ro;
+    int *row_start;   // [H+1]
+    int *row_cursor;  // [H]
+    uint16_t *items;  // [cap]
+    int *patch;       // [TK_WARPS][patch_ints]
+    int *scan_tmp;    // [32]
+    int *misc;        // [16]
+};
+
+FT_DEV int phase1(const TrackArgs &a, const StereoSmem &sm, int64_t lk, int lane, int &cdist) {
+    const double v = a.L.v[lk], u = a.L.u[lk];
+    const int o = a.L.octave[lk];
+    const double band = a.sp.band_factor * a.sp.scale_pow[clampi(o, 0, FT_MAX_LEVELS - 1)];
+    long long r0 = (long long)floor(v - band);
+    long long r1 = (long long)ceil(v + band);
+    const int H = a.sp.height;
+    if (r0 < 0) r0 = 0;
+    if (r1 > H - 1) r1 = H - 1;
+    uint32_t best = NO_KEY;
+    if (r0 <= r1) {
+        const int beg = sm.row_start[r0], end = sm.row_start[r1 + 1];
+        if (beg < end) {
+            const Desc ld = load_desc(a.L.desc, lk);
+            for (int ii = beg + lane; ii < end; ii += 32) {
+                const int j = sm.items[ii];
+                const int ro = sm.ro[j];
+                if (ro < o - 1 || ro > o + 1) continue;
+                if (fabs(sm.rv[j] - v) > band) continue;
+                const double disp = u - sm.ru[j];
+                if (disp < a.sp.min_disparity || disp > a.sp.max_disparity) continue;
+                Desc rd;
+                rd.lo = sm.rd[2 * j];
+                rd.hi = sm.rd[2 * j + 1];
+                best = min(best, (hamming(ld, rd) << 16) | (uint32_t)j);
+            }
+        }
+    }
+    best = __reduce_min_sync(FULL, best);
+    if (best != NO_KEY && (int)(best >> 16) <= a.sp.t_match) {
+        cdist = (int)(best >> 16);
+        return (int)(best & 0xffffu);
+    }
+    cdist = 10000;
+    return -1;
+}
+
+// Phase 2 for one candidate; every lane returns the same verdict.
+FT_DEV bool phase2(const TrackArgs &a, int *patch, int f, int64_t lk, double ur_cand, int lane,
+                   double &disp_out, double &ur_out, int &sad_out) {
+    const int o = clampi(a.L.octave[lk], 0, a.PL.n_levels - 1);
+    const double s = a.sp.scale_pow[o];
+    const double ulev = a.L.u[lk] / s, vlev = a.L.v[lk] / s, urlev = ur_cand / s;
+    const long long xi = round_half_even(ulev), yi = round_half_even(vlev),
+                    xr0 = round_half_even(urlev);
+    const int hw = a.sp.half_window, hs = a.sp.half_slide;
+    const long long wl = a.PL.widths[o], hl = a.PL.heights[o];
+    const long long wr = a.PR.widths[o], hr = a.PR.heights[o];
+    if (xi - hw < 0 || xi + hw >= wl || yi - hw < 0 || yi + hw >= hl) return false;
+    if (xr0 - hs - hw < 0 || xr0 + hs + hw >= wr || yi - hw < 0 || yi + hw >= hr) return false;
+    const uint8_t *lp = a.PL.data + (int64_t)f * a.PL.frame_bytes + a.PL.offsets[o];
+    const uint8_t *rp = a.PR.data + (int64_t)f * a.PR.frame_bytes + a.PR.offsets[o];
+    const int nw = 2 * hw + 1, nr = 2 * hs + 2 * hw + 1, noff = 2 * hs + 1;
+    int *pl = patch;           // [nw][nw]  L - cl
+    int *pr = pl + nw * nw;    // [nw][nr]  R
+    int *sads = pr + nw * nr;  // [noff]
+    const int cl = __ldg(lp + yi * wl + xi);
+    for (int t = lane; t < nw * nw; t += 32) {
+        const int dy = t / nw, dx = t - dy * nw;
+        pl[t] = (int)__ldg(lp + (yi - hw + dy) * wl + (xi - hw + dx)) - cl;
+    }
+    for (int t = lane; t < nw * nr; t += 32) {
+        const int dy = t / nr, dx = t - dy * nr;
+        pr[t] = __ldg(rp + (yi - hw + dy) * wr + (xr0 - hs - hw + dx));
+    }
+    for (int t = lane; t < noff; t += 32) sads[t] = 0;
+    __syncwarp();
+    for (int t = lane; t < noff * nw; t += 32) {  // job = (offset, row)
+        const int oi = t / nw, dy = t - oi * nw;
+        const int cr = pr[hw * nr + oi + hw];  // R[yi, xr0 + off]
+        const int *lrow = pl + dy * nw;
+        const int *rrow = pr + dy * nr + oi;
+        int acc = 0;
+        for (int dx = 0; dx < nw; ++dx) acc += abs(lrow[dx] + cr - rrow[dx]);
+        atomicAdd(&sads[oi], acc);
+    }
+    __syncwarp();
+    int best_sad = 0x7fffffff, best_oi = 0;
+    for (int oi = 0; oi < noff; ++oi) {  // strict <: lowest offset wins ties
+        const int sv = sads[oi];
+        if (sv < best_sad) {
+            best_sad = sv;
+            best_oi = oi;
+        }
+    }
+    const bool interior = best_oi > 0 && best_oi < noff - 1;
+    const int s_m = interior ? sads[best_oi - 1] : 0;
+    const int s_p = interior ? sads[best_oi + 1] : 0;
+    __syncwarp();
+    if (!interior) return false;
+    const double d_m = (double)s_m, d_0 = (double)best_sad, d_p = (double)s_p;
+    const double denom = d_m + d_p - 2.0 * d_0;
+    if (denom <= 0.0) return false;
+    const double delta = (d_m - d_p) / (2.0 * denom);
+    if (delta < -1.0 || delta > 1.0) return false;
+    const double ur_ref = ((double)(xr0 + (best_oi - hs)) + delta) * s;
+    const double disp = a.L.u[lk] - ur_ref;
+    if (disp < a.sp.min_disparity || disp > a.sp.max_disparity) return false;
+    disp_out = disp;
+    ur_out = ur_ref;
+    sad_out = best_sad;
+    return true;
+}
+
+__device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long long *bar,
+                             unsigned char *smem) {
+    const int G = a.Gs;
+    const int n_left = min(a.L.count[f], a.L.cap);
+    const int n_right = min(a.R.count[f], a.R.cap);
+    const int64_t lbase = (int64_t)f * a.L.cap, rbase = (int64_t)f * a.R.cap;
+    const int chunk = (n_left + G - 1) / G;
+    const int k0 = rank * chunk, k1 = min(n_left, k0 + chunk);
+    const int H = a.sp.height;
+    const bool do_p1 = a.smode & FT_STEREO_PHASE1;
+    const bool do_ref = a.smode & FT_STEREO_REFINE;
+    const bool do_fc = a.smode & FT_STEREO_FROM_CAND;
+    const bool do_rej = a.smode & FT_STEREO_REJECT;
+    const bool finalize = do_ref || do_fc;
+    const int cap_r = a.R.cap;
+
+    StereoSmem sm;
+    unsigned char *p = smem;
+    sm.rd = reinterpret_cast<uint4 *>(p);
+    p += (size_t)32 * cap_r;
+    sm.ru = reinterpret_cast<double *>(p);
+    p += (size_t)8 * cap_r;
+    sm.rv = reinterpret_cast<double *>(p);
+    p += (size_t)8 * cap_r;
+    sm.scan_tmp = reinterpret_cast<int *>(p);
+    p += 32 * 4;
+    sm.misc = reinterpret_cast<int *>(p);
+    p += 16 * 4;
+    sm.row_start = reinterpret_cast<int *>(p);
+    p += (size_t)4 * (H + 1);
+    sm.row_cursor = reinterpret_cast<int *>(p);
+    p += (size_t)4 * H;
+    sm.patch = reinterpret_cast<int *>(p);
+    p += (size_t)4 * TK_WARPS * a.patch_ints;
+    sm.ro = reinterpret_cast<int *>(p);
+    p += (size_t)4 * cap_r;
+    sm.items = reinterpret_cast<uint16_t *>(p);
+
+    if (rank == 0 && threadIdx.x == 0 && a.so.n_matched) a.so.n_matched[f] = 0;
+
+    if (k0 < k1 && (do_p1 || finalize)) {
+        if (do_p1) {
+            // stage the right table: coalesced, two items in flight per thread
+            const uint4 *rdg = reinterpret_cast<const uint4 *>(a.R.desc + 4 * rbase);
+            for (int j = threadIdx.x; j < n_right; j += TK_THREADS) {
+                const uint4 d0 = __ldg(rdg + 2 * j), d1 = __ldg(rdg + 2 * j + 1);
+                const double u = __ldg(a.R.u + rbase + j), v = __ldg(a.R.v + rbase + j);
+                const int o = __ldg(a.R.octave + rbase + j);
+                sm.rd[2 * j] = d0;
+                sm.rd[2 * j + 1] = d1;
+                sm.ru[j] = u;
+                sm.rv[j] = v;
+                sm.ro[j] = o;
+            }
+            __syncthreads();
+            block_csr<TK_THREADS>(
+                n_right, H,
+                [&](int j) {
+                    long long r = round_half_even(sm.rv[j]);  // np.round: half-even
+                    return (int)(r < 0 ? 0 : (r > H - 1 ? H - 1 : r));
+                },
+                sm.row_start, sm.row_cursor, sm.items, sm.scan_tmp);
+        }
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        int *patch = sm.patch + wid * a.patch_ints;
+        for (int k = k0 + wid; k < k1; k += TK_WARPS) {
+            const int64_t lk = lbase + k;
+            int cand, cdist;
+            if (do_p1) {
+                cand = phase1(a, sm, lk, lane, cdist);
+                if (lane == 0 && a.so.cand_idx) {
+                    a.so.cand_idx[lk] = cand;
+                    a.so.cand_dist[lk] = cdist;
+                }
+            } else {
+                cand = (int)a.so.cand_idx[lk];
+                cdist = (int)a.so.cand_dist[lk];
+            }
+            if (!finalize) continue;
+            bool ok = false;
+            double disp = 0.0, ur = 0.0;
+            int sad = 0;
+            if (cand >= 0 && cand < n_right) {
+                const double urc = do_p1 ? sm.ru[cand] : a.R.u[rbase + cand];
+                if (do_ref) {
+                    ok = phase2(a, patch, f, lk, urc, lane, disp, ur, sad);
+                } else {  // matches_from_candidates (stereo.py:154-160)
+                    disp = a.L.u[lk] - urc;
+                    ok = !(disp < a.sp.min_disparity || disp > a.sp.max_disparity);
+                    ur = urc;
+                }
+            }
+            if (lane == 0) {
+                a.so.right_idx[lk] = ok ? cand : -1;
+                a.so.distance[lk] = ok ? cdist : 10000;
+                a.so.disparity[lk] = ok ? disp : 0.0;
+                a.so.refined_u[lk] = ok ? ur : 0.0;
+                a.so.depth[lk] = ok ? a.sp.baseline_times_fx / disp : 0.0;
+                a.so.sad[lk] = ok ? sad : 0;
+            }
+        }
+    }
+    if (!do_rej && !a.so.n_matched) return;
+    group_barrier(bar, G);
+    int kept = 0;
+    if (do_rej) {
+        // every block computes the same median over the frame's accepted SADs
+        uint32_t *vals = reinterpret_cast<uint32_t *>(sm.rd);  // table no longer needed
+        int *hist = reinterpret_cast<int *>(sm.ru);
+        if (threadIdx.x == 0) sm.misc[4] = 0;
+        __syncthreads();
+        for (int k = threadIdx.x; k < n_left; k += TK_THREADS) {
+            if (__ldcg(a.so.right_idx + lbase + k) >= 0) {
+                const int pos = atomicAdd(&sm.misc[4], 1);
+                vals[pos] = (uint32_t)__ldcg(a.so.sad + lbase + k);
+            }
+        }
+        __syncthreads();
+        const int nm = sm.misc[4];
+        if (nm > 0) {
+            const int k_lo = (nm - 1) / 2, k_hi = nm / 2;
+            const uint32_t v_lo = block_select(vals, nm, k_lo, hist, sm.scan_tmp, sm.misc);
+            uint32_t v_hi = v_lo;
+            if (k_hi != k_lo) {
+                if (threadIdx.x == 0) {
+                    sm.misc[5] = 0;
+                    sm.misc[6] = 0x7fffffff;
+                }
+                __syncthreads();
+                int cle = 0, above = 0x7fffffff;
+                for (int i = threadIdx.x; i < nm; i += TK_THREADS) {
+                    const uint32_t x = vals[i];
+                    if (x <= v_lo) ++cle;
+                    else above = min(above, (int)x);
+                }
+                cle = __reduce_add_sync(FULL, cle);
+                above = __reduce_min_sync(FULL, above);
+                if ((threadIdx.x & 31) == 0) {
+                    atomicAdd(&sm.misc[5], cle);
+                    atomicMin(&sm.misc[6], above);
+                }
+                __syncthreads();
+                v_hi = sm.misc[5] > k_hi ? v_lo : (uint32_t)sm.misc[6];
+            }
+            const double med = (k_hi == k_lo) ? (double)v_lo : ((double)v_lo + (double)v_hi) / 2.0;
+            const double thr = a.sp.outlier_multiplier * med;
+            for (int k = k0 + threadIdx.x; k < k1; k += TK_THREADS) {
+                const int64_t i = lbase + k;
+                if (__ldcg(a.so.right_idx + i) < 0) continue;
+                if ((double)__ldcg(a.so.sad + i) > thr) {
+                    a.so.right_idx[i] = -1;
+                    a.so.distance[i] = 10000;
+                    a.so.disparity[i] = 0.0;
+                    a.so.refined_u[i] = 0.0;
+                    a.so.depth[i] = 0.0;
+                    a.so.sad[i] = 0;
+                } else {
+                    ++kept;
+                }
+            }
+        }
+    } else {
+        for (int k = k0 + threadIdx.x; k < k1; k += TK_THREADS)
+            kept += __ldcg(a.so.right_idx + lbase + k) >= 0;
+    }
+    if (a.so.n_matched) {
+        kept = __reduce_add_sync(FULL, kept);
+        if ((threadIdx.x & 31) == 0 && kept) atomicAdd(a.so.n_matched + f, kept);
+    }
+    __syncthreads();  // smem reuse by the next frame of this slot
+}
+
+// ---------------------------------------------------------------------------
+// map role
+
+struct QItem {
+    double ucen, v, r;
+    int i;  // point index within the frame
+    int lvl;
+    int cx0, cx1, cy0, cy1;
+};
+
+struct MapSmem {
+    uint4 *kd;  // [2*cap_kp]
+    double *ku, *kv;
+    int *ko;
+    int *cell_start, *cell_cursor;
+    uint16_t *items;
+    long long *htab;
+    QItem *queue;
+    int *res;  // [map_chunk_cap] packed claim (kp | dist << 16 | lvl << 25) or -1
+    int *scan_tmp, *misc;
+    int *hist;  // [TK_MAX_BINS]
+};
+
+FT_DEV unsigned hash_slot(long long id, int bits) {
+    return (unsigned)(((unsigned long long)id * 0x9E3779B97F4A7C15ull) >> (64 - bits));
+}
+
+FT_DEV void hash_insert(long long *tab, int bits, long long id) {
+    const unsigned mask = (1u << bits) - 1u;
+    unsigned h = hash_slot(id, bits);
+    while (true) {
+        const long long prev = (long long)atomicCAS(reinterpret_cast<unsigned long long *>(tab + h),
+                                                    (unsigned long long)HASH_EMPTY,
+                                                    (unsigned long long)id);
+        if (prev == HASH_EMPTY || prev == id) return;
+        h = (h + 1) & mask;
+    }
+}
+
+FT_DEV bool hash_contains(const long long *tab, int bits, long long id) {
+    const unsigned mask = (1u << bits) - 1u;
+    unsigned h = hash_slot(id, bits);
+    while (true) {
+        const long long x = tab[h];
+        if (x == id) return true;
+        if (x == HASH_EMPTY) return false;
+        h = (h + 1) & mask;
+    }
+}
+
+// kernels.py:496-551: visibility gate of one point; fills the window item.
+FT_DEV bool project_point(const TrackArgs &a, int64_t gi, double ccx, double ccy, double ccz,
+                          const double *R, const double *T, QItem &q) {
+    const ft_project_params &p = a.pp;
+    const double px = a.P.positions[3 * gi], py = a.P.positions[3 * gi + 1],
+                 pz = a.P.positions[3 * gi + 2];
+    const double pcx = R[0] * px + R[1] * py + R[2] * pz + T[0];
+    const double pcy = R[3] * px + R[4] * py + R[5] * pz + T[1];
+    const double pcz = R[6] * px + R[7] * py + R[8] * pz + T[2];
+    if (pcz <= 1e-6) return false;
+    double u, v;
+    if (p.cam_kind == 0) {
+        u = p.fx * pcx / pcz + p.cx;
+        v = p.fy * pcy / pcz + p.cy;
+    } else {
+        const double r = hypot(pcx, pcy);
+        if (r < 1e-12) {
+            u = p.cx;
+            v = p.cy;
+        } else {
+            const double theta = atan2(r, pcz);
+            const double t2 = theta * theta;
+            const double dth = theta * (1.0 + t2 * (p.k1 + t2 * (p.k2 + t2 * (p.k3 + t2 * p.k4))));
+            u = p.fx * dth * pcx / r + p.cx;
+            v = p.fy * dth * pcy / r + p.cy;
+        }
+    }
+    if (u < 0.0 || u >= p.width || v < 0.0 || v >= p.height) return false;
+    const double dist = sqrt(pcx * pcx + pcy * pcy + pcz * pcz);
+    const double mind = a.P.min_dist[gi], maxd = a.P.max_dist[gi];
+    if (dist < mind || dist > maxd) return false;
+    const double vx = px - ccx, vy = py - ccy, vz = pz - ccz;
+    const double cosang = (vx * a.P.normals[3 * gi] + vy * a.P.normals[3 * gi + 1] +
+                           vz * a.P.normals[3 * gi + 2]) / dist;
+    if (cosang < p.view_cos_min) return false;
+    long long lvl = (long long)ceil(log(maxd / dist) * p.inv_log_scale - 1e-9);
+    if (lvl < 0) lvl = 0;
+    if (lvl > p.n_levels - 1) lvl = p.n_levels - 1;
+    const double r_win = p.window_px * p.scale_pow[lvl];
+    const double ucen = u + p.u_offset;
+    const double cell = (double)p.cell_px;
+    long long cx0 = (long long)((ucen - r_win) / cell);
+    long long cx1 = (long long)((ucen + r_win) / cell);
+    long long cy0 = (long long)((v - r_win) / cell);
+    long long cy1 = (long long)((v + r_win) / cell);
+    if (cx1 < 0 || cy1 < 0 || cx0 > p.grid_nx - 1 || cy0 > p.grid_ny - 1) return false;
+    if (cx0 < 0) cx0 = 0;
+    if (cy0 < 0) cy0 = 0;
+    if (cx1 > p.grid_nx - 1) cx1 = p.grid_nx - 1;
+    if (cy1 > p.grid_ny - 1) cy1 = p.grid_ny - 1;
+    q.ucen = ucen;
+    q.v = v;
+    q.r = r_win;
+    q.lvl = (int)lvl;
+    q.cx0 = (int)cx0;
+    q.cx1 = (int)cx1;
+    q.cy0 = (int)cy0;
+    q.cy1 = (int)cy1;
+    return true;
+}
+
+FT_DEV double py_mod(double a, double b) {  // numpy float remainder
+    double r = fmod(a, b);
+    if (r != 0.0 && ((b < 0.0) != (r < 0.0))) r += b;
+    return r;
+}
+
+FT_DEV int rotation_bin(const TrackArgs &a, int64_t kbase, int64_t pbase, int kp, int pi) {
+    const double two_pi = 2.0 * 3.141592653589793;
+    const int nb = a.pp.histogram_bins;
+    const double diff = py_mod(a.K.angle[kbase + kp] - a.io.ref_angles[pbase + pi], two_pi);
+    long long b = (long long)floor(diff / two_pi * (double)nb);
+    return (int)(b < 0 ? 0 : (b > nb - 1 ? nb - 1 : b));
+}
+
+__device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigned char *smem) {
+    const int G = a.Gm;
+    const int n_pts = min(a.P.count[f], a.P.cap);
+    const int n_kp = min(a.K.count[f], a.K.cap);
+    const int64_t pbase = (int64_t)f * a.P.cap, kbase = (int64_t)f * a.K.cap;
+    const int chunk = (n_pts + G - 1) / G;
+    const int p0 = rank * chunk, p1 = min(n_pts, p0 + chunk);
+    const ft_project_params &pp = a.pp;
+    const int nx = pp.grid_nx, ny = pp.grid_ny, ncell = nx * ny;
+    const int cap_kp = a.K.cap;
+    const bool resolve = a.pmode & FT_PROJ_RESOLVE;
+    const bool rotation = (a.pmode & FT_PROJ_ROTATION) && a.io.ref_angles && a.K.angle;
+    const bool use_hash = (a.pmode & FT_PROJ_SKIP_SLOTS) && a.hash_bits;
+    const bool write_slots = a.pmode & FT_PROJ_WRITE_SLOTS;
+    const bool ordered = resolve && a.po.corr_point;
+    unsigned long long *bar = a.bar_m + slot;
+
+    MapSmem sm;
+    unsigned char *p = smem;
+    sm.kd = reinterpret_cast<uint4 *>(p);
+    p += (size_t)32 * cap_kp;
+    sm.ku = reinterpret_cast<double *>(p);
+    p += (size_t)8 * cap_kp;
+    sm.kv = reinterpret_cast<double *>(p);
+    p += (size_t)8 * cap_kp;
+    sm.queue = reinterpret_cast<QItem *>(p);
+    p += sizeof(QItem) * TK_THREADS;
+    sm.htab = reinterpret_cast<long long *>(p);
+    p += a.hash_bits ? (sizeof(long long) << a.hash_bits) : 0;
+    sm.scan_tmp = reinterpret_cast<int *>(p);
+    p += 32 * 4;
+    sm.misc = reinterpret_cast<int *>(p);
+    p += 16 * 4;
+    sm.hist = reinterpret_cast<int *>(p);
+    p += TK_MAX_BINS * 4;
+    sm.res = reinterpret_cast<int *>(p);
+    p += (size_t)4 * a.map_chunk_cap;
+    sm.cell_start = reinterpret_cast<int *>(p);
+    p += (size_t)4 * (ncell + 1);
+    sm.cell_cursor = reinterpret_cast<int *>(p);
+    p += (size_t)4 * ncell;
+    sm.ko = reinterpret_cast<int *>(p);
+    p += (size_t)4 * cap_kp;
+    sm.items = reinterpret_cast<uint16_t *>(p);
+
+    // launch epoch: the same for every block of this slot's frame instance
+    if (threadIdx.x == 0) {
+        const unsigned long long t = atomicAdd(a.ep_m + slot, 1ull);
+        sm.misc[0] = (int)(unsigned)(t / G);
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        if (a.po.slot_count) a.po.slot_count[f] = 0;
+        if (a.po.corr_count) a.po.corr_count[f] = 0;
+    }
+    if (rank == 0 && rotation)
+        for (int b = threadIdx.x; b < TK_MAX_BINS; b += TK_THREADS) a.hist[(int64_t)f * TK_MAX_BINS + b] = 0;
+    __syncthreads();
+    const unsigned epoch_hi = 0xffffffffu - (unsigned)sm.misc[0];
+
+    // slots_out <- slots_in (this block's share) and its pre-filled count
+    int prefilled = 0;
+    if (write_slots) {
+        const int sc = (n_kp + G - 1) / G, s0 = rank * sc, s1 = min(n_kp, s0 + sc);
+        for (int k = s0 + threadIdx.x; k < s1; k += TK_THREADS) {
+            const long long v = a.io.slots_in[kbase + k];
+            if (a.io.slots_out != a.io.slots_in) a.io.slots_out[kbase + k] = v;
+            prefilled += v != NO_PID;
+        }
+    }
+
+    if (p0 < p1) {
+        // stage the keypoint table
+        const uint4 *kdg = reinterpret_cast<const uint4 *>(a.K.desc + 4 * kbase);
+        for (int j = threadIdx.x; j < n_kp; j += TK_THREADS) {
+            const uint4 d0 = __ldg(kdg + 2 * j), d1 = __ldg(kdg + 2 * j + 1);
+            const double u = __ldg(a.K.u + kbase + j), v = __ldg(a.K.v + kbase + j);
+            const int o = __ldg(a.K.octave + kbase + j);
+            sm.kd[2 * j] = d0;
+            sm.kd[2 * j + 1] = d1;
+            sm.ku[j] = u;
+            sm.kv[j] = v;
+            sm.ko[j] = o;
+        }
+        if (use_hash)
+            for (int h = threadIdx.x; h < (1 << a.hash_bits); h += TK_THREADS) sm.htab[h] = HASH_EMPTY;
+        __syncthreads();
+        const double cellf = (double)pp.cell_px;
+        block_csr<TK_THREADS>(
+            n_kp, ncell,
+            [&](int j) {  // FrameGrid cell: truncation, then clip (mapping.py:81-83)
+                long long cx = (long long)(sm.ku[j] / cellf), cy = (long long)(sm.kv[j] / cellf);
+                cx = cx < 0 ? 0 : (cx > nx - 1 ? nx - 1 : cx);
+                cy = cy < 0 ? 0 : (cy > ny - 1 ? ny - 1 : cy);
+                return (int)(cy * nx + cx);
+            },
+            sm.cell_start, sm.cell_cursor, sm.items, sm.scan_tmp);
+        if (use_hash) {
+            for (int k = threadIdx.x; k < n_kp; k += TK_THREADS) {
+                const long long id = a.io.slots_in[kbase + k];
+                if (id != NO_PID) hash_insert(sm.htab, a.hash_bits, id);
+            }
+            __syncthreads();
+        }
+        const double *R = a.io.rot + 9 * f, *T = a.io.trans + 3 * f;
+        const double ccx = -(R[0] * T[0] + R[3] * T[1] + R[6] * T[2]);
+        const double ccy = -(R[1] * T[0] + R[4] * T[1] + R[7] * T[2]);
+        const double ccz = -(R[2] * T[0] + R[5] * T[1] + R[8] * T[2]);
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        for (int r0 = p0; r0 < p1; r0 += TK_THREADS) {
+            if (threadIdx.x == 0) sm.misc[1] = 0;
+            __syncthreads();
+            const int i = r0 + threadIdx.x;
+            if (i < p1) {
+                const int64_t gi = pbase + i;
+                sm.res[i - p0] = -1;
+                if (a.po.out_kp) {
+                    a.po.out_kp[gi] = -1;
+                    a.po.out_dist[gi] = 10000;
+                    a.po.out_oct[gi] = -1;
+                }
+                bool skip = a.io.skip && a.io.skip[gi] != 0;
+                if (!skip && use_hash) skip = hash_contains(sm.htab, a.hash_bits, a.P.point_ids[gi]);
+                QItem q;
+                if (!skip && project_point(a, gi, ccx, ccy, ccz, R, T, q)) {
+                    q.i = i;
+                    sm.queue[atomicAdd(&sm.misc[1], 1)] = q;
+                }
+            }
+            __syncthreads();
+            const int nq = sm.misc[1];
+            for (int qi = wid; qi < nq; qi += TK_WARPS) {  // warp per visible point
+                const QItem q = sm.queue[qi];
+                const int64_t gi = pbase + q.i;
+                const Desc pd = load_desc(a.P.desc, gi);
+                Best2 b;
+                best2_init(b);
+                for (int gy = q.cy0; gy <= q.cy1; ++gy) {
+                    const int beg = sm.cell_start[gy * nx + q.cx0];
+                    const int end = sm.cell_start[gy * nx + q.cx1 + 1];
+                    for (int ii = beg + lane; ii < end; ii += 32) {
+                        const int j = sm.items[ii];
+                        if (fabs(sm.ku[j] - q.ucen) > q.r || fabs(sm.kv[j] - q.v) > q.r) continue;
+                        const int ko = sm.ko[j];
+                        if (ko < q.lvl - 1 || ko > q.lvl + 1) continue;
+                        Desc kd;
+                        kd.lo = sm.kd[2 * j];
+                        kd.hi = sm.kd[2 * j + 1];
+                        best2_push(b, hamming(pd, kd), (uint32_t)j);
+                    }
+                }
+                best2_warp_reduce(b);
+                if (lane == 0 && ratio_accept(b, pp.t_proj, pp.ratio)) {
+                    const int kp = (int)(b.key & 0xffffu), d = (int)(b.key >> 16);
+                    if (a.po.out_kp) {
+                        a.po.out_kp[gi] = kp;
+                        a.po.out_dist[gi] = d;
+                        a.po.out_oct[gi] = q.lvl;
+                    }
+                    sm.res[q.i - p0] = kp | (d << 16) | (q.lvl << 25);
+                    if (resolve)
+                        atomicMin(a.claims + kbase + kp, ((unsigned long long)epoch_hi << 32) |
+                                                             ((unsigned long long)d << 23) |
+                                                             (unsigned)q.i);
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (!resolve) {
+        __syncthreads();
+        return;
+    }
+    group_barrier(bar, G);
+
+    // phase B on this block's points: winner iff its claim is the minimum
+    int n_win = 0;
+    for (int i = p0 + threadIdx.x; i < p1; i += TK_THREADS) {
+        const int r = sm.res[i - p0];
+        if (r < 0) continue;
+        const int kp = r & 0xffff, d = (r >> 16) & 0x1ff;
+        const unsigned long long key = ((unsigned long long)epoch_hi << 32) |
+                                       ((unsigned long long)d << 23) | (unsigned)i;
+        if (__ldcg(a.claims + kbase + kp) != key) {
+            sm.res[i - p0] = -1;
+            continue;
+        }
+        ++n_win;
+        if (rotation) atomicAdd(a.hist + (int64_t)f * TK_MAX_BINS + rotation_bin(a, kbase, pbase, kp, i), 1);
+    }
+    if (rotation) {
+        group_barrier(bar, G);
+        if (threadIdx.x == 0) {  // top-K bins by (-count, bin)
+            const int nb = pp.histogram_bins;
+            const int *h = a.hist + (int64_t)f * TK_MAX_BINS;
+            unsigned keep[TK_MAX_BINS / 32] = {0};
+            for (int t = 0; t < pp.histogram_keep && t < nb; ++t) {
+                int sel = -1, best = -1;
+                for (int b = 0; b < nb; ++b) {
+                    if (keep[b >> 5] & (1u << (b & 31))) continue;
+                    const int c = __ldcg(h + b);
+                    if (sel < 0 || c > best) {
+                        sel = b;
+                        best = c;
+                    }
+                }
+                if (sel >= 0) keep[sel >> 5] |= 1u << (sel & 31);
+            }
+            for (int w = 0; w < TK_MAX_BINS / 32; ++w) sm.hist[w] = (int)keep[w];
+        }
+        __syncthreads();
+        n_win = 0;
+        for (int i = p0 + threadIdx.x; i < p1; i += TK_THREADS) {
+            const int r = sm.res[i - p0];
+            if (r < 0) continue;
+            const int b = rotation_bin(a, kbase, pbase, r & 0xffff, i);
+            if ((sm.hist[b >> 5] >> (b & 31)) & 1) ++n_win;
+            else sm.res[i - p0] = -1;
+        }
+    }
+    __syncthreads();
+    // search_local_points slot write (localmap.py:113-121): only slots empty
+    // before the search; winners hold distinct keypoints, so no races.
+    if (write_slots) {
+        int added = 0;
+        for (int i = p0 + threadIdx.x; i < p1; i += TK_THREADS) {
+            const int r = sm.res[i - p0];
+            if (r < 0) continue;
+            const int kp = r & 0xffff;
+            if (a.io.slots_in[kbase + kp] == NO_PID) {
+                a.io.slots_out[kbase + kp] = a.P.point_ids[pbase + i];
+                ++added;
+            }
+        }
+        int tot = __reduce_add_sync(FULL, added + prefilled);
+        if ((threadIdx.x & 31) == 0 && tot && a.po.slot_count) atomicAdd(a.po.slot_count + f, tot);
+    }
+    if (!ordered) {
+        if (a.po.corr_count) {
+            int tot = __reduce_add_sync(FULL, n_win);
+            if ((threadIdx.x & 31) == 0 && tot) atomicAdd(a.po.corr_count + f, tot);
+        }
+        __syncthreads();
+        return;
+    }
+    // ordered correspondences: block counts -> prefix over ranks -> write
+    {
+        int tot = __reduce_add_sync(FULL, n_win);
+        if (threadIdx.x == 0) sm.misc[2] = 0;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&sm.misc[2], tot);
+        __syncthreads();
+        if (threadIdx.x == 0) a.blk_counts[(int64_t)f * G + rank] = sm.misc[2];
+    }
+    group_barrier(bar, G);
+    int before = 0, all = 0;
+    for (int b = threadIdx.x; b < G; b += TK_THREADS) {
+        const int c = __ldcg(a.blk_counts + (int64_t)f * G + b);
+        all += c;
+        if (b < rank) before += c;
+    }
+    before = __reduce_add_sync(FULL, before);
+    all = __reduce_add_sync(FULL, all);
+    if (threadIdx.x == 0) {
+        sm.misc[3] = 0;
+        sm.misc[4] = 0;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&sm.misc[3], before);
+        atomicAdd(&sm.misc[4], all);
+    }
+    __syncthreads();
+    int base = sm.misc[3];
+    if (rank == 0 && threadIdx.x == 0 && a.po.corr_count) a.po.corr_count[f] = sm.misc[4];
+    for (int r0 = p0; r0 < p1; r0 += TK_THREADS) {
+        const int i = r0 + threadIdx.x;
+        const int r = i < p1 ? sm.res[i - p0] : -1;
+        const int win = r >= 0;
+        int total;
+        const int pos = base + block_exclusive_scan<TK_THREADS>(win, sm.scan_tmp, total);
+        if (win) {
+            a.po.corr_point[pbase + pos] = i;
+            a.po.corr_kp[pbase + pos] = r & 0xffff;
+            a.po.corr_dist[pbase + pos] = (r >> 16) & 0x1ff;
+            a.po.corr_oct[pbase + pos] = r >> 25;
+        }
+        base += total;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int per = a.Gs + a.Gm;
+    const int slot = blockIdx.x / per, r = blockIdx.x - slot * per;
+    for (int f = slot; f < a.F; f += a.W) {
+        if (r < a.Gs) stereo_frame(a, f, r, a.bar_s + slot, smem);
+        else map_frame(a, f, r - a.Gs, slot, smem);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+size_t stereo_smem(const TrackArgs &a) {
+    const int cap = a.R.cap, H = a.sp.height;
+    size_t b = (size_t)52 * cap + 4 * (32 + 16) + 4 * (size_t)(2 * H + 1) +
+               4 * (size_t)TK_WARPS * a.patch_ints + 2 * (size_t)cap + 64;
+    const size_t med = (size_t)4 * a.L.cap + 4 * 256;  // vals + hist (reuse table region)
+    return b > med ? b : med;
+}
+
+size_t map_smem(const TrackArgs &a) {
+    const int cap = a.K.cap, ncell = a.pp.grid_nx * a.pp.grid_ny;
+    return (size_t)52 * cap + sizeof(QItem) * TK_THREADS +
+           (a.hash_bits ? (sizeof(long long) << a.hash_bits) : 0) + 4 * (32 + 16 + TK_MAX_BINS) +
+           4 * (size_t)a.map_chunk_cap + 4 * (size_t)(2 * ncell + 1) + 2 * (size_t)cap + 64;
+}
+
+}  // namespace ft
+
+using namespace ft;
+
+namespace {
+// Launch geometry depends only on shapes; cache it so graph capture and
+// steady-state launches make no attribute / occupancy queries.
+struct GeomKey {
+    int dev, F, lcap, rcap, pcap, kcap, H, patch_ints, ncell, hash_bits, ws, wm;
+    bool operator==(const GeomKey &o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
+};
+struct Geom {
+    int Gs, Gm, W, chunk;
+    size_t smem;
+};
+constexpr int GEOM_CACHE = 8;
+thread_local GeomKey g_keys[GEOM_CACHE];
+thread_local Geom g_vals[GEOM_CACHE];
+thread_local int g_n = 0, g_next = 0;
+thread_local size_t g_attr_smem[64] = {0};
+}  // namespace
+
+static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out);
+
+static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_workspace *ws,
+                        cudaStream_t stream) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    GeomKey key;
+    memset(&key, 0, sizeof(key));
+    key.dev = dev;
+    key.F = a.F;
+    key.lcap = want_stereo ? a.L.cap : 0;
+    key.rcap = want_stereo ? a.R.cap : 0;
+    key.pcap = want_map ? a.P.cap : 0;
+    key.kcap = want_map ? a.K.cap : 0;
+    key.H = want_stereo ? a.sp.height : 0;
+    key.patch_ints = a.patch_ints;
+    key.ncell = want_map ? a.pp.grid_nx * a.pp.grid_ny : 0;
+    key.hash_bits = a.hash_bits;
+    key.ws = want_stereo;
+    key.wm = want_map;
+    Geom g;
+    int hit = -1;
+    for (int i = 0; i < g_n; ++i)
+        if (g_keys[i] == key) hit = i;
+    if (hit >= 0) {
+        g = g_vals[hit];
+    } else {
+        const int st = track_geometry(a, want_stereo, want_map, g);
+        if (st != FT_OK) return st;
+        g_keys[g_next] = key;
+        g_vals[g_next] = g;
+        g_next = (g_next + 1) % GEOM_CACHE;
+        if (g_n < GEOM_CACHE) ++g_n;
+    }
+    a.Gs = g.Gs;
+    a.Gm = g.Gm;
+    a.W = g.W;
+    a.map_chunk_cap = g.chunk;
+    if (dev >= 0 && dev < 64 && g.smem > g_attr_smem[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(track_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+        if (e != cudaSuccess) return (int)e;
+        g_attr_smem[dev] = g.smem;
+    }
+    if (a.W > ws->n_frames || a.Gm > WS_MAX_GROUP) return FT_E_WORKSPACE;
+    const WsLayout wl = ws_layout(ws);
+    a.bar_s = ws_ptr<unsigned long long>(ws, wl.track_bar_s);
+    a.bar_m = ws_ptr<unsigned long long>(ws, wl.track_bar_m);
+    a.ep_m = ws_ptr<unsigned long long>(ws, wl.track_ep_m);
+    a.claims = ws_ptr<unsigned long long>(ws, wl.proj_claims);
+    a.blk_counts = ws_ptr<int>(ws, wl.track_blk_counts);
+    a.hist = ws_ptr<int>(ws, wl.track_hist);
+
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.W * (a.Gs + a.Gm));
+    cfg.blockDim = dim3(TK_THREADS);
+    cfg.dynamicSmemBytes = g.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, track_kernel, a);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+
+static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int F = a.F;
+    // per-frame block budget: ~1 warp per left keypoint, ~128 map points per block
+    int gs_ideal = want_stereo ? (a.L.cap + TK_WARPS - 1) / TK_WARPS : 0;
+    int gm_ideal = want_map ? (a.P.cap + 127) / 128 : 0;
+    if (gs_ideal > 96) gs_ideal = 96;
+    if (gm_ideal > 64) gm_ideal = 64;
+    int Gs = gs_ideal, Gm = gm_ideal, W = F;
+    size_t smem = 0;
+    for (int iter = 0; iter < 4; ++iter) {
+        if (want_map) a.map_chunk_cap = (a.P.cap + Gm - 1) / Gm;
+        smem = want_stereo ? stereo_smem(a) : 0;
+        if (want_map) {
+            const size_t m = map_smem(a);
+            smem = m > smem ? m : smem;
+        }
+        if (smem > 227 * 1024) return FT_E_RANGE;
+        cudaError_t e = cudaFuncSetAttribute(track_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, track_kernel, TK_THREADS, smem);
+        if (occ < 1) return FT_E_RANGE;
+        const int capacity = occ * sms;
+        const int per_ideal = gs_ideal + gm_ideal;
+        int nGs, nGm, nW;
+        if ((long long)F * per_ideal <= capacity) {
+            nW = F;
+            nGs = gs_ideal;
+            nGm = gm_ideal;
+        } else {
+            const int min_per = (want_stereo ? 1 : 0) + (want_map ? 1 : 0);
+            nW = F < capacity / min_per ? F : capacity / min_per;
+            const int per = capacity / nW;
+            if (want_stereo && want_map) {
+                nGs = (int)((long long)per * gs_ideal / per_ideal);
+                if (nGs < 1) nGs = 1;
+                nGm = per - nGs;
+                if (nGm < 1) {
+                    nGm = 1;
+                    nGs = per - 1;
+                }
+            } else {
+                nGs = want_stereo ? per : 0;
+                nGm = want_map ? per : 0;
+            }
+        }
+        const bool same = nGs == Gs && nGm == Gm && nW == W;
+        Gs = nGs;
+        Gm = nGm;
+        W = nW;
+        if (same && iter > 0) break;
+    }
+    if (want_map) a.map_chunk_cap = (a.P.cap + Gm - 1) / Gm;
+    smem = want_stereo ? stereo_smem(a) : 0;
+    if (want_map) {
+        const size_t m = map_smem(a);
+        smem = m > smem ? m : smem;
+    }
+    if (smem > 227 * 1024) return FT_E_RANGE;
+    if (cudaFuncSetAttribute(track_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return FT_E_RANGE;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, track_kernel, TK_THREADS, smem);
+    while (W > 1 && (long long)W * (Gs + Gm) > (long long)occ * sms) --W;
+    if ((long long)W * (Gs + Gm) > (long long)occ * sms) return FT_E_RANGE;
+    out.Gs = Gs;
+    out.Gm = Gm;
+    out.W = W;
+    out.chunk = want_map ? a.map_chunk_cap : 0;
+    out.smem = smem;
+    return FT_OK;
+}
+
+static bool fill_stereo(TrackArgs &a, int32_t n_frames, const ft_keypoints *left,
+                        const ft_keypoints *right, const ft_pyramid *left_pyr,
+                        const ft_pyramid *right_pyr, const ft_stereo_params *params, int32_t mode,
+                        const ft_stereo_out *out, int *status) {
+    *status = FT_OK;
+    if (!left || !right || !params || !out) {
+        *status = FT_E_NULL;
+        return false;
+    }
+    if (n_frames < 1 || left->cap < 1 || right->cap < 1 || left->cap > 65535 ||
+        right->cap > 65535 || params->height < 1 || params->height > 65535 ||
+        params->n_levels < 1 || params->n_levels > FT_MAX_LEVELS) {
+        *status = FT_E_RANGE;
+        return false;
+    }
+    if (params->half_window < 1 || params->half_slide < 1 || params->half_window > 32 ||
+        params->half_slide > 32 || ((mode & FT_STEREO_REFINE) && (mode & FT_STEREO_FROM_CAND))) {
+        *status = FT_E_CONFIG;
+        return false;
+    }
+    const bool finalize = mode & (FT_STEREO_REFINE | FT_STEREO_FROM_CAND | FT_STEREO_REJECT);
+    if (((mode & FT_STEREO_PHASE1) && !out->cand_idx && !finalize) ||
+        (!(mode & FT_STEREO_PHASE1) && (mode & (FT_STEREO_REFINE | FT_STEREO_FROM_CAND)) &&
+         (!out->cand_idx || !out->cand_dist)) ||
+        (out->cand_idx && !out->cand_dist) ||
+        (finalize && (!out->right_idx || !out->distance || !out->disparity || !out->refined_u ||
+                      !out->depth || !out->sad)) ||
+        ((mode & FT_STEREO_REFINE) && (!left_pyr || !right_pyr || !left_pyr->data || !right_pyr->data))) {
+        *status = FT_E_NULL;
+        return false;
+    }
+    if ((mode & FT_STEREO_REFINE) &&
+        (left_pyr->n_levels < params->n_levels || right_pyr->n_levels < params->n_levels)) {
+        *status = FT_E_RANGE;
+        return false;
+    }
+    a.smode = mode;
+    a.L = *left;
+    a.R = *right;
+    if (left_pyr) a.PL = *left_pyr;
+    else memset(&a.PL, 0, sizeof(a.PL));
+    if (right_pyr) a.PR = *right_pyr;
+    else memset(&a.PR, 0, sizeof(a.PR));
+    a.sp = *params;
+    a.so = *out;
+    const int nw = 2 * params->half_window + 1;
+    const int nr = 2 * params->half_slide + 2 * params->half_window + 1;
+    a.patch_ints = (mode & FT_STEREO_REFINE) ? nw * nw + nw * nr + 2 * params->half_slide + 1 : 0;
+    return true;
+}
+
+static bool fill_map(TrackArgs &a, int32_t n_frames, const ft_map_points *points,
+                     const ft_keypoints *frame, const ft_project_params *params,
+                     const ft_project_io *io, int32_t mode, const ft_project_out *out, int *status) {
+    *status = FT_OK;
+    if (!points || !frame || !params || !io || !out) {
+        *status = FT_E_NULL;
+        return false;
+    }
+    if (n_frames < 1 || points->cap < 1 || frame->cap < 1 || frame->cap > 65535 ||
+        points->cap > (1 << 23) || params->n_levels < 1 || params->n_levels > FT_MAX_LEVELS ||
+        params->cell_px < 1 || params->grid_nx < 1 || params->grid_ny < 1 ||
+        params->grid_nx * params->grid_ny > 16384) {
+        *status = FT_E_RANGE;
+        return false;
+    }
+    if (params->histogram_bins < 1 || params->histogram_bins > TK_MAX_BINS ||
+        params->histogram_keep < 1 || params->histogram_keep > params->histogram_bins ||
+        ((mode & FT_PROJ_WRITE_SLOTS) && !(mode & FT_PROJ_RESOLVE))) {
+        *status = FT_E_CONFIG;
+        return false;
+    }
+    if (!io->rot || !io->trans || ((mode & (FT_PROJ_SKIP_SLOTS | FT_PROJ_WRITE_SLOTS)) && !io->slots_in) ||
+        ((mode & FT_PROJ_WRITE_SLOTS) && !io->slots_out) ||
+        (out->out_kp && (!out->out_dist || !out->out_oct)) ||
+        (out->corr_point && (!out->corr_kp || !out->corr_dist || !out->corr_oct))) {
+        *status = FT_E_NULL;
+        return false;
+    }
+    a.pmode = mode;
+    a.P = *points;
+    a.K = *frame;
+    a.pp = *params;
+    a.io = *io;
+    a.po = *out;
+    a.hash_bits = 0;
+    if (mode & FT_PROJ_SKIP_SLOTS) {
+        int bits = 1;
+        while ((1 << bits) < 2 * frame->cap) ++bits;
+        a.hash_bits = bits;
+    }
+    a.map_chunk_cap = 0;
+    return true;
+}
+
+extern "C" int ft_track_frames(int32_t n_frames, const ft_keypoints *left,
+                               const ft_keypoints *right, const ft_pyramid *left_pyr,
+                               const ft_pyramid *right_pyr, const ft_stereo_params *sparams,
+                               int32_t smode, const ft_stereo_out *sout,
+                               const ft_map_points *points, const ft_project_params *pparams,
+                               const ft_project_io *io, int32_t pmode, const ft_project_out *pout,
+                               const ft_workspace *ws, ft_stream_t stream) {
+    TrackArgs a;
+    memset(&a, 0, sizeof(a));
+    a.F = n_frames;
+    int st;
+    if (!fill_stereo(a, n_frames, left, right, left_pyr, right_pyr, sparams, smode, sout, &st))
+        return st;
+    if (!fill_map(a, n_frames, points, left, pparams, io, pmode, pout, &st)) return st;
+    const int capl = left->cap > right->cap ? left->cap : right->cap;
+    st = ws_check(ws, n_frames, capl, points->cap);
+    if (st != FT_OK) return st;
+    return track_launch(a, true, true, ws, (cudaStream_t)stream);
+}
+
+extern "C" int ft_stereo_pinhole(int32_t n_frames, const ft_keypoints *left,
+                                 const ft_keypoints *right, const ft_pyramid *left_pyr,
+                                 const ft_pyramid *right_pyr, const ft_stereo_params *params,
+                                 int32_t mode, const ft_stereo_out *out, const ft_workspace *ws,
+                                 ft_stream_t stream) {
+    TrackArgs a;
+    memset(&a, 0, sizeof(a));
+    a.F = n_frames;
+    int st;
+    if (!fill_stereo(a, n_frames, left, right, left_pyr, right_pyr, params, mode, out, &st))
+        return st;
+    if (!ws) return FT_E_NULL;
+    const int capl = left->cap > right->cap ? left->cap : right->cap;
+    st = ws_check(ws, n_frames, capl, 1);
+    if (st != FT_OK) return st;
+    return track_launch(a, true, false, ws, (cudaStream_t)stream);
+}
+
+extern "C" int ft_project_search(int32_t n_frames, const ft_map_points *points,
+                                 const ft_keypoints *frame, const ft_project_params *params,
+                                 const ft_project_io *io, int32_t mode, const ft_project_out *out,
+                                 const ft_workspace *ws, ft_stream_t stream) {
+    TrackArgs a;
+    memset(&a, 0, sizeof(a));
+    a.F = n_frames;
+    int st;
+    if (!fill_map(a, n_frames, points, frame, params, io, mode, out, &st)) return st;
+    if (!ws) return FT_E_NULL;
+    st = ws_check(ws, n_frames, frame->cap, points->cap);
+    if (st != FT_OK) return st;
+    return track_launch(a, false, true, ws, (cudaStream_t)stream);
+}

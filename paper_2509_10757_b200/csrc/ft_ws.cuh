@@ -5,9 +5,12 @@
 // use it, and the stereo and projection entries may run concurrently):
 //   stereo   counters u32[F]
 //   fisheye  counters u32[F * tiles(cap_left)] | partials uint2[fisheye_entries]
-//   project  counters u32[F] | blk_count i32[F * nb(cap_points)]
-//            | claims u64[F * cap_left] | blk_list uint2[F * cap_points]
-// Counters start at 0 and claims at ~0; kernels restore both before exit.
+//   project  claims u64[F * cap_left]
+//   track    barrier counters u64[F] (stereo) | u64[F] (map) | epoch counters
+//            u64[F] | per-block counts i32[F * WS_MAX_GROUP] | hist i32[F * 256]
+// Counters start at 0 and claims at ~0 (ft_workspace_init).  Barrier and
+// epoch counters only grow; claims carry the launch epoch in their high word,
+// so no kernel has to reset anything.
 #pragma once
 
 #include <stddef.h>
@@ -19,12 +22,11 @@ namespace ft {
 
 constexpr size_t WS_ALIGN = 256;
 constexpr int WS_BF_TL = 128;   // fisheye left tile (ft_fisheye.cu)
-constexpr int WS_PPB = 256;     // map points per block (ft_project.cu)
+constexpr int WS_MAX_GROUP = 1024;  // max map blocks per frame (ft_track.cu)
 constexpr int WS_SM_HINT = 148;
 
 inline size_t ws_align(size_t x) { return (x + WS_ALIGN - 1) & ~(WS_ALIGN - 1); }
 inline int ws_tiles(int cap_left) { return (cap_left + WS_BF_TL - 1) / WS_BF_TL; }
-inline int ws_nb(int cap_points) { return (cap_points + WS_PPB - 1) / WS_PPB; }
 
 // Right-set splits of the fisheye all-pairs kernel: about 4 blocks per SM.
 inline int fisheye_splits(int F, int cap_left, int cap_right) {
@@ -42,12 +44,13 @@ inline size_t fisheye_entries(int F, int cap_left) {
 }
 
 struct WsLayout {
-    size_t stereo_counters, fisheye_counters, fisheye_partials, proj_counters, proj_blk_count,
-        proj_claims, proj_blk_list, total;
+    size_t stereo_counters, fisheye_counters, fisheye_partials, proj_claims, track_bar_s,
+        track_bar_m, track_ep_m, track_blk_counts, track_hist, total;
     size_t fisheye_partial_entries;
 };
 
 inline WsLayout ws_layout(int F, int cap_left, int cap_points) {
+    (void)cap_points;
     WsLayout L;
     size_t o = 0;
     L.stereo_counters = o;
@@ -57,14 +60,18 @@ inline WsLayout ws_layout(int F, int cap_left, int cap_points) {
     L.fisheye_partials = o;
     L.fisheye_partial_entries = fisheye_entries(F, cap_left);
     o += ws_align(L.fisheye_partial_entries * 8);
-    L.proj_counters = o;
-    o += ws_align((size_t)F * 4);
-    L.proj_blk_count = o;
-    o += ws_align((size_t)F * ws_nb(cap_points) * 4);
     L.proj_claims = o;
     o += ws_align((size_t)F * cap_left * 8);
-    L.proj_blk_list = o;
-    o += ws_align((size_t)F * cap_points * 8);
+    L.track_bar_s = o;
+    o += ws_align((size_t)F * 8);
+    L.track_bar_m = o;
+    o += ws_align((size_t)F * 8);
+    L.track_ep_m = o;
+    o += ws_align((size_t)F * 8);
+    L.track_blk_counts = o;
+    o += ws_align((size_t)F * WS_MAX_GROUP * 4);
+    L.track_hist = o;
+    o += ws_align((size_t)F * 256 * 4);
     L.total = o;
     return L;
 }

@@ -4,13 +4,14 @@ streams on one B200 (BASELINE cfg 2/4/5).
 One step processes one frame of every stream:
 
     pinned staging --(1 H2D)--> device inputs
-        stream A: ft_stereo_pinhole   phase 1 -> phase 2 | from-candidates -> reject
-        stream B: ft_project_search   skip-slotted -> phase A -> resolve -> slot write
+        ft_track_frames (ONE cooperative launch):
+            stereo blocks: phase 1 -> phase 2 | from-candidates -> reject
+            map blocks:    skip slotted -> phase A -> resolve -> slot write
     device results --(1 D2H)--> pinned results
 
 Stereo and the local-map search are independent within a frame (the
 reference runs them in sequence only because it is single-threaded,
-tracker.py:268-358), so they run concurrently on two streams.  The whole step
+tracker.py:268-358), so they run side by side in one launch.  The whole step
 is captured ONCE as a CUDA graph; per-frame counts live in device memory, so
 replays need no re-capture.  Layout: every per-frame array is at a fixed
 stride (capacity) per stream, inputs packed first (one contiguous H2D range),
@@ -100,7 +101,6 @@ class FramePipeline:
         self.host = torch.zeros(lay.total, dtype=torch.uint8).pin_memory()
         self.hnp = self.host.numpy()
         self.stream = torch.cuda.Stream(self.device)
-        self.stream_b = torch.cuda.Stream(self.device)
         self.ws = make_workspace(self.lib, self.device, self.stream, S, ck, cp)
         self._build_structs()
         self.graph = None
@@ -210,15 +210,18 @@ class FramePipeline:
                                               self.pio, self.pmode, self.pout, self.ws,
                                               stream.cuda_stream), "ft_project_search")
 
+    def launch_track(self, stream) -> None:
+        _lib.check(self.lib.ft_track_frames(self.S, self.kl, self.kr, self.pl, self.pr,
+                                            self.sparams, self.smode, self.sout, self.points,
+                                            self.pparams, self.pio, self.pmode, self.pout,
+                                            self.ws, stream.cuda_stream), "ft_track_frames")
+
     def _step(self, copies: bool) -> None:
-        a, b = self.stream, self.stream_b
+        a = self.stream
         if copies:
             with torch.cuda.stream(a):
                 self.dev[:self.in_end].copy_(self.host[:self.in_end], non_blocking=True)
-        b.wait_stream(a)
-        self.launch_stereo(a)
-        self.launch_project(b)
-        a.wait_stream(b)
+        self.launch_track(a)
         if copies:
             with torch.cuda.stream(a):
                 self.host[self.out_begin:self.out_end].copy_(
