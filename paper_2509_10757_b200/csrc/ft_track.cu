@@ -37,7 +37,10 @@
 //   stale claims from earlier launches always lose (no reset pass).  After a
 //   group barrier each block resolves its own points; ordered outputs use
 //   one more barrier for the cross-block prefix.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "ft_common.cuh"
 #include "ft_ws.cuh"
@@ -75,7 +78,22 @@ struct TrackArgs {
     unsigned long long *claims;  // [F][cap_kp]
     int *blk_counts;             // [F][Gm]
     int *hist;                   // [F][TK_MAX_BINS]
+    unsigned long long *tl;      // optional timeline [grid][TL_SLOTS] (FT_DEBUG_TIMELINE)
 };
+
+constexpr int TL_SLOTS = 8;
+
+FT_DEV unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// timeline mark (debug only): slot k of this block
+#define TL_MARK(a, k)                                                               \
+    do {                                                                            \
+        if ((a).tl && threadIdx.x == 0) (a).tl[blockIdx.x * TL_SLOTS + (k)] = global_ns(); \
+    } while (0)
 
 // ---------------------------------------------------------------------------
 // group barrier among the G blocks of one role in one slot.  The counter only
@@ -298,6 +316,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
     sm.items = reinterpret_cast<uint16_t *>(p);
 
     if (rank == 0 && threadIdx.x == 0 && a.so.n_matched) a.so.n_matched[f] = 0;
+    TL_MARK(a, 0);
 
     if (k0 < k1 && (do_p1 || finalize)) {
         if (do_p1) {
@@ -322,6 +341,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
                 },
                 sm.row_start, sm.row_cursor, sm.items, sm.scan_tmp);
         }
+        TL_MARK(a, 1);
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         int *patch = sm.patch + wid * a.patch_ints;
         for (int k = k0 + wid; k < k1; k += TK_WARPS) {
@@ -361,8 +381,11 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
             }
         }
     }
+    __syncthreads();
+    TL_MARK(a, 2);
     if (!do_rej && !a.so.n_matched) return;
     group_barrier(bar, G);
+    TL_MARK(a, 3);
     int kept = 0;
     if (do_rej) {
         // every block computes the same median over the frame's accepted SADs
@@ -429,6 +452,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
         if ((threadIdx.x & 31) == 0 && kept) atomicAdd(a.so.n_matched + f, kept);
     }
     __syncthreads();  // smem reuse by the next frame of this slot
+    TL_MARK(a, 4);
 }
 
 // ---------------------------------------------------------------------------
@@ -601,6 +625,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     p += (size_t)4 * cap_kp;
     sm.items = reinterpret_cast<uint16_t *>(p);
 
+    TL_MARK(a, 0);
     // launch epoch: the same for every block of this slot's frame instance
     if (threadIdx.x == 0) {
         const unsigned long long t = atomicAdd(a.ep_m + slot, 1ull);
@@ -659,6 +684,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             }
             __syncthreads();
         }
+        TL_MARK(a, 1);
         const double *R = a.io.rot + 9 * f, *T = a.io.trans + 3 * f;
         const double ccx = -(R[0] * T[0] + R[3] * T[1] + R[6] * T[2]);
         const double ccy = -(R[1] * T[0] + R[4] * T[1] + R[7] * T[2]);
@@ -685,6 +711,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                 }
             }
             __syncthreads();
+            TL_MARK(a, 2);
             const int nq = sm.misc[1];
             for (int qi = wid; qi < nq; qi += TK_WARPS) {  // warp per visible point
                 const QItem q = sm.queue[qi];
@@ -724,11 +751,11 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             __syncthreads();
         }
     }
-    if (!resolve) {
-        __syncthreads();
-        return;
-    }
+    __syncthreads();
+    TL_MARK(a, 3);
+    if (!resolve) return;
     group_barrier(bar, G);
+    TL_MARK(a, 4);
 
     // phase B on this block's points: winner iff its claim is the minimum
     int n_win = 0;
@@ -798,6 +825,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             if ((threadIdx.x & 31) == 0 && tot) atomicAdd(a.po.corr_count + f, tot);
         }
         __syncthreads();
+        TL_MARK(a, 5);
         return;
     }
     // ordered correspondences: block counts -> prefix over ranks -> write
@@ -845,6 +873,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
         base += total;
     }
     __syncthreads();
+    TL_MARK(a, 5);
 }
 
 __global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
@@ -894,10 +923,24 @@ constexpr int GEOM_CACHE = 8;
 thread_local GeomKey g_keys[GEOM_CACHE];
 thread_local Geom g_vals[GEOM_CACHE];
 thread_local int g_n = 0, g_next = 0;
-thread_local size_t g_attr_smem[64] = {0};
+size_t g_attr_smem[64] = {0};  // process-wide, guarded by g_attr_mu
+std::mutex g_attr_mu;
 }  // namespace
 
 static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out);
+
+// The kernel's max-dynamic-smem attribute only ever grows (one attribute per
+// function: lowering it for a small launch would break a cached large one).
+static int raise_smem_attr(int dev, size_t smem) {
+    if (dev < 0 || dev >= 64) return FT_E_RANGE;
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    if (smem <= g_attr_smem[dev]) return FT_OK;
+    const cudaError_t e =
+        cudaFuncSetAttribute(track_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    g_attr_smem[dev] = smem;
+    return FT_OK;
+}
 
 static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_workspace *ws,
                         cudaStream_t stream) {
@@ -935,11 +978,20 @@ static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_
     a.Gm = g.Gm;
     a.W = g.W;
     a.map_chunk_cap = g.chunk;
-    if (dev >= 0 && dev < 64 && g.smem > g_attr_smem[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(track_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
-        if (e != cudaSuccess) return (int)e;
-        g_attr_smem[dev] = g.smem;
+    {
+        const int st = raise_smem_attr(dev, g.smem);
+        if (st != FT_OK) return st;
+    }
+    if (getenv("FT_DEBUG_GEOMETRY")) {
+        int occ = -1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, track_kernel, TK_THREADS, g.smem);
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, track_kernel);
+        fprintf(stderr,
+                "[ft_track] F=%d W=%d Gs=%d Gm=%d smem=%zu grid=%d cached=%d occ=%d "
+                "maxDyn=%d regs=%d\n",
+                a.F, a.W, a.Gs, a.Gm, g.smem, a.W * (a.Gs + a.Gm), hit >= 0, occ,
+                fa.maxDynamicSharedSizeBytes, fa.numRegs);
     }
     if (a.W > ws->n_frames || a.Gm > WS_MAX_GROUP) return FT_E_WORKSPACE;
     const WsLayout wl = ws_layout(ws);
@@ -949,6 +1001,16 @@ static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_
     a.claims = ws_ptr<unsigned long long>(ws, wl.proj_claims);
     a.blk_counts = ws_ptr<int>(ws, wl.track_blk_counts);
     a.hist = ws_ptr<int>(ws, wl.track_hist);
+    a.tl = nullptr;
+    static unsigned long long *tl_buf = nullptr;
+    if (getenv("FT_DEBUG_TIMELINE")) {
+        const size_t n = (size_t)a.W * (a.Gs + a.Gm) * TL_SLOTS;
+        if (!tl_buf) cudaMalloc(&tl_buf, 1 << 20);
+        if (n * 8 <= (1 << 20)) {
+            cudaMemsetAsync(tl_buf, 0, n * 8, stream);
+            a.tl = tl_buf;
+        }
+    }
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.W * (a.Gs + a.Gm));
@@ -962,6 +1024,22 @@ static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, track_kernel, a);
     if (e != cudaSuccess) return (int)e;
+    if (a.tl) {  // debug: dump the per-block timeline (ns) after the launch
+        const size_t n = (size_t)a.W * (a.Gs + a.Gm) * TL_SLOTS;
+        static unsigned long long host[1 << 17];
+        cudaMemcpyAsync(host, a.tl, n * 8, cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
+        FILE *fp = fopen(getenv("FT_DEBUG_TIMELINE"), "a");
+        if (fp) {
+            fprintf(fp, "launch F=%d W=%d Gs=%d Gm=%d\n", a.F, a.W, a.Gs, a.Gm);
+            for (size_t b = 0; b < n / TL_SLOTS; ++b) {
+                fprintf(fp, "%zu", b);
+                for (int k = 0; k < TL_SLOTS; ++k) fprintf(fp, " %llu", host[b * TL_SLOTS + k]);
+                fprintf(fp, "\n");
+            }
+            fclose(fp);
+        }
+    }
     return (int)cudaGetLastError();
 }
 
@@ -985,9 +1063,8 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
             smem = m > smem ? m : smem;
         }
         if (smem > 227 * 1024) return FT_E_RANGE;
-        cudaError_t e = cudaFuncSetAttribute(track_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
+        const int st = raise_smem_attr(dev, smem);
+        if (st != FT_OK) return st;
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, track_kernel, TK_THREADS, smem);
         if (occ < 1) return FT_E_RANGE;
@@ -1028,9 +1105,7 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
         smem = m > smem ? m : smem;
     }
     if (smem > 227 * 1024) return FT_E_RANGE;
-    if (cudaFuncSetAttribute(track_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return FT_E_RANGE;
+    if (raise_smem_attr(dev, smem) != FT_OK) return FT_E_RANGE;
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, track_kernel, TK_THREADS, smem);
     while (W > 1 && (long long)W * (Gs + Gm) > (long long)occ * sms) --W;

@@ -1,0 +1,79 @@
+"""GPU parity of the resident, graph-captured FramePipeline (ft_track_frames):
+several independent frame streams per launch, repeated graph replays (the
+barrier / epoch counters must carry across launches), and enough streams to
+force multiple frame waves per group slot."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("right_idx", "distance", "disparity", "refined_u", "depth", "sad")
+
+
+@pytest.fixture(scope="module")
+def workloads():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_10757_b200.synthetic import make_workload
+    return [make_workload(seed=100 + i, n_landmarks=12000, map_points=5000, images=True,
+                          offset=0.05 * i) for i in range(4)]
+
+
+@pytest.fixture(scope="module")
+def expected(workloads, oracle):
+    from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
+    out = []
+    for i, w in enumerate(workloads):
+        m = oracle.stereo_pinhole(w.left, w.right, w.pyr_left, w.pyr_right, w.cam,
+                                  StereoMatchConfig(), w.scale_pow)
+        rng = np.random.default_rng(i)
+        slots_in = np.full(len(w.left.u), -1, np.int64)
+        k = rng.choice(len(slots_in), size=60, replace=False)
+        slots_in[k] = rng.choice(w.local.point_ids, size=60, replace=False)
+        slots = slots_in.copy()
+        grid = oracle.frame_grid(w.left.u, w.left.v, w.cam.width, w.cam.height, 48) + (48,)
+        n = oracle.search_local_points(w.local.point_ids, w.local.soa, w.left.u, w.left.v,
+                                       w.left.octave, w.left.descriptors, grid, slots, w.pose,
+                                       w.cam, ProjectionSearchConfig(), 1.2, 8)
+        out.append((m, slots_in, slots, n))
+    return out
+
+
+def _run(workloads, expected, n_streams, replays):
+    from paper_2509_10757_b200.pipeline import FramePipeline
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    cap_pts = max(len(w.local.point_ids) for w in workloads)
+    pipe = FramePipeline(w0.cam, n_streams=n_streams, cap_kp=(cap_kp + 31) // 32 * 32,
+                         cap_points=(cap_pts + 255) // 256 * 256, pyramid_geometry=w0.pyr_left)
+    for s in range(n_streams):
+        w = workloads[s % len(workloads)]
+        pipe.load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                        slots=expected[s % len(workloads)][1])
+    for r in range(replays):
+        pipe.replay(copies=True)
+        pipe.synchronize()
+        for s in range(n_streams):
+            w = workloads[s % len(workloads)]
+            m, _, slots, n = expected[s % len(workloads)]
+            res = pipe.result(s, len(w.left.u))
+            for f in FIELDS:
+                np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f),
+                                              err_msg=f"stream {s} replay {r} {f}")
+            np.testing.assert_array_equal(res.slots, slots, err_msg=f"stream {s} replay {r}")
+            assert res.n_slots == n
+            assert res.n_matched == int((m.right_idx >= 0).sum())
+
+
+def test_single_stream_replays(workloads, expected):
+    _run(workloads, expected, 1, 5)
+
+
+def test_four_streams(workloads, expected):
+    _run(workloads, expected, 4, 3)
+
+
+def test_many_streams_multiple_waves(workloads, expected):
+    _run(workloads, expected, 200, 2)
