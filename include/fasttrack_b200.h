@@ -19,7 +19,11 @@
  *
  * Descriptors are 256-bit ORB strings, 32 bytes per row, bit b in 64-bit word
  * b >> 6 at bit b & 63 (reference descriptors.py:7-9,23-30); the kernels read
- * them as 8 x u32 with two 16-byte vector loads, so rows must be 16-B aligned.
+ * them as 8 x u32 with two 16-byte vector loads.
+ *
+ * Alignment: per-frame tables are staged into shared memory with TMA bulk
+ * copies, so every array base must be 16-byte aligned and every capacity a
+ * multiple of 4 (FT_E_RANGE otherwise).
  *
  * Reference interface each entry replaces:
  *   ft_hamming_pairs        kernels.py:48-51        hamming_pairs_kernel

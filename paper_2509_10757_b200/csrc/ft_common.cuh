@@ -176,3 +176,52 @@ __device__ inline bool last_block_ticket(unsigned *counter, unsigned n_blocks, i
 }
 
 }  // namespace ft
+
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, global -> shared) completed on an mbarrier.
+// Sizes and addresses must be multiples of 16 bytes.
+
+namespace ft {
+
+FT_DEV unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+FT_DEV void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+FT_DEV void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+FT_DEV void mbar_wait(unsigned long long *bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// Order earlier generic-proxy shared-memory accesses before later async
+// (TMA) writes into the same buffers.
+FT_DEV void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+FT_DEV void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+FT_DEV unsigned round16(unsigned b) { return (b + 15u) & ~15u; }
+
+}  // namespace ft

@@ -70,7 +70,9 @@ struct TrackArgs {
     ft_project_io io;
     ft_project_out po;
     int32_t hash_bits;
-    int32_t map_chunk_cap;  // max points per map block (smem sizing)
+    int32_t map_chunk_cap;  // max points per map block (smem sizing), even
+    int32_t stage_rdesc;    // stereo: right descriptors staged in smem (else read from L2)
+    int32_t stage_kdesc;    // map: keypoint descriptors staged in smem
     // workspace
     unsigned long long *bar_s;   // [W]
     unsigned long long *bar_m;   // [W]
@@ -163,7 +165,8 @@ __device__ uint32_t block_select(const uint32_t *vals, int n, int k, int *hist, 
 
 struct StereoSmem {
     double *ru, *rv;
-    uint4 *rd;        // [2*cap]
+    uint4 *rd;        // [2*cap] (when staged)
+    const uint4 *rdg; // global right descriptors of the frame
     int *ro;
     int *row_start;   // [H+1]
     int *row_cursor;  // [H]
@@ -173,32 +176,52 @@ struct StereoSmem {
     int *misc;        // [16]
 };
 
-FT_DEV int phase1(const TrackArgs &a, const StereoSmem &sm, int64_t lk, int lane, int &cdist) {
-    const double v = a.L.v[lk], u = a.L.u[lk];
-    const int o = a.L.octave[lk];
-    const double band = a.sp.band_factor * a.sp.scale_pow[clampi(o, 0, FT_MAX_LEVELS - 1)];
-    long long r0 = (long long)floor(v - band);
-    long long r1 = (long long)ceil(v + band);
+// One warp's left keypoint, loaded once (every lane issues the same
+// broadcast loads, so the values are warp-uniform).
+struct LeftKp {
+    double u, v;
+    int o;
+    Desc d;
+};
+
+FT_DEV LeftKp load_left(const TrackArgs &a, int64_t lk) {
+    LeftKp k;
+    k.u = __ldg(a.L.u + lk);
+    k.v = __ldg(a.L.v + lk);
+    k.o = __ldg(a.L.octave + lk);
+    k.d = load_desc(a.L.desc, lk);
+    return k;
+}
+
+// Phase 1 (kernels.py:312-345) over the contiguous CSR range of rows
+// [floor(v - band), ceil(v + band)] held in shared memory.
+FT_DEV int phase1(const TrackArgs &a, const StereoSmem &sm, const LeftKp &kp, int lane,
+                  int &cdist) {
+    const double band = a.sp.band_factor * a.sp.scale_pow[clampi(kp.o, 0, FT_MAX_LEVELS - 1)];
+    long long r0 = (long long)floor(kp.v - band);
+    long long r1 = (long long)ceil(kp.v + band);
     const int H = a.sp.height;
     if (r0 < 0) r0 = 0;
     if (r1 > H - 1) r1 = H - 1;
     uint32_t best = NO_KEY;
     if (r0 <= r1) {
         const int beg = sm.row_start[r0], end = sm.row_start[r1 + 1];
-        if (beg < end) {
-            const Desc ld = load_desc(a.L.desc, lk);
-            for (int ii = beg + lane; ii < end; ii += 32) {
-                const int j = sm.items[ii];
-                const int ro = sm.ro[j];
-                if (ro < o - 1 || ro > o + 1) continue;
-                if (fabs(sm.rv[j] - v) > band) continue;
-                const double disp = u - sm.ru[j];
-                if (disp < a.sp.min_disparity || disp > a.sp.max_disparity) continue;
-                Desc rd;
+        for (int ii = beg + lane; ii < end; ii += 32) {
+            const int j = sm.items[ii];
+            const int ro = sm.ro[j];
+            if (ro < kp.o - 1 || ro > kp.o + 1) continue;
+            if (fabs(sm.rv[j] - kp.v) > band) continue;
+            const double disp = kp.u - sm.ru[j];
+            if (disp < a.sp.min_disparity || disp > a.sp.max_disparity) continue;
+            Desc rd;
+            if (a.stage_rdesc) {
                 rd.lo = sm.rd[2 * j];
                 rd.hi = sm.rd[2 * j + 1];
-                best = min(best, (hamming(ld, rd) << 16) | (uint32_t)j);
+            } else {
+                rd.lo = __ldg(sm.rdg + 2 * j);
+                rd.hi = __ldg(sm.rdg + 2 * j + 1);
             }
+            best = min(best, (hamming(kp.d, rd) << 16) | (uint32_t)j);
         }
     }
     best = __reduce_min_sync(FULL, best);
@@ -210,34 +233,40 @@ FT_DEV int phase1(const TrackArgs &a, const StereoSmem &sm, int64_t lk, int lane
     return -1;
 }
 
-// Phase 2 for one candidate; every lane returns the same verdict.
-FT_DEV bool phase2(const TrackArgs &a, int *patch, int f, int64_t lk, double ur_cand, int lane,
-                   double &disp_out, double &ur_out, int &sad_out) {
-    const int o = clampi(a.L.octave[lk], 0, a.PL.n_levels - 1);
-    const double s = a.sp.scale_pow[o];
-    const double ulev = a.L.u[lk] / s, vlev = a.L.v[lk] / s, urlev = ur_cand / s;
-    const long long xi = round_half_even(ulev), yi = round_half_even(vlev),
-                    xr0 = round_half_even(urlev);
+// Phase-2 patch geometry on the keypoint's octave level (kernels.py:371-387).
+struct P2Geom {
+    int o;
+    double s;
+    long long xi, yi, wl, wr;
+    bool left_ok;
+    const uint8_t *lp, *rp;
+};
+
+FT_DEV P2Geom p2_geom(const TrackArgs &a, int f, const LeftKp &kp) {
+    P2Geom g;
+    g.o = clampi(kp.o, 0, a.PL.n_levels - 1);
+    g.s = a.sp.scale_pow[g.o];
+    const double ulev = kp.u / g.s, vlev = kp.v / g.s;
+    g.xi = round_half_even(ulev);
+    g.yi = round_half_even(vlev);
+    const int hw = a.sp.half_window;
+    g.wl = a.PL.widths[g.o];
+    g.wr = a.PR.widths[g.o];
+    const long long hl = a.PL.heights[g.o];
+    g.left_ok = !(g.xi - hw < 0 || g.xi + hw >= g.wl || g.yi - hw < 0 || g.yi + hw >= hl);
+    g.lp = a.PL.data + (int64_t)f * a.PL.frame_bytes + a.PL.offsets[g.o];
+    g.rp = a.PR.data + (int64_t)f * a.PR.frame_bytes + a.PR.offsets[g.o];
+    return g;
+}
+
+// SAD sweep + parabola (kernels.py:388-428) on patches staged in `patch`:
+// pl [nw][nw] = L - cl, pr [nw][nr] = R.  Every lane returns the same verdict.
+FT_DEV bool p2_sweep(const TrackArgs &a, int *patch, const LeftKp &kp, const P2Geom &g,
+                     long long xr0, int lane, double &disp_out, double &ur_out, int &sad_out) {
     const int hw = a.sp.half_window, hs = a.sp.half_slide;
-    const long long wl = a.PL.widths[o], hl = a.PL.heights[o];
-    const long long wr = a.PR.widths[o], hr = a.PR.heights[o];
-    if (xi - hw < 0 || xi + hw >= wl || yi - hw < 0 || yi + hw >= hl) return false;
-    if (xr0 - hs - hw < 0 || xr0 + hs + hw >= wr || yi - hw < 0 || yi + hw >= hr) return false;
-    const uint8_t *lp = a.PL.data + (int64_t)f * a.PL.frame_bytes + a.PL.offsets[o];
-    const uint8_t *rp = a.PR.data + (int64_t)f * a.PR.frame_bytes + a.PR.offsets[o];
     const int nw = 2 * hw + 1, nr = 2 * hs + 2 * hw + 1, noff = 2 * hs + 1;
-    int *pl = patch;           // [nw][nw]  L - cl
-    int *pr = pl + nw * nw;    // [nw][nr]  R
-    int *sads = pr + nw * nr;  // [noff]
-    const int cl = __ldg(lp + yi * wl + xi);
-    for (int t = lane; t < nw * nw; t += 32) {
-        const int dy = t / nw, dx = t - dy * nw;
-        pl[t] = (int)__ldg(lp + (yi - hw + dy) * wl + (xi - hw + dx)) - cl;
-    }
-    for (int t = lane; t < nw * nr; t += 32) {
-        const int dy = t / nr, dx = t - dy * nr;
-        pr[t] = __ldg(rp + (yi - hw + dy) * wr + (xr0 - hs - hw + dx));
-    }
+    const int *pl = patch, *pr = patch + nw * nw;
+    int *sads = patch + nw * nw + nw * nr;
     for (int t = lane; t < noff; t += 32) sads[t] = 0;
     __syncwarp();
     for (int t = lane; t < noff * nw; t += 32) {  // job = (offset, row)
@@ -268,8 +297,8 @@ FT_DEV bool phase2(const TrackArgs &a, int *patch, int f, int64_t lk, double ur_
     if (denom <= 0.0) return false;
     const double delta = (d_m - d_p) / (2.0 * denom);
     if (delta < -1.0 || delta > 1.0) return false;
-    const double ur_ref = ((double)(xr0 + (best_oi - hs)) + delta) * s;
-    const double disp = a.L.u[lk] - ur_ref;
+    const double ur_ref = ((double)(xr0 + (best_oi - hs)) + delta) * g.s;
+    const double disp = kp.u - ur_ref;
     if (disp < a.sp.min_disparity || disp > a.sp.max_disparity) return false;
     disp_out = disp;
     ur_out = ur_ref;
@@ -277,8 +306,112 @@ FT_DEV bool phase2(const TrackArgs &a, int *patch, int f, int64_t lk, double ur_
     return true;
 }
 
+// Full per-keypoint stereo step for one warp.  The left patch loads are
+// issued before phase 1 (they depend only on the keypoint), so their latency
+// hides behind the candidate search; the right strip follows phase 1.
+template <int HW, int HS>
+FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int f, int64_t lk,
+                      int64_t rbase, int n_right, const LeftKp &kp, int lane) {
+    constexpr bool FIXED = HW > 0;
+    const int hw = FIXED ? HW : a.sp.half_window;
+    const int hs = FIXED ? HS : a.sp.half_slide;
+    const int nw = 2 * hw + 1, nr = 2 * hs + 2 * hw + 1;
+    constexpr int LPL = FIXED ? ((2 * HW + 1) * (2 * HW + 1) + 31) / 32 : 1;
+    constexpr int RPL = FIXED ? ((2 * HW + 1) * (2 * HS + 2 * HW + 1) + 31) / 32 : 1;
+    const bool do_p1 = a.smode & FT_STEREO_PHASE1;
+    const bool do_ref = a.smode & FT_STEREO_REFINE;
+
+    P2Geom g;
+    int lreg[LPL];
+    if (do_ref) {
+        g = p2_geom(a, f, kp);
+        if (FIXED && g.left_ok) {
+#pragma unroll
+            for (int q = 0; q < LPL; ++q) {
+                const int t = lane + 32 * q;
+                const int dy = t / nw, dx = t - dy * nw;
+                lreg[q] = t < nw * nw ? __ldg(g.lp + (g.yi - hw + dy) * g.wl + (g.xi - hw + dx)) : 0;
+            }
+        }
+    }
+    int cand, cdist;
+    if (do_p1) {
+        cand = phase1(a, sm, kp, lane, cdist);
+        if (lane == 0 && a.so.cand_idx) {
+            a.so.cand_idx[lk] = cand;
+            a.so.cand_dist[lk] = cdist;
+        }
+    } else {
+        cand = (int)a.so.cand_idx[lk];
+        cdist = (int)a.so.cand_dist[lk];
+    }
+    if (!(do_ref || (a.smode & FT_STEREO_FROM_CAND))) return;
+    bool ok = false;
+    double disp = 0.0, ur = 0.0;
+    int sad = 0;
+    if (cand >= 0 && cand < n_right) {
+        const double urc = do_p1 ? sm.ru[cand] : a.R.u[rbase + cand];
+        if (do_ref) {
+            if (g.left_ok) {
+                const long long xr0 = round_half_even(urc / g.s);
+                const long long hr = a.PR.heights[g.o];
+                if (!(xr0 - hs - hw < 0 || xr0 + hs + hw >= g.wr || g.yi - hw < 0 ||
+                      g.yi + hw >= hr)) {
+                    int *pl = patch, *pr = patch + nw * nw;
+                    if (FIXED) {
+                        int rreg[RPL];
+#pragma unroll
+                        for (int q = 0; q < RPL; ++q) {
+                            const int t = lane + 32 * q;
+                            const int dy = t / nr, dx = t - dy * nr;
+                            rreg[q] = t < nw * nr
+                                          ? __ldg(g.rp + (g.yi - hw + dy) * g.wr + (xr0 - hs - hw + dx))
+                                          : 0;
+                        }
+                        const int c_idx = hw * nw + hw;  // centre pixel of the left patch
+                        const int cl = __shfl_sync(FULL, lreg[c_idx / 32], c_idx % 32);
+#pragma unroll
+                        for (int q = 0; q < LPL; ++q) {
+                            const int t = lane + 32 * q;
+                            if (t < nw * nw) pl[t] = lreg[q] - cl;
+                        }
+#pragma unroll
+                        for (int q = 0; q < RPL; ++q) {
+                            const int t = lane + 32 * q;
+                            if (t < nw * nr) pr[t] = rreg[q];
+                        }
+                    } else {
+                        const int cl = __ldg(g.lp + g.yi * g.wl + g.xi);
+                        for (int t = lane; t < nw * nw; t += 32) {
+                            const int dy = t / nw, dx = t - dy * nw;
+                            pl[t] = (int)__ldg(g.lp + (g.yi - hw + dy) * g.wl + (g.xi - hw + dx)) - cl;
+                        }
+                        for (int t = lane; t < nw * nr; t += 32) {
+                            const int dy = t / nr, dx = t - dy * nr;
+                            pr[t] = __ldg(g.rp + (g.yi - hw + dy) * g.wr + (xr0 - hs - hw + dx));
+                        }
+                    }
+                    ok = p2_sweep(a, patch, kp, g, xr0, lane, disp, ur, sad);
+                }
+            }
+        } else {  // matches_from_candidates (stereo.py:154-160)
+            disp = kp.u - urc;
+            ok = !(disp < a.sp.min_disparity || disp > a.sp.max_disparity);
+            ur = urc;
+        }
+    }
+    if (lane == 0) {
+        a.so.right_idx[lk] = ok ? cand : -1;
+        a.so.distance[lk] = ok ? cdist : 10000;
+        a.so.disparity[lk] = ok ? disp : 0.0;
+        a.so.refined_u[lk] = ok ? ur : 0.0;
+        a.so.depth[lk] = ok ? a.sp.baseline_times_fx / disp : 0.0;
+        a.so.sad[lk] = ok ? sad : 0;
+    }
+}
+
 __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long long *bar,
-                             unsigned char *smem) {
+                             unsigned char *smem, unsigned long long *mbar, unsigned &mphase) {
     const int G = a.Gs;
     const int n_left = min(a.L.count[f], a.L.cap);
     const int n_right = min(a.R.count[f], a.R.cap);
@@ -292,15 +425,18 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
     const bool do_rej = a.smode & FT_STEREO_REJECT;
     const bool finalize = do_ref || do_fc;
     const int cap_r = a.R.cap;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
     StereoSmem sm;
     unsigned char *p = smem;
     sm.rd = reinterpret_cast<uint4 *>(p);
-    p += (size_t)32 * cap_r;
+    p += a.stage_rdesc ? (size_t)32 * cap_r : 0;
     sm.ru = reinterpret_cast<double *>(p);
     p += (size_t)8 * cap_r;
     sm.rv = reinterpret_cast<double *>(p);
     p += (size_t)8 * cap_r;
+    sm.ro = reinterpret_cast<int *>(p);
+    p += (size_t)4 * cap_r;
     sm.scan_tmp = reinterpret_cast<int *>(p);
     p += 32 * 4;
     sm.misc = reinterpret_cast<int *>(p);
@@ -311,28 +447,30 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
     p += (size_t)4 * H;
     sm.patch = reinterpret_cast<int *>(p);
     p += (size_t)4 * TK_WARPS * a.patch_ints;
-    sm.ro = reinterpret_cast<int *>(p);
-    p += (size_t)4 * cap_r;
     sm.items = reinterpret_cast<uint16_t *>(p);
+    sm.rdg = reinterpret_cast<const uint4 *>(a.R.desc + 4 * rbase);
 
     if (rank == 0 && threadIdx.x == 0 && a.so.n_matched) a.so.n_matched[f] = 0;
     TL_MARK(a, 0);
 
     if (k0 < k1 && (do_p1 || finalize)) {
+        const int kf = k0 + wid;
         if (do_p1) {
-            // stage the right table: coalesced, two items in flight per thread
-            const uint4 *rdg = reinterpret_cast<const uint4 *>(a.R.desc + 4 * rbase);
-            for (int j = threadIdx.x; j < n_right; j += TK_THREADS) {
-                const uint4 d0 = __ldg(rdg + 2 * j), d1 = __ldg(rdg + 2 * j + 1);
-                const double u = __ldg(a.R.u + rbase + j), v = __ldg(a.R.v + rbase + j);
-                const int o = __ldg(a.R.octave + rbase + j);
-                sm.rd[2 * j] = d0;
-                sm.rd[2 * j + 1] = d1;
-                sm.ru[j] = u;
-                sm.rv[j] = v;
-                sm.ro[j] = o;
+            // right keypoint table -> shared memory with TMA bulk copies
+            if (threadIdx.x == 0) {
+                fence_proxy_async_smem();
+                const unsigned b8 = round16(8u * n_right), b4 = round16(4u * n_right);
+                const unsigned b32 = a.stage_rdesc ? 32u * n_right : 0u;
+                mbar_arrive_expect_tx(mbar, 2 * b8 + b4 + b32);
+                if (n_right > 0) {
+                    bulk_g2s(sm.ru, a.R.u + rbase, b8, mbar);
+                    bulk_g2s(sm.rv, a.R.v + rbase, b8, mbar);
+                    bulk_g2s(sm.ro, a.R.octave + rbase, b4, mbar);
+                    if (b32) bulk_g2s(sm.rd, a.R.desc + 4 * rbase, b32, mbar);
+                }
             }
-            __syncthreads();
+            mbar_wait(mbar, mphase & 1u);  // bit 0: phase of mbar[0]
+            mphase ^= 1u;
             block_csr<TK_THREADS>(
                 n_right, H,
                 [&](int j) {
@@ -342,43 +480,12 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
                 sm.row_start, sm.row_cursor, sm.items, sm.scan_tmp);
         }
         TL_MARK(a, 1);
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         int *patch = sm.patch + wid * a.patch_ints;
-        for (int k = k0 + wid; k < k1; k += TK_WARPS) {
-            const int64_t lk = lbase + k;
-            int cand, cdist;
-            if (do_p1) {
-                cand = phase1(a, sm, lk, lane, cdist);
-                if (lane == 0 && a.so.cand_idx) {
-                    a.so.cand_idx[lk] = cand;
-                    a.so.cand_dist[lk] = cdist;
-                }
-            } else {
-                cand = (int)a.so.cand_idx[lk];
-                cdist = (int)a.so.cand_dist[lk];
-            }
-            if (!finalize) continue;
-            bool ok = false;
-            double disp = 0.0, ur = 0.0;
-            int sad = 0;
-            if (cand >= 0 && cand < n_right) {
-                const double urc = do_p1 ? sm.ru[cand] : a.R.u[rbase + cand];
-                if (do_ref) {
-                    ok = phase2(a, patch, f, lk, urc, lane, disp, ur, sad);
-                } else {  // matches_from_candidates (stereo.py:154-160)
-                    disp = a.L.u[lk] - urc;
-                    ok = !(disp < a.sp.min_disparity || disp > a.sp.max_disparity);
-                    ur = urc;
-                }
-            }
-            if (lane == 0) {
-                a.so.right_idx[lk] = ok ? cand : -1;
-                a.so.distance[lk] = ok ? cdist : 10000;
-                a.so.disparity[lk] = ok ? disp : 0.0;
-                a.so.refined_u[lk] = ok ? ur : 0.0;
-                a.so.depth[lk] = ok ? a.sp.baseline_times_fx / disp : 0.0;
-                a.so.sad[lk] = ok ? sad : 0;
-            }
+        const bool fixed55 = a.sp.half_window == 5 && a.sp.half_slide == 5;
+        for (int k = kf; k < k1; k += TK_WARPS) {
+            const LeftKp kp = load_left(a, lbase + k);
+            if (fixed55) stereo_kp<5, 5>(a, sm, patch, f, lbase + k, rbase, n_right, kp, lane);
+            else stereo_kp<0, 0>(a, sm, patch, f, lbase + k, rbase, n_right, kp, lane);
         }
     }
     __syncthreads();
@@ -389,8 +496,8 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
     int kept = 0;
     if (do_rej) {
         // every block computes the same median over the frame's accepted SADs
-        uint32_t *vals = reinterpret_cast<uint32_t *>(sm.rd);  // table no longer needed
-        int *hist = reinterpret_cast<int *>(sm.ru);
+        uint32_t *vals = reinterpret_cast<uint32_t *>(sm.ru);  // table no longer needed
+        int *hist = reinterpret_cast<int *>(sm.rv);
         if (threadIdx.x == 0) sm.misc[4] = 0;
         __syncthreads();
         for (int k = threadIdx.x; k < n_left; k += TK_THREADS) {
@@ -419,7 +526,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
                 }
                 cle = __reduce_add_sync(FULL, cle);
                 above = __reduce_min_sync(FULL, above);
-                if ((threadIdx.x & 31) == 0) {
+                if (lane == 0) {
                     atomicAdd(&sm.misc[5], cle);
                     atomicMin(&sm.misc[6], above);
                 }
@@ -449,7 +556,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
     }
     if (a.so.n_matched) {
         kept = __reduce_add_sync(FULL, kept);
-        if ((threadIdx.x & 31) == 0 && kept) atomicAdd(a.so.n_matched + f, kept);
+        if (lane == 0 && kept) atomicAdd(a.so.n_matched + f, kept);
     }
     __syncthreads();  // smem reuse by the next frame of this slot
     TL_MARK(a, 4);
@@ -460,57 +567,83 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
 
 struct QItem {
     double ucen, v, r;
-    int i;  // point index within the frame
+    int li;   // point index within the staged round
     int lvl;
-    int cx0, cx1, cy0, cy1;
+    short cx0, cx1, cy0, cy1;
 };
 
 struct MapSmem {
-    uint4 *kd;  // [2*cap_kp]
+    uint4 *kd;          // [2*cap_kp] keypoint descriptors (when staged)
+    const uint4 *kdg;   // global keypoint descriptors of the frame
     double *ku, *kv;
     int *ko;
+    long long *kslots;  // [cap_kp] slots_in (hash source)
+    int *htab;          // [1 << hash_bits] indices into kslots, -1 = empty
+    double *ppos, *pnrm, *pmin, *pmax;  // staged round of map points
+    long long *pid;
+    uint4 *pdesc;
     int *cell_start, *cell_cursor;
     uint16_t *items;
-    long long *htab;
-    QItem *queue;
-    int *res;  // [map_chunk_cap] packed claim (kp | dist << 16 | lvl << 25) or -1
+    QItem *queue;       // [round_cap]
+    int *res;           // [chunk] packed claim (kp | dist << 16 | lvl << 25) or -1
+    long long *res_pid; // [chunk] id of the claiming point
+    int *res_empty;     // [chunk] slots_in[kp] == NO_POINT
     int *scan_tmp, *misc;
-    int *hist;  // [TK_MAX_BINS]
+    int *hist;  // [TK_MAX_BINS / 32] kept-bin mask
 };
 
 FT_DEV unsigned hash_slot(long long id, int bits) {
     return (unsigned)(((unsigned long long)id * 0x9E3779B97F4A7C15ull) >> (64 - bits));
 }
 
-FT_DEV void hash_insert(long long *tab, int bits, long long id) {
+// Open-addressing set of slotted point ids: the table stores indices k into
+// kslots (4 B per entry); duplicates of an id are inserted once.
+FT_DEV void hash_insert(int *tab, int bits, const long long *kslots, int k) {
     const unsigned mask = (1u << bits) - 1u;
+    const long long id = kslots[k];
     unsigned h = hash_slot(id, bits);
     while (true) {
-        const long long prev = (long long)atomicCAS(reinterpret_cast<unsigned long long *>(tab + h),
-                                                    (unsigned long long)HASH_EMPTY,
-                                                    (unsigned long long)id);
-        if (prev == HASH_EMPTY || prev == id) return;
+        const int prev = atomicCAS(tab + h, -1, k);
+        if (prev == -1 || kslots[prev] == id) return;
         h = (h + 1) & mask;
     }
 }
 
-FT_DEV bool hash_contains(const long long *tab, int bits, long long id) {
+FT_DEV bool hash_contains(const int *tab, int bits, const long long *kslots, long long id) {
     const unsigned mask = (1u << bits) - 1u;
     unsigned h = hash_slot(id, bits);
     while (true) {
-        const long long x = tab[h];
-        if (x == id) return true;
-        if (x == HASH_EMPTY) return false;
+        const int x = tab[h];
+        if (x == -1) return false;
+        if (kslots[x] == id) return true;
         h = (h + 1) & mask;
     }
 }
 
-// kernels.py:496-551: visibility gate of one point; fills the window item.
-FT_DEV bool project_point(const TrackArgs &a, int64_t gi, double ccx, double ccy, double ccz,
-                          const double *R, const double *T, QItem &q) {
+// One map point's inputs, loaded once.
+struct PointIn {
+    double px, py, pz, nx, ny, nz, mind, maxd;
+};
+
+FT_DEV PointIn staged_point(const MapSmem &sm, int li) {
+    PointIn q;
+    q.px = sm.ppos[3 * li];
+    q.py = sm.ppos[3 * li + 1];
+    q.pz = sm.ppos[3 * li + 2];
+    q.nx = sm.pnrm[3 * li];
+    q.ny = sm.pnrm[3 * li + 1];
+    q.nz = sm.pnrm[3 * li + 2];
+    q.mind = sm.pmin[li];
+    q.maxd = sm.pmax[li];
+    return q;
+}
+
+// kernels.py:496-551: visibility gate of one point in the reference's fp64
+// evaluation order; fills the window of the candidate scan.
+FT_DEV bool project_point(const TrackArgs &a, const PointIn &pt, double ccx, double ccy,
+                          double ccz, const double *R, const double *T, QItem &q) {
     const ft_project_params &p = a.pp;
-    const double px = a.P.positions[3 * gi], py = a.P.positions[3 * gi + 1],
-                 pz = a.P.positions[3 * gi + 2];
+    const double px = pt.px, py = pt.py, pz = pt.pz;
     const double pcx = R[0] * px + R[1] * py + R[2] * pz + T[0];
     const double pcy = R[3] * px + R[4] * py + R[5] * pz + T[1];
     const double pcz = R[6] * px + R[7] * py + R[8] * pz + T[2];
@@ -534,13 +667,11 @@ FT_DEV bool project_point(const TrackArgs &a, int64_t gi, double ccx, double ccy
     }
     if (u < 0.0 || u >= p.width || v < 0.0 || v >= p.height) return false;
     const double dist = sqrt(pcx * pcx + pcy * pcy + pcz * pcz);
-    const double mind = a.P.min_dist[gi], maxd = a.P.max_dist[gi];
-    if (dist < mind || dist > maxd) return false;
+    if (dist < pt.mind || dist > pt.maxd) return false;
     const double vx = px - ccx, vy = py - ccy, vz = pz - ccz;
-    const double cosang = (vx * a.P.normals[3 * gi] + vy * a.P.normals[3 * gi + 1] +
-                           vz * a.P.normals[3 * gi + 2]) / dist;
+    const double cosang = (vx * pt.nx + vy * pt.ny + vz * pt.nz) / dist;
     if (cosang < p.view_cos_min) return false;
-    long long lvl = (long long)ceil(log(maxd / dist) * p.inv_log_scale - 1e-9);
+    long long lvl = (long long)ceil(log(pt.maxd / dist) * p.inv_log_scale - 1e-9);
     if (lvl < 0) lvl = 0;
     if (lvl > p.n_levels - 1) lvl = p.n_levels - 1;
     const double r_win = p.window_px * p.scale_pow[lvl];
@@ -559,10 +690,10 @@ FT_DEV bool project_point(const TrackArgs &a, int64_t gi, double ccx, double ccy
     q.v = v;
     q.r = r_win;
     q.lvl = (int)lvl;
-    q.cx0 = (int)cx0;
-    q.cx1 = (int)cx1;
-    q.cy0 = (int)cy0;
-    q.cy1 = (int)cy1;
+    q.cx0 = (short)cx0;
+    q.cx1 = (short)cx1;
+    q.cy0 = (short)cy0;
+    q.cy1 = (short)cy1;
     return true;
 }
 
@@ -580,13 +711,31 @@ FT_DEV int rotation_bin(const TrackArgs &a, int64_t kbase, int64_t pbase, int kp
     return (int)(b < 0 ? 0 : (b > nb - 1 ? nb - 1 : b));
 }
 
-__device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigned char *smem) {
+// Stage points [q0, q1) of the frame into the shared round buffers (TMA).
+FT_DEV void stage_points(const TrackArgs &a, const MapSmem &sm, int64_t pbase, int q0, int q1,
+                         unsigned long long *mbar) {
+    const unsigned n = (unsigned)(q1 - q0);
+    const unsigned b24 = round16(24u * n), b8 = round16(8u * n), b32 = 32u * n;
+    mbar_arrive_expect_tx(mbar, n ? 2 * b24 + 3 * b8 + b32 : 0u);
+    if (n) {
+        const int64_t g = pbase + q0;
+        bulk_g2s(sm.ppos, a.P.positions + 3 * g, b24, mbar);
+        bulk_g2s(sm.pnrm, a.P.normals + 3 * g, b24, mbar);
+        bulk_g2s(sm.pmin, a.P.min_dist + g, b8, mbar);
+        bulk_g2s(sm.pmax, a.P.max_dist + g, b8, mbar);
+        bulk_g2s(sm.pid, a.P.point_ids + g, b8, mbar);
+        bulk_g2s(sm.pdesc, a.P.desc + 4 * g, b32, mbar);
+    }
+}
+
+__device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigned char *smem,
+                          unsigned long long *mbar, unsigned &mphase) {
     const int G = a.Gm;
     const int n_pts = min(a.P.count[f], a.P.cap);
     const int n_kp = min(a.K.count[f], a.K.cap);
     const int64_t pbase = (int64_t)f * a.P.cap, kbase = (int64_t)f * a.K.cap;
-    const int chunk = (n_pts + G - 1) / G;
-    const int p0 = rank * chunk, p1 = min(n_pts, p0 + chunk);
+    const int chunk = (((n_pts + G - 1) / G) + 1) & ~1;  // even: 16-B aligned TMA sources
+    const int p0 = min(n_pts, rank * chunk), p1 = min(n_pts, p0 + chunk);
     const ft_project_params &pp = a.pp;
     const int nx = pp.grid_nx, ny = pp.grid_ny, ncell = nx * ny;
     const int cap_kp = a.K.cap;
@@ -595,78 +744,106 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     const bool use_hash = (a.pmode & FT_PROJ_SKIP_SLOTS) && a.hash_bits;
     const bool write_slots = a.pmode & FT_PROJ_WRITE_SLOTS;
     const bool ordered = resolve && a.po.corr_point;
+    const int round_cap = min(TK_THREADS, a.map_chunk_cap);
     unsigned long long *bar = a.bar_m + slot;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
     MapSmem sm;
     unsigned char *p = smem;
     sm.kd = reinterpret_cast<uint4 *>(p);
-    p += (size_t)32 * cap_kp;
+    p += a.stage_kdesc ? (size_t)32 * cap_kp : 0;
     sm.ku = reinterpret_cast<double *>(p);
     p += (size_t)8 * cap_kp;
     sm.kv = reinterpret_cast<double *>(p);
     p += (size_t)8 * cap_kp;
+    sm.kslots = reinterpret_cast<long long *>(p);
+    p += use_hash ? (size_t)8 * cap_kp : 0;
+    sm.ppos = reinterpret_cast<double *>(p);
+    p += (size_t)24 * round_cap;
+    sm.pnrm = reinterpret_cast<double *>(p);
+    p += (size_t)24 * round_cap;
+    sm.pmin = reinterpret_cast<double *>(p);
+    p += (size_t)8 * round_cap;
+    sm.pmax = reinterpret_cast<double *>(p);
+    p += (size_t)8 * round_cap;
+    sm.pid = reinterpret_cast<long long *>(p);
+    p += (size_t)8 * round_cap;
+    sm.pdesc = reinterpret_cast<uint4 *>(p);
+    p += (size_t)32 * round_cap;
+    sm.res_pid = reinterpret_cast<long long *>(p);
+    p += (size_t)8 * a.map_chunk_cap;
     sm.queue = reinterpret_cast<QItem *>(p);
-    p += sizeof(QItem) * TK_THREADS;
-    sm.htab = reinterpret_cast<long long *>(p);
-    p += a.hash_bits ? (sizeof(long long) << a.hash_bits) : 0;
+    p += sizeof(QItem) * (size_t)round_cap;
+    sm.ko = reinterpret_cast<int *>(p);
+    p += (size_t)4 * cap_kp;
+    sm.htab = reinterpret_cast<int *>(p);
+    p += a.hash_bits ? ((size_t)4 << a.hash_bits) : 0;
     sm.scan_tmp = reinterpret_cast<int *>(p);
     p += 32 * 4;
     sm.misc = reinterpret_cast<int *>(p);
     p += 16 * 4;
     sm.hist = reinterpret_cast<int *>(p);
-    p += TK_MAX_BINS * 4;
+    p += (TK_MAX_BINS / 32) * 4;
     sm.res = reinterpret_cast<int *>(p);
+    p += (size_t)4 * a.map_chunk_cap;
+    sm.res_empty = reinterpret_cast<int *>(p);
     p += (size_t)4 * a.map_chunk_cap;
     sm.cell_start = reinterpret_cast<int *>(p);
     p += (size_t)4 * (ncell + 1);
     sm.cell_cursor = reinterpret_cast<int *>(p);
     p += (size_t)4 * ncell;
-    sm.ko = reinterpret_cast<int *>(p);
-    p += (size_t)4 * cap_kp;
     sm.items = reinterpret_cast<uint16_t *>(p);
+    sm.kdg = reinterpret_cast<const uint4 *>(a.K.desc + 4 * kbase);
 
     TL_MARK(a, 0);
-    // launch epoch: the same for every block of this slot's frame instance
-    if (threadIdx.x == 0) {
-        const unsigned long long t = atomicAdd(a.ep_m + slot, 1ull);
-        sm.misc[0] = (int)(unsigned)(t / G);
+    const bool have_pts = p0 < p1;
+    // ---- every first-touch global read of the setup is one TMA batch -------
+    if (threadIdx.x == 0 && have_pts) {
+        fence_proxy_async_smem();
+        const unsigned b8 = round16(8u * n_kp), b4 = round16(4u * n_kp);
+        const unsigned b32 = a.stage_kdesc ? 32u * n_kp : 0u;
+        const unsigned bsl = use_hash ? b8 : 0u;
+        mbar_arrive_expect_tx(mbar, n_kp ? 2 * b8 + b4 + b32 + bsl : 0u);
+        if (n_kp) {
+            bulk_g2s(sm.ku, a.K.u + kbase, b8, mbar);
+            bulk_g2s(sm.kv, a.K.v + kbase, b8, mbar);
+            bulk_g2s(sm.ko, a.K.octave + kbase, b4, mbar);
+            if (b32) bulk_g2s(sm.kd, a.K.desc + 4 * kbase, b32, mbar);
+            if (bsl) bulk_g2s(sm.kslots, a.io.slots_in + kbase, bsl, mbar);
+        }
+        stage_points(a, sm, pbase, p0, min(p1, p0 + round_cap), mbar + 1);
     }
+    // launch epoch (same for every block of this slot's frame instance)
+    unsigned long long ticket = 0;
+    if (threadIdx.x == 0 && resolve) ticket = atomicAdd(a.ep_m + slot, 1ull);
     if (rank == 0 && threadIdx.x == 0) {
         if (a.po.slot_count) a.po.slot_count[f] = 0;
         if (a.po.corr_count) a.po.corr_count[f] = 0;
     }
     if (rank == 0 && rotation)
-        for (int b = threadIdx.x; b < TK_MAX_BINS; b += TK_THREADS) a.hist[(int64_t)f * TK_MAX_BINS + b] = 0;
-    __syncthreads();
-    const unsigned epoch_hi = 0xffffffffu - (unsigned)sm.misc[0];
-
-    // slots_out <- slots_in (this block's share) and its pre-filled count
+        for (int b = threadIdx.x; b < TK_MAX_BINS; b += TK_THREADS)
+            a.hist[(int64_t)f * TK_MAX_BINS + b] = 0;
     int prefilled = 0;
-    if (write_slots) {
+    if (write_slots) {  // slots_out <- slots_in (this block's share)
         const int sc = (n_kp + G - 1) / G, s0 = rank * sc, s1 = min(n_kp, s0 + sc);
         for (int k = s0 + threadIdx.x; k < s1; k += TK_THREADS) {
-            const long long v = a.io.slots_in[kbase + k];
+            const long long v = __ldg(a.io.slots_in + kbase + k);
             if (a.io.slots_out != a.io.slots_in) a.io.slots_out[kbase + k] = v;
             prefilled += v != NO_PID;
         }
     }
+    if (have_pts && use_hash)
+        for (int h = threadIdx.x; h < (1 << a.hash_bits); h += TK_THREADS) sm.htab[h] = -1;
+    if (threadIdx.x == 0) sm.misc[0] = (int)(unsigned)(ticket / (resolve ? G : 1));
+    __syncthreads();
+    const unsigned epoch_hi = 0xffffffffu - (unsigned)sm.misc[0];
 
-    if (p0 < p1) {
-        // stage the keypoint table
-        const uint4 *kdg = reinterpret_cast<const uint4 *>(a.K.desc + 4 * kbase);
-        for (int j = threadIdx.x; j < n_kp; j += TK_THREADS) {
-            const uint4 d0 = __ldg(kdg + 2 * j), d1 = __ldg(kdg + 2 * j + 1);
-            const double u = __ldg(a.K.u + kbase + j), v = __ldg(a.K.v + kbase + j);
-            const int o = __ldg(a.K.octave + kbase + j);
-            sm.kd[2 * j] = d0;
-            sm.kd[2 * j + 1] = d1;
-            sm.ku[j] = u;
-            sm.kv[j] = v;
-            sm.ko[j] = o;
-        }
+    if (have_pts) {
+        mbar_wait(mbar, mphase & 1u);  // keypoint table (+ slots) landed
+        mphase ^= 1u;
         if (use_hash)
-            for (int h = threadIdx.x; h < (1 << a.hash_bits); h += TK_THREADS) sm.htab[h] = HASH_EMPTY;
-        __syncthreads();
+            for (int k = threadIdx.x; k < n_kp; k += TK_THREADS)
+                if (sm.kslots[k] != NO_PID) hash_insert(sm.htab, a.hash_bits, sm.kslots, k);
         const double cellf = (double)pp.cell_px;
         block_csr<TK_THREADS>(
             n_kp, ncell,
@@ -677,24 +854,27 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                 return (int)(cy * nx + cx);
             },
             sm.cell_start, sm.cell_cursor, sm.items, sm.scan_tmp);
-        if (use_hash) {
-            for (int k = threadIdx.x; k < n_kp; k += TK_THREADS) {
-                const long long id = a.io.slots_in[kbase + k];
-                if (id != NO_PID) hash_insert(sm.htab, a.hash_bits, id);
-            }
-            __syncthreads();
-        }
         TL_MARK(a, 1);
         const double *R = a.io.rot + 9 * f, *T = a.io.trans + 3 * f;
         const double ccx = -(R[0] * T[0] + R[3] * T[1] + R[6] * T[2]);
         const double ccy = -(R[1] * T[0] + R[4] * T[1] + R[7] * T[2]);
         const double ccz = -(R[2] * T[0] + R[5] * T[1] + R[8] * T[2]);
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        for (int r0 = p0; r0 < p1; r0 += TK_THREADS) {
+        for (int r0 = p0; r0 < p1; r0 += round_cap) {
+            const int r1 = min(p1, r0 + round_cap);
+            if (r0 != p0) {  // later rounds (batched mode): stage this round's points
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    fence_proxy_async_smem();
+                    stage_points(a, sm, pbase, r0, r1, mbar + 1);
+                }
+            }
             if (threadIdx.x == 0) sm.misc[1] = 0;
+            mbar_wait(mbar + 1, (mphase >> 1) & 1u);  // bit 1: phase of mbar[1]
+            mphase ^= 2u;
             __syncthreads();
-            const int i = r0 + threadIdx.x;
-            if (i < p1) {
+            const int li = threadIdx.x;
+            const int i = r0 + li;
+            if (i < r1) {
                 const int64_t gi = pbase + i;
                 sm.res[i - p0] = -1;
                 if (a.po.out_kp) {
@@ -702,11 +882,10 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                     a.po.out_dist[gi] = 10000;
                     a.po.out_oct[gi] = -1;
                 }
-                bool skip = a.io.skip && a.io.skip[gi] != 0;
-                if (!skip && use_hash) skip = hash_contains(sm.htab, a.hash_bits, a.P.point_ids[gi]);
+                const bool skip = a.io.skip && a.io.skip[gi] != 0;
                 QItem q;
-                if (!skip && project_point(a, gi, ccx, ccy, ccz, R, T, q)) {
-                    q.i = i;
+                if (!skip && project_point(a, staged_point(sm, li), ccx, ccy, ccz, R, T, q)) {
+                    q.li = li;
                     sm.queue[atomicAdd(&sm.misc[1], 1)] = q;
                 }
             }
@@ -714,9 +893,12 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             TL_MARK(a, 2);
             const int nq = sm.misc[1];
             for (int qi = wid; qi < nq; qi += TK_WARPS) {  // warp per visible point
-                const QItem q = sm.queue[qi];
-                const int64_t gi = pbase + q.i;
-                const Desc pd = load_desc(a.P.desc, gi);
+                const QItem &q = sm.queue[qi];
+                const long long qpid = sm.pid[q.li];
+                if (use_hash && hash_contains(sm.htab, a.hash_bits, sm.kslots, qpid)) continue;
+                Desc pd;
+                pd.lo = sm.pdesc[2 * q.li];
+                pd.hi = sm.pdesc[2 * q.li + 1];
                 Best2 b;
                 best2_init(b);
                 for (int gy = q.cy0; gy <= q.cy1; ++gy) {
@@ -728,30 +910,39 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                         const int ko = sm.ko[j];
                         if (ko < q.lvl - 1 || ko > q.lvl + 1) continue;
                         Desc kd;
-                        kd.lo = sm.kd[2 * j];
-                        kd.hi = sm.kd[2 * j + 1];
+                        if (a.stage_kdesc) {
+                            kd.lo = sm.kd[2 * j];
+                            kd.hi = sm.kd[2 * j + 1];
+                        } else {
+                            kd.lo = __ldg(sm.kdg + 2 * j);
+                            kd.hi = __ldg(sm.kdg + 2 * j + 1);
+                        }
                         best2_push(b, hamming(pd, kd), (uint32_t)j);
                     }
                 }
                 best2_warp_reduce(b);
                 if (lane == 0 && ratio_accept(b, pp.t_proj, pp.ratio)) {
                     const int kp = (int)(b.key & 0xffffu), d = (int)(b.key >> 16);
+                    const int i = r0 + q.li;
+                    const int64_t gi = pbase + i;
                     if (a.po.out_kp) {
                         a.po.out_kp[gi] = kp;
                         a.po.out_dist[gi] = d;
                         a.po.out_oct[gi] = q.lvl;
                     }
-                    sm.res[q.i - p0] = kp | (d << 16) | (q.lvl << 25);
+                    sm.res[i - p0] = kp | (d << 16) | (q.lvl << 25);
+                    sm.res_pid[i - p0] = qpid;
+                    if (write_slots)
+                        sm.res_empty[i - p0] = __ldg(a.io.slots_in + kbase + kp) == NO_PID;
                     if (resolve)
                         atomicMin(a.claims + kbase + kp, ((unsigned long long)epoch_hi << 32) |
                                                              ((unsigned long long)d << 23) |
-                                                             (unsigned)q.i);
+                                                             (unsigned)i);
                 }
             }
             __syncthreads();
         }
     }
-    __syncthreads();
     TL_MARK(a, 3);
     if (!resolve) return;
     group_barrier(bar, G);
@@ -770,7 +961,8 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             continue;
         }
         ++n_win;
-        if (rotation) atomicAdd(a.hist + (int64_t)f * TK_MAX_BINS + rotation_bin(a, kbase, pbase, kp, i), 1);
+        if (rotation)
+            atomicAdd(a.hist + (int64_t)f * TK_MAX_BINS + rotation_bin(a, kbase, pbase, kp, i), 1);
     }
     if (rotation) {
         group_barrier(bar, G);
@@ -809,20 +1001,17 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
         int added = 0;
         for (int i = p0 + threadIdx.x; i < p1; i += TK_THREADS) {
             const int r = sm.res[i - p0];
-            if (r < 0) continue;
-            const int kp = r & 0xffff;
-            if (a.io.slots_in[kbase + kp] == NO_PID) {
-                a.io.slots_out[kbase + kp] = a.P.point_ids[pbase + i];
-                ++added;
-            }
+            if (r < 0 || !sm.res_empty[i - p0]) continue;
+            a.io.slots_out[kbase + (r & 0xffff)] = sm.res_pid[i - p0];
+            ++added;
         }
-        int tot = __reduce_add_sync(FULL, added + prefilled);
-        if ((threadIdx.x & 31) == 0 && tot && a.po.slot_count) atomicAdd(a.po.slot_count + f, tot);
+        const int tot = __reduce_add_sync(FULL, added + prefilled);
+        if (lane == 0 && tot && a.po.slot_count) atomicAdd(a.po.slot_count + f, tot);
     }
     if (!ordered) {
         if (a.po.corr_count) {
-            int tot = __reduce_add_sync(FULL, n_win);
-            if ((threadIdx.x & 31) == 0 && tot) atomicAdd(a.po.corr_count + f, tot);
+            const int tot = __reduce_add_sync(FULL, n_win);
+            if (lane == 0 && tot) atomicAdd(a.po.corr_count + f, tot);
         }
         __syncthreads();
         TL_MARK(a, 5);
@@ -830,10 +1019,10 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     }
     // ordered correspondences: block counts -> prefix over ranks -> write
     {
-        int tot = __reduce_add_sync(FULL, n_win);
+        const int tot = __reduce_add_sync(FULL, n_win);
         if (threadIdx.x == 0) sm.misc[2] = 0;
         __syncthreads();
-        if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&sm.misc[2], tot);
+        if (lane == 0 && tot) atomicAdd(&sm.misc[2], tot);
         __syncthreads();
         if (threadIdx.x == 0) a.blk_counts[(int64_t)f * G + rank] = sm.misc[2];
     }
@@ -851,7 +1040,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
         sm.misc[4] = 0;
     }
     __syncthreads();
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         atomicAdd(&sm.misc[3], before);
         atomicAdd(&sm.misc[4], all);
     }
@@ -877,12 +1066,22 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
 }
 
 __global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem_all[];
+    // two mbarriers (table / point rounds) ahead of the role's buffers
+    unsigned long long *mbar = reinterpret_cast<unsigned long long *>(smem_all);
+    unsigned char *smem = smem_all + 16;
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        mbar_init(mbar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned mphase = 0;
     const int per = a.Gs + a.Gm;
     const int slot = blockIdx.x / per, r = blockIdx.x - slot * per;
     for (int f = slot; f < a.F; f += a.W) {
-        if (r < a.Gs) stereo_frame(a, f, r, a.bar_s + slot, smem);
-        else map_frame(a, f, r - a.Gs, slot, smem);
+        if (r < a.Gs) stereo_frame(a, f, r, a.bar_s + slot, smem, mbar, mphase);
+        else map_frame(a, f, r - a.Gs, slot, smem, mbar, mphase);
     }
 }
 
@@ -891,17 +1090,21 @@ __global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
 
 size_t stereo_smem(const TrackArgs &a) {
     const int cap = a.R.cap, H = a.sp.height;
-    size_t b = (size_t)52 * cap + 4 * (32 + 16) + 4 * (size_t)(2 * H + 1) +
-               4 * (size_t)TK_WARPS * a.patch_ints + 2 * (size_t)cap + 64;
-    const size_t med = (size_t)4 * a.L.cap + 4 * 256;  // vals + hist (reuse table region)
+    size_t b = 16 + (a.stage_rdesc ? (size_t)32 * cap : 0) + (size_t)20 * cap + 4 * (32 + 16) +
+               4 * (size_t)(2 * H + 1) + 4 * (size_t)TK_WARPS * a.patch_ints + 2 * (size_t)cap + 64;
+    const size_t med = 16 + (size_t)16 * cap + 4 * 256;  // median scratch reuses ru / rv
     return b > med ? b : med;
 }
 
 size_t map_smem(const TrackArgs &a) {
     const int cap = a.K.cap, ncell = a.pp.grid_nx * a.pp.grid_ny;
-    return (size_t)52 * cap + sizeof(QItem) * TK_THREADS +
-           (a.hash_bits ? (sizeof(long long) << a.hash_bits) : 0) + 4 * (32 + 16 + TK_MAX_BINS) +
-           4 * (size_t)a.map_chunk_cap + 4 * (size_t)(2 * ncell + 1) + 2 * (size_t)cap + 64;
+    const int round_cap = a.map_chunk_cap < TK_THREADS ? a.map_chunk_cap : TK_THREADS;
+    const bool hash = a.hash_bits > 0;
+    return 16 + (a.stage_kdesc ? (size_t)32 * cap : 0) + (size_t)20 * cap +
+           (hash ? (size_t)8 * cap : 0) + (size_t)104 * round_cap +
+           sizeof(QItem) * (size_t)round_cap + (hash ? ((size_t)4 << a.hash_bits) : 0) +
+           4 * (32 + 16 + TK_MAX_BINS / 32) + 16 * (size_t)a.map_chunk_cap +
+           4 * (size_t)(2 * ncell + 1) + 2 * (size_t)cap + 64;
 }
 
 }  // namespace ft
@@ -916,7 +1119,7 @@ struct GeomKey {
     bool operator==(const GeomKey &o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
 };
 struct Geom {
-    int Gs, Gm, W, chunk;
+    int Gs, Gm, W, chunk, stage_rdesc, stage_kdesc;
     size_t smem;
 };
 constexpr int GEOM_CACHE = 8;
@@ -978,6 +1181,8 @@ static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_
     a.Gm = g.Gm;
     a.W = g.W;
     a.map_chunk_cap = g.chunk;
+    a.stage_rdesc = g.stage_rdesc;
+    a.stage_kdesc = g.stage_kdesc;
     {
         const int st = raise_smem_attr(dev, g.smem);
         if (st != FT_OK) return st;
@@ -1055,8 +1260,15 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
     if (gm_ideal > 64) gm_ideal = 64;
     int Gs = gs_ideal, Gm = gm_ideal, W = F;
     size_t smem = 0;
+    a.stage_rdesc = 1;
+    a.stage_kdesc = 1;
     for (int iter = 0; iter < 4; ++iter) {
-        if (want_map) a.map_chunk_cap = (a.P.cap + Gm - 1) / Gm;
+        if (want_map) a.map_chunk_cap = (((a.P.cap + Gm - 1) / Gm) + 1) & ~1;
+        // descriptors stay in L2 when the staged tables would not fit
+        a.stage_rdesc = 1;
+        a.stage_kdesc = 1;
+        if (want_stereo && stereo_smem(a) > 227 * 1024) a.stage_rdesc = 0;
+        if (want_map && map_smem(a) > 227 * 1024) a.stage_kdesc = 0;
         smem = want_stereo ? stereo_smem(a) : 0;
         if (want_map) {
             const size_t m = map_smem(a);
@@ -1098,7 +1310,11 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
         W = nW;
         if (same && iter > 0) break;
     }
-    if (want_map) a.map_chunk_cap = (a.P.cap + Gm - 1) / Gm;
+    if (want_map) a.map_chunk_cap = (((a.P.cap + Gm - 1) / Gm) + 1) & ~1;
+    a.stage_rdesc = 1;
+    a.stage_kdesc = 1;
+    if (want_stereo && stereo_smem(a) > 227 * 1024) a.stage_rdesc = 0;
+    if (want_map && map_smem(a) > 227 * 1024) a.stage_kdesc = 0;
     smem = want_stereo ? stereo_smem(a) : 0;
     if (want_map) {
         const size_t m = map_smem(a);
@@ -1114,9 +1330,13 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
     out.Gm = Gm;
     out.W = W;
     out.chunk = want_map ? a.map_chunk_cap : 0;
+    out.stage_rdesc = a.stage_rdesc;
+    out.stage_kdesc = a.stage_kdesc;
     out.smem = smem;
     return FT_OK;
 }
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
 static bool fill_stereo(TrackArgs &a, int32_t n_frames, const ft_keypoints *left,
                         const ft_keypoints *right, const ft_pyramid *left_pyr,
@@ -1151,6 +1371,13 @@ static bool fill_stereo(TrackArgs &a, int32_t n_frames, const ft_keypoints *left
     }
     if ((mode & FT_STEREO_REFINE) &&
         (left_pyr->n_levels < params->n_levels || right_pyr->n_levels < params->n_levels)) {
+        *status = FT_E_RANGE;
+        return false;
+    }
+    // TMA staging: per-frame arrays start 16-B aligned (caps multiple of 4)
+    if ((left->cap & 3) || (right->cap & 3) || !aligned16(left->u) || !aligned16(left->v) ||
+        !aligned16(left->octave) || !aligned16(left->desc) || !aligned16(right->u) ||
+        !aligned16(right->v) || !aligned16(right->octave) || !aligned16(right->desc)) {
         *status = FT_E_RANGE;
         return false;
     }
@@ -1195,6 +1422,15 @@ static bool fill_map(TrackArgs &a, int32_t n_frames, const ft_map_points *points
         (out->out_kp && (!out->out_dist || !out->out_oct)) ||
         (out->corr_point && (!out->corr_kp || !out->corr_dist || !out->corr_oct))) {
         *status = FT_E_NULL;
+        return false;
+    }
+    if ((points->cap & 3) || (frame->cap & 3) || !aligned16(points->positions) ||
+        !aligned16(points->normals) || !aligned16(points->min_dist) ||
+        !aligned16(points->max_dist) || !aligned16(points->desc) ||
+        !aligned16(points->point_ids) || !aligned16(frame->u) || !aligned16(frame->v) ||
+        !aligned16(frame->octave) || !aligned16(frame->desc) ||
+        ((mode & FT_PROJ_SKIP_SLOTS) && !aligned16(io->slots_in))) {
+        *status = FT_E_RANGE;
         return false;
     }
     a.pmode = mode;

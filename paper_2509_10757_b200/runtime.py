@@ -107,13 +107,13 @@ class Runtime:
         self.stream.synchronize()
 
     def caps(self, n_kp: int, n_pts: int = 0) -> tuple[int, int]:
-        """High-water capacities (powers of two >= 1024) for single-frame
-        calls; every launch of this runtime uses them so the workspace layout
-        never changes between calls."""
-        while self.cap_kp < n_kp:
-            self.cap_kp *= 2
-        while self.cap_pts < n_pts:
-            self.cap_pts *= 2
+        """High-water capacities (multiples of 256 keypoints / 1024 points,
+        >= 1024) for single-frame calls; every launch of this runtime uses
+        them so the workspace layout only changes when they grow."""
+        if n_kp > self.cap_kp:
+            self.cap_kp = (n_kp + 255) // 256 * 256
+        if n_pts > self.cap_pts:
+            self.cap_pts = (n_pts + 1023) // 1024 * 1024
         return self.cap_kp, self.cap_pts
 
     def workspace(self) -> _lib.FtWorkspace:
