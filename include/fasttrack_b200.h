@@ -17,13 +17,14 @@
  * of each array; the per-frame counts n_f are read from DEVICE memory, so a
  * CUDA graph captured once replays every frame with new counts.
  *
- * Descriptors are 256-bit ORB strings, 32 bytes per row, bit b in 64-bit word
- * b >> 6 at bit b & 63 (reference descriptors.py:7-9,23-30); the kernels read
- * them as 8 x u32 with two 16-byte vector loads.
+ * Inputs are packed records (ft_kp_record, ft_point_record): a frame's table
+ * is staged into shared memory with ONE TMA bulk copy.  ft_pack_keypoints /
+ * ft_pack_points build them from the reference's SoA arrays (FeatureSet /
+ * MapPointSoA) on the device.  Descriptors are 256-bit ORB strings, bit b in
+ * 64-bit word b >> 6 at bit b & 63 (reference descriptors.py:7-9,23-30).
  *
- * Alignment: per-frame tables are staged into shared memory with TMA bulk
- * copies, so every array base must be 16-byte aligned and every capacity a
- * multiple of 4 (FT_E_RANGE otherwise).
+ * Alignment: record arrays must be 16-byte aligned and capacities even
+ * (FT_E_RANGE otherwise).
  *
  * Reference interface each entry replaces:
  *   ft_hamming_pairs        kernels.py:48-51        hamming_pairs_kernel
@@ -74,17 +75,22 @@ typedef struct {
     int32_t cap_points;  /* max map points per frame */
 } ft_workspace;
 
-/* Keypoints of one image side, F frames at stride `cap`
- * (reference mapping.py:18-65 FeatureSet). */
+/* One keypoint, packed (64 B) so a frame's table is one contiguous TMA copy.
+ * Fields are the reference FeatureSet's (mapping.py:18-65). */
 typedef struct {
-    const double *u;        /* [F*cap] level-0 column */
-    const double *v;        /* [F*cap] level-0 row */
-    const int32_t *octave;  /* [F*cap] pyramid level */
-    const double *angle;    /* [F*cap] orientation (rad); may be NULL unless
-                               the rotation check runs */
-    const uint64_t *desc;   /* [F*cap][4] */
-    const int32_t *count;   /* DEVICE [F] keypoints per frame */
-    int32_t cap;            /* per-frame stride (>= every count) */
+    double u;            /* level-0 column */
+    double v;            /* level-0 row */
+    uint64_t desc[4];    /* 256-bit descriptor (descriptors.py:23-30 bit order) */
+    double angle;        /* orientation (rad), rotation check only */
+    int32_t octave;      /* pyramid level */
+    int32_t pad;
+} ft_kp_record;
+
+/* Keypoints of one image side, F frames at stride `cap` records. */
+typedef struct {
+    const ft_kp_record *rec;  /* [F*cap] */
+    const int32_t *count;     /* DEVICE [F] keypoints per frame */
+    int32_t cap;              /* per-frame stride (>= every count) */
 } ft_keypoints;
 
 /* Flat u8 image pyramid, F frames at stride `frame_bytes`
@@ -135,16 +141,21 @@ typedef struct {
     int32_t *n_matched;  /* DEVICE [F] matches after rejection; may be NULL */
 } ft_stereo_out;
 
-/* Map points of F local maps at stride `cap`
- * (reference mapping.py:163-201 MapPointSoA). */
+/* One map point, packed (112 B) (reference mapping.py:163-201 MapPointSoA). */
 typedef struct {
-    const double *positions;  /* [F*cap][3] */
-    const double *normals;    /* [F*cap][3] */
-    const double *min_dist;   /* [F*cap] */
-    const double *max_dist;   /* [F*cap] */
-    const uint64_t *desc;     /* [F*cap][4] */
-    const int64_t *point_ids; /* [F*cap], ascending per frame (LocalMap contract) */
-    const int32_t *count;     /* DEVICE [F] */
+    uint64_t desc[4];    /* representative descriptor */
+    double pos[3];       /* world position */
+    double nrm[3];       /* mean viewing direction */
+    double min_dist;
+    double max_dist;
+    int64_t id;          /* point id; ascending per frame (LocalMap contract) */
+    int64_t pad;
+} ft_point_record;
+
+/* Map points of F local maps at stride `cap` records. */
+typedef struct {
+    const ft_point_record *rec;  /* [F*cap] */
+    const int32_t *count;        /* DEVICE [F] */
     int32_t cap;
 } ft_map_points;
 
@@ -207,6 +218,17 @@ size_t ft_workspace_bytes(int32_t n_frames, int32_t cap_left, int32_t cap_points
 /* Initialise a workspace once after allocation (counters to 0, claims to
  * ~0); every kernel restores that state on exit. */
 int ft_workspace_init(const ft_workspace *ws, ft_stream_t stream);
+
+/* SoA -> packed records for F frames (any pointer but u/v/octave/desc/ids may
+ * be NULL: angle -> 0).  Caller-held reference-layout device arrays at
+ * stride cap per frame. */
+int ft_pack_keypoints(int32_t n_frames, const double *u, const double *v, const int32_t *octave,
+                      const double *angle, const uint64_t *desc, const int32_t *count,
+                      int32_t cap, ft_kp_record *out, ft_stream_t stream);
+int ft_pack_points(int32_t n_frames, const double *positions, const double *normals,
+                   const double *min_dist, const double *max_dist, const uint64_t *desc,
+                   const int64_t *point_ids, const int32_t *count, int32_t cap,
+                   ft_point_record *out, ft_stream_t stream);
 
 /* kernels.py:48-51: out[i] = popcount(a[i] ^ b[i]) over 256 bits. */
 int ft_hamming_pairs(const uint64_t *a, const uint64_t *b, int64_t n, int64_t *out,

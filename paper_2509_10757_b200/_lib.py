@@ -36,8 +36,7 @@ class FtWorkspace(ctypes.Structure):
 
 
 class FtKeypoints(ctypes.Structure):
-    _fields_ = [("u", vp), ("v", vp), ("octave", vp), ("angle", vp), ("desc", vp),
-                ("count", vp), ("cap", i32)]
+    _fields_ = [("rec", vp), ("count", vp), ("cap", i32)]
 
 
 class FtPyramid(ctypes.Structure):
@@ -60,8 +59,18 @@ class FtStereoOut(ctypes.Structure):
 
 
 class FtMapPoints(ctypes.Structure):
-    _fields_ = [("positions", vp), ("normals", vp), ("min_dist", vp), ("max_dist", vp),
-                ("desc", vp), ("point_ids", vp), ("count", vp), ("cap", i32)]
+    _fields_ = [("rec", vp), ("count", vp), ("cap", i32)]
+
+
+# numpy views of the packed records (include/fasttrack_b200.h)
+import numpy as _np  # noqa: E402
+
+KP_RECORD = _np.dtype([("u", "<f8"), ("v", "<f8"), ("desc", "<u8", (4,)), ("angle", "<f8"),
+                       ("octave", "<i4"), ("pad", "<i4")])
+POINT_RECORD = _np.dtype([("desc", "<u8", (4,)), ("pos", "<f8", (3,)), ("nrm", "<f8", (3,)),
+                          ("min_dist", "<f8"), ("max_dist", "<f8"), ("id", "<i8"),
+                          ("pad", "<i8")])
+assert KP_RECORD.itemsize == 64 and POINT_RECORD.itemsize == 112
 
 
 class FtProjectParams(ctypes.Structure):
@@ -92,7 +101,8 @@ _lib = None
 
 EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_workspace_init",
            "ft_hamming_pairs", "ft_stereo_pinhole", "ft_stereo_fisheye_bf", "ft_project_search",
-           "ft_track_frames", "ft_resolve_conflicts", "ft_rotation_filter", "ft_bench_popc")
+           "ft_track_frames", "ft_resolve_conflicts", "ft_rotation_filter", "ft_bench_popc",
+           "ft_pack_keypoints", "ft_pack_points")
 
 
 def build(force: bool = False) -> Path:
@@ -133,6 +143,8 @@ def load() -> ctypes.CDLL:
     L.ft_resolve_conflicts.argtypes = [i32, vp, vp, vp, i32, P(FtProjectOut), W, vp]
     L.ft_rotation_filter.argtypes = [i32, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp]
     L.ft_bench_popc.argtypes = [i32, i32, i32, vp, vp]
+    L.ft_pack_keypoints.argtypes = [i32, vp, vp, vp, vp, vp, vp, i32, vp, vp]
+    L.ft_pack_points.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp]
     _lib = L
     return L
 

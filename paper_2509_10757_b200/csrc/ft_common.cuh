@@ -125,34 +125,45 @@ __device__ int block_exclusive_scan(int v, int *tmp, int &total) {
 }
 
 // Counting-sort CSR of n items over nbins bins, built by one block in shared
-// memory: start[nbins + 1], cursor[nbins], items[n].  bin_of(j) must be
-// deterministic.  Order inside a bin is arbitrary (atomics); every consumer
-// in this library reduces order-independently.
+// memory: start[nbins + 1], cursor[nbins], items[n], binbuf[n] (bin cache).
+// `cursor` must be zeroed and a __syncthreads() passed before the call
+// (callers fold that into an earlier barrier).  Three block barriers: after
+// counting, after the single-warp scan, after the scatter.  Order inside a
+// bin is arbitrary (atomics); every consumer reduces order-independently.
 template <int NT, typename BinFn>
 __device__ void block_csr(int n, int nbins, BinFn bin_of, int *start, int *cursor,
-                          uint16_t *items, int *scan_tmp) {
-    for (int b = threadIdx.x; b < nbins; b += NT) cursor[b] = 0;
+                          uint16_t *items, uint16_t *binbuf) {
+    for (int j = threadIdx.x; j < n; j += NT) {
+        const int b = bin_of(j);
+        binbuf[j] = (uint16_t)b;
+        atomicAdd(&cursor[b], 1);
+    }
     __syncthreads();
-    for (int j = threadIdx.x; j < n; j += NT) atomicAdd(&cursor[bin_of(j)], 1);
-    __syncthreads();
-    const int per = (nbins + NT - 1) / NT;
-    const int b0 = threadIdx.x * per;
-    int local = 0;
-    for (int i = 0; i < per; ++i)
-        if (b0 + i < nbins) local += cursor[b0 + i];
-    int total;
-    int run = block_exclusive_scan<NT>(local, scan_tmp, total);
-    for (int i = 0; i < per; ++i)
-        if (b0 + i < nbins) {
-            const int c = cursor[b0 + i];
-            start[b0 + i] = run;
-            cursor[b0 + i] = run;
-            run += c;
+    if (threadIdx.x < 32) {  // one warp scans the bin counts
+        const int lane = threadIdx.x;
+        const int per = (nbins + 31) / 32, b0 = lane * per;
+        int local = 0;
+        for (int i = 0; i < per; ++i)
+            if (b0 + i < nbins) local += cursor[b0 + i];
+        int incl = local;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, s);
+            if (lane >= s) incl += y;
         }
-    if (threadIdx.x == 0) start[nbins] = total;
+        int run = incl - local;
+        for (int i = 0; i < per; ++i)
+            if (b0 + i < nbins) {
+                const int c = cursor[b0 + i];
+                start[b0 + i] = run;
+                cursor[b0 + i] = run;
+                run += c;
+            }
+        if (lane == 31) start[nbins] = incl;
+    }
     __syncthreads();
     for (int j = threadIdx.x; j < n; j += NT) {
-        const int pos = atomicAdd(&cursor[bin_of(j)], 1);
+        const int pos = atomicAdd(&cursor[binbuf[j]], 1);
         items[pos] = (uint16_t)j;
     }
     __syncthreads();

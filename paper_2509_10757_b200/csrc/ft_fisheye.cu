@@ -50,14 +50,15 @@ __global__ void __launch_bounds__(BF_TL) fisheye_bf_kernel(const BfArgs a) {
     best2_init(b);
     if (tile_live && j0 < j1) {
         Desc ld;
-        if (k < n_left) ld = load_desc(a.L.desc, lbase + k);
+        if (k < n_left) ld = load_desc(a.L.rec[lbase + k].desc, 0);
         else ld = Desc{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
         for (int c0 = j0; c0 < j1; c0 += BF_CHUNK) {
             const int cn = min(BF_CHUNK, j1 - c0);
             __syncthreads();
-            const uint4 *src = reinterpret_cast<const uint4 *>(a.R.desc + 4 * (rbase + c0));
+            // descriptor = 2nd and 3rd uint4 of each 64-B record
+            const uint4 *src = reinterpret_cast<const uint4 *>(a.R.rec + rbase + c0);
             for (int t = threadIdx.x; t < 2 * cn; t += BF_TL)
-                (&rdesc[0][0])[t] = __ldg(src + t);
+                (&rdesc[0][0])[t] = __ldg(src + 4 * (t >> 1) + 1 + (t & 1));
             __syncthreads();
 #pragma unroll 4
             for (int jj = 0; jj < cn; ++jj) {
@@ -98,7 +99,8 @@ extern "C" int ft_stereo_fisheye_bf(int32_t n_frames, const ft_keypoints *left,
                                     const ft_keypoints *right, int32_t t_match, double ratio,
                                     int64_t *out_idx, int64_t *out_dist, const ft_workspace *ws,
                                     ft_stream_t stream) {
-    if (!left || !right || !out_idx || !out_dist || !ws) return FT_E_NULL;
+    if (!left || !right || !out_idx || !out_dist || !ws || !left->rec || !right->rec)
+        return FT_E_NULL;
     if (n_frames < 1 || left->cap < 1 || right->cap < 1 || left->cap > 65535 ||
         right->cap > 65535)
         return FT_E_RANGE;

@@ -186,3 +186,80 @@ extern "C" int ft_rotation_filter(int32_t m, int64_t *corr_point, int64_t *corr_
         histogram_keep, count);
     return (int)cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// SoA (reference FeatureSet / MapPointSoA layout) -> packed records.
+
+namespace ft {
+
+__global__ void pack_kp_kernel(int F, const double *u, const double *v, const int32_t *octave,
+                               const double *angle, const uint64_t *desc, const int32_t *count,
+                               int cap, ft_kp_record *out) {
+    const int64_t total = (int64_t)F * cap;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int f = (int)(g / cap), i = (int)(g - (int64_t)f * cap);
+        if (i >= count[f]) continue;
+        ft_kp_record r;
+        r.u = u[g];
+        r.v = v[g];
+        for (int w = 0; w < 4; ++w) r.desc[w] = desc[4 * g + w];
+        r.angle = angle ? angle[g] : 0.0;
+        r.octave = octave[g];
+        r.pad = 0;
+        out[g] = r;
+    }
+}
+
+__global__ void pack_pt_kernel(int F, const double *pos, const double *nrm, const double *mind,
+                               const double *maxd, const uint64_t *desc, const int64_t *ids,
+                               const int32_t *count, int cap, ft_point_record *out) {
+    const int64_t total = (int64_t)F * cap;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int f = (int)(g / cap), i = (int)(g - (int64_t)f * cap);
+        if (i >= count[f]) continue;
+        ft_point_record r;
+        for (int w = 0; w < 4; ++w) r.desc[w] = desc[4 * g + w];
+        for (int c = 0; c < 3; ++c) {
+            r.pos[c] = pos[3 * g + c];
+            r.nrm[c] = nrm[3 * g + c];
+        }
+        r.min_dist = mind[g];
+        r.max_dist = maxd[g];
+        r.id = ids[g];
+        r.pad = 0;
+        out[g] = r;
+    }
+}
+
+}  // namespace ft
+
+extern "C" int ft_pack_keypoints(int32_t n_frames, const double *u, const double *v,
+                                 const int32_t *octave, const double *angle,
+                                 const uint64_t *desc, const int32_t *count, int32_t cap,
+                                 ft_kp_record *out, ft_stream_t stream) {
+    if (!u || !v || !octave || !desc || !count || !out) return FT_E_NULL;
+    if (n_frames < 1 || cap < 1) return FT_E_RANGE;
+    const int64_t total = (int64_t)n_frames * cap;
+    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    pack_kp_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_frames, u, v, octave, angle, desc,
+                                                             count, cap, out);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int ft_pack_points(int32_t n_frames, const double *positions, const double *normals,
+                              const double *min_dist, const double *max_dist,
+                              const uint64_t *desc, const int64_t *point_ids,
+                              const int32_t *count, int32_t cap, ft_point_record *out,
+                              ft_stream_t stream) {
+    if (!positions || !normals || !min_dist || !max_dist || !desc || !point_ids || !count || !out)
+        return FT_E_NULL;
+    if (n_frames < 1 || cap < 1) return FT_E_RANGE;
+    const int64_t total = (int64_t)n_frames * cap;
+    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    pack_pt_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_frames, positions, normals,
+                                                             min_dist, max_dist, desc, point_ids,
+                                                             count, cap, out);
+    return (int)cudaGetLastError();
+}

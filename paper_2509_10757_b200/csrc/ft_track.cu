@@ -83,7 +83,7 @@ struct TrackArgs {
     unsigned long long *tl;      // optional timeline [grid][TL_SLOTS] (FT_DEBUG_TIMELINE)
 };
 
-constexpr int TL_SLOTS = 8;
+constexpr int TL_SLOTS = 16;
 
 FT_DEV unsigned long long global_ns() {
     unsigned long long t;
@@ -100,6 +100,11 @@ FT_DEV unsigned long long global_ns() {
 // ---------------------------------------------------------------------------
 // group barrier among the G blocks of one role in one slot.  The counter only
 // grows; the generation is the arrival ticket / G, so no reset is needed.
+
+// Warm the TLB / L2 for a page the block will touch later (no data use).
+FT_DEV void prefetch_l2(const void *p) {
+    if (p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 FT_DEV unsigned long long ld_acquire_u64(const unsigned long long *p) {
     unsigned long long v;
@@ -120,60 +125,109 @@ __device__ void group_barrier(unsigned long long *ctr, int G) {
 }
 
 // ---------------------------------------------------------------------------
-// k-th smallest (0-based) of vals[0..n) by 8-bit radix select, skipping the
-// all-zero high digits (SAD values are < 2^16 for the default 11x11 window).
+// np.median of the accepted SADs (stereo.py:180): the values of ranks
+// (n-1)/2 and n/2 found together by an 8-bit radix select from the top
+// non-zero digit.  vals[k] holds the SAD of left keypoint k or 0xffffffff
+// when unmatched (skipped).  Per digit: two shared histograms (one per
+// rank), warp 0 / warp 1 locate the digits, 2 block barriers.
 
-__device__ uint32_t block_select(const uint32_t *vals, int n, int k, int *hist, int *scan_tmp,
-                                 int *misc) {
-    uint32_t mx = 0;
-    for (int i = threadIdx.x; i < n; i += TK_THREADS) mx = max(mx, vals[i]);
-    mx = __reduce_max_sync(FULL, mx);
-    if (threadIdx.x == 0) misc[0] = 0;
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned *>(misc), mx);
-    __syncthreads();
-    mx = (uint32_t)misc[0];
+// Warp-level search of a 256-bin histogram for the bin holding rank k.
+FT_DEV void warp_find_rank(const int *hist, int k, int *out_digit, int *out_k) {
+    const int lane = threadIdx.x & 31;
+    int c[8], loc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        c[i] = hist[lane * 8 + i];
+        loc += c[i];
+    }
+    int incl = loc;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, s);
+        if (lane >= s) incl += y;
+    }
+    int run = incl - loc;
+    if (k >= run && k < incl) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (k < run + c[i]) {
+                *out_digit = lane * 8 + i;
+                *out_k = k - run;
+                break;
+            }
+            run += c[i];
+        }
+    }
+}
+
+__device__ void block_median_pair(const uint32_t *vals, int n, int nm, uint32_t vmax, int *hist,
+                                  int *misc, uint32_t &v_lo, uint32_t &v_hi) {
+    int k_lo = (nm - 1) / 2, k_hi = nm / 2;
     int top = 24;
-    while (top > 0 && (mx >> top) == 0) top -= 8;
-    uint32_t prefix = 0, mask = 0;
+    while (top > 0 && (vmax >> top) == 0) top -= 8;
+    uint32_t pre_lo = 0, pre_hi = 0, mask = 0;
+    int *h_lo = hist, *h_hi = hist + 256;
     for (int sh = top; sh >= 0; sh -= 8) {
-        if (threadIdx.x < 256) hist[threadIdx.x] = 0;
+        if (threadIdx.x < 256) {
+            h_lo[threadIdx.x] = 0;
+            h_hi[threadIdx.x] = 0;
+        }
         __syncthreads();
         for (int i = threadIdx.x; i < n; i += TK_THREADS) {
             const uint32_t x = vals[i];
-            if ((x & mask) == prefix) atomicAdd(&hist[(x >> sh) & 0xffu], 1);
+            if (x == 0xffffffffu) continue;
+            const int d = (x >> sh) & 0xffu;
+            if ((x & mask) == pre_lo) atomicAdd(&h_lo[d], 1);
+            if ((x & mask) == pre_hi) atomicAdd(&h_hi[d], 1);
         }
         __syncthreads();
-        const int c = threadIdx.x < 256 ? hist[threadIdx.x] : 0;
-        int total;
-        const int run = block_exclusive_scan<TK_THREADS>(c, scan_tmp, total);
-        if (threadIdx.x < 256 && k >= run && k < run + c) {
-            misc[1] = threadIdx.x;
-            misc[2] = k - run;
-        }
+        const int wid = threadIdx.x >> 5;
+        if (wid == 0) warp_find_rank(h_lo, k_lo, &misc[8], &misc[9]);
+        if (wid == 1) warp_find_rank(h_hi, k_hi, &misc[10], &misc[11]);
         __syncthreads();
-        prefix |= (uint32_t)misc[1] << sh;
+        pre_lo |= (uint32_t)misc[8] << sh;
+        pre_hi |= (uint32_t)misc[10] << sh;
+        k_lo = misc[9];
+        k_hi = misc[11];
         mask |= 0xffu << sh;
-        k = misc[2];
-        __syncthreads();
     }
-    return prefix;
+    v_lo = pre_lo;
+    v_hi = pre_hi;
+}
+
+// ---------------------------------------------------------------------------
+// packed records (include/fasttrack_b200.h)
+
+FT_DEV Desc rec_desc(const ft_kp_record &r) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(r.desc);
+    Desc d;
+    d.lo = p[0];
+    d.hi = p[1];
+    return d;
+}
+
+FT_DEV Desc rec_desc(const ft_point_record &r) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(r.desc);
+    Desc d;
+    d.lo = p[0];
+    d.hi = p[1];
+    return d;
 }
 
 // ---------------------------------------------------------------------------
 // stereo role
 
 struct StereoSmem {
-    double *ru, *rv;
-    uint4 *rd;        // [2*cap] (when staged)
-    const uint4 *rdg; // global right descriptors of the frame
-    int *ro;
+    const ft_kp_record *rtab;  // right table: shared copy (staged) or global
+    ft_kp_record *rtab_s;      // shared table region (also the median scratch)
     int *row_start;   // [H+1]
     int *row_cursor;  // [H]
     uint16_t *items;  // [cap]
+    uint16_t *binbuf; // [cap]
     int *patch;       // [TK_WARPS][patch_ints]
     int *scan_tmp;    // [32]
     int *misc;        // [16]
+    int *hist;        // [512] median digit histograms
 };
 
 // One warp's left keypoint, loaded once (every lane issues the same
@@ -186,10 +240,17 @@ struct LeftKp {
 
 FT_DEV LeftKp load_left(const TrackArgs &a, int64_t lk) {
     LeftKp k;
-    k.u = __ldg(a.L.u + lk);
-    k.v = __ldg(a.L.v + lk);
-    k.o = __ldg(a.L.octave + lk);
-    k.d = load_desc(a.L.desc, lk);
+    // volatile: issued where written (the prefetch before the TMA wait must
+    // not be sunk to the first use by the compiler)
+    const ft_kp_record *r = a.L.rec + lk;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(k.u), "=d"(k.v) : "l"(r));
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(k.d.lo.x), "=r"(k.d.lo.y), "=r"(k.d.lo.z), "=r"(k.d.lo.w)
+                 : "l"(r->desc));
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(k.d.hi.x), "=r"(k.d.hi.y), "=r"(k.d.hi.z), "=r"(k.d.hi.w)
+                 : "l"(r->desc + 2));
+    asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(k.o) : "l"(&r->octave));
     return k;
 }
 
@@ -208,20 +269,13 @@ FT_DEV int phase1(const TrackArgs &a, const StereoSmem &sm, const LeftKp &kp, in
         const int beg = sm.row_start[r0], end = sm.row_start[r1 + 1];
         for (int ii = beg + lane; ii < end; ii += 32) {
             const int j = sm.items[ii];
-            const int ro = sm.ro[j];
+            const ft_kp_record &rr = sm.rtab[j];
+            const int ro = rr.octave;
             if (ro < kp.o - 1 || ro > kp.o + 1) continue;
-            if (fabs(sm.rv[j] - kp.v) > band) continue;
-            const double disp = kp.u - sm.ru[j];
+            if (fabs(rr.v - kp.v) > band) continue;
+            const double disp = kp.u - rr.u;
             if (disp < a.sp.min_disparity || disp > a.sp.max_disparity) continue;
-            Desc rd;
-            if (a.stage_rdesc) {
-                rd.lo = sm.rd[2 * j];
-                rd.hi = sm.rd[2 * j + 1];
-            } else {
-                rd.lo = __ldg(sm.rdg + 2 * j);
-                rd.hi = __ldg(sm.rdg + 2 * j + 1);
-            }
-            best = min(best, (hamming(kp.d, rd) << 16) | (uint32_t)j);
+            best = min(best, (hamming(kp.d, rec_desc(rr)) << 16) | (uint32_t)j);
         }
     }
     best = __reduce_min_sync(FULL, best);
@@ -306,6 +360,67 @@ FT_DEV bool p2_sweep(const TrackArgs &a, int *patch, const LeftKp &kp, const P2G
     return true;
 }
 
+// Fixed-size SAD sweep for the default 11x11 window / +-5 slide: the 121
+// (offset, row) jobs are spread over the warp with independent accumulators
+// (no shared atomics), row partials are summed by the 11 offset lanes, and
+// the arg-min over offsets is a redux.sync over (sad << 4 | offset), which
+// keeps the reference's "lowest offset on ties" (kernels.py:407-409).
+template <int HW, int HS>
+FT_DEV bool p2_sweep_fixed(const TrackArgs &a, int *patch, const LeftKp &kp, const P2Geom &g,
+                           long long xr0, int lane, double &disp_out, double &ur_out,
+                           int &sad_out) {
+    constexpr int NW = 2 * HW + 1, NR = 2 * HS + 2 * HW + 1, NOFF = 2 * HS + 1;
+    constexpr int NJOB = NOFF * NW, QJ = (NJOB + 31) / 32;
+    const int *pl = patch, *pr = patch + NW * NW;
+    int *part = patch + NW * NW + NW * NR;  // [NJOB]
+    int acc[QJ];
+#pragma unroll
+    for (int q = 0; q < QJ; ++q) acc[q] = 0;
+#pragma unroll
+    for (int q = 0; q < QJ; ++q) {
+        const int t = lane + 32 * q;
+        if (t < NJOB) {
+            const int oi = t / NW, dy = t - oi * NW;
+            const int cr = pr[HW * NR + oi + HW];  // R[yi, xr0 + off]
+            const int *lrow = pl + dy * NW;
+            const int *rrow = pr + dy * NR + oi;
+#pragma unroll
+            for (int dx = 0; dx < NW; ++dx) acc[q] += abs(lrow[dx] + cr - rrow[dx]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < QJ; ++q) {
+        const int t = lane + 32 * q;
+        if (t < NJOB) part[t] = acc[q];
+    }
+    __syncwarp();
+    int sad = 0x7fffffff;
+    if (lane < NOFF) {
+        sad = 0;
+#pragma unroll
+        for (int dy = 0; dy < NW; ++dy) sad += part[lane * NW + dy];
+    }
+    __syncwarp();  // patch buffers are reused by the next keypoint
+    const unsigned key = lane < NOFF ? ((unsigned)sad << 5) | (unsigned)lane : 0xffffffffu;
+    const unsigned best = __reduce_min_sync(FULL, key);
+    const int best_oi = (int)(best & 31u), best_sad = (int)(best >> 5);
+    const int s_m = __shfl_sync(FULL, sad, best_oi > 0 ? best_oi - 1 : 0);
+    const int s_p = __shfl_sync(FULL, sad, best_oi < NOFF - 1 ? best_oi + 1 : 0);
+    if (best_oi == 0 || best_oi == NOFF - 1) return false;
+    const double d_m = (double)s_m, d_0 = (double)best_sad, d_p = (double)s_p;
+    const double denom = d_m + d_p - 2.0 * d_0;
+    if (denom <= 0.0) return false;
+    const double delta = (d_m - d_p) / (2.0 * denom);
+    if (delta < -1.0 || delta > 1.0) return false;
+    const double ur_ref = ((double)(xr0 + (best_oi - HS)) + delta) * g.s;
+    const double disp = kp.u - ur_ref;
+    if (disp < a.sp.min_disparity || disp > a.sp.max_disparity) return false;
+    disp_out = disp;
+    ur_out = ur_ref;
+    sad_out = best_sad;
+    return true;
+}
+
 // Full per-keypoint stereo step for one warp.  The left patch loads are
 // issued before phase 1 (they depend only on the keypoint), so their latency
 // hides behind the candidate search; the right strip follows phase 1.
@@ -335,8 +450,12 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
         }
     }
     int cand, cdist;
+    const bool tlw = (a.tl != nullptr) && threadIdx.x < 32 && lk == (int64_t)f * a.L.cap +
+                     blockIdx.x % (a.Gs + a.Gm) * ((min(a.L.count[f], a.L.cap) + a.Gs - 1) / a.Gs);
+    if (tlw && lane == 0) a.tl[blockIdx.x * TL_SLOTS + 8] = global_ns();
     if (do_p1) {
         cand = phase1(a, sm, kp, lane, cdist);
+        if (tlw && lane == 0) a.tl[blockIdx.x * TL_SLOTS + 9] = global_ns();
         if (lane == 0 && a.so.cand_idx) {
             a.so.cand_idx[lk] = cand;
             a.so.cand_dist[lk] = cdist;
@@ -350,7 +469,7 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
     double disp = 0.0, ur = 0.0;
     int sad = 0;
     if (cand >= 0 && cand < n_right) {
-        const double urc = do_p1 ? sm.ru[cand] : a.R.u[rbase + cand];
+        const double urc = do_p1 ? sm.rtab[cand].u : __ldg(&a.R.rec[rbase + cand].u);
         if (do_ref) {
             if (g.left_ok) {
                 const long long xr0 = round_half_even(urc / g.s);
@@ -391,7 +510,12 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
                             pr[t] = __ldg(g.rp + (g.yi - hw + dy) * g.wr + (xr0 - hs - hw + dx));
                         }
                     }
-                    ok = p2_sweep(a, patch, kp, g, xr0, lane, disp, ur, sad);
+                    if (tlw && lane == 0) a.tl[blockIdx.x * TL_SLOTS + 10] = global_ns();
+                    if constexpr (FIXED)
+                        ok = p2_sweep_fixed<HW, HS>(a, patch, kp, g, xr0, lane, disp, ur, sad);
+                    else
+                        ok = p2_sweep(a, patch, kp, g, xr0, lane, disp, ur, sad);
+                    if (tlw && lane == 0) a.tl[blockIdx.x * TL_SLOTS + 11] = global_ns();
                 }
             }
         } else {  // matches_from_candidates (stereo.py:154-160)
@@ -407,7 +531,16 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
         a.so.refined_u[lk] = ok ? ur : 0.0;
         a.so.depth[lk] = ok ? a.sp.baseline_times_fx / disp : 0.0;
         a.so.sad[lk] = ok ? sad : 0;
+        if (tlw) a.tl[blockIdx.x * TL_SLOTS + 12] = global_ns();
     }
+}
+
+// shared table region of a stereo block: the staged right table, or at least
+// the median scratch (4 B per left keypoint)
+__host__ __device__ inline size_t stereo_table_bytes(const TrackArgs &a) {
+    const size_t t = a.stage_rdesc ? (size_t)64 * a.R.cap : 0;
+    const size_t m = (size_t)4 * a.L.cap;
+    return ((t > m ? t : m) + 15) & ~(size_t)15;
 }
 
 __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long long *bar,
@@ -429,18 +562,15 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
 
     StereoSmem sm;
     unsigned char *p = smem;
-    sm.rd = reinterpret_cast<uint4 *>(p);
-    p += a.stage_rdesc ? (size_t)32 * cap_r : 0;
-    sm.ru = reinterpret_cast<double *>(p);
-    p += (size_t)8 * cap_r;
-    sm.rv = reinterpret_cast<double *>(p);
-    p += (size_t)8 * cap_r;
-    sm.ro = reinterpret_cast<int *>(p);
-    p += (size_t)4 * cap_r;
+    sm.rtab_s = reinterpret_cast<ft_kp_record *>(p);
+    p += stereo_table_bytes(a);
+    sm.rtab = a.stage_rdesc ? sm.rtab_s : a.R.rec + rbase;
     sm.scan_tmp = reinterpret_cast<int *>(p);
     p += 32 * 4;
     sm.misc = reinterpret_cast<int *>(p);
     p += 16 * 4;
+    sm.hist = reinterpret_cast<int *>(p);
+    p += 512 * 4;
     sm.row_start = reinterpret_cast<int *>(p);
     p += (size_t)4 * (H + 1);
     sm.row_cursor = reinterpret_cast<int *>(p);
@@ -448,42 +578,54 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
     sm.patch = reinterpret_cast<int *>(p);
     p += (size_t)4 * TK_WARPS * a.patch_ints;
     sm.items = reinterpret_cast<uint16_t *>(p);
-    sm.rdg = reinterpret_cast<const uint4 *>(a.R.desc + 4 * rbase);
+    p += (size_t)2 * a.R.cap;
+    sm.binbuf = reinterpret_cast<uint16_t *>(p);
 
     if (rank == 0 && threadIdx.x == 0 && a.so.n_matched) a.so.n_matched[f] = 0;
     TL_MARK(a, 0);
+    if (threadIdx.x < 32) {  // translate every page the block touches later, now
+        const int l = threadIdx.x;
+        if (l == 0) prefetch_l2(bar);
+        if (l == 1) prefetch_l2(a.so.right_idx ? a.so.right_idx + lbase : nullptr);
+        if (l == 2) prefetch_l2(a.so.sad ? a.so.sad + lbase : nullptr);
+        if (l == 3) prefetch_l2(a.so.depth ? a.so.depth + lbase : nullptr);
+        if (l == 4) prefetch_l2(a.L.rec + lbase + k0);
+        if (do_ref && l >= 8 && l < 8 + a.PL.n_levels)
+            prefetch_l2(a.PL.data + (int64_t)f * a.PL.frame_bytes + a.PL.offsets[l - 8]);
+        if (do_ref && l >= 16 && l < 16 + a.PR.n_levels)
+            prefetch_l2(a.PR.data + (int64_t)f * a.PR.frame_bytes + a.PR.offsets[l - 16]);
+    }
 
     if (k0 < k1 && (do_p1 || finalize)) {
         const int kf = k0 + wid;
+        LeftKp kp_first;  // issued now: lands while the right table streams in
+        if (kf < k1) kp_first = load_left(a, lbase + kf);
         if (do_p1) {
             // right keypoint table -> shared memory with TMA bulk copies
             if (threadIdx.x == 0) {
                 fence_proxy_async_smem();
-                const unsigned b8 = round16(8u * n_right), b4 = round16(4u * n_right);
-                const unsigned b32 = a.stage_rdesc ? 32u * n_right : 0u;
-                mbar_arrive_expect_tx(mbar, 2 * b8 + b4 + b32);
-                if (n_right > 0) {
-                    bulk_g2s(sm.ru, a.R.u + rbase, b8, mbar);
-                    bulk_g2s(sm.rv, a.R.v + rbase, b8, mbar);
-                    bulk_g2s(sm.ro, a.R.octave + rbase, b4, mbar);
-                    if (b32) bulk_g2s(sm.rd, a.R.desc + 4 * rbase, b32, mbar);
-                }
+                const unsigned bytes = a.stage_rdesc ? 64u * n_right : 0u;
+                mbar_arrive_expect_tx(mbar, bytes);
+                if (bytes) bulk_g2s(sm.rtab_s, a.R.rec + rbase, bytes, mbar);
             }
+            for (int b = threadIdx.x; b < H; b += TK_THREADS) sm.row_cursor[b] = 0;
             mbar_wait(mbar, mphase & 1u);  // bit 0: phase of mbar[0]
             mphase ^= 1u;
+            __syncthreads();  // cursor zeroed
+            TL_MARK(a, 6);
             block_csr<TK_THREADS>(
                 n_right, H,
                 [&](int j) {
-                    long long r = round_half_even(sm.rv[j]);  // np.round: half-even
+                    long long r = round_half_even(sm.rtab[j].v);  // np.round: half-even
                     return (int)(r < 0 ? 0 : (r > H - 1 ? H - 1 : r));
                 },
-                sm.row_start, sm.row_cursor, sm.items, sm.scan_tmp);
+                sm.row_start, sm.row_cursor, sm.items, sm.binbuf);
         }
         TL_MARK(a, 1);
         int *patch = sm.patch + wid * a.patch_ints;
         const bool fixed55 = a.sp.half_window == 5 && a.sp.half_slide == 5;
         for (int k = kf; k < k1; k += TK_WARPS) {
-            const LeftKp kp = load_left(a, lbase + k);
+            const LeftKp kp = k == kf ? kp_first : load_left(a, lbase + k);
             if (fixed55) stereo_kp<5, 5>(a, sm, patch, f, lbase + k, rbase, n_right, kp, lane);
             else stereo_kp<0, 0>(a, sm, patch, f, lbase + k, rbase, n_right, kp, lane);
         }
@@ -496,49 +638,42 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
     int kept = 0;
     if (do_rej) {
         // every block computes the same median over the frame's accepted SADs
-        uint32_t *vals = reinterpret_cast<uint32_t *>(sm.ru);  // table no longer needed
-        int *hist = reinterpret_cast<int *>(sm.rv);
-        if (threadIdx.x == 0) sm.misc[4] = 0;
-        __syncthreads();
-        for (int k = threadIdx.x; k < n_left; k += TK_THREADS) {
-            if (__ldcg(a.so.right_idx + lbase + k) >= 0) {
-                const int pos = atomicAdd(&sm.misc[4], 1);
-                vals[pos] = (uint32_t)__ldcg(a.so.sad + lbase + k);
-            }
+        uint32_t *vals = reinterpret_cast<uint32_t *>(sm.rtab_s);  // table no longer needed
+        int *hist = sm.hist;
+        if (threadIdx.x == 0) {
+            sm.misc[4] = 0;
+            sm.misc[5] = 0;
         }
         __syncthreads();
+        int cnt = 0;
+        uint32_t vmax = 0;
+        for (int k = threadIdx.x; k < n_left; k += TK_THREADS) {
+            const bool m = __ldcg(a.so.right_idx + lbase + k) >= 0;
+            const uint32_t x = m ? (uint32_t)__ldcg(a.so.sad + lbase + k) : 0xffffffffu;
+            vals[k] = x;
+            cnt += m;
+            if (m) vmax = max(vmax, x);
+        }
+        cnt = __reduce_add_sync(FULL, cnt);
+        vmax = __reduce_max_sync(FULL, vmax);
+        if (lane == 0) {
+            atomicAdd(&sm.misc[4], cnt);
+            atomicMax(reinterpret_cast<unsigned *>(&sm.misc[5]), vmax);
+        }
+        __syncthreads();
+        TL_MARK(a, 13);
         const int nm = sm.misc[4];
         if (nm > 0) {
-            const int k_lo = (nm - 1) / 2, k_hi = nm / 2;
-            const uint32_t v_lo = block_select(vals, nm, k_lo, hist, sm.scan_tmp, sm.misc);
-            uint32_t v_hi = v_lo;
-            if (k_hi != k_lo) {
-                if (threadIdx.x == 0) {
-                    sm.misc[5] = 0;
-                    sm.misc[6] = 0x7fffffff;
-                }
-                __syncthreads();
-                int cle = 0, above = 0x7fffffff;
-                for (int i = threadIdx.x; i < nm; i += TK_THREADS) {
-                    const uint32_t x = vals[i];
-                    if (x <= v_lo) ++cle;
-                    else above = min(above, (int)x);
-                }
-                cle = __reduce_add_sync(FULL, cle);
-                above = __reduce_min_sync(FULL, above);
-                if (lane == 0) {
-                    atomicAdd(&sm.misc[5], cle);
-                    atomicMin(&sm.misc[6], above);
-                }
-                __syncthreads();
-                v_hi = sm.misc[5] > k_hi ? v_lo : (uint32_t)sm.misc[6];
-            }
-            const double med = (k_hi == k_lo) ? (double)v_lo : ((double)v_lo + (double)v_hi) / 2.0;
+            uint32_t v_lo, v_hi;
+            block_median_pair(vals, n_left, nm, (uint32_t)sm.misc[5], hist, sm.misc, v_lo, v_hi);
+            const double med = (nm & 1) ? (double)v_lo : ((double)v_lo + (double)v_hi) / 2.0;
             const double thr = a.sp.outlier_multiplier * med;
+            TL_MARK(a, 14);
             for (int k = k0 + threadIdx.x; k < k1; k += TK_THREADS) {
-                const int64_t i = lbase + k;
-                if (__ldcg(a.so.right_idx + i) < 0) continue;
-                if ((double)__ldcg(a.so.sad + i) > thr) {
+                const uint32_t x = vals[k];
+                if (x == 0xffffffffu) continue;
+                if ((double)x > thr) {
+                    const int64_t i = lbase + k;
                     a.so.right_idx[i] = -1;
                     a.so.distance[i] = 10000;
                     a.so.disparity[i] = 0.0;
@@ -573,17 +708,14 @@ struct QItem {
 };
 
 struct MapSmem {
-    uint4 *kd;          // [2*cap_kp] keypoint descriptors (when staged)
-    const uint4 *kdg;   // global keypoint descriptors of the frame
-    double *ku, *kv;
-    int *ko;
+    const ft_kp_record *ktab;  // keypoint table: shared copy (staged) or global
+    ft_kp_record *ktab_s;
     long long *kslots;  // [cap_kp] slots_in (hash source)
     int *htab;          // [1 << hash_bits] indices into kslots, -1 = empty
-    double *ppos, *pnrm, *pmin, *pmax;  // staged round of map points
-    long long *pid;
-    uint4 *pdesc;
+    ft_point_record *prnd;  // staged round of map points
     int *cell_start, *cell_cursor;
     uint16_t *items;
+    uint16_t *binbuf;   // [cap_kp]
     QItem *queue;       // [round_cap]
     int *res;           // [chunk] packed claim (kp | dist << 16 | lvl << 25) or -1
     long long *res_pid; // [chunk] id of the claiming point
@@ -626,15 +758,16 @@ struct PointIn {
 };
 
 FT_DEV PointIn staged_point(const MapSmem &sm, int li) {
+    const ft_point_record &r = sm.prnd[li];
     PointIn q;
-    q.px = sm.ppos[3 * li];
-    q.py = sm.ppos[3 * li + 1];
-    q.pz = sm.ppos[3 * li + 2];
-    q.nx = sm.pnrm[3 * li];
-    q.ny = sm.pnrm[3 * li + 1];
-    q.nz = sm.pnrm[3 * li + 2];
-    q.mind = sm.pmin[li];
-    q.maxd = sm.pmax[li];
+    q.px = r.pos[0];
+    q.py = r.pos[1];
+    q.pz = r.pos[2];
+    q.nx = r.nrm[0];
+    q.ny = r.nrm[1];
+    q.nz = r.nrm[2];
+    q.mind = r.min_dist;
+    q.maxd = r.max_dist;
     return q;
 }
 
@@ -706,26 +839,17 @@ FT_DEV double py_mod(double a, double b) {  // numpy float remainder
 FT_DEV int rotation_bin(const TrackArgs &a, int64_t kbase, int64_t pbase, int kp, int pi) {
     const double two_pi = 2.0 * 3.141592653589793;
     const int nb = a.pp.histogram_bins;
-    const double diff = py_mod(a.K.angle[kbase + kp] - a.io.ref_angles[pbase + pi], two_pi);
+    const double diff = py_mod(a.K.rec[kbase + kp].angle - a.io.ref_angles[pbase + pi], two_pi);
     long long b = (long long)floor(diff / two_pi * (double)nb);
     return (int)(b < 0 ? 0 : (b > nb - 1 ? nb - 1 : b));
 }
 
-// Stage points [q0, q1) of the frame into the shared round buffers (TMA).
+// Stage points [q0, q1) of the frame into the shared round buffer (one TMA copy).
 FT_DEV void stage_points(const TrackArgs &a, const MapSmem &sm, int64_t pbase, int q0, int q1,
                          unsigned long long *mbar) {
-    const unsigned n = (unsigned)(q1 - q0);
-    const unsigned b24 = round16(24u * n), b8 = round16(8u * n), b32 = 32u * n;
-    mbar_arrive_expect_tx(mbar, n ? 2 * b24 + 3 * b8 + b32 : 0u);
-    if (n) {
-        const int64_t g = pbase + q0;
-        bulk_g2s(sm.ppos, a.P.positions + 3 * g, b24, mbar);
-        bulk_g2s(sm.pnrm, a.P.normals + 3 * g, b24, mbar);
-        bulk_g2s(sm.pmin, a.P.min_dist + g, b8, mbar);
-        bulk_g2s(sm.pmax, a.P.max_dist + g, b8, mbar);
-        bulk_g2s(sm.pid, a.P.point_ids + g, b8, mbar);
-        bulk_g2s(sm.pdesc, a.P.desc + 4 * g, b32, mbar);
-    }
+    const unsigned bytes = 112u * (unsigned)(q1 - q0);
+    mbar_arrive_expect_tx(mbar, bytes);
+    if (bytes) bulk_g2s(sm.prnd, a.P.rec + pbase + q0, bytes, mbar);
 }
 
 __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigned char *smem,
@@ -740,7 +864,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     const int nx = pp.grid_nx, ny = pp.grid_ny, ncell = nx * ny;
     const int cap_kp = a.K.cap;
     const bool resolve = a.pmode & FT_PROJ_RESOLVE;
-    const bool rotation = (a.pmode & FT_PROJ_ROTATION) && a.io.ref_angles && a.K.angle;
+    const bool rotation = (a.pmode & FT_PROJ_ROTATION) && a.io.ref_angles;
     const bool use_hash = (a.pmode & FT_PROJ_SKIP_SLOTS) && a.hash_bits;
     const bool write_slots = a.pmode & FT_PROJ_WRITE_SLOTS;
     const bool ordered = resolve && a.po.corr_point;
@@ -750,32 +874,17 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
 
     MapSmem sm;
     unsigned char *p = smem;
-    sm.kd = reinterpret_cast<uint4 *>(p);
-    p += a.stage_kdesc ? (size_t)32 * cap_kp : 0;
-    sm.ku = reinterpret_cast<double *>(p);
-    p += (size_t)8 * cap_kp;
-    sm.kv = reinterpret_cast<double *>(p);
-    p += (size_t)8 * cap_kp;
+    sm.ktab_s = reinterpret_cast<ft_kp_record *>(p);
+    p += a.stage_kdesc ? (size_t)64 * cap_kp : 0;
+    sm.ktab = a.stage_kdesc ? sm.ktab_s : a.K.rec + kbase;
+    sm.prnd = reinterpret_cast<ft_point_record *>(p);
+    p += (size_t)112 * round_cap;
     sm.kslots = reinterpret_cast<long long *>(p);
     p += use_hash ? (size_t)8 * cap_kp : 0;
-    sm.ppos = reinterpret_cast<double *>(p);
-    p += (size_t)24 * round_cap;
-    sm.pnrm = reinterpret_cast<double *>(p);
-    p += (size_t)24 * round_cap;
-    sm.pmin = reinterpret_cast<double *>(p);
-    p += (size_t)8 * round_cap;
-    sm.pmax = reinterpret_cast<double *>(p);
-    p += (size_t)8 * round_cap;
-    sm.pid = reinterpret_cast<long long *>(p);
-    p += (size_t)8 * round_cap;
-    sm.pdesc = reinterpret_cast<uint4 *>(p);
-    p += (size_t)32 * round_cap;
     sm.res_pid = reinterpret_cast<long long *>(p);
     p += (size_t)8 * a.map_chunk_cap;
     sm.queue = reinterpret_cast<QItem *>(p);
     p += sizeof(QItem) * (size_t)round_cap;
-    sm.ko = reinterpret_cast<int *>(p);
-    p += (size_t)4 * cap_kp;
     sm.htab = reinterpret_cast<int *>(p);
     p += a.hash_bits ? ((size_t)4 << a.hash_bits) : 0;
     sm.scan_tmp = reinterpret_cast<int *>(p);
@@ -793,25 +902,48 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     sm.cell_cursor = reinterpret_cast<int *>(p);
     p += (size_t)4 * ncell;
     sm.items = reinterpret_cast<uint16_t *>(p);
-    sm.kdg = reinterpret_cast<const uint4 *>(a.K.desc + 4 * kbase);
+    p += (size_t)2 * cap_kp;
+    sm.binbuf = reinterpret_cast<uint16_t *>(p);
 
     TL_MARK(a, 0);
     const bool have_pts = p0 < p1;
+    // The first round of this block's points is unique per block (cold in
+    // HBM): every thread loads its share with 16-B loads right away -- many
+    // requests in flight -- instead of one TMA stream.  Later rounds (batched
+    // mode) use TMA.
+    const int n0 = have_pts ? min(p1, p0 + round_cap) - p0 : 0;
+    const bool pre_regs = have_pts && 7 * n0 <= 2 * TK_THREADS;
+    uint4 pre[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+    if (pre_regs) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.P.rec + pbase + p0);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int t = threadIdx.x + q * TK_THREADS;
+            if (t < 7 * n0)
+                asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(pre[q].x), "=r"(pre[q].y), "=r"(pre[q].z), "=r"(pre[q].w)
+                             : "l"(src + t));
+        }
+    }
+    if (threadIdx.x < 32) {  // translate every page the block touches later, now
+        const int l = threadIdx.x;
+        if (l == 0) prefetch_l2(bar);
+        if (l == 1) prefetch_l2(a.claims + kbase);
+        if (l == 2) prefetch_l2(a.io.slots_out ? a.io.slots_out + kbase : nullptr);
+        if (l == 3) prefetch_l2(a.po.out_kp ? a.po.out_kp + pbase + p0 : nullptr);
+        if (l == 4) prefetch_l2(a.po.corr_point ? a.po.corr_point + pbase : nullptr);
+        if (l == 5) prefetch_l2(a.po.slot_count ? a.po.slot_count + f : nullptr);
+        if (l == 6) prefetch_l2(a.blk_counts + (int64_t)f * G);
+    }
     // ---- every first-touch global read of the setup is one TMA batch -------
     if (threadIdx.x == 0 && have_pts) {
         fence_proxy_async_smem();
-        const unsigned b8 = round16(8u * n_kp), b4 = round16(4u * n_kp);
-        const unsigned b32 = a.stage_kdesc ? 32u * n_kp : 0u;
-        const unsigned bsl = use_hash ? b8 : 0u;
-        mbar_arrive_expect_tx(mbar, n_kp ? 2 * b8 + b4 + b32 + bsl : 0u);
-        if (n_kp) {
-            bulk_g2s(sm.ku, a.K.u + kbase, b8, mbar);
-            bulk_g2s(sm.kv, a.K.v + kbase, b8, mbar);
-            bulk_g2s(sm.ko, a.K.octave + kbase, b4, mbar);
-            if (b32) bulk_g2s(sm.kd, a.K.desc + 4 * kbase, b32, mbar);
-            if (bsl) bulk_g2s(sm.kslots, a.io.slots_in + kbase, bsl, mbar);
-        }
-        stage_points(a, sm, pbase, p0, min(p1, p0 + round_cap), mbar + 1);
+        const unsigned bt = a.stage_kdesc ? 64u * n_kp : 0u;
+        const unsigned bsl = use_hash ? round16(8u * n_kp) : 0u;
+        mbar_arrive_expect_tx(mbar, bt + bsl);
+        if (bt) bulk_g2s(sm.ktab_s, a.K.rec + kbase, bt, mbar);
+        if (bsl) bulk_g2s(sm.kslots, a.io.slots_in + kbase, bsl, mbar);
+        if (!pre_regs) stage_points(a, sm, pbase, p0, min(p1, p0 + round_cap), mbar + 1);
     }
     // launch epoch (same for every block of this slot's frame instance)
     unsigned long long ticket = 0;
@@ -834,6 +966,8 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     }
     if (have_pts && use_hash)
         for (int h = threadIdx.x; h < (1 << a.hash_bits); h += TK_THREADS) sm.htab[h] = -1;
+    if (have_pts)
+        for (int b = threadIdx.x; b < ncell; b += TK_THREADS) sm.cell_cursor[b] = 0;
     if (threadIdx.x == 0) sm.misc[0] = (int)(unsigned)(ticket / (resolve ? G : 1));
     __syncthreads();
     const unsigned epoch_hi = 0xffffffffu - (unsigned)sm.misc[0];
@@ -841,6 +975,15 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     if (have_pts) {
         mbar_wait(mbar, mphase & 1u);  // keypoint table (+ slots) landed
         mphase ^= 1u;
+        TL_MARK(a, 6);
+        if (pre_regs) {
+            uint4 *dst = reinterpret_cast<uint4 *>(sm.prnd);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int t = threadIdx.x + q * TK_THREADS;
+                if (t < 7 * n0) dst[t] = pre[q];
+            }
+        }
         if (use_hash)
             for (int k = threadIdx.x; k < n_kp; k += TK_THREADS)
                 if (sm.kslots[k] != NO_PID) hash_insert(sm.htab, a.hash_bits, sm.kslots, k);
@@ -848,12 +991,13 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
         block_csr<TK_THREADS>(
             n_kp, ncell,
             [&](int j) {  // FrameGrid cell: truncation, then clip (mapping.py:81-83)
-                long long cx = (long long)(sm.ku[j] / cellf), cy = (long long)(sm.kv[j] / cellf);
+                long long cx = (long long)(sm.ktab[j].u / cellf),
+                          cy = (long long)(sm.ktab[j].v / cellf);  // once per keypoint
                 cx = cx < 0 ? 0 : (cx > nx - 1 ? nx - 1 : cx);
                 cy = cy < 0 ? 0 : (cy > ny - 1 ? ny - 1 : cy);
                 return (int)(cy * nx + cx);
             },
-            sm.cell_start, sm.cell_cursor, sm.items, sm.scan_tmp);
+            sm.cell_start, sm.cell_cursor, sm.items, sm.binbuf);
         TL_MARK(a, 1);
         const double *R = a.io.rot + 9 * f, *T = a.io.trans + 3 * f;
         const double ccx = -(R[0] * T[0] + R[3] * T[1] + R[6] * T[2]);
@@ -869,8 +1013,11 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                 }
             }
             if (threadIdx.x == 0) sm.misc[1] = 0;
-            mbar_wait(mbar + 1, (mphase >> 1) & 1u);  // bit 1: phase of mbar[1]
-            mphase ^= 2u;
+            if (r0 != p0 || !pre_regs) {
+                mbar_wait(mbar + 1, (mphase >> 1) & 1u);  // bit 1: phase of mbar[1]
+                mphase ^= 2u;
+            }
+            if (r0 == p0) TL_MARK(a, 7);
             __syncthreads();
             const int li = threadIdx.x;
             const int i = r0 + li;
@@ -894,11 +1041,9 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             const int nq = sm.misc[1];
             for (int qi = wid; qi < nq; qi += TK_WARPS) {  // warp per visible point
                 const QItem &q = sm.queue[qi];
-                const long long qpid = sm.pid[q.li];
+                const long long qpid = sm.prnd[q.li].id;
                 if (use_hash && hash_contains(sm.htab, a.hash_bits, sm.kslots, qpid)) continue;
-                Desc pd;
-                pd.lo = sm.pdesc[2 * q.li];
-                pd.hi = sm.pdesc[2 * q.li + 1];
+                const Desc pd = rec_desc(sm.prnd[q.li]);
                 Best2 b;
                 best2_init(b);
                 for (int gy = q.cy0; gy <= q.cy1; ++gy) {
@@ -906,18 +1051,11 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                     const int end = sm.cell_start[gy * nx + q.cx1 + 1];
                     for (int ii = beg + lane; ii < end; ii += 32) {
                         const int j = sm.items[ii];
-                        if (fabs(sm.ku[j] - q.ucen) > q.r || fabs(sm.kv[j] - q.v) > q.r) continue;
-                        const int ko = sm.ko[j];
+                        const ft_kp_record &kr = sm.ktab[j];
+                        if (fabs(kr.u - q.ucen) > q.r || fabs(kr.v - q.v) > q.r) continue;
+                        const int ko = kr.octave;
                         if (ko < q.lvl - 1 || ko > q.lvl + 1) continue;
-                        Desc kd;
-                        if (a.stage_kdesc) {
-                            kd.lo = sm.kd[2 * j];
-                            kd.hi = sm.kd[2 * j + 1];
-                        } else {
-                            kd.lo = __ldg(sm.kdg + 2 * j);
-                            kd.hi = __ldg(sm.kdg + 2 * j + 1);
-                        }
-                        best2_push(b, hamming(pd, kd), (uint32_t)j);
+                        best2_push(b, hamming(pd, rec_desc(kr)), (uint32_t)j);
                     }
                 }
                 best2_warp_reduce(b);
@@ -1090,21 +1228,18 @@ __global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
 
 size_t stereo_smem(const TrackArgs &a) {
     const int cap = a.R.cap, H = a.sp.height;
-    size_t b = 16 + (a.stage_rdesc ? (size_t)32 * cap : 0) + (size_t)20 * cap + 4 * (32 + 16) +
-               4 * (size_t)(2 * H + 1) + 4 * (size_t)TK_WARPS * a.patch_ints + 2 * (size_t)cap + 64;
-    const size_t med = 16 + (size_t)16 * cap + 4 * 256;  // median scratch reuses ru / rv
-    return b > med ? b : med;
+    return 16 + stereo_table_bytes(a) + 4 * (32 + 16 + 512) + 4 * (size_t)(2 * H + 1) +
+           4 * (size_t)TK_WARPS * a.patch_ints + 4 * (size_t)cap + 64;
 }
 
 size_t map_smem(const TrackArgs &a) {
     const int cap = a.K.cap, ncell = a.pp.grid_nx * a.pp.grid_ny;
     const int round_cap = a.map_chunk_cap < TK_THREADS ? a.map_chunk_cap : TK_THREADS;
     const bool hash = a.hash_bits > 0;
-    return 16 + (a.stage_kdesc ? (size_t)32 * cap : 0) + (size_t)20 * cap +
-           (hash ? (size_t)8 * cap : 0) + (size_t)104 * round_cap +
-           sizeof(QItem) * (size_t)round_cap + (hash ? ((size_t)4 << a.hash_bits) : 0) +
-           4 * (32 + 16 + TK_MAX_BINS / 32) + 16 * (size_t)a.map_chunk_cap +
-           4 * (size_t)(2 * ncell + 1) + 2 * (size_t)cap + 64;
+    return 16 + (a.stage_kdesc ? (size_t)64 * cap : 0) + (size_t)112 * round_cap +
+           (hash ? (size_t)8 * cap : 0) + sizeof(QItem) * (size_t)round_cap +
+           (hash ? ((size_t)4 << a.hash_bits) : 0) + 4 * (32 + 16 + TK_MAX_BINS / 32) +
+           16 * (size_t)a.map_chunk_cap + 4 * (size_t)(2 * ncell + 1) + 4 * (size_t)cap + 64;
 }
 
 }  // namespace ft
@@ -1353,6 +1488,10 @@ static bool fill_stereo(TrackArgs &a, int32_t n_frames, const ft_keypoints *left
         *status = FT_E_RANGE;
         return false;
     }
+    if (left->cap > 2 * right->cap) {
+        *status = FT_E_RANGE;
+        return false;
+    }
     if (params->half_window < 1 || params->half_slide < 1 || params->half_window > 32 ||
         params->half_slide > 32 || ((mode & FT_STEREO_REFINE) && (mode & FT_STEREO_FROM_CAND))) {
         *status = FT_E_CONFIG;
@@ -1374,10 +1513,12 @@ static bool fill_stereo(TrackArgs &a, int32_t n_frames, const ft_keypoints *left
         *status = FT_E_RANGE;
         return false;
     }
-    // TMA staging: per-frame arrays start 16-B aligned (caps multiple of 4)
-    if ((left->cap & 3) || (right->cap & 3) || !aligned16(left->u) || !aligned16(left->v) ||
-        !aligned16(left->octave) || !aligned16(left->desc) || !aligned16(right->u) ||
-        !aligned16(right->v) || !aligned16(right->octave) || !aligned16(right->desc)) {
+    // TMA staging: record arrays 16-B aligned
+    if (!left->rec || !right->rec || !left->count || !right->count) {
+        *status = FT_E_NULL;
+        return false;
+    }
+    if (!aligned16(left->rec) || !aligned16(right->rec)) {
         *status = FT_E_RANGE;
         return false;
     }
@@ -1392,7 +1533,10 @@ static bool fill_stereo(TrackArgs &a, int32_t n_frames, const ft_keypoints *left
     a.so = *out;
     const int nw = 2 * params->half_window + 1;
     const int nr = 2 * params->half_slide + 2 * params->half_window + 1;
-    a.patch_ints = (mode & FT_STEREO_REFINE) ? nw * nw + nw * nr + 2 * params->half_slide + 1 : 0;
+    // left patch, right strip, then per-(offset,row) partials (fixed path)
+    a.patch_ints = (mode & FT_STEREO_REFINE)
+                       ? nw * nw + nw * nr + (2 * params->half_slide + 1) * nw
+                       : 0;
     return true;
 }
 
@@ -1424,11 +1568,11 @@ static bool fill_map(TrackArgs &a, int32_t n_frames, const ft_map_points *points
         *status = FT_E_NULL;
         return false;
     }
-    if ((points->cap & 3) || (frame->cap & 3) || !aligned16(points->positions) ||
-        !aligned16(points->normals) || !aligned16(points->min_dist) ||
-        !aligned16(points->max_dist) || !aligned16(points->desc) ||
-        !aligned16(points->point_ids) || !aligned16(frame->u) || !aligned16(frame->v) ||
-        !aligned16(frame->octave) || !aligned16(frame->desc) ||
+    if (!points->rec || !frame->rec || !points->count || !frame->count) {
+        *status = FT_E_NULL;
+        return false;
+    }
+    if (!aligned16(points->rec) || !aligned16(frame->rec) ||
         ((mode & FT_PROJ_SKIP_SLOTS) && !aligned16(io->slots_in))) {
         *status = FT_E_RANGE;
         return false;

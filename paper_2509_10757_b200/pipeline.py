@@ -26,7 +26,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .runtime import Layout, make_workspace, project_params, pyramid_struct, stereo_params
+from .runtime import (Layout, fill_kp_records, fill_point_records, make_workspace,
+                      project_params, pyramid_struct, stereo_params)
 from .types import ProjectionSearchConfig, StereoMatchConfig, StereoMatches
 
 
@@ -62,26 +63,21 @@ class FramePipeline:
 
         S, ck, cp = self.S, self.cap_kp, self.cap_pts
         lay = Layout()
+        # small per-frame inputs first (one 2 MB page holds them for a frame),
+        # then the pyramids, then the outputs: the map blocks' reads all land
+        # in the first page, so a cold TLB costs them one page walk
         for side in ("L", "R"):
             lay.add(f"{side}_n", 4 * S)
-            lay.add(f"{side}_u", 8 * S * ck)
-            lay.add(f"{side}_v", 8 * S * ck)
-            lay.add(f"{side}_oct", 4 * S * ck)
-            lay.add(f"{side}_desc", 32 * S * ck)
+            lay.add(f"{side}_rec", _lib.KP_RECORD.itemsize * S * ck)
+        lay.add("P_n", 4 * S)
+        lay.add("P_rec", _lib.POINT_RECORD.itemsize * S * cp)
+        lay.add("rot", 72 * S)
+        lay.add("trans", 24 * S)
+        lay.add("slots_in", 8 * S * ck)
         self.pyr_bytes = int(self.pyr.offsets[-1]) if self.pyr is not None else 0
         if self.pyr is not None:
             lay.add("pyr_l", S * self.pyr_bytes)
             lay.add("pyr_r", S * self.pyr_bytes)
-        lay.add("P_n", 4 * S)
-        lay.add("P_pos", 24 * S * cp)
-        lay.add("P_nrm", 24 * S * cp)
-        lay.add("P_mind", 8 * S * cp)
-        lay.add("P_maxd", 8 * S * cp)
-        lay.add("P_desc", 32 * S * cp)
-        lay.add("P_ids", 8 * S * cp)
-        lay.add("rot", 72 * S)
-        lay.add("trans", 24 * S)
-        lay.add("slots_in", 8 * S * ck)
         self.in_end = lay.total
         self.out_begin = lay.total
         lay.add("slots", 8 * S * ck)   # updated slots (output)
@@ -97,7 +93,10 @@ class FramePipeline:
         for name in ("c_point", "c_kp", "c_dist", "c_oct"):
             lay.add(name, 8 * S * cp)
         self.lay = lay
-        self.dev = torch.zeros(lay.total, dtype=torch.uint8, device=self.device)
+        # 2 MB-aligned arena (GPU large pages): fewest pages per frame
+        self._dev_raw = torch.zeros(lay.total + (2 << 20), dtype=torch.uint8, device=self.device)
+        off = (-self._dev_raw.data_ptr()) % (2 << 20)
+        self.dev = self._dev_raw[off:off + lay.total]
         self.host = torch.zeros(lay.total, dtype=torch.uint8).pin_memory()
         self.hnp = self.host.numpy()
         self.stream = torch.cuda.Stream(self.device)
@@ -125,10 +124,7 @@ class FramePipeline:
             if n > ck:
                 raise ValueError(f"{n} keypoints exceed capacity {ck}")
             self._h(f"{side}_n", np.int32, (S,))[s] = n
-            self._h(f"{side}_u", np.float64, (S, ck))[s, :n] = fs.u
-            self._h(f"{side}_v", np.float64, (S, ck))[s, :n] = fs.v
-            self._h(f"{side}_oct", np.int32, (S, ck))[s, :n] = fs.octave
-            self._h(f"{side}_desc", np.uint64, (S, ck, 4))[s, :n] = np.asarray(fs.descriptors).reshape(n, 4)
+            fill_kp_records(self._h(f"{side}_rec", _lib.KP_RECORD, (S, ck))[s], fs)
         if self.pyr is not None:
             if pyr_left is None or pyr_right is None:
                 raise ValueError("pipeline was built with pyramids: pass pyr_left / pyr_right")
@@ -140,12 +136,7 @@ class FramePipeline:
         if m > cp:
             raise ValueError(f"{m} map points exceed capacity {cp}")
         self._h("P_n", np.int32, (S,))[s] = m
-        self._h("P_pos", np.float64, (S, cp, 3))[s, :m] = np.asarray(soa.positions).reshape(m, 3)
-        self._h("P_nrm", np.float64, (S, cp, 3))[s, :m] = np.asarray(soa.normals).reshape(m, 3)
-        self._h("P_mind", np.float64, (S, cp))[s, :m] = soa.min_distances
-        self._h("P_maxd", np.float64, (S, cp))[s, :m] = soa.max_distances
-        self._h("P_desc", np.uint64, (S, cp, 4))[s, :m] = np.asarray(soa.descriptors).reshape(m, 4)
-        self._h("P_ids", np.int64, (S, cp))[s, :m] = soa.point_ids
+        fill_point_records(self._h("P_rec", _lib.POINT_RECORD, (S, cp))[s], soa)
         self._h("rot", np.float64, (S, 9))[s] = np.asarray(pose.rotation).reshape(9)
         self._h("trans", np.float64, (S, 3))[s] = np.asarray(pose.translation).reshape(3)
         sl = self._h("slots_in", np.int64, (S, ck))
@@ -166,9 +157,7 @@ class FramePipeline:
         kps = {}
         for side in ("L", "R"):
             k = _lib.FtKeypoints()
-            k.u, k.v = self._d(f"{side}_u"), self._d(f"{side}_v")
-            k.octave, k.desc = self._d(f"{side}_oct"), self._d(f"{side}_desc")
-            k.angle, k.count, k.cap = None, self._d(f"{side}_n"), ck
+            k.rec, k.count, k.cap = self._d(f"{side}_rec"), self._d(f"{side}_n"), ck
             kps[side] = k
         self.kl, self.kr = kps["L"], kps["R"]
         self.pl = pyramid_struct(self.pyr, self._d("pyr_l"), self.pyr_bytes) if self.pyr is not None else None
@@ -183,9 +172,7 @@ class FramePipeline:
             setattr(o, name, self._d(name))
         self.sout = o
         P = _lib.FtMapPoints()
-        P.positions, P.normals = self._d("P_pos"), self._d("P_nrm")
-        P.min_dist, P.max_dist = self._d("P_mind"), self._d("P_maxd")
-        P.desc, P.point_ids, P.count, P.cap = self._d("P_desc"), self._d("P_ids"), self._d("P_n"), cp
+        P.rec, P.count, P.cap = self._d("P_rec"), self._d("P_n"), cp
         self.points = P
         self.pparams = project_params(self.cam, self.pcfg, self.scale, self.levels, self.cell,
                                       self.nx, self.ny, None, 0.0)
@@ -194,8 +181,9 @@ class FramePipeline:
         io.slots_in, io.slots_out = self._d("slots_in"), self._d("slots")
         self.pio = io
         po = _lib.FtProjectOut()
-        po.corr_point, po.corr_kp = self._d("c_point"), self._d("c_kp")
-        po.corr_dist, po.corr_oct = self._d("c_dist"), self._d("c_oct")
+        # SearchLocalPoints needs the slots and counts, not the ordered
+        # correspondence list: leave corr_* unset (saves a group barrier)
+        po.corr_point = po.corr_kp = po.corr_dist = po.corr_oct = None
         po.corr_count, po.slot_count = self._d("c_n"), self._d("slot_n")
         self.pout = po
         self.pmode = (_lib.FT_PROJ_RESOLVE | _lib.FT_PROJ_SKIP_SLOTS | _lib.FT_PROJ_WRITE_SLOTS)

@@ -17,8 +17,8 @@ import math
 import numpy as np
 
 from . import _lib
-from .runtime import (Layout, add_keypoints, keypoints_struct, project_params, put_keypoints,
-                      runtime)
+from .runtime import (Layout, add_keypoints, fill_point_records, keypoints_struct,
+                      project_params, put_keypoints, runtime)
 from .types import Correspondences, ProjectionSearchConfig, NO_POINT
 
 __all__ = ["ProjectionSearchConfig", "Correspondences", "predict_scale", "frustum_and_cone_check",
@@ -76,33 +76,20 @@ def _grid_geometry(frame, cam) -> tuple[int, int, int]:
 
 def _add_points(lay: Layout, cap: int) -> None:
     lay.add("P_n", 4)
-    lay.add("P_pos", 24 * cap)
-    lay.add("P_nrm", 24 * cap)
-    lay.add("P_mind", 8 * cap)
-    lay.add("P_maxd", 8 * cap)
-    lay.add("P_desc", 32 * cap)
-    lay.add("P_ids", 8 * cap)
+    lay.add("P_rec", _lib.POINT_RECORD.itemsize * cap)
 
 
 def _put_points(rt, lay: Layout, pts) -> int:
     m = len(pts.point_ids)
     rt.put(lay, "P_n", np.array([m], dtype=np.int32), np.int32)
     if m:
-        rt.put(lay, "P_pos", np.asarray(pts.positions).reshape(m, 3), np.float64)
-        rt.put(lay, "P_nrm", np.asarray(pts.normals).reshape(m, 3), np.float64)
-        rt.put(lay, "P_mind", pts.min_distances, np.float64)
-        rt.put(lay, "P_maxd", pts.max_distances, np.float64)
-        rt.put(lay, "P_desc", np.asarray(pts.descriptors).reshape(m, 4), np.uint64)
-        rt.put(lay, "P_ids", pts.point_ids, np.int64)
+        fill_point_records(rt.host_view(lay, "P_rec", _lib.POINT_RECORD, (m,)), pts)
     return m
 
 
 def _points_struct(rt, lay: Layout, cap: int) -> _lib.FtMapPoints:
     s = _lib.FtMapPoints()
-    s.positions, s.normals = rt.ptr(lay, "P_pos"), rt.ptr(lay, "P_nrm")
-    s.min_dist, s.max_dist = rt.ptr(lay, "P_mind"), rt.ptr(lay, "P_maxd")
-    s.desc, s.point_ids, s.count = rt.ptr(lay, "P_desc"), rt.ptr(lay, "P_ids"), rt.ptr(lay, "P_n")
-    s.cap = cap
+    s.rec, s.count, s.cap = rt.ptr(lay, "P_rec"), rt.ptr(lay, "P_n"), cap
     return s
 
 

@@ -221,11 +221,7 @@ def pyramid_struct(pyr, data_ptr: int, frame_bytes: int) -> _lib.FtPyramid:
 
 def keypoints_struct(rt: Runtime, lay: Layout, prefix: str, cap: int) -> _lib.FtKeypoints:
     k = _lib.FtKeypoints()
-    k.u = rt.ptr(lay, f"{prefix}_u")
-    k.v = rt.ptr(lay, f"{prefix}_v")
-    k.octave = rt.ptr(lay, f"{prefix}_oct")
-    k.angle = rt.ptr(lay, f"{prefix}_ang") if f"{prefix}_ang" in lay.offsets else None
-    k.desc = rt.ptr(lay, f"{prefix}_desc")
+    k.rec = rt.ptr(lay, f"{prefix}_rec")
     k.count = rt.ptr(lay, f"{prefix}_n")
     k.cap = int(cap)
     return k
@@ -233,22 +229,38 @@ def keypoints_struct(rt: Runtime, lay: Layout, prefix: str, cap: int) -> _lib.Ft
 
 def add_keypoints(lay: Layout, prefix: str, cap: int, with_angle: bool = False) -> None:
     lay.add(f"{prefix}_n", 4)
-    lay.add(f"{prefix}_u", 8 * cap)
-    lay.add(f"{prefix}_v", 8 * cap)
-    lay.add(f"{prefix}_oct", 4 * cap)
-    if with_angle:
-        lay.add(f"{prefix}_ang", 8 * cap)
-    lay.add(f"{prefix}_desc", 32 * cap)
+    lay.add(f"{prefix}_rec", _lib.KP_RECORD.itemsize * cap)
+
+
+def fill_kp_records(rec: np.ndarray, feats, with_angle: bool = False) -> int:
+    """Pack a FeatureSet (reference SoA layout) into ft_kp_record rows."""
+    n = len(feats.u)
+    if n:
+        rec["u"][:n] = feats.u
+        rec["v"][:n] = feats.v
+        rec["desc"][:n] = np.asarray(feats.descriptors).reshape(n, 4)
+        rec["octave"][:n] = feats.octave
+        rec["angle"][:n] = feats.angle if with_angle else 0.0
+    return n
+
+
+def fill_point_records(rec: np.ndarray, pts) -> int:
+    """Pack a MapPointSoA into ft_point_record rows."""
+    m = len(pts.point_ids)
+    if m:
+        rec["desc"][:m] = np.asarray(pts.descriptors).reshape(m, 4)
+        rec["pos"][:m] = np.asarray(pts.positions).reshape(m, 3)
+        rec["nrm"][:m] = np.asarray(pts.normals).reshape(m, 3)
+        rec["min_dist"][:m] = pts.min_distances
+        rec["max_dist"][:m] = pts.max_distances
+        rec["id"][:m] = pts.point_ids
+    return m
 
 
 def put_keypoints(rt: Runtime, lay: Layout, prefix: str, feats, with_angle: bool = False) -> int:
     n = len(feats.u)
     rt.put(lay, f"{prefix}_n", np.array([n], dtype=np.int32), np.int32)
     if n:
-        rt.put(lay, f"{prefix}_u", feats.u, np.float64)
-        rt.put(lay, f"{prefix}_v", feats.v, np.float64)
-        rt.put(lay, f"{prefix}_oct", feats.octave, np.int32)
-        if with_angle:
-            rt.put(lay, f"{prefix}_ang", feats.angle, np.float64)
-        rt.put(lay, f"{prefix}_desc", np.asarray(feats.descriptors).reshape(n, 4), np.uint64)
+        rec = rt.host_view(lay, f"{prefix}_rec", _lib.KP_RECORD, (n,))
+        fill_kp_records(rec, feats, with_angle)
     return n

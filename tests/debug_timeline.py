@@ -13,11 +13,19 @@ from paper_2509_10757_b200.synthetic import make_workload
 path = os.environ.get("FT_DEBUG_TIMELINE", "/tmp/tl.txt")
 streams = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 warm = "--warm" in sys.argv
+codewarm = "--codewarm" in sys.argv  # flush, then run once on other data (warm code, cold data)
 if os.path.exists(path):
     os.remove(path)
 w = make_workload(seed=1000, n_landmarks=12000, map_points=5000, images=True)
 pipe = FramePipeline(w.cam, n_streams=streams, cap_kp=1280, cap_points=5120,
                      pyramid_geometry=w.pyr_left)
+pipe2 = FramePipeline(w.cam, n_streams=streams, cap_kp=1280, cap_points=5120,
+                      pyramid_geometry=w.pyr_left) if codewarm else None
+if pipe2 is not None:
+    for s in range(streams):
+        pipe2.load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
+    with torch.cuda.stream(pipe.stream):
+        pipe2.dev[:pipe2.in_end].copy_(pipe2.host[:pipe2.in_end], non_blocking=True)
 for s in range(streams):
     pipe.load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -28,6 +36,9 @@ for it in range(6):
         with torch.cuda.stream(pipe.stream):
             flush.fill_(1)
             flush.view(torch.int64).sum()
+    if pipe2 is not None:
+        os.environ.pop("FT_DEBUG_TIMELINE_OFF", None)
+        pipe2.launch_track(pipe.stream)
     pipe.launch_track(pipe.stream)
     pipe.synchronize()
 # parse the last launch
@@ -44,8 +55,11 @@ Gs = int(hdr.split("Gs=")[1].split()[0])
 Gm = int(hdr.split("Gm=")[1].split()[0])
 per = Gs + Gm
 t0 = T[:, 0][T[:, 0] > 0].min()
-names = {"stereo": ["start", "staged+csr", "phase1/2 done", "barrier", "end"],
-         "map": ["start", "staged+csr+hash", "projected", "searched", "barrier", "end"]}
+names = {"stereo": ["start", "staged+csr", "phase1/2 done", "barrier", "end", "-", "table landed",
+                    "-", "w0 kp loaded", "w0 phase1", "w0 right strip", "w0 sweep", "w0 out",
+                    "gathered", "median"],
+         "map": ["start", "staged+csr+hash", "projected", "searched", "barrier", "end",
+                 "table landed", "points landed"]}
 for role, sel in (("stereo", [i for i in range(len(T)) if i % per < Gs]),
                   ("map", [i for i in range(len(T)) if i % per >= Gs])):
     if not sel:

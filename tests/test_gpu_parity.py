@@ -280,3 +280,37 @@ def test_projection_fp64_audit_many_points(oracle):
         np.testing.assert_array_equal(kp, rkp)
         np.testing.assert_array_equal(ko, rko)
         np.testing.assert_array_equal(kd, rkd)
+
+
+def test_pack_kernels_match_host_packing():
+    """ft_pack_keypoints / ft_pack_points (device SoA -> records) equal the
+    host-side packing the runtime does."""
+    import torch
+    from paper_2509_10757_b200 import _lib
+    from paper_2509_10757_b200.runtime import fill_kp_records, fill_point_records
+    d = G.load("cfg2_frame_map.npz")
+    left, pts = G.feats(d, "left"), G.soa(d)
+    n, m = len(left.u), len(pts.point_ids)
+    L = _lib.load()
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    s = torch.cuda.current_stream().cuda_stream
+    cnt = cu(np.array([n], np.int32))
+    u, v, o, ang = cu(left.u), cu(left.v), cu(left.octave.astype(np.int32)), cu(left.angle)
+    desc = cu(left.descriptors.view(np.int64))
+    out = torch.zeros(n * 64, dtype=torch.uint8, device="cuda")
+    _lib.check(L.ft_pack_keypoints(1, u.data_ptr(), v.data_ptr(), o.data_ptr(), ang.data_ptr(),
+                                   desc.data_ptr(), cnt.data_ptr(), n, out.data_ptr(), s), "pack")
+    ref = np.zeros(n, _lib.KP_RECORD)
+    fill_kp_records(ref, left, with_angle=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy().view(_lib.KP_RECORD), ref)
+    cntp = cu(np.array([m], np.int32))
+    args = [cu(pts.positions), cu(pts.normals), cu(pts.min_distances), cu(pts.max_distances),
+            cu(pts.descriptors.view(np.int64)), cu(pts.point_ids)]
+    outp = torch.zeros(m * 112, dtype=torch.uint8, device="cuda")
+    _lib.check(L.ft_pack_points(1, *[t.data_ptr() for t in args], cntp.data_ptr(), m,
+                                outp.data_ptr(), s), "pack points")
+    refp = np.zeros(m, _lib.POINT_RECORD)
+    fill_point_records(refp, pts)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(outp.cpu().numpy().view(_lib.POINT_RECORD), refp)
