@@ -17,6 +17,7 @@ from .projection import (frustum_and_cone_check, predict_scale, resolve_conflict
                          rotation_consistency_filter, run_phase_a, search_by_projection,
                          search_prev_frame)
 from .localmap import search_local_points
+from .install import install, uninstall
 
 # ORB-SLAM-style names (BASELINE.json north star)
 SearchByProjection = search_by_projection
@@ -33,5 +34,6 @@ __all__ = [
     "refine_match_phase2", "reject_outliers", "triangulate_rays", "frustum_and_cone_check",
     "predict_scale", "resolve_conflicts", "rotation_consistency_filter", "run_phase_a",
     "search_by_projection", "search_prev_frame", "search_local_points", "SearchByProjection",
-    "SearchLocalPoints", "ComputeStereoMatches", "ComputeStereoFishEyeMatches",
+    "SearchLocalPoints", "ComputeStereoMatches", "ComputeStereoFishEyeMatches", "install",
+    "uninstall",
 ]
