@@ -47,6 +47,8 @@ def parse() -> argparse.Namespace:
     p.add_argument("--frames", type=int, default=8, help="distinct frames cycled per stream")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-images", action="store_true", help="feature bundles only (no phase 2)")
+    p.add_argument("--ship-pyramids", action="store_true",
+                   help="upload full pyramids instead of raw images + device pyramid build")
     p.add_argument("--batched-streams", type=int, default=64,
                    help="extra batched measurement (0 disables)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -226,9 +228,15 @@ def run_reference(args) -> None:
 
 
 def config_dict(args) -> dict:
+    if args.no_images:
+        img = ", feature bundle (no phase 2)"
+    elif args.ship_pyramids:
+        img = ", rendered images shipped as pyramids -> SAD phase 2"
+    else:
+        img = (", rendered images shipped raw (0.36 MB each) -> device pyramid build "
+               "(bit-exact build_pyramid) -> SAD phase 2")
     return {"workload": "cfg2: EuRoC-shaped stereo frame 752x480 (~1270 kps/image, 8 levels, "
-                        "scale 1.2" + (", rendered pyramids -> SAD phase 2" if not args.no_images
-                                       else ", feature bundle") +
+                        "scale 1.2" + img +
                         ") + 5000-point local map; stereo + SearchLocalPoints per frame",
             "streams_per_gpu": args.streams, "frames_cycled": args.frames,
             "l2": "flushed before every timed step (256 MiB write, then read back)",
@@ -261,8 +269,9 @@ def main() -> None:
     cap_kp = int(max(max(len(f.left.u), len(f.right.u)) for f in frames) + 31) // 32 * 32
     cap_pts = int(max(len(f.local.point_ids) for f in frames) + 255) // 256 * 256
     S = args.streams
+    raw = images and not args.ship_pyramids
     pipe = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
-                         pyramid_geometry=w0.pyr_left if images else None)
+                         pyramid_geometry=w0.pyr_left if images else None, raw_images=raw)
 
     def load(step: int) -> None:
         for s in range(S):
@@ -328,13 +337,13 @@ def main() -> None:
     clocks = clk.summary()
 
     # ---- per-kernel timing for the roofline (eager, on the launching stream)
-    kern = {"track": [], "stereo_only": [], "map_only": []}
+    kern = {"pyramids": [], "track": [], "stereo_only": [], "map_only": []}
     for k in range(max(10, args.steps // 2)):
         load(k)
         with torch.cuda.stream(pipe.stream):
             pipe.dev[:pipe.in_end].copy_(pipe.host[:pipe.in_end], non_blocking=True)
-        for name, fn in (("track", pipe.launch_track), ("stereo_only", pipe.launch_stereo),
-                         ("map_only", pipe.launch_project)):
+        for name, fn in (("pyramids", pipe.launch_pyramids), ("track", pipe.launch_track),
+                         ("stereo_only", pipe.launch_stereo), ("map_only", pipe.launch_project)):
             l2_flush()
             a, b = ev(), ev()
             a.record(pipe.stream)
@@ -388,10 +397,11 @@ def main() -> None:
                              "peak_gpopc_s": popc, "peak_source": "ft_bench_popc (measured)",
                              "frac": (8 * ham / (track_ms / 1e3) / 1e9) / popc if popc else None},
             "kernels_ms": {"ft_track_frames": track_ms,
+                           "ft_build_pyramids": float(np.median(kern["pyramids"])) if raw else 0.0,
                            "stereo_only": float(np.median(kern["stereo_only"])),
                            "map_only": float(np.median(kern["map_only"]))},
             "work_per_frame": units, "clocks": clocks,
-            "gpu_launches": 2 * args.steps, "parity_spot_check": check}
+            "gpu_launches": (2 + 2 * raw) * args.steps, "parity_spot_check": check}
     if not args.quick:
         if args.batched_streams > 0 and world == 1:
             line["batched"] = batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts,
@@ -443,7 +453,8 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
     S = args.batched_streams
     w0 = frames[0]
     pipe = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
-                         pyramid_geometry=w0.pyr_left if images else None)
+                         pyramid_geometry=w0.pyr_left if images else None,
+                         raw_images=images and not args.ship_pyramids)
     for s in range(S):
         f = frames[s % len(frames)]
         pipe.load_frame(s, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)

@@ -36,6 +36,7 @@
  *   ft_stereo_fisheye_bf    stereo.py:238-244       bruteforce_match_kernel as
  *                                                   launched by match_fisheye
  *   ft_track_frames         tracker.py:279 + :354   stereo + SearchLocalPoints fused
+ *   ft_build_pyramids       extraction.py:97-125    build_pyramid
  *   ft_project_search       projection.py:118-221   run_phase_a ->
  *                                                   resolve_conflicts ->
  *                                                   rotation_consistency_filter
@@ -218,6 +219,15 @@ size_t ft_workspace_bytes(int32_t n_frames, int32_t cap_left, int32_t cap_points
 /* Initialise a workspace once after allocation (counters to 0, claims to
  * ~0); every kernel restores that state on exit. */
 int ft_workspace_init(const ft_workspace *ws, ft_stream_t stream);
+
+/* extraction.py:97-125 build_pyramid for n_images flat pyramids (image i at
+ * pyr->data + i * frame_bytes).  Level 0 comes from `images` (image i at
+ * images + i * image_stride; copied into the pyramid) or, when `images` is
+ * NULL, is already in place.  Levels 1..L-1 (5x5 binomial, reflect-101,
+ * round half up; then fp64 bilinear to floor(dims / scale^l)) are written
+ * bit-exact with the reference.  n_images <= 2 * ws->n_frames. */
+int ft_build_pyramids(int32_t n_images, const ft_pyramid *pyr, const uint8_t *images,
+                      int64_t image_stride, const ft_workspace *ws, ft_stream_t stream);
 
 /* SoA -> packed records for F frames (any pointer but u/v/octave/desc/ids may
  * be NULL: angle -> 0).  Caller-held reference-layout device arrays at

@@ -102,7 +102,7 @@ _lib = None
 EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_workspace_init",
            "ft_hamming_pairs", "ft_stereo_pinhole", "ft_stereo_fisheye_bf", "ft_project_search",
            "ft_track_frames", "ft_resolve_conflicts", "ft_rotation_filter", "ft_bench_popc",
-           "ft_pack_keypoints", "ft_pack_points")
+           "ft_pack_keypoints", "ft_pack_points", "ft_build_pyramids")
 
 
 def build(force: bool = False) -> Path:
@@ -145,6 +145,7 @@ def load() -> ctypes.CDLL:
     L.ft_bench_popc.argtypes = [i32, i32, i32, vp, vp]
     L.ft_pack_keypoints.argtypes = [i32, vp, vp, vp, vp, vp, vp, i32, vp, vp]
     L.ft_pack_points.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp]
+    L.ft_build_pyramids.argtypes = [i32, P(FtPyramid), vp, i64, W, vp]
     _lib = L
     return L
 

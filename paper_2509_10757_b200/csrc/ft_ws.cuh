@@ -8,6 +8,7 @@
 //   project  claims u64[F * cap_left]
 //   track    barrier counters u64[F] (stereo) | u64[F] (map) | epoch counters
 //            u64[F] | per-block counts i32[F * WS_MAX_GROUP] | hist i32[F * 256]
+//   pyramid  barrier counters u64[2F]
 // Counters start at 0 and claims at ~0 (ft_workspace_init).  Barrier and
 // epoch counters only grow; claims carry the launch epoch in their high word,
 // so no kernel has to reset anything.
@@ -45,7 +46,7 @@ inline size_t fisheye_entries(int F, int cap_left) {
 
 struct WsLayout {
     size_t stereo_counters, fisheye_counters, fisheye_partials, proj_claims, track_bar_s,
-        track_bar_m, track_ep_m, track_blk_counts, track_hist, total;
+        track_bar_m, track_ep_m, track_blk_counts, track_hist, pyr_bar, total;
     size_t fisheye_partial_entries;
 };
 
@@ -72,6 +73,8 @@ inline WsLayout ws_layout(int F, int cap_left, int cap_points) {
     o += ws_align((size_t)F * WS_MAX_GROUP * 4);
     L.track_hist = o;
     o += ws_align((size_t)F * 256 * 4);
+    L.pyr_bar = o;  // two images (left, right) per frame
+    o += ws_align((size_t)F * 2 * 8);
     L.total = o;
     return L;
 }

@@ -43,7 +43,8 @@ class FramePipeline:
     def __init__(self, cam, n_streams: int = 1, cap_kp: int = 2048, cap_points: int = 8192,
                  pyramid_geometry=None, stereo_cfg: StereoMatchConfig | None = None,
                  proj_cfg: ProjectionSearchConfig | None = None, scale: float = 1.2,
-                 levels: int = 8, grid_cell_px: int = 48, device: int | None = None):
+                 levels: int = 8, grid_cell_px: int = 48, device: int | None = None,
+                 raw_images: bool = False):
         if not torch.cuda.is_available():
             raise _lib.FtError("FramePipeline needs a CUDA device (no CPU fallback)")
         self.lib = _lib.load()
@@ -57,6 +58,8 @@ class FramePipeline:
         self.scale, self.levels = float(scale), int(levels)
         self.scale_pow = self.scale ** np.arange(self.levels, dtype=np.float64)
         self.pyr = pyramid_geometry  # object with widths / heights / offsets, or None
+        # raw_images: frames ship level 0 only; ft_build_pyramids builds the rest
+        self.raw = bool(raw_images) and pyramid_geometry is not None
         self.cell = int(grid_cell_px)
         self.nx = max(1, (int(cam.width) + self.cell - 1) // self.cell)
         self.ny = max(1, (int(cam.height) + self.cell - 1) // self.cell)
@@ -75,9 +78,11 @@ class FramePipeline:
         lay.add("trans", 24 * S)
         lay.add("slots_in", 8 * S * ck)
         self.pyr_bytes = int(self.pyr.offsets[-1]) if self.pyr is not None else 0
-        if self.pyr is not None:
-            lay.add("pyr_l", S * self.pyr_bytes)
-            lay.add("pyr_r", S * self.pyr_bytes)
+        self.img_bytes = int(self.pyr.widths[0]) * int(self.pyr.heights[0]) if self.pyr is not None else 0
+        if self.raw:
+            lay.add("imgs", 2 * S * self.img_bytes)  # [left x S | right x S]
+        elif self.pyr is not None:
+            lay.add("pyrs", 2 * S * self.pyr_bytes)
         self.in_end = lay.total
         self.out_begin = lay.total
         lay.add("slots", 8 * S * ck)   # updated slots (output)
@@ -87,6 +92,8 @@ class FramePipeline:
         lay.add("slot_n", 4 * S)
         lay.add("c_n", 4 * S)
         self.out_end = lay.total
+        if self.raw:  # device-built pyramids: not copied
+            lay.add("pyrs", 2 * S * self.pyr_bytes)
         # device-only scratch (not copied)
         lay.add("cand_idx", 8 * S * ck)
         lay.add("cand_dist", 8 * S * ck)
@@ -127,10 +134,18 @@ class FramePipeline:
             fill_kp_records(self._h(f"{side}_rec", _lib.KP_RECORD, (S, ck))[s], fs)
         if self.pyr is not None:
             if pyr_left is None or pyr_right is None:
-                raise ValueError("pipeline was built with pyramids: pass pyr_left / pyr_right")
-            pb = self.pyr_bytes
-            self._h("pyr_l", np.uint8, (S, pb))[s] = pyr_left.data
-            self._h("pyr_r", np.uint8, (S, pb))[s] = pyr_right.data
+                raise ValueError("pipeline was built with pyramids: pass pyr_left / pyr_right "
+                                 "(raw_images: level 0 is used)")
+            if self.raw:
+                ib = self.img_bytes
+                imgs = self._h("imgs", np.uint8, (2, S, ib))
+                imgs[0, s] = np.asarray(pyr_left.data)[:ib]
+                imgs[1, s] = np.asarray(pyr_right.data)[:ib]
+            else:
+                pb = self.pyr_bytes
+                pyrs = self._h("pyrs", np.uint8, (2, S, pb))
+                pyrs[0, s] = pyr_left.data
+                pyrs[1, s] = pyr_right.data
         soa = local.soa
         m = len(local.point_ids)
         if m > cp:
@@ -160,8 +175,12 @@ class FramePipeline:
             k.rec, k.count, k.cap = self._d(f"{side}_rec"), self._d(f"{side}_n"), ck
             kps[side] = k
         self.kl, self.kr = kps["L"], kps["R"]
-        self.pl = pyramid_struct(self.pyr, self._d("pyr_l"), self.pyr_bytes) if self.pyr is not None else None
-        self.pr = pyramid_struct(self.pyr, self._d("pyr_r"), self.pyr_bytes) if self.pyr is not None else None
+        if self.pyr is not None:
+            pyrs = self._d("pyrs")
+            self.pl = pyramid_struct(self.pyr, pyrs, self.pyr_bytes)
+            self.pr = pyramid_struct(self.pyr, pyrs + S * self.pyr_bytes, self.pyr_bytes)
+        else:
+            self.pl = self.pr = None
         self.sparams = stereo_params(self.scfg, int(self.cam.height), self.scale_pow,
                                      float(self.cam.baseline_times_fx))
         self.smode = _lib.FT_STEREO_PHASE1 | _lib.FT_STEREO_REJECT | (
@@ -204,11 +223,18 @@ class FramePipeline:
                                             self.pparams, self.pio, self.pmode, self.pout,
                                             self.ws, stream.cuda_stream), "ft_track_frames")
 
+    def launch_pyramids(self, stream) -> None:
+        if self.raw:
+            _lib.check(self.lib.ft_build_pyramids(2 * self.S, self.pl, self._d("imgs"),
+                                                  self.img_bytes, self.ws, stream.cuda_stream),
+                       "ft_build_pyramids")
+
     def _step(self, copies: bool) -> None:
         a = self.stream
         if copies:
             with torch.cuda.stream(a):
                 self.dev[:self.in_end].copy_(self.host[:self.in_end], non_blocking=True)
+        self.launch_pyramids(a)
         self.launch_track(a)
         if copies:
             with torch.cuda.stream(a):

@@ -314,3 +314,19 @@ def test_pack_kernels_match_host_packing():
     fill_point_records(refp, pts)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(outp.cpu().numpy().view(_lib.POINT_RECORD), refp)
+
+
+def test_device_pyramid_matches_reference_pyramids():
+    """ft_build_pyramids rebuilds the reference's cfg1 pyramids (levels 1..7)
+    bit-exactly from level 0 (the raw image)."""
+    from types import SimpleNamespace
+    from paper_2509_10757_b200.pyramid import build_pyramid
+    d = G.load("cfg1_stereo.npz")
+    for side in ("l", "r"):
+        ref = G.pyramid(d, side)
+        h, w = int(ref.heights[0]), int(ref.widths[0])
+        img = ref.data[:h * w].reshape(h, w)
+        got = build_pyramid(img, SimpleNamespace(levels=8, scale=1.2, patch_size=31))
+        np.testing.assert_array_equal(got.offsets, ref.offsets)
+        for lvl in range(8):
+            np.testing.assert_array_equal(got.level(lvl), ref.level(lvl), err_msg=f"{side} level {lvl}")

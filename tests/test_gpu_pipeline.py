@@ -41,13 +41,14 @@ def expected(workloads, oracle):
     return out
 
 
-def _run(workloads, expected, n_streams, replays):
+def _run(workloads, expected, n_streams, replays, raw=False):
     from paper_2509_10757_b200.pipeline import FramePipeline
     w0 = workloads[0]
     cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
     cap_pts = max(len(w.local.point_ids) for w in workloads)
     pipe = FramePipeline(w0.cam, n_streams=n_streams, cap_kp=(cap_kp + 31) // 32 * 32,
-                         cap_points=(cap_pts + 255) // 256 * 256, pyramid_geometry=w0.pyr_left)
+                         cap_points=(cap_pts + 255) // 256 * 256, pyramid_geometry=w0.pyr_left,
+                         raw_images=raw)
     for s in range(n_streams):
         w = workloads[s % len(workloads)]
         pipe.load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
@@ -77,3 +78,21 @@ def test_four_streams(workloads, expected):
 
 def test_many_streams_multiple_waves(workloads, expected):
     _run(workloads, expected, 200, 2)
+
+
+def test_raw_images_pipeline(workloads, expected):
+    """Frames ship level-0 images; the device builds the pyramids."""
+    _run(workloads, expected, 1, 3, raw=True)
+    _run(workloads, expected, 8, 2, raw=True)
+
+
+def test_synthetic_pyramids_equal_device_build(workloads):
+    """The workload generator's numpy pyramid equals the bit-exact device
+    build (so raw-image runs compare against the same oracle inputs)."""
+    from types import SimpleNamespace
+    from paper_2509_10757_b200.pyramid import build_pyramid
+    w = workloads[0]
+    h, wd = int(w.pyr_left.heights[0]), int(w.pyr_left.widths[0])
+    got = build_pyramid(w.pyr_left.data[:h * wd].reshape(h, wd),
+                        SimpleNamespace(levels=8, scale=1.2, patch_size=31))
+    np.testing.assert_array_equal(got.data, w.pyr_left.data)
