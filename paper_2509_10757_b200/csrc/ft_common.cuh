@@ -37,6 +37,34 @@ FT_DEV uint32_t hamming(const Desc &a, const Desc &b) {
            __popc(a.hi.z ^ b.hi.z) + __popc(a.hi.w ^ b.hi.w);
 }
 
+FT_DEV unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Barrier among the G co-resident blocks sharing `ctr` (cooperative
+// launches only).  ctr = (generation << 32) | arrivals; the G-th arrival
+// resets the arrivals and bumps the generation in ONE atomic, so the counter
+// returns to (gen, 0) after every barrier: launches of any G may reuse it and
+// nothing has to be reset between launches or graph replays.  Writes before
+// the barrier are visible after it (fence + release sequence on ctr).
+__device__ inline void group_barrier(unsigned long long *ctr, int G) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long old = atomicAdd(ctr, 1ull);
+        if ((uint32_t)old == (uint32_t)(G - 1)) {
+            atomicAdd(ctr, (1ull << 32) - (unsigned long long)G);
+        } else {
+            const uint32_t gen = (uint32_t)(old >> 32);
+            while ((uint32_t)(ld_acquire_u64(ctr) >> 32) == gen) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // numba int(round(x)) and np.round are round-half-to-even.
 FT_DEV long long round_half_even(double x) { return __double2ll_rn(x); }
 

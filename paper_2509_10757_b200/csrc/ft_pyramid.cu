@@ -20,6 +20,7 @@ namespace ft {
 
 constexpr int PY_THREADS = 512;
 constexpr int PY_MAX_W = 4096;
+constexpr int PY_SUB = 8;  // output rows per shared-memory pass
 
 struct PyrArgs {
     uint8_t *data;
@@ -28,7 +29,7 @@ struct PyrArgs {
     int64_t offsets[FT_MAX_LEVELS];
     int32_t widths[FT_MAX_LEVELS];
     int32_t heights[FT_MAX_LEVELS];
-    int32_t n_images, G, max_band_src;
+    int32_t n_images, G, sub;  // G blocks per image, <= sub output rows per pass
     unsigned long long *bar;  // [n_images]
     const uint8_t *src0;      // optional separate level-0 images (else in place)
     int64_t src0_stride;
@@ -38,21 +39,6 @@ FT_DEV int reflect101(int i, int n) {  // kernels.py:196-201
     if (i < 0) return -i;
     if (i >= n) return 2 * n - 2 - i;
     return i;
-}
-
-FT_DEV void pyr_barrier(unsigned long long *ctr, int G) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned long long t = atomicAdd(ctr, 1ull);
-        const unsigned long long target = (t / G + 1) * (unsigned long long)G;
-        unsigned long long v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
-        } while (v < target);
-        __threadfence();
-    }
-    __syncthreads();
 }
 
 // Source-row span [lo, hi] of the smoothed previous level that output rows
@@ -91,8 +77,9 @@ __global__ void __launch_bounds__(PY_THREADS) pyramid_kernel(const PyrArgs a) {
         uint8_t *dst = base + a.offsets[l];
         const double sy = (double)hs / (double)hd, sx = (double)ws / (double)wd;
         const int band = (hd + a.G - 1) / a.G;
-        const int r0 = rank * band, r1 = min(hd, r0 + band);
-        if (r0 < r1) {
+        const int b0 = rank * band, b1 = min(hd, b0 + band);
+        for (int r0 = b0; r0 < b1; r0 += a.sub) {  // shared memory holds `sub` rows
+            const int r1 = min(b1, r0 + a.sub);
             int slo, shi;  // smoothed rows needed
             needed_rows(r0, r1, sy, hs, slo, shi);
             const int tlo = slo - 2, thi = shi + 2;  // blurred rows (pre-reflection)
@@ -135,8 +122,9 @@ __global__ void __launch_bounds__(PY_THREADS) pyramid_kernel(const PyrArgs a) {
                 const double bot = (1.0 - ax) * (double)s1[x0c] + ax * (double)s1[x1c];
                 dst[(int64_t)i * wd + j] = (uint8_t)(int)((1.0 - ay) * top + ay * bot + 0.5);
             }
+            __syncthreads();
         }
-        if (l + 1 < a.n_levels) pyr_barrier(a.bar + img, a.G);
+        if (l + 1 < a.n_levels) group_barrier(a.bar + img, a.G);
     }
 }
 
@@ -169,27 +157,33 @@ extern "C" int ft_build_pyramids(int32_t n_images, const ft_pyramid *pyr,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     a.bar = ws_ptr<unsigned long long>(ws, ws_layout(ws).pyr_bar);
     if (images && image_stride < (int64_t)a.widths[0] * a.heights[0]) return FT_E_RANGE;
-    // images are processed in chunks that fit one resident wave
+    // shared memory for one pass of PY_SUB output rows (worst level)
+    a.sub = PY_SUB;
+    size_t smem = 0;
+    for (int l = 1; l < pyr->n_levels; ++l) {
+        const int hd = a.heights[l], hs = a.heights[l - 1], ws_ = a.widths[l - 1];
+        const int src_rows = (int)ceil((double)PY_SUB * hs / hd) + 4;
+        const size_t b = (size_t)(src_rows + 4) * ws_ * 4 + (size_t)src_rows * ws_ + 64;
+        smem = b > smem ? b : smem;
+    }
+    if (smem > 227 * 1024) return FT_E_RANGE;
+    cudaError_t e = cudaFuncSetAttribute(pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pyramid_kernel, PY_THREADS, smem);
+    if (occ < 1) return FT_E_RANGE;
+    const int resident = occ * sms;
+    // images in chunks that fit one resident wave (cooperative launch);
+    // G blocks per image: bands of ~PY_SUB rows at level 1 when they fit
     for (int i0 = 0; i0 < n_images;) {
         const int rem = n_images - i0;
-        const int chunk = rem < sms ? rem : sms;
-        int G = (a.heights[1] + 7) / 8;  // bands of ~8 output rows at level 1
-        if ((long long)G * chunk > sms) G = sms / chunk;
+        const int chunk = rem < resident ? rem : resident;
+        int G = (a.heights[1] + PY_SUB - 1) / PY_SUB;
+        if ((long long)G * chunk > resident) G = resident / chunk;
+        if (G < 1) G = 1;
         a.G = G;
         a.n_images = chunk;
-        size_t smem = 0;  // worst level: (blurred rows * 4 + smoothed rows) * width
-        for (int l = 1; l < pyr->n_levels; ++l) {
-            const int hd = a.heights[l], hs = a.heights[l - 1], ws_ = a.widths[l - 1];
-            const int band = (hd + G - 1) / G;
-            const int src_rows = (int)ceil((double)band * hs / hd) + 4;
-            const size_t b = (size_t)(src_rows + 4) * ws_ * 4 + (size_t)src_rows * ws_ + 64;
-            smem = b > smem ? b : smem;
-        }
-        if (smem > 227 * 1024) return FT_E_RANGE;
-        cudaFuncSetAttribute(pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pyramid_kernel, PY_THREADS, smem);
-        if ((long long)occ * sms < (long long)G * chunk) return FT_E_RANGE;
         a.data = const_cast<uint8_t *>(pyr->data) + (int64_t)i0 * pyr->frame_bytes;
         a.src0 = images ? images + (int64_t)i0 * image_stride : nullptr;
         a.src0_stride = image_stride;
@@ -203,7 +197,7 @@ extern "C" int ft_build_pyramids(int32_t n_images, const ft_pyramid *pyr,
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, pyramid_kernel, a);
+        e = cudaLaunchKernelEx(&cfg, pyramid_kernel, a);
         if (e != cudaSuccess) return (int)e;
         i0 += chunk;
     }

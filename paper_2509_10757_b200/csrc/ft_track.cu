@@ -98,31 +98,17 @@ FT_DEV unsigned long long global_ns() {
     } while (0)
 
 // ---------------------------------------------------------------------------
-// group barrier among the G blocks of one role in one slot.  The counter only
-// grows; the generation is the arrival ticket / G, so no reset is needed.
+// group barrier among the G blocks of one role in one slot: one 64-bit
+// counter, low word = arrivals, high word = generation.  The last arrival
+// resets the count and bumps the generation in one atomic, so the counter is
+// back to (gen, 0) after every barrier and launches of any geometry may share
+// a workspace.
 
 // Warm the TLB / L2 for a page the block will touch later (no data use).
 FT_DEV void prefetch_l2(const void *p) {
     if (p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-FT_DEV unsigned long long ld_acquire_u64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ void group_barrier(unsigned long long *ctr, int G) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned long long t = atomicAdd(ctr, 1ull);
-        const unsigned long long target = (t / G + 1) * (unsigned long long)G;
-        while (ld_acquire_u64(ctr) < target) __nanosleep(32);
-        __threadfence();
-    }
-    __syncthreads();
-}
 
 // ---------------------------------------------------------------------------
 // np.median of the accepted SADs (stereo.py:180): the values of ranks

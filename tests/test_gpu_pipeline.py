@@ -86,6 +86,13 @@ def test_raw_images_pipeline(workloads, expected):
     _run(workloads, expected, 8, 2, raw=True)
 
 
+def test_raw_images_many_streams(workloads, expected):
+    """More images than one cooperative wave holds: the pyramid build runs in
+    chunks with different blocks-per-image, sharing the barrier counters."""
+    _run(workloads, expected, 64, 2, raw=True)
+    _run(workloads, expected, 300, 1, raw=True)
+
+
 def test_synthetic_pyramids_equal_device_build(workloads):
     """The workload generator's numpy pyramid equals the bit-exact device
     build (so raw-image runs compare against the same oracle inputs)."""
