@@ -75,6 +75,7 @@ def lib():
         L.fto_median_i64.argtypes = [c_i64p, I64]
         L.fto_median_i64.restype = F64
         L.fto_num_threads_available.restype = INT
+        L.fto_build_pyramid.argtypes = [c_u8p, I64, c_i64p, c_i64p, c_i64p, c_u8p]
         _lib = L
     return _lib
 
@@ -400,6 +401,26 @@ def stereo_pinhole(left, right, left_pyr, right_pyr, cam, cfg, scale_pow,
     else:
         m = refine_match_phase2(left_pyr, right_pyr, left, right, idx, dist, cam, cfg, nthreads)
     return reject_outliers(m, cfg)
+
+
+def pyramid_level_dims(width: int, height: int, scale: float, levels: int):
+    """extraction.py:58-64: floor(dims / scale ** level)."""
+    powers = scale ** np.arange(levels, dtype=np.float64)
+    return (np.floor(width / powers).astype(np.int64), np.floor(height / powers).astype(np.int64))
+
+
+def build_pyramid(image, levels: int = 8, scale: float = 1.2):
+    """extraction.py:97-125 build_pyramid -> (data u8[total], offsets, widths,
+    heights), via fto_build_pyramid (kernels.py:230-268)."""
+    image = np.ascontiguousarray(image, dtype=np.uint8)
+    h, w = image.shape
+    ws, hs = pyramid_level_dims(w, h, scale, levels)
+    offsets = np.zeros(levels + 1, dtype=np.int64)
+    np.cumsum(ws * hs, out=offsets[1:])
+    data = np.zeros(int(offsets[-1]), dtype=np.uint8)
+    lib().fto_build_pyramid(_p(image, c_u8p), levels, _p(offsets, c_i64p), _p(ws, c_i64p),
+                            _p(hs, c_i64p), _p(data, c_u8p))
+    return data, offsets, ws, hs
 
 
 def _env_threads() -> int:

@@ -77,7 +77,9 @@ class FramePipeline:
         lay.add("rot", 72 * S)
         lay.add("trans", 24 * S)
         lay.add("slots_in", 8 * S * ck)
-        self.pyr_bytes = int(self.pyr.offsets[-1]) if self.pyr is not None else 0
+        # per-image pyramid stride padded to 256 B: 16-B vector copies of level 0
+        self.pyr_total = int(self.pyr.offsets[-1]) if self.pyr is not None else 0
+        self.pyr_bytes = (self.pyr_total + 255) // 256 * 256
         self.img_bytes = int(self.pyr.widths[0]) * int(self.pyr.heights[0]) if self.pyr is not None else 0
         if self.raw:
             lay.add("imgs", 2 * S * self.img_bytes)  # [left x S | right x S]
@@ -144,8 +146,8 @@ class FramePipeline:
             else:
                 pb = self.pyr_bytes
                 pyrs = self._h("pyrs", np.uint8, (2, S, pb))
-                pyrs[0, s] = pyr_left.data
-                pyrs[1, s] = pyr_right.data
+                pyrs[0, s, :self.pyr_total] = pyr_left.data
+                pyrs[1, s, :self.pyr_total] = pyr_right.data
         soa = local.soa
         m = len(local.point_ids)
         if m > cp:
