@@ -47,8 +47,10 @@ def parse() -> argparse.Namespace:
     p.add_argument("--frames", type=int, default=8, help="distinct frames cycled per stream")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-images", action="store_true", help="feature bundles only (no phase 2)")
-    p.add_argument("--ship-pyramids", action="store_true",
-                   help="upload full pyramids instead of raw images + device pyramid build")
+    p.add_argument("--raw-images", action="store_true",
+                   help="ship level-0 images and build the pyramids on the device "
+                        "(default: ship pyramids, the reference's phase-2 input)")
+    p.add_argument("--ship-pyramids", action="store_true", help=argparse.SUPPRESS)
     p.add_argument("--batched-streams", type=int, default=64,
                    help="extra batched measurement (0 disables)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -230,8 +232,8 @@ def run_reference(args) -> None:
 def config_dict(args) -> dict:
     if args.no_images:
         img = ", feature bundle (no phase 2)"
-    elif args.ship_pyramids:
-        img = ", rendered images shipped as pyramids -> SAD phase 2"
+    elif not args.raw_images:
+        img = ", rendered images shipped as pyramids (phase-2 input) -> SAD phase 2"
     else:
         img = (", rendered images shipped raw (0.36 MB each) -> device pyramid build "
                "(bit-exact build_pyramid) -> SAD phase 2")
@@ -269,7 +271,7 @@ def main() -> None:
     cap_kp = int(max(max(len(f.left.u), len(f.right.u)) for f in frames) + 31) // 32 * 32
     cap_pts = int(max(len(f.local.point_ids) for f in frames) + 255) // 256 * 256
     S = args.streams
-    raw = images and not args.ship_pyramids
+    raw = images and args.raw_images
     pipe = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
                          pyramid_geometry=w0.pyr_left if images else None, raw_images=raw)
 
@@ -406,6 +408,9 @@ def main() -> None:
         if args.batched_streams > 0 and world == 1:
             line["batched"] = batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts,
                                           images, flush)
+        if images and not raw and world == 1:
+            line["raw_images_mode"] = raw_mode_run(args, frames, torch, FramePipeline, cap_kp,
+                                                   cap_pts, flush)
         line["cpu_baseline"] = cpu_baseline(frames[:2], args.cpu_seconds)
     print(json.dumps(line))
     if dist:
@@ -449,12 +454,57 @@ def popc_peak(torch, _lib) -> float | None:
     return blocks * threads * iters * 8 / (ms / 1e3) / 1e9
 
 
+def raw_mode_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, flush) -> dict:
+    """The same single-stream step with raw level-0 images shipped and the
+    pyramids built on the device (ft_build_pyramids, SURVEY 8(f) #1)."""
+    w0 = frames[0]
+    pipe = FramePipeline(w0.cam, n_streams=1, cap_kp=cap_kp, cap_points=cap_pts,
+                         pyramid_geometry=w0.pyr_left, raw_images=True)
+    def load(k):
+        f = frames[k % len(frames)]
+        pipe.load_frame(0, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
+    load(0)
+    pipe.capture()
+    for k in range(3):
+        load(k)
+        pipe.replay(copies=True)
+    pipe.synchronize()
+    comp, e2e = [], []
+    for k in range(args.steps):
+        load(k)
+        with torch.cuda.stream(pipe.stream):
+            pipe.dev[:pipe.in_end].copy_(pipe.host[:pipe.in_end], non_blocking=True)
+            flush.fill_(1)
+            flush.view(torch.int64).sum()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(pipe.stream)
+        pipe.replay(copies=False)
+        b.record(pipe.stream)
+        pipe.synchronize()
+        comp.append(a.elapsed_time(b))
+    for k in range(args.steps):
+        load(k)
+        with torch.cuda.stream(pipe.stream):
+            flush.fill_(1)
+            flush.view(torch.int64).sum()
+        pipe.synchronize()
+        t0 = time.perf_counter()
+        pipe.replay(copies=True)
+        pipe.synchronize()
+        e2e.append(1e3 * (time.perf_counter() - t0))
+    return {"frames_per_s": args.steps / (sum(comp) / 1e3),
+            "ms_per_step": float(np.mean(comp)),
+            "e2e_frames_per_s": args.steps / (sum(e2e) / 1e3),
+            "e2e_ms_per_step": float(np.mean(e2e)),
+            "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes()}
+
+
 def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flush) -> dict:
     S = args.batched_streams
     w0 = frames[0]
     pipe = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
                          pyramid_geometry=w0.pyr_left if images else None,
-                         raw_images=images and not args.ship_pyramids)
+                         raw_images=images and args.raw_images)
     for s in range(S):
         f = frames[s % len(frames)]
         pipe.load_frame(s, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)

