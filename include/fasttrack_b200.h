@@ -35,6 +35,10 @@
  *                           (also tracker.py:415-427 _run_stereo, pinhole branch)
  *   ft_stereo_fisheye_bf    stereo.py:238-244       bruteforce_match_kernel as
  *                                                   launched by match_fisheye
+ *   ft_stereo_fisheye       stereo.py:223-273       match_fisheye: brute force +
+ *                                                   ray triangulation (cameras.py
+ *                                                   :139-157 unproject, stereo.py
+ *                                                   :200-220 closest points)
  *   ft_track_frames         tracker.py:279 + :354   stereo + SearchLocalPoints fused
  *   ft_build_pyramids       extraction.py:97-125    build_pyramid
  *   ft_project_search       projection.py:118-221   run_phase_a ->
@@ -254,6 +258,29 @@ int ft_stereo_pinhole(int32_t n_frames, const ft_keypoints *left, const ft_keypo
 int ft_stereo_fisheye_bf(int32_t n_frames, const ft_keypoints *left, const ft_keypoints *right,
                          int32_t t_match, double ratio, int64_t *out_idx, int64_t *out_dist,
                          const ft_workspace *ws, ft_stream_t stream);
+
+/* Fisheye triangulation terms (reference FisheyeCamera, cameras.py:100-157,
+ * and StereoMatchConfig.ray_gap_ceiling, stereo.py:32).  rot_lr / trans_lr
+ * = right_extrinsic.inverse() computed on the host (geometry.py:84-86). */
+typedef struct {
+    double fx, fy, cx, cy, k1, k2, k3, k4;
+    double rot_rl[9], trans_rl[3];   /* left -> right camera (right_extrinsic) */
+    double rot_lr[9], trans_lr[3];   /* right -> left camera */
+    double ray_gap_ceiling;
+    int32_t corrected;  /* 0: the reference's t at stereo.py:216 (its tracker's
+                           behaviour); 1: least-squares closest points */
+} ft_fisheye_tri;
+
+/* stereo.py:223-273 match_fisheye for F frames: brute force + ratio test as
+ * ft_stereo_fisheye_bf, then for every accepted pair the unproject / closest-
+ * point triangulation and its gap / positive-depth checks, in the same
+ * launch.  Per left keypoint: out_idx / out_dist (brute-force result),
+ * out_ok = 1 if the pair survived triangulation (a member of the reference's
+ * returned lists), out_points[3k..3k+2] = the left-frame point when ok. */
+int ft_stereo_fisheye(int32_t n_frames, const ft_keypoints *left, const ft_keypoints *right,
+                      int32_t t_match, double ratio, const ft_fisheye_tri *tri,
+                      int64_t *out_idx, int64_t *out_dist, int32_t *out_ok, double *out_points,
+                      const ft_workspace *ws, ft_stream_t stream);
 
 /* projection.py:118-221 + localmap.py:79-122. */
 int ft_project_search(int32_t n_frames, const ft_map_points *points, const ft_keypoints *frame,

@@ -262,6 +262,84 @@ def bruteforce(ldesc, rdesc, t_match: int, ratio: float,
     return idx, dist
 
 
+def fisheye_unproject(cam, u: float, v: float) -> np.ndarray:
+    """cameras.py:139-157 FisheyeCamera.unproject (Kannala-Brandt Newton
+    inversion), term for term."""
+    mx = (u - cam.cx) / cam.fx
+    my = (v - cam.cy) / cam.fy
+    rd = float(np.hypot(mx, my))
+    if rd < 1e-12:
+        return np.array([0.0, 0.0, 1.0])
+    theta = min(rd, np.pi / 2)
+    for _ in range(20):
+        t2 = theta * theta
+        f = theta * (1.0 + t2 * (cam.k1 + t2 * (cam.k2 + t2 * (cam.k3 + t2 * cam.k4)))) - rd
+        df = 1.0 + t2 * (3 * cam.k1 + t2 * (5 * cam.k2 + t2 * (7 * cam.k3 + t2 * 9 * cam.k4)))
+        step = f / df
+        theta -= step
+        if abs(step) < 1e-14:
+            break
+    s = np.sin(theta) / rd
+    ray = np.array([s * mx, s * my, np.cos(theta)])
+    return ray / np.linalg.norm(ray)
+
+
+def closest_ray_points(oa, da, ob, db, corrected: bool = False):
+    """stereo.py:200-220 _closest_ray_points.  corrected=False keeps the
+    reference's t = (a11 b2 - a12 b1) / den (stereo.py:216); corrected=True is
+    the least-squares t = (a12 b1 - a11 b2) / den."""
+    da = np.asarray(da, dtype=np.float64)
+    db = np.asarray(db, dtype=np.float64)
+    oa = np.asarray(oa, dtype=np.float64)
+    ob = np.asarray(ob, dtype=np.float64)
+    if np.linalg.norm(np.cross(da, db)) < 1e-9:
+        return None, None, None, None
+    r = ob - oa
+    a11 = da @ da
+    a12 = da @ db
+    a22 = db @ db
+    b1 = da @ r
+    b2 = db @ r
+    den = a11 * a22 - a12 * a12
+    s = (b1 * a22 - a12 * b2) / den
+    t = ((a12 * b1 - a11 * b2) if corrected else (a11 * b2 - a12 * b1)) / den
+    pa = oa + s * da
+    pb = ob + t * db
+    gap = float(np.linalg.norm(pa - pb))
+    return (pa + pb) / 2.0, gap, s, t
+
+
+def fisheye_triangulate(left, right, idx, dist, cam, ray_gap_ceiling: float,
+                        corrected: bool = False):
+    """stereo.py:245-273: triangulate the accepted brute-force pairs ->
+    (left_ids, right_ids, points, dists)."""
+    rot_rl = np.asarray(cam.right_extrinsic.rotation, dtype=np.float64)
+    tr_rl = np.asarray(cam.right_extrinsic.translation, dtype=np.float64)
+    rot_lr = rot_rl.T
+    tr_lr = -rot_lr @ tr_rl
+    left_ids, right_ids, points, dists = [], [], [], []
+    for i in np.nonzero(np.asarray(idx) >= 0)[0]:
+        j = int(idx[i])
+        ray_l = fisheye_unproject(cam, float(left.u[i]), float(left.v[i]))
+        ray_r = fisheye_unproject(cam, float(right.u[j]), float(right.v[j]))
+        dir_r = rot_lr @ ray_r
+        pt, gap, _, _ = closest_ray_points(np.zeros(3), ray_l, tr_lr, dir_r, corrected)
+        if pt is None or gap is None or gap > ray_gap_ceiling:
+            continue
+        p_right = rot_rl @ pt + tr_rl
+        if pt[2] <= 0 or p_right[2] <= 0:
+            continue
+        left_ids.append(int(i))
+        right_ids.append(j)
+        points.append(pt)
+        dists.append(int(dist[i]))
+    if not left_ids:
+        return (np.empty(0, dtype=np.int64), np.empty(0, dtype=np.int64), np.empty((0, 3)),
+                np.empty(0, dtype=np.int64))
+    return (np.asarray(left_ids, dtype=np.int64), np.asarray(right_ids, dtype=np.int64),
+            np.asarray(points), np.asarray(dists, dtype=np.int64))
+
+
 # ---------------------------------------------------------------------------
 # search by projection
 

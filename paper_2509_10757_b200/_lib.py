@@ -93,6 +93,13 @@ class FtProjectOut(ctypes.Structure):
                 ("slot_count", vp)]
 
 
+class FtFisheyeTri(ctypes.Structure):
+    _fields_ = [("fx", f64), ("fy", f64), ("cx", f64), ("cy", f64), ("k1", f64), ("k2", f64),
+                ("k3", f64), ("k4", f64), ("rot_rl", f64 * 9), ("trans_rl", f64 * 3),
+                ("rot_lr", f64 * 9), ("trans_lr", f64 * 3), ("ray_gap_ceiling", f64),
+                ("corrected", i32)]
+
+
 class FtError(RuntimeError):
     """A C-ABI call returned a non-zero status."""
 
@@ -102,7 +109,7 @@ _lib = None
 EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_workspace_init",
            "ft_hamming_pairs", "ft_stereo_pinhole", "ft_stereo_fisheye_bf", "ft_project_search",
            "ft_track_frames", "ft_resolve_conflicts", "ft_rotation_filter", "ft_bench_popc",
-           "ft_pack_keypoints", "ft_pack_points", "ft_build_pyramids")
+           "ft_pack_keypoints", "ft_pack_points", "ft_build_pyramids", "ft_stereo_fisheye")
 
 
 def build(force: bool = False) -> Path:
@@ -134,6 +141,8 @@ def load() -> ctypes.CDLL:
                                     P(FtPyramid), P(FtStereoParams), i32, P(FtStereoOut), W, vp]
     L.ft_stereo_fisheye_bf.argtypes = [i32, P(FtKeypoints), P(FtKeypoints), i32, f64, vp, vp,
                                        W, vp]
+    L.ft_stereo_fisheye.argtypes = [i32, P(FtKeypoints), P(FtKeypoints), i32, f64,
+                                    P(FtFisheyeTri), vp, vp, vp, vp, W, vp]
     L.ft_project_search.argtypes = [i32, P(FtMapPoints), P(FtKeypoints), P(FtProjectParams),
                                     P(FtProjectIO), i32, P(FtProjectOut), W, vp]
     L.ft_track_frames.argtypes = [i32, P(FtKeypoints), P(FtKeypoints), P(FtPyramid),

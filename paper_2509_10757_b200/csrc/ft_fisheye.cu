@@ -13,6 +13,8 @@
 //   associative and commutative, so the result is the reference's
 //   ascending-j scan -- and applies the ratio test.  On rejection dist = best
 //   (kernels.py:462-464).
+#include <cstring>
+
 #include "ft_common.cuh"
 #include "ft_ws.cuh"
 
@@ -31,7 +33,77 @@ struct BfArgs {
     unsigned *counters;  // [F][tiles]
     int32_t splits;
     int32_t split_len;   // right descriptors per split (of cap)
+    int32_t tri_on;      // ft_stereo_fisheye: triangulate accepted pairs
+    ft_fisheye_tri tri;
+    int32_t *out_ok;
+    double *out_points;
 };
+
+// cameras.py:139-157 FisheyeCamera.unproject: unit ray through (u, v),
+// Newton inversion of the Kannala-Brandt radial polynomial (<= 20 steps,
+// stop when |step| < 1e-14), in the reference's evaluation order.
+FT_DEV void kb_unproject(const ft_fisheye_tri &c, double u, double v, double r[3]) {
+    const double mx = (u - c.cx) / c.fx, my = (v - c.cy) / c.fy;
+    const double rd = hypot(mx, my);
+    if (rd < 1e-12) {
+        r[0] = 0.0;
+        r[1] = 0.0;
+        r[2] = 1.0;
+        return;
+    }
+    const double half_pi = 1.5707963267948966;
+    double theta = rd < half_pi ? rd : half_pi;
+    for (int it = 0; it < 20; ++it) {
+        const double t2 = theta * theta;
+        const double f = theta * (1.0 + t2 * (c.k1 + t2 * (c.k2 + t2 * (c.k3 + t2 * c.k4)))) - rd;
+        const double df =
+            1.0 + t2 * (3 * c.k1 + t2 * (5 * c.k2 + t2 * (7 * c.k3 + t2 * 9 * c.k4)));
+        const double step = f / df;
+        theta -= step;
+        if (fabs(step) < 1e-14) break;
+    }
+    const double s = sin(theta) / rd;
+    const double x = s * mx, y = s * my, z = cos(theta);
+    const double n = sqrt(x * x + y * y + z * z);
+    r[0] = x / n;
+    r[1] = y / n;
+    r[2] = z / n;
+}
+
+FT_DEV double dot3(const double a[3], const double b[3]) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+
+// stereo.py:245-268 for one accepted pair: returns true and the left-frame
+// point when the pair survives the parallel / gap / depth checks.
+FT_DEV bool fisheye_triangulate(const ft_fisheye_tri &c, double ul, double vl, double ur,
+                                double vr, double pt[3]) {
+    double da[3], rr[3], db[3];
+    kb_unproject(c, ul, vl, da);
+    kb_unproject(c, ur, vr, rr);
+    for (int k = 0; k < 3; ++k)  // dir_r = T_lr.rotation @ ray_r
+        db[k] = c.rot_lr[3 * k] * rr[0] + c.rot_lr[3 * k + 1] * rr[1] + c.rot_lr[3 * k + 2] * rr[2];
+    // _closest_ray_points(0, da, trans_lr, db) (stereo.py:200-220)
+    const double cx = da[1] * db[2] - da[2] * db[1], cy = da[2] * db[0] - da[0] * db[2],
+                 cz = da[0] * db[1] - da[1] * db[0];
+    if (sqrt(cx * cx + cy * cy + cz * cz) < 1e-9) return false;
+    const double *ob = c.trans_lr;
+    const double a11 = dot3(da, da), a12 = dot3(da, db), a22 = dot3(db, db);
+    const double b1 = dot3(da, ob), b2 = dot3(db, ob);  // r = ob - oa = ob
+    const double den = a11 * a22 - a12 * a12;
+    const double s = (b1 * a22 - a12 * b2) / den;
+    const double t = (c.corrected ? (a12 * b1 - a11 * b2) : (a11 * b2 - a12 * b1)) / den;
+    double pa[3], pb[3];
+    for (int k = 0; k < 3; ++k) {
+        pa[k] = 0.0 + s * da[k];
+        pb[k] = ob[k] + t * db[k];
+    }
+    const double gx = pa[0] - pb[0], gy = pa[1] - pb[1], gz = pa[2] - pb[2];
+    const double gap = sqrt(gx * gx + gy * gy + gz * gz);
+    if (gap > c.ray_gap_ceiling) return false;
+    for (int k = 0; k < 3; ++k) pt[k] = (pa[k] + pb[k]) / 2.0;
+    if (pt[2] <= 0) return false;
+    const double zr = c.rot_rl[6] * pt[0] + c.rot_rl[7] * pt[1] + c.rot_rl[8] * pt[2] + c.trans_rl[2];
+    return zr > 0;
+}
 
 __global__ void __launch_bounds__(BF_TL) fisheye_bf_kernel(const BfArgs a) {
     __shared__ uint4 rdesc[BF_CHUNK][2];
@@ -77,17 +149,39 @@ __global__ void __launch_bounds__(BF_TL) fisheye_bf_kernel(const BfArgs a) {
     if (k >= n_left) return;
     Best2 m;
     best2_init(m);
-    for (int s = 0; s < a.splits; ++s) {
-        const uint2 p = __ldcg(a.partials + ((int64_t)f * a.splits + s) * a.L.cap + k);
-        best2_merge(m, p.x, p.y);
+    // issue the partial loads in groups of 8 before merging (independent L2
+    // round trips overlap instead of serialising on the merge chain)
+    const uint2 *pp = a.partials + (int64_t)f * a.splits * a.L.cap + k;
+    for (int s0 = 0; s0 < a.splits; s0 += 8) {
+        uint2 p[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            p[u] = s0 + u < a.splits ? __ldcg(pp + (int64_t)(s0 + u) * a.L.cap)
+                                     : make_uint2(NO_KEY, NO_SECOND);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) best2_merge(m, p[u].x, p[u].y);
     }
     const int64_t lk = lbase + k;
-    if (ratio_accept(m, a.t_match, a.ratio)) {
+    const bool acc = ratio_accept(m, a.t_match, a.ratio);
+    if (acc) {
         a.out_idx[lk] = m.key & 0xffffu;
         a.out_dist[lk] = m.key >> 16;
     } else {
         a.out_idx[lk] = -1;
         a.out_dist[lk] = key_dist(m.key);
+    }
+    if (a.tri_on) {  // stereo.py:245-268 for the accepted pair
+        double pt[3] = {0.0, 0.0, 0.0};
+        bool ok = false;
+        if (acc) {
+            const ft_kp_record &kl = a.L.rec[lk];
+            const ft_kp_record &kr = a.R.rec[rbase + (m.key & 0xffffu)];
+            ok = fisheye_triangulate(a.tri, kl.u, kl.v, kr.u, kr.v, pt);
+        }
+        a.out_ok[lk] = ok ? 1 : 0;
+        a.out_points[3 * lk] = ok ? pt[0] : 0.0;
+        a.out_points[3 * lk + 1] = ok ? pt[1] : 0.0;
+        a.out_points[3 * lk + 2] = ok ? pt[2] : 0.0;
     }
 }
 
@@ -95,24 +189,30 @@ __global__ void __launch_bounds__(BF_TL) fisheye_bf_kernel(const BfArgs a) {
 
 using namespace ft;
 
-extern "C" int ft_stereo_fisheye_bf(int32_t n_frames, const ft_keypoints *left,
-                                    const ft_keypoints *right, int32_t t_match, double ratio,
-                                    int64_t *out_idx, int64_t *out_dist, const ft_workspace *ws,
-                                    ft_stream_t stream) {
+static int fisheye_launch(int32_t n_frames, const ft_keypoints *left, const ft_keypoints *right,
+                          int32_t t_match, double ratio, const ft_fisheye_tri *tri,
+                          int64_t *out_idx, int64_t *out_dist, int32_t *out_ok,
+                          double *out_points, const ft_workspace *ws, ft_stream_t stream) {
     if (!left || !right || !out_idx || !out_dist || !ws || !left->rec || !right->rec)
         return FT_E_NULL;
+    if (tri && (!out_ok || !out_points)) return FT_E_NULL;
     if (n_frames < 1 || left->cap < 1 || right->cap < 1 || left->cap > 65535 ||
         right->cap > 65535)
         return FT_E_RANGE;
     const int wst = ws_check(ws, n_frames, left->cap > right->cap ? left->cap : right->cap, 1);
     if (wst != FT_OK) return wst;
     BfArgs a;
+    memset(&a, 0, sizeof(a));
     a.L = *left;
     a.R = *right;
     a.t_match = t_match;
     a.ratio = ratio;
     a.out_idx = out_idx;
     a.out_dist = out_dist;
+    a.tri_on = tri != nullptr;
+    if (tri) a.tri = *tri;
+    a.out_ok = out_ok;
+    a.out_points = out_points;
     const int tiles = (left->cap + BF_TL - 1) / BF_TL;
     const WsLayout wl = ws_layout(ws);
     int splits = fisheye_splits(n_frames, left->cap, right->cap);
@@ -126,4 +226,23 @@ extern "C" int ft_stereo_fisheye_bf(int32_t n_frames, const ft_keypoints *left,
     dim3 grid(tiles, a.splits, n_frames);
     fisheye_bf_kernel<<<grid, BF_TL, 0, (cudaStream_t)stream>>>(a);
     return (int)cudaGetLastError();
+}
+
+extern "C" int ft_stereo_fisheye_bf(int32_t n_frames, const ft_keypoints *left,
+                                    const ft_keypoints *right, int32_t t_match, double ratio,
+                                    int64_t *out_idx, int64_t *out_dist, const ft_workspace *ws,
+                                    ft_stream_t stream) {
+    return fisheye_launch(n_frames, left, right, t_match, ratio, nullptr, out_idx, out_dist,
+                          nullptr, nullptr, ws, stream);
+}
+
+extern "C" int ft_stereo_fisheye(int32_t n_frames, const ft_keypoints *left,
+                                 const ft_keypoints *right, int32_t t_match, double ratio,
+                                 const ft_fisheye_tri *tri, int64_t *out_idx, int64_t *out_dist,
+                                 int32_t *out_ok, double *out_points, const ft_workspace *ws,
+                                 ft_stream_t stream) {
+    if (!tri) return FT_E_NULL;
+    if (!(tri->fx != 0.0 && tri->fy != 0.0)) return FT_E_CONFIG;
+    return fisheye_launch(n_frames, left, right, t_match, ratio, tri, out_idx, out_dist, out_ok,
+                          out_points, ws, stream);
 }

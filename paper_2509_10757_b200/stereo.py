@@ -240,8 +240,29 @@ def _closest_ray_points(oa, da, ob, db):
     return (pa + pb) / 2.0, gap, s, t
 
 
-def fisheye_bruteforce(left, right, cfg: StereoMatchConfig) -> tuple[np.ndarray, np.ndarray]:
-    """kernels.py:434-464 over all left keypoints on the device: (idx, dist)."""
+def fisheye_tri_params(cam, cfg: StereoMatchConfig, corrected: bool = False) -> _lib.FtFisheyeTri:
+    """ft_fisheye_tri from a FisheyeCamera (cameras.py:100-157) and the config;
+    the right->left transform is right_extrinsic.inverse() as the reference
+    computes it (geometry.py:84-86, stereo.py:247)."""
+    t = _lib.FtFisheyeTri()
+    for k in ("fx", "fy", "cx", "cy", "k1", "k2", "k3", "k4"):
+        setattr(t, k, float(getattr(cam, k)))
+    rot_rl = np.asarray(cam.right_extrinsic.rotation, dtype=np.float64)
+    tr_rl = np.asarray(cam.right_extrinsic.translation, dtype=np.float64)
+    rot_lr = rot_rl.T
+    tr_lr = -rot_lr @ tr_rl
+    t.rot_rl[:] = [float(x) for x in rot_rl.reshape(9)]
+    t.trans_rl[:] = [float(x) for x in tr_rl]
+    t.rot_lr[:] = [float(x) for x in np.ascontiguousarray(rot_lr).reshape(9)]
+    t.trans_lr[:] = [float(x) for x in tr_lr]
+    t.ray_gap_ceiling = float(cfg.ray_gap_ceiling)
+    t.corrected = 1 if corrected else 0
+    return t
+
+
+def _fisheye_device(left, right, cfg: StereoMatchConfig, tri):
+    """One ft_stereo_fisheye_bf (tri None) or ft_stereo_fisheye launch for a
+    frame -> (idx, dist[, ok, points])."""
     rt = runtime()
     n, nr = len(left.u), len(right.u)
     cap, _ = rt.caps(max(n, nr))
@@ -251,6 +272,8 @@ def fisheye_bruteforce(left, right, cfg: StereoMatchConfig) -> tuple[np.ndarray,
     in_end = lay.total
     lay.add("idx", 8 * cap)
     lay.add("dist", 8 * cap)
+    lay.add("ok", 4 * cap)
+    lay.add("pts", 24 * cap)
     with rt.lock:
         rt.reserve(lay.total)
         put_keypoints(rt, lay, "L", left)
@@ -259,58 +282,58 @@ def fisheye_bruteforce(left, right, cfg: StereoMatchConfig) -> tuple[np.ndarray,
         ws = rt.workspace()
         kl = keypoints_struct(rt, lay, "L", cap)
         kr = keypoints_struct(rt, lay, "R", cap)
-        st = rt.lib.ft_stereo_fisheye_bf(1, kl, kr, int(cfg.t_match), float(cfg.ratio),
-                                         rt.ptr(lay, "idx"), rt.ptr(lay, "dist"), ws,
-                                         rt.stream.cuda_stream)
-        _lib.check(st, "ft_stereo_fisheye_bf")
+        if tri is None:
+            st = rt.lib.ft_stereo_fisheye_bf(1, kl, kr, int(cfg.t_match), float(cfg.ratio),
+                                             rt.ptr(lay, "idx"), rt.ptr(lay, "dist"), ws,
+                                             rt.stream.cuda_stream)
+        else:
+            st = rt.lib.ft_stereo_fisheye(1, kl, kr, int(cfg.t_match), float(cfg.ratio), tri,
+                                          rt.ptr(lay, "idx"), rt.ptr(lay, "dist"),
+                                          rt.ptr(lay, "ok"), rt.ptr(lay, "pts"), ws,
+                                          rt.stream.cuda_stream)
+        _lib.check(st, "ft_stereo_fisheye_bf" if tri is None else "ft_stereo_fisheye")
         rt.d2h(lay.offsets["idx"], lay.total)
         rt.sync()
         idx = rt.host_view(lay, "idx", np.int64, (n,)).copy()
         dist = rt.host_view(lay, "dist", np.int64, (n,)).copy()
-    return idx, dist
+        if tri is None:
+            return idx, dist
+        ok = rt.host_view(lay, "ok", np.int32, (n,)).copy()
+        pts = rt.host_view(lay, "pts", np.float64, (n, 3)).copy()
+    return idx, dist, ok, pts
 
 
-def match_fisheye(left, right, cam, cfg: StereoMatchConfig, engine=None
+def fisheye_bruteforce(left, right, cfg: StereoMatchConfig) -> tuple[np.ndarray, np.ndarray]:
+    """kernels.py:434-464 over all left keypoints on the device: (idx, dist)."""
+    return _fisheye_device(left, right, cfg, None)
+
+
+def match_fisheye(left, right, cam, cfg: StereoMatchConfig, engine=None, corrected: bool = False
                   ) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
     """Brute-force fisheye matching plus ray-midpoint triangulation
-    (reference stereo.py:223-273).  The all-pairs matching runs on the B200;
-    the per-accepted-pair triangulation is the reference's host loop."""
+    (reference stereo.py:223-273), both on the B200 in one launch
+    (ft_stereo_fisheye).  corrected=False reproduces the reference's closest-
+    point solve including the sign of t at stereo.py:216 (its tracker's
+    behaviour); corrected=True uses the least-squares solution."""
     n = len(left.u)
     empty = (np.empty(0, dtype=np.int64), np.empty(0, dtype=np.int64), np.empty((0, 3)),
              np.empty(0, dtype=np.int64))
     if n == 0 or len(right.u) == 0:
         return empty
-    idx, dist = fisheye_bruteforce(left, right, cfg)
-    t_rl = cam.right_extrinsic
-    t_lr = t_rl.inverse()
-    left_ids, right_ids, points, dists = [], [], [], []
-    for i in np.nonzero(idx >= 0)[0]:
-        j = int(idx[i])
-        ray_l = cam.unproject(float(left.u[i]), float(left.v[i]))
-        ray_r = cam.unproject(float(right.u[j]), float(right.v[j]))
-        dir_r = t_lr.rotation @ ray_r
-        pt, gap, _, _ = _closest_ray_points(np.zeros(3), ray_l, t_lr.translation, dir_r)
-        if pt is None or gap is None or gap > cfg.ray_gap_ceiling:
-            continue
-        p_right = t_rl.transform(pt)
-        if pt[2] <= 0 or p_right[2] <= 0:
-            continue
-        left_ids.append(int(i))
-        right_ids.append(j)
-        points.append(pt)
-        dists.append(int(dist[i]))
-    if not left_ids:
+    idx, dist, ok, pts = _fisheye_device(left, right, cfg,
+                                         fisheye_tri_params(cam, cfg, corrected))
+    keep = np.nonzero(ok)[0]
+    if len(keep) == 0:
         return empty
-    return (np.asarray(left_ids, dtype=np.int64), np.asarray(right_ids, dtype=np.int64),
-            np.asarray(points), np.asarray(dists, dtype=np.int64))
+    return keep.astype(np.int64), idx[keep], pts[keep], dist[keep]
 
 
-def compute_stereo_fisheye_matches(left, right, cam, cfg: StereoMatchConfig | None = None
-                                   ) -> StereoMatches:
+def compute_stereo_fisheye_matches(left, right, cam, cfg: StereoMatchConfig | None = None,
+                                   corrected: bool = False) -> StereoMatches:
     """ORB-SLAM ComputeStereoFishEyeMatches: the reference tracker's fisheye
     ``_run_stereo`` branch (tracker.py:399-414) -> per-left StereoMatches."""
     cfg = cfg or StereoMatchConfig()
-    lidx, ridx, points, dists = match_fisheye(left, right, cam, cfg)
+    lidx, ridx, points, dists = match_fisheye(left, right, cam, cfg, corrected=corrected)
     n = len(left.u)
     out = StereoMatches(right_idx=np.full(n, -1, dtype=np.int64),
                         distance=np.full(n, 10000, dtype=np.int64), disparity=np.zeros(n),

@@ -140,7 +140,10 @@ def test_cfg3_fisheye():
     lidx, ridx, pts3, dists = ft.match_fisheye(left, right, cam, cfg)
     np.testing.assert_array_equal(lidx, d["mf_lidx"])
     np.testing.assert_array_equal(ridx, d["mf_ridx"])
-    np.testing.assert_array_equal(pts3, d["mf_pts"])
+    # device unproject / closest points (CUDA sin, cos, hypot, sqrt) vs the
+    # reference's numpy + glibc: accepted sets exact, points within 1e-12 rel
+    np.testing.assert_allclose(pts3, d["mf_pts"], rtol=1e-12, atol=1e-15)
+    np.testing.assert_array_equal(dists, d["mf_dists"])
     pcfg = ProjectionSearchConfig()
     pts, pose = G.soa(d), G.pose(d)
     frame = make_frame(left, right, cam, pose)
@@ -368,3 +371,26 @@ def test_device_pyramid_batched_vs_oracle(oracle, shape, levels, n_images):
     for i in range(n_ref, n_images, 37):  # spot-check the later chunks
         np.testing.assert_array_equal(got[i], oracle.build_pyramid(imgs[i], levels, 1.2)[0],
                                       err_msg=f"image {i}")
+
+
+@pytest.mark.parametrize("corrected", [False, True])
+def test_fisheye_triangulation_vs_oracle(oracle, corrected):
+    """ft_stereo_fisheye (brute force + unproject + closest points + checks in
+    one launch) vs the oracle's restatement of stereo.py:245-273, in the
+    reference's mode (its t sign, stereo.py:216) and the corrected
+    least-squares mode (1397 triangulated pairs on cfg3)."""
+    d = G.load("cfg3_fisheye.npz")
+    left, right = G.feats(d, "left"), G.feats(d, "right")
+    cfg, cam = StereoMatchConfig(), G.fisheye()
+    got = ft.match_fisheye(left, right, cam, cfg, corrected=corrected)
+    ref = oracle.fisheye_triangulate(left, right, d["bf_idx"], d["bf_dist"], cam,
+                                     cfg.ray_gap_ceiling, corrected)
+    for a, b, name in zip(got, ref, ("left_ids", "right_ids", "points", "dists")):
+        if name == "points":
+            np.testing.assert_allclose(a, b, rtol=1e-9, atol=1e-12, err_msg=name)
+        else:
+            np.testing.assert_array_equal(a, b, err_msg=name)
+    if corrected:
+        assert len(got[0]) > 1000
+        m = ft.compute_stereo_fisheye_matches(left, right, cam, cfg, corrected=True)
+        np.testing.assert_allclose(m.depth[got[0]], got[2][:, 2], rtol=0, atol=0)
