@@ -51,6 +51,9 @@ def parse() -> argparse.Namespace:
                    help="ship level-0 images and build the pyramids on the device "
                         "(default: ship pyramids, the reference's phase-2 input)")
     p.add_argument("--ship-pyramids", action="store_true", help=argparse.SUPPRESS)
+    p.add_argument("--no-map-table", action="store_true",
+                   help="ship every frame's local-map records instead of table slots into "
+                        "the resident map table")
     p.add_argument("--batched-streams", type=int, default=64,
                    help="extra batched measurement (0 disables)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -62,9 +65,23 @@ def parse() -> argparse.Namespace:
 # workload
 
 def make_frames(n: int, seed0: int, images: bool):
+    """n independent cfg2 frames (distinct worlds: map point ids offset per
+    frame so they can share one resident map table)."""
     from paper_2509_10757_b200.synthetic import make_workload
     return [make_workload(seed=seed0 + i, n_landmarks=12000, map_points=5000, images=images,
-                          offset=0.05 * i) for i in range(n)]
+                          offset=0.05 * i, id_base=100_000 * (i + 1)) for i in range(n)]
+
+
+def make_table(args, frames, cap_pts, S=1):
+    """Resident map table holding every frame's local map (uploaded once,
+    before timing); None with --no-map-table."""
+    if args.no_map_table:
+        return None, 0
+    from paper_2509_10757_b200.maptable import MapTable
+    table = MapTable(capacity=max(len(frames), S) * cap_pts + 1024)
+    for f in frames:
+        table.upsert(f.local.point_ids, f.local.soa, only_missing=True)
+    return table, table.bytes_uploaded
 
 
 def algorithmic_units(w) -> dict:
@@ -237,9 +254,11 @@ def config_dict(args) -> dict:
     else:
         img = (", rendered images shipped raw (0.36 MB each) -> device pyramid build "
                "(bit-exact build_pyramid) -> SAD phase 2")
+    mp = ("5000-point local map shipped as records every frame" if args.no_map_table else
+          "5000-point local map resident in the device map table (frames ship 4-B slots; "
+          "ft_gather_points)")
     return {"workload": "cfg2: EuRoC-shaped stereo frame 752x480 (~1270 kps/image, 8 levels, "
-                        "scale 1.2" + img +
-                        ") + 5000-point local map; stereo + SearchLocalPoints per frame",
+                        "scale 1.2" + img + ") + " + mp + "; stereo + SearchLocalPoints per frame",
             "streams_per_gpu": args.streams, "frames_cycled": args.frames,
             "l2": "flushed before every timed step (256 MiB write, then read back)",
             "parallelism": f"independent frame streams x {args.gpus} GPU (no collective)"}
@@ -272,8 +291,10 @@ def main() -> None:
     cap_pts = int(max(len(f.local.point_ids) for f in frames) + 255) // 256 * 256
     S = args.streams
     raw = images and args.raw_images
+    table, table_bytes = make_table(args, frames, cap_pts)
     pipe = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
-                         pyramid_geometry=w0.pyr_left if images else None, raw_images=raw)
+                         pyramid_geometry=w0.pyr_left if images else None, raw_images=raw,
+                         map_table=table)
 
     def load(step: int) -> None:
         for s in range(S):
@@ -322,6 +343,7 @@ def main() -> None:
         torch.cuda.synchronize()
         # ---- e2e: pinned host inputs -> H2D -> compute -> D2H, host wall clock
         e2e_ms, e2e_ev_ms = [], []
+        delta0 = pipe.delta_bytes
         for k in range(args.steps):
             load(k)
             l2_flush()
@@ -334,6 +356,23 @@ def main() -> None:
             pipe.synchronize()
             e2e_ms.append(1e3 * (time.perf_counter() - t0))
             e2e_ev_ms.append(a.elapsed_time(b))
+        e2e_delta = pipe.delta_bytes - delta0
+        # ---- e2e, overlapped: AsyncRunner (H2D of k+1 / compute of k / D2H of
+        # k-1 concurrently), inputs pre-staged in pinned memory per frame
+        runner, staged = make_runner(args, frames, pipe, table, load)
+        if dist:
+            dist.barrier()
+        for k in range(2):
+            runner.submit(k, staged[k % len(staged)])
+        runner.synchronize()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            if k >= 2:
+                runner.wait(k - 2)
+            runner.submit(k, staged[k % len(staged)])
+        runner.wait(args.steps - 1)
+        runner.wait(args.steps - 2)
+        async_ms = 1e3 * (time.perf_counter() - t0)
         if dist:
             dist.barrier()
     clocks = clk.summary()
@@ -358,12 +397,13 @@ def main() -> None:
     tot_comp = sum(comp_ms)
     tot_e2e = sum(e2e_ms)
     if dist:
-        t = torch.tensor([tot_comp, tot_e2e], dtype=torch.float64, device="cuda")
+        t = torch.tensor([tot_comp, tot_e2e, async_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_comp, tot_e2e = float(t[0]), float(t[1])
+        tot_comp, tot_e2e, async_ms = float(t[0]), float(t[1]), float(t[2])
     frames_total = world * S * args.steps
     value = frames_total / (tot_comp / 1e3)
-    e2e_value = frames_total / (tot_e2e / 1e3)
+    e2e_serial = frames_total / (tot_e2e / 1e3)
+    e2e_value = frames_total / (async_ms / 1e3)
 
     if rank != 0:
         if dist:
@@ -389,7 +429,15 @@ def main() -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64+u32", "data": "synthetic", "config": config_dict(args),
             "e2e": {"value": e2e_value, "unit": "frames/s",
-                    "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes(),
+                    "method": "AsyncRunner: per step H2D of that step's inputs from pinned host "
+                              "memory, compute, D2H of its results; copies of neighbouring "
+                              "steps overlap the compute (host wall clock over all steps)",
+                    "serial_value": e2e_serial,
+                    "h2d_bytes_per_step": pipe.h2d_bytes() + e2e_delta // max(1, args.steps),
+                    "d2h_bytes_per_step": pipe.d2h_bytes(),
+                    "map_table": None if table is None else {
+                        "resident_points": table.size, "upload_bytes_once": table_bytes,
+                        "delta_bytes_per_step": e2e_delta / max(1, args.steps)},
                     "ms_per_step_wall": tot_e2e / args.steps,
                     "ms_per_step_events": float(np.sum(e2e_ev_ms)) / args.steps},
             "roofline": roofline,
@@ -403,7 +451,8 @@ def main() -> None:
                            "stereo_only": float(np.median(kern["stereo_only"])),
                            "map_only": float(np.median(kern["map_only"]))},
             "work_per_frame": units, "clocks": clocks,
-            "gpu_launches": (2 + 2 * raw) * args.steps, "parity_spot_check": check}
+            "gpu_launches": 2 * (1 + int(raw) + int(table is not None)) * args.steps,
+            "parity_spot_check": check}
     if not args.quick:
         if args.batched_streams > 0 and world == 1:
             line["batched"] = batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts,
@@ -454,12 +503,27 @@ def popc_peak(torch, _lib) -> float | None:
     return blocks * threads * iters * 8 / (ms / 1e3) / 1e9
 
 
+def make_runner(args, frames, pipe, table, load):
+    """A second pipeline of the same shape + AsyncRunner, and every cycled
+    frame's inputs pre-staged in pinned host memory (one tensor per step)."""
+    from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
+    twin = FramePipeline(pipe.cam, n_streams=pipe.S, cap_kp=pipe.cap_kp, cap_points=pipe.cap_pts,
+                         pyramid_geometry=pipe.pyr, raw_images=pipe.raw, map_table=table)
+    staged = []
+    for k in range(len(frames)):
+        load(k)
+        staged.append(pipe.staged_inputs())
+    twin.capture()
+    return AsyncRunner([pipe, twin]), staged
+
+
 def raw_mode_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, flush) -> dict:
     """The same single-stream step with raw level-0 images shipped and the
     pyramids built on the device (ft_build_pyramids, SURVEY 8(f) #1)."""
     w0 = frames[0]
+    table, _ = make_table(args, frames, cap_pts)
     pipe = FramePipeline(w0.cam, n_streams=1, cap_kp=cap_kp, cap_points=cap_pts,
-                         pyramid_geometry=w0.pyr_left, raw_images=True)
+                         pyramid_geometry=w0.pyr_left, raw_images=True, map_table=table)
     def load(k):
         f = frames[k % len(frames)]
         pipe.load_frame(0, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
@@ -502,9 +566,10 @@ def raw_mode_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, flush) -> 
 def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flush) -> dict:
     S = args.batched_streams
     w0 = frames[0]
+    table, _ = make_table(args, frames, cap_pts, S)
     pipe = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
                          pyramid_geometry=w0.pyr_left if images else None,
-                         raw_images=images and args.raw_images)
+                         raw_images=images and args.raw_images, map_table=table)
     for s in range(S):
         f = frames[s % len(frames)]
         pipe.load_frame(s, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)

@@ -41,6 +41,8 @@
  *                                                   :200-220 closest points)
  *   ft_track_frames         tracker.py:279 + :354   stereo + SearchLocalPoints fused
  *   ft_build_pyramids       extraction.py:97-125    build_pyramid
+ *   ft_gather_points /      mapping.py:204-235      decompose_map_points (per-frame
+ *   ft_scatter_points                               local map from a resident table)
  *   ft_project_search       projection.py:118-221   run_phase_a ->
  *                                                   resolve_conflicts ->
  *                                                   rotation_consistency_filter
@@ -243,6 +245,21 @@ int ft_pack_points(int32_t n_frames, const double *positions, const double *norm
                    const double *min_dist, const double *max_dist, const uint64_t *desc,
                    const int64_t *point_ids, const int32_t *count, int32_t cap,
                    ft_point_record *out, ft_stream_t stream);
+
+/* Device-resident map-point table (north star (1)): the reference rebuilds a
+ * frame's LocalMap SoA on the host every frame (mapping.py:204-235,
+ * localmap.py:22-39); here every point record lives once in `table` and a
+ * frame names its local map as table slots in LocalMap order.
+ * ft_gather_points: out[f*cap + i] = table[index[f*cap + i]] for i < count[f]
+ *   (the ft_map_points input of ft_track_frames / ft_project_search); an
+ *   out-of-range slot sets *status (DEVICE, may be NULL) to FT_E_RANGE.
+ * ft_scatter_points: table[slots[i]] = recs[i] -- upload new / changed points
+ *   (the per-frame map delta). */
+int ft_gather_points(int32_t n_frames, const ft_point_record *table, int64_t table_size,
+                     const int32_t *index, const int32_t *count, int32_t cap,
+                     ft_point_record *out, int32_t *status, ft_stream_t stream);
+int ft_scatter_points(int32_t n, const ft_point_record *recs, const int32_t *slots,
+                      ft_point_record *table, int64_t table_size, ft_stream_t stream);
 
 /* kernels.py:48-51: out[i] = popcount(a[i] ^ b[i]) over 256 bits. */
 int ft_hamming_pairs(const uint64_t *a, const uint64_t *b, int64_t n, int64_t *out,

@@ -109,7 +109,8 @@ _lib = None
 EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_workspace_init",
            "ft_hamming_pairs", "ft_stereo_pinhole", "ft_stereo_fisheye_bf", "ft_project_search",
            "ft_track_frames", "ft_resolve_conflicts", "ft_rotation_filter", "ft_bench_popc",
-           "ft_pack_keypoints", "ft_pack_points", "ft_build_pyramids", "ft_stereo_fisheye")
+           "ft_pack_keypoints", "ft_pack_points", "ft_build_pyramids", "ft_stereo_fisheye",
+           "ft_gather_points", "ft_scatter_points")
 
 
 def build(force: bool = False) -> Path:
@@ -143,6 +144,8 @@ def load() -> ctypes.CDLL:
                                        W, vp]
     L.ft_stereo_fisheye.argtypes = [i32, P(FtKeypoints), P(FtKeypoints), i32, f64,
                                     P(FtFisheyeTri), vp, vp, vp, vp, W, vp]
+    L.ft_gather_points.argtypes = [i32, vp, i64, vp, vp, i32, vp, vp, vp]
+    L.ft_scatter_points.argtypes = [i32, vp, vp, vp, i64, vp]
     L.ft_project_search.argtypes = [i32, P(FtMapPoints), P(FtKeypoints), P(FtProjectParams),
                                     P(FtProjectIO), i32, P(FtProjectOut), W, vp]
     L.ft_track_frames.argtypes = [i32, P(FtKeypoints), P(FtKeypoints), P(FtPyramid),

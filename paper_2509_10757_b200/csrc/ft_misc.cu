@@ -263,3 +263,82 @@ extern "C" int ft_pack_points(int32_t n_frames, const double *positions, const d
                                                              count, cap, out);
     return (int)cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// Device-resident map-point table (north star (1): the map stays in HBM and
+// only pose + map-point deltas cross PCIe).  The reference rebuilds each
+// frame's LocalMap SoA on the host (mapping.py:204-235 decompose_map_points,
+// localmap.py:22-39); here the table holds every point record once, frames
+// name their local map as a list of table slots (in LocalMap order), and
+// ft_gather_points builds the per-frame contiguous record table the track
+// kernel stages with one bulk copy.  One 16-B vector per lane: a warp moves
+// 4.5 records per instruction.
+
+namespace {
+constexpr int PT_VEC = sizeof(ft_point_record) / 16;  // 7 x uint4
+static_assert(sizeof(ft_point_record) % 16 == 0, "record must be uint4-sized");
+
+__global__ void gather_pt_kernel(int32_t n_frames, const uint4 *table, int64_t table_size,
+                                 const int32_t *index, const int32_t *count, int32_t cap,
+                                 uint4 *out, int32_t *status) {
+    const int64_t total = (int64_t)n_frames * cap * PT_VEC;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t rec = e / PT_VEC;
+        const int w = (int)(e - rec * PT_VEC);
+        const int f = (int)(rec / cap), i = (int)(rec - (int64_t)f * cap);
+        if (i >= min(count[f], cap)) continue;
+        const int32_t slot = __ldg(index + rec);
+        if (slot < 0 || slot >= table_size) {  // caller error: flag it, write a dead record
+            if (status) atomicExch(status, FT_E_RANGE);
+            continue;
+        }
+        out[e] = __ldg(table + (int64_t)slot * PT_VEC + w);
+    }
+}
+
+__global__ void scatter_pt_kernel(int32_t n, const uint4 *recs, const int32_t *slots,
+                                  uint4 *table, int64_t table_size) {
+    const int64_t total = (int64_t)n * PT_VEC;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / PT_VEC;
+        const int32_t slot = slots[r];
+        if (slot < 0 || slot >= table_size) continue;
+        table[(int64_t)slot * PT_VEC + (e - r * PT_VEC)] = recs[e];
+    }
+}
+}  // namespace
+
+extern "C" int ft_gather_points(int32_t n_frames, const ft_point_record *table,
+                                int64_t table_size, const int32_t *index, const int32_t *count,
+                                int32_t cap, ft_point_record *out, int32_t *status,
+                                ft_stream_t stream) {
+    if (!table || !index || !count || !out) return FT_E_NULL;
+    if (n_frames < 1 || cap < 1 || table_size < 1) return FT_E_RANGE;
+    if ((((uintptr_t)table) | ((uintptr_t)out)) & 15) return FT_E_RANGE;
+    const int64_t total = (int64_t)n_frames * cap * PT_VEC;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (total + 255) / 256;
+    const int blocks = (int)(want < 4 * sms ? want : 4 * sms);
+    gather_pt_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        n_frames, reinterpret_cast<const uint4 *>(table), table_size, index, count, cap,
+        reinterpret_cast<uint4 *>(out), status);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int ft_scatter_points(int32_t n, const ft_point_record *recs, const int32_t *slots,
+                                 ft_point_record *table, int64_t table_size, ft_stream_t stream) {
+    if (n == 0) return FT_OK;
+    if (!recs || !slots || !table) return FT_E_NULL;
+    if (n < 0 || table_size < 1) return FT_E_RANGE;
+    if ((((uintptr_t)table) | ((uintptr_t)recs)) & 15) return FT_E_RANGE;
+    const int64_t total = (int64_t)n * PT_VEC;
+    const int blocks = (int)((total + 255) / 256 < 1024 ? (total + 255) / 256 : 1024);
+    scatter_pt_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        n, reinterpret_cast<const uint4 *>(recs), slots, reinterpret_cast<uint4 *>(table),
+        table_size);
+    return (int)cudaGetLastError();
+}

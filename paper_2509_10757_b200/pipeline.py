@@ -44,7 +44,7 @@ class FramePipeline:
                  pyramid_geometry=None, stereo_cfg: StereoMatchConfig | None = None,
                  proj_cfg: ProjectionSearchConfig | None = None, scale: float = 1.2,
                  levels: int = 8, grid_cell_px: int = 48, device: int | None = None,
-                 raw_images: bool = False):
+                 raw_images: bool = False, map_table=None):
         if not torch.cuda.is_available():
             raise _lib.FtError("FramePipeline needs a CUDA device (no CPU fallback)")
         self.lib = _lib.load()
@@ -60,6 +60,10 @@ class FramePipeline:
         self.pyr = pyramid_geometry  # object with widths / heights / offsets, or None
         # raw_images: frames ship level 0 only; ft_build_pyramids builds the rest
         self.raw = bool(raw_images) and pyramid_geometry is not None
+        # map_table (maptable.MapTable): frames ship table slots (4 B / point)
+        # instead of point records; ft_gather_points builds the per-frame table
+        self.table = map_table
+        self.delta_bytes = 0
         self.cell = int(grid_cell_px)
         self.nx = max(1, (int(cam.width) + self.cell - 1) // self.cell)
         self.ny = max(1, (int(cam.height) + self.cell - 1) // self.cell)
@@ -73,7 +77,10 @@ class FramePipeline:
             lay.add(f"{side}_n", 4 * S)
             lay.add(f"{side}_rec", _lib.KP_RECORD.itemsize * S * ck)
         lay.add("P_n", 4 * S)
-        lay.add("P_rec", _lib.POINT_RECORD.itemsize * S * cp)
+        if self.table is None:
+            lay.add("P_rec", _lib.POINT_RECORD.itemsize * S * cp)
+        else:
+            lay.add("P_idx", 4 * S * cp)
         lay.add("rot", 72 * S)
         lay.add("trans", 24 * S)
         lay.add("slots_in", 8 * S * ck)
@@ -96,6 +103,9 @@ class FramePipeline:
         self.out_end = lay.total
         if self.raw:  # device-built pyramids: not copied
             lay.add("pyrs", 2 * S * self.pyr_bytes)
+        if self.table is not None:  # gathered from the resident table: not copied
+            lay.add("P_rec", _lib.POINT_RECORD.itemsize * S * cp)
+            lay.add("gather_status", 4)
         # device-only scratch (not copied)
         lay.add("cand_idx", 8 * S * ck)
         lay.add("cand_dist", 8 * S * ck)
@@ -153,7 +163,12 @@ class FramePipeline:
         if m > cp:
             raise ValueError(f"{m} map points exceed capacity {cp}")
         self._h("P_n", np.int32, (S,))[s] = m
-        fill_point_records(self._h("P_rec", _lib.POINT_RECORD, (S, cp))[s], soa)
+        if self.table is None:
+            fill_point_records(self._h("P_rec", _lib.POINT_RECORD, (S, cp))[s], soa)
+        else:
+            # points new to the table are the frame's map delta (uploaded now)
+            self.delta_bytes += self.table.upsert(local.point_ids, soa, only_missing=True)
+            self._h("P_idx", np.int32, (S, cp))[s, :m] = self.table.slots(local.point_ids)
         self._h("rot", np.float64, (S, 9))[s] = np.asarray(pose.rotation).reshape(9)
         self._h("trans", np.float64, (S, 3))[s] = np.asarray(pose.translation).reshape(3)
         sl = self._h("slots_in", np.int64, (S, ck))
@@ -231,11 +246,19 @@ class FramePipeline:
                                                   self.img_bytes, self.ws, stream.cuda_stream),
                        "ft_build_pyramids")
 
+    def launch_gather(self, stream) -> None:
+        if self.table is not None:
+            _lib.check(self.lib.ft_gather_points(self.S, self.table.ptr, self.table.capacity,
+                                                 self._d("P_idx"), self._d("P_n"), self.cap_pts,
+                                                 self._d("P_rec"), self._d("gather_status"),
+                                                 stream.cuda_stream), "ft_gather_points")
+
     def _step(self, copies: bool) -> None:
         a = self.stream
         if copies:
             with torch.cuda.stream(a):
                 self.dev[:self.in_end].copy_(self.host[:self.in_end], non_blocking=True)
+        self.launch_gather(a)
         self.launch_pyramids(a)
         self.launch_track(a)
         if copies:
@@ -280,3 +303,72 @@ class FramePipeline:
         return StreamResult(matches=m, slots=g("slots", np.int64),
                             n_slots=int(self._h("slot_n", np.int32, (S,))[s]),
                             n_matched=int(self._h("n_matched", np.int32, (S,))[s]))
+
+    def staged_inputs(self) -> torch.Tensor:
+        """A pinned copy of the current input staging (what load_frame wrote):
+        one step's inputs, ready for AsyncRunner.submit."""
+        return self.host[:self.in_end].clone().pin_memory()
+
+
+class AsyncRunner:
+    """Copy / compute overlapped driver for a stream of steps (the real-time
+    shape of the tracker: the next frame's images and keypoints upload while
+    the current one tracks).  Two FramePipelines of identical shape take
+    alternate steps; per step k:
+
+        H2D stream:     inputs(k)          -> pipe[k % 2] device inputs
+        compute stream: gather / pyramids / ft_track_frames (graph replay)
+        D2H stream:     pipe[k % 2] outputs -> its pinned result area
+
+    Compute is serialised on one stream (one cooperative launch at a time);
+    H2D of step k+1 and D2H of step k-1 run on the two copy engines while
+    step k computes.  Events order buffer reuse: step k's H2D waits for step
+    k-2's compute, step k's compute for step k-2's D2H.  ``wait(k)`` blocks
+    until step k's results are in ``pipes[k % 2]`` host memory."""
+
+    def __init__(self, pipes):
+        if len(pipes) != 2:
+            raise ValueError("AsyncRunner takes two identically shaped FramePipelines")
+        a, b = pipes
+        if (a.S, a.cap_kp, a.cap_pts, a.in_end, a.out_begin, a.out_end) != \
+                (b.S, b.cap_kp, b.cap_pts, b.in_end, b.out_begin, b.out_end):
+            raise ValueError("AsyncRunner pipelines differ in shape")
+        self.pipes = pipes
+        dev = a.device
+        self.h2d = torch.cuda.Stream(dev)
+        self.comp = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self.ev = [{k: torch.cuda.Event() for k in ("h2d", "comp", "d2h")} for _ in pipes]
+        for p in pipes:
+            if p.graph_compute is None:
+                p.capture()
+
+    def submit(self, k: int, inputs: torch.Tensor | None = None) -> None:
+        """Enqueue step k; inputs = a pinned tensor in the pipelines' input
+        layout (staged_inputs()), or None to send pipes[k % 2]'s own staging."""
+        i = k % 2
+        p, e = self.pipes[i], self.ev[i]
+        src = p.host[:p.in_end] if inputs is None else inputs
+        self.h2d.wait_event(e["comp"])  # step k-2 no longer reads the inputs
+        with torch.cuda.stream(self.h2d):
+            p.dev[:p.in_end].copy_(src, non_blocking=True)
+            e["h2d"].record(self.h2d)
+        self.comp.wait_event(e["h2d"])
+        self.comp.wait_event(e["d2h"])  # step k-2's outputs are out
+        with torch.cuda.stream(self.comp):
+            p.graph_compute.replay()
+            e["comp"].record(self.comp)
+        self.d2h.wait_event(e["comp"])
+        with torch.cuda.stream(self.d2h):
+            p.host[p.out_begin:p.out_end].copy_(p.dev[p.out_begin:p.out_end], non_blocking=True)
+            e["d2h"].record(self.d2h)
+
+    def wait(self, k: int) -> FramePipeline:
+        """Block until step k's results are on the host; returns its pipeline
+        (read them with .result(s, n_left))."""
+        self.ev[k % 2]["d2h"].synchronize()
+        return self.pipes[k % 2]
+
+    def synchronize(self) -> None:
+        for s in (self.h2d, self.comp, self.d2h):
+            s.synchronize()

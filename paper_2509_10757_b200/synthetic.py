@@ -182,9 +182,10 @@ class Workload:
 
 def make_workload(seed: int = 0, n_landmarks: int = 12000, map_points: int = 5000,
                   images: bool = False, fisheye: bool = False, noise_px: float = 0.5,
-                  offset: float = 0.0) -> Workload:
+                  offset: float = 0.0, id_base: int = 0) -> Workload:
     """One frame + local map.  ``offset`` slides the camera along the shell
-    axis so consecutive frames of a stream differ."""
+    axis so consecutive frames of a stream differ; ``id_base`` is added to the
+    map point ids (distinct worlds sharing one resident map table)."""
     rng = np.random.default_rng(seed)
     cam = tumvi_camera() if fisheye else euroc_camera()
     a = rng.uniform(0, 2 * math.pi, n_landmarks)
@@ -217,7 +218,7 @@ def make_workload(seed: int = 0, n_landmarks: int = 12000, map_points: int = 500
     max_d = d * SCALE ** octs
     soa = MapPointSoA(positions=pos.copy(), descriptors=_flip(desc[ids], rng, 8),
                       normals=(pos - center) / d[:, None], min_distances=max_d / SCALE ** (LEVELS - 1),
-                      max_distances=max_d, point_ids=ids.astype(np.int64))
+                      max_distances=max_d, point_ids=ids.astype(np.int64) + int(id_base))
     local = LocalMap((0,), soa.point_ids.copy(), soa)
     pert = _rot_axis(np.array([0.3, -0.5, 0.2]), 0.002)
     query = Pose(pert @ pose_left.rotation, pose_left.translation + np.array([0.01, 0.0, -0.01]))

@@ -18,7 +18,7 @@ def workloads():
         pytest.skip("no CUDA device")
     from paper_2509_10757_b200.synthetic import make_workload
     return [make_workload(seed=100 + i, n_landmarks=12000, map_points=5000, images=True,
-                          offset=0.05 * i) for i in range(4)]
+                          offset=0.05 * i, id_base=100_000 * i) for i in range(4)]
 
 
 @pytest.fixture(scope="module")
@@ -41,14 +41,14 @@ def expected(workloads, oracle):
     return out
 
 
-def _run(workloads, expected, n_streams, replays, raw=False):
+def _run(workloads, expected, n_streams, replays, raw=False, table=None):
     from paper_2509_10757_b200.pipeline import FramePipeline
     w0 = workloads[0]
     cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
     cap_pts = max(len(w.local.point_ids) for w in workloads)
     pipe = FramePipeline(w0.cam, n_streams=n_streams, cap_kp=(cap_kp + 31) // 32 * 32,
                          cap_points=(cap_pts + 255) // 256 * 256, pyramid_geometry=w0.pyr_left,
-                         raw_images=raw)
+                         raw_images=raw, map_table=table)
     for s in range(n_streams):
         w = workloads[s % len(workloads)]
         pipe.load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
@@ -103,3 +103,97 @@ def test_synthetic_pyramids_equal_device_build(workloads):
     got = build_pyramid(w.pyr_left.data[:h * wd].reshape(h, wd),
                         SimpleNamespace(levels=8, scale=1.2, patch_size=31))
     np.testing.assert_array_equal(got.data, w.pyr_left.data)
+
+
+def test_resident_map_table(workloads, expected):
+    """Frames ship table slots; ft_gather_points rebuilds each frame's local
+    map from the resident table (same order -> same tie-breaks)."""
+    from paper_2509_10757_b200.maptable import MapTable
+    table = MapTable(capacity=64 * 1024)
+    _run(workloads, expected, 4, 2, table=table)
+    first = table.bytes_uploaded
+    assert first > 0
+    _run(workloads, expected, 8, 2, table=table)  # all points resident: no delta
+    assert table.bytes_uploaded == first
+
+
+def test_map_table_slots_and_update(workloads):
+    import torch
+    from paper_2509_10757_b200 import _lib
+    from paper_2509_10757_b200.maptable import MapTable
+    w = workloads[0]
+    t = MapTable(capacity=16384)
+    t.upsert(w.local.point_ids, w.local.soa)
+    s = t.slots(w.local.point_ids)
+    assert len(set(s.tolist())) == len(s)
+    rec = t.table.cpu().numpy().view(_lib.POINT_RECORD)
+    np.testing.assert_array_equal(rec["id"][s], w.local.point_ids)
+    np.testing.assert_array_equal(rec["pos"][s], w.local.soa.positions)
+    # overwrite one point (a map update) and read it back through the gather
+    soa2 = type(w.local.soa)(**{k: np.array(getattr(w.local.soa, k)) for k in
+                                ("positions", "descriptors", "normals", "min_distances",
+                                 "max_distances", "point_ids")})
+    soa2.positions[3] += 1.0
+    t.upsert(w.local.point_ids[3:4], _Rows(soa2, [3]))
+    out = torch.zeros(len(s) * 112, dtype=torch.uint8, device="cuda")
+    idx = torch.from_numpy(s).cuda()
+    cnt = torch.tensor([len(s)], dtype=torch.int32, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    L = _lib.load()
+    _lib.check(L.ft_gather_points(1, t.ptr, t.capacity, idx.data_ptr(), cnt.data_ptr(), len(s),
+                                  out.data_ptr(), st.data_ptr(), None), "gather")
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(_lib.POINT_RECORD)
+    np.testing.assert_array_equal(got["pos"][3], soa2.positions[3])
+    np.testing.assert_array_equal(got["pos"][4], w.local.soa.positions[4])
+    assert int(st.item()) == 0
+    with pytest.raises(KeyError):
+        t.slots(np.array([10 ** 12]))
+
+
+class _Rows:
+    def __init__(self, soa, rows):
+        for k in ("positions", "descriptors", "normals", "min_distances", "max_distances",
+                  "point_ids"):
+            setattr(self, k, np.asarray(getattr(soa, k))[rows])
+
+
+def test_async_runner_overlapped_steps(workloads, expected):
+    """AsyncRunner: H2D of step k+1 / compute of k / D2H of k-1 overlapped on
+    two pipelines; every step's results equal the oracle's."""
+    from paper_2509_10757_b200.maptable import MapTable
+    from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    table = MapTable(capacity=32 * 1024)
+    pipes = [FramePipeline(w0.cam, n_streams=2, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left, map_table=table)
+             for _ in range(2)]
+    staged = []
+    for k in range(4):  # step k: streams carry workloads k and k+1
+        p = pipes[k % 2]
+        for s in range(2):
+            w = workloads[(k + s) % 4]
+            p.load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                         slots=expected[(k + s) % 4][1])
+        staged.append(p.staged_inputs())
+    runner = AsyncRunner(pipes)
+    n_steps = 10
+    for k in range(n_steps):
+        if k >= 2:
+            _check_step(runner.wait(k - 2), workloads, expected, k - 2)
+        runner.submit(k, staged[k % 4])
+    for k in (n_steps - 2, n_steps - 1):
+        _check_step(runner.wait(k), workloads, expected, k)
+
+
+def _check_step(pipe, workloads, expected, k):
+    for s in range(2):
+        w = workloads[(k % 4 + s) % 4]
+        m, _, slots, n = expected[(k % 4 + s) % 4]
+        res = pipe.result(s, len(w.left.u))
+        for f in FIELDS:
+            np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f),
+                                          err_msg=f"step {k} stream {s} {f}")
+        np.testing.assert_array_equal(res.slots, slots, err_msg=f"step {k} stream {s}")
+        assert res.n_slots == n
