@@ -255,8 +255,8 @@ def config_dict(args) -> dict:
         img = (", rendered images shipped raw (0.36 MB each) -> device pyramid build "
                "(bit-exact build_pyramid) -> SAD phase 2")
     mp = ("5000-point local map shipped as records every frame" if args.no_map_table else
-          "5000-point local map resident in the device map table (frames ship 4-B slots; "
-          "ft_gather_points)")
+          "5000-point local map resident in the device map table (frames ship 4-B slots, "
+          "read in place by the map role)")
     return {"workload": "cfg2: EuRoC-shaped stereo frame 752x480 (~1270 kps/image, 8 levels, "
                         "scale 1.2" + img + ") + " + mp + "; stereo + SearchLocalPoints per frame",
             "streams_per_gpu": args.streams, "frames_cycled": args.frames,
@@ -396,14 +396,12 @@ def main() -> None:
 
     tot_comp = sum(comp_ms)
     tot_e2e = sum(e2e_ms)
-    if dist:
-        t = torch.tensor([tot_comp, tot_e2e, async_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_comp, tot_e2e, async_ms = float(t[0]), float(t[1]), float(t[2])
-    frames_total = world * S * args.steps
-    value = frames_total / (tot_comp / 1e3)
-    e2e_serial = frames_total / (tot_e2e / 1e3)
-    e2e_value = frames_total / (async_ms / 1e3)
+    from paper_2509_10757_b200.sharding import job_frames_per_s, max_over_ranks
+    tot_comp, tot_e2e, async_ms = max_over_ranks([tot_comp, tot_e2e, async_ms], dist,
+                                                 device="cuda")
+    value = job_frames_per_s(S * args.steps, world, tot_comp)
+    e2e_serial = job_frames_per_s(S * args.steps, world, tot_e2e)
+    e2e_value = job_frames_per_s(S * args.steps, world, async_ms)
 
     if rank != 0:
         if dist:
@@ -451,12 +449,15 @@ def main() -> None:
                            "stereo_only": float(np.median(kern["stereo_only"])),
                            "map_only": float(np.median(kern["map_only"]))},
             "work_per_frame": units, "clocks": clocks,
-            "gpu_launches": 2 * (1 + int(raw) + int(table is not None)) * args.steps,
+            "gpu_launches": 2 * (1 + int(raw)) * args.steps,
             "parity_spot_check": check}
     if not args.quick:
         if args.batched_streams > 0 and world == 1:
             line["batched"] = batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts,
                                           images, flush)
+            if images and not raw:
+                line["batched_raw_images"] = batched_run(args, frames, torch, FramePipeline,
+                                                         cap_kp, cap_pts, images, flush, True)
         if images and not raw and world == 1:
             line["raw_images_mode"] = raw_mode_run(args, frames, torch, FramePipeline, cap_kp,
                                                    cap_pts, flush)
@@ -563,22 +564,29 @@ def raw_mode_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, flush) -> 
             "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes()}
 
 
-def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flush) -> dict:
+def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flush,
+                raw: bool | None = None) -> dict:
+    """S frame streams per launch on this GPU (one frame of every stream per
+    step): device-resident throughput, and e2e through AsyncRunner."""
+    from paper_2509_10757_b200.pipeline import AsyncRunner
     S = args.batched_streams
     w0 = frames[0]
+    raw = (images and args.raw_images) if raw is None else raw
     table, _ = make_table(args, frames, cap_pts, S)
-    pipe = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
-                         pyramid_geometry=w0.pyr_left if images else None,
-                         raw_images=images and args.raw_images, map_table=table)
+    pipes = [FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
+                           pyramid_geometry=w0.pyr_left if images else None, raw_images=raw,
+                           map_table=table) for _ in range(2)]
+    pipe = pipes[0]
     for s in range(S):
         f = frames[s % len(frames)]
         pipe.load_frame(s, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
+    staged = pipe.staged_inputs()
     pipe.capture()
     steps = max(5, args.steps // 5)
     for _ in range(3):
         pipe.replay(copies=True)
     pipe.synchronize()
-    comp, e2e = [], []
+    comp = []
     for _ in range(steps):
         with torch.cuda.stream(pipe.stream):
             flush.fill_(1)
@@ -589,19 +597,23 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
         b.record(pipe.stream)
         pipe.synchronize()
         comp.append(a.elapsed_time(b))
-        with torch.cuda.stream(pipe.stream):
-            flush.fill_(1)
-            flush.view(torch.int64).sum()
-        pipe.synchronize()
-        t0 = time.perf_counter()
-        pipe.replay(copies=True)
-        pipe.synchronize()
-        e2e.append(1e3 * (time.perf_counter() - t0))
-    return {"streams": S, "steps": steps, "ms_per_step": float(np.mean(comp)),
+    runner = AsyncRunner(pipes)
+    for k in range(2):
+        runner.submit(k, staged)
+    runner.synchronize()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        if k >= 2:
+            runner.wait(k - 2)
+        runner.submit(k, staged)
+    runner.wait(steps - 1)
+    runner.wait(steps - 2)
+    e2e_ms = 1e3 * (time.perf_counter() - t0)
+    return {"streams": S, "steps": steps, "raw_images": bool(raw),
+            "ms_per_step": float(np.mean(comp)),
             "frames_per_s": S * steps / (sum(comp) / 1e3),
-            "e2e_frames_per_s": S * steps / (sum(e2e) / 1e3),
+            "e2e_frames_per_s": S * steps / (e2e_ms / 1e3),
             "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes()}
-
 
 if __name__ == "__main__":
     main()

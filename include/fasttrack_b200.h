@@ -159,11 +159,15 @@ typedef struct {
     int64_t pad;
 } ft_point_record;
 
-/* Map points of F local maps at stride `cap` records. */
+/* Map points of F local maps at stride `cap` records.  With `index` NULL,
+ * point i of frame f is rec[f*cap + i]; otherwise rec is a resident map
+ * table (ft_gather_points) and point i of frame f is rec[index[f*cap + i]]
+ * -- read in place, no per-frame copy. */
 typedef struct {
-    const ft_point_record *rec;  /* [F*cap] */
+    const ft_point_record *rec;  /* [F*cap], or the table */
     const int32_t *count;        /* DEVICE [F] */
     int32_t cap;
+    const int32_t *index;        /* DEVICE [F*cap] table slots, or NULL */
 } ft_map_points;
 
 /* reference projection.py:26-45 ProjectionSearchConfig + camera + grid. */

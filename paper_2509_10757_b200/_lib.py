@@ -59,7 +59,7 @@ class FtStereoOut(ctypes.Structure):
 
 
 class FtMapPoints(ctypes.Structure):
-    _fields_ = [("rec", vp), ("count", vp), ("cap", i32)]
+    _fields_ = [("rec", vp), ("count", vp), ("cap", i32), ("index", vp)]
 
 
 # numpy views of the packed records (include/fasttrack_b200.h)

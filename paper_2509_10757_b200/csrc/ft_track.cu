@@ -838,6 +838,18 @@ FT_DEV void stage_points(const TrackArgs &a, const MapSmem &sm, int64_t pbase, i
     if (bytes) bulk_g2s(sm.prnd, a.P.rec + pbase + q0, bytes, mbar);
 }
 
+// Resident-table variant: points [q0, q1) gathered through the slot index
+// into the round buffer by all threads (16-B loads; visible after the
+// caller's next __syncthreads).
+FT_DEV void gather_points(const TrackArgs &a, const MapSmem &sm, const int32_t *pidx, int q0,
+                          int q1) {
+    uint4 *dst = reinterpret_cast<uint4 *>(sm.prnd);
+    for (int t = threadIdx.x; t < 7 * (q1 - q0); t += TK_THREADS) {
+        const int r = t / 7;
+        dst[t] = __ldg(reinterpret_cast<const uint4 *>(a.P.rec + __ldg(pidx + q0 + r)) + (t - 7 * r));
+    }
+}
+
 __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigned char *smem,
                           unsigned long long *mbar, unsigned &mphase) {
     const int G = a.Gm;
@@ -899,17 +911,28 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     // mode) use TMA.
     const int n0 = have_pts ? min(p1, p0 + round_cap) - p0 : 0;
     const bool pre_regs = have_pts && 7 * n0 <= 2 * TK_THREADS;
+    // resident map table: point i of the frame is P.rec[pidx[i]] (gathered
+    // by the threads; no TMA stream, no per-frame copy)
+    const int32_t *pidx = a.P.index ? a.P.index + pbase : nullptr;
     uint4 pre[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
     if (pre_regs) {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.P.rec + pbase + p0);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             const int t = threadIdx.x + q * TK_THREADS;
-            if (t < 7 * n0)
+            if (t < 7 * n0) {
+                const uint4 *s = src + t;
+                if (pidx) {
+                    const int r = t / 7;
+                    s = reinterpret_cast<const uint4 *>(a.P.rec + __ldg(pidx + p0 + r)) + (t - 7 * r);
+                }
                 asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(pre[q].x), "=r"(pre[q].y), "=r"(pre[q].z), "=r"(pre[q].w)
-                             : "l"(src + t));
+                             : "l"(s));
+            }
         }
+    } else if (pidx && have_pts) {
+        gather_points(a, sm, pidx, p0, min(p1, p0 + round_cap));
     }
     if (threadIdx.x < 32) {  // translate every page the block touches later, now
         const int l = threadIdx.x;
@@ -929,7 +952,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
         mbar_arrive_expect_tx(mbar, bt + bsl);
         if (bt) bulk_g2s(sm.ktab_s, a.K.rec + kbase, bt, mbar);
         if (bsl) bulk_g2s(sm.kslots, a.io.slots_in + kbase, bsl, mbar);
-        if (!pre_regs) stage_points(a, sm, pbase, p0, min(p1, p0 + round_cap), mbar + 1);
+        if (!pre_regs && !pidx) stage_points(a, sm, pbase, p0, min(p1, p0 + round_cap), mbar + 1);
     }
     // launch epoch (same for every block of this slot's frame instance)
     unsigned long long ticket = 0;
@@ -993,13 +1016,15 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             const int r1 = min(p1, r0 + round_cap);
             if (r0 != p0) {  // later rounds (batched mode): stage this round's points
                 __syncthreads();
-                if (threadIdx.x == 0) {
+                if (pidx) {
+                    gather_points(a, sm, pidx, r0, r1);
+                } else if (threadIdx.x == 0) {
                     fence_proxy_async_smem();
                     stage_points(a, sm, pbase, r0, r1, mbar + 1);
                 }
             }
             if (threadIdx.x == 0) sm.misc[1] = 0;
-            if (r0 != p0 || !pre_regs) {
+            if (!pidx && (r0 != p0 || !pre_regs)) {
                 mbar_wait(mbar + 1, (mphase >> 1) & 1u);  // bit 1: phase of mbar[1]
                 mphase ^= 2u;
             }

@@ -61,7 +61,7 @@ class FramePipeline:
         # raw_images: frames ship level 0 only; ft_build_pyramids builds the rest
         self.raw = bool(raw_images) and pyramid_geometry is not None
         # map_table (maptable.MapTable): frames ship table slots (4 B / point)
-        # instead of point records; ft_gather_points builds the per-frame table
+        # instead of point records; the map role reads the table in place
         self.table = map_table
         self.delta_bytes = 0
         self.cell = int(grid_cell_px)
@@ -103,9 +103,7 @@ class FramePipeline:
         self.out_end = lay.total
         if self.raw:  # device-built pyramids: not copied
             lay.add("pyrs", 2 * S * self.pyr_bytes)
-        if self.table is not None:  # gathered from the resident table: not copied
-            lay.add("P_rec", _lib.POINT_RECORD.itemsize * S * cp)
-            lay.add("gather_status", 4)
+
         # device-only scratch (not copied)
         lay.add("cand_idx", 8 * S * ck)
         lay.add("cand_dist", 8 * S * ck)
@@ -208,7 +206,10 @@ class FramePipeline:
             setattr(o, name, self._d(name))
         self.sout = o
         P = _lib.FtMapPoints()
-        P.rec, P.count, P.cap = self._d("P_rec"), self._d("P_n"), cp
+        if self.table is None:
+            P.rec, P.count, P.cap, P.index = self._d("P_rec"), self._d("P_n"), cp, None
+        else:  # read in place from the resident table through the slot list
+            P.rec, P.count, P.cap, P.index = self.table.ptr, self._d("P_n"), cp, self._d("P_idx")
         self.points = P
         self.pparams = project_params(self.cam, self.pcfg, self.scale, self.levels, self.cell,
                                       self.nx, self.ny, None, 0.0)
@@ -246,19 +247,11 @@ class FramePipeline:
                                                   self.img_bytes, self.ws, stream.cuda_stream),
                        "ft_build_pyramids")
 
-    def launch_gather(self, stream) -> None:
-        if self.table is not None:
-            _lib.check(self.lib.ft_gather_points(self.S, self.table.ptr, self.table.capacity,
-                                                 self._d("P_idx"), self._d("P_n"), self.cap_pts,
-                                                 self._d("P_rec"), self._d("gather_status"),
-                                                 stream.cuda_stream), "ft_gather_points")
-
     def _step(self, copies: bool) -> None:
         a = self.stream
         if copies:
             with torch.cuda.stream(a):
                 self.dev[:self.in_end].copy_(self.host[:self.in_end], non_blocking=True)
-        self.launch_gather(a)
         self.launch_pyramids(a)
         self.launch_track(a)
         if copies:
