@@ -415,9 +415,15 @@ def main() -> None:
     achieved = dom_bytes / (track_ms / 1e3) / 1e9
     popc = popc_peak(torch, _lib)
     ham = S * (units["hamming_phase1"] + units["hamming_projection"])
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists() and S == 1:  # ncu --set full DRAM bytes of this kernel, this config
+        t = json.loads(tf.read_text()).get("ft_track_frames", {})
+        if "dram_bytes_read_per_launch" in t:
+            traffic = t["dram_bytes_read_per_launch"] + t.get("dram_bytes_write_per_launch", 0)
     roofline = {"bound": "hbm", "kernel": "ft_track_frames", "achieved": achieved,
                 "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": None, "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+                "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)", "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
                 "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": track_ms,
                 "note": "one frame per launch is latency-bound (dependent L2/HBM round trips "
                         "and group barriers); see roofline_int and batched"}
