@@ -265,6 +265,21 @@ int ft_gather_points(int32_t n_frames, const ft_point_record *table, int64_t tab
 int ft_scatter_points(int32_t n, const ft_point_record *recs, const int32_t *slots,
                       ft_point_record *table, int64_t table_size, ft_stream_t stream);
 
+/* Native double-buffered step executor (csrc/ft_runner.cu): per step k, on
+ * three streams, H2D of host_in into slot k % 2's device inputs, a launch of
+ * that slot's instantiated compute graph (cudaGraphExec_t, captured by the
+ * caller), and D2H of its outputs into the slot's pinned host range.
+ * Neighbouring steps' copies overlap the compute; computes are serialised.
+ * ft_runner_wait(k) blocks until step k's outputs are on the host.  Slot
+ * buffers are reused two steps later (the runner orders that itself). */
+typedef struct ft_runner ft_runner;
+int ft_runner_create(const void *const graph_exec[2], void *const dev_in[2], size_t in_bytes,
+                     void *const dev_out[2], void *const host_out[2], size_t out_bytes,
+                     ft_runner **out);
+int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in);
+int ft_runner_wait(ft_runner *r, int64_t k);
+int ft_runner_destroy(ft_runner *r);
+
 /* kernels.py:48-51: out[i] = popcount(a[i] ^ b[i]) over 256 bits. */
 int ft_hamming_pairs(const uint64_t *a, const uint64_t *b, int64_t n, int64_t *out,
                      ft_stream_t stream);

@@ -157,8 +157,21 @@ inline void pyr_axis_tables(int first, int last, int T, const int32_t *dims, con
 
 __host__ __device__ inline size_t pyr_al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
+// Everything one level of one tile needs, copied out of the (large) kernel
+// parameter tables into shared memory once per tile by parallel loads: the
+// constant cache does not hold the tables, and dependent misses at every
+// phase would serialise the block.
+struct PyrLevelDesc {
+    PyrRect reg, own, src;        // computed region, own rectangle, source region
+    int slo, shi, clo, chi;       // smoothed span sampled (kernels.py:255-264)
+    int hs, ws, wd, pad;          // source dims, destination width (stride)
+    long long off_dst, off_src;   // level byte offsets in the image's pyramid
+    double sy, sx;
+};
+
 // Shared-memory layout of one block (host sizing and device carving agree).
 struct PyrSmem {
+    PyrLevelDesc *desc;  // [FT_MAX_LEVELS]
     uint8_t *reg[2];    // ping-pong u8 regions
     uint2 *hsum;        // packed horizontal sums
     float *smooth;      // smoothed pixels (u8 values, exact in fp32)
@@ -170,12 +183,13 @@ struct PyrSmem {
 };
 
 __host__ __device__ inline size_t pyr_layout(const PyrPlan &p, unsigned char *base, PyrSmem *S) {
-    size_t o = 0, off[9];
+    size_t o = 0, off[10];
     off[0] = o; o += pyr_al16((size_t)p.cap_region + 32);
     off[1] = o; o += pyr_al16((size_t)p.cap_region + 32);
     off[2] = o; o += pyr_al16((size_t)p.cap_hsum * 8);
     off[3] = o; o += pyr_al16((size_t)p.cap_smooth * 4);
     off[8] = o; o += pyr_al16((size_t)p.cap_h * 8);
+    off[9] = o; o += pyr_al16(sizeof(PyrLevelDesc) * FT_MAX_LEVELS);
     off[4] = o; o += pyr_al16((size_t)p.cap_rows * 16);
     off[5] = o; o += pyr_al16((size_t)p.cap_rows * 8);
     off[6] = o; o += pyr_al16((size_t)p.cap_cols * 16);
@@ -186,6 +200,7 @@ __host__ __device__ inline size_t pyr_layout(const PyrPlan &p, unsigned char *ba
         S->hsum = reinterpret_cast<uint2 *>(base + off[2]);
         S->smooth = reinterpret_cast<float *>(base + off[3]);
         S->hint = reinterpret_cast<double *>(base + off[8]);
+        S->desc = reinterpret_cast<PyrLevelDesc *>(base + off[9]);
         S->roww = reinterpret_cast<double2 *>(base + off[4]);
         S->rowy = reinterpret_cast<int2 *>(base + off[5]);
         S->colw = reinterpret_cast<double2 *>(base + off[6]);
@@ -373,14 +388,13 @@ FT_DEV unsigned long long pyr_ns() {
 // `dst` (stride c.x1 - c.x0).  Thread mapping is warp-per-row, lanes over
 // columns (no integer division): warp w of NW takes rows w, w + NW, ...
 // Starts by writing tables (caller synchronised the buffers), ends synced.
-FT_DEV void pyr_level_region(const PyrGeom &g, const PyrPlan &p, int l, int ty, int tx,
-                             const PyrRect &sr, const uint8_t *src, const PyrRect &c,
-                             uint8_t *dst, const PyrSmem &S, unsigned long long *tl = nullptr,
+FT_DEV void pyr_level_region(const PyrLevelDesc &d, const uint8_t *src, uint8_t *dst,
+                             const PyrSmem &S, unsigned long long *tl = nullptr,
                              int *tk = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, NW = blockDim.x >> 5;
-    const int hs = g.heights[l - 1], ws = g.widths[l - 1];
-    const int slo = p.smp_y[l][ty][0], shi = p.smp_y[l][ty][1];
-    const int clo = p.smp_x[l][tx][0], chi = p.smp_x[l][tx][1];
+    const PyrRect sr = d.src, c = d.reg;
+    const int hs = d.hs, ws = d.ws;
+    const int slo = d.slo, shi = d.shi, clo = d.clo, chi = d.chi;
     const int t0 = max(slo - 2, 0), t1 = min(shi + 2, hs - 1);
     const int nr = t1 - t0 + 1, ns = shi - slo + 1;
     const int ncol = chi - clo + 1, nq = (ncol + 3) >> 2, sstr = 4 * nq;
@@ -388,7 +402,7 @@ FT_DEV void pyr_level_region(const PyrGeom &g, const PyrPlan &p, int l, int ty, 
     const int crow = c.y1 - c.y0, ccol = c.x1 - c.x0;
     // coefficient tables (kernels.py:255-264)
     {
-        const double sy = g.sy[l], sx = g.sx[l];
+        const double sy = d.sy, sx = d.sx;
         for (int i = tid; i < crow; i += blockDim.x) {
             const double fy = ((double)(c.y0 + i) + 0.5) * sy - 0.5;
             const int y0 = (int)floor(fy);
@@ -517,20 +531,38 @@ FT_DEV void pyr_build_image(const PyrGeom &g, const PyrPlan &p, uint8_t *base,
         for (int t = rank; t < tiles; t += G) {
             const int ty = t / p.tx[s], tx = t - ty * p.tx[s];
             __syncthreads();  // previous tile done with the buffers
-            const PyrRect in = pyr_rect_in(p, s, ty, tx);
-            const uint8_t *srcimg = first == 1 ? lvl0 : base + g.offsets[first - 1];
-            pyr_load_region(srcimg, g.widths[first - 1], in, S.reg[0]);
+            if (threadIdx.x <= last - first) {  // one thread per level: parallel loads
+                const int l = first + threadIdx.x;
+                PyrLevelDesc d;
+                d.reg = pyr_rect_reg(p, l, ty, tx);
+                d.own = pyr_rect_own(p, l, ty, tx);
+                d.src = l == first ? pyr_rect_in(p, s, ty, tx) : pyr_rect_reg(p, l - 1, ty, tx);
+                d.slo = p.smp_y[l][ty][0];
+                d.shi = p.smp_y[l][ty][1];
+                d.clo = p.smp_x[l][tx][0];
+                d.chi = p.smp_x[l][tx][1];
+                d.hs = g.heights[l - 1];
+                d.ws = g.widths[l - 1];
+                d.wd = g.widths[l];
+                d.pad = 0;
+                d.off_dst = g.offsets[l];
+                d.off_src = g.offsets[l - 1];
+                d.sy = g.sy[l];
+                d.sx = g.sx[l];
+                S.desc[l] = d;
+            }
+            __syncthreads();
+            const PyrLevelDesc &d0 = S.desc[first];
+            const uint8_t *srcimg = first == 1 ? lvl0 : base + d0.off_src;
+            pyr_load_region(srcimg, d0.ws, d0.src, S.reg[0]);
             __syncthreads();
             PYR_MARK();
             int cur = 0;
-            PyrRect sr = in;
             for (int l = first; l <= last; ++l) {
-                const PyrRect c = pyr_rect_reg(p, l, ty, tx);
-                pyr_level_region(g, p, l, ty, tx, sr, S.reg[cur], c, S.reg[cur ^ 1], S, tl, tk);
-                pyr_store_own(S.reg[cur ^ 1], c, pyr_rect_own(p, l, ty, tx), base + g.offsets[l],
-                              g.widths[l]);
+                const PyrLevelDesc &d = S.desc[l];
+                pyr_level_region(d, S.reg[cur], S.reg[cur ^ 1], S, tl, tk);
+                pyr_store_own(S.reg[cur ^ 1], d.reg, d.own, base + d.off_dst, d.wd);
                 cur ^= 1;
-                sr = c;
                 PYR_MARK();
             }
         }

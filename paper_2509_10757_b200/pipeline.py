@@ -303,23 +303,35 @@ class FramePipeline:
         return self.host[:self.in_end].clone().pin_memory()
 
 
+def _graph_exec_ptr(graph) -> int:
+    """cudaGraphExec_t of an instantiated torch.cuda.CUDAGraph."""
+    h = graph.raw_cuda_graph_exec()
+    if isinstance(h, int):
+        return h
+    import ctypes
+    get = ctypes.pythonapi.PyCapsule_GetPointer
+    get.restype, get.argtypes = ctypes.c_void_p, [ctypes.py_object, ctypes.c_char_p]
+    return get(h, None)
+
+
 class AsyncRunner:
     """Copy / compute overlapped driver for a stream of steps (the real-time
     shape of the tracker: the next frame's images and keypoints upload while
     the current one tracks).  Two FramePipelines of identical shape take
-    alternate steps; per step k:
+    alternate steps; per step k, issued natively by ft_runner_submit
+    (csrc/ft_runner.cu, one host call):
 
         H2D stream:     inputs(k)          -> pipe[k % 2] device inputs
-        compute stream: gather / pyramids / ft_track_frames (graph replay)
+        compute stream: pipe[k % 2]'s compute graph (gather / pyramids / track)
         D2H stream:     pipe[k % 2] outputs -> its pinned result area
 
     Compute is serialised on one stream (one cooperative launch at a time);
     H2D of step k+1 and D2H of step k-1 run on the two copy engines while
-    step k computes.  Events order buffer reuse: step k's H2D waits for step
-    k-2's compute, step k's compute for step k-2's D2H.  ``wait(k)`` blocks
-    until step k's results are in ``pipes[k % 2]`` host memory."""
+    step k computes.  ``wait(k)`` blocks until step k's results are in
+    ``pipes[k % 2]`` host memory."""
 
     def __init__(self, pipes):
+        import ctypes
         if len(pipes) != 2:
             raise ValueError("AsyncRunner takes two identically shaped FramePipelines")
         a, b = pipes
@@ -327,41 +339,45 @@ class AsyncRunner:
                 (b.S, b.cap_kp, b.cap_pts, b.in_end, b.out_begin, b.out_end):
             raise ValueError("AsyncRunner pipelines differ in shape")
         self.pipes = pipes
-        dev = a.device
-        self.h2d = torch.cuda.Stream(dev)
-        self.comp = torch.cuda.Stream(dev)
-        self.d2h = torch.cuda.Stream(dev)
-        self.ev = [{k: torch.cuda.Event() for k in ("h2d", "comp", "d2h")} for _ in pipes]
+        self.lib = a.lib
         for p in pipes:
             if p.graph_compute is None:
                 p.capture()
+        vp2 = ctypes.c_void_p * 2
+        execs = vp2(*[_graph_exec_ptr(p.graph_compute) for p in pipes])
+        dev_in = vp2(*[p.dev.data_ptr() for p in pipes])
+        dev_out = vp2(*[p.dev.data_ptr() + p.out_begin for p in pipes])
+        host_out = vp2(*[p.host.data_ptr() + p.out_begin for p in pipes])
+        self._r = ctypes.c_void_p()
+        torch.cuda.synchronize(a.device)
+        _lib.check(self.lib.ft_runner_create(execs, dev_in, a.in_end, dev_out, host_out,
+                                             a.out_end - a.out_begin, ctypes.byref(self._r)),
+                   "ft_runner_create")
+        self._keep = (execs, dev_in, dev_out, host_out)
 
     def submit(self, k: int, inputs: torch.Tensor | None = None) -> None:
         """Enqueue step k; inputs = a pinned tensor in the pipelines' input
         layout (staged_inputs()), or None to send pipes[k % 2]'s own staging."""
-        i = k % 2
-        p, e = self.pipes[i], self.ev[i]
-        src = p.host[:p.in_end] if inputs is None else inputs
-        self.h2d.wait_event(e["comp"])  # step k-2 no longer reads the inputs
-        with torch.cuda.stream(self.h2d):
-            p.dev[:p.in_end].copy_(src, non_blocking=True)
-            e["h2d"].record(self.h2d)
-        self.comp.wait_event(e["h2d"])
-        self.comp.wait_event(e["d2h"])  # step k-2's outputs are out
-        with torch.cuda.stream(self.comp):
-            p.graph_compute.replay()
-            e["comp"].record(self.comp)
-        self.d2h.wait_event(e["comp"])
-        with torch.cuda.stream(self.d2h):
-            p.host[p.out_begin:p.out_end].copy_(p.dev[p.out_begin:p.out_end], non_blocking=True)
-            e["d2h"].record(self.d2h)
+        p = self.pipes[k % 2]
+        src = p.host.data_ptr() if inputs is None else inputs.data_ptr()
+        _lib.check(self.lib.ft_runner_submit(self._r, k, src), "ft_runner_submit")
 
     def wait(self, k: int) -> FramePipeline:
         """Block until step k's results are on the host; returns its pipeline
         (read them with .result(s, n_left))."""
-        self.ev[k % 2]["d2h"].synchronize()
+        _lib.check(self.lib.ft_runner_wait(self._r, k), "ft_runner_wait")
         return self.pipes[k % 2]
 
     def synchronize(self) -> None:
-        for s in (self.h2d, self.comp, self.d2h):
-            s.synchronize()
+        torch.cuda.synchronize(self.pipes[0].device)
+
+    def close(self) -> None:
+        if self._r:
+            self.lib.ft_runner_destroy(self._r)
+            self._r = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -17,10 +17,15 @@ codewarm = "--codewarm" in sys.argv  # flush, then run once on other data (warm 
 if os.path.exists(path):
     os.remove(path)
 w = make_workload(seed=1000, n_landmarks=12000, map_points=5000, images=True)
+table = None
+if "--table" in sys.argv:
+    from paper_2509_10757_b200.maptable import MapTable
+    table = MapTable(capacity=8192)
+    table.upsert(w.local.point_ids, w.local.soa)
 pipe = FramePipeline(w.cam, n_streams=streams, cap_kp=1280, cap_points=5120,
-                     pyramid_geometry=w.pyr_left)
+                     pyramid_geometry=w.pyr_left, map_table=table)
 pipe2 = FramePipeline(w.cam, n_streams=streams, cap_kp=1280, cap_points=5120,
-                      pyramid_geometry=w.pyr_left) if codewarm else None
+                      pyramid_geometry=w.pyr_left, map_table=table) if codewarm else None
 if pipe2 is not None:
     for s in range(streams):
         pipe2.load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)

@@ -1,0 +1,123 @@
+"""Diagnose AsyncRunner overlap: per-step wall time of (a) the native runner,
+(b) a torch-stream version of the same schedule, (c) H2D alone, (d) compute
+alone, on the cfg2 single-stream pipeline."""
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2509_10757_b200.maptable import MapTable  # noqa: E402
+from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline  # noqa: E402
+from paper_2509_10757_b200.synthetic import make_workload  # noqa: E402
+
+w = make_workload(seed=1000, n_landmarks=12000, map_points=5000, images=True, id_base=1)
+table = MapTable(capacity=8192)
+table.upsert(w.local.point_ids, w.local.soa)
+pipes = [FramePipeline(w.cam, n_streams=1, cap_kp=1280, cap_points=5120,
+                       pyramid_geometry=w.pyr_left, map_table=table) for _ in range(2)]
+for p in pipes:
+    p.load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
+    p.capture()
+staged = pipes[0].staged_inputs()
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+many = [pipes[0].staged_inputs() for _ in range(8)]
+
+
+def run_native_many():
+    r = AsyncRunner(pipes)
+    for k in range(2):
+        r.submit(k, many[k % 8])
+    r.synchronize()
+    t0 = time.perf_counter()
+    for k in range(N):
+        if k >= 2:
+            r.wait(k - 2)
+        r.submit(k, many[k % 8])
+    r.wait(N - 1)
+    r.wait(N - 2)
+    dt = time.perf_counter() - t0
+    r.close()
+    return 1e6 * dt / N
+
+
+def run_native():
+    r = AsyncRunner(pipes)
+    for k in range(2):
+        r.submit(k, staged)
+    r.synchronize()
+    t0 = time.perf_counter()
+    for k in range(N):
+        if k >= 2:
+            r.wait(k - 2)
+        r.submit(k, staged)
+    r.wait(N - 1)
+    r.wait(N - 2)
+    dt = time.perf_counter() - t0
+    r.close()
+    return 1e6 * dt / N
+
+
+def run_torch():
+    h2d, comp, d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    ev = [{k: torch.cuda.Event() for k in ("h2d", "comp", "d2h")} for _ in pipes]
+
+    def submit(k):
+        i = k % 2
+        p, e = pipes[i], ev[i]
+        h2d.wait_event(e["comp"])
+        with torch.cuda.stream(h2d):
+            p.dev[:p.in_end].copy_(staged, non_blocking=True)
+            e["h2d"].record(h2d)
+        comp.wait_event(e["h2d"])
+        comp.wait_event(e["d2h"])
+        with torch.cuda.stream(comp):
+            p.graph_compute.replay()
+            e["comp"].record(comp)
+        d2h.wait_event(e["comp"])
+        with torch.cuda.stream(d2h):
+            p.host[p.out_begin:p.out_end].copy_(p.dev[p.out_begin:p.out_end], non_blocking=True)
+            e["d2h"].record(d2h)
+
+    for k in range(2):
+        submit(k)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(N):
+        if k >= 2:
+            ev[(k - 2) % 2]["d2h"].synchronize()
+        submit(k)
+    torch.cuda.synchronize()
+    return 1e6 * (time.perf_counter() - t0) / N
+
+
+def run_h2d():
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with torch.cuda.stream(s):
+        for k in range(N):
+            pipes[0].dev[:pipes[0].in_end].copy_(staged, non_blocking=True)
+    s.synchronize()
+    return 1e6 * (time.perf_counter() - t0) / N
+
+
+def run_comp():
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with torch.cuda.stream(s):
+        for k in range(N):
+            pipes[0].graph_compute.replay()
+    s.synchronize()
+    return 1e6 * (time.perf_counter() - t0) / N
+
+
+for name, fn in (("h2d alone", run_h2d), ("h2d alone", run_h2d), ("compute alone", run_comp),
+                 ("native runner", run_native), ("native 8 bufs", run_native_many),
+                 ("native 8 bufs", run_native_many), ("torch schedule", run_torch),
+                 ("native runner", run_native)):
+    print(f"{name:16s} {fn():8.1f} us/step")
