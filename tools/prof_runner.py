@@ -121,3 +121,22 @@ for name, fn in (("h2d alone", run_h2d), ("h2d alone", run_h2d), ("compute alone
                  ("native 8 bufs", run_native_many), ("torch schedule", run_torch),
                  ("native runner", run_native)):
     print(f"{name:16s} {fn():8.1f} us/step")
+
+
+def run_h2d_split(parts):
+    ss = [torch.cuda.Stream() for _ in range(parts)]
+    n = pipes[0].in_end
+    bounds = [n * i // parts // 256 * 256 for i in range(parts)] + [n]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(N):
+        for i, s in enumerate(ss):
+            with torch.cuda.stream(s):
+                pipes[0].dev[bounds[i]:bounds[i + 1]].copy_(staged[bounds[i]:bounds[i + 1]],
+                                                            non_blocking=True)
+    torch.cuda.synchronize()
+    return 1e6 * (time.perf_counter() - t0) / N
+
+
+for parts in (1, 2, 4, 1, 2, 4):
+    print(f"h2d split {parts}    {run_h2d_split(parts):8.1f} us/step")
