@@ -58,6 +58,7 @@ def parse() -> argparse.Namespace:
                    help="extra batched measurement (0 disables)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--quick", action="store_true", help="skip cpu baseline / batched (profiling)")
+    p.add_argument("--no-configs", action="store_true", help="skip the cfg3 / cfg5 measurements")
     return p.parse_args()
 
 
@@ -483,6 +484,8 @@ def main() -> None:
         if images and not raw and world == 1:
             line["raw_images_mode"] = raw_mode_run(args, frames, torch, FramePipeline, cap_kp,
                                                    cap_pts, flush)
+        if world == 1 and not args.no_configs:
+            line["other_configs"] = other_configs(args, torch, flush)
         line["cpu_baseline"] = cpu_baseline(frames[:2], args.cpu_seconds)
     print(json.dumps(line))
     if dist:
@@ -538,6 +541,102 @@ def make_runner(args, frames, pipe, table, load):
         staged.append(pipe.staged_inputs())
     twin.capture()
     return AsyncRunner([pipe, twin]), staged
+
+
+def _pipe_rates(torch, pipes, staged, steps, flush, S) -> dict:
+    """Device frames/s (compute graph, L2 flushed) and e2e frames/s through
+    AsyncRunner for a pair of identically shaped pipelines."""
+    from paper_2509_10757_b200.pipeline import AsyncRunner
+    p = pipes[0]
+    comp = []
+    for _ in range(steps):
+        with torch.cuda.stream(p.stream):
+            p.dev[:p.in_end].copy_(staged[0], non_blocking=True)
+            flush.fill_(1)
+            flush.view(torch.int64).sum()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(p.stream)
+        p.replay(copies=False)
+        b.record(p.stream)
+        p.synchronize()
+        comp.append(a.elapsed_time(b))
+    runner = AsyncRunner(pipes)
+    for k in range(len(staged) + 2):
+        if k >= 2:
+            runner.wait(k - 2)
+        runner.submit(k, staged[k % len(staged)])
+    runner.synchronize()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        if k >= 2:
+            runner.wait(k - 2)
+        runner.submit(k, staged[k % len(staged)])
+    runner.wait(steps - 1)
+    runner.wait(steps - 2)
+    e2e_ms = 1e3 * (time.perf_counter() - t0)
+    runner.close()
+    return {"streams": S, "ms_per_step": float(np.median(comp)),
+            "frames_per_s": S * steps / (sum(comp) / 1e3),
+            "e2e_frames_per_s": S * steps / (e2e_ms / 1e3),
+            "h2d_bytes_per_step": p.h2d_bytes(), "d2h_bytes_per_step": p.d2h_bytes()}
+
+
+def other_configs(args, torch, flush) -> dict:
+    """BASELINE configs[2] (cfg3: TUM-VI fisheye stereo 512x512 ~1500 kps +
+    3050-point local map; FisheyePipeline) and configs[4] (cfg5 high load:
+    ~2000 kps / image, 20k-point local map; FramePipeline), each at 1 stream
+    and 64 streams per launch, local maps resident in a MapTable."""
+    from paper_2509_10757_b200.maptable import MapTable
+    from paper_2509_10757_b200.pipeline import FisheyePipeline, FramePipeline
+    from paper_2509_10757_b200.synthetic import make_workload
+    steps = max(10, args.steps // 2)
+    out = {}
+    fw = [make_workload(seed=700 + i, n_landmarks=4800, map_points=3050, fisheye=True,
+                        offset=0.05 * i, id_base=100_000 * (i + 1)) for i in range(4)]
+    cap = (max(max(len(w.left.u), len(w.right.u)) for w in fw) + 255) // 256 * 256
+    res = {}
+    for S in (1, 64):
+        table = MapTable(capacity=4 * 4096 + 1024)
+        pipes = [FisheyePipeline(fw[0].cam, n_streams=S, cap_kp=cap, cap_points=4096,
+                                 map_table=table) for _ in range(2)]
+        staged = []
+        for k in range(min(4, S * 4)):
+            for s in range(S):
+                w = fw[(k + s) % 4]
+                pipes[0].load_frame(s, w.left, w.right, w.local, w.pose)
+            staged.append(pipes[0].staged_inputs())
+        for p in pipes:
+            p.capture()
+        res[f"S{S}"] = _pipe_rates(torch, pipes, staged, steps, flush, S)
+    out["cfg3_fisheye"] = {"workload": f"TUM-VI-shaped fisheye pair 512x512, "
+                                       f"~{int(np.mean([len(w.left.u) for w in fw]))} kps/image, "
+                                       "3050-point local map: ft_stereo_fisheye (brute force + "
+                                       "KB triangulation) + fisheye SearchLocalPoints",
+                           "hamming_per_frame": int(np.mean([len(w.left.u) * len(w.right.u)
+                                                             for w in fw])), **res}
+    hw = [make_workload(seed=800 + i, n_landmarks=20000, map_points=20000, images=True,
+                        offset=0.05 * i, id_base=1_000_000 * (i + 1)) for i in range(2)]
+    cap = (max(max(len(w.left.u), len(w.right.u)) for w in hw) + 31) // 32 * 32
+    res = {}
+    for S in (1, 64):
+        table = MapTable(capacity=2 * 20480 + 1024)
+        pipes = [FramePipeline(hw[0].cam, n_streams=S, cap_kp=cap, cap_points=20480,
+                               pyramid_geometry=hw[0].pyr_left, map_table=table)
+                 for _ in range(2)]
+        staged = []
+        for k in range(2):
+            for s in range(S):
+                w = hw[(k + s) % 2]
+                pipes[0].load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
+            staged.append(pipes[0].staged_inputs())
+        for p in pipes:
+            p.capture()
+        res[f"S{S}"] = _pipe_rates(torch, pipes, staged, steps, flush, S)
+    out["cfg5_high_load"] = {"workload": f"~{int(np.mean([len(w.left.u) for w in hw]))} "
+                                         "kps/image 752x480 (pyramids shipped) + 20000-point "
+                                         "local map; stereo + SearchLocalPoints",
+                             **res}
+    return out
 
 
 def raw_mode_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, flush) -> dict:

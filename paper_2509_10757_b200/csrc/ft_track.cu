@@ -50,6 +50,7 @@ namespace ft {
 constexpr int TK_THREADS = 512;
 constexpr int TK_WARPS = TK_THREADS / 32;
 constexpr int TK_MAX_BINS = 256;
+constexpr int TK_MAP_CHUNK_MAX = 2048;  // points per map block (shared per-point arrays)
 constexpr long long NO_PID = -1;  // mapping.py:13 NO_POINT
 constexpr long long HASH_EMPTY = (long long)0x8000000000000000ull;
 
@@ -1404,6 +1405,10 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
     int gm_ideal = want_map ? (a.P.cap + 127) / 128 : 0;
     if (gs_ideal > 96) gs_ideal = 96;
     if (gm_ideal > 64) gm_ideal = 64;
+    // the map role's per-point shared arrays (32 B / point of its chunk) must
+    // fit: at most TK_MAP_CHUNK_MAX points per map block
+    const int gm_min = want_map ? (a.P.cap + TK_MAP_CHUNK_MAX - 1) / TK_MAP_CHUNK_MAX : 0;
+    if (gm_ideal < gm_min) gm_ideal = gm_min;
     int Gs = gs_ideal, Gm = gm_ideal, W = F;
     size_t smem = 0;
     a.stage_rdesc = 1;
@@ -1434,16 +1439,17 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
             nGs = gs_ideal;
             nGm = gm_ideal;
         } else {
-            const int min_per = (want_stereo ? 1 : 0) + (want_map ? 1 : 0);
+            const int min_per = (want_stereo ? 1 : 0) + (want_map ? gm_min : 0);
+            if (min_per > capacity) return FT_E_RANGE;
             nW = F < capacity / min_per ? F : capacity / min_per;
             const int per = capacity / nW;
             if (want_stereo && want_map) {
                 nGs = (int)((long long)per * gs_ideal / per_ideal);
                 if (nGs < 1) nGs = 1;
                 nGm = per - nGs;
-                if (nGm < 1) {
-                    nGm = 1;
-                    nGs = per - 1;
+                if (nGm < gm_min) {
+                    nGm = gm_min;
+                    nGs = per - gm_min;
                 }
             } else {
                 nGs = want_stereo ? per : 0;

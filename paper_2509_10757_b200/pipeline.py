@@ -381,3 +381,156 @@ class AsyncRunner:
             self.close()
         except Exception:
             pass
+
+
+class FisheyePipeline:
+    """Resident, graph-captured per-frame step of the reference tracker's
+    fisheye branch (BASELINE cfg 3, TUM-VI shape): ComputeStereoFishEyeMatches
+    (tracker.py:399-414 -> match_fisheye, stereo.py:223-273: all-pairs
+    Hamming + ratio test + KB triangulation, ft_stereo_fisheye) then
+    SearchLocalPoints with the Kannala-Brandt projection (localmap.py:79-122,
+    ft_project_search).  S independent frame streams per launch; the local
+    map is shipped as records or read in place from a resident MapTable.
+
+    Per left keypoint outputs: right_idx / distance (brute force), ok (pair
+    survived triangulation), point (left-camera frame), and the frame slots
+    after the local-map search."""
+
+    def __init__(self, cam, n_streams: int = 1, cap_kp: int = 2048, cap_points: int = 8192,
+                 stereo_cfg: StereoMatchConfig | None = None,
+                 proj_cfg: ProjectionSearchConfig | None = None, scale: float = 1.2,
+                 levels: int = 8, grid_cell_px: int = 48, corrected: bool = False,
+                 map_table=None, device: int | None = None):
+        from .stereo import fisheye_tri_params
+        if not torch.cuda.is_available():
+            raise _lib.FtError("FisheyePipeline needs a CUDA device (no CPU fallback)")
+        self.lib = _lib.load()
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else device)
+        self.cam = cam
+        self.S, self.cap_kp, self.cap_pts = int(n_streams), int(cap_kp), int(cap_points)
+        self.scfg = stereo_cfg or StereoMatchConfig()
+        self.pcfg = proj_cfg or ProjectionSearchConfig()
+        self.scale, self.levels = float(scale), int(levels)
+        self.cell = int(grid_cell_px)
+        self.nx = max(1, (int(cam.width) + self.cell - 1) // self.cell)
+        self.ny = max(1, (int(cam.height) + self.cell - 1) // self.cell)
+        self.table = map_table
+        self.delta_bytes = 0
+        self.tri = fisheye_tri_params(cam, self.scfg, corrected)
+        S, ck, cp = self.S, self.cap_kp, self.cap_pts
+        lay = Layout()
+        for side in ("L", "R"):
+            lay.add(f"{side}_n", 4 * S)
+            lay.add(f"{side}_rec", _lib.KP_RECORD.itemsize * S * ck)
+        lay.add("P_n", 4 * S)
+        if self.table is None:
+            lay.add("P_rec", _lib.POINT_RECORD.itemsize * S * cp)
+        else:
+            lay.add("P_idx", 4 * S * cp)
+        lay.add("rot", 72 * S)
+        lay.add("trans", 24 * S)
+        lay.add("slots_in", 8 * S * ck)
+        self.in_end = lay.total
+        self.out_begin = lay.total
+        lay.add("slots", 8 * S * ck)
+        lay.add("idx", 8 * S * ck)
+        lay.add("dist", 8 * S * ck)
+        lay.add("ok", 4 * S * ck)
+        lay.add("pts", 24 * S * ck)
+        lay.add("slot_n", 4 * S)
+        lay.add("c_n", 4 * S)
+        self.out_end = lay.total
+        self.lay = lay
+        self._dev_raw = torch.zeros(lay.total + (2 << 20), dtype=torch.uint8, device=self.device)
+        off = (-self._dev_raw.data_ptr()) % (2 << 20)
+        self.dev = self._dev_raw[off:off + lay.total]
+        self.host = torch.zeros(lay.total, dtype=torch.uint8).pin_memory()
+        self.hnp = self.host.numpy()
+        self.stream = torch.cuda.Stream(self.device)
+        self.ws = make_workspace(self.lib, self.device, self.stream, S, ck, cp)
+        k = {}
+        for side in ("L", "R"):
+            s_ = _lib.FtKeypoints()
+            s_.rec, s_.count, s_.cap = self._d(f"{side}_rec"), self._d(f"{side}_n"), ck
+            k[side] = s_
+        self.kl, self.kr = k["L"], k["R"]
+        P = _lib.FtMapPoints()
+        if self.table is None:
+            P.rec, P.count, P.cap, P.index = self._d("P_rec"), self._d("P_n"), cp, None
+        else:
+            P.rec, P.count, P.cap, P.index = self.table.ptr, self._d("P_n"), cp, self._d("P_idx")
+        self.points = P
+        self.pparams = project_params(cam, self.pcfg, self.scale, self.levels, self.cell,
+                                      self.nx, self.ny, None, 0.0)
+        io = _lib.FtProjectIO()
+        io.rot, io.trans, io.skip, io.ref_angles = self._d("rot"), self._d("trans"), None, None
+        io.slots_in, io.slots_out = self._d("slots_in"), self._d("slots")
+        self.pio = io
+        po = _lib.FtProjectOut()
+        po.corr_point = po.corr_kp = po.corr_dist = po.corr_oct = None
+        po.corr_count, po.slot_count = self._d("c_n"), self._d("slot_n")
+        self.pout = po
+        self.pmode = (_lib.FT_PROJ_RESOLVE | _lib.FT_PROJ_SKIP_SLOTS | _lib.FT_PROJ_WRITE_SLOTS)
+        self.graph = None
+        self.graph_compute = None
+
+    _h = FramePipeline._h
+    _d = FramePipeline._d
+    h2d_bytes = FramePipeline.h2d_bytes
+    d2h_bytes = FramePipeline.d2h_bytes
+    synchronize = FramePipeline.synchronize
+    capture = FramePipeline.capture
+    replay = FramePipeline.replay
+    staged_inputs = FramePipeline.staged_inputs
+    run_eager = FramePipeline.run_eager
+
+    def load_frame(self, s: int, left, right, local, pose, slots=None) -> None:
+        S, ck, cp = self.S, self.cap_kp, self.cap_pts
+        for side, fs in (("L", left), ("R", right)):
+            n = len(fs.u)
+            if n > ck:
+                raise ValueError(f"{n} keypoints exceed capacity {ck}")
+            self._h(f"{side}_n", np.int32, (S,))[s] = n
+            fill_kp_records(self._h(f"{side}_rec", _lib.KP_RECORD, (S, ck))[s], fs)
+        m = len(local.point_ids)
+        if m > cp:
+            raise ValueError(f"{m} map points exceed capacity {cp}")
+        self._h("P_n", np.int32, (S,))[s] = m
+        if self.table is None:
+            fill_point_records(self._h("P_rec", _lib.POINT_RECORD, (S, cp))[s], local.soa)
+        else:
+            self.delta_bytes += self.table.upsert(local.point_ids, local.soa, only_missing=True)
+            self._h("P_idx", np.int32, (S, cp))[s, :m] = self.table.slots(local.point_ids)
+        self._h("rot", np.float64, (S, 9))[s] = np.asarray(pose.rotation).reshape(9)
+        self._h("trans", np.float64, (S, 3))[s] = np.asarray(pose.translation).reshape(3)
+        sl = self._h("slots_in", np.int64, (S, ck))
+        sl[s] = -1
+        if slots is not None:
+            sl[s, :len(left.u)] = slots
+
+    def _step(self, copies: bool) -> None:
+        a = self.stream
+        if copies:
+            with torch.cuda.stream(a):
+                self.dev[:self.in_end].copy_(self.host[:self.in_end], non_blocking=True)
+        _lib.check(self.lib.ft_stereo_fisheye(self.S, self.kl, self.kr, int(self.scfg.t_match),
+                                              float(self.scfg.ratio), self.tri, self._d("idx"),
+                                              self._d("dist"), self._d("ok"), self._d("pts"),
+                                              self.ws, a.cuda_stream), "ft_stereo_fisheye")
+        _lib.check(self.lib.ft_project_search(self.S, self.points, self.kl, self.pparams,
+                                              self.pio, self.pmode, self.pout, self.ws,
+                                              a.cuda_stream), "ft_project_search")
+        if copies:
+            with torch.cuda.stream(a):
+                self.host[self.out_begin:self.out_end].copy_(
+                    self.dev[self.out_begin:self.out_end], non_blocking=True)
+
+    def result(self, s: int, n_left: int) -> dict:
+        S, ck = self.S, self.cap_kp
+        g = lambda name, dt: self._h(name, dt, (S, ck))[s, :n_left].copy()  # noqa: E731
+        return {"right_idx": g("idx", np.int64), "distance": g("dist", np.int64),
+                "ok": g("ok", np.int32).astype(bool),
+                "points": self._h("pts", np.float64, (S, ck, 3))[s, :n_left].copy(),
+                "slots": g("slots", np.int64),
+                "n_slots": int(self._h("slot_n", np.int32, (S,))[s])}

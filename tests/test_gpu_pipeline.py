@@ -197,3 +197,77 @@ def _check_step(pipe, workloads, expected, k):
                                           err_msg=f"step {k} stream {s} {f}")
         np.testing.assert_array_equal(res.slots, slots, err_msg=f"step {k} stream {s}")
         assert res.n_slots == n
+
+
+@pytest.mark.parametrize("use_table", [False, True])
+def test_fisheye_pipeline(oracle, use_table):
+    """FisheyePipeline (cfg3 shape): ft_stereo_fisheye + fisheye
+    SearchLocalPoints per stream, vs the oracle's brute force, triangulation
+    (reference mode) and search_local_points with the KB projection."""
+    from paper_2509_10757_b200.maptable import MapTable
+    from paper_2509_10757_b200.pipeline import FisheyePipeline
+    from paper_2509_10757_b200.synthetic import make_workload
+    from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
+    ws = [make_workload(seed=500 + i, n_landmarks=4800, map_points=3050, fisheye=True,
+                        offset=0.05 * i, id_base=100_000 * i) for i in range(3)]
+    cfg, pcfg = StereoMatchConfig(), ProjectionSearchConfig()
+    table = MapTable(capacity=16384) if use_table else None
+    pipe = FisheyePipeline(ws[0].cam, n_streams=3, cap_kp=2048, cap_points=4096,
+                           map_table=table)
+    for s, w in enumerate(ws):
+        pipe.load_frame(s, w.left, w.right, w.local, w.pose)
+    for rep in range(2):
+        pipe.replay(copies=True)
+        pipe.synchronize()
+        for s, w in enumerate(ws):
+            r = pipe.result(s, len(w.left.u))
+            idx, dist = oracle.bruteforce(w.left.descriptors, w.right.descriptors, cfg.t_match,
+                                          cfg.ratio)
+            np.testing.assert_array_equal(r["right_idx"], idx)
+            np.testing.assert_array_equal(r["distance"], dist)
+            lidx, _, pts, _ = oracle.fisheye_triangulate(w.left, w.right, idx, dist, w.cam,
+                                                         cfg.ray_gap_ceiling)
+            np.testing.assert_array_equal(np.nonzero(r["ok"])[0], lidx)
+            np.testing.assert_allclose(r["points"][lidx], pts.reshape(-1, 3), rtol=1e-9,
+                                       atol=1e-12)
+            slots = np.full(len(w.left.u), -1, np.int64)
+            grid = oracle.frame_grid(w.left.u, w.left.v, w.cam.width, w.cam.height, 48) + (48,)
+            n = oracle.search_local_points(w.local.point_ids, w.local.soa, w.left.u, w.left.v,
+                                           w.left.octave, w.left.descriptors, grid, slots,
+                                           w.pose, w.cam, pcfg, 1.2, 8)
+            np.testing.assert_array_equal(r["slots"], slots, err_msg=f"stream {s}")
+            assert r["n_slots"] == n
+
+
+def test_high_load_batched(oracle):
+    """cfg5 shape (~2000 kps / image, 20k-point local maps) at 64 streams per
+    launch: the map role must split each frame's 20k points over several
+    blocks (per-block shared arrays), results equal the oracle's."""
+    from paper_2509_10757_b200.pipeline import FramePipeline
+    from paper_2509_10757_b200.synthetic import make_workload
+    from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
+    ws = [make_workload(seed=900 + i, n_landmarks=20000, map_points=20000, images=True,
+                        offset=0.05 * i) for i in range(2)]
+    cap = (max(max(len(w.left.u), len(w.right.u)) for w in ws) + 31) // 32 * 32
+    pipe = FramePipeline(ws[0].cam, n_streams=64, cap_kp=cap, cap_points=20480,
+                         pyramid_geometry=ws[0].pyr_left)
+    for s in range(64):
+        w = ws[s % 2]
+        pipe.load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
+    pipe.replay(copies=True)
+    pipe.synchronize()
+    for i, w in enumerate(ws):
+        m = oracle.stereo_pinhole(w.left, w.right, w.pyr_left, w.pyr_right, w.cam,
+                                  StereoMatchConfig(), w.scale_pow)
+        slots = np.full(len(w.left.u), -1, np.int64)
+        grid = oracle.frame_grid(w.left.u, w.left.v, w.cam.width, w.cam.height, 48) + (48,)
+        n = oracle.search_local_points(w.local.point_ids, w.local.soa, w.left.u, w.left.v,
+                                       w.left.octave, w.left.descriptors, grid, slots, w.pose,
+                                       w.cam, ProjectionSearchConfig(), 1.2, 8)
+        for s in (i, i + 62):
+            r = pipe.result(s, len(w.left.u))
+            for f in FIELDS:
+                np.testing.assert_array_equal(getattr(r.matches, f), getattr(m, f),
+                                              err_msg=f"stream {s} {f}")
+            np.testing.assert_array_equal(r.slots, slots, err_msg=f"stream {s}")
+            assert r.n_slots == n
