@@ -20,7 +20,7 @@ __all__ = ["LocalMap", "search_local_points"]
 
 
 def search_local_points(local, frame, cam, cfg, scale: float, levels: int, engine=None,
-                        world=None, pool=None) -> int:
+                        world=None, pool=None, table=None) -> int:
     """Associate unmatched local points with frame keypoints; mutates
     ``frame.slots`` (and world point flags when ``world`` is given)."""
     if len(local.point_ids) == 0:
@@ -41,7 +41,7 @@ def search_local_points(local, frame, cam, cfg, scale: float, levels: int, engin
     before = np.asarray(frame.slots).copy()
     r = project_search(local.soa, frame, frame.pose, cam, cfg, scale, levels,
                        ref_angles=ref_angles, rotation=rotation_check, slots=before,
-                       skip_slotted=True, write_slots=True)
+                       skip_slotted=True, write_slots=True, table=table)
     after = r["slots"]
     frame.slots[...] = after
     if world is not None:

@@ -74,22 +74,35 @@ def _grid_geometry(frame, cam) -> tuple[int, int, int]:
     return cell, max(1, (int(cam.width) + cell - 1) // cell), max(1, (int(cam.height) + cell - 1) // cell)
 
 
-def _add_points(lay: Layout, cap: int) -> None:
+def _add_points(lay: Layout, cap: int, table=None) -> None:
     lay.add("P_n", 4)
-    lay.add("P_rec", _lib.POINT_RECORD.itemsize * cap)
+    if table is None:
+        lay.add("P_rec", _lib.POINT_RECORD.itemsize * cap)
+    else:
+        lay.add("P_idx", 4 * cap)
 
 
-def _put_points(rt, lay: Layout, pts) -> int:
+def _put_points(rt, lay: Layout, pts, table=None) -> int:
+    """Records (reference SoA -> ft_point_record) or, with a resident
+    MapTable, 4-B table slots (points missing from the table are uploaded
+    first: the map delta)."""
     m = len(pts.point_ids)
     rt.put(lay, "P_n", np.array([m], dtype=np.int32), np.int32)
-    if m:
+    if m and table is None:
         fill_point_records(rt.host_view(lay, "P_rec", _lib.POINT_RECORD, (m,)), pts)
+    elif m:
+        if getattr(pts, "positions", None) is not None:
+            table.upsert(pts.point_ids, pts, only_missing=True)
+        rt.put(lay, "P_idx", table.slots(pts.point_ids), np.int32)
     return m
 
 
-def _points_struct(rt, lay: Layout, cap: int) -> _lib.FtMapPoints:
+def _points_struct(rt, lay: Layout, cap: int, table=None) -> _lib.FtMapPoints:
     s = _lib.FtMapPoints()
-    s.rec, s.count, s.cap = rt.ptr(lay, "P_rec"), rt.ptr(lay, "P_n"), cap
+    if table is None:
+        s.rec, s.count, s.cap, s.index = rt.ptr(lay, "P_rec"), rt.ptr(lay, "P_n"), cap, None
+    else:
+        s.rec, s.count, s.cap, s.index = table.ptr, rt.ptr(lay, "P_n"), cap, rt.ptr(lay, "P_idx")
     return s
 
 
@@ -107,7 +120,7 @@ def _out_struct(rt, lay: Layout, phase_a: bool) -> _lib.FtProjectOut:
 def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale: float,
                    levels: int, *, skip_mask=None, ref_angles=None, rotation: bool = False,
                    window_px=None, u_offset: float = 0.0, slots=None, skip_slotted=False,
-                   write_slots=False, resolve=True, phase_a_out=False):
+                   write_slots=False, resolve=True, phase_a_out=False, table=None):
     """One fused ``ft_project_search`` launch on one frame.
 
     Returns a dict with any of: out_kp/out_dist/out_oct (phase A),
@@ -120,7 +133,7 @@ def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale:
     with_angle = bool(rotation and ref_angles is not None)
     lay = Layout()
     add_keypoints(lay, "K", cap_kp, with_angle=with_angle)
-    _add_points(lay, cap_pts)
+    _add_points(lay, cap_pts, table)
     lay.add("rot", 72)
     lay.add("trans", 24)
     if skip_mask is not None:
@@ -151,7 +164,7 @@ def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale:
     with rt.lock:
         rt.reserve(lay.total)
         put_keypoints(rt, lay, "K", left, with_angle=with_angle)
-        _put_points(rt, lay, points)
+        _put_points(rt, lay, points, table)
         rt.put(lay, "rot", np.asarray(pose.rotation, dtype=np.float64).reshape(9), np.float64)
         rt.put(lay, "trans", np.asarray(pose.translation, dtype=np.float64).reshape(3), np.float64)
         if skip_mask is not None:
@@ -168,7 +181,7 @@ def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale:
         io.skip = rt.ptr(lay, "skip") if skip_mask is not None else None
         io.ref_angles = rt.ptr(lay, "ref_ang") if with_angle else None
         io.slots_in = io.slots_out = rt.ptr(lay, "slots") if slots is not None else None
-        st = rt.lib.ft_project_search(1, _points_struct(rt, lay, cap_pts),
+        st = rt.lib.ft_project_search(1, _points_struct(rt, lay, cap_pts, table),
                                       keypoints_struct(rt, lay, "K", cap_kp), params, io, mode,
                                       _out_struct(rt, lay, phase_a_out), ws,
                                       rt.stream.cuda_stream)
@@ -287,39 +300,63 @@ def search_by_projection(points, frame, pose, cam, cfg: ProjectionSearchConfig, 
                          levels: int, engine=None, skip_mask: np.ndarray | None = None,
                          ref_angles: np.ndarray | None = None, rotation_check: bool = False,
                          window_px: float | None = None, u_offset: float = 0.0,
-                         pool=None) -> Correspondences:
+                         pool=None, table=None) -> Correspondences:
     """Project map points into the frame and resolve the best associations
-    (reference projection.py:203-221) -- phases A, B and C in ONE launch."""
+    (reference projection.py:203-221) -- phases A, B and C in ONE launch.
+    table: optional resident MapTable (the points are read in place through
+    their slots; only points missing from it are uploaded)."""
     if len(points.point_ids) == 0:
         return Correspondences.empty()
     r = project_search(points, frame, pose, cam, cfg, scale, levels, skip_mask=skip_mask,
                        ref_angles=ref_angles, rotation=bool(rotation_check),
-                       window_px=window_px, u_offset=u_offset)
+                       window_px=window_px, u_offset=u_offset, table=table)
     return r["corr"]
 
 
 def search_prev_frame(prev, cur, pose, world, cam, cfg: ProjectionSearchConfig, scale: float,
-                      levels: int, engine=None, soa_out=None, pool=None):
+                      levels: int, engine=None, soa_out=None, pool=None, table=None):
     """Match the previous frame's map points into the current frame
-    (reference projection.py:224-253).  Decomposition of the host-side world
-    map stays on the host, as in the reference."""
+    (reference projection.py:224-253).  Without a table the previous frame's
+    slotted points are decomposed on the host (mapping.py:204-235), as in the
+    reference; with a resident MapTable only points missing from the table
+    are decomposed and uploaded (the map delta) and the search reads the rest
+    in place (SURVEY 8(f) #2)."""
     from .types import MapPointSoA
     slot_idx = np.nonzero(prev.slots != NO_POINT)[0]
     if len(slot_idx) == 0:
         return Correspondences.empty(), np.empty(0, dtype=np.int64)
-    pids = prev.slots[slot_idx]
-    mps = [world.points[int(p)] for p in pids]
-    soa = MapPointSoA(positions=np.array([p.position for p in mps], dtype=np.float64).reshape(-1, 3),
-                      descriptors=np.array([p.descriptor for p in mps], dtype=np.uint64).reshape(-1, 4),
-                      normals=np.array([p.normal for p in mps], dtype=np.float64).reshape(-1, 3),
-                      min_distances=np.array([p.min_distance for p in mps], dtype=np.float64),
-                      max_distances=np.array([p.max_distance for p in mps], dtype=np.float64),
-                      point_ids=np.array([p.point_id for p in mps], dtype=np.int64))
+    pids = np.asarray(prev.slots[slot_idx], dtype=np.int64)
+
+    def decompose(ids):
+        mps = [world.points[int(p)] for p in ids]
+        return MapPointSoA(
+            positions=np.array([p.position for p in mps], dtype=np.float64).reshape(-1, 3),
+            descriptors=np.array([p.descriptor for p in mps], dtype=np.uint64).reshape(-1, 4),
+            normals=np.array([p.normal for p in mps], dtype=np.float64).reshape(-1, 3),
+            min_distances=np.array([p.min_distance for p in mps], dtype=np.float64),
+            max_distances=np.array([p.max_distance for p in mps], dtype=np.float64),
+            point_ids=np.array([p.point_id for p in mps], dtype=np.int64))
+
+    if table is None:
+        points = decompose(pids)
+    else:
+        missing = pids[table._lookup(pids) < 0]
+        if len(missing):
+            table.upsert(missing, decompose(missing))
+        points = _IdsOnly(pids)
     ref_angles = prev.left.angle[slot_idx]
     rel = pose.matrix() @ np.linalg.inv(prev.pose.matrix())
     forward = float(rel[2, 3])
     u_offset = math.copysign(cfg.prev_u_offset_px, forward) if abs(forward) > 1e-9 else 0.0
-    corr = search_by_projection(soa, cur, pose, cam, cfg, scale, levels, ref_angles=ref_angles,
+    corr = search_by_projection(points, cur, pose, cam, cfg, scale, levels, ref_angles=ref_angles,
                                 rotation_check=cfg.rotation_check_prev,
-                                window_px=cfg.window_prev_px, u_offset=u_offset)
-    return corr, soa.point_ids
+                                window_px=cfg.window_prev_px, u_offset=u_offset, table=table)
+    return corr, np.asarray(points.point_ids)
+
+
+class _IdsOnly:
+    """Points named by id only (their records are resident in a MapTable)."""
+
+    def __init__(self, point_ids):
+        self.point_ids = np.asarray(point_ids, dtype=np.int64)
+        self.positions = None

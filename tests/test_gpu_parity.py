@@ -394,3 +394,64 @@ def test_fisheye_triangulation_vs_oracle(oracle, corrected):
         assert len(got[0]) > 1000
         m = ft.compute_stereo_fisheye_matches(left, right, cam, cfg, corrected=True)
         np.testing.assert_allclose(m.depth[got[0]], got[2][:, 2], rtol=0, atol=0)
+
+
+def _world_from_soa(soa):
+    """Minimal host world map (reference mapping.py MapPoint fields used by
+    decompose_map_points) keyed by point id."""
+    from types import SimpleNamespace
+    pts = {}
+    for i, pid in enumerate(soa.point_ids):
+        pts[int(pid)] = SimpleNamespace(point_id=int(pid), position=soa.positions[i],
+                                        descriptor=soa.descriptors[i], normal=soa.normals[i],
+                                        min_distance=float(soa.min_distances[i]),
+                                        max_distance=float(soa.max_distances[i]))
+    return SimpleNamespace(points=pts)
+
+
+@pytest.mark.parametrize("use_table", [False, True])
+def test_search_prev_frame(oracle, use_table):
+    """projection.py:224-253 on cfg2: the previous frame's slotted points
+    (from SearchLocalPoints) searched in the current frame with the rotation
+    check, the 15-px window and the +-1 px offset from the relative forward
+    translation; host-decomposed SoA, or resident MapTable slots."""
+    import math
+    from paper_2509_10757_b200.maptable import MapTable
+    from paper_2509_10757_b200.types import Pose
+    d = G.load("cfg2_frame_map.npz")
+    left, right = G.feats(d, "left"), G.feats(d, "right")
+    cam, cfg = G.pinhole(), ProjectionSearchConfig()
+    local, pose = G.local_map(d), G.pose(d)
+    prev = make_frame(left, right, cam, pose)
+    prev.slots[...] = d["slots_a"]
+    world = _world_from_soa(local.soa)
+    cur_pose = Pose(pose.rotation, pose.translation + np.array([0.002, -0.001, 0.004]))
+    cur = make_frame(left, right, cam, cur_pose)
+    table = MapTable(capacity=8192) if use_table else None
+    corr, pids = ft.search_prev_frame(prev, cur, cur_pose, world, cam, cfg, 1.2, 8, table=table)
+    # oracle composition (reference projection.py:231-253)
+    slot_idx = np.nonzero(prev.slots != -1)[0]
+    ids = prev.slots[slot_idx]
+    order = {int(p): i for i, p in enumerate(local.soa.point_ids)}
+    rows = np.array([order[int(p)] for p in ids])
+    sub = type(local.soa)(positions=local.soa.positions[rows],
+                          descriptors=local.soa.descriptors[rows], normals=local.soa.normals[rows],
+                          min_distances=local.soa.min_distances[rows],
+                          max_distances=local.soa.max_distances[rows], point_ids=ids)
+    rel = cur_pose.matrix() @ np.linalg.inv(prev.pose.matrix())
+    fwd = float(rel[2, 3])
+    u_off = math.copysign(cfg.prev_u_offset_px, fwd) if abs(fwd) > 1e-9 else 0.0
+    grid = oracle.frame_grid(left.u, left.v, cam.width, cam.height, 48) + (48,)
+    ref = oracle.search_by_projection(sub, left.u, left.v, left.octave, left.descriptors,
+                                      left.angle, grid, cur_pose, cam, cfg, 1.2, 8,
+                                      ref_angles=left.angle[slot_idx],
+                                      rotation_check=cfg.rotation_check_prev,
+                                      window_px=cfg.window_prev_px, u_offset=u_off)
+    np.testing.assert_array_equal(pids, ids)
+    assert len(ref.point_idx) > 100
+    for f in ("point_idx", "keypoint_idx", "distance", "octave"):
+        np.testing.assert_array_equal(getattr(corr, f), getattr(ref, f), err_msg=f)
+    if use_table:  # a second call finds every point resident: no upload
+        before = table.bytes_uploaded
+        ft.search_prev_frame(prev, cur, cur_pose, world, cam, cfg, 1.2, 8, table=table)
+        assert table.bytes_uploaded == before
