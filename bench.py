@@ -486,7 +486,8 @@ def main() -> None:
                                                    cap_pts, flush)
         if world == 1 and not args.no_configs:
             line["other_configs"] = other_configs(args, torch, flush)
-        line["cpu_baseline"] = cpu_baseline(frames[:2], args.cpu_seconds)
+        if world == 1:  # reported baseline: rank 0 at N=1 only
+            line["cpu_baseline"] = cpu_baseline(frames[:2], args.cpu_seconds)
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
