@@ -41,15 +41,18 @@ FALLBACK_HBM = 6650.0
 def parse() -> argparse.Namespace:
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--streams", type=int, default=1, help="frame streams per GPU")
     p.add_argument("--frames", type=int, default=8, help="distinct frames cycled per stream")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-images", action="store_true", help="feature bundles only (no phase 2)")
-    p.add_argument("--raw-images", action="store_true",
-                   help="ship level-0 images and build the pyramids on the device "
-                        "(default: ship pyramids, the reference's phase-2 input)")
+    p.add_argument("--pyramid-mode", default="ship", choices=["hybrid", "ship", "device"],
+                   help="ship: ship whole pyramids, the reference's phase-2 input (default); "
+                        "hybrid: ship level 0 + levels > --build-levels, build levels "
+                        "1..build-levels on the device; device: ship level 0, build all")
+    p.add_argument("--build-levels", type=int, default=1)
+    p.add_argument("--raw-images", action="store_true", help=argparse.SUPPRESS)
     p.add_argument("--ship-pyramids", action="store_true", help=argparse.SUPPRESS)
     p.add_argument("--no-map-table", action="store_true",
                    help="ship every frame's local-map records instead of table slots into "
@@ -247,14 +250,28 @@ def run_reference(args) -> None:
     print(json.dumps(line))
 
 
+def pyramid_mode(args):
+    """(raw_images, build_levels) of the pipeline for --pyramid-mode."""
+    mode = "device" if args.raw_images else args.pyramid_mode
+    if mode == "ship":
+        return False, None
+    if mode == "device":
+        return True, None
+    return True, max(1, args.build_levels)
+
+
 def config_dict(args) -> dict:
+    raw, b = pyramid_mode(args)
     if args.no_images:
         img = ", feature bundle (no phase 2)"
-    elif not args.raw_images:
+    elif not raw:
         img = ", rendered images shipped as pyramids (phase-2 input) -> SAD phase 2"
-    else:
+    elif b is None:
         img = (", rendered images shipped raw (0.36 MB each) -> device pyramid build "
                "(bit-exact build_pyramid) -> SAD phase 2")
+    else:
+        img = (f", level-0 images + pyramid levels > {b} shipped, levels 1..{b} built on the "
+               "device (bit-exact build_pyramid) -> SAD phase 2")
     mp = ("5000-point local map shipped as records every frame" if args.no_map_table else
           "5000-point local map resident in the device map table (frames ship 4-B slots, "
           "read in place by the map role)")
@@ -291,11 +308,12 @@ def main() -> None:
     cap_kp = int(max(max(len(f.left.u), len(f.right.u)) for f in frames) + 31) // 32 * 32
     cap_pts = int(max(len(f.local.point_ids) for f in frames) + 255) // 256 * 256
     S = args.streams
-    raw = images and args.raw_images
+    raw, build_levels = pyramid_mode(args)
+    raw = raw and images
     table, table_bytes = make_table(args, frames, cap_pts)
     pipe = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
                          pyramid_geometry=w0.pyr_left if images else None, raw_images=raw,
-                         map_table=table)
+                         map_table=table, build_levels=build_levels)
 
     def load(step: int) -> None:
         for s in range(S):
@@ -478,12 +496,13 @@ def main() -> None:
         if args.batched_streams > 0 and world == 1:
             line["batched"] = batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts,
                                           images, flush)
-            if images and not raw:
-                line["batched_raw_images"] = batched_run(args, frames, torch, FramePipeline,
-                                                         cap_kp, cap_pts, images, flush, True)
-        if images and not raw and world == 1:
-            line["raw_images_mode"] = raw_mode_run(args, frames, torch, FramePipeline, cap_kp,
-                                                   cap_pts, flush)
+            if images:
+                line["batched_pyramids_shipped"] = batched_run(args, frames, torch, FramePipeline,
+                                                               cap_kp, cap_pts, images, flush,
+                                                               False)
+        if images and world == 1:
+            line["pyramid_modes"] = raw_mode_run(args, frames, torch, FramePipeline, cap_kp,
+                                                 cap_pts, flush)
         if world == 1 and not args.no_configs:
             line["other_configs"] = other_configs(args, torch, flush)
         if world == 1:  # reported baseline: rank 0 at N=1 only
@@ -535,7 +554,8 @@ def make_runner(args, frames, pipe, table, load):
     frame's inputs pre-staged in pinned host memory (one tensor per step)."""
     from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
     twin = FramePipeline(pipe.cam, n_streams=pipe.S, cap_kp=pipe.cap_kp, cap_points=pipe.cap_pts,
-                         pyramid_geometry=pipe.pyr, raw_images=pipe.raw, map_table=table)
+                         pyramid_geometry=pipe.pyr, raw_images=pipe.raw, map_table=table,
+                         build_levels=pipe.build_levels if pipe.raw else None)
     staged = []
     for k in range(len(frames)):
         load(k)
@@ -641,49 +661,27 @@ def other_configs(args, torch, flush) -> dict:
 
 
 def raw_mode_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, flush) -> dict:
-    """The same single-stream step with raw level-0 images shipped and the
-    pyramids built on the device (ft_build_pyramids, SURVEY 8(f) #1)."""
+    """The single-stream step with raw level-0 images shipped and pyramid
+    levels 1..b built on the device (ft_build_pyramids), the
+    levels above b shipped: device value and AsyncRunner e2e per b."""
     w0 = frames[0]
-    table, _ = make_table(args, frames, cap_pts)
-    pipe = FramePipeline(w0.cam, n_streams=1, cap_kp=cap_kp, cap_points=cap_pts,
-                         pyramid_geometry=w0.pyr_left, raw_images=True, map_table=table)
-    def load(k):
-        f = frames[k % len(frames)]
-        pipe.load_frame(0, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
-    load(0)
-    pipe.capture()
-    for k in range(3):
-        load(k)
-        pipe.replay(copies=True)
-    pipe.synchronize()
-    comp, e2e = [], []
-    for k in range(args.steps):
-        load(k)
-        with torch.cuda.stream(pipe.stream):
-            pipe.dev[:pipe.in_end].copy_(pipe.host[:pipe.in_end], non_blocking=True)
-            flush.fill_(1)
-            flush.view(torch.int64).sum()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(pipe.stream)
-        pipe.replay(copies=False)
-        b.record(pipe.stream)
-        pipe.synchronize()
-        comp.append(a.elapsed_time(b))
-    for k in range(args.steps):
-        load(k)
-        with torch.cuda.stream(pipe.stream):
-            flush.fill_(1)
-            flush.view(torch.int64).sum()
-        pipe.synchronize()
-        t0 = time.perf_counter()
-        pipe.replay(copies=True)
-        pipe.synchronize()
-        e2e.append(1e3 * (time.perf_counter() - t0))
-    return {"frames_per_s": args.steps / (sum(comp) / 1e3),
-            "ms_per_step": float(np.mean(comp)),
-            "e2e_frames_per_s": args.steps / (sum(e2e) / 1e3),
-            "e2e_ms_per_step": float(np.mean(e2e)),
-            "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes()}
+    out = {}
+    L = len(w0.pyr_left.widths)
+    for b in (0, 1, 2, 3, L - 1):  # 0: whole pyramids shipped
+        table, _ = make_table(args, frames, cap_pts)
+        pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=cap_kp, cap_points=cap_pts,
+                               pyramid_geometry=w0.pyr_left, raw_images=b > 0, map_table=table,
+                               build_levels=b if b > 0 else None) for _ in range(2)]
+        staged = []
+        for k in range(len(frames)):
+            f = frames[k]
+            pipes[0].load_frame(0, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
+            staged.append(pipes[0].staged_inputs())
+        for p in pipes:
+            p.capture()
+        r = _pipe_rates(torch, pipes, staged, args.steps, flush, 1)
+        out["pyramids_shipped" if b == 0 else f"build_levels_1_to_{b}"] = r
+    return out
 
 
 def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flush,
@@ -693,11 +691,16 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
     from paper_2509_10757_b200.pipeline import AsyncRunner
     S = args.batched_streams
     w0 = frames[0]
-    raw = (images and args.raw_images) if raw is None else raw
+    mode_raw, b = pyramid_mode(args)
+    if raw is None:
+        raw = images and mode_raw
+    elif not raw:
+        b = None
     table, _ = make_table(args, frames, cap_pts, S)
     pipes = [FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
                            pyramid_geometry=w0.pyr_left if images else None, raw_images=raw,
-                           map_table=table) for _ in range(2)]
+                           map_table=table, build_levels=b if raw else None)
+             for _ in range(2)]
     pipe = pipes[0]
     for s in range(S):
         f = frames[s % len(frames)]
@@ -734,6 +737,7 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
     runner.wait(steps - 2)
     e2e_ms = 1e3 * (time.perf_counter() - t0)
     return {"streams": S, "steps": steps, "raw_images": bool(raw),
+            "build_levels": (pipe.build_levels if raw else None),
             "ms_per_step": float(np.mean(comp)),
             "frames_per_s": S * steps / (sum(comp) / 1e3),
             "e2e_frames_per_s": S * steps / (e2e_ms / 1e3),

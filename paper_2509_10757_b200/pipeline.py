@@ -44,7 +44,7 @@ class FramePipeline:
                  pyramid_geometry=None, stereo_cfg: StereoMatchConfig | None = None,
                  proj_cfg: ProjectionSearchConfig | None = None, scale: float = 1.2,
                  levels: int = 8, grid_cell_px: int = 48, device: int | None = None,
-                 raw_images: bool = False, map_table=None):
+                 raw_images: bool = False, map_table=None, build_levels: int | None = None):
         if not torch.cuda.is_available():
             raise _lib.FtError("FramePipeline needs a CUDA device (no CPU fallback)")
         self.lib = _lib.load()
@@ -58,8 +58,15 @@ class FramePipeline:
         self.scale, self.levels = float(scale), int(levels)
         self.scale_pow = self.scale ** np.arange(self.levels, dtype=np.float64)
         self.pyr = pyramid_geometry  # object with widths / heights / offsets, or None
-        # raw_images: frames ship level 0 only; ft_build_pyramids builds the rest
+        # raw_images: frames ship level 0 and ft_build_pyramids builds levels
+        # 1..build_levels on the device (default: all); the levels above
+        # build_levels are shipped (one contiguous range per image) -- a
+        # copy / compute balance: the big levels are cheaper to build, the
+        # small ones to ship
         self.raw = bool(raw_images) and pyramid_geometry is not None
+        n_lv = len(pyramid_geometry.widths) if pyramid_geometry is not None else 0
+        self.build_levels = (n_lv - 1 if build_levels is None else
+                             max(1, min(int(build_levels), n_lv - 1))) if self.raw else 0
         # map_table (maptable.MapTable): frames ship table slots (4 B / point)
         # instead of point records; the map role reads the table in place
         self.table = map_table
@@ -88,8 +95,12 @@ class FramePipeline:
         self.pyr_total = int(self.pyr.offsets[-1]) if self.pyr is not None else 0
         self.pyr_bytes = (self.pyr_total + 255) // 256 * 256
         self.img_bytes = int(self.pyr.widths[0]) * int(self.pyr.heights[0]) if self.pyr is not None else 0
+        self.upper_off = int(self.pyr.offsets[self.build_levels + 1]) if self.raw else 0
+        self.upper_bytes = self.pyr_total - self.upper_off if self.raw else 0
         if self.raw:
             lay.add("imgs", 2 * S * self.img_bytes)  # [left x S | right x S]
+            if self.upper_bytes:
+                lay.add("upper", 2 * S * self.upper_bytes)
         elif self.pyr is not None:
             lay.add("pyrs", 2 * S * self.pyr_bytes)
         self.in_end = lay.total
@@ -151,6 +162,10 @@ class FramePipeline:
                 imgs = self._h("imgs", np.uint8, (2, S, ib))
                 imgs[0, s] = np.asarray(pyr_left.data)[:ib]
                 imgs[1, s] = np.asarray(pyr_right.data)[:ib]
+                if self.upper_bytes:
+                    up = self._h("upper", np.uint8, (2, S, self.upper_bytes))
+                    up[0, s] = np.asarray(pyr_left.data)[self.upper_off:self.pyr_total]
+                    up[1, s] = np.asarray(pyr_right.data)[self.upper_off:self.pyr_total]
             else:
                 pb = self.pyr_bytes
                 pyrs = self._h("pyrs", np.uint8, (2, S, pb))
@@ -194,6 +209,9 @@ class FramePipeline:
             pyrs = self._d("pyrs")
             self.pl = pyramid_struct(self.pyr, pyrs, self.pyr_bytes)
             self.pr = pyramid_struct(self.pyr, pyrs + S * self.pyr_bytes, self.pyr_bytes)
+            if self.raw:  # levels 0..build_levels built on the device, all 2S images
+                self.pl_build = pyramid_struct(self.pyr, pyrs, self.pyr_bytes)
+                self.pl_build.n_levels = self.build_levels + 1
         else:
             self.pl = self.pr = None
         self.sparams = stereo_params(self.scfg, int(self.cam.height), self.scale_pow,
@@ -243,7 +261,15 @@ class FramePipeline:
 
     def launch_pyramids(self, stream) -> None:
         if self.raw:
-            _lib.check(self.lib.ft_build_pyramids(2 * self.S, self.pl, self._d("imgs"),
+            S2 = 2 * self.S
+            if self.upper_bytes:  # shipped upper levels into place (strided D2D)
+                with torch.cuda.stream(stream):
+                    base = self.lay.offsets["pyrs"]
+                    dst = self.dev[base:base + S2 * self.pyr_bytes].view(S2, self.pyr_bytes)
+                    ub = self.lay.offsets["upper"]
+                    src = self.dev[ub:ub + S2 * self.upper_bytes].view(S2, self.upper_bytes)
+                    dst[:, self.upper_off:self.pyr_total].copy_(src, non_blocking=True)
+            _lib.check(self.lib.ft_build_pyramids(S2, self.pl_build, self._d("imgs"),
                                                   self.img_bytes, self.ws, stream.cuda_stream),
                        "ft_build_pyramids")
 

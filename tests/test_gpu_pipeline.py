@@ -41,14 +41,14 @@ def expected(workloads, oracle):
     return out
 
 
-def _run(workloads, expected, n_streams, replays, raw=False, table=None):
+def _run(workloads, expected, n_streams, replays, raw=False, table=None, build_levels=None):
     from paper_2509_10757_b200.pipeline import FramePipeline
     w0 = workloads[0]
     cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
     cap_pts = max(len(w.local.point_ids) for w in workloads)
     pipe = FramePipeline(w0.cam, n_streams=n_streams, cap_kp=(cap_kp + 31) // 32 * 32,
                          cap_points=(cap_pts + 255) // 256 * 256, pyramid_geometry=w0.pyr_left,
-                         raw_images=raw, map_table=table)
+                         raw_images=raw, map_table=table, build_levels=build_levels)
     for s in range(n_streams):
         w = workloads[s % len(workloads)]
         pipe.load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
@@ -84,6 +84,14 @@ def test_raw_images_pipeline(workloads, expected):
     """Frames ship level-0 images; the device builds the pyramids."""
     _run(workloads, expected, 1, 3, raw=True)
     _run(workloads, expected, 8, 2, raw=True)
+
+
+def test_hybrid_pyramid_levels(workloads, expected):
+    """Raw level 0 + shipped upper levels: the device builds levels
+    1..build_levels only (truncated geometry) and the upper levels are
+    copied into place; results equal the oracle's."""
+    for b in (1, 2, 3, 5):
+        _run(workloads, expected, 2, 2, raw=True, build_levels=b)
 
 
 def test_raw_images_many_streams(workloads, expected):
