@@ -536,17 +536,26 @@ class FisheyePipeline:
             sl[s, :len(left.u)] = slots
 
     def _step(self, copies: bool) -> None:
+        # the fisheye stereo and the local-map search only share the left
+        # keypoints (read-only): they run on two branches of the graph
         a = self.stream
+        if not hasattr(self, "side"):
+            self.side = torch.cuda.Stream(self.device)
+            self.ev_fork, self.ev_join = torch.cuda.Event(), torch.cuda.Event()
         if copies:
             with torch.cuda.stream(a):
                 self.dev[:self.in_end].copy_(self.host[:self.in_end], non_blocking=True)
+        self.ev_fork.record(a)
+        self.side.wait_event(self.ev_fork)
         _lib.check(self.lib.ft_stereo_fisheye(self.S, self.kl, self.kr, int(self.scfg.t_match),
                                               float(self.scfg.ratio), self.tri, self._d("idx"),
                                               self._d("dist"), self._d("ok"), self._d("pts"),
-                                              self.ws, a.cuda_stream), "ft_stereo_fisheye")
+                                              self.ws, self.side.cuda_stream), "ft_stereo_fisheye")
+        self.ev_join.record(self.side)
         _lib.check(self.lib.ft_project_search(self.S, self.points, self.kl, self.pparams,
                                               self.pio, self.pmode, self.pout, self.ws,
                                               a.cuda_stream), "ft_project_search")
+        a.wait_event(self.ev_join)
         if copies:
             with torch.cuda.stream(a):
                 self.host[self.out_begin:self.out_end].copy_(
