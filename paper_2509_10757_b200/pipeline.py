@@ -545,16 +545,19 @@ class FisheyePipeline:
         if copies:
             with torch.cuda.stream(a):
                 self.dev[:self.in_end].copy_(self.host[:self.in_end], non_blocking=True)
+        # the map search is launched first: its blocks need a whole SM's
+        # register file each, so it must claim its SMs before the brute-force
+        # blocks spread over all of them
         self.ev_fork.record(a)
+        _lib.check(self.lib.ft_project_search(self.S, self.points, self.kl, self.pparams,
+                                              self.pio, self.pmode, self.pout, self.ws,
+                                              a.cuda_stream), "ft_project_search")
         self.side.wait_event(self.ev_fork)
         _lib.check(self.lib.ft_stereo_fisheye(self.S, self.kl, self.kr, int(self.scfg.t_match),
                                               float(self.scfg.ratio), self.tri, self._d("idx"),
                                               self._d("dist"), self._d("ok"), self._d("pts"),
                                               self.ws, self.side.cuda_stream), "ft_stereo_fisheye")
         self.ev_join.record(self.side)
-        _lib.check(self.lib.ft_project_search(self.S, self.points, self.kl, self.pparams,
-                                              self.pio, self.pmode, self.pout, self.ws,
-                                              a.cuda_stream), "ft_project_search")
         a.wait_event(self.ev_join)
         if copies:
             with torch.cuda.stream(a):
