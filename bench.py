@@ -376,28 +376,37 @@ def main() -> None:
             e2e_ms.append(1e3 * (time.perf_counter() - t0))
             e2e_ev_ms.append(a.elapsed_time(b))
         e2e_delta = pipe.delta_bytes - delta0
-        # ---- e2e, overlapped: AsyncRunner (H2D of k+1 / compute of k / D2H of
-        # k-1 concurrently), inputs pre-staged in pinned memory per frame
-        runner, staged = make_runner(args, frames, pipe, table, load)
-        if dist:
-            dist.barrier()
-        # warm-up: every staged pinned buffer's first DMA is slow (one cycle)
-        for k in range(max(args.warmup, len(staged) + 2)):
-            if k >= 2:
-                runner.wait(k - 2)
-            runner.submit(k, staged[k % len(staged)])
-        runner.synchronize()
-        t0 = time.perf_counter()
-        for k in range(args.steps):
-            if k >= 2:
-                runner.wait(k - 2)
-            runner.submit(k, staged[k % len(staged)])
-        runner.wait(args.steps - 1)
-        runner.wait(args.steps - 2)
-        async_ms = 1e3 * (time.perf_counter() - t0)
         if dist:
             dist.barrier()
     clocks = clk.summary()
+    # ---- e2e, overlapped: AsyncRunner (H2D of k+1 / compute of k / D2H of k-1
+    # concurrently), inputs pre-staged in pinned memory per frame.  Timed outside
+    # the nvidia-smi sampler: its polling stalls the host for milliseconds, which
+    # is noise at ~50 us per step.
+    runner, staged = make_runner(args, frames, pipe, table, load)
+    if dist:
+        dist.barrier()
+    # warm-up: every staged pinned buffer's first DMA is slow (one cycle)
+    for k in range(max(args.warmup, 4 * len(staged) + 2)):
+        if k >= 2:
+            runner.wait(k - 2)
+        runner.submit(k, staged[k % len(staged)])
+    runner.synchronize()
+    t0 = time.perf_counter()
+    marks = []
+    for k in range(args.steps):
+        if k >= 2:
+            runner.wait(k - 2)
+        runner.submit(k, staged[k % len(staged)])
+        marks.append(time.perf_counter())
+    runner.wait(args.steps - 1)
+    runner.wait(args.steps - 2)
+    async_ms = 1e3 * (time.perf_counter() - t0)
+    if os.environ.get("FT_BENCH_DIAG"):
+        d = np.diff(np.array([t0] + marks)) * 1e6
+        print(f"[diag] async step us: median {np.median(d):.1f} p90 {np.percentile(d, 90):.1f} "
+              f"max {d.max():.1f} first {np.round(d[:12], 1).tolist()}", file=sys.stderr)
+    runner.close()
 
     # ---- per-kernel timing for the roofline (eager, on the launching stream)
     kern = {"pyramids": [], "track": [], "stereo_only": [], "map_only": []}
@@ -556,12 +565,12 @@ def make_runner(args, frames, pipe, table, load):
     twin = FramePipeline(pipe.cam, n_streams=pipe.S, cap_kp=pipe.cap_kp, cap_points=pipe.cap_pts,
                          pyramid_geometry=pipe.pyr, raw_images=pipe.raw, map_table=table,
                          build_levels=pipe.build_levels if pipe.raw else None)
-    staged = []
+    ring = pipe.staging_ring(len(frames))
     for k in range(len(frames)):
         load(k)
-        staged.append(pipe.staged_inputs())
+        pipe.stage_into(ring[k])
     twin.capture()
-    return AsyncRunner([pipe, twin]), staged
+    return AsyncRunner([pipe, twin]), [ring[k] for k in range(len(frames))]
 
 
 def _pipe_rates(torch, pipes, staged, steps, flush, S) -> dict:
@@ -582,7 +591,7 @@ def _pipe_rates(torch, pipes, staged, steps, flush, S) -> dict:
         p.synchronize()
         comp.append(a.elapsed_time(b))
     runner = AsyncRunner(pipes)
-    for k in range(len(staged) + 2):
+    for k in range(4 * len(staged) + 2):
         if k >= 2:
             runner.wait(k - 2)
         runner.submit(k, staged[k % len(staged)])
@@ -620,12 +629,14 @@ def other_configs(args, torch, flush) -> dict:
         table = MapTable(capacity=4 * 4096 + 1024)
         pipes = [FisheyePipeline(fw[0].cam, n_streams=S, cap_kp=cap, cap_points=4096,
                                  map_table=table) for _ in range(2)]
-        staged = []
-        for k in range(min(4, S * 4)):
+        nst = min(4, S * 4)
+        ring = pipes[0].staging_ring(nst)
+        for k in range(nst):
             for s in range(S):
                 w = fw[(k + s) % 4]
                 pipes[0].load_frame(s, w.left, w.right, w.local, w.pose)
-            staged.append(pipes[0].staged_inputs())
+            pipes[0].stage_into(ring[k])
+        staged = [ring[k] for k in range(nst)]
         for p in pipes:
             p.capture()
         res[f"S{S}"] = _pipe_rates(torch, pipes, staged, steps, flush, S)
@@ -644,12 +655,13 @@ def other_configs(args, torch, flush) -> dict:
         pipes = [FramePipeline(hw[0].cam, n_streams=S, cap_kp=cap, cap_points=20480,
                                pyramid_geometry=hw[0].pyr_left, map_table=table)
                  for _ in range(2)]
-        staged = []
+        ring = pipes[0].staging_ring(2)
         for k in range(2):
             for s in range(S):
                 w = hw[(k + s) % 2]
                 pipes[0].load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
-            staged.append(pipes[0].staged_inputs())
+            pipes[0].stage_into(ring[k])
+        staged = [ring[0], ring[1]]
         for p in pipes:
             p.capture()
         res[f"S{S}"] = _pipe_rates(torch, pipes, staged, steps, flush, S)
@@ -672,11 +684,12 @@ def raw_mode_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, flush) -> 
         pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=cap_kp, cap_points=cap_pts,
                                pyramid_geometry=w0.pyr_left, raw_images=b > 0, map_table=table,
                                build_levels=b if b > 0 else None) for _ in range(2)]
-        staged = []
+        ring = pipes[0].staging_ring(len(frames))
         for k in range(len(frames)):
             f = frames[k]
             pipes[0].load_frame(0, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
-            staged.append(pipes[0].staged_inputs())
+            pipes[0].stage_into(ring[k])
+        staged = [ring[k] for k in range(len(frames))]
         for p in pipes:
             p.capture()
         r = _pipe_rates(torch, pipes, staged, args.steps, flush, 1)
@@ -705,7 +718,9 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
     for s in range(S):
         f = frames[s % len(frames)]
         pipe.load_frame(s, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
-    staged = pipe.staged_inputs()
+    ring = pipe.staging_ring(1)
+    pipe.stage_into(ring[0])
+    staged = ring[0]
     pipe.capture()
     steps = max(5, args.steps // 5)
     for _ in range(3):

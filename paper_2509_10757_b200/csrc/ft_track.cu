@@ -1439,21 +1439,47 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
             nGs = gs_ideal;
             nGm = gm_ideal;
         } else {
+            // more frames than one resident wave holds: pick slots W and the
+            // stereo / map split minimising the modelled job time
+            //   waves(W) * (c0 + max(stereo rounds * cs, map rounds * cm)),
+            // a stereo round = one keypoint per warp, a map round = one
+            // 512-point staging round (c0, cs, cm: measured us, round 1)
             const int min_per = (want_stereo ? 1 : 0) + (want_map ? gm_min : 0);
             if (min_per > capacity) return FT_E_RANGE;
-            nW = F < capacity / min_per ? F : capacity / min_per;
-            const int per = capacity / nW;
-            if (want_stereo && want_map) {
-                nGs = (int)((long long)per * gs_ideal / per_ideal);
-                if (nGs < 1) nGs = 1;
-                nGm = per - nGs;
-                if (nGm < gm_min) {
-                    nGm = gm_min;
-                    nGs = per - gm_min;
+            const double c0 = 8.0, cs = 3.6, cm = 8.0;
+            double best = 1e30;
+            nW = 1;
+            nGs = want_stereo ? 1 : 0;
+            nGm = want_map ? gm_min : 0;
+            const int wmax = F < capacity / min_per ? F : capacity / min_per;
+            for (int w = 1; w <= wmax; ++w) {
+                const int per = capacity / w;
+                const int waves = (F + w - 1) / w;
+                const int g_lo = want_map ? gm_min : 0;
+                const int g_hi = want_map ? (want_stereo ? per - 1 : per) : 0;
+                for (int gm = g_lo; gm <= g_hi; ++gm) {
+                    const int gs = want_stereo ? (want_map ? per - gm : per) : 0;
+                    if (want_stereo && gs < 1) continue;
+                    double t = 0.0;
+                    if (want_stereo) {
+                        const int kw = gs * TK_WARPS;
+                        const double r = (double)((a.L.cap + kw - 1) / kw);
+                        t = r * cs;
+                    }
+                    if (want_map) {
+                        const int chunk = (a.P.cap + gm - 1) / gm;
+                        const double r = (double)((chunk + TK_THREADS - 1) / TK_THREADS);
+                        t = t > r * cm ? t : r * cm;
+                    }
+                    const double total = waves * (c0 + t);
+                    if (total < best * 0.999) {
+                        best = total;
+                        nW = w;
+                        nGs = gs;
+                        nGm = gm;
+                    }
+                    if (!want_stereo) break;  // map-only: all blocks to the map
                 }
-            } else {
-                nGs = want_stereo ? per : 0;
-                nGm = want_map ? per : 0;
             }
         }
         const bool same = nGs == Gs && nGm == Gm && nW == W;

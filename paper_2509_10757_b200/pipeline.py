@@ -328,6 +328,18 @@ class FramePipeline:
         one step's inputs, ready for AsyncRunner.submit."""
         return self.host[:self.in_end].clone().pin_memory()
 
+    def staging_ring(self, n: int) -> torch.Tensor:
+        """One pinned allocation of n input slots ([n, in_end], rows 256-B
+        aligned): a ring a frame source fills and AsyncRunner.submit reads.
+        One allocation keeps the DMA mappings few (IOMMU / TLB friendly)."""
+        stride = (self.in_end + 255) // 256 * 256
+        ring = torch.zeros((n, stride), dtype=torch.uint8).pin_memory()
+        return ring[:, :self.in_end]
+
+    def stage_into(self, dst: torch.Tensor) -> None:
+        """Copy the current input staging into a ring slot."""
+        dst.copy_(self.host[:self.in_end])
+
 
 def _graph_exec_ptr(graph) -> int:
     """cudaGraphExec_t of an instantiated torch.cuda.CUDAGraph."""
