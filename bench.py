@@ -295,6 +295,8 @@ def main() -> None:
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
+    from paper_2509_10757_b200.runtime import bind_host_to_gpu_numa
+    numa_cpus = bind_host_to_gpu_numa(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -432,7 +434,13 @@ def main() -> None:
                                                  device="cuda")
     value = job_frames_per_s(S * args.steps, world, tot_comp)
     e2e_serial = job_frames_per_s(S * args.steps, world, tot_e2e)
-    e2e_value = job_frames_per_s(S * args.steps, world, async_ms)
+    e2e_async = job_frames_per_s(S * args.steps, world, async_ms)
+    # both are the public API end to end (every step's inputs H2D, results
+    # D2H); the overlapped runner wins unless the host's PCIe path is
+    # contended (shared node), where its concurrent DMA streams lose -- report
+    # the faster, name it, keep both
+    e2e_value = max(e2e_async, e2e_serial)
+    e2e_method = "async" if e2e_async >= e2e_serial else "serial"
 
     if rank != 0:
         if dist:
@@ -475,11 +483,17 @@ def main() -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64+u32", "data": "synthetic", "config": config_dict(args),
             "e2e": {"value": e2e_value, "unit": "frames/s",
-                    "method": "AsyncRunner: per step H2D of that step's inputs from pinned host "
-                              "memory, compute, D2H of its results; copies of neighbouring "
-                              "steps overlap the compute (host wall clock over all steps)",
+                    "method": e2e_method,
+                    "methods": {"async": "AsyncRunner (native ft_runner): per step H2D of that "
+                                         "step's inputs from pinned host memory, compute, D2H "
+                                         "of its results; neighbouring steps' copies overlap "
+                                         "the compute; host wall clock over all steps",
+                                "serial": "FramePipeline.replay(copies=True) per step: H2D, "
+                                          "compute, D2H, synchronise; host wall clock"},
+                    "async_value": e2e_async,
                     "serial_value": e2e_serial,
                     "h2d_alone_ms": h2d_ms,
+                    "host_cpus": "all" if numa_cpus is None else f"{len(numa_cpus)} on the GPU's NUMA node",
                     "h2d_gbs": pipe.h2d_bytes() / (h2d_ms / 1e3) / 1e9,
                     "h2d_bytes_per_step": pipe.h2d_bytes() + e2e_delta // max(1, args.steps),
                     "d2h_bytes_per_step": pipe.d2h_bytes(),
@@ -502,20 +516,28 @@ def main() -> None:
             "gpu_launches": 2 * (1 + int(raw)) * args.steps,
             "parity_spot_check": check}
     if not args.quick:
+        # extra measurements: a failure in one is recorded, never loses the line
+        def extra(key, fn):
+            try:
+                line[key] = fn()
+            except Exception as exc:  # noqa: BLE001
+                line[key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
         if args.batched_streams > 0 and world == 1:
-            line["batched"] = batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts,
-                                          images, flush)
-            if images:
-                line["batched_pyramids_shipped"] = batched_run(args, frames, torch, FramePipeline,
-                                                               cap_kp, cap_pts, images, flush,
-                                                               False)
+            extra("batched", lambda: batched_run(args, frames, torch, FramePipeline, cap_kp,
+                                                 cap_pts, images, flush))
+            if images:  # the other pyramid input mode at batch
+                other_raw = not raw
+                extra("batched_hybrid_pyramids" if other_raw else "batched_pyramids_shipped",
+                      lambda: batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts,
+                                          images, flush, other_raw))
         if images and world == 1:
-            line["pyramid_modes"] = raw_mode_run(args, frames, torch, FramePipeline, cap_kp,
-                                                 cap_pts, flush)
+            extra("pyramid_modes", lambda: raw_mode_run(args, frames, torch, FramePipeline,
+                                                        cap_kp, cap_pts, flush))
         if world == 1 and not args.no_configs:
-            line["other_configs"] = other_configs(args, torch, flush)
+            extra("other_configs", lambda: other_configs(args, torch, flush))
         if world == 1:  # reported baseline: rank 0 at N=1 only
-            line["cpu_baseline"] = cpu_baseline(frames[:2], args.cpu_seconds)
+            extra("cpu_baseline", lambda: cpu_baseline(frames[:2], args.cpu_seconds))
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
@@ -565,12 +587,13 @@ def make_runner(args, frames, pipe, table, load):
     twin = FramePipeline(pipe.cam, n_streams=pipe.S, cap_kp=pipe.cap_kp, cap_points=pipe.cap_pts,
                          pyramid_geometry=pipe.pyr, raw_images=pipe.raw, map_table=table,
                          build_levels=pipe.build_levels if pipe.raw else None)
-    ring = pipe.staging_ring(len(frames))
-    for k in range(len(frames)):
+    n = max(1, min(len(frames), int(os.environ.get("FT_BENCH_RING", str(len(frames))))))
+    ring = pipe.staging_ring(n)
+    for k in range(n):
         load(k)
         pipe.stage_into(ring[k])
     twin.capture()
-    return AsyncRunner([pipe, twin]), [ring[k] for k in range(len(frames))]
+    return AsyncRunner([pipe, twin]), [ring[k] for k in range(n)]
 
 
 def _pipe_rates(torch, pipes, staged, steps, flush, S) -> dict:
@@ -709,6 +732,8 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
         raw = images and mode_raw
     elif not raw:
         b = None
+    elif not mode_raw:  # explicit raw from a ship-mode run: hybrid at --build-levels
+        b = max(1, args.build_levels)
     table, _ = make_table(args, frames, cap_pts, S)
     pipes = [FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
                            pyramid_geometry=w0.pyr_left if images else None, raw_images=raw,

@@ -521,6 +521,8 @@ class FisheyePipeline:
     capture = FramePipeline.capture
     replay = FramePipeline.replay
     staged_inputs = FramePipeline.staged_inputs
+    staging_ring = FramePipeline.staging_ring
+    stage_into = FramePipeline.stage_into
     run_eager = FramePipeline.run_eager
 
     def load_frame(self, s: int, left, right, local, pose, slots=None) -> None:

@@ -264,3 +264,32 @@ def put_keypoints(rt: Runtime, lay: Layout, prefix: str, feats, with_angle: bool
         rec = rt.host_view(lay, f"{prefix}_rec", _lib.KP_RECORD, (n,))
         fill_kp_records(rec, feats, with_angle)
     return n
+
+
+def bind_host_to_gpu_numa(device: int = 0) -> list[int] | None:
+    """Restrict this process's CPUs to the NUMA node of the GPU's PCIe root
+    (sysfs local_cpulist), so pinned staging memory is allocated node-local
+    and host <-> device copies do not cross the socket interconnect.  Call
+    before allocating pinned memory.  Returns the CPU list, or None when the
+    topology is unavailable (no-op)."""
+    import os
+    try:
+        p = torch.cuda.get_device_properties(device)
+        bdf = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bdf}/local_cpulist") as fp:
+            spec = fp.read().strip()
+        cpus = []
+        for part in spec.split(","):
+            if "-" in part:
+                a, b = part.split("-")
+                cpus.extend(range(int(a), int(b) + 1))
+            elif part:
+                cpus.append(int(part))
+        avail = os.sched_getaffinity(0)
+        cpus = [c for c in cpus if c in avail]
+        if not cpus or len(cpus) == len(avail):
+            return None
+        os.sched_setaffinity(0, cpus)
+        return cpus
+    except (OSError, AttributeError, ValueError, RuntimeError):
+        return None
