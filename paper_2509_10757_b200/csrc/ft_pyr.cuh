@@ -252,7 +252,7 @@ inline size_t pyr_plan_capacities(const PyrGeom &g, PyrPlan &p) {
 // barrier), tiles of about `tile_px` pixels of the stage's first level with the
 // level's aspect ratio.  FT_PYR_STAGES="3,7" / FT_PYR_TILE_PX="1600,1600"
 // override (profiling).  Default 900 px: measured best single-frame latency.
-inline bool pyr_make_plan(const PyrGeom &g, PyrPlan &p, int g_blocks) {
+inline bool pyr_make_plan(const PyrGeom &g, PyrPlan &p, int g_blocks, int n_images = 1) {
     const int L = g.n_levels;
     if (L < 2) return false;
     int ends[PY_MAX_STAGES], n = 0;
@@ -279,7 +279,9 @@ inline bool pyr_make_plan(const PyrGeom &g, PyrPlan &p, int g_blocks) {
         }
     }
     int px[PY_MAX_STAGES];
-    for (int s = 0; s < PY_MAX_STAGES; ++s) px[s] = 900;
+    // latency (few images): small tiles, more blocks; throughput (many
+    // images): bigger tiles, less halo recompute (measured, r1)
+    for (int s = 0; s < PY_MAX_STAGES; ++s) px[s] = n_images <= 8 ? 900 : 2500;
     if (const char *e = getenv("FT_PYR_TILE_PX")) {
         int v = 0, k = 0, have = 0;
         for (const char *c = e;; ++c) {

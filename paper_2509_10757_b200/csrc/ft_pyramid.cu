@@ -77,7 +77,7 @@ extern "C" int ft_build_pyramids(int32_t n_images, const ft_pyramid *pyr,
     if (images && image_stride < (int64_t)a.g.widths[0] * a.g.heights[0]) return FT_E_RANGE;
     pyr_geom_scales(a.g);
     // plan for the first chunk's blocks-per-image (occupancy from a probe plan)
-    if (!pyr_make_plan(a.g, a.p, 1 << 30)) return FT_E_RANGE;
+    if (!pyr_make_plan(a.g, a.p, 1 << 30, n_images)) return FT_E_RANGE;
     size_t smem = pyr_plan_capacities(a.g, a.p);
     if (smem > 227 * 1024) return FT_E_RANGE;
     cudaError_t e = cudaFuncSetAttribute(pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -89,7 +89,7 @@ extern "C" int ft_build_pyramids(int32_t n_images, const ft_pyramid *pyr,
     {
         const int chunk0 = n_images < occ * sms ? n_images : occ * sms;
         PyrPlan q = a.p;
-        if (pyr_make_plan(a.g, q, occ * sms / chunk0)) {
+        if (pyr_make_plan(a.g, q, occ * sms / chunk0, n_images)) {
             const size_t sq = pyr_plan_capacities(a.g, q);
             int occ_q = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_q, pyramid_kernel, PY_THREADS, sq);
