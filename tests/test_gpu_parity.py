@@ -455,3 +455,81 @@ def test_search_prev_frame(oracle, use_table):
         before = table.bytes_uploaded
         ft.search_prev_frame(prev, cur, cur_pose, world, cam, cfg, 1.2, 8, table=table)
         assert table.bytes_uploaded == before
+
+
+STEREO_CFGS = [
+    dict(t_match=40),
+    dict(band_factor=1.0, half_window=3, half_slide=3),
+    dict(band_factor=3.5, half_window=7, half_slide=8, outlier_multiplier=1.5),
+    dict(min_disparity=2.0, max_disparity=60.0, outlier_multiplier=4.0),
+    dict(t_match=256, half_window=1, half_slide=1, ratio=0.6),
+]
+
+
+@pytest.mark.parametrize("kw", STEREO_CFGS)
+def test_stereo_config_sweep_vs_oracle(oracle, kw):
+    """Non-default StereoMatchConfig values (thresholds, band, window /
+    slide sizes incl. the 1x1 and 15x15 extremes, disparity range,
+    outlier multiplier) through phase 1 -> phase 2 -> reject and the fisheye
+    ratio test, bit-exact with the oracle."""
+    from paper_2509_10757_b200.synthetic import make_workload
+    w = make_workload(seed=31, n_landmarks=12000, map_points=2000, images=True)
+    cfg = StereoMatchConfig(**kw)
+    ref = oracle.stereo_pinhole(w.left, w.right, w.pyr_left, w.pyr_right, w.cam, cfg,
+                                w.scale_pow)
+    got = ft.compute_stereo_matches(w.left, w.right, w.cam, cfg, w.scale_pow, w.pyr_left,
+                                    w.pyr_right)
+    for f in FIELDS:
+        np.testing.assert_array_equal(getattr(got, f), getattr(ref, f), err_msg=f"{kw} {f}")
+    from paper_2509_10757_b200.stereo import fisheye_bruteforce
+    idx, dist = fisheye_bruteforce(w.left, w.right, cfg)
+    ridx, rdist = oracle.bruteforce(w.left.descriptors, w.right.descriptors, cfg.t_match,
+                                    cfg.ratio, 4)
+    np.testing.assert_array_equal(idx, ridx)
+    np.testing.assert_array_equal(dist, rdist)
+
+
+PROJ_CFGS = [
+    dict(window_px=2.0, t_proj=50),
+    dict(window_px=12.0, ratio=0.7, view_cos_min=0.9),
+    dict(window_px=30.0, ratio=1.0, view_cos_min=-1.0, t_proj=256),
+    dict(histogram_bins=12, histogram_keep=1),
+]
+
+
+@pytest.mark.parametrize("kw", PROJ_CFGS)
+@pytest.mark.parametrize("scale,levels", [(1.2, 8), (1.3, 6), (2.0, 4)])
+def test_projection_config_sweep_vs_oracle(oracle, kw, scale, levels):
+    """Non-default ProjectionSearchConfig values and pyramid scale / level
+    counts (level prediction uses 1 / log(scale)) through phase A, resolve,
+    rotation filter and SearchLocalPoints, bit-exact with the oracle."""
+    from paper_2509_10757_b200.synthetic import make_workload
+    w = make_workload(seed=41, n_landmarks=12000, map_points=5000)
+    pcfg = ProjectionSearchConfig(**kw)
+    frame = w.frame()
+    grid = oracle.frame_grid(w.left.u, w.left.v, w.cam.width, w.cam.height, 48) + (48,)
+    kp, kd, ko = ft.run_phase_a(w.local.soa, frame, w.pose, w.cam, pcfg, scale, levels)
+    rkp, rkd, rko = oracle.run_phase_a(w.local.soa, w.left.u, w.left.v, w.left.octave,
+                                       w.left.descriptors, grid, w.pose, w.cam, pcfg, scale,
+                                       levels)
+    np.testing.assert_array_equal(kp, rkp)
+    np.testing.assert_array_equal(kd, rkd)
+    np.testing.assert_array_equal(ko, rko)
+    rng = np.random.default_rng(7)
+    ref_ang = rng.uniform(0, 2 * np.pi, len(w.local.point_ids))
+    c = ft.search_by_projection(w.local.soa, frame, w.pose, w.cam, pcfg, scale, levels,
+                                ref_angles=ref_ang, rotation_check=True, u_offset=-1.0)
+    rc = oracle.search_by_projection(w.local.soa, w.left.u, w.left.v, w.left.octave,
+                                     w.left.descriptors, w.left.angle, grid, w.pose, w.cam, pcfg,
+                                     scale, levels, ref_angles=ref_ang, rotation_check=True,
+                                     u_offset=-1.0)
+    for f in ("point_idx", "keypoint_idx", "distance", "octave"):
+        np.testing.assert_array_equal(getattr(c, f), getattr(rc, f), err_msg=f)
+    slots = np.full(len(w.left.u), -1, np.int64)
+    n_ref = oracle.search_local_points(w.local.point_ids, w.local.soa, w.left.u, w.left.v,
+                                       w.left.octave, w.left.descriptors, grid, slots, w.pose,
+                                       w.cam, pcfg, scale, levels)
+    f2 = w.frame()
+    n = ft.search_local_points(w.local, f2, w.cam, pcfg, scale, levels)
+    assert n == n_ref
+    np.testing.assert_array_equal(f2.slots, slots)
