@@ -281,7 +281,7 @@ inline bool pyr_make_plan(const PyrGeom &g, PyrPlan &p, int g_blocks, int n_imag
     int px[PY_MAX_STAGES];
     // latency (few images): small tiles, more blocks; throughput (many
     // images): bigger tiles, less halo recompute (measured, r1)
-    for (int s = 0; s < PY_MAX_STAGES; ++s) px[s] = n_images <= 8 ? 900 : 2500;
+    for (int s = 0; s < PY_MAX_STAGES; ++s) px[s] = n_images <= 8 ? 900 : 1600;
     if (const char *e = getenv("FT_PYR_TILE_PX")) {
         int v = 0, k = 0, have = 0;
         for (const char *c = e;; ++c) {
