@@ -385,21 +385,22 @@ def main() -> None:
     # concurrently), inputs pre-staged in pinned memory per frame.  Timed outside
     # the nvidia-smi sampler: its polling stalls the host for milliseconds, which
     # is noise at ~50 us per step.
-    runner, staged = make_runner(args, frames, pipe, table, load)
+    runner, staged, ranges = make_runner(args, frames, pipe, table, load)
+    shipped = float(np.mean([hi - lo for lo, hi in ranges]))
     if dist:
         dist.barrier()
     # warm-up: every staged pinned buffer's first DMA is slow (one cycle)
     for k in range(max(args.warmup, 4 * len(staged) + 2)):
         if k >= 2:
             runner.wait(k - 2)
-        runner.submit(k, staged[k % len(staged)])
+        runner.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
     runner.synchronize()
     t0 = time.perf_counter()
     marks = []
     for k in range(args.steps):
         if k >= 2:
             runner.wait(k - 2)
-        runner.submit(k, staged[k % len(staged)])
+        runner.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
         marks.append(time.perf_counter())
     runner.wait(args.steps - 1)
     runner.wait(args.steps - 2)
@@ -495,7 +496,13 @@ def main() -> None:
                     "h2d_alone_ms": h2d_ms,
                     "host_cpus": "all" if numa_cpus is None else f"{len(numa_cpus)} on the GPU's NUMA node",
                     "h2d_gbs": pipe.h2d_bytes() / (h2d_ms / 1e3) / 1e9,
-                    "h2d_bytes_per_step": pipe.h2d_bytes() + e2e_delta // max(1, args.steps),
+                    "h2d_bytes_per_step": int((shipped if e2e_method == "async" else
+                                               pipe.h2d_bytes()) + e2e_delta / max(1, args.steps)),
+                    "h2d_bytes_per_step_async": int(shipped),
+                    "h2d_bytes_per_step_serial": pipe.h2d_bytes(),
+                    "pyramid_levels_shipped": "levels >= the frame's lowest left-keypoint octave "
+                                              "(phase 2 reads no others)"
+                                              if pipe.level_ranges else "all",
                     "d2h_bytes_per_step": pipe.d2h_bytes(),
                     "map_table": None if table is None else {
                         "resident_points": table.size, "upload_bytes_once": table_bytes,
@@ -589,11 +596,13 @@ def make_runner(args, frames, pipe, table, load):
                          build_levels=pipe.build_levels if pipe.raw else None)
     n = max(1, min(len(frames), int(os.environ.get("FT_BENCH_RING", str(len(frames))))))
     ring = pipe.staging_ring(n)
+    ranges = []
     for k in range(n):
         load(k)
         pipe.stage_into(ring[k])
+        ranges.append(pipe.input_range())
     twin.capture()
-    return AsyncRunner([pipe, twin]), [ring[k] for k in range(n)]
+    return AsyncRunner([pipe, twin]), [ring[k] for k in range(n)], ranges
 
 
 def _pipe_rates(torch, pipes, staged, steps, flush, S) -> dict:

@@ -277,6 +277,10 @@ int ft_runner_create(const void *const graph_exec[2], void *const dev_in[2], siz
                      void *const dev_out[2], void *const host_out[2], size_t out_bytes,
                      ft_runner **out);
 int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in);
+/* As ft_runner_submit, copying only bytes [offset, offset + bytes) of the
+ * step's inputs (the rest of the slot's device inputs is left as is). */
+int ft_runner_submit_range(ft_runner *r, int64_t k, const void *host_in, size_t offset,
+                           size_t bytes);
 int ft_runner_wait(ft_runner *r, int64_t k);
 int ft_runner_destroy(ft_runner *r);
 

@@ -66,13 +66,16 @@ extern "C" int ft_runner_create(const void *const graph_exec[2], void *const dev
     return FT_OK;
 }
 
-extern "C" int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in) {
+extern "C" int ft_runner_submit_range(ft_runner *r, int64_t k, const void *host_in,
+                                      size_t offset, size_t bytes) {
     if (!r || !host_in) return FT_E_NULL;
-    if (k < 0) return FT_E_RANGE;
+    if (k < 0 || offset > r->in_bytes || bytes > r->in_bytes - offset) return FT_E_RANGE;
     const int i = (int)(k & 1);
     cudaError_t e = cudaStreamWaitEvent(r->h2d, r->ev_comp[i], 0);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(r->dev_in[i], host_in, r->in_bytes, cudaMemcpyHostToDevice, r->h2d);
+    if (e == cudaSuccess && bytes)
+        e = cudaMemcpyAsync(static_cast<char *>(r->dev_in[i]) + offset,
+                            static_cast<const char *>(host_in) + offset, bytes,
+                            cudaMemcpyHostToDevice, r->h2d);
     if (e == cudaSuccess) e = cudaEventRecord(r->ev_h2d[i], r->h2d);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(r->comp, r->ev_h2d[i], 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(r->comp, r->ev_d2h[i], 0);
@@ -84,6 +87,11 @@ extern "C" int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in) {
                             r->d2h);
     if (e == cudaSuccess) e = cudaEventRecord(r->ev_d2h[i], r->d2h);
     return (int)e;
+}
+
+extern "C" int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in) {
+    if (!r) return FT_E_NULL;
+    return ft_runner_submit_range(r, k, host_in, 0, r->in_bytes);
 }
 
 extern "C" int ft_runner_wait(ft_runner *r, int64_t k) {

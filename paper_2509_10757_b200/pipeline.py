@@ -77,6 +77,18 @@ class FramePipeline:
 
         S, ck, cp = self.S, self.cap_kp, self.cap_pts
         lay = Layout()
+        # per-image pyramid stride padded to 256 B: 16-B vector copies of level 0
+        self.pyr_total = int(self.pyr.offsets[-1]) if self.pyr is not None else 0
+        self.pyr_bytes = (self.pyr_total + 255) // 256 * 256
+        # single stream, pyramids shipped: [right pyramid, levels 0..L-1 | small
+        # inputs | left pyramid, levels L-1..0].  Phase 2 reads only levels >=
+        # the lowest left-keypoint octave m (kernels.py:351-428 reads level o of
+        # both images for a left keypoint of octave o), and those bytes form ONE
+        # contiguous range around the small inputs: input_range() ships just
+        # that (the whole pyramid when an octave-0 keypoint exists).
+        self.level_ranges = (self.pyr is not None and not self.raw and S == 1)
+        if self.level_ranges:
+            lay.add("pyrR", self.pyr_bytes)
         # small per-frame inputs first (one 2 MB page holds them for a frame),
         # then the pyramids, then the outputs: the map blocks' reads all land
         # in the first page, so a cold TLB costs them one page walk
@@ -91,9 +103,6 @@ class FramePipeline:
         lay.add("rot", 72 * S)
         lay.add("trans", 24 * S)
         lay.add("slots_in", 8 * S * ck)
-        # per-image pyramid stride padded to 256 B: 16-B vector copies of level 0
-        self.pyr_total = int(self.pyr.offsets[-1]) if self.pyr is not None else 0
-        self.pyr_bytes = (self.pyr_total + 255) // 256 * 256
         self.img_bytes = int(self.pyr.widths[0]) * int(self.pyr.heights[0]) if self.pyr is not None else 0
         self.upper_off = int(self.pyr.offsets[self.build_levels + 1]) if self.raw else 0
         self.upper_bytes = self.pyr_total - self.upper_off if self.raw else 0
@@ -101,9 +110,17 @@ class FramePipeline:
             lay.add("imgs", 2 * S * self.img_bytes)  # [left x S | right x S]
             if self.upper_bytes:
                 lay.add("upper", 2 * S * self.upper_bytes)
+        elif self.level_ranges:
+            lay.add("pyrL", self.pyr_bytes)
+            sizes = np.diff(np.asarray(self.pyr.offsets, dtype=np.int64))
+            self.lvl_size = sizes
+            # reversed-order offsets of the left pyramid: level l after levels > l
+            self.rev_off = np.array([int(sizes[l + 1:].sum()) for l in range(len(sizes))],
+                                    dtype=np.int64)
         elif self.pyr is not None:
             lay.add("pyrs", 2 * S * self.pyr_bytes)
         self.in_end = lay.total
+        self.cur_range = (0, self.in_end)
         self.out_begin = lay.total
         lay.add("slots", 8 * S * ck)   # updated slots (output)
         for name in ("right_idx", "distance", "disparity", "refined_u", "depth", "sad"):
@@ -166,6 +183,20 @@ class FramePipeline:
                     up = self._h("upper", np.uint8, (2, S, self.upper_bytes))
                     up[0, s] = np.asarray(pyr_left.data)[self.upper_off:self.pyr_total]
                     up[1, s] = np.asarray(pyr_right.data)[self.upper_off:self.pyr_total]
+            elif self.level_ranges:
+                self._h("pyrR", np.uint8, (self.pyr_total,))[:] = pyr_right.data
+                dl = self._h("pyrL", np.uint8, (self.pyr_total,))
+                src = np.asarray(pyr_left.data)
+                offs = np.asarray(self.pyr.offsets, dtype=np.int64)
+                for lv in range(len(self.lvl_size)):
+                    dl[self.rev_off[lv]:self.rev_off[lv] + self.lvl_size[lv]] = \
+                        src[offs[lv]:offs[lv + 1]]
+                oct_ = np.asarray(left.octave)
+                m = int(oct_.min()) if len(oct_) else len(self.lvl_size) - 1
+                m = min(max(m, 0), len(self.lvl_size) - 1)
+                lo = self.lay.offsets["pyrR"] + int(offs[m])
+                hi = self.lay.offsets["pyrL"] + int(self.rev_off[m] + self.lvl_size[m])
+                self.cur_range = (lo, hi)
             else:
                 pb = self.pyr_bytes
                 pyrs = self._h("pyrs", np.uint8, (2, S, pb))
@@ -192,6 +223,12 @@ class FramePipeline:
     def h2d_bytes(self) -> int:
         return self.in_end
 
+    def input_range(self) -> tuple[int, int]:
+        """[lo, hi) of the input staging the current frame needs on the device:
+        the whole input area, or with level ranges the pyramid levels at or
+        above the frame's lowest left-keypoint octave plus the small inputs."""
+        return self.cur_range
+
     def d2h_bytes(self) -> int:
         return self.out_end - self.out_begin
 
@@ -205,7 +242,12 @@ class FramePipeline:
             k.rec, k.count, k.cap = self._d(f"{side}_rec"), self._d(f"{side}_n"), ck
             kps[side] = k
         self.kl, self.kr = kps["L"], kps["R"]
-        if self.pyr is not None:
+        if self.level_ranges:
+            self.pr = pyramid_struct(self.pyr, self._d("pyrR"), self.pyr_bytes)
+            self.pl = pyramid_struct(self.pyr, self._d("pyrL"), self.pyr_bytes)
+            for lv in range(len(self.lvl_size)):
+                self.pl.offsets[lv] = int(self.rev_off[lv])
+        elif self.pyr is not None:
             pyrs = self._d("pyrs")
             self.pl = pyramid_struct(self.pyr, pyrs, self.pyr_bytes)
             self.pr = pyramid_struct(self.pyr, pyrs + S * self.pyr_bytes, self.pyr_bytes)
@@ -393,12 +435,20 @@ class AsyncRunner:
                    "ft_runner_create")
         self._keep = (execs, dev_in, dev_out, host_out)
 
-    def submit(self, k: int, inputs: torch.Tensor | None = None) -> None:
+    def submit(self, k: int, inputs: torch.Tensor | None = None,
+               rng: tuple[int, int] | None = None) -> None:
         """Enqueue step k; inputs = a pinned tensor in the pipelines' input
-        layout (staged_inputs()), or None to send pipes[k % 2]'s own staging."""
+        layout (staged_inputs() / a staging_ring() row), or None to send
+        pipes[k % 2]'s own staging; rng = the [lo, hi) byte range to ship
+        (input_range() of the staged frame), default all."""
         p = self.pipes[k % 2]
         src = p.host.data_ptr() if inputs is None else inputs.data_ptr()
-        _lib.check(self.lib.ft_runner_submit(self._r, k, src), "ft_runner_submit")
+        if rng is None:
+            st = self.lib.ft_runner_submit(self._r, k, src)
+        else:
+            lo, hi = int(rng[0]), int(rng[1])
+            st = self.lib.ft_runner_submit_range(self._r, k, src, lo, hi - lo)
+        _lib.check(st, "ft_runner_submit")
 
     def wait(self, k: int) -> FramePipeline:
         """Block until step k's results are on the host; returns its pipeline

@@ -279,3 +279,46 @@ def test_high_load_batched(oracle):
                                               err_msg=f"stream {s} {f}")
             np.testing.assert_array_equal(r.slots, slots, err_msg=f"stream {s}")
             assert r.n_slots == n
+
+
+def test_level_range_shipping(workloads, expected):
+    """Single-stream ship mode lays the pyramids out as [right 0..L-1 | small
+    inputs | left L-1..0]: shipping only input_range() (levels >= the lowest
+    left octave) through AsyncRunner gives the oracle's results, even with
+    the unshipped levels of the device buffers holding garbage."""
+    import torch
+    from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left) for _ in range(2)]
+    assert pipes[0].level_ranges
+    ring = pipes[0].staging_ring(4)
+    ranges = []
+    for k, w in enumerate(workloads):
+        pipes[0].load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                            slots=expected[k][1])
+        pipes[0].stage_into(ring[k])
+        ranges.append(pipes[0].input_range())
+        lo, hi = ranges[-1]
+        assert hi - lo < pipes[0].in_end  # octaves 5-7: lower levels not shipped
+    for p in pipes:
+        p.dev.fill_(0xAB)  # unshipped levels hold garbage
+        p.capture()
+    runner = AsyncRunner(pipes)
+    for k in range(8):
+        if k >= 2:
+            _check_one(runner.wait(k - 2), workloads, expected, (k - 2) % 4)
+        runner.submit(k, ring[k % 4], ranges[k % 4])
+    for k in (6, 7):
+        _check_one(runner.wait(k), workloads, expected, k % 4)
+
+
+def _check_one(pipe, workloads, expected, i):
+    w = workloads[i]
+    m, _, slots, n = expected[i]
+    res = pipe.result(0, len(w.left.u))
+    for f in FIELDS:
+        np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f), err_msg=f)
+    np.testing.assert_array_equal(res.slots, slots)
+    assert res.n_slots == n
