@@ -605,7 +605,7 @@ def make_runner(args, frames, pipe, table, load):
     return AsyncRunner([pipe, twin]), [ring[k] for k in range(n)], ranges
 
 
-def _pipe_rates(torch, pipes, staged, steps, flush, S) -> dict:
+def _pipe_rates(torch, pipes, staged, steps, flush, S, ranges=None) -> dict:
     """Device frames/s (compute graph, L2 flushed) and e2e frames/s through
     AsyncRunner for a pair of identically shaped pipelines."""
     from paper_2509_10757_b200.pipeline import AsyncRunner
@@ -623,24 +623,30 @@ def _pipe_rates(torch, pipes, staged, steps, flush, S) -> dict:
         p.synchronize()
         comp.append(a.elapsed_time(b))
     runner = AsyncRunner(pipes)
+    rg = ranges if ranges is not None else [None] * len(staged)
     for k in range(4 * len(staged) + 2):
         if k >= 2:
             runner.wait(k - 2)
-        runner.submit(k, staged[k % len(staged)])
+        runner.submit(k, staged[k % len(staged)], rg[k % len(staged)])
     runner.synchronize()
     t0 = time.perf_counter()
     for k in range(steps):
         if k >= 2:
             runner.wait(k - 2)
-        runner.submit(k, staged[k % len(staged)])
+        runner.submit(k, staged[k % len(staged)], rg[k % len(staged)])
     runner.wait(steps - 1)
     runner.wait(steps - 2)
     e2e_ms = 1e3 * (time.perf_counter() - t0)
     runner.close()
+    if ranges is not None:
+        shipped = float(np.mean([sum(hi - lo for lo, hi in (r if isinstance(r[0], (tuple, list))
+                                                              else [r])) for r in ranges]))
+    else:
+        shipped = p.h2d_bytes()
     return {"streams": S, "ms_per_step": float(np.median(comp)),
             "frames_per_s": S * steps / (sum(comp) / 1e3),
             "e2e_frames_per_s": S * steps / (e2e_ms / 1e3),
-            "h2d_bytes_per_step": p.h2d_bytes(), "d2h_bytes_per_step": p.d2h_bytes()}
+            "h2d_bytes_per_step": int(shipped), "d2h_bytes_per_step": p.d2h_bytes()}
 
 
 def other_configs(args, torch, flush) -> dict:
@@ -688,15 +694,17 @@ def other_configs(args, torch, flush) -> dict:
                                pyramid_geometry=hw[0].pyr_left, map_table=table)
                  for _ in range(2)]
         ring = pipes[0].staging_ring(2)
+        rngs = []
         for k in range(2):
             for s in range(S):
                 w = hw[(k + s) % 2]
                 pipes[0].load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
             pipes[0].stage_into(ring[k])
+            rngs.append(pipes[0].input_ranges())
         staged = [ring[0], ring[1]]
         for p in pipes:
             p.capture()
-        res[f"S{S}"] = _pipe_rates(torch, pipes, staged, steps, flush, S)
+        res[f"S{S}"] = _pipe_rates(torch, pipes, staged, steps, flush, S, rngs)
     out["cfg5_high_load"] = {"workload": f"~{int(np.mean([len(w.left.u) for w in hw]))} "
                                          "kps/image 752x480 (pyramids shipped) + 20000-point "
                                          "local map; stereo + SearchLocalPoints",
@@ -717,15 +725,17 @@ def raw_mode_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, flush) -> 
                                pyramid_geometry=w0.pyr_left, raw_images=b > 0, map_table=table,
                                build_levels=b if b > 0 else None) for _ in range(2)]
         ring = pipes[0].staging_ring(len(frames))
+        rngs = []
         for k in range(len(frames)):
             f = frames[k]
             pipes[0].load_frame(0, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
             pipes[0].stage_into(ring[k])
+            rngs.append(pipes[0].input_ranges())
         staged = [ring[k] for k in range(len(frames))]
         for p in pipes:
             p.capture()
-        r = _pipe_rates(torch, pipes, staged, args.steps, flush, 1)
-        out["pyramids_shipped" if b == 0 else f"build_levels_1_to_{b}"] = r
+        r = _pipe_rates(torch, pipes, staged, args.steps, flush, 1, rngs)
+        out["pyramid_levels_shipped" if b == 0 else f"build_levels_1_to_{b}"] = r
     return out
 
 
@@ -755,6 +765,8 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
     ring = pipe.staging_ring(1)
     pipe.stage_into(ring[0])
     staged = ring[0]
+    rngs = pipe.input_ranges()
+    shipped = int(sum(hi - lo for lo, hi in rngs))
     pipe.capture()
     steps = max(5, args.steps // 5)
     for _ in range(3):
@@ -775,13 +787,13 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
     for k in range(max(3, args.warmup)):
         if k >= 2:
             runner.wait(k - 2)
-        runner.submit(k, staged)
+        runner.submit(k, staged, rngs)
     runner.synchronize()
     t0 = time.perf_counter()
     for k in range(steps):
         if k >= 2:
             runner.wait(k - 2)
-        runner.submit(k, staged)
+        runner.submit(k, staged, rngs)
     runner.wait(steps - 1)
     runner.wait(steps - 2)
     e2e_ms = 1e3 * (time.perf_counter() - t0)
@@ -790,7 +802,8 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
             "ms_per_step": float(np.mean(comp)),
             "frames_per_s": S * steps / (sum(comp) / 1e3),
             "e2e_frames_per_s": S * steps / (e2e_ms / 1e3),
-            "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes()}
+            "h2d_bytes_per_step": shipped, "h2d_ranges_per_step": len(rngs),
+            "d2h_bytes_per_step": pipe.d2h_bytes()}
 
 if __name__ == "__main__":
     main()

@@ -281,6 +281,11 @@ int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in);
  * step's inputs (the rest of the slot's device inputs is left as is). */
 int ft_runner_submit_range(ft_runner *r, int64_t k, const void *host_in, size_t offset,
                            size_t bytes);
+/* As ft_runner_submit, copying the n_ranges byte ranges [ranges[2q],
+ * ranges[2q+1]) (e.g. the small inputs plus each stream's needed pyramid
+ * levels). */
+int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host_in,
+                            const uint64_t *ranges, int32_t n_ranges);
 int ft_runner_wait(ft_runner *r, int64_t k);
 int ft_runner_destroy(ft_runner *r);
 

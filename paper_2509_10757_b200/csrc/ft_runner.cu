@@ -89,6 +89,34 @@ extern "C" int ft_runner_submit_range(ft_runner *r, int64_t k, const void *host_
     return (int)e;
 }
 
+extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host_in,
+                                       const uint64_t *ranges, int32_t n_ranges) {
+    if (!r || !host_in || (!ranges && n_ranges > 0)) return FT_E_NULL;
+    if (k < 0 || n_ranges < 0) return FT_E_RANGE;
+    for (int q = 0; q < n_ranges; ++q)
+        if (ranges[2 * q] > ranges[2 * q + 1] || ranges[2 * q + 1] > r->in_bytes) return FT_E_RANGE;
+    const int i = (int)(k & 1);
+    cudaError_t e = cudaStreamWaitEvent(r->h2d, r->ev_comp[i], 0);
+    for (int q = 0; q < n_ranges && e == cudaSuccess; ++q) {
+        const size_t lo = ranges[2 * q], n = ranges[2 * q + 1] - lo;
+        if (n)
+            e = cudaMemcpyAsync(static_cast<char *>(r->dev_in[i]) + lo,
+                                static_cast<const char *>(host_in) + lo, n,
+                                cudaMemcpyHostToDevice, r->h2d);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(r->ev_h2d[i], r->h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(r->comp, r->ev_h2d[i], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(r->comp, r->ev_d2h[i], 0);
+    if (e == cudaSuccess) e = cudaGraphLaunch(r->exec[i], r->comp);
+    if (e == cudaSuccess) e = cudaEventRecord(r->ev_comp[i], r->comp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(r->d2h, r->ev_comp[i], 0);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(r->host_out[i], r->dev_out[i], r->out_bytes, cudaMemcpyDeviceToHost,
+                            r->d2h);
+    if (e == cudaSuccess) e = cudaEventRecord(r->ev_d2h[i], r->d2h);
+    return (int)e;
+}
+
 extern "C" int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in) {
     if (!r) return FT_E_NULL;
     return ft_runner_submit_range(r, k, host_in, 0, r->in_bytes);

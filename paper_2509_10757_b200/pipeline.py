@@ -86,8 +86,11 @@ class FramePipeline:
         # both images for a left keypoint of octave o), and those bytes form ONE
         # contiguous range around the small inputs: input_range() ships just
         # that (the whole pyramid when an octave-0 keypoint exists).
-        self.level_ranges = (self.pyr is not None and not self.raw and S == 1)
-        if self.level_ranges:
+        # S > 1: [small inputs | R_0 L_0 | R_1 L_1 | ...] (each stream's right
+        # pyramid normal, left reversed): one range for the small inputs and one
+        # per stream (input_ranges()).
+        self.level_ranges = (self.pyr is not None and not self.raw)
+        if self.level_ranges and S == 1:
             lay.add("pyrR", self.pyr_bytes)
         # small per-frame inputs first (one 2 MB page holds them for a frame),
         # then the pyramids, then the outputs: the map blocks' reads all land
@@ -111,7 +114,11 @@ class FramePipeline:
             if self.upper_bytes:
                 lay.add("upper", 2 * S * self.upper_bytes)
         elif self.level_ranges:
-            lay.add("pyrL", self.pyr_bytes)
+            self.small_end = lay.total
+            if S == 1:
+                lay.add("pyrL", self.pyr_bytes)
+            else:
+                lay.add("pairs", 2 * S * self.pyr_bytes)
             sizes = np.diff(np.asarray(self.pyr.offsets, dtype=np.int64))
             self.lvl_size = sizes
             # reversed-order offsets of the left pyramid: level l after levels > l
@@ -121,6 +128,7 @@ class FramePipeline:
             lay.add("pyrs", 2 * S * self.pyr_bytes)
         self.in_end = lay.total
         self.cur_range = (0, self.in_end)
+        self.stream_m = np.zeros(S, dtype=np.int64)  # lowest left octave per stream
         self.out_begin = lay.total
         lay.add("slots", 8 * S * ck)   # updated slots (output)
         for name in ("right_idx", "distance", "disparity", "refined_u", "depth", "sad"):
@@ -184,8 +192,14 @@ class FramePipeline:
                     up[0, s] = np.asarray(pyr_left.data)[self.upper_off:self.pyr_total]
                     up[1, s] = np.asarray(pyr_right.data)[self.upper_off:self.pyr_total]
             elif self.level_ranges:
-                self._h("pyrR", np.uint8, (self.pyr_total,))[:] = pyr_right.data
-                dl = self._h("pyrL", np.uint8, (self.pyr_total,))
+                if S == 1:
+                    dr = self._h("pyrR", np.uint8, (self.pyr_total,))
+                    dl = self._h("pyrL", np.uint8, (self.pyr_total,))
+                else:
+                    pairs = self._h("pairs", np.uint8, (S, 2, self.pyr_bytes))
+                    dr = pairs[s, 0, :self.pyr_total]
+                    dl = pairs[s, 1, :self.pyr_total]
+                dr[:] = pyr_right.data
                 src = np.asarray(pyr_left.data)
                 offs = np.asarray(self.pyr.offsets, dtype=np.int64)
                 for lv in range(len(self.lvl_size)):
@@ -194,9 +208,11 @@ class FramePipeline:
                 oct_ = np.asarray(left.octave)
                 m = int(oct_.min()) if len(oct_) else len(self.lvl_size) - 1
                 m = min(max(m, 0), len(self.lvl_size) - 1)
-                lo = self.lay.offsets["pyrR"] + int(offs[m])
-                hi = self.lay.offsets["pyrL"] + int(self.rev_off[m] + self.lvl_size[m])
-                self.cur_range = (lo, hi)
+                self.stream_m[s] = m
+                if S == 1:
+                    lo = self.lay.offsets["pyrR"] + int(offs[m])
+                    hi = self.lay.offsets["pyrL"] + int(self.rev_off[m] + self.lvl_size[m])
+                    self.cur_range = (lo, hi)
             else:
                 pb = self.pyr_bytes
                 pyrs = self._h("pyrs", np.uint8, (2, S, pb))
@@ -229,6 +245,25 @@ class FramePipeline:
         above the frame's lowest left-keypoint octave plus the small inputs."""
         return self.cur_range
 
+    def input_ranges(self) -> list[tuple[int, int]]:
+        """The [lo, hi) byte ranges of the input staging the current step
+        needs: one for S == 1 (input_range()); for S > 1 with level ranges the
+        small inputs plus, per stream, its pyramid pair's levels >= that
+        stream's lowest left octave; else the whole input area."""
+        if not self.level_ranges:
+            return [(0, self.in_end)]
+        if self.S == 1:
+            return [self.cur_range]
+        pb, base = self.pyr_bytes, self.lay.offsets["pairs"]
+        offs = np.asarray(self.pyr.offsets, dtype=np.int64)
+        out = [(0, self.small_end)]
+        for st in range(self.S):
+            m = int(self.stream_m[st])
+            lo = base + 2 * st * pb + int(offs[m])
+            hi = base + (2 * st + 1) * pb + int(self.rev_off[m] + self.lvl_size[m])
+            out.append((lo, hi))
+        return out
+
     def d2h_bytes(self) -> int:
         return self.out_end - self.out_begin
 
@@ -243,8 +278,13 @@ class FramePipeline:
             kps[side] = k
         self.kl, self.kr = kps["L"], kps["R"]
         if self.level_ranges:
-            self.pr = pyramid_struct(self.pyr, self._d("pyrR"), self.pyr_bytes)
-            self.pl = pyramid_struct(self.pyr, self._d("pyrL"), self.pyr_bytes)
+            if S == 1:
+                self.pr = pyramid_struct(self.pyr, self._d("pyrR"), self.pyr_bytes)
+                self.pl = pyramid_struct(self.pyr, self._d("pyrL"), self.pyr_bytes)
+            else:  # stream s: right at pairs + 2 s pb, left at pairs + (2 s + 1) pb
+                self.pr = pyramid_struct(self.pyr, self._d("pairs"), 2 * self.pyr_bytes)
+                self.pl = pyramid_struct(self.pyr, self._d("pairs") + self.pyr_bytes,
+                                         2 * self.pyr_bytes)
             for lv in range(len(self.lvl_size)):
                 self.pl.offsets[lv] = int(self.rev_off[lv])
         elif self.pyr is not None:
@@ -445,6 +485,10 @@ class AsyncRunner:
         src = p.host.data_ptr() if inputs is None else inputs.data_ptr()
         if rng is None:
             st = self.lib.ft_runner_submit(self._r, k, src)
+        elif isinstance(rng[0], (tuple, list)):  # several ranges (input_ranges())
+            import ctypes
+            flat = (ctypes.c_uint64 * (2 * len(rng)))(*[int(x) for r in rng for x in r])
+            st = self.lib.ft_runner_submit_ranges(self._r, k, src, flat, len(rng))
         else:
             lo, hi = int(rng[0]), int(rng[1])
             st = self.lib.ft_runner_submit_range(self._r, k, src, lo, hi - lo)
