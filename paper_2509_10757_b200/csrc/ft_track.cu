@@ -709,6 +709,7 @@ struct MapSmem {
     int *res_empty;     // [chunk] slots_in[kp] == NO_POINT
     int *scan_tmp, *misc;
     int *hist;  // [TK_MAX_BINS / 32] kept-bin mask
+    double *pose;  // [12] R (row-major) | t of the frame, loaded at block start
 };
 
 FT_DEV unsigned hash_slot(long long id, int bits) {
@@ -903,6 +904,14 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     sm.items = reinterpret_cast<uint16_t *>(p);
     p += (size_t)2 * cap_kp;
     sm.binbuf = reinterpret_cast<uint16_t *>(p);
+    p += (size_t)2 * cap_kp;
+    sm.pose = reinterpret_cast<double *>(((uintptr_t)p + 7) & ~(uintptr_t)7);
+    // the frame's pose is read by every projection: fetch it now, off the
+    // critical path (cold HBM), with the other first-touch loads
+    if (threadIdx.x >= TK_THREADS - 12) {
+        const int t = threadIdx.x - (TK_THREADS - 12);
+        sm.pose[t] = t < 9 ? __ldg(a.io.rot + 9 * (int64_t)f + t) : __ldg(a.io.trans + 3 * (int64_t)f + t - 9);
+    }
 
     TL_MARK(a, 0);
     const bool have_pts = p0 < p1;
@@ -1009,7 +1018,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             },
             sm.cell_start, sm.cell_cursor, sm.items, sm.binbuf);
         TL_MARK(a, 1);
-        const double *R = a.io.rot + 9 * f, *T = a.io.trans + 3 * f;
+        const double *R = sm.pose, *T = sm.pose + 9;
         const double ccx = -(R[0] * T[0] + R[3] * T[1] + R[6] * T[2]);
         const double ccy = -(R[1] * T[0] + R[4] * T[1] + R[7] * T[2]);
         const double ccz = -(R[2] * T[0] + R[5] * T[1] + R[8] * T[2]);
@@ -1251,7 +1260,8 @@ size_t map_smem(const TrackArgs &a) {
     return 16 + (a.stage_kdesc ? (size_t)64 * cap : 0) + (size_t)112 * round_cap +
            (hash ? (size_t)8 * cap : 0) + sizeof(QItem) * (size_t)round_cap +
            (hash ? ((size_t)4 << a.hash_bits) : 0) + 4 * (32 + 16 + TK_MAX_BINS / 32) +
-           16 * (size_t)a.map_chunk_cap + 4 * (size_t)(2 * ncell + 1) + 4 * (size_t)cap + 64;
+           16 * (size_t)a.map_chunk_cap + 4 * (size_t)(2 * ncell + 1) + 4 * (size_t)cap + 64 +
+           12 * 8 + 8;  // pose
 }
 
 }  // namespace ft
