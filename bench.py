@@ -543,6 +543,7 @@ def main() -> None:
                                                         cap_kp, cap_pts, flush))
         if world == 1 and not args.no_configs:
             extra("other_configs", lambda: other_configs(args, torch, flush))
+            extra("roofline_hamming", lambda: hamming_roofline(torch, _lib, popc))
         if world == 1:  # reported baseline: rank 0 at N=1 only
             extra("cpu_baseline", lambda: cpu_baseline(frames[:2], args.cpu_seconds))
     print(json.dumps(line))
@@ -647,6 +648,62 @@ def _pipe_rates(torch, pipes, staged, steps, flush, S, ranges=None) -> dict:
             "frames_per_s": S * steps / (sum(comp) / 1e3),
             "e2e_frames_per_s": S * steps / (e2e_ms / 1e3),
             "h2d_bytes_per_step": int(shipped), "d2h_bytes_per_step": p.d2h_bytes()}
+
+
+def hamming_roofline(torch, _lib, popc_peak_g) -> dict:
+    """The all-pairs Hamming kernel (fisheye stereo, kernels.py:434-464) at
+    cfg3 shape, 1 and 64 frames per launch: achieved POPC/s (8 per 256-bit
+    Hamming, the algorithmic count) over the measured POPC peak -- the north
+    star's integer-pipe roofline target for the Hamming kernels."""
+    from paper_2509_10757_b200.runtime import fill_kp_records, make_workspace
+    from paper_2509_10757_b200.synthetic import make_workload
+    from paper_2509_10757_b200.types import StereoMatchConfig
+    w = make_workload(seed=700, n_landmarks=4800, map_points=100, fisheye=True)
+    nl, nr = len(w.left.u), len(w.right.u)
+    cap = (max(nl, nr) + 255) // 256 * 256
+    lib = _lib.load()
+    cfg = StereoMatchConfig()
+    out = {"bound": "popc (XU pipe)", "unit": "G popc/s", "peak": popc_peak_g,
+           "peak_source": "ft_bench_popc (measured, same run)",
+           "work": f"{nl} x {nr} Hamming per frame, 8 POPC each"}
+    for F in (1, 64):
+        recs = np.zeros((2, F, cap), dtype=_lib.KP_RECORD)
+        for f in range(F):
+            fill_kp_records(recs[0, f], w.left)
+            fill_kp_records(recs[1, f], w.right)
+        dev = torch.from_numpy(recs.view(np.uint8).reshape(-1)).cuda()
+        cnt = torch.tensor([nl] * F + [nr] * F, dtype=torch.int32, device="cuda")
+        kl, kr = _lib.FtKeypoints(), _lib.FtKeypoints()
+        kl.rec, kl.count, kl.cap = dev.data_ptr(), cnt.data_ptr(), cap
+        kr.rec, kr.count, kr.cap = dev.data_ptr() + F * cap * 64, cnt.data_ptr() + 4 * F, cap
+        idx = torch.empty(F * cap, dtype=torch.int64, device="cuda")
+        dist = torch.empty_like(idx)
+        stream = torch.cuda.Stream()
+        ws = make_workspace(lib, torch.device("cuda"), stream, F, cap, 1)
+
+        def launch():
+            _lib.check(lib.ft_stereo_fisheye_bf(F, kl, kr, cfg.t_match, cfg.ratio, idx.data_ptr(),
+                                                dist.data_ptr(), ws, stream.cuda_stream), "bf")
+
+        launch()
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            launch()
+        ts = []
+        with torch.cuda.stream(stream):
+            for _ in range(20):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                g.replay()
+                b.record(stream)
+                stream.synchronize()
+                ts.append(a.elapsed_time(b))
+        ms = float(np.median(ts))
+        achieved = 8 * F * nl * nr / (ms / 1e3) / 1e9
+        out[f"frames_{F}"] = {"launch_ms": ms, "achieved": achieved,
+                              "frac": achieved / popc_peak_g if popc_peak_g else None}
+    return out
 
 
 def other_configs(args, torch, flush) -> dict:

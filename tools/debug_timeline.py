@@ -1,5 +1,5 @@
 """Per-block phase timeline of ft_track_frames (debug tool, run on the GPU box):
-    FT_DEBUG_TIMELINE=gpurun_out/tl.txt python tests/debug_timeline.py"""
+    FT_DEBUG_TIMELINE=gpurun_out/tl.txt python tools/debug_timeline.py"""
 import os
 import sys
 
