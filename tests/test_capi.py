@@ -62,3 +62,34 @@ def test_argument_validation_without_gpu():
     assert L.ft_resolve_conflicts(0, None, None, None, 0, None, None, None) == -1
     assert L.ft_rotation_filter(0, None, None, None, None, None, None, 0, 1,
                                 ctypes.byref(ctypes.c_int32()), None) == -4
+
+
+def test_new_entries_validate_without_gpu():
+    """Entries added with the resident map, the fisheye triangulation, the
+    pyramid build and the native runner reject bad arguments before any CUDA
+    call."""
+    L = _lib.load()
+    kp = _lib.FtKeypoints()
+    ws = _lib.FtWorkspace()
+    # ft_stereo_fisheye: missing triangulation terms / outputs
+    assert L.ft_stereo_fisheye(1, kp, kp, 100, 0.8, None, None, None, None, None, ws, None) == -1
+    tri = _lib.FtFisheyeTri()
+    assert L.ft_stereo_fisheye(1, kp, kp, 100, 0.8, tri, None, None, None, None, ws, None) == -4
+    tri.fx = tri.fy = 190.0
+    assert L.ft_stereo_fisheye(1, kp, kp, 100, 0.8, tri, None, None, None, None, ws, None) == -1
+    # map table gather / scatter
+    assert L.ft_gather_points(1, None, 10, None, None, 4, None, None, None) == -1
+    assert L.ft_scatter_points(0, None, None, None, 10, None) == 0  # empty delta: no-op
+    assert L.ft_scatter_points(3, None, None, None, 10, None) == -1
+    # pyramid build
+    assert L.ft_build_pyramids(1, None, None, 0, ws, None) == -1
+    # native runner
+    vp2 = ctypes.c_void_p * 2
+    out = ctypes.c_void_p()
+    assert L.ft_runner_create(vp2(None, None), vp2(None, None), 16, vp2(None, None),
+                              vp2(None, None), 16, ctypes.byref(out)) == -1
+    assert L.ft_runner_submit(None, 0, None) == -1
+    assert L.ft_runner_submit_range(None, 0, None, 0, 0) == -1
+    assert L.ft_runner_submit_ranges(None, 0, None, None, 0) == -1
+    assert L.ft_runner_wait(None, 0) == -1
+    assert L.ft_runner_destroy(None) == 0
