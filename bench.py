@@ -391,19 +391,19 @@ def main() -> None:
         dist.barrier()
     # warm-up: every staged pinned buffer's first DMA is slow (one cycle)
     for k in range(max(args.warmup, 4 * len(staged) + 2)):
-        if k >= 2:
-            runner.wait(k - 2)
+        if k >= runner.n:
+            runner.wait(k - runner.n)
         runner.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
     runner.synchronize()
     t0 = time.perf_counter()
     marks = []
     for k in range(args.steps):
-        if k >= 2:
-            runner.wait(k - 2)
+        if k >= runner.n:
+            runner.wait(k - runner.n)
         runner.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
         marks.append(time.perf_counter())
-    runner.wait(args.steps - 1)
-    runner.wait(args.steps - 2)
+    for k in range(max(0, args.steps - runner.n), args.steps):
+        runner.wait(k)
     async_ms = 1e3 * (time.perf_counter() - t0)
     if os.environ.get("FT_BENCH_DIAG"):
         d = np.diff(np.array([t0] + marks)) * 1e6
@@ -592,9 +592,12 @@ def make_runner(args, frames, pipe, table, load):
     """A second pipeline of the same shape + AsyncRunner, and every cycled
     frame's inputs pre-staged in pinned host memory (one tensor per step)."""
     from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
-    twin = FramePipeline(pipe.cam, n_streams=pipe.S, cap_kp=pipe.cap_kp, cap_points=pipe.cap_pts,
-                         pyramid_geometry=pipe.pyr, raw_images=pipe.raw, map_table=table,
-                         build_levels=pipe.build_levels if pipe.raw else None)
+    n_slots = max(2, min(4, int(os.environ.get("FT_BENCH_SLOTS", "4"))))
+    twins = [FramePipeline(pipe.cam, n_streams=pipe.S, cap_kp=pipe.cap_kp,
+                           cap_points=pipe.cap_pts, pyramid_geometry=pipe.pyr,
+                           raw_images=pipe.raw, map_table=table,
+                           build_levels=pipe.build_levels if pipe.raw else None)
+             for _ in range(n_slots - 1)]
     n = max(1, min(len(frames), int(os.environ.get("FT_BENCH_RING", str(len(frames))))))
     ring = pipe.staging_ring(n)
     ranges = []
@@ -602,8 +605,9 @@ def make_runner(args, frames, pipe, table, load):
         load(k)
         pipe.stage_into(ring[k])
         ranges.append(pipe.input_range())
-    twin.capture()
-    return AsyncRunner([pipe, twin]), [ring[k] for k in range(n)], ranges
+    for t in twins:
+        t.capture()
+    return AsyncRunner([pipe] + twins), [ring[k] for k in range(n)], ranges
 
 
 def _pipe_rates(torch, pipes, staged, steps, flush, S, ranges=None) -> dict:
@@ -626,17 +630,17 @@ def _pipe_rates(torch, pipes, staged, steps, flush, S, ranges=None) -> dict:
     runner = AsyncRunner(pipes)
     rg = ranges if ranges is not None else [None] * len(staged)
     for k in range(4 * len(staged) + 2):
-        if k >= 2:
-            runner.wait(k - 2)
+        if k >= runner.n:
+            runner.wait(k - runner.n)
         runner.submit(k, staged[k % len(staged)], rg[k % len(staged)])
     runner.synchronize()
     t0 = time.perf_counter()
     for k in range(steps):
-        if k >= 2:
-            runner.wait(k - 2)
+        if k >= runner.n:
+            runner.wait(k - runner.n)
         runner.submit(k, staged[k % len(staged)], rg[k % len(staged)])
-    runner.wait(steps - 1)
-    runner.wait(steps - 2)
+    for k in range(max(0, steps - runner.n), steps):
+        runner.wait(k)
     e2e_ms = 1e3 * (time.perf_counter() - t0)
     runner.close()
     if ranges is not None:
@@ -842,17 +846,17 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
         comp.append(a.elapsed_time(b))
     runner = AsyncRunner(pipes)
     for k in range(max(3, args.warmup)):
-        if k >= 2:
-            runner.wait(k - 2)
+        if k >= runner.n:
+            runner.wait(k - runner.n)
         runner.submit(k, staged, rngs)
     runner.synchronize()
     t0 = time.perf_counter()
     for k in range(steps):
-        if k >= 2:
-            runner.wait(k - 2)
+        if k >= runner.n:
+            runner.wait(k - runner.n)
         runner.submit(k, staged, rngs)
-    runner.wait(steps - 1)
-    runner.wait(steps - 2)
+    for k in range(max(0, steps - runner.n), steps):
+        runner.wait(k)
     e2e_ms = 1e3 * (time.perf_counter() - t0)
     return {"streams": S, "steps": steps, "raw_images": bool(raw),
             "build_levels": (pipe.build_levels if raw else None),

@@ -265,17 +265,22 @@ int ft_gather_points(int32_t n_frames, const ft_point_record *table, int64_t tab
 int ft_scatter_points(int32_t n, const ft_point_record *recs, const int32_t *slots,
                       ft_point_record *table, int64_t table_size, ft_stream_t stream);
 
-/* Native double-buffered step executor (csrc/ft_runner.cu): per step k, on
- * three streams, H2D of host_in into slot k % 2's device inputs, a launch of
+/* Native multi-buffered step executor (csrc/ft_runner.cu): per step k, on
+ * three streams, H2D of host_in into slot k % n's device inputs, a launch of
  * that slot's instantiated compute graph (cudaGraphExec_t, captured by the
  * caller), and D2H of its outputs into the slot's pinned host range.
  * Neighbouring steps' copies overlap the compute; computes are serialised.
  * ft_runner_wait(k) blocks until step k's outputs are on the host.  Slot
- * buffers are reused two steps later (the runner orders that itself). */
+ * buffers are reused n steps later (the runner orders that itself). */
 typedef struct ft_runner ft_runner;
+#define FT_RUNNER_MAX_SLOTS 4
 int ft_runner_create(const void *const graph_exec[2], void *const dev_in[2], size_t in_bytes,
                      void *const dev_out[2], void *const host_out[2], size_t out_bytes,
                      ft_runner **out);
+/* n_slots (2..FT_RUNNER_MAX_SLOTS) buffer sets used round robin (slot k % n). */
+int ft_runner_create_n(int32_t n_slots, const void *const *graph_exec, void *const *dev_in,
+                       size_t in_bytes, void *const *dev_out, void *const *host_out,
+                       size_t out_bytes, ft_runner **out);
 int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in);
 /* As ft_runner_submit, copying only bytes [offset, offset + bytes) of the
  * step's inputs (the rest of the slot's device inputs is left as is). */

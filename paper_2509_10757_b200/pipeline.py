@@ -452,27 +452,29 @@ class AsyncRunner:
 
     def __init__(self, pipes):
         import ctypes
-        if len(pipes) != 2:
-            raise ValueError("AsyncRunner takes two identically shaped FramePipelines")
-        a, b = pipes
-        if (a.S, a.cap_kp, a.cap_pts, a.in_end, a.out_begin, a.out_end) != \
-                (b.S, b.cap_kp, b.cap_pts, b.in_end, b.out_begin, b.out_end):
-            raise ValueError("AsyncRunner pipelines differ in shape")
+        if not 2 <= len(pipes) <= 4:
+            raise ValueError("AsyncRunner takes 2..4 identically shaped pipelines")
+        a = pipes[0]
+        for b in pipes[1:]:
+            if (a.S, a.cap_kp, a.cap_pts, a.in_end, a.out_begin, a.out_end) != \
+                    (b.S, b.cap_kp, b.cap_pts, b.in_end, b.out_begin, b.out_end):
+                raise ValueError("AsyncRunner pipelines differ in shape")
         self.pipes = pipes
+        self.n = len(pipes)
         self.lib = a.lib
         for p in pipes:
             if p.graph_compute is None:
                 p.capture()
-        vp2 = ctypes.c_void_p * 2
-        execs = vp2(*[_graph_exec_ptr(p.graph_compute) for p in pipes])
-        dev_in = vp2(*[p.dev.data_ptr() for p in pipes])
-        dev_out = vp2(*[p.dev.data_ptr() + p.out_begin for p in pipes])
-        host_out = vp2(*[p.host.data_ptr() + p.out_begin for p in pipes])
+        vpn = ctypes.c_void_p * self.n
+        execs = vpn(*[_graph_exec_ptr(p.graph_compute) for p in pipes])
+        dev_in = vpn(*[p.dev.data_ptr() for p in pipes])
+        dev_out = vpn(*[p.dev.data_ptr() + p.out_begin for p in pipes])
+        host_out = vpn(*[p.host.data_ptr() + p.out_begin for p in pipes])
         self._r = ctypes.c_void_p()
         torch.cuda.synchronize(a.device)
-        _lib.check(self.lib.ft_runner_create(execs, dev_in, a.in_end, dev_out, host_out,
-                                             a.out_end - a.out_begin, ctypes.byref(self._r)),
-                   "ft_runner_create")
+        _lib.check(self.lib.ft_runner_create_n(self.n, execs, dev_in, a.in_end, dev_out,
+                                               host_out, a.out_end - a.out_begin,
+                                               ctypes.byref(self._r)), "ft_runner_create")
         self._keep = (execs, dev_in, dev_out, host_out)
 
     def submit(self, k: int, inputs: torch.Tensor | None = None,
@@ -481,7 +483,7 @@ class AsyncRunner:
         layout (staged_inputs() / a staging_ring() row), or None to send
         pipes[k % 2]'s own staging; rng = the [lo, hi) byte range to ship
         (input_range() of the staged frame), default all."""
-        p = self.pipes[k % 2]
+        p = self.pipes[k % self.n]
         src = p.host.data_ptr() if inputs is None else inputs.data_ptr()
         if rng is None:
             st = self.lib.ft_runner_submit(self._r, k, src)
@@ -498,7 +500,7 @@ class AsyncRunner:
         """Block until step k's results are on the host; returns its pipeline
         (read them with .result(s, n_left))."""
         _lib.check(self.lib.ft_runner_wait(self._r, k), "ft_runner_wait")
-        return self.pipes[k % 2]
+        return self.pipes[k % self.n]
 
     def synchronize(self) -> None:
         torch.cuda.synchronize(self.pipes[0].device)

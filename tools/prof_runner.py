@@ -140,3 +140,29 @@ def run_h2d_split(parts):
 
 for parts in (1, 2, 4, 1, 2, 4):
     print(f"h2d split {parts}    {run_h2d_split(parts):8.1f} us/step")
+
+
+def run_native_split():
+    """Host time per submit / per wait in the 2-deep loop."""
+    r = AsyncRunner(pipes)
+    for k in range(4):
+        if k >= 2:
+            r.wait(k - 2)
+        r.submit(k, staged)
+    r.synchronize()
+    ts, tw = [], []
+    for k in range(N):
+        t0 = time.perf_counter()
+        if k >= 2:
+            r.wait(k - 2)
+        t1 = time.perf_counter()
+        r.submit(k, staged)
+        t2 = time.perf_counter()
+        tw.append(t1 - t0)
+        ts.append(t2 - t1)
+    r.synchronize()
+    r.close()
+    return 1e6 * np.median(ts), 1e6 * np.median(tw)
+
+
+print("native submit/wait host us: %.1f / %.1f" % run_native_split())
