@@ -727,7 +727,7 @@ def other_configs(args, torch, flush) -> dict:
     for S in (1, 64):
         table = MapTable(capacity=4 * 4096 + 1024)
         pipes = [FisheyePipeline(fw[0].cam, n_streams=S, cap_kp=cap, cap_points=4096,
-                                 map_table=table) for _ in range(2)]
+                                 map_table=table) for _ in range(4)]
         nst = min(4, S * 4)
         ring = pipes[0].staging_ring(nst)
         for k in range(nst):
@@ -753,7 +753,7 @@ def other_configs(args, torch, flush) -> dict:
         table = MapTable(capacity=2 * 20480 + 1024)
         pipes = [FramePipeline(hw[0].cam, n_streams=S, cap_kp=cap, cap_points=20480,
                                pyramid_geometry=hw[0].pyr_left, map_table=table)
-                 for _ in range(2)]
+                 for _ in range(4)]
         ring = pipes[0].staging_ring(2)
         rngs = []
         for k in range(2):
@@ -784,7 +784,7 @@ def raw_mode_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, flush) -> 
         table, _ = make_table(args, frames, cap_pts)
         pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=cap_kp, cap_points=cap_pts,
                                pyramid_geometry=w0.pyr_left, raw_images=b > 0, map_table=table,
-                               build_levels=b if b > 0 else None) for _ in range(2)]
+                               build_levels=b if b > 0 else None) for _ in range(4)]
         ring = pipes[0].staging_ring(len(frames))
         rngs = []
         for k in range(len(frames)):
@@ -818,7 +818,7 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
     pipes = [FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
                            pyramid_geometry=w0.pyr_left if images else None, raw_images=raw,
                            map_table=table, build_levels=b if raw else None)
-             for _ in range(2)]
+             for _ in range(4)]
     pipe = pipes[0]
     for s in range(S):
         f = frames[s % len(frames)]
