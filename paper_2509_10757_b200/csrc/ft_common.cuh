@@ -52,7 +52,11 @@ FT_DEV unsigned long long ld_acquire_u64(const unsigned long long *p) {
 __device__ inline void group_barrier(unsigned long long *ctr, int G) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
+        // acq_rel fences (not the sequentially consistent __threadfence): the
+        // bar.sync above makes the block's writes visible to thread 0, the
+        // release side publishes them with the arrival, the acquire side
+        // orders the block's later reads after every other block's arrival
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         const unsigned long long old = atomicAdd(ctr, 1ull);
         if ((uint32_t)old == (uint32_t)(G - 1)) {
             atomicAdd(ctr, (1ull << 32) - (unsigned long long)G);
@@ -60,7 +64,7 @@ __device__ inline void group_barrier(unsigned long long *ctr, int G) {
             const uint32_t gen = (uint32_t)(old >> 32);
             while ((uint32_t)(ld_acquire_u64(ctr) >> 32) == gen) __nanosleep(32);
         }
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
 }
