@@ -487,7 +487,7 @@ class AsyncRunner:
         src = p.host.data_ptr() if inputs is None else inputs.data_ptr()
         if rng is None:
             st = self.lib.ft_runner_submit(self._r, k, src)
-        elif isinstance(rng[0], (tuple, list)):  # several ranges (input_ranges())
+        elif len(rng) == 0 or isinstance(rng[0], (tuple, list)):  # several (input_ranges())
             import ctypes
             flat = (ctypes.c_uint64 * (2 * len(rng)))(*[int(x) for r in rng for x in r])
             st = self.lib.ft_runner_submit_ranges(self._r, k, src, flat, len(rng))

@@ -59,3 +59,10 @@ t = graph_time(lambda: pipe.launch_track(pipe.stream), reps=50)
 import os  # noqa: E402
 print("track empty frame (cooperative): "
       f"{t:.2f} us per launch (back to back in a graph)")
+
+# real cfg2 frame, back to back (no flush: the e2e steady state's compute)
+pipe.load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
+with torch.cuda.stream(pipe.stream):
+    pipe.dev[:pipe.in_end].copy_(pipe.host[:pipe.in_end])
+t = graph_time(lambda: pipe.launch_track(pipe.stream), reps=50)
+print(f"track real frame (cooperative): {t:.2f} us per launch (back to back in a graph)")

@@ -166,3 +166,35 @@ def run_native_split():
 
 
 print("native submit/wait host us: %.1f / %.1f" % run_native_split())
+
+
+def run_native_ranges(rng, n_slots):
+    """Per-step wall time of the native runner with n_slots pipelines and the
+    given per-step H2D ranges ([] = no upload)."""
+    ps = pipes + [FramePipeline(w.cam, n_streams=1, cap_kp=1280, cap_points=5120,
+                                pyramid_geometry=w.pyr_left, map_table=table)
+                  for _ in range(n_slots - 2)]
+    for p in ps[2:]:
+        p.load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
+        p.capture()
+    r = AsyncRunner(ps)
+    for k in range(8):
+        if k >= n_slots:
+            r.wait(k - n_slots)
+        r.submit(k, staged, rng)
+    r.synchronize()
+    t0 = time.perf_counter()
+    for k in range(N):
+        if k >= n_slots:
+            r.wait(k - n_slots)
+        r.submit(k, staged, rng)
+    r.synchronize()
+    dt = time.perf_counter() - t0
+    r.close()
+    return 1e6 * dt / N
+
+
+lo_hi = pipes[0].input_range()
+for n_slots in (2, 4):
+    print(f"slots={n_slots}: no upload {run_native_ranges([], n_slots):.1f} us/step, "
+          f"level range {run_native_ranges([lo_hi], n_slots):.1f} us/step")
