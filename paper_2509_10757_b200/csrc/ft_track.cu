@@ -147,6 +147,49 @@ FT_DEV void warp_find_rank(const int *hist, int k, int *out_digit, int *out_k) {
     }
 }
 
+// Single-pass variant for small SADs (vmax < MED_SMALL_BINS, the common case:
+// an accepted 11x11 SAD of normalised intensities is a few hundred): one
+// value histogram in shared memory, one block scan, both ranks (n-1)/2 and
+// n/2 located in the same pass.  Same result as block_median_pair.
+constexpr int MED_SMALL_BINS = 4096;
+constexpr int MED_PER_THREAD = MED_SMALL_BINS / TK_THREADS;
+
+__device__ void block_median_pair_small(const uint32_t *vals, int n, int nm, int *hist,
+                                        int *scan_tmp, int *misc, uint32_t &v_lo,
+                                        uint32_t &v_hi) {
+    const int k_lo = (nm - 1) / 2, k_hi = nm / 2;
+    for (int b = threadIdx.x; b < MED_SMALL_BINS; b += TK_THREADS) hist[b] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += TK_THREADS) {
+        const uint32_t x = vals[i];
+        if (x != 0xffffffffu) atomicAdd(&hist[x], 1);
+    }
+    __syncthreads();
+    // thread t owns bins [t * PT, (t + 1) * PT)
+    const int b0 = threadIdx.x * MED_PER_THREAD;
+    int local[MED_PER_THREAD];
+    int sum = 0;
+#pragma unroll
+    for (int j = 0; j < MED_PER_THREAD; ++j) {
+        local[j] = hist[b0 + j];
+        sum += local[j];
+    }
+    int total;
+    int before = block_exclusive_scan<TK_THREADS>(sum, scan_tmp, total);
+#pragma unroll
+    for (int j = 0; j < MED_PER_THREAD; ++j) {
+        const int c = local[j];
+        if (c > 0) {
+            if (before <= k_lo && k_lo < before + c) misc[8] = b0 + j;
+            if (before <= k_hi && k_hi < before + c) misc[10] = b0 + j;
+        }
+        before += c;
+    }
+    __syncthreads();
+    v_lo = (uint32_t)misc[8];
+    v_hi = (uint32_t)misc[10];
+}
+
 __device__ void block_median_pair(const uint32_t *vals, int n, int nm, uint32_t vmax, int *hist,
                                   int *misc, uint32_t &v_lo, uint32_t &v_hi) {
     int k_lo = (nm - 1) / 2, k_hi = nm / 2;
@@ -652,7 +695,18 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
         const int nm = sm.misc[4];
         if (nm > 0) {
             uint32_t v_lo, v_hi;
-            block_median_pair(vals, n_left, nm, (uint32_t)sm.misc[5], hist, sm.misc, v_lo, v_hi);
+            // histogram after the values in the (no longer needed) table area
+            const size_t vbytes = ((size_t)4 * a.L.cap + 15) & ~(size_t)15;
+            if ((uint32_t)sm.misc[5] < (uint32_t)MED_SMALL_BINS &&
+                stereo_table_bytes(a) >= vbytes + 4 * (size_t)MED_SMALL_BINS)
+                block_median_pair_small(vals, n_left, nm,
+                                        reinterpret_cast<int *>(
+                                            reinterpret_cast<unsigned char *>(sm.rtab_s) + vbytes),
+                                        sm.scan_tmp,
+                                        sm.misc, v_lo, v_hi);
+            else
+                block_median_pair(vals, n_left, nm, (uint32_t)sm.misc[5], hist, sm.misc, v_lo,
+                                  v_hi);
             const double med = (nm & 1) ? (double)v_lo : ((double)v_lo + (double)v_hi) / 2.0;
             const double thr = a.sp.outlier_multiplier * med;
             TL_MARK(a, 14);
