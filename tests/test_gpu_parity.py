@@ -533,3 +533,23 @@ def test_projection_config_sweep_vs_oracle(oracle, kw, scale, levels):
     n = ft.search_local_points(w.local, f2, w.cam, pcfg, scale, levels)
     assert n == n_ref
     np.testing.assert_array_equal(f2.slots, slots)
+
+
+def test_rejection_median_large_sads(oracle):
+    """Median rejection when accepted SADs exceed the single-pass histogram
+    range (>= 4096): a right pyramid of uncorrelated noise makes every SAD
+    large, so the radix-select path runs; bit-exact with the oracle."""
+    from copy import deepcopy
+    from paper_2509_10757_b200.synthetic import make_workload
+    w = make_workload(seed=51, n_landmarks=12000, map_points=1000, images=True)
+    pr = deepcopy(w.pyr_right)
+    rng = np.random.default_rng(3)
+    pr.data = rng.integers(0, 256, size=pr.data.shape, dtype=np.uint8)
+    cfg = StereoMatchConfig()
+    ref = oracle.stereo_pinhole(w.left, w.right, w.pyr_left, pr, w.cam, cfg, w.scale_pow)
+    idx, dist = oracle.match_pinhole_phase1(w.left, w.right, 480, w.scale_pow, cfg)
+    pre = oracle.refine_match_phase2(w.pyr_left, pr, w.left, w.right, idx, dist, w.cam, cfg)
+    assert pre.sad[pre.right_idx >= 0].max() >= 4096
+    got = ft.compute_stereo_matches(w.left, w.right, w.cam, cfg, w.scale_pow, w.pyr_left, pr)
+    for f in FIELDS:
+        np.testing.assert_array_equal(getattr(got, f), getattr(ref, f), err_msg=f)
