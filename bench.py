@@ -294,13 +294,20 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n_dev = torch.cuda.device_count()
+    if local_rank >= n_dev and os.environ.get("FT_BENCH_DIST_BACKEND", "nccl") != "nccl":
+        local_rank = local_rank % n_dev  # rehearsal: several ranks share the visible GPUs
     torch.cuda.set_device(local_rank)
     from paper_2509_10757_b200.runtime import bind_host_to_gpu_numa
     numa_cpus = bind_host_to_gpu_numa(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("FT_BENCH_DIST_BACKEND", "nccl")  # gloo: 1-GPU rehearsal
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     from paper_2509_10757_b200 import _lib
     from paper_2509_10757_b200.pipeline import FramePipeline
 

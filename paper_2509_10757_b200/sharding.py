@@ -29,6 +29,8 @@ def max_over_ranks(values, dist=None, device=None):
     vals = [float(v) for v in values]
     if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
         return vals
+    if dist.get_backend() == "gloo":
+        device = None  # gloo reduces host tensors
     t = torch.tensor(vals, dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(x) for x in t.tolist()]
