@@ -278,7 +278,9 @@ def config_dict(args) -> dict:
     return {"workload": "cfg2: EuRoC-shaped stereo frame 752x480 (~1270 kps/image, 8 levels, "
                         "scale 1.2" + img + ") + " + mp + "; stereo + SearchLocalPoints per frame",
             "streams_per_gpu": args.streams, "frames_cycled": args.frames,
-            "l2": "flushed before every timed step (256 MiB write, then read back)",
+            "l2": "value: inputs > L2 (resident ring of pipelines, >= 256 MiB of step "
+                  "inputs cycled); latency / kernel timings: flushed before every step "
+                  "(256 MiB write, then read back)",
             "parallelism": f"independent frame streams x {args.gpus} GPU (no collective)"}
 
 
@@ -339,6 +341,26 @@ def main() -> None:
             flush.fill_(1)
             flush_sink.copy_(flush.view(torch.int64).sum())
 
+    # resident ring for the throughput value: R pipelines, each holding one
+    # frame's inputs in HBM, together > 2x L2, so back-to-back steps read
+    # their inputs cold without a flush between them
+    n_res = max(2, min(160, -(-(256 << 20) // pipe.in_end)))
+    res_pipes = []
+    for i in range(n_res):
+        rp = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
+                           pyramid_geometry=w0.pyr_left if images else None, raw_images=raw,
+                           map_table=table, build_levels=build_levels)
+        for s_ in range(S):
+            f = frames[(i + s_) % len(frames)]
+            rp.load_frame(s_, f.left, f.right, f.local, f.pose, f.pyr_left, f.pyr_right)
+        rp.capture()  # runs the step once with copies: inputs now resident
+        res_pipes.append(rp)
+    torch.cuda.synchronize()
+    res_stream = pipe.stream
+
+    def resident_step(k: int) -> None:
+        res_pipes[k % n_res].graph_compute.replay()
+
     load(0)
     pipe.capture()
     # correctness spot check of the resident pipeline against the oracle (rank 0, stream 0)
@@ -354,9 +376,25 @@ def main() -> None:
     pipe.synchronize()
     comp_ms = []
     with ClockSampler(local_rank) as clk:
+        # ---- value: back-to-back steps over the resident ring, one stream
+        with torch.cuda.stream(res_stream):
+            for k in range(max(args.warmup, n_res)):
+                resident_step(k)
+        torch.cuda.synchronize()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
+        ra, rb = ev(), ev()
+        with torch.cuda.stream(res_stream):
+            ra.record(res_stream)
+            for k in range(args.steps):
+                resident_step(k)
+            rb.record(res_stream)
+        torch.cuda.synchronize()
+        stream_ms = ra.elapsed_time(rb)
+        if dist:
+            dist.barrier()
+        # ---- latency: one isolated step at a time, L2 flushed before each
         for k in range(args.steps):
             load(k)
             with torch.cuda.stream(pipe.stream):
@@ -396,20 +434,26 @@ def main() -> None:
     shipped = float(np.mean([hi - lo for lo, hi in ranges]))
     if dist:
         dist.barrier()
-    # warm-up: every staged pinned buffer's first DMA is slow (one cycle)
-    for k in range(max(args.warmup, 4 * len(staged) + 2)):
+    # warm-up: every staged pinned buffer's first DMA is slow (one cycle), and
+    # the GPU / host clocks ramp back up after the staging pause (>= 0.3 s of
+    # steps)
+    k, tw = 0, time.perf_counter()
+    while k < max(args.warmup, 4 * len(staged) + 2) or time.perf_counter() - tw < 0.3:
         if k >= runner.n:
             runner.wait(k - runner.n)
         runner.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
-    runner.synchronize()
+        k += 1
+    for j in range(max(0, k - runner.n), k):
+        runner.wait(j)
+    k0 = k
     t0 = time.perf_counter()
     marks = []
-    for k in range(args.steps):
-        if k >= runner.n:
+    for k in range(k0, k0 + args.steps):
+        if k - k0 >= runner.n:
             runner.wait(k - runner.n)
         runner.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
         marks.append(time.perf_counter())
-    for k in range(max(0, args.steps - runner.n), args.steps):
+    for k in range(max(k0, k0 + args.steps - runner.n), k0 + args.steps):
         runner.wait(k)
     async_ms = 1e3 * (time.perf_counter() - t0)
     if os.environ.get("FT_BENCH_DIAG"):
@@ -438,9 +482,10 @@ def main() -> None:
     tot_comp = sum(comp_ms)
     tot_e2e = sum(e2e_ms)
     from paper_2509_10757_b200.sharding import job_frames_per_s, max_over_ranks
-    tot_comp, tot_e2e, async_ms = max_over_ranks([tot_comp, tot_e2e, async_ms], dist,
-                                                 device="cuda")
-    value = job_frames_per_s(S * args.steps, world, tot_comp)
+    tot_comp, tot_e2e, async_ms, stream_ms = max_over_ranks(
+        [tot_comp, tot_e2e, async_ms, stream_ms], dist, device="cuda")
+    value = job_frames_per_s(S * args.steps, world, stream_ms)
+    isolated_value = job_frames_per_s(S * args.steps, world, tot_comp)
     e2e_serial = job_frames_per_s(S * args.steps, world, tot_e2e)
     e2e_async = job_frames_per_s(S * args.steps, world, async_ms)
     # both are the public API end to end (every step's inputs H2D, results
@@ -487,7 +532,14 @@ def main() -> None:
     h2d_ms = float(np.median(h2d_times))
     line = {"metric": "stereo+local-map tracking frames/s at EuRoC shape", "value": value,
             "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot_comp / args.steps, "latency_ms_per_frame": tot_comp / args.steps,
+            "ms_per_step": stream_ms / args.steps,
+            "value_method": f"compute graphs replayed back to back on one stream over {n_res} "
+                            "resident pipelines (each one frame's inputs in HBM; "
+                            f"{n_res * pipe.in_end / 2**20:.0f} MiB of inputs > 2x L2), "
+                            "CUDA events around all K steps",
+            "latency_ms_per_frame": tot_comp / args.steps,
+            "isolated_step": {"value": isolated_value, "unit": "frames/s",
+                              "method": "one step at a time: L2 flushed, events, synchronise"},
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64+u32", "data": "synthetic", "config": config_dict(args),
             "e2e": {"value": e2e_value, "unit": "frames/s",
@@ -527,7 +579,10 @@ def main() -> None:
                            "stereo_only": float(np.median(kern["stereo_only"])),
                            "map_only": float(np.median(kern["map_only"]))},
             "work_per_frame": units, "clocks": clocks,
-            "gpu_launches": 2 * (1 + int(raw)) * args.steps,
+            "gpu_launches": (1 + int(raw)) * args.steps,
+            "gpu_launches_note": "our kernels per step: ft_track_frames (+ ft_build_pyramids "
+                                 "in raw / hybrid mode); counted over the value region's K "
+                                 "steps (each other timed region launches the same per step)",
             "parity_spot_check": check}
     if not args.quick:
         # extra measurements: a failure in one is recorded, never loses the line
@@ -822,9 +877,11 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
     elif not mode_raw:  # explicit raw from a ship-mode run: hybrid at --build-levels
         b = max(1, args.build_levels)
     table, _ = make_table(args, frames, cap_pts, S)
+    packed = os.environ.get("FT_BENCH_PACKED", "1") != "0"
     pipes = [FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
                            pyramid_geometry=w0.pyr_left if images else None, raw_images=raw,
-                           map_table=table, build_levels=b if raw else None)
+                           map_table=table, build_levels=b if raw else None,
+                           packed_upload=packed)
              for _ in range(4)]
     pipe = pipes[0]
     for s in range(S):
@@ -871,6 +928,7 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
             "frames_per_s": S * steps / (sum(comp) / 1e3),
             "e2e_frames_per_s": S * steps / (e2e_ms / 1e3),
             "h2d_bytes_per_step": shipped, "h2d_ranges_per_step": len(rngs),
+            "packed_upload": bool(pipe.packed),
             "d2h_bytes_per_step": pipe.d2h_bytes()}
 
 if __name__ == "__main__":

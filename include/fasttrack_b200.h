@@ -294,6 +294,13 @@ int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host_in,
 int ft_runner_wait(ft_runner *r, int64_t k);
 int ft_runner_destroy(ft_runner *r);
 
+/* Packed upload: after one contiguous H2D of a step's needed bytes, place
+ * segment i (desc[3i] = source offset, desc[3i+1] = destination offset,
+ * desc[3i+2] = length, bytes relative to `base`; desc in DEVICE memory, e.g.
+ * uploaded with the segments) at its destination.  Segments must not overlap
+ * each other's destinations. */
+int ft_copy_ranges(void *base, const int64_t *desc, int32_t n, ft_stream_t stream);
+
 /* kernels.py:48-51: out[i] = popcount(a[i] ^ b[i]) over 256 bits. */
 int ft_hamming_pairs(const uint64_t *a, const uint64_t *b, int64_t n, int64_t *out,
                      ft_stream_t stream);

@@ -110,7 +110,7 @@ EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_works
            "ft_hamming_pairs", "ft_stereo_pinhole", "ft_stereo_fisheye_bf", "ft_project_search",
            "ft_track_frames", "ft_resolve_conflicts", "ft_rotation_filter", "ft_bench_popc",
            "ft_pack_keypoints", "ft_pack_points", "ft_build_pyramids", "ft_stereo_fisheye",
-           "ft_gather_points", "ft_scatter_points", "ft_runner_create", "ft_runner_create_n", "ft_runner_submit", "ft_runner_submit_range", "ft_runner_submit_ranges",
+           "ft_gather_points", "ft_scatter_points", "ft_copy_ranges", "ft_runner_create", "ft_runner_create_n", "ft_runner_submit", "ft_runner_submit_range", "ft_runner_submit_ranges",
            "ft_runner_wait", "ft_runner_destroy")
 
 
@@ -147,6 +147,7 @@ def load() -> ctypes.CDLL:
                                     P(FtFisheyeTri), vp, vp, vp, vp, W, vp]
     L.ft_gather_points.argtypes = [i32, vp, i64, vp, vp, i32, vp, vp, vp]
     L.ft_scatter_points.argtypes = [i32, vp, vp, vp, i64, vp]
+    L.ft_copy_ranges.argtypes = [vp, vp, i32, vp]
     L.ft_runner_create.argtypes = [vp * 2, vp * 2, ctypes.c_size_t, vp * 2, vp * 2,
                                    ctypes.c_size_t, P(vp)]
     L.ft_runner_create_n.argtypes = [i32, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_size_t,

@@ -342,3 +342,46 @@ extern "C" int ft_scatter_points(int32_t n, const ft_point_record *recs, const i
         table_size);
     return (int)cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// Packed-upload scatter: one contiguous H2D of a step's needed bytes (the
+// small inputs plus every stream's needed pyramid levels, packed by the host
+// at staging time), then this kernel places each segment at its arena offset.
+// desc[3i..3i+2] = (src offset, dst offset, length) relative to `base`; the
+// host packs segments with src = dst (mod 16), so the body moves as uint4.
+namespace {
+__global__ void copy_ranges_kernel(unsigned char *base, const int64_t *desc, int32_t n,
+                                   int32_t blocks_per) {
+    const int seg = blockIdx.x / blocks_per, part = blockIdx.x - seg * blocks_per;
+    if (seg >= n) return;
+    const int64_t so = desc[3 * seg], dof = desc[3 * seg + 1], len = desc[3 * seg + 2];
+    if (len <= 0) return;
+    const unsigned char *src = base + so;
+    unsigned char *dst = base + dof;
+    const int64_t head = min(len, (int64_t)((16 - ((uintptr_t)dst & 15)) & 15));
+    const bool vec = (((uintptr_t)src ^ (uintptr_t)dst) & 15) == 0;
+    const int64_t nv = vec ? (len - head) >> 4 : 0;
+    const int64_t tail0 = vec ? head + (nv << 4) : 0;
+    const int64_t stride = (int64_t)blocks_per * blockDim.x;
+    const int64_t t0 = (int64_t)part * blockDim.x + threadIdx.x;
+    if (vec) {
+        for (int64_t t = t0; t < head; t += stride) dst[t] = src[t];
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src + head);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst + head);
+        for (int64_t q = t0; q < nv; q += stride) d4[q] = __ldcs(s4 + q);
+        for (int64_t t = tail0 + t0; t < len; t += stride) dst[t] = src[t];
+    } else {
+        for (int64_t t = t0; t < len; t += stride) dst[t] = src[t];
+    }
+}
+}  // namespace
+
+extern "C" int ft_copy_ranges(void *base, const int64_t *desc, int32_t n, ft_stream_t stream) {
+    if (!base || (!desc && n > 0)) return FT_E_NULL;
+    if (n < 0) return FT_E_RANGE;
+    if (n == 0) return FT_OK;
+    const int blocks_per = 4;
+    copy_ranges_kernel<<<n * blocks_per, 512, 0, (cudaStream_t)stream>>>(
+        static_cast<unsigned char *>(base), desc, n, blocks_per);
+    return (int)cudaGetLastError();
+}

@@ -44,7 +44,8 @@ class FramePipeline:
                  pyramid_geometry=None, stereo_cfg: StereoMatchConfig | None = None,
                  proj_cfg: ProjectionSearchConfig | None = None, scale: float = 1.2,
                  levels: int = 8, grid_cell_px: int = 48, device: int | None = None,
-                 raw_images: bool = False, map_table=None, build_levels: int | None = None):
+                 raw_images: bool = False, map_table=None, build_levels: int | None = None,
+                 packed_upload: bool | None = None):
         if not torch.cuda.is_available():
             raise _lib.FtError("FramePipeline needs a CUDA device (no CPU fallback)")
         self.lib = _lib.load()
@@ -126,6 +127,19 @@ class FramePipeline:
                                     dtype=np.int64)
         elif self.pyr is not None:
             lay.add("pyrs", 2 * S * self.pyr_bytes)
+        # packed upload (S > 1, level ranges): the step's S + 1 needed ranges
+        # are packed on the host into ONE contiguous region -- a descriptor
+        # header (src, dst, len per segment) then the segments, each placed so
+        # src = dst (mod 16) -- shipped as one H2D and placed by ft_copy_ranges
+        # ahead of the track kernel (one large DMA instead of S + 1 small ones)
+        self.packed = bool(self.level_ranges and S > 1 and
+                           (packed_upload is None or packed_upload))
+        if self.packed:
+            self.pack_hdr = (24 * (S + 1) + 255) // 256 * 256
+            lay.add("pack", self.pack_hdr + self.small_end + 16 +
+                    S * (2 * self.pyr_bytes + 16))
+            self.pack_used = self.pack_hdr
+            self._pack_dirty = True
         self.in_end = lay.total
         self.cur_range = (0, self.in_end)
         self.stream_m = np.zeros(S, dtype=np.int64)  # lowest left octave per stream
@@ -157,6 +171,7 @@ class FramePipeline:
         self._build_structs()
         self.graph = None
         self.graph_compute = None
+        self.graph_runner = None
 
     # -- host views ------------------------------------------------------------
 
@@ -235,14 +250,52 @@ class FramePipeline:
         sl[s] = -1
         if slots is not None:
             sl[s, :len(left.u)] = slots
+        if self.packed:
+            self._pack_dirty = True
+
+    def _segments(self) -> list[tuple[int, int]]:
+        """The [lo, hi) ranges of the regular input layout the current step
+        needs (level ranges, S > 1)."""
+        pb, base = self.pyr_bytes, self.lay.offsets["pairs"]
+        offs = np.asarray(self.pyr.offsets, dtype=np.int64)
+        out = [(0, self.small_end)]
+        for st in range(self.S):
+            m = int(self.stream_m[st])
+            lo = base + 2 * st * pb + int(offs[m])
+            hi = base + (2 * st + 1) * pb + int(self.rev_off[m] + self.lvl_size[m])
+            out.append((lo, hi))
+        return out
+
+    def pack(self) -> tuple[int, int]:
+        """Pack the current step's needed ranges into the pack region of the
+        staging (no-op when unchanged); returns the [lo, hi) to ship."""
+        base = self.lay.offsets["pack"]
+        if self._pack_dirty:
+            segs = self._segments()
+            desc = self.hnp[base:base + 24 * len(segs)].view(np.int64).reshape(-1, 3)
+            cur = base + self.pack_hdr
+            for q, (lo, hi) in enumerate(segs):
+                cur += (lo - cur) % 16
+                n = hi - lo
+                self.hnp[cur:cur + n] = self.hnp[lo:hi]
+                desc[q] = (cur, lo, n)
+                cur += n
+            self.pack_used = cur - base
+            self._pack_dirty = False
+        return (base, base + self.pack_used)
 
     def h2d_bytes(self) -> int:
+        if self.packed:
+            return self.in_end - self.lay.offsets["pack"]
         return self.in_end
 
     def input_range(self) -> tuple[int, int]:
         """[lo, hi) of the input staging the current frame needs on the device:
         the whole input area, or with level ranges the pyramid levels at or
-        above the frame's lowest left-keypoint octave plus the small inputs."""
+        above the frame's lowest left-keypoint octave plus the small inputs
+        (S > 1: the packed region)."""
+        if self.packed:
+            return self.pack()
         return self.cur_range
 
     def input_ranges(self) -> list[tuple[int, int]]:
@@ -254,15 +307,9 @@ class FramePipeline:
             return [(0, self.in_end)]
         if self.S == 1:
             return [self.cur_range]
-        pb, base = self.pyr_bytes, self.lay.offsets["pairs"]
-        offs = np.asarray(self.pyr.offsets, dtype=np.int64)
-        out = [(0, self.small_end)]
-        for st in range(self.S):
-            m = int(self.stream_m[st])
-            lo = base + 2 * st * pb + int(offs[m])
-            hi = base + (2 * st + 1) * pb + int(self.rev_off[m] + self.lvl_size[m])
-            out.append((lo, hi))
-        return out
+        if self.packed:
+            return [self.pack()]
+        return self._segments()
 
     def d2h_bytes(self) -> int:
         return self.out_end - self.out_begin
@@ -355,11 +402,20 @@ class FramePipeline:
                                                   self.img_bytes, self.ws, stream.cuda_stream),
                        "ft_build_pyramids")
 
-    def _step(self, copies: bool) -> None:
+    def launch_unpack(self, stream) -> None:
+        """Place the packed upload's segments (packed pipelines only)."""
+        if self.packed:
+            _lib.check(self.lib.ft_copy_ranges(self.dev.data_ptr(), self._d("pack"), self.S + 1,
+                                               stream.cuda_stream), "ft_copy_ranges")
+
+    def _step(self, copies: bool, unpack: bool | None = None) -> None:
         a = self.stream
         if copies:
+            lo = self.lay.offsets["pack"] if self.packed else 0
             with torch.cuda.stream(a):
-                self.dev[:self.in_end].copy_(self.host[:self.in_end], non_blocking=True)
+                self.dev[lo:self.in_end].copy_(self.host[lo:self.in_end], non_blocking=True)
+        if copies if unpack is None else unpack:
+            self.launch_unpack(a)
         self.launch_pyramids(a)
         self.launch_track(a)
         if copies:
@@ -368,10 +424,14 @@ class FramePipeline:
                     self.dev[self.out_begin:self.out_end], non_blocking=True)
 
     def run_eager(self, copies: bool = True) -> None:
+        if copies and self.packed:
+            self.pack()
         self._step(copies)
 
     def capture(self) -> None:
-        """Capture the full step (with copies) and the compute-only step."""
+        """Capture the full step (with copies), the compute-only step (inputs
+        resident in place) and, for packed pipelines, the step AsyncRunner
+        launches after its H2D (unpack + compute)."""
         self.run_eager(True)  # warm: sets kernel attributes, loads modules
         self.stream.synchronize()
         self.graph = torch.cuda.CUDAGraph()
@@ -380,11 +440,18 @@ class FramePipeline:
         self.graph_compute = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph_compute, stream=self.stream):
             self._step(False)
+        self.graph_runner = self.graph_compute
+        if self.packed:
+            self.graph_runner = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph_runner, stream=self.stream):
+                self._step(False, unpack=True)
         self.stream.synchronize()
 
     def replay(self, copies: bool = True) -> None:
         if self.graph is None:
             self.capture()
+        if copies and self.packed:
+            self.pack()
         # CUDAGraph.replay() launches on torch's current stream
         with torch.cuda.stream(self.stream):
             (self.graph if copies else self.graph_compute).replay()
@@ -408,6 +475,8 @@ class FramePipeline:
     def staged_inputs(self) -> torch.Tensor:
         """A pinned copy of the current input staging (what load_frame wrote):
         one step's inputs, ready for AsyncRunner.submit."""
+        if self.packed:
+            self.pack()
         return self.host[:self.in_end].clone().pin_memory()
 
     def staging_ring(self, n: int) -> torch.Tensor:
@@ -420,6 +489,8 @@ class FramePipeline:
 
     def stage_into(self, dst: torch.Tensor) -> None:
         """Copy the current input staging into a ring slot."""
+        if self.packed:
+            self.pack()
         dst.copy_(self.host[:self.in_end])
 
 
@@ -463,10 +534,10 @@ class AsyncRunner:
         self.n = len(pipes)
         self.lib = a.lib
         for p in pipes:
-            if p.graph_compute is None:
+            if p.graph_runner is None:
                 p.capture()
         vpn = ctypes.c_void_p * self.n
-        execs = vpn(*[_graph_exec_ptr(p.graph_compute) for p in pipes])
+        execs = vpn(*[_graph_exec_ptr(p.graph_runner) for p in pipes])
         dev_in = vpn(*[p.dev.data_ptr() for p in pipes])
         dev_out = vpn(*[p.dev.data_ptr() + p.out_begin for p in pipes])
         host_out = vpn(*[p.host.data_ptr() + p.out_begin for p in pipes])
@@ -606,8 +677,10 @@ class FisheyePipeline:
         po.corr_count, po.slot_count = self._d("c_n"), self._d("slot_n")
         self.pout = po
         self.pmode = (_lib.FT_PROJ_RESOLVE | _lib.FT_PROJ_SKIP_SLOTS | _lib.FT_PROJ_WRITE_SLOTS)
+        self.packed = False
         self.graph = None
         self.graph_compute = None
+        self.graph_runner = None
 
     _h = FramePipeline._h
     _d = FramePipeline._d

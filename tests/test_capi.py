@@ -81,6 +81,10 @@ def test_new_entries_validate_without_gpu():
     assert L.ft_gather_points(1, None, 10, None, None, 4, None, None, None) == -1
     assert L.ft_scatter_points(0, None, None, None, 10, None) == 0  # empty delta: no-op
     assert L.ft_scatter_points(3, None, None, None, 10, None) == -1
+    # packed-upload scatter
+    assert L.ft_copy_ranges(None, None, 1, None) == -1
+    assert L.ft_copy_ranges(ctypes.c_void_p(16), None, 0, None) == 0  # nothing to place
+    assert L.ft_copy_ranges(ctypes.c_void_p(16), ctypes.c_void_p(16), -1, None) == -2
     # pyramid build
     assert L.ft_build_pyramids(1, None, None, 0, ws, None) == -1
     # native runner

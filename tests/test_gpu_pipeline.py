@@ -322,3 +322,81 @@ def _check_one(pipe, workloads, expected, i):
         np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f), err_msg=f)
     np.testing.assert_array_equal(res.slots, slots)
     assert res.n_slots == n
+
+
+@pytest.mark.parametrize("packed", [True, False])
+def test_multi_stream_level_ranges(workloads, expected, packed):
+    """S > 1 ship mode: per step only the small inputs and each stream's
+    needed pyramid levels cross PCIe -- packed into one region and placed by
+    ft_copy_ranges (packed) or as S + 1 separate ranges -- with every other
+    byte of the device inputs holding garbage; results equal the oracle's."""
+    from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
+    w0 = workloads[0]
+    S = 5
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    pipes = [FramePipeline(w0.cam, n_streams=S, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left,
+                           packed_upload=packed) for _ in range(3)]
+    assert pipes[0].packed == packed
+    ring = pipes[0].staging_ring(4)
+    ranges = []
+    for k in range(4):
+        for s in range(S):
+            w = workloads[(k + s) % 4]
+            pipes[0].load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                                slots=expected[(k + s) % 4][1])
+        pipes[0].stage_into(ring[k])
+        ranges.append(pipes[0].input_ranges())
+        assert len(ranges[-1]) == (1 if packed else S + 1)
+        assert sum(hi - lo for lo, hi in ranges[-1]) < pipes[0].h2d_bytes()
+    for p in pipes:
+        p.dev.fill_(0xAB)
+        p.capture()
+    runner = AsyncRunner(pipes)
+
+    def check(pipe, k):
+        for s in range(S):
+            i = (k % 4 + s) % 4
+            w = workloads[i]
+            m, _, slots, n = expected[i]
+            res = pipe.result(s, len(w.left.u))
+            for f in FIELDS:
+                np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f),
+                                              err_msg=f"step {k} stream {s} {f}")
+            np.testing.assert_array_equal(res.slots, slots, err_msg=f"step {k} stream {s}")
+            assert res.n_slots == n
+
+    for k in range(9):
+        if k >= 3:
+            check(runner.wait(k - 3), k - 3)
+        runner.submit(k, ring[k % 4], ranges[k % 4])
+    for k in (6, 7, 8):
+        check(runner.wait(k), k)
+    runner.close()
+
+
+def test_copy_ranges_alignments():
+    """ft_copy_ranges at every source/destination alignment and odd length
+    (vector body + byte head/tail, and the byte path for mismatched
+    residues); zero-length segments are no-ops."""
+    import ctypes
+    import torch
+    from paper_2509_10757_b200 import _lib
+    lib = _lib.load()
+    base = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    src = torch.randint(0, 256, (200_000,), dtype=torch.uint8, device="cuda")
+    base[:200_000] = src
+    desc, want, dst = [], [], 300_000
+    for so, n in ((0, 1), (3, 17), (16, 4096), (5, 12345), (7, 0), (1, 70_001)):
+        d = dst + (so % 16 if n % 2 else (so + 3) % 16)
+        desc.append((so, d, n))
+        want.append((d, src[so:so + n].clone()))
+        dst = d + n + 64
+    dd = torch.tensor(desc, dtype=torch.int64, device="cuda").reshape(-1)
+    _lib.check(lib.ft_copy_ranges(base.data_ptr(), dd.data_ptr(), len(desc),
+                                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "ft_copy_ranges")
+    torch.cuda.synchronize()
+    for d, v in want:
+        assert torch.equal(base[d:d + len(v)], v)
+    assert lib.ft_copy_ranges(None, dd.data_ptr(), 1, None) == -1
