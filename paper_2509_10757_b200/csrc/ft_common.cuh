@@ -43,13 +43,23 @@ FT_DEV unsigned long long ld_acquire_u64(const unsigned long long *p) {
     return v;
 }
 
-// Barrier among the G co-resident blocks sharing `ctr` (cooperative
-// launches only).  ctr = (generation << 32) | arrivals; the G-th arrival
-// resets the arrivals and bumps the generation in ONE atomic, so the counter
-// returns to (gen, 0) after every barrier: launches of any G may reuse it and
-// nothing has to be reset between launches or graph replays.  Writes before
-// the barrier are visible after it (fence + release sequence on ctr).
-__device__ inline void group_barrier(unsigned long long *ctr, int G) {
+// Barrier among the G co-resident blocks sharing `ctr2` (cooperative
+// launches only).  Two counter words used alternately (`parity`, a per-block
+// count of barriers passed, identical in every block of the group); each is
+// (generation << 32) | arrivals.  A block arrives with one atomic add and
+// leaves as soon as it reads arrivals == G -- one L2 round trip after the
+// last arrival, with no release write on the critical path.  The last
+// arrival then resets its word (arrivals 0, generation + 1; a late poller
+// accepts the new generation too).  The word is reused two barriers later,
+// which no block reaches before the last arrival of the barrier in between --
+// ordered after this reset by its release fence -- so arrivals never see a
+// stale count.  Every word returns to arrivals == 0 after each barrier:
+// launches of any G may reuse the pair, starting at parity 0, and nothing
+// has to be reset between launches or graph replays.  Writes before the
+// barrier are visible after it (release fence + acquire polls).
+__device__ inline void group_barrier(unsigned long long *ctr2, int G, unsigned &parity) {
+    unsigned long long *ctr = ctr2 + (parity & 1u);
+    ++parity;
     __syncthreads();
     if (threadIdx.x == 0) {
         // acq_rel fences (not the sequentially consistent __threadfence): the
@@ -62,7 +72,11 @@ __device__ inline void group_barrier(unsigned long long *ctr, int G) {
             atomicAdd(ctr, (1ull << 32) - (unsigned long long)G);
         } else {
             const uint32_t gen = (uint32_t)(old >> 32);
-            while ((uint32_t)(ld_acquire_u64(ctr) >> 32) == gen) __nanosleep(32);
+            for (;;) {
+                const unsigned long long cur = ld_acquire_u64(ctr);
+                if ((uint32_t)cur == (uint32_t)G || (uint32_t)(cur >> 32) != gen) break;
+                __nanosleep(20);
+            }
         }
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }

@@ -517,13 +517,14 @@ FT_DEV void pyr_store_own(const uint8_t *src, const PyrRect &c, const PyrRect &o
 
 // Build levels 1..L-1 of one image (this block = `rank` of G).  `base` is the
 // image's flat pyramid; `lvl0` the level-0 pixels (== base + offsets[0] or a
-// separate raw image).  `bar` is the image's group-barrier counter.  Every
+// separate raw image).  `bar` is the image's group-barrier word pair.  Every
 // thread of the block calls this; on return this block's tiles are written
 // (other blocks' may not be).
 FT_DEV void pyr_build_image(const PyrGeom &g, const PyrPlan &p, uint8_t *base,
                             const uint8_t *lvl0, int rank, int G, unsigned long long *bar,
                             unsigned char *smem, unsigned long long *tl = nullptr) {
     int tk_ = 0, *tk = &tk_;
+    unsigned bpar = 0;
     PYR_MARK();
     PyrSmem S;
     pyr_layout(p, smem, &S);
@@ -568,7 +569,7 @@ FT_DEV void pyr_build_image(const PyrGeom &g, const PyrPlan &p, uint8_t *base,
                 PYR_MARK();
             }
         }
-        if (s + 1 < p.n_stages) group_barrier(bar, G);
+        if (s + 1 < p.n_stages) group_barrier(bar, G, bpar);
         PYR_MARK();
     }
 }

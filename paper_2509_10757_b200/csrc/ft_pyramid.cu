@@ -20,7 +20,7 @@ struct PyrArgs {
     uint8_t *data;
     int64_t frame_bytes;
     int32_t n_images, G;      // G blocks per image
-    unsigned long long *bar;  // [n_images]
+    unsigned long long *bar;  // [n_images][2]
     const uint8_t *src0;      // optional separate level-0 images (else in place)
     int64_t src0_stride;
     unsigned long long *tl;  // debug timeline [grid][16] (FT_DEBUG_PYR_TIMELINE)
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(PY_THREADS, 2) pyramid_kernel(const PyrArgs a)
                 __ldg(reinterpret_cast<const uint4 *>(img0 + b0 + 16 * q));
         for (int64_t t = b0 + 16 * nvec + threadIdx.x; t < b1; t += PY_THREADS) l0[t] = img0[t];
     }
-    pyr_build_image(a.g, a.p, base, img0 ? img0 : base + a.g.offsets[0], rank, a.G, a.bar + img,
+    pyr_build_image(a.g, a.p, base, img0 ? img0 : base + a.g.offsets[0], rank, a.G, a.bar + 2 * img,
                     smem, a.tl ? a.tl + 64 * blockIdx.x : nullptr);
 }
 

@@ -75,9 +75,11 @@ struct TrackArgs {
     int32_t stage_rdesc;    // stereo: right descriptors staged in smem (else read from L2)
     int32_t stage_kdesc;    // map: keypoint descriptors staged in smem
     // workspace
-    unsigned long long *bar_s;   // [W]
-    unsigned long long *bar_m;   // [W]
-    unsigned long long *ep_m;    // [W]
+    unsigned long long *bar_s;   // [W][2]
+    unsigned long long *bar_m;   // [W][2]
+    unsigned long long *ep_m;    // [W] map-group instance tickets (group_ticket)
+    unsigned long long *ep_s;    // [W] stereo-group instance tickets
+    unsigned *med;               // [W][3][MED_WS] SAD-median histograms
     unsigned long long *claims;  // [F][cap_kp]
     int *blk_counts;             // [F][Gm]
     int *hist;                   // [F][TK_MAX_BINS]
@@ -108,6 +110,18 @@ FT_DEV unsigned long long global_ns() {
 // Warm the TLB / L2 for a page the block will touch later (no data use).
 FT_DEV void prefetch_l2(const void *p) {
     if (p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Instance number of a group's current frame: each of the G blocks takes
+// one ticket ((instance << 32) | tickets); the G-th resets the tickets and
+// bumps the instance in one atomic.  Every block of an instance reads the
+// same instance number, for any G -- the next instance's tickets are taken
+// after a group barrier that orders them behind this reset.  Monotonic
+// across launches sharing the workspace.
+FT_DEV unsigned group_ticket(unsigned long long *ctr, int G) {
+    const unsigned long long old = atomicAdd(ctr, 1ull);
+    if ((uint32_t)old == (uint32_t)(G - 1)) atomicAdd(ctr, (1ull << 32) - (unsigned long long)G);
+    return (unsigned)(old >> 32);
 }
 
 
@@ -456,7 +470,7 @@ FT_DEV bool p2_sweep_fixed(const TrackArgs &a, int *patch, const LeftKp &kp, con
 // hides behind the candidate search; the right strip follows phase 1.
 template <int HW, int HS>
 FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int f, int64_t lk,
-                      int64_t rbase, int n_right, const LeftKp &kp, int lane) {
+                      int64_t rbase, int n_right, const LeftKp &kp, int lane, unsigned *medh) {
     constexpr bool FIXED = HW > 0;
     const int hw = FIXED ? HW : a.sp.half_window;
     const int hs = FIXED ? HS : a.sp.half_slide;
@@ -555,6 +569,11 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
         }
     }
     if (lane == 0) {
+        if (ok && medh) {  // SAD-median histogram of the frame (fire-and-forget reds)
+            const uint32_t x = (uint32_t)sad;
+            atomicAdd(medh + (x < MED_FINE ? x / MED_CW : MED_NC), 1u);
+            if (x < MED_FINE) atomicAdd(medh + 128 + x, 1u);
+        }
         a.so.right_idx[lk] = ok ? cand : -1;
         a.so.distance[lk] = ok ? cdist : 10000;
         a.so.disparity[lk] = ok ? disp : 0.0;
@@ -573,8 +592,10 @@ __host__ __device__ inline size_t stereo_table_bytes(const TrackArgs &a) {
     return ((t > m ? t : m) + 15) & ~(size_t)15;
 }
 
-__device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long long *bar,
-                             unsigned char *smem, unsigned long long *mbar, unsigned &mphase) {
+__device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
+                             unsigned char *smem, unsigned long long *mbar, unsigned &mphase,
+                             unsigned &bpar) {
+    unsigned long long *bar = a.bar_s + 2 * slot;
     const int G = a.Gs;
     const int n_left = min(a.L.count[f], a.L.cap);
     const int n_right = min(a.R.count[f], a.R.cap);
@@ -612,6 +633,9 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
     sm.binbuf = reinterpret_cast<uint16_t *>(p);
 
     if (rank == 0 && threadIdx.x == 0 && a.so.n_matched) a.so.n_matched[f] = 0;
+    // SAD median through the group's histograms (hot path), see below
+    const bool med_h = do_rej && finalize && a.med;  // SADs produced by this launch
+    if (med_h && threadIdx.x == 32) sm.misc[6] = (int)group_ticket(a.ep_s + slot, G);
     TL_MARK(a, 0);
     if (threadIdx.x < 32) {  // translate every page the block touches later, now
         const int l = threadIdx.x;
@@ -641,7 +665,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
             for (int b = threadIdx.x; b < H; b += TK_THREADS) sm.row_cursor[b] = 0;
             mbar_wait(mbar, mphase & 1u);  // bit 0: phase of mbar[0]
             mphase ^= 1u;
-            __syncthreads();  // cursor zeroed
+            __syncthreads();  // cursor zeroed, ticket in misc[6]
             TL_MARK(a, 6);
             block_csr<TK_THREADS>(
                 n_right, H,
@@ -652,21 +676,134 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
                 sm.row_start, sm.row_cursor, sm.items, sm.binbuf);
         }
         TL_MARK(a, 1);
+        if (!do_p1) __syncthreads();  // ticket in misc[6]
+        unsigned *medh = med_h ? a.med + ((size_t)slot * 3 + (unsigned)sm.misc[6] % 3u) * MED_WS
+                               : nullptr;
         int *patch = sm.patch + wid * a.patch_ints;
         const bool fixed55 = a.sp.half_window == 5 && a.sp.half_slide == 5;
         for (int k = kf; k < k1; k += TK_WARPS) {
             const LeftKp kp = k == kf ? kp_first : load_left(a, lbase + k);
-            if (fixed55) stereo_kp<5, 5>(a, sm, patch, f, lbase + k, rbase, n_right, kp, lane);
-            else stereo_kp<0, 0>(a, sm, patch, f, lbase + k, rbase, n_right, kp, lane);
+            if (fixed55)
+                stereo_kp<5, 5>(a, sm, patch, f, lbase + k, rbase, n_right, kp, lane, medh);
+            else
+                stereo_kp<0, 0>(a, sm, patch, f, lbase + k, rbase, n_right, kp, lane, medh);
         }
     }
     __syncthreads();
     TL_MARK(a, 2);
     if (!do_rej && !a.so.n_matched) return;
-    group_barrier(bar, G);
+    if (med_h) {  // zero this block's share of the next instance's buffer
+        const unsigned ep = (unsigned)sm.misc[6];
+        unsigned *nb = a.med + ((size_t)slot * 3 + (ep + 1u) % 3u) * MED_WS;
+        const int per = (MED_WS + G - 1) / G, z0 = rank * per, z1 = min(MED_WS, z0 + per);
+        for (int i = z0 + threadIdx.x; i < z1; i += TK_THREADS) nb[i] = 0u;
+    }
+    group_barrier(bar, G, bpar);
     TL_MARK(a, 3);
     int kept = 0;
-    if (do_rej) {
+    bool med_done = false;
+    if (med_h) {
+        // np.median (stereo.py:180) from the group's histograms: coarse bins
+        // locate the bins of ranks (n-1)/2 and n/2, one fine read resolves
+        // them -- two dependent L2 reads by warp 0 instead of gathering every
+        // SAD into every block.  A median among values >= MED_FINE (not seen
+        // in practice) takes the gather path below.
+        const unsigned ep = (unsigned)sm.misc[6];
+        const unsigned *hb = a.med + ((size_t)slot * 3 + ep % 3u) * MED_WS;
+        int64_t ri0 = -1;
+        uint32_t x0 = 0;
+        if (k0 + (int)threadIdx.x < k1) {  // own values, loaded beside the histogram reads
+            ri0 = __ldcg(a.so.right_idx + lbase + k0 + threadIdx.x);
+            x0 = (uint32_t)__ldcg(a.so.sad + lbase + k0 + threadIdx.x);
+        }
+        if (wid == 0) {
+            const unsigned c0 = __ldcg(hb + 2 * lane), c1 = __ldcg(hb + 2 * lane + 1);
+            const unsigned ov = __ldcg(hb + MED_NC);
+            const int sl = (int)(c0 + c1);
+            int incl = sl;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, d);
+                if (lane >= d) incl += y;
+            }
+            const int below = __shfl_sync(FULL, incl, 31);
+            const int nm = below + (int)ov;
+            const int k_lo = (nm - 1) / 2, k_hi = nm / 2;
+            const bool fast = nm == 0 || k_hi < below;
+            int v[2] = {0, 0};
+            if (nm > 0 && fast) {
+                const int excl = incl - sl;
+                int bin[2], rk[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int kk = q ? k_hi : k_lo;
+                    const unsigned bl = __ballot_sync(FULL, excl <= kk && kk < incl);
+                    const int src = __ffs(bl) - 1;
+                    const int e = __shfl_sync(FULL, excl, src);
+                    const int cz = __shfl_sync(FULL, (int)c0, src);
+                    bin[q] = kk < e + cz ? 2 * src : 2 * src + 1;
+                    rk[q] = kk < e + cz ? kk - e : kk - e - cz;
+                }
+                const unsigned *fb = hb + 128;
+                const unsigned f0 = __ldcg(fb + bin[0] * MED_CW + 2 * lane);
+                const unsigned f1 = __ldcg(fb + bin[0] * MED_CW + 2 * lane + 1);
+                const unsigned g0 = __ldcg(fb + bin[1] * MED_CW + 2 * lane);
+                const unsigned g1 = __ldcg(fb + bin[1] * MED_CW + 2 * lane + 1);
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int a0 = (int)(q ? g0 : f0), a1 = (int)(q ? g1 : f1);
+                    int in2 = a0 + a1;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int y = __shfl_up_sync(FULL, in2, d);
+                        if (lane >= d) in2 += y;
+                    }
+                    const int ex2 = in2 - a0 - a1;
+                    const unsigned bl = __ballot_sync(FULL, ex2 <= rk[q] && rk[q] < in2);
+                    const int src = __ffs(bl) - 1;
+                    const int e = __shfl_sync(FULL, ex2, src);
+                    const int cz = __shfl_sync(FULL, a0, src);
+                    v[q] = bin[q] * MED_CW + 2 * src + (rk[q] < e + cz ? 0 : 1);
+                }
+            }
+            if (lane == 0) {
+                sm.misc[4] = nm;
+                sm.misc[7] = fast;
+                sm.misc[8] = v[0];
+                sm.misc[10] = v[1];
+            }
+        }
+        __syncthreads();
+        if (sm.misc[7]) {
+            med_done = true;
+            const int nm = sm.misc[4];
+            const uint32_t v_lo = (uint32_t)sm.misc[8], v_hi = (uint32_t)sm.misc[10];
+            const double med = (nm & 1) ? (double)v_lo : ((double)v_lo + (double)v_hi) / 2.0;
+            const double thr = a.sp.outlier_multiplier * med;
+            TL_MARK(a, 14);
+            for (int k = k0 + threadIdx.x; k < k1; k += TK_THREADS) {
+                int64_t ri = ri0;
+                uint32_t x = x0;
+                if (k != k0 + (int)threadIdx.x) {
+                    ri = __ldcg(a.so.right_idx + lbase + k);
+                    x = (uint32_t)__ldcg(a.so.sad + lbase + k);
+                }
+                if (ri < 0) continue;
+                if ((double)x > thr) {
+                    const int64_t i = lbase + k;
+                    a.so.right_idx[i] = -1;
+                    a.so.distance[i] = 10000;
+                    a.so.disparity[i] = 0.0;
+                    a.so.refined_u[i] = 0.0;
+                    a.so.depth[i] = 0.0;
+                    a.so.sad[i] = 0;
+                } else {
+                    ++kept;
+                }
+            }
+        }
+    }
+    if (do_rej && !med_done) {
         // every block computes the same median over the frame's accepted SADs
         uint32_t *vals = reinterpret_cast<uint32_t *>(sm.rtab_s);  // table no longer needed
         int *hist = sm.hist;
@@ -726,7 +863,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, unsigned long 
                 }
             }
         }
-    } else {
+    } else if (!do_rej) {
         for (int k = k0 + threadIdx.x; k < k1; k += TK_THREADS)
             kept += __ldcg(a.so.right_idx + lbase + k) >= 0;
     }
@@ -907,7 +1044,7 @@ FT_DEV void gather_points(const TrackArgs &a, const MapSmem &sm, const int32_t *
 }
 
 __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigned char *smem,
-                          unsigned long long *mbar, unsigned &mphase) {
+                          unsigned long long *mbar, unsigned &mphase, unsigned &bpar) {
     const int G = a.Gm;
     const int n_pts = min(a.P.count[f], a.P.cap);
     const int n_kp = min(a.K.count[f], a.K.cap);
@@ -923,7 +1060,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     const bool write_slots = a.pmode & FT_PROJ_WRITE_SLOTS;
     const bool ordered = resolve && a.po.corr_point;
     const int round_cap = min(TK_THREADS, a.map_chunk_cap);
-    unsigned long long *bar = a.bar_m + slot;
+    unsigned long long *bar = a.bar_m + 2 * slot;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
     MapSmem sm;
@@ -1019,8 +1156,8 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
         if (!pre_regs && !pidx) stage_points(a, sm, pbase, p0, min(p1, p0 + round_cap), mbar + 1);
     }
     // launch epoch (same for every block of this slot's frame instance)
-    unsigned long long ticket = 0;
-    if (threadIdx.x == 0 && resolve) ticket = atomicAdd(a.ep_m + slot, 1ull);
+    unsigned ticket = 0;
+    if (threadIdx.x == 0 && resolve) ticket = group_ticket(a.ep_m + slot, G);
     if (rank == 0 && threadIdx.x == 0) {
         if (a.po.slot_count) a.po.slot_count[f] = 0;
         if (a.po.corr_count) a.po.corr_count[f] = 0;
@@ -1041,7 +1178,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
         for (int h = threadIdx.x; h < (1 << a.hash_bits); h += TK_THREADS) sm.htab[h] = -1;
     if (have_pts)
         for (int b = threadIdx.x; b < ncell; b += TK_THREADS) sm.cell_cursor[b] = 0;
-    if (threadIdx.x == 0) sm.misc[0] = (int)(unsigned)(ticket / (resolve ? G : 1));
+    if (threadIdx.x == 0) sm.misc[0] = (int)ticket;
     __syncthreads();
     const unsigned epoch_hi = 0xffffffffu - (unsigned)sm.misc[0];
 
@@ -1158,7 +1295,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     }
     TL_MARK(a, 3);
     if (!resolve) return;
-    group_barrier(bar, G);
+    group_barrier(bar, G, bpar);
     TL_MARK(a, 4);
 
     // phase B on this block's points: winner iff its claim is the minimum
@@ -1178,7 +1315,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             atomicAdd(a.hist + (int64_t)f * TK_MAX_BINS + rotation_bin(a, kbase, pbase, kp, i), 1);
     }
     if (rotation) {
-        group_barrier(bar, G);
+        group_barrier(bar, G, bpar);
         if (threadIdx.x == 0) {  // top-K bins by (-count, bin)
             const int nb = pp.histogram_bins;
             const int *h = a.hist + (int64_t)f * TK_MAX_BINS;
@@ -1239,7 +1376,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
         __syncthreads();
         if (threadIdx.x == 0) a.blk_counts[(int64_t)f * G + rank] = sm.misc[2];
     }
-    group_barrier(bar, G);
+    group_barrier(bar, G, bpar);
     int before = 0, all = 0;
     for (int b = threadIdx.x; b < G; b += TK_THREADS) {
         const int c = __ldcg(a.blk_counts + (int64_t)f * G + b);
@@ -1289,12 +1426,12 @@ __global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    unsigned mphase = 0;
+    unsigned mphase = 0, bpar = 0;
     const int per = a.Gs + a.Gm;
     const int slot = blockIdx.x / per, r = blockIdx.x - slot * per;
     for (int f = slot; f < a.F; f += a.W) {
-        if (r < a.Gs) stereo_frame(a, f, r, a.bar_s + slot, smem, mbar, mphase);
-        else map_frame(a, f, r - a.Gs, slot, smem, mbar, mphase);
+        if (r < a.Gs) stereo_frame(a, f, r, slot, smem, mbar, mphase, bpar);
+        else map_frame(a, f, r - a.Gs, slot, smem, mbar, mphase, bpar);
     }
 }
 
@@ -1414,6 +1551,8 @@ static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_
     a.bar_s = ws_ptr<unsigned long long>(ws, wl.track_bar_s);
     a.bar_m = ws_ptr<unsigned long long>(ws, wl.track_bar_m);
     a.ep_m = ws_ptr<unsigned long long>(ws, wl.track_ep_m);
+    a.ep_s = ws_ptr<unsigned long long>(ws, wl.track_ep_s);
+    a.med = getenv("FT_MEDIAN_GATHER") ? nullptr : ws_ptr<unsigned>(ws, wl.track_med);
     a.claims = ws_ptr<unsigned long long>(ws, wl.proj_claims);
     a.blk_counts = ws_ptr<int>(ws, wl.track_blk_counts);
     a.hist = ws_ptr<int>(ws, wl.track_hist);

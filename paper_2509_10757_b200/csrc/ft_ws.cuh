@@ -44,9 +44,16 @@ inline size_t fisheye_entries(int F, int cap_left) {
     return e > floor_e ? e : floor_e;
 }
 
+// SAD-median histogram buffer of one stereo group (ft_track.cu): coarse bins
+// of MED_CW values over [0, MED_FINE) + one overflow bin, padded to 128
+// words, then the fine (one bin per value) histogram.
+constexpr int MED_FINE = 4096, MED_CW = 64, MED_NC = MED_FINE / MED_CW;
+constexpr int MED_WS = 128 + MED_FINE;
+
 struct WsLayout {
     size_t stereo_counters, fisheye_counters, fisheye_partials, proj_claims, track_bar_s,
-        track_bar_m, track_ep_m, track_blk_counts, track_hist, pyr_bar, total;
+        track_bar_m, track_ep_m, track_ep_s, track_med, track_blk_counts, track_hist, pyr_bar,
+        total;
     size_t fisheye_partial_entries;
 };
 
@@ -63,18 +70,22 @@ inline WsLayout ws_layout(int F, int cap_left, int cap_points) {
     o += ws_align(L.fisheye_partial_entries * 8);
     L.proj_claims = o;
     o += ws_align((size_t)F * cap_left * 8);
-    L.track_bar_s = o;
-    o += ws_align((size_t)F * 8);
+    L.track_bar_s = o;  // two barrier words per group (group_barrier)
+    o += ws_align((size_t)F * 16);
     L.track_bar_m = o;
-    o += ws_align((size_t)F * 8);
+    o += ws_align((size_t)F * 16);
     L.track_ep_m = o;
     o += ws_align((size_t)F * 8);
+    L.track_ep_s = o;
+    o += ws_align((size_t)F * 8);
+    L.track_med = o;  // SAD-median histograms: 3 rotating buffers per stereo group
+    o += ws_align((size_t)F * 3 * MED_WS * 4);
     L.track_blk_counts = o;
     o += ws_align((size_t)F * WS_MAX_GROUP * 4);
     L.track_hist = o;
     o += ws_align((size_t)F * 256 * 4);
-    L.pyr_bar = o;  // two images (left, right) per frame
-    o += ws_align((size_t)F * 2 * 8);
+    L.pyr_bar = o;  // two images (left, right) per frame, two words each
+    o += ws_align((size_t)F * 2 * 16);
     L.total = o;
     return L;
 }
