@@ -294,6 +294,19 @@ int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host_in,
 int ft_runner_wait(ft_runner *r, int64_t k);
 int ft_runner_destroy(ft_runner *r);
 
+/* Persistent runner: instead of a graph launch per step, ONE long-lived
+ * ft_track_frames kernel serves the n slots (2..4).  plans[i] holds slot i's
+ * launch (ft_track_plan over that slot's device buffers; all slots the same
+ * shapes).  The H2D stream hands a step to the kernel with a device flag
+ * (stream write), the kernel hands it to the D2H stream with another (stream
+ * wait), so no launch, block scheduling or drain sits between frames.
+ * Submit / wait as above; ft_runner_destroy finishes every submitted step,
+ * then ends the kernel.  The plan's grid must leave SMs free (FT_E_RANGE
+ * otherwise); other kernels may run beside it on those SMs. */
+int ft_runner_create_persistent(int32_t n_slots, const void *const *plans, void *const *dev_in,
+                                size_t in_bytes, void *const *dev_out, void *const *host_out,
+                                size_t out_bytes, ft_runner **out);
+
 /* Packed upload: after one contiguous H2D of a step's needed bytes, place
  * segment i (desc[3i] = source offset, desc[3i+1] = destination offset,
  * desc[3i+2] = length, bytes relative to `base`; desc in DEVICE memory, e.g.
@@ -356,6 +369,17 @@ int ft_track_frames(int32_t n_frames, const ft_keypoints *left, const ft_keypoin
                     const ft_map_points *points, const ft_project_params *pparams,
                     const ft_project_io *io, int32_t pmode, const ft_project_out *pout,
                     const ft_workspace *ws, ft_stream_t stream);
+
+/* The launch ft_track_frames would make with these arguments, recorded into
+ * caller memory (ft_track_plan_bytes() bytes) instead of launched: the input
+ * of ft_runner_create_persistent.  The pointed-to buffers must outlive it. */
+size_t ft_track_plan_bytes(void);
+int ft_track_plan(int32_t n_frames, const ft_keypoints *left, const ft_keypoints *right,
+                  const ft_pyramid *left_pyr, const ft_pyramid *right_pyr,
+                  const ft_stereo_params *sparams, int32_t smode, const ft_stereo_out *sout,
+                  const ft_map_points *points, const ft_project_params *pparams,
+                  const ft_project_io *io, int32_t pmode, const ft_project_out *pout,
+                  const ft_workspace *ws, void *plan, size_t plan_bytes);
 
 /* projection.py:161-178 resolve_conflicts on caller-held phase-A arrays
  * (one frame): correspondences in point order into out->corr_* and

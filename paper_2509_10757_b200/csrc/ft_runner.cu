@@ -17,6 +17,16 @@
 // Compute is one stream, so cooperative kernels never overlap each other.
 // Everything is issued from C: one host call per step.  With n = 3 the host
 // may submit step k once step k-3 is out, so uploads run a full step ahead.
+//
+// Persistent mode (ft_runner_create_persistent): no per-step launch.  One
+// long-lived track kernel (ft_track.cu track_persist_kernel) serves the n
+// slots; the streams hand steps over through device flags with stream memory
+// operations:
+//   H2D stream : wait d2h[i] (step k-n fully out); memcpy ranges;
+//                write ready[i] = k + 1
+//   kernel     : polls ready[i], computes, publishes done[i] = k + 1
+//   D2H stream : wait done[i] >= k + 1; memcpy outputs; record d2h[i]
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -24,8 +34,47 @@
 
 #include "../../include/fasttrack_b200.h"
 
+extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
+                                          cudaStream_t stream);
+extern "C" void ft_internal_persist_dump(void);
+
+namespace {
+constexpr int PERSIST_MAX_SLOTS = 4;  // == ft_track.cu
+constexpr unsigned PERSIST_STOP = 0xffffffffu;
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+// cuStreamWaitValue32 / cuStreamWriteValue32 through the runtime's driver
+// entry-point query (no link-time libcuda dependency)
+bool stream_memops(WaitValue32Fn *wait, WriteValue32Fn *write) {
+    static WaitValue32Fn w = nullptr;
+    static WriteValue32Fn v = nullptr;
+    if (!w || !v) {
+        void *a = nullptr, *b = nullptr;
+        cudaDriverEntryPointQueryResult qa, qb;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &a, cudaEnableDefault, &qa) !=
+                cudaSuccess ||
+            qa != cudaDriverEntryPointSuccess)
+            return false;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &b, cudaEnableDefault, &qb) !=
+                cudaSuccess ||
+            qb != cudaDriverEntryPointSuccess)
+            return false;
+        w = (WaitValue32Fn)a;
+        v = (WriteValue32Fn)b;
+    }
+    *wait = w;
+    *write = v;
+    return true;
+}
+}  // namespace
+
 struct ft_runner {
     int n;
+    bool persistent;
+    unsigned *flags;  // persistent: [ready x 4 | done x 4 | arrive x 4] device words
+    WaitValue32Fn wait32;
+    WriteValue32Fn write32;
     cudaStream_t h2d, comp, d2h;
     cudaEvent_t ev_h2d[FT_RUNNER_MAX_SLOTS], ev_comp[FT_RUNNER_MAX_SLOTS],
         ev_d2h[FT_RUNNER_MAX_SLOTS];
@@ -73,6 +122,48 @@ extern "C" int ft_runner_create_n(int32_t n_slots, const void *const *graph_exec
     return FT_OK;
 }
 
+extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *plans,
+                                           void *const *dev_in, size_t in_bytes,
+                                           void *const *dev_out, void *const *host_out,
+                                           size_t out_bytes, ft_runner **out) {
+    if (!plans || !dev_in || !dev_out || !host_out || !out) return FT_E_NULL;
+    if (n_slots < 2 || n_slots > FT_RUNNER_MAX_SLOTS || n_slots > PERSIST_MAX_SLOTS)
+        return FT_E_RANGE;
+    WaitValue32Fn w;
+    WriteValue32Fn v;
+    if (!stream_memops(&w, &v)) return FT_E_CONFIG;
+    // graph_exec slots are unused in persistent mode: reuse the plan pointers
+    // as non-null placeholders for the shared constructor
+    int st = ft_runner_create_n(n_slots, plans, dev_in, in_bytes, dev_out, host_out, out_bytes,
+                                out);
+    if (st != FT_OK) return st;
+    ft_runner *r = *out;
+    r->persistent = true;
+    r->wait32 = w;
+    r->write32 = v;
+    cudaError_t e = cudaMalloc(&r->flags, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned));
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(r->flags, 0, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned), r->comp);
+    if (e == cudaSuccess) {
+        st = ft_internal_persist_launch(plans, n_slots, r->flags, r->comp);
+        if (st != FT_OK) {
+            cudaStreamSynchronize(r->comp);
+            cudaFree(r->flags);
+            r->flags = nullptr;
+            r->persistent = false;
+            ft_runner_destroy(r);
+            *out = nullptr;
+            return st;
+        }
+    }
+    if (e != cudaSuccess) {
+        ft_runner_destroy(r);
+        *out = nullptr;
+        return (int)e;
+    }
+    return FT_OK;
+}
+
 extern "C" int ft_runner_create(const void *const graph_exec[2], void *const dev_in[2],
                                 size_t in_bytes, void *const dev_out[2],
                                 void *const host_out[2], size_t out_bytes, ft_runner **out) {
@@ -86,6 +177,32 @@ extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host
     for (int q = 0; q < n_ranges; ++q)
         if (ranges[2 * q] > ranges[2 * q + 1] || ranges[2 * q + 1] > r->in_bytes) return FT_E_RANGE;
     const int i = (int)(k % r->n);
+    if (r->persistent) {
+        // slot i's step k-n is out (its outputs copied, so its inputs are
+        // consumed too); then inputs -> ready -> (kernel) -> done -> outputs
+        cudaError_t e = cudaStreamWaitEvent(r->h2d, r->ev_d2h[i], 0);
+        for (int q = 0; q < n_ranges && e == cudaSuccess; ++q) {
+            const size_t lo = ranges[2 * q], n = ranges[2 * q + 1] - lo;
+            if (n)
+                e = cudaMemcpyAsync(static_cast<char *>(r->dev_in[i]) + lo,
+                                    static_cast<const char *>(host_in) + lo, n,
+                                    cudaMemcpyHostToDevice, r->h2d);
+        }
+        const cuuint32_t step = (cuuint32_t)(k + 1);
+        if (e == cudaSuccess &&
+            r->write32((CUstream)r->h2d, (CUdeviceptr)(r->flags + i), step,
+                       CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            return FT_E_CONFIG;
+        if (e == cudaSuccess &&
+            r->wait32((CUstream)r->d2h, (CUdeviceptr)(r->flags + PERSIST_MAX_SLOTS + i), step,
+                      CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            return FT_E_CONFIG;
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(r->host_out[i], r->dev_out[i], r->out_bytes,
+                                cudaMemcpyDeviceToHost, r->d2h);
+        if (e == cudaSuccess) e = cudaEventRecord(r->ev_d2h[i], r->d2h);
+        return (int)e;
+    }
     cudaError_t e = cudaStreamWaitEvent(r->h2d, r->ev_comp[i], 0);
     for (int q = 0; q < n_ranges && e == cudaSuccess; ++q) {
         const size_t lo = ranges[2 * q], n = ranges[2 * q + 1] - lo;
@@ -128,6 +245,22 @@ extern "C" int ft_runner_wait(ft_runner *r, int64_t k) {
 
 extern "C" int ft_runner_destroy(ft_runner *r) {
     if (!r) return FT_OK;
+    if (r->persistent && r->flags) {
+        // every submitted step completes first (its done flag releases the D2H
+        // stream), so all blocks are polling the next ready word -- then stop
+        // the persistent kernel (a stop seen mid-step by a late block would
+        // leave its group at a barrier)
+        cudaStreamSynchronize(r->h2d);
+        cudaStreamSynchronize(r->d2h);
+        for (int i = 0; i < PERSIST_MAX_SLOTS; ++i)
+            r->write32((CUstream)r->h2d, (CUdeviceptr)(r->flags + i), PERSIST_STOP,
+                       CU_STREAM_WRITE_VALUE_DEFAULT);
+        cudaStreamSynchronize(r->h2d);
+        cudaStreamSynchronize(r->comp);
+        ft_internal_persist_dump();
+        cudaFree(r->flags);
+        r->flags = nullptr;
+    }
     cudaStreamSynchronize(r->h2d);
     cudaStreamSynchronize(r->comp);
     cudaStreamSynchronize(r->d2h);

@@ -25,9 +25,11 @@
 //   one warp per left keypoint: phase 1 over the contiguous CSR range of rows
 //   [r0, r1] with a redux.sync min of (dist << 16 | j) (= the reference's
 //   lexicographic (dist, j) order), then phase 2 with the 11x11 / 11x21
-//   patches staged per warp in shared memory.  REJECT: group barrier, then
-//   every stereo block radix-selects the same median over the frame's
-//   accepted SADs and resets its own rejected matches (no serial tail).
+//   patches staged per warp in shared memory.  REJECT: each accepted SAD is
+//   added to the group's coarse + fine histograms (L2 reds) as it is found;
+//   after the group barrier every stereo block locates the same median with
+//   two dependent histogram reads and resets its own rejected matches (no
+//   serial tail; a median above the fine range gathers every SAD instead).
 // Map block: stage the frame's keypoint table + cell-grid CSR (+ a hash set
 //   of slotted point ids) in shared memory; thread-per-point fp64 projection
 //   in the reference's evaluation order; warp per visible point over the
@@ -1436,6 +1438,81 @@ __global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Persistent mode (ft_runner_create_persistent): ONE long-lived cooperative
+// launch steps through a ring of n input/output slots, removing the per-frame
+// launch (graph launch, block scheduling, drain).  Step k uses slot k % n:
+// every block waits until ready[slot] >= k + 1 (written by the runner's H2D
+// stream after the slot's inputs landed), runs its role on that slot's
+// arguments, then arrives on arrive[slot]; the last arrival of the step
+// publishes done[slot] = k + 1, which releases the runner's D2H stream.
+// Blocks run ahead independently -- a block that finished step k starts
+// step k + 1 while others finish k (each slot has its own workspace, so the
+// groups' barrier words and tickets never mix).  ready[] == FT_PERSIST_STOP
+// ends the launch.
+constexpr int PERSIST_MAX_SLOTS = 4;
+constexpr unsigned FT_PERSIST_STOP = 0xffffffffu;
+
+struct PersistArgs {
+    TrackArgs a[PERSIST_MAX_SLOTS];  // identical geometry (W, Gs, Gm) in every slot
+    int n;
+    unsigned *ready;   // [n] step + 1 whose inputs are in the slot (H2D stream)
+    unsigned *done;    // [n] step + 1 whose outputs are complete (this kernel)
+    unsigned *arrive;  // [n] block arrivals (monotonic)
+    unsigned long long *ts;  // debug (FT_DEBUG_PERSIST): [4096][2] step start / done (ns)
+};
+
+FT_DEV unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_constant__ PersistArgs p) {
+    extern __shared__ __align__(16) unsigned char smem_all[];
+    __shared__ int s_go;
+    unsigned long long *mbar = reinterpret_cast<unsigned long long *>(smem_all);
+    unsigned char *smem = smem_all + 16;
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        mbar_init(mbar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned mphase = 0, bpar = 0;
+    const int per = p.a[0].Gs + p.a[0].Gm;
+    const unsigned B = (unsigned)(p.a[0].W * per);
+    const int wslot = blockIdx.x / per, r = blockIdx.x - wslot * per;
+    for (unsigned k = 0;; ++k) {
+        const int i = (int)(k % (unsigned)p.n);
+        if (threadIdx.x == 0) {
+            unsigned v;
+            while ((v = ld_acquire_u32(p.ready + i)) != FT_PERSIST_STOP && v < k + 1)
+                __nanosleep(64);
+            s_go = v != FT_PERSIST_STOP;
+            if (p.ts && blockIdx.x == 0 && s_go) p.ts[2 * (k & 4095u)] = global_ns();
+        }
+        __syncthreads();
+        if (!s_go) break;
+        const TrackArgs &a = p.a[i];
+        for (int f = wslot; f < a.F; f += a.W) {
+            if (r < a.Gs) stereo_frame(a, f, r, wslot, smem, mbar, mphase, bpar);
+            else map_frame(a, f, r - a.Gs, wslot, smem, mbar, mphase, bpar);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            const unsigned old = atomicAdd(p.arrive + i, 1u);
+            if (old + 1u == (k / (unsigned)p.n + 1u) * B) {  // the step's last block
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done + i), "r"(k + 1u)
+                             : "memory");
+                if (p.ts) p.ts[2 * (k & 4095u) + 1] = global_ns();
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 size_t stereo_smem(const TrackArgs &a) {
@@ -1493,8 +1570,10 @@ static int raise_smem_attr(int dev, size_t smem) {
     return FT_OK;
 }
 
-static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_workspace *ws,
-                        cudaStream_t stream) {
+// Geometry, kernel attribute and workspace pointers of a launch (shared by
+// the per-launch path and the persistent plans).
+static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft_workspace *ws,
+                         Geom &g_out) {
     int dev = 0;
     cudaGetDevice(&dev);
     GeomKey key;
@@ -1557,6 +1636,17 @@ static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_
     a.blk_counts = ws_ptr<int>(ws, wl.track_blk_counts);
     a.hist = ws_ptr<int>(ws, wl.track_hist);
     a.tl = nullptr;
+    g_out = g;
+    return FT_OK;
+}
+
+static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_workspace *ws,
+                        cudaStream_t stream) {
+    Geom g;
+    {
+        const int st = track_prepare(a, want_stereo, want_map, ws, g);
+        if (st != FT_OK) return st;
+    }
     static unsigned long long *tl_buf = nullptr;
     if (getenv("FT_DEBUG_TIMELINE")) {
         const size_t n = (size_t)a.W * (a.Gs + a.Gm) * TL_SLOTS;
@@ -1857,6 +1947,112 @@ extern "C" int ft_track_frames(int32_t n_frames, const ft_keypoints *left,
     st = ws_check(ws, n_frames, capl, points->cap);
     if (st != FT_OK) return st;
     return track_launch(a, true, true, ws, (cudaStream_t)stream);
+}
+
+namespace {
+struct TrackPlan {
+    uint32_t magic, version;
+    TrackArgs a;
+    size_t smem;
+};
+constexpr uint32_t PLAN_MAGIC = 0x46545450u;  // "FTTP"
+}  // namespace
+
+extern "C" size_t ft_track_plan_bytes(void) { return sizeof(TrackPlan); }
+
+extern "C" int ft_track_plan(int32_t n_frames, const ft_keypoints *left,
+                             const ft_keypoints *right, const ft_pyramid *left_pyr,
+                             const ft_pyramid *right_pyr, const ft_stereo_params *sparams,
+                             int32_t smode, const ft_stereo_out *sout,
+                             const ft_map_points *points, const ft_project_params *pparams,
+                             const ft_project_io *io, int32_t pmode, const ft_project_out *pout,
+                             const ft_workspace *ws, void *plan, size_t plan_bytes) {
+    if (!plan) return FT_E_NULL;
+    if (plan_bytes < sizeof(TrackPlan)) return FT_E_RANGE;
+    TrackPlan *tp = static_cast<TrackPlan *>(plan);
+    memset(tp, 0, sizeof(*tp));
+    TrackArgs &a = tp->a;
+    a.F = n_frames;
+    int st;
+    if (!fill_stereo(a, n_frames, left, right, left_pyr, right_pyr, sparams, smode, sout, &st))
+        return st;
+    if (!fill_map(a, n_frames, points, left, pparams, io, pmode, pout, &st)) return st;
+    const int capl = left->cap > right->cap ? left->cap : right->cap;
+    st = ws_check(ws, n_frames, capl, points->cap);
+    if (st != FT_OK) return st;
+    Geom g;
+    st = track_prepare(a, true, true, ws, g);
+    if (st != FT_OK) return st;
+    tp->smem = g.smem;
+    tp->magic = PLAN_MAGIC;
+    tp->version = 1;
+    return FT_OK;
+}
+
+static unsigned long long *g_persist_ts = nullptr;
+
+// debug: write the persistent kernel's per-step (start, done) timestamps
+extern "C" void ft_internal_persist_dump(void) {
+    const char *path = getenv("FT_DEBUG_PERSIST");
+    if (!path || !g_persist_ts) return;
+    static unsigned long long h[4096 * 2];
+    cudaMemcpy(h, g_persist_ts, sizeof(h), cudaMemcpyDeviceToHost);
+    FILE *fp = fopen(path, "w");
+    if (!fp) return;
+    for (int k = 0; k < 4096; ++k) fprintf(fp, "%d %llu %llu\n", k, h[2 * k], h[2 * k + 1]);
+    fclose(fp);
+}
+
+// Launch the persistent kernel over n plans (internal: ft_runner.cu).  The
+// plans must share one geometry and leave SMs free for other work (the
+// launch never ends on its own: it would starve every later kernel).
+extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
+                                          cudaStream_t stream) {
+    if (!plans || !flags) return FT_E_NULL;
+    if (n < 1 || n > PERSIST_MAX_SLOTS) return FT_E_RANGE;
+    PersistArgs p;
+    memset(&p, 0, sizeof(p));
+    size_t smem = 0;
+    for (int i = 0; i < n; ++i) {
+        const TrackPlan *tp = static_cast<const TrackPlan *>(plans[i]);
+        if (!tp) return FT_E_NULL;
+        if (tp->magic != PLAN_MAGIC) return FT_E_CONFIG;
+        p.a[i] = tp->a;
+        const TrackArgs &a0 = p.a[0];
+        if (tp->a.W != a0.W || tp->a.Gs != a0.Gs || tp->a.Gm != a0.Gm) return FT_E_CONFIG;
+        smem = tp->smem > smem ? tp->smem : smem;
+    }
+    p.n = n;
+    static unsigned long long *ts_buf = nullptr;
+    if (getenv("FT_DEBUG_PERSIST")) {
+        if (!ts_buf) cudaMalloc(&ts_buf, 4096 * 2 * 8);
+        cudaMemsetAsync(ts_buf, 0, 4096 * 2 * 8, stream);
+        p.ts = ts_buf;
+        g_persist_ts = ts_buf;
+    }
+    p.ready = flags;
+    p.done = flags + PERSIST_MAX_SLOTS;
+    p.arrive = flags + 2 * PERSIST_MAX_SLOTS;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = p.a[0].W * (p.a[0].Gs + p.a[0].Gm);
+    if (grid > sms - 4) return FT_E_RANGE;  // keep SMs for the copies' helper kernels
+    cudaError_t e = cudaFuncSetAttribute(track_persist_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(TK_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, track_persist_kernel, p);
+    return (int)e;
 }
 
 extern "C" int ft_stereo_pinhole(int32_t n_frames, const ft_keypoints *left,

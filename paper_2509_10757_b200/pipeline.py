@@ -388,6 +388,20 @@ class FramePipeline:
                                             self.pparams, self.pio, self.pmode, self.pout,
                                             self.ws, stream.cuda_stream), "ft_track_frames")
 
+    def plan(self):
+        """The track launch of this pipeline's step recorded as an
+        ft_track_plan (input of the persistent runner); None when the step is
+        more than that one launch (device pyramid build / packed upload)."""
+        import ctypes
+        if self.raw or self.packed:
+            return None
+        buf = (ctypes.c_ubyte * int(self.lib.ft_track_plan_bytes()))()
+        _lib.check(self.lib.ft_track_plan(self.S, self.kl, self.kr, self.pl, self.pr,
+                                          self.sparams, self.smode, self.sout, self.points,
+                                          self.pparams, self.pio, self.pmode, self.pout,
+                                          self.ws, buf, len(buf)), "ft_track_plan")
+        return buf
+
     def launch_pyramids(self, stream) -> None:
         if self.raw:
             S2 = 2 * self.S
@@ -519,9 +533,15 @@ class AsyncRunner:
     Compute is serialised on one stream (one cooperative launch at a time);
     H2D of step k+1 and D2H of step k-1 run on the two copy engines while
     step k computes.  ``wait(k)`` blocks until step k's results are in
-    ``pipes[k % 2]`` host memory."""
+    ``pipes[k % 2]`` host memory.
 
-    def __init__(self, pipes):
+    persistent=True (pipelines whose step is the one track launch): no launch
+    per step -- one long-lived track kernel serves the slots, handed each
+    step by device flags the copy streams write / wait on
+    (ft_runner_create_persistent).  close() ends it after the submitted
+    steps; until then the kernel holds its SMs."""
+
+    def __init__(self, pipes, persistent: bool = False):
         import ctypes
         if not 2 <= len(pipes) <= 4:
             raise ValueError("AsyncRunner takes 2..4 identically shaped pipelines")
@@ -533,20 +553,30 @@ class AsyncRunner:
         self.pipes = pipes
         self.n = len(pipes)
         self.lib = a.lib
-        for p in pipes:
-            if p.graph_runner is None:
-                p.capture()
+        self.persistent = bool(persistent)
         vpn = ctypes.c_void_p * self.n
-        execs = vpn(*[_graph_exec_ptr(p.graph_runner) for p in pipes])
+        if self.persistent:
+            plans = [p.plan() for p in pipes]
+            if any(pl is None for pl in plans):
+                raise ValueError("persistent runner: each step must be the one track launch "
+                                 "(no raw images / packed upload)")
+            execs = vpn(*[ctypes.addressof(pl) for pl in plans])
+        else:
+            plans = None
+            for p in pipes:
+                if p.graph_runner is None:
+                    p.capture()
+            execs = vpn(*[_graph_exec_ptr(p.graph_runner) for p in pipes])
         dev_in = vpn(*[p.dev.data_ptr() for p in pipes])
         dev_out = vpn(*[p.dev.data_ptr() + p.out_begin for p in pipes])
         host_out = vpn(*[p.host.data_ptr() + p.out_begin for p in pipes])
         self._r = ctypes.c_void_p()
         torch.cuda.synchronize(a.device)
-        _lib.check(self.lib.ft_runner_create_n(self.n, execs, dev_in, a.in_end, dev_out,
-                                               host_out, a.out_end - a.out_begin,
-                                               ctypes.byref(self._r)), "ft_runner_create")
-        self._keep = (execs, dev_in, dev_out, host_out)
+        create = (self.lib.ft_runner_create_persistent if self.persistent
+                  else self.lib.ft_runner_create_n)
+        _lib.check(create(self.n, execs, dev_in, a.in_end, dev_out, host_out,
+                          a.out_end - a.out_begin, ctypes.byref(self._r)), "ft_runner_create")
+        self._keep = (execs, dev_in, dev_out, host_out, plans)
 
     def submit(self, k: int, inputs: torch.Tensor | None = None,
                rng: tuple[int, int] | None = None) -> None:

@@ -400,3 +400,64 @@ def test_copy_ranges_alignments():
     for d, v in want:
         assert torch.equal(base[d:d + len(v)], v)
     assert lib.ft_copy_ranges(None, dd.data_ptr(), 1, None) == -1
+
+
+@pytest.mark.parametrize("n_streams", [1, 2])
+def test_persistent_runner(workloads, expected, n_streams):
+    """Persistent runner: one long-lived track kernel serves 3 slots, steps
+    handed over by device flags (no launch per step); every step's results
+    equal the oracle's, including with level-range shipping (S = 1) and
+    garbage in the unshipped bytes."""
+    from paper_2509_10757_b200 import _lib
+    from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
+    w0 = workloads[0]
+    S = n_streams
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    pipes = [FramePipeline(w0.cam, n_streams=S, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left,
+                           packed_upload=False) for _ in range(3)]
+    ring = pipes[0].staging_ring(4)
+    ranges = []
+    for k in range(4):
+        for s in range(S):
+            w = workloads[(k + s) % 4]
+            pipes[0].load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                                slots=expected[(k + s) % 4][1])
+        pipes[0].stage_into(ring[k])
+        ranges.append(pipes[0].input_ranges())
+    for p in pipes:
+        p.dev.fill_(0xAB)
+    try:
+        runner = AsyncRunner(pipes, persistent=True)
+    except _lib.FtError as exc:
+        # a grid that would hold (nearly) every SM is refused up front
+        assert "status -2" in str(exc) and S > 1
+        pipes[0].replay(copies=False)
+        pipes[0].synchronize()
+        return
+
+    def check(pipe, k):
+        for s in range(S):
+            i = (k % 4 + s) % 4
+            w = workloads[i]
+            m, _, slots, n = expected[i]
+            res = pipe.result(s, len(w.left.u))
+            for f in FIELDS:
+                np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f),
+                                              err_msg=f"step {k} stream {s} {f}")
+            np.testing.assert_array_equal(res.slots, slots, err_msg=f"step {k} stream {s}")
+            assert res.n_slots == n
+
+    try:
+        n_steps = 40
+        for k in range(n_steps):
+            if k >= 3:
+                check(runner.wait(k - 3), k - 3)
+            runner.submit(k, ring[k % 4], ranges[k % 4])
+        for k in range(n_steps - 3, n_steps):
+            check(runner.wait(k), k)
+    finally:
+        runner.close()
+    # the kernel has ended: ordinary launches run again on the same pipelines
+    pipes[0].replay(copies=False)
+    pipes[0].synchronize()
