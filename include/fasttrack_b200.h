@@ -273,7 +273,7 @@ int ft_scatter_points(int32_t n, const ft_point_record *recs, const int32_t *slo
  * ft_runner_wait(k) blocks until step k's outputs are on the host.  Slot
  * buffers are reused n steps later (the runner orders that itself). */
 typedef struct ft_runner ft_runner;
-#define FT_RUNNER_MAX_SLOTS 4
+#define FT_RUNNER_MAX_SLOTS 8
 int ft_runner_create(const void *const graph_exec[2], void *const dev_in[2], size_t in_bytes,
                      void *const dev_out[2], void *const host_out[2], size_t out_bytes,
                      ft_runner **out);
@@ -295,7 +295,7 @@ int ft_runner_wait(ft_runner *r, int64_t k);
 int ft_runner_destroy(ft_runner *r);
 
 /* Persistent runner: instead of a graph launch per step, ONE long-lived
- * ft_track_frames kernel serves the n slots (2..4).  plans[i] holds slot i's
+ * ft_track_frames kernel serves the n slots (2..8).  plans[i] holds slot i's
  * launch (ft_track_plan over that slot's device buffers; all slots the same
  * shapes).  The H2D stream hands a step to the kernel with a device flag
  * (stream write), the kernel hands it to the D2H stream with another (stream

@@ -39,7 +39,7 @@ extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsig
 extern "C" void ft_internal_persist_dump(void);
 
 namespace {
-constexpr int PERSIST_MAX_SLOTS = 4;  // == ft_track.cu
+constexpr int PERSIST_MAX_SLOTS = 8;  // == ft_track.cu
 constexpr unsigned PERSIST_STOP = 0xffffffffu;
 typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);

@@ -82,6 +82,12 @@ struct TrackArgs {
     unsigned long long *ep_m;    // [W] map-group instance tickets (group_ticket)
     unsigned long long *ep_s;    // [W] stereo-group instance tickets
     unsigned *med;               // [W][3][MED_WS] SAD-median histograms
+    unsigned long long *tail_s;  // [W] stereo-group arrivals (tail mode)
+    unsigned long long *tail_m;  // [W] map-group arrivals (tail mode)
+    int4 *mcand;                 // [W][cap_points] map candidates (tail mode)
+    int *mcnt;                   // [W][WS_MAX_GROUP][2] candidates, prefilled slots per block
+    int32_t stereo_tail;         // one frame per group: a dedicated block runs the stereo tail
+    int32_t map_tail;            // ... and the map resolve
     unsigned long long *claims;  // [F][cap_kp]
     int *blk_counts;             // [F][Gm]
     int *hist;                   // [F][TK_MAX_BINS]
@@ -586,12 +592,162 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
     }
 }
 
+// np.median (stereo.py:180) of a group's accepted SADs from its histograms
+// (warp 0): coarse bins locate the bins of ranks (n-1)/2 and n/2, one fine
+// read resolves them.  misc[4] = n, misc[7] = resolved (0: the median lies
+// at or above MED_FINE -- decide from the values), misc[8] / misc[10] = the
+// two order statistics.
+FT_DEV void warp_hist_median(const unsigned *hb, int lane, int *misc) {
+    const unsigned c0 = __ldcg(hb + 2 * lane), c1 = __ldcg(hb + 2 * lane + 1);
+    const unsigned ov = __ldcg(hb + MED_NC);
+    const int sl = (int)(c0 + c1);
+    int incl = sl;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += y;
+    }
+    const int below = __shfl_sync(FULL, incl, 31);
+    const int nm = below + (int)ov;
+    const int k_lo = (nm - 1) / 2, k_hi = nm / 2;
+    const bool fast = nm == 0 || k_hi < below;
+    int v[2] = {0, 0};
+    if (nm > 0 && fast) {
+        const int excl = incl - sl;
+        int bin[2], rk[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int kk = q ? k_hi : k_lo;
+            const unsigned bl = __ballot_sync(FULL, excl <= kk && kk < incl);
+            const int src = __ffs(bl) - 1;
+            const int e = __shfl_sync(FULL, excl, src);
+            const int cz = __shfl_sync(FULL, (int)c0, src);
+            bin[q] = kk < e + cz ? 2 * src : 2 * src + 1;
+            rk[q] = kk < e + cz ? kk - e : kk - e - cz;
+        }
+        const unsigned *fb = hb + 128;
+        const unsigned f0 = __ldcg(fb + bin[0] * MED_CW + 2 * lane);
+        const unsigned f1 = __ldcg(fb + bin[0] * MED_CW + 2 * lane + 1);
+        const unsigned g0 = __ldcg(fb + bin[1] * MED_CW + 2 * lane);
+        const unsigned g1 = __ldcg(fb + bin[1] * MED_CW + 2 * lane + 1);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int a0 = (int)(q ? g0 : f0), a1 = (int)(q ? g1 : f1);
+            int in2 = a0 + a1;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(FULL, in2, d);
+                if (lane >= d) in2 += y;
+            }
+            const int ex2 = in2 - a0 - a1;
+            const unsigned bl = __ballot_sync(FULL, ex2 <= rk[q] && rk[q] < in2);
+            const int src = __ffs(bl) - 1;
+            const int e = __shfl_sync(FULL, ex2, src);
+            const int cz = __shfl_sync(FULL, a0, src);
+            v[q] = bin[q] * MED_CW + 2 * src + (rk[q] < e + cz ? 0 : 1);
+        }
+    }
+    if (lane == 0) {
+        misc[4] = nm;
+        misc[7] = fast;
+        misc[8] = v[0];
+        misc[10] = v[1];
+    }
+}
+
 // shared table region of a stereo block: the staged right table, or at least
 // the median scratch (4 B per left keypoint)
 __host__ __device__ inline size_t stereo_table_bytes(const TrackArgs &a) {
     const size_t t = a.stage_rdesc ? (size_t)64 * a.R.cap : 0;
     const size_t m = (size_t)4 * a.L.cap;
     return ((t > m ? t : m) + 15) & ~(size_t)15;
+}
+
+// The frame's stereo tail in one block (tail mode): every keypoint's
+// (right_idx, sad) into shared memory, the median of the accepted SADs (the
+// group histograms when this launch produced them, else radix select over
+// the values), rejection (stereo.py:171-188) and the match count.
+__device__ void stereo_tail(const TrackArgs &a, const StereoSmem &sm, int f, int slot,
+                            int n_left, int64_t lbase, bool med_h) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool do_rej = a.smode & FT_STEREO_REJECT;
+    uint32_t *vals = reinterpret_cast<uint32_t *>(sm.rtab_s);  // table no longer needed
+    const unsigned ep = med_h ? (unsigned)sm.misc[6] : 0u;
+    const unsigned *hb = med_h ? a.med + ((size_t)slot * 3 + ep % 3u) * MED_WS : nullptr;
+    if (threadIdx.x == 0) {
+        sm.misc[4] = 0;
+        sm.misc[5] = 0;
+        sm.misc[12] = 0;
+    }
+    __syncthreads();
+    if (med_h && do_rej && wid == 0) warp_hist_median(hb, lane, sm.misc);
+    int cnt = 0;
+    uint32_t vmax = 0;
+    for (int k = threadIdx.x; k < n_left; k += TK_THREADS) {
+        const bool m = __ldcg(a.so.right_idx + lbase + k) >= 0;
+        const uint32_t x = m ? (uint32_t)__ldcg(a.so.sad + lbase + k) : 0xffffffffu;
+        vals[k] = x;
+        cnt += m;
+        if (m) vmax = max(vmax, x);
+    }
+    cnt = __reduce_add_sync(FULL, cnt);
+    vmax = __reduce_max_sync(FULL, vmax);
+    __syncthreads();  // warp 0's histogram result in misc[4, 7, 8, 10]
+    const bool resolved = med_h && do_rej && sm.misc[7];
+    if (lane == 0) {
+        atomicAdd(&sm.misc[12], cnt);
+        atomicMax(reinterpret_cast<unsigned *>(&sm.misc[5]), vmax);
+    }
+    __syncthreads();
+    const int nm = sm.misc[12];
+    int kept = 0;
+    if (do_rej && nm > 0) {
+        uint32_t v_lo, v_hi;
+        if (resolved) {
+            v_lo = (uint32_t)sm.misc[8];
+            v_hi = (uint32_t)sm.misc[10];
+        } else {
+            const size_t vbytes = ((size_t)4 * a.L.cap + 15) & ~(size_t)15;
+            if ((uint32_t)sm.misc[5] < (uint32_t)MED_SMALL_BINS &&
+                stereo_table_bytes(a) >= vbytes + 4 * (size_t)MED_SMALL_BINS)
+                block_median_pair_small(vals, n_left, nm,
+                                        reinterpret_cast<int *>(
+                                            reinterpret_cast<unsigned char *>(sm.rtab_s) + vbytes),
+                                        sm.scan_tmp, sm.misc, v_lo, v_hi);
+            else
+                block_median_pair(vals, n_left, nm, (uint32_t)sm.misc[5], sm.hist, sm.misc, v_lo,
+                                  v_hi);
+        }
+        const double med = (nm & 1) ? (double)v_lo : ((double)v_lo + (double)v_hi) / 2.0;
+        const double thr = a.sp.outlier_multiplier * med;
+        TL_MARK(a, 14);
+        for (int k = threadIdx.x; k < n_left; k += TK_THREADS) {
+            const uint32_t x = vals[k];
+            if (x == 0xffffffffu) continue;
+            if ((double)x > thr) {
+                const int64_t i = lbase + k;
+                a.so.right_idx[i] = -1;
+                a.so.distance[i] = 10000;
+                a.so.disparity[i] = 0.0;
+                a.so.refined_u[i] = 0.0;
+                a.so.depth[i] = 0.0;
+                a.so.sad[i] = 0;
+            } else {
+                ++kept;
+            }
+        }
+    } else {
+        for (int k = threadIdx.x; k < n_left; k += TK_THREADS) kept += vals[k] != 0xffffffffu;
+    }
+    if (a.so.n_matched) {
+        kept = __reduce_add_sync(FULL, kept);
+        if (lane == 0 && kept) atomicAdd(a.so.n_matched + f, kept);
+    }
+    if (med_h) {  // next instance's histogram buffer: zero (nobody else is on it)
+        unsigned *nb = a.med + ((size_t)slot * 3 + (ep + 1u) % 3u) * MED_WS;
+        for (int i = threadIdx.x; i < MED_WS; i += TK_THREADS) nb[i] = 0u;
+    }
+    __syncthreads();  // smem reuse by the next frame of this block
 }
 
 __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
@@ -602,8 +758,10 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
     const int n_left = min(a.L.count[f], a.L.cap);
     const int n_right = min(a.R.count[f], a.R.cap);
     const int64_t lbase = (int64_t)f * a.L.cap, rbase = (int64_t)f * a.R.cap;
-    const int chunk = (n_left + G - 1) / G;
-    const int k0 = rank * chunk, k1 = min(n_left, k0 + chunk);
+    // tail mode: rank G-1 is the group's tail block (no keypoints)
+    const int Gw = a.stereo_tail ? G - 1 : G;
+    const int chunk = (n_left + Gw - 1) / Gw;
+    const int k0 = rank < Gw ? rank * chunk : n_left, k1 = min(n_left, k0 + chunk);
     const int H = a.sp.height;
     const bool do_p1 = a.smode & FT_STEREO_PHASE1;
     const bool do_ref = a.smode & FT_STEREO_REFINE;
@@ -694,6 +852,33 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
     __syncthreads();
     TL_MARK(a, 2);
     if (!do_rej && !a.so.n_matched) return;
+    if (a.stereo_tail) {
+        // Tail mode (one frame per group in this launch): no group barrier.
+        // The G-1 keypoint blocks publish their results with one release
+        // reduction each and are done (persistent mode: on to the next
+        // step); the dedicated tail block waits for them and runs the frame's
+        // tail -- median, rejection, match count over every keypoint.
+        if (rank < Gw) {
+            if (threadIdx.x == 0) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                atomicAdd(a.tail_s + slot, 1ull);
+            }
+            return;
+        }
+        if (threadIdx.x == 0) {
+            unsigned long long v;
+            while ((uint32_t)(v = ld_acquire_u64(a.tail_s + slot)) != (uint32_t)Gw)
+                __nanosleep(20);
+            // arrivals back to 0 for the group's next frame (after this one)
+            atomicAdd(a.tail_s + slot, (1ull << 32) - (unsigned long long)Gw);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        __syncthreads();
+        TL_MARK(a, 3);
+        stereo_tail(a, sm, f, slot, n_left, lbase, med_h);
+        TL_MARK(a, 4);
+        return;
+    }
     if (med_h) {  // zero this block's share of the next instance's buffer
         const unsigned ep = (unsigned)sm.misc[6];
         unsigned *nb = a.med + ((size_t)slot * 3 + (ep + 1u) % 3u) * MED_WS;
@@ -718,63 +903,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
             ri0 = __ldcg(a.so.right_idx + lbase + k0 + threadIdx.x);
             x0 = (uint32_t)__ldcg(a.so.sad + lbase + k0 + threadIdx.x);
         }
-        if (wid == 0) {
-            const unsigned c0 = __ldcg(hb + 2 * lane), c1 = __ldcg(hb + 2 * lane + 1);
-            const unsigned ov = __ldcg(hb + MED_NC);
-            const int sl = (int)(c0 + c1);
-            int incl = sl;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int y = __shfl_up_sync(FULL, incl, d);
-                if (lane >= d) incl += y;
-            }
-            const int below = __shfl_sync(FULL, incl, 31);
-            const int nm = below + (int)ov;
-            const int k_lo = (nm - 1) / 2, k_hi = nm / 2;
-            const bool fast = nm == 0 || k_hi < below;
-            int v[2] = {0, 0};
-            if (nm > 0 && fast) {
-                const int excl = incl - sl;
-                int bin[2], rk[2];
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int kk = q ? k_hi : k_lo;
-                    const unsigned bl = __ballot_sync(FULL, excl <= kk && kk < incl);
-                    const int src = __ffs(bl) - 1;
-                    const int e = __shfl_sync(FULL, excl, src);
-                    const int cz = __shfl_sync(FULL, (int)c0, src);
-                    bin[q] = kk < e + cz ? 2 * src : 2 * src + 1;
-                    rk[q] = kk < e + cz ? kk - e : kk - e - cz;
-                }
-                const unsigned *fb = hb + 128;
-                const unsigned f0 = __ldcg(fb + bin[0] * MED_CW + 2 * lane);
-                const unsigned f1 = __ldcg(fb + bin[0] * MED_CW + 2 * lane + 1);
-                const unsigned g0 = __ldcg(fb + bin[1] * MED_CW + 2 * lane);
-                const unsigned g1 = __ldcg(fb + bin[1] * MED_CW + 2 * lane + 1);
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int a0 = (int)(q ? g0 : f0), a1 = (int)(q ? g1 : f1);
-                    int in2 = a0 + a1;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const int y = __shfl_up_sync(FULL, in2, d);
-                        if (lane >= d) in2 += y;
-                    }
-                    const int ex2 = in2 - a0 - a1;
-                    const unsigned bl = __ballot_sync(FULL, ex2 <= rk[q] && rk[q] < in2);
-                    const int src = __ffs(bl) - 1;
-                    const int e = __shfl_sync(FULL, ex2, src);
-                    const int cz = __shfl_sync(FULL, a0, src);
-                    v[q] = bin[q] * MED_CW + 2 * src + (rk[q] < e + cz ? 0 : 1);
-                }
-            }
-            if (lane == 0) {
-                sm.misc[4] = nm;
-                sm.misc[7] = fast;
-                sm.misc[8] = v[0];
-                sm.misc[10] = v[1];
-            }
-        }
+        if (wid == 0) warp_hist_median(hb, lane, sm.misc);
         __syncthreads();
         if (sm.misc[7]) {
             med_done = true;
@@ -1045,14 +1174,125 @@ FT_DEV void gather_points(const TrackArgs &a, const MapSmem &sm, const int32_t *
     }
 }
 
+// Tail mode of the map group (one frame per group, resolve without ordered
+// outputs / rotation filter): no group barrier.  The Gw point blocks publish
+// their accepted candidates -- (point id, point index | slot-was-empty << 31,
+// keypoint | dist << 16 | level << 25) -- compactly at [p0, p0 + n) of the
+// frame slot's candidate list plus (n, prefilled slots), arrive with one
+// release reduction and are done.  The dedicated resolve block (rank Gw)
+// waits for them, then runs phase B (projection.py:161-178: a candidate wins
+// iff its claim is the keypoint's minimum) and the slot writes
+// (localmap.py:113-121) over every candidate, and stores the counts.
+__device__ void map_tail(const TrackArgs &a, const MapSmem &sm, int f, int rank, int slot, int Gw,
+                         int chunk, int p0, int p1, int n_pts, int64_t pbase, int64_t kbase,
+                         unsigned epoch_hi, bool write_slots, int prefilled) {
+    const int lane = threadIdx.x & 31;
+    int4 *list = a.mcand + (size_t)slot * a.P.cap;
+    int *cnt = a.mcnt + (size_t)slot * WS_MAX_GROUP * 2;
+    if (threadIdx.x == 0) sm.misc[9] = 0;
+    __syncthreads();
+    {
+        const int pf = __reduce_add_sync(FULL, prefilled);
+        if (lane == 0 && pf) atomicAdd(&sm.misc[9], pf);
+    }
+    if (rank < Gw) {
+        int base = p0;
+        for (int r0 = p0; r0 < p1; r0 += TK_THREADS) {
+            const int i = r0 + threadIdx.x;
+            const int r = i < p1 ? sm.res[i - p0] : -1;
+            int total;
+            const int pos = base + block_exclusive_scan<TK_THREADS>(r >= 0, sm.scan_tmp, total);
+            if (r >= 0) {
+                const long long pid = sm.res_pid[i - p0];
+                const int em = write_slots && sm.res_empty[i - p0];
+                list[pos] = make_int4((int)(unsigned long long)pid, (int)((unsigned long long)pid >> 32),
+                                      i | (em << 31), r);
+            }
+            base += total;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            cnt[2 * rank] = base - p0;
+            cnt[2 * rank + 1] = sm.misc[9];
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            atomicAdd(a.tail_m + slot, 1ull);
+        }
+        return;
+    }
+    if (threadIdx.x == 0) {
+        while ((uint32_t)ld_acquire_u64(a.tail_m + slot) != (uint32_t)Gw) __nanosleep(20);
+        atomicAdd(a.tail_m + slot, (1ull << 32) - (unsigned long long)Gw);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    __syncthreads();
+    TL_MARK(a, 4);
+    // per-block counts -> prefix in sm.res (host guarantees map_chunk_cap > Gw)
+    int c = 0, pf = 0;
+    if (threadIdx.x < Gw) {
+        c = __ldcg(cnt + 2 * threadIdx.x);
+        pf = __ldcg(cnt + 2 * threadIdx.x + 1);
+    }
+    int total;
+    const int before = block_exclusive_scan<TK_THREADS>(c, sm.scan_tmp, total);
+    int *pre = sm.res;
+    if (threadIdx.x < Gw) pre[threadIdx.x] = before;
+    if (threadIdx.x == 0) pre[Gw] = total;
+    pf = __reduce_add_sync(FULL, pf);
+    if (lane == 0 && pf) atomicAdd(&sm.misc[9], pf);
+    __syncthreads();
+    int added = 0, n_win = 0;
+    for (int q = threadIdx.x; q < total; q += TK_THREADS) {
+        int lo = 0, hi = Gw - 1;  // block b: pre[b] <= q < pre[b + 1]
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pre[mid] <= q) lo = mid;
+            else hi = mid - 1;
+        }
+        const int4 e = __ldcg(list + lo * chunk + (q - pre[lo]));
+        const int i = e.z & 0x7fffffff, r = e.w;
+        const int kp = r & 0xffff, d = (r >> 16) & 0x1ff;
+        const unsigned long long key = ((unsigned long long)epoch_hi << 32) |
+                                       ((unsigned long long)d << 23) | (unsigned)i;
+        if (__ldcg(a.claims + kbase + kp) != key) continue;
+        ++n_win;
+        if (e.z < 0) {  // slot empty before the search
+            a.io.slots_out[kbase + kp] =
+                (long long)(((unsigned long long)(unsigned)e.y << 32) | (unsigned)e.x);
+            ++added;
+        }
+    }
+    added = __reduce_add_sync(FULL, added);
+    n_win = __reduce_add_sync(FULL, n_win);
+    if (threadIdx.x == 0) {
+        sm.misc[10] = 0;
+        sm.misc[11] = 0;
+    }
+    __syncthreads();
+    if (lane == 0) {
+        if (added) atomicAdd(&sm.misc[10], added);
+        if (n_win) atomicAdd(&sm.misc[11], n_win);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (write_slots && a.po.slot_count) a.po.slot_count[f] = sm.misc[9] + sm.misc[10];
+        if (a.po.corr_count) a.po.corr_count[f] = sm.misc[11];
+    }
+    (void)n_pts;
+    (void)pbase;
+    __syncthreads();
+    TL_MARK(a, 5);
+}
+
 __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigned char *smem,
                           unsigned long long *mbar, unsigned &mphase, unsigned &bpar) {
     const int G = a.Gm;
     const int n_pts = min(a.P.count[f], a.P.cap);
     const int n_kp = min(a.K.count[f], a.K.cap);
     const int64_t pbase = (int64_t)f * a.P.cap, kbase = (int64_t)f * a.K.cap;
-    const int chunk = (((n_pts + G - 1) / G) + 1) & ~1;  // even: 16-B aligned TMA sources
-    const int p0 = min(n_pts, rank * chunk), p1 = min(n_pts, p0 + chunk);
+    // tail mode: rank G-1 is the group's resolve block (no points)
+    const int Gw = a.map_tail ? G - 1 : G;
+    const int chunk = (((n_pts + Gw - 1) / Gw) + 1) & ~1;  // even: 16-B aligned TMA sources
+    const int p0 = rank < Gw ? min(n_pts, rank * chunk) : n_pts, p1 = min(n_pts, p0 + chunk);
     const ft_project_params &pp = a.pp;
     const int nx = pp.grid_nx, ny = pp.grid_ny, ncell = nx * ny;
     const int cap_kp = a.K.cap;
@@ -1297,6 +1537,11 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     }
     TL_MARK(a, 3);
     if (!resolve) return;
+    if (a.map_tail) {
+        map_tail(a, sm, f, rank, slot, Gw, chunk, p0, p1, n_pts, pbase, kbase, epoch_hi,
+                 write_slots, prefilled);
+        return;
+    }
     group_barrier(bar, G, bpar);
     TL_MARK(a, 4);
 
@@ -1449,7 +1694,7 @@ __global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
 // step k + 1 while others finish k (each slot has its own workspace, so the
 // groups' barrier words and tickets never mix).  ready[] == FT_PERSIST_STOP
 // ends the launch.
-constexpr int PERSIST_MAX_SLOTS = 4;
+constexpr int PERSIST_MAX_SLOTS = 8;
 constexpr unsigned FT_PERSIST_STOP = 0xffffffffu;
 
 struct PersistArgs {
@@ -1573,7 +1818,7 @@ static int raise_smem_attr(int dev, size_t smem) {
 // Geometry, kernel attribute and workspace pointers of a launch (shared by
 // the per-launch path and the persistent plans).
 static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft_workspace *ws,
-                         Geom &g_out) {
+                         Geom &g_out, bool tails) {
     int dev = 0;
     cudaGetDevice(&dev);
     GeomKey key;
@@ -1632,6 +1877,38 @@ static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft
     a.ep_m = ws_ptr<unsigned long long>(ws, wl.track_ep_m);
     a.ep_s = ws_ptr<unsigned long long>(ws, wl.track_ep_s);
     a.med = getenv("FT_MEDIAN_GATHER") ? nullptr : ws_ptr<unsigned>(ws, wl.track_med);
+    a.tail_s = ws_ptr<unsigned long long>(ws, wl.track_tail_s);
+    a.tail_m = ws_ptr<unsigned long long>(ws, wl.track_tail_m);
+    a.mcand = ws_ptr<int4>(ws, wl.track_mcand);
+    a.mcnt = ws_ptr<int>(ws, wl.track_mcnt);
+    // one frame per group slot: a dedicated tail block (one more stereo
+    // block) runs the frame's stereo tail, the keypoint blocks never wait
+    a.stereo_tail = 0;
+    // (persistent plans: the keypoint / point blocks go straight on to the
+    // next step; a single launch gains nothing from it -- the kernel still
+    // ends with the tail -- so per-launch calls keep the group barriers)
+    tails = tails || getenv("FT_TAIL_LAUNCH");
+    if (tails && want_stereo && a.W >= a.F && !getenv("FT_STEREO_BARRIER")) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (a.W * (a.Gs + 1 + a.Gm) <= sms) {
+            a.Gs += 1;
+            a.stereo_tail = 1;
+        }
+    }
+    // ... and a dedicated resolve block for the map group (plain resolve:
+    // no ordered correspondences, no rotation filter)
+    a.map_tail = 0;
+    if (tails && want_map && a.W >= a.F && (a.pmode & FT_PROJ_RESOLVE) && !a.po.corr_point &&
+        !((a.pmode & FT_PROJ_ROTATION) && a.io.ref_angles) && a.map_chunk_cap > a.Gm + 1 &&
+        a.Gm + 1 <= WS_MAX_GROUP && !getenv("FT_MAP_BARRIER")) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (a.W * (a.Gs + a.Gm + 1) <= sms) {
+            a.Gm += 1;
+            a.map_tail = 1;
+        }
+    }
     a.claims = ws_ptr<unsigned long long>(ws, wl.proj_claims);
     a.blk_counts = ws_ptr<int>(ws, wl.track_blk_counts);
     a.hist = ws_ptr<int>(ws, wl.track_hist);
@@ -1644,7 +1921,7 @@ static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_
                         cudaStream_t stream) {
     Geom g;
     {
-        const int st = track_prepare(a, want_stereo, want_map, ws, g);
+        const int st = track_prepare(a, want_stereo, want_map, ws, g, false);
         if (st != FT_OK) return st;
     }
     static unsigned long long *tl_buf = nullptr;
@@ -1958,6 +2235,10 @@ struct TrackPlan {
 constexpr uint32_t PLAN_MAGIC = 0x46545450u;  // "FTTP"
 }  // namespace
 
+static unsigned long long *g_plan_tl = nullptr;
+static size_t g_plan_tl_n = 0;
+static int g_plan_tl_hdr[4];
+
 extern "C" size_t ft_track_plan_bytes(void) { return sizeof(TrackPlan); }
 
 extern "C" int ft_track_plan(int32_t n_frames, const ft_keypoints *left,
@@ -1981,8 +2262,20 @@ extern "C" int ft_track_plan(int32_t n_frames, const ft_keypoints *left,
     st = ws_check(ws, n_frames, capl, points->cap);
     if (st != FT_OK) return st;
     Geom g;
-    st = track_prepare(a, true, true, ws, g);
+    st = track_prepare(a, true, true, ws, g, true);
     if (st != FT_OK) return st;
+    if (getenv("FT_DEBUG_TIMELINE")) {  // debug: every step overwrites one timeline
+        const size_t n = (size_t)a.W * (a.Gs + a.Gm) * TL_SLOTS;
+        if (!g_plan_tl) cudaMalloc(&g_plan_tl, 1 << 20);
+        if (n * 8 <= (1 << 20)) {
+            a.tl = g_plan_tl;
+            g_plan_tl_n = n;
+            g_plan_tl_hdr[0] = a.F;
+            g_plan_tl_hdr[1] = a.W;
+            g_plan_tl_hdr[2] = a.Gs;
+            g_plan_tl_hdr[3] = a.Gm;
+        }
+    }
     tp->smem = g.smem;
     tp->magic = PLAN_MAGIC;
     tp->version = 1;
@@ -2001,6 +2294,21 @@ extern "C" void ft_internal_persist_dump(void) {
     if (!fp) return;
     for (int k = 0; k < 4096; ++k) fprintf(fp, "%d %llu %llu\n", k, h[2 * k], h[2 * k + 1]);
     fclose(fp);
+    const char *tl_path = getenv("FT_DEBUG_TIMELINE");
+    if (tl_path && g_plan_tl && g_plan_tl_n) {  // the last step's per-block timeline
+        static unsigned long long t[1 << 17];
+        cudaMemcpy(t, g_plan_tl, g_plan_tl_n * 8, cudaMemcpyDeviceToHost);
+        FILE *ft = fopen(tl_path, "a");
+        if (!ft) return;
+        fprintf(ft, "launch F=%d W=%d Gs=%d Gm=%d\n", g_plan_tl_hdr[0], g_plan_tl_hdr[1],
+                g_plan_tl_hdr[2], g_plan_tl_hdr[3]);
+        for (size_t b = 0; b < g_plan_tl_n / TL_SLOTS; ++b) {
+            fprintf(ft, "%zu", b);
+            for (int k = 0; k < TL_SLOTS; ++k) fprintf(ft, " %llu", t[b * TL_SLOTS + k]);
+            fprintf(ft, "\n");
+        }
+        fclose(ft);
+    }
 }
 
 // Launch the persistent kernel over n plans (internal: ft_runner.cu).  The

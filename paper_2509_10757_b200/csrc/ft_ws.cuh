@@ -52,13 +52,12 @@ constexpr int MED_WS = 128 + MED_FINE;
 
 struct WsLayout {
     size_t stereo_counters, fisheye_counters, fisheye_partials, proj_claims, track_bar_s,
-        track_bar_m, track_ep_m, track_ep_s, track_med, track_blk_counts, track_hist, pyr_bar,
-        total;
+        track_bar_m, track_ep_m, track_ep_s, track_tail_s, track_tail_m, track_mcand,
+        track_mcnt, track_med, track_blk_counts, track_hist, pyr_bar, total;
     size_t fisheye_partial_entries;
 };
 
 inline WsLayout ws_layout(int F, int cap_left, int cap_points) {
-    (void)cap_points;
     WsLayout L;
     size_t o = 0;
     L.stereo_counters = o;
@@ -78,6 +77,14 @@ inline WsLayout ws_layout(int F, int cap_left, int cap_points) {
     o += ws_align((size_t)F * 8);
     L.track_ep_s = o;
     o += ws_align((size_t)F * 8);
+    L.track_tail_s = o;
+    o += ws_align((size_t)F * 8);
+    L.track_tail_m = o;
+    o += ws_align((size_t)F * 8);
+    L.track_mcand = o;  // map resolve candidates (tail mode), 16 B per point
+    o += ws_align((size_t)F * cap_points * 16);
+    L.track_mcnt = o;
+    o += ws_align((size_t)F * WS_MAX_GROUP * 8);
     L.track_med = o;  // SAD-median histograms: 3 rotating buffers per stereo group
     o += ws_align((size_t)F * 3 * MED_WS * 4);
     L.track_blk_counts = o;

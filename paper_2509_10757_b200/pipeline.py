@@ -543,8 +543,8 @@ class AsyncRunner:
 
     def __init__(self, pipes, persistent: bool = False):
         import ctypes
-        if not 2 <= len(pipes) <= 4:
-            raise ValueError("AsyncRunner takes 2..4 identically shaped pipelines")
+        if not 2 <= len(pipes) <= 8:
+            raise ValueError("AsyncRunner takes 2..8 identically shaped pipelines")
         a = pipes[0]
         for b in pipes[1:]:
             if (a.S, a.cap_kp, a.cap_pts, a.in_end, a.out_begin, a.out_end) != \
