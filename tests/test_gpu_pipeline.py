@@ -461,3 +461,13 @@ def test_persistent_runner(workloads, expected, n_streams):
     # the kernel has ended: ordinary launches run again on the same pipelines
     pipes[0].replay(copies=False)
     pipes[0].synchronize()
+
+
+def test_tail_blocks_per_launch(workloads, expected, monkeypatch):
+    """The dedicated stereo-tail / map-resolve blocks (persistent plans' mode)
+    forced on ordinary launches: same results as the group-barrier path."""
+    monkeypatch.setenv("FT_TAIL_LAUNCH", "1")
+    _run(workloads, expected, 1, 3)
+    _run(workloads, expected, 3, 2)
+    from paper_2509_10757_b200.maptable import MapTable
+    _run(workloads, expected, 1, 2, table=MapTable(capacity=32 * 1024))
