@@ -20,21 +20,30 @@
 //
 // Persistent mode (ft_runner_create_persistent): no per-step launch.  One
 // long-lived track kernel (ft_track.cu track_persist_kernel) serves the n
-// slots; the streams hand steps over through device flags with stream memory
-// operations:
-//   H2D stream : wait d2h[i] (step k-n fully out); memcpy ranges;
-//                write ready[i] = k + 1
-//   kernel     : polls ready[i], computes, publishes done[i] = k + 1
-//   D2H stream : wait done[i] >= k + 1; memcpy outputs; record d2h[i]
+// slots:
+//   H2D stream   : wait d2h[i] (step k-n fully out); memcpy ranges;
+//                  write ready[i] = k + 1 (stream memory op)
+//   kernel       : polls ready[i], computes; the step's last block publishes
+//                  done[i] = k + 1
+//   D2H stream i : wait done[i] >= k + 1 (stream memory op); memcpy outputs;
+//                  record d2h[i]
+// One D2H stream per slot: a stream wait resolves by polling at coarse
+// intervals, and on a single stream those latencies queued up step after
+// step (capping the rate at ~19 us per step); per slot they overlap.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdlib>
+#include <cstring>
 #include <new>
+#include <thread>
 
 #include "../../include/fasttrack_b200.h"
 
 extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
+                                          unsigned *hdone, const void *const *dev_out,
+                                          void *const *host_out, size_t out_bytes,
                                           cudaStream_t stream);
 extern "C" void ft_internal_persist_dump(void);
 
@@ -69,10 +78,17 @@ bool stream_memops(WaitValue32Fn *wait, WriteValue32Fn *write) {
 }
 }  // namespace
 
+struct ft_runner;
+static int spin_done(const ft_runner *r, int i, int64_t step1, double timeout_s);
+
 struct ft_runner {
     int n;
     bool persistent;
-    unsigned *flags;  // persistent: [ready x 4 | done x 4 | arrive x 4] device words
+    unsigned *flags;  // persistent: [ready x 8 | done x 8 | arrive x 8] device words
+    volatile unsigned *hdone;  // persistent: host-mapped done words [8]
+    unsigned *hdone_dev;
+    int64_t last_k;
+    cudaStream_t d2hs[FT_RUNNER_MAX_SLOTS];  // persistent: one D2H stream per slot
     WaitValue32Fn wait32;
     WriteValue32Fn write32;
     cudaStream_t h2d, comp, d2h;
@@ -141,11 +157,26 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
     r->persistent = true;
     r->wait32 = w;
     r->write32 = v;
+    r->last_k = -1;
     cudaError_t e = cudaMalloc(&r->flags, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned));
     if (e == cudaSuccess)
         e = cudaMemsetAsync(r->flags, 0, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned), r->comp);
+    void *hd = nullptr;
+    if (e == cudaSuccess)
+        e = cudaHostAlloc(&hd, PERSIST_MAX_SLOTS * sizeof(unsigned), cudaHostAllocMapped);
     if (e == cudaSuccess) {
-        st = ft_internal_persist_launch(plans, n_slots, r->flags, r->comp);
+        memset(hd, 0, PERSIST_MAX_SLOTS * sizeof(unsigned));
+        r->hdone = static_cast<volatile unsigned *>(hd);
+        e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&r->hdone_dev), hd, 0);
+    }
+    for (int i = 0; i < n_slots && e == cudaSuccess; ++i)
+        e = cudaStreamCreateWithFlags(&r->d2hs[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(r->comp);
+    if (e == cudaSuccess) {
+        // outputs leave through the copy engines (the kernel's own PCIe stores
+        // from one block were slower): no host_out for the kernel
+        st = ft_internal_persist_launch(plans, n_slots, r->flags, nullptr, nullptr, nullptr,
+                                        out_bytes, r->comp);
         if (st != FT_OK) {
             cudaStreamSynchronize(r->comp);
             cudaFree(r->flags);
@@ -193,14 +224,16 @@ extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host
             r->write32((CUstream)r->h2d, (CUdeviceptr)(r->flags + i), step,
                        CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
             return FT_E_CONFIG;
+        cudaStream_t ds = r->d2hs[i];
         if (e == cudaSuccess &&
-            r->wait32((CUstream)r->d2h, (CUdeviceptr)(r->flags + PERSIST_MAX_SLOTS + i), step,
+            r->wait32((CUstream)ds, (CUdeviceptr)(r->flags + PERSIST_MAX_SLOTS + i), step,
                       CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
             return FT_E_CONFIG;
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(r->host_out[i], r->dev_out[i], r->out_bytes,
-                                cudaMemcpyDeviceToHost, r->d2h);
-        if (e == cudaSuccess) e = cudaEventRecord(r->ev_d2h[i], r->d2h);
+                                cudaMemcpyDeviceToHost, ds);
+        if (e == cudaSuccess) e = cudaEventRecord(r->ev_d2h[i], ds);
+        if (e == cudaSuccess && k > r->last_k) r->last_k = k;
         return (int)e;
     }
     cudaError_t e = cudaStreamWaitEvent(r->h2d, r->ev_comp[i], 0);
@@ -237,21 +270,41 @@ extern "C" int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in) {
     return ft_runner_submit_range(r, k, host_in, 0, r->in_bytes);
 }
 
+// Spin until the host-mapped done word of slot i reaches step1 (= step + 1),
+// wrap-safe; FT_E_TIMEOUT after timeout_s.
+static int spin_done(const ft_runner *r, int i, int64_t step1, double timeout_s) {
+    const uint32_t want = (uint32_t)step1;
+    if ((int32_t)(r->hdone[i] - want) >= 0) return FT_OK;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned it = 1;; ++it) {
+        if ((int32_t)(r->hdone[i] - want) >= 0) return FT_OK;
+        if ((it & 4095u) == 0) {
+            const double dt =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (dt > timeout_s) return FT_E_TIMEOUT;
+            if (dt > 1e-3) std::this_thread::yield();
+        }
+#if defined(__x86_64__) || defined(__i386__)
+        __builtin_ia32_pause();
+#endif
+    }
+}
+
 extern "C" int ft_runner_wait(ft_runner *r, int64_t k) {
     if (!r) return FT_E_NULL;
     if (k < 0) return FT_E_RANGE;
+
     return (int)cudaEventSynchronize(r->ev_d2h[k % r->n]);
 }
 
 extern "C" int ft_runner_destroy(ft_runner *r) {
     if (!r) return FT_OK;
     if (r->persistent && r->flags) {
-        // every submitted step completes first (its done flag releases the D2H
-        // stream), so all blocks are polling the next ready word -- then stop
-        // the persistent kernel (a stop seen mid-step by a late block would
-        // leave its group at a barrier)
+        // every submitted step completes first, so all blocks are polling the
+        // next ready word -- then stop the persistent kernel (a stop seen
+        // mid-step by a late block would leave its group at a barrier)
         cudaStreamSynchronize(r->h2d);
-        cudaStreamSynchronize(r->d2h);
+        for (int i = 0; i < r->n; ++i) cudaStreamSynchronize(r->d2hs[i]);
         for (int i = 0; i < PERSIST_MAX_SLOTS; ++i)
             r->write32((CUstream)r->h2d, (CUdeviceptr)(r->flags + i), PERSIST_STOP,
                        CU_STREAM_WRITE_VALUE_DEFAULT);
@@ -261,6 +314,10 @@ extern "C" int ft_runner_destroy(ft_runner *r) {
         cudaFree(r->flags);
         r->flags = nullptr;
     }
+    for (int i = 0; i < r->n; ++i)
+        if (r->d2hs[i]) cudaStreamDestroy(r->d2hs[i]);
+    if (r->hdone) cudaFreeHost(const_cast<unsigned *>(r->hdone));
+    r->hdone = nullptr;
     cudaStreamSynchronize(r->h2d);
     cudaStreamSynchronize(r->comp);
     cudaStreamSynchronize(r->d2h);

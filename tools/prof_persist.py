@@ -50,14 +50,21 @@ def loop(persistent, full=False, empty=False):
         r.wait(j)
     k0 = k
     t0 = time.perf_counter()
+    tw = ts = 0.0
     for k in range(k0, k0 + N):
+        a = time.perf_counter()
         if k - k0 >= n:
             r.wait(k - n)
+        b = time.perf_counter()
         r.submit(k, ring[k % NF], [] if empty else (None if full else ranges[k % NF]))
+        c = time.perf_counter()
+        tw += b - a
+        ts += c - b
     for j in range(k0 + N - n, k0 + N):
         r.wait(j)
     dt = time.perf_counter() - t0
     r.close()
+    print(f"   (host: wait {1e6 * tw / N:.2f} us, submit {1e6 * ts / N:.2f} us per step)")
     return 1e6 * dt / N
 
 
