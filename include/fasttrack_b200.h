@@ -67,8 +67,7 @@ enum {
     FT_E_NULL = -1,       /* required pointer is NULL */
     FT_E_RANGE = -2,      /* size / capacity / level count out of range */
     FT_E_WORKSPACE = -3,  /* workspace too small */
-    FT_E_CONFIG = -4,     /* invalid parameter value */
-    FT_E_TIMEOUT = -5     /* persistent runner: a step did not complete in time */
+    FT_E_CONFIG = -4      /* invalid parameter value */
 };
 
 typedef void *ft_stream_t; /* cudaStream_t */

@@ -33,17 +33,12 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-#include <chrono>
 #include <cstdlib>
-#include <cstring>
 #include <new>
-#include <thread>
 
 #include "../../include/fasttrack_b200.h"
 
 extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
-                                          unsigned *hdone, const void *const *dev_out,
-                                          void *const *host_out, size_t out_bytes,
                                           cudaStream_t stream);
 extern "C" void ft_internal_persist_dump(void);
 
@@ -78,15 +73,10 @@ bool stream_memops(WaitValue32Fn *wait, WriteValue32Fn *write) {
 }
 }  // namespace
 
-struct ft_runner;
-static int spin_done(const ft_runner *r, int i, int64_t step1, double timeout_s);
-
 struct ft_runner {
     int n;
     bool persistent;
     unsigned *flags;  // persistent: [ready x 8 | done x 8 | arrive x 8] device words
-    volatile unsigned *hdone;  // persistent: host-mapped done words [8]
-    unsigned *hdone_dev;
     int64_t last_k;
     cudaStream_t d2hs[FT_RUNNER_MAX_SLOTS];  // persistent: one D2H stream per slot
     WaitValue32Fn wait32;
@@ -161,22 +151,11 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
     cudaError_t e = cudaMalloc(&r->flags, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned));
     if (e == cudaSuccess)
         e = cudaMemsetAsync(r->flags, 0, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned), r->comp);
-    void *hd = nullptr;
-    if (e == cudaSuccess)
-        e = cudaHostAlloc(&hd, PERSIST_MAX_SLOTS * sizeof(unsigned), cudaHostAllocMapped);
-    if (e == cudaSuccess) {
-        memset(hd, 0, PERSIST_MAX_SLOTS * sizeof(unsigned));
-        r->hdone = static_cast<volatile unsigned *>(hd);
-        e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&r->hdone_dev), hd, 0);
-    }
     for (int i = 0; i < n_slots && e == cudaSuccess; ++i)
         e = cudaStreamCreateWithFlags(&r->d2hs[i], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamSynchronize(r->comp);
     if (e == cudaSuccess) {
-        // outputs leave through the copy engines (the kernel's own PCIe stores
-        // from one block were slower): no host_out for the kernel
-        st = ft_internal_persist_launch(plans, n_slots, r->flags, nullptr, nullptr, nullptr,
-                                        out_bytes, r->comp);
+        st = ft_internal_persist_launch(plans, n_slots, r->flags, r->comp);
         if (st != FT_OK) {
             cudaStreamSynchronize(r->comp);
             cudaFree(r->flags);
@@ -270,26 +249,6 @@ extern "C" int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in) {
     return ft_runner_submit_range(r, k, host_in, 0, r->in_bytes);
 }
 
-// Spin until the host-mapped done word of slot i reaches step1 (= step + 1),
-// wrap-safe; FT_E_TIMEOUT after timeout_s.
-static int spin_done(const ft_runner *r, int i, int64_t step1, double timeout_s) {
-    const uint32_t want = (uint32_t)step1;
-    if ((int32_t)(r->hdone[i] - want) >= 0) return FT_OK;
-    const auto t0 = std::chrono::steady_clock::now();
-    for (unsigned it = 1;; ++it) {
-        if ((int32_t)(r->hdone[i] - want) >= 0) return FT_OK;
-        if ((it & 4095u) == 0) {
-            const double dt =
-                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            if (dt > timeout_s) return FT_E_TIMEOUT;
-            if (dt > 1e-3) std::this_thread::yield();
-        }
-#if defined(__x86_64__) || defined(__i386__)
-        __builtin_ia32_pause();
-#endif
-    }
-}
-
 extern "C" int ft_runner_wait(ft_runner *r, int64_t k) {
     if (!r) return FT_E_NULL;
     if (k < 0) return FT_E_RANGE;
@@ -316,8 +275,6 @@ extern "C" int ft_runner_destroy(ft_runner *r) {
     }
     for (int i = 0; i < r->n; ++i)
         if (r->d2hs[i]) cudaStreamDestroy(r->d2hs[i]);
-    if (r->hdone) cudaFreeHost(const_cast<unsigned *>(r->hdone));
-    r->hdone = nullptr;
     cudaStreamSynchronize(r->h2d);
     cudaStreamSynchronize(r->comp);
     cudaStreamSynchronize(r->d2h);

@@ -1689,10 +1689,7 @@ __global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
 // every block waits until ready[slot] >= k + 1 (written by the runner's H2D
 // stream after the slot's inputs landed), runs its role on that slot's
 // arguments, then arrives on arrive[slot]; the last arrival of the step
-// copies the slot's outputs straight into the caller's pinned host range
-// (mapped memory, 16-B stores) and publishes done[slot] = k + 1 both in
-// device memory and in a host-mapped word the runner's wait() spins on -- no
-// D2H stream, no stream-side wait in the step's path.
+// publishes done[slot] = k + 1, which releases the slot's D2H stream.
 // Blocks run ahead independently -- a block that finished step k starts
 // step k + 1 while others finish k (each slot has its own workspace, so the
 // groups' barrier words and tickets never mix).  ready[] == FT_PERSIST_STOP
@@ -1706,10 +1703,6 @@ struct PersistArgs {
     unsigned *ready;   // [n] step + 1 whose inputs are in the slot (H2D stream)
     unsigned *done;    // [n] step + 1 whose outputs are complete (this kernel)
     unsigned *arrive;  // [n] block arrivals (monotonic)
-    unsigned *hdone;   // [n] host-mapped copy of done (the runner's wait spins on it)
-    const unsigned char *dev_out[PERSIST_MAX_SLOTS];  // slot outputs (device)
-    unsigned char *host_out[PERSIST_MAX_SLOTS];       // ... and their pinned host copy
-    unsigned long long out_bytes;
     unsigned long long *ts;  // debug (FT_DEBUG_PERSIST): [4096][2] step start / done (ns)
 };
 
@@ -1760,26 +1753,9 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
         }
         __syncthreads();
         if (s_last) {
-            if (p.host_out[i]) {  // outputs -> pinned host memory (PCIe writes)
-                const uint4 *src = reinterpret_cast<const uint4 *>(p.dev_out[i]);
-                uint4 *dst = reinterpret_cast<uint4 *>(p.host_out[i]);
-                const bool vec = ((((uintptr_t)src) | ((uintptr_t)dst)) & 15) == 0;
-                const unsigned long long nv = vec ? p.out_bytes >> 4 : 0;
-                for (unsigned long long q = threadIdx.x; q < nv; q += TK_THREADS)
-                    dst[q] = __ldcg(src + q);
-                for (unsigned long long t = (nv << 4) + threadIdx.x; t < p.out_bytes;
-                     t += TK_THREADS)
-                    p.host_out[i][t] = __ldcg(p.dev_out[i] + t);
-                __syncthreads();
-            }
             if (threadIdx.x == 0) {
-                if (p.host_out[i]) asm volatile("fence.sc.sys;" ::: "memory");
                 asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done + i), "r"(k + 1u)
                              : "memory");
-                if (p.hdone)
-                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.hdone + i),
-                                 "r"(k + 1u)
-                                 : "memory");
                 if (p.ts) p.ts[2 * (k & 4095u) + 1] = global_ns();
             }
         }
@@ -2344,8 +2320,6 @@ extern "C" void ft_internal_persist_dump(void) {
 // plans must share one geometry and leave SMs free for other work (the
 // launch never ends on its own: it would starve every later kernel).
 extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
-                                          unsigned *hdone, const void *const *dev_out,
-                                          void *const *host_out, size_t out_bytes,
                                           cudaStream_t stream) {
     if (!plans || !flags) return FT_E_NULL;
     if (n < 1 || n > PERSIST_MAX_SLOTS) return FT_E_RANGE;
@@ -2372,12 +2346,6 @@ extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsig
     p.ready = flags;
     p.done = flags + PERSIST_MAX_SLOTS;
     p.arrive = flags + 2 * PERSIST_MAX_SLOTS;
-    p.hdone = hdone;
-    p.out_bytes = out_bytes;
-    for (int i = 0; i < n; ++i) {
-        p.dev_out[i] = dev_out ? static_cast<const unsigned char *>(dev_out[i]) : nullptr;
-        p.host_out[i] = host_out ? static_cast<unsigned char *>(host_out[i]) : nullptr;
-    }
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
