@@ -67,7 +67,8 @@ enum {
     FT_E_NULL = -1,       /* required pointer is NULL */
     FT_E_RANGE = -2,      /* size / capacity / level count out of range */
     FT_E_WORKSPACE = -3,  /* workspace too small */
-    FT_E_CONFIG = -4      /* invalid parameter value */
+    FT_E_CONFIG = -4,     /* invalid parameter value */
+    FT_E_TIMEOUT = -5     /* persistent runner: a step did not complete within 20 s */
 };
 
 typedef void *ft_stream_t; /* cudaStream_t */
@@ -297,12 +298,14 @@ int ft_runner_destroy(ft_runner *r);
 /* Persistent runner: instead of a graph launch per step, ONE long-lived
  * ft_track_frames kernel serves the n slots (2..8).  plans[i] holds slot i's
  * launch (ft_track_plan over that slot's device buffers; all slots the same
- * shapes).  The H2D stream hands a step to the kernel with a device flag
- * (stream write), the kernel hands it to the D2H stream with another (stream
- * wait), so no launch, block scheduling or drain sits between frames.
- * Submit / wait as above; ft_runner_destroy finishes every submitted step,
- * then ends the kernel.  The plan's grid must leave SMs free (FT_E_RANGE
- * otherwise); other kernels may run beside it on those SMs. */
+ * shapes).  The runner's host thread hands a step to the kernel through a
+ * pinned, mapped flag once the step's inputs have landed, and issues the
+ * step's D2H when the kernel's done flag (also mapped) shows up -- no launch,
+ * block scheduling or drain sits between frames.  Submit / wait as above
+ * (both drive that hand-off; wait returns FT_E_TIMEOUT after 20 s);
+ * ft_runner_destroy finishes every submitted step, then ends the kernel.
+ * The plan's grid must leave SMs free (FT_E_RANGE otherwise); other kernels
+ * may run beside it on those SMs. */
 int ft_runner_create_persistent(int32_t n_slots, const void *const *plans, void *const *dev_in,
                                 size_t in_bytes, void *const *dev_out, void *const *host_out,
                                 size_t out_bytes, ft_runner **out);

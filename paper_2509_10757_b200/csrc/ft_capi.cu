@@ -19,6 +19,7 @@ const char *ft_status_string(int status) {
         case FT_E_RANGE: return "size, capacity or level count out of range";
         case FT_E_WORKSPACE: return "workspace too small for this launch";
         case FT_E_CONFIG: return "invalid parameter value";
+        case FT_E_TIMEOUT: return "step did not complete in time";
         default: break;
     }
     if (status > 0) return cudaGetErrorString((cudaError_t)status);

@@ -20,67 +20,43 @@
 //
 // Persistent mode (ft_runner_create_persistent): no per-step launch.  One
 // long-lived track kernel (ft_track.cu track_persist_kernel) serves the n
-// slots:
-//   H2D stream   : wait d2h[i] (step k-n fully out); memcpy ranges;
-//                  write ready[i] = k + 1 (stream memory op)
-//   kernel       : polls ready[i], computes; the step's last block publishes
-//                  done[i] = k + 1
-//   D2H stream i : wait done[i] >= k + 1 (stream memory op); memcpy outputs;
-//                  record d2h[i]
-// One D2H stream per slot: a stream wait resolves by polling at coarse
-// intervals, and on a single stream those latencies queued up step after
-// step (capping the rate at ~19 us per step); per slot they overlap.
-#include <cuda.h>
+// slots, and the runner's host thread schedules the copies around it:
+//   submit(k)  : H2D of slot i's ranges + event h2d[i]
+//   pump       : h2d[i] complete -> ready[i] = k + 1 (pinned, mapped word the
+//                kernel watches); done[i] >= k + 1 (mapped word the kernel
+//                publishes) -> D2H of the outputs on slot i's stream + d2h[i]
+//   wait(k)    : pump until d2h[i] of step k has completed
+// No stream memory operations: each costs several microseconds of stream
+// time, and one per step on the H2D stream capped the step rate.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <chrono>
 #include <cstdlib>
 #include <new>
 
 #include "../../include/fasttrack_b200.h"
 
 extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
+                                          const unsigned *h_ready, unsigned *h_done,
                                           cudaStream_t stream);
 extern "C" void ft_internal_persist_dump(void);
 
 namespace {
 constexpr int PERSIST_MAX_SLOTS = 8;  // == ft_track.cu
 constexpr unsigned PERSIST_STOP = 0xffffffffu;
-typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-
-// cuStreamWaitValue32 / cuStreamWriteValue32 through the runtime's driver
-// entry-point query (no link-time libcuda dependency)
-bool stream_memops(WaitValue32Fn *wait, WriteValue32Fn *write) {
-    static WaitValue32Fn w = nullptr;
-    static WriteValue32Fn v = nullptr;
-    if (!w || !v) {
-        void *a = nullptr, *b = nullptr;
-        cudaDriverEntryPointQueryResult qa, qb;
-        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &a, cudaEnableDefault, &qa) !=
-                cudaSuccess ||
-            qa != cudaDriverEntryPointSuccess)
-            return false;
-        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &b, cudaEnableDefault, &qb) !=
-                cudaSuccess ||
-            qb != cudaDriverEntryPointSuccess)
-            return false;
-        w = (WaitValue32Fn)a;
-        v = (WriteValue32Fn)b;
-    }
-    *wait = w;
-    *write = v;
-    return true;
-}
 }  // namespace
 
 struct ft_runner {
     int n;
     bool persistent;
-    unsigned *flags;  // persistent: [ready x 8 | done x 8 | arrive x 8] device words
+    unsigned *flags;  // persistent: [device ready x 8 | - x 8 | arrive x 8] device words
+    volatile unsigned *hflags;  // persistent: pinned mapped [ready x 8 | done x 8]
+    unsigned *hflags_dev;
     int64_t last_k;
+    int64_t next_ready;  // oldest step whose ready word is not yet published
+    int64_t next_d2h;    // oldest step whose D2H is not yet issued
     cudaStream_t d2hs[FT_RUNNER_MAX_SLOTS];  // persistent: one D2H stream per slot
-    WaitValue32Fn wait32;
-    WriteValue32Fn write32;
     cudaStream_t h2d, comp, d2h;
     cudaEvent_t ev_h2d[FT_RUNNER_MAX_SLOTS], ev_comp[FT_RUNNER_MAX_SLOTS],
         ev_d2h[FT_RUNNER_MAX_SLOTS];
@@ -135,36 +111,37 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
     if (!plans || !dev_in || !dev_out || !host_out || !out) return FT_E_NULL;
     if (n_slots < 2 || n_slots > FT_RUNNER_MAX_SLOTS || n_slots > PERSIST_MAX_SLOTS)
         return FT_E_RANGE;
-    WaitValue32Fn w;
-    WriteValue32Fn v;
-    if (!stream_memops(&w, &v)) return FT_E_CONFIG;
     // graph_exec slots are unused in persistent mode: reuse the plan pointers
     // as non-null placeholders for the shared constructor
     int st = ft_runner_create_n(n_slots, plans, dev_in, in_bytes, dev_out, host_out, out_bytes,
                                 out);
     if (st != FT_OK) return st;
     ft_runner *r = *out;
-    r->persistent = true;
-    r->wait32 = w;
-    r->write32 = v;
     r->last_k = -1;
+    r->next_ready = r->next_d2h = 0;
     cudaError_t e = cudaMalloc(&r->flags, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned));
     if (e == cudaSuccess)
         e = cudaMemsetAsync(r->flags, 0, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned), r->comp);
+    void *hf = nullptr;
+    if (e == cudaSuccess)
+        e = cudaHostAlloc(&hf, 2 * PERSIST_MAX_SLOTS * sizeof(unsigned), cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+        r->hflags = static_cast<volatile unsigned *>(hf);
+        for (int i = 0; i < 2 * PERSIST_MAX_SLOTS; ++i) r->hflags[i] = 0;
+        e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&r->hflags_dev), hf, 0);
+    }
     for (int i = 0; i < n_slots && e == cudaSuccess; ++i)
         e = cudaStreamCreateWithFlags(&r->d2hs[i], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamSynchronize(r->comp);
     if (e == cudaSuccess) {
-        st = ft_internal_persist_launch(plans, n_slots, r->flags, r->comp);
-        if (st != FT_OK) {
-            cudaStreamSynchronize(r->comp);
-            cudaFree(r->flags);
-            r->flags = nullptr;
-            r->persistent = false;
+        st = ft_internal_persist_launch(plans, n_slots, r->flags, r->hflags_dev,
+                                        r->hflags_dev + PERSIST_MAX_SLOTS, r->comp);
+        if (st != FT_OK) {  // no kernel to stop
             ft_runner_destroy(r);
             *out = nullptr;
             return st;
         }
+        r->persistent = true;
     }
     if (e != cudaSuccess) {
         ft_runner_destroy(r);
@@ -172,6 +149,53 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
         return (int)e;
     }
     return FT_OK;
+}
+
+// Persistent mode: publish the ready words of landed inputs and issue the D2H
+// copies of finished steps, oldest first (the H2D stream completes steps in
+// order, the kernel too), so each call checks one event and one flag.
+static int persist_pump(ft_runner *r) {
+    while (r->next_ready <= r->last_k) {
+        const int i = (int)(r->next_ready % r->n);
+        const cudaError_t q = cudaEventQuery(r->ev_h2d[i]);
+        if (q == cudaErrorNotReady) break;
+        if (q != cudaSuccess) return (int)q;
+        r->hflags[i] = (unsigned)(r->next_ready + 1);
+        ++r->next_ready;
+    }
+    while (r->next_d2h < r->next_ready) {
+        const int i = (int)(r->next_d2h % r->n);
+        const uint32_t want = (uint32_t)(r->next_d2h + 1);
+        if ((int32_t)(r->hflags[PERSIST_MAX_SLOTS + i] - want) < 0) break;
+        cudaError_t e = cudaMemcpyAsync(r->host_out[i], r->dev_out[i], r->out_bytes,
+                                        cudaMemcpyDeviceToHost, r->d2hs[i]);
+        if (e == cudaSuccess) e = cudaEventRecord(r->ev_d2h[i], r->d2hs[i]);
+        if (e != cudaSuccess) return (int)e;
+        ++r->next_d2h;
+    }
+    return FT_OK;
+}
+
+// Persistent mode: pump until step k's outputs are on the host.
+static int persist_wait(ft_runner *r, int64_t k) {
+    const int i = (int)(k % r->n);
+    if (k > r->last_k) return FT_E_RANGE;  // never submitted
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned it = 1;; ++it) {
+        const int st = persist_pump(r);
+        if (st != FT_OK) return st;
+        if (r->next_d2h > k) {
+            const cudaError_t q = cudaEventQuery(r->ev_d2h[i]);
+            if (q == cudaSuccess) return FT_OK;
+            if (q != cudaErrorNotReady) return (int)q;
+        }
+        if ((it & 1023u) == 0 &&
+            std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+            return FT_E_TIMEOUT;
+#if defined(__x86_64__) || defined(__i386__)
+        __builtin_ia32_pause();
+#endif
+    }
 }
 
 extern "C" int ft_runner_create(const void *const graph_exec[2], void *const dev_in[2],
@@ -188,9 +212,13 @@ extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host
         if (ranges[2 * q] > ranges[2 * q + 1] || ranges[2 * q + 1] > r->in_bytes) return FT_E_RANGE;
     const int i = (int)(k % r->n);
     if (r->persistent) {
-        // slot i's step k-n is out (its outputs copied, so its inputs are
-        // consumed too); then inputs -> ready -> (kernel) -> done -> outputs
-        cudaError_t e = cudaStreamWaitEvent(r->h2d, r->ev_d2h[i], 0);
+        if (k != r->last_k + 1) return FT_E_RANGE;  // steps are submitted in order
+        // slot i's step k-n must be fully out (outputs on the host, inputs consumed)
+        if (k >= r->n) {
+            const int st = persist_wait(r, k - r->n);
+            if (st != FT_OK) return st;
+        }
+        cudaError_t e = cudaSuccess;
         for (int q = 0; q < n_ranges && e == cudaSuccess; ++q) {
             const size_t lo = ranges[2 * q], n = ranges[2 * q + 1] - lo;
             if (n)
@@ -198,22 +226,10 @@ extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host
                                     static_cast<const char *>(host_in) + lo, n,
                                     cudaMemcpyHostToDevice, r->h2d);
         }
-        const cuuint32_t step = (cuuint32_t)(k + 1);
-        if (e == cudaSuccess &&
-            r->write32((CUstream)r->h2d, (CUdeviceptr)(r->flags + i), step,
-                       CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
-            return FT_E_CONFIG;
-        cudaStream_t ds = r->d2hs[i];
-        if (e == cudaSuccess &&
-            r->wait32((CUstream)ds, (CUdeviceptr)(r->flags + PERSIST_MAX_SLOTS + i), step,
-                      CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-            return FT_E_CONFIG;
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(r->host_out[i], r->dev_out[i], r->out_bytes,
-                                cudaMemcpyDeviceToHost, ds);
-        if (e == cudaSuccess) e = cudaEventRecord(r->ev_d2h[i], ds);
-        if (e == cudaSuccess && k > r->last_k) r->last_k = k;
-        return (int)e;
+        if (e == cudaSuccess) e = cudaEventRecord(r->ev_h2d[i], r->h2d);
+        if (e != cudaSuccess) return (int)e;
+        r->last_k = k;
+        return persist_pump(r);
     }
     cudaError_t e = cudaStreamWaitEvent(r->h2d, r->ev_comp[i], 0);
     for (int q = 0; q < n_ranges && e == cudaSuccess; ++q) {
@@ -252,27 +268,26 @@ extern "C" int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in) {
 extern "C" int ft_runner_wait(ft_runner *r, int64_t k) {
     if (!r) return FT_E_NULL;
     if (k < 0) return FT_E_RANGE;
-
+    if (r->persistent) return persist_wait(r, k);
     return (int)cudaEventSynchronize(r->ev_d2h[k % r->n]);
 }
 
 extern "C" int ft_runner_destroy(ft_runner *r) {
     if (!r) return FT_OK;
-    if (r->persistent && r->flags) {
+    if (r->persistent) {
         // every submitted step completes first, so all blocks are polling the
         // next ready word -- then stop the persistent kernel (a stop seen
         // mid-step by a late block would leave its group at a barrier)
-        cudaStreamSynchronize(r->h2d);
-        for (int i = 0; i < r->n; ++i) cudaStreamSynchronize(r->d2hs[i]);
-        for (int i = 0; i < PERSIST_MAX_SLOTS; ++i)
-            r->write32((CUstream)r->h2d, (CUdeviceptr)(r->flags + i), PERSIST_STOP,
-                       CU_STREAM_WRITE_VALUE_DEFAULT);
-        cudaStreamSynchronize(r->h2d);
+        for (int64_t k = r->last_k - r->n + 1; k <= r->last_k; ++k)
+            if (k >= 0) persist_wait(r, k);
+        for (int i = 0; i < PERSIST_MAX_SLOTS; ++i) r->hflags[i] = PERSIST_STOP;
         cudaStreamSynchronize(r->comp);
         ft_internal_persist_dump();
-        cudaFree(r->flags);
-        r->flags = nullptr;
     }
+    if (r->flags) cudaFree(r->flags);
+    r->flags = nullptr;
+    if (r->hflags) cudaFreeHost(const_cast<unsigned *>(r->hflags));
+    r->hflags = nullptr;
     for (int i = 0; i < r->n; ++i)
         if (r->d2hs[i]) cudaStreamDestroy(r->d2hs[i]);
     cudaStreamSynchronize(r->h2d);

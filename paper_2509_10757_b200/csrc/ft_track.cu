@@ -1686,10 +1686,12 @@ __global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
 // Persistent mode (ft_runner_create_persistent): ONE long-lived cooperative
 // launch steps through a ring of n input/output slots, removing the per-frame
 // launch (graph launch, block scheduling, drain).  Step k uses slot k % n:
-// every block waits until ready[slot] >= k + 1 (written by the runner's H2D
-// stream after the slot's inputs landed), runs its role on that slot's
-// arguments, then arrives on arrive[slot]; the last arrival of the step
-// publishes done[slot] = k + 1, which releases the slot's D2H stream.
+// the runner's host thread sets ready[slot] = k + 1 (pinned, mapped host
+// memory) once the slot's inputs have landed; block 0 watches that word and
+// forwards it to a device word every other block polls (one PCIe poller,
+// not 120); each block runs its role on the slot's arguments and arrives on
+// arrive[slot]; the step's last arrival publishes done[slot] = k + 1 into
+// mapped host memory, where the runner picks it up and issues the D2H copy.
 // Blocks run ahead independently -- a block that finished step k starts
 // step k + 1 while others finish k (each slot has its own workspace, so the
 // groups' barrier words and tickets never mix).  ready[] == FT_PERSIST_STOP
@@ -1700,15 +1702,22 @@ constexpr unsigned FT_PERSIST_STOP = 0xffffffffu;
 struct PersistArgs {
     TrackArgs a[PERSIST_MAX_SLOTS];  // identical geometry (W, Gs, Gm) in every slot
     int n;
-    unsigned *ready;   // [n] step + 1 whose inputs are in the slot (H2D stream)
-    unsigned *done;    // [n] step + 1 whose outputs are complete (this kernel)
-    unsigned *arrive;  // [n] block arrivals (monotonic)
+    const unsigned *ready;  // [n] host-mapped: step + 1 whose inputs are in the slot
+    unsigned *dready;       // [n] device copy of ready (forwarded by block 0)
+    unsigned *done;         // [n] host-mapped: step + 1 whose outputs are complete
+    unsigned *arrive;       // [n] block arrivals (monotonic)
     unsigned long long *ts;  // debug (FT_DEBUG_PERSIST): [4096][2] step start / done (ns)
 };
 
 FT_DEV unsigned ld_acquire_u32(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+FT_DEV unsigned ld_acquire_sys_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -1731,8 +1740,15 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
         const int i = (int)(k % (unsigned)p.n);
         if (threadIdx.x == 0) {
             unsigned v;
-            while ((v = ld_acquire_u32(p.ready + i)) != FT_PERSIST_STOP && v < k + 1)
-                __nanosleep(64);
+            if (blockIdx.x == 0) {  // the PCIe watcher
+                while ((v = ld_acquire_sys_u32(p.ready + i)) != FT_PERSIST_STOP && v < k + 1)
+                    __nanosleep(100);
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.dready + i), "r"(v)
+                             : "memory");
+            } else {
+                while ((v = ld_acquire_u32(p.dready + i)) != FT_PERSIST_STOP && v < k + 1)
+                    __nanosleep(64);
+            }
             s_go = v != FT_PERSIST_STOP;
             if (p.ts && blockIdx.x == 0 && s_go) p.ts[2 * (k & 4095u)] = global_ns();
         }
@@ -2320,9 +2336,11 @@ extern "C" void ft_internal_persist_dump(void) {
 // plans must share one geometry and leave SMs free for other work (the
 // launch never ends on its own: it would starve every later kernel).
 extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
+                                          const unsigned *h_ready, unsigned *h_done,
                                           cudaStream_t stream) {
     if (!plans || !flags) return FT_E_NULL;
     if (n < 1 || n > PERSIST_MAX_SLOTS) return FT_E_RANGE;
+    // (the flag words: see track_persist_kernel)
     PersistArgs p;
     memset(&p, 0, sizeof(p));
     size_t smem = 0;
@@ -2343,8 +2361,10 @@ extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsig
         p.ts = ts_buf;
         g_persist_ts = ts_buf;
     }
-    p.ready = flags;
-    p.done = flags + PERSIST_MAX_SLOTS;
+    if (!h_ready || !h_done) return FT_E_NULL;
+    p.ready = h_ready;
+    p.done = h_done;
+    p.dready = flags;
     p.arrive = flags + 2 * PERSIST_MAX_SLOTS;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);

@@ -519,6 +519,17 @@ def _graph_exec_ptr(graph) -> int:
     return get(h, None)
 
 
+class _Ranges:
+    """Byte ranges of a step's inputs as the C ABI's flat uint64 pairs."""
+
+    def __init__(self, rng):
+        import ctypes
+        pairs = [rng] if len(rng) == 2 and not isinstance(rng[0], (tuple, list)) else list(rng)
+        self.n = len(pairs)
+        self.flat = (ctypes.c_uint64 * max(1, 2 * self.n))(*[int(x) for r in pairs for x in r])
+        self.bytes = sum(int(hi) - int(lo) for lo, hi in pairs)
+
+
 class AsyncRunner:
     """Copy / compute overlapped driver for a stream of steps (the real-time
     shape of the tracker: the next frame's images and keypoints upload while
@@ -577,17 +588,30 @@ class AsyncRunner:
         _lib.check(create(self.n, execs, dev_in, a.in_end, dev_out, host_out,
                           a.out_end - a.out_begin, ctypes.byref(self._r)), "ft_runner_create")
         self._keep = (execs, dev_in, dev_out, host_out, plans)
+        self._submit_ranges = self.lib.ft_runner_submit_ranges
+        self._wait = self.lib.ft_runner_wait
 
     def submit(self, k: int, inputs: torch.Tensor | None = None,
                rng: tuple[int, int] | None = None) -> None:
         """Enqueue step k; inputs = a pinned tensor in the pipelines' input
-        layout (staged_inputs() / a staging_ring() row), or None to send
-        pipes[k % 2]'s own staging; rng = the [lo, hi) byte range to ship
-        (input_range() of the staged frame), default all."""
-        p = self.pipes[k % self.n]
-        src = p.host.data_ptr() if inputs is None else inputs.data_ptr()
+        layout (staged_inputs() / a staging_ring() row) or its data pointer,
+        or None to send pipes[k % n]'s own staging; rng = the [lo, hi) byte
+        range(s) to ship (input_range() / input_ranges() of the staged frame,
+        or ranges_arg() of them), default all."""
+        if type(inputs) is int:
+            src = inputs
+        else:
+            src = (self.pipes[k % self.n].host.data_ptr() if inputs is None
+                   else inputs.data_ptr())
+        if type(rng) is _Ranges:  # hot path: nothing to marshal
+            st = self._submit_ranges(self._r, k, src, rng.flat, rng.n)
+            if st:
+                _lib.check(st, "ft_runner_submit")
+            return
         if rng is None:
             st = self.lib.ft_runner_submit(self._r, k, src)
+        elif isinstance(rng, _Ranges):  # pre-converted (ranges_arg)
+            st = self.lib.ft_runner_submit_ranges(self._r, k, src, rng.flat, rng.n)
         elif len(rng) == 0 or isinstance(rng[0], (tuple, list)):  # several (input_ranges())
             import ctypes
             flat = (ctypes.c_uint64 * (2 * len(rng)))(*[int(x) for r in rng for x in r])
@@ -597,10 +621,18 @@ class AsyncRunner:
             st = self.lib.ft_runner_submit_range(self._r, k, src, lo, hi - lo)
         _lib.check(st, "ft_runner_submit")
 
+    @staticmethod
+    def ranges_arg(rng) -> "_Ranges":
+        """rng (input_range() / input_ranges()) converted once for submit():
+        saves the per-step argument marshalling on the host's critical path."""
+        return _Ranges(rng)
+
     def wait(self, k: int) -> FramePipeline:
         """Block until step k's results are on the host; returns its pipeline
         (read them with .result(s, n_left))."""
-        _lib.check(self.lib.ft_runner_wait(self._r, k), "ft_runner_wait")
+        st = self._wait(self._r, k)
+        if st:
+            _lib.check(st, "ft_runner_wait")
         return self.pipes[k % self.n]
 
     def synchronize(self) -> None:

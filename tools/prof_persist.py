@@ -28,7 +28,7 @@ ranges = []
 for k, w in enumerate(ws):
     pipes[0].load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
     pipes[0].stage_into(ring[k])
-    ranges.append(pipes[0].input_ranges())
+    ranges.append(AsyncRunner.ranges_arg(pipes[0].input_ranges()))
 for i, p in enumerate(pipes):
     if not os.environ.get("PERSIST_TL_ONLY"):  # (the timeline hook syncs: no capture)
         p.capture()
