@@ -20,20 +20,25 @@
 //
 // Persistent mode (ft_runner_create_persistent): no per-step launch.  One
 // long-lived track kernel (ft_track.cu track_persist_kernel) serves the n
-// slots, and the runner's host thread schedules the copies around it:
-//   submit(k)  : H2D of slot i's ranges + event h2d[i]
+// slots, and a native pump thread schedules the copies around it:
+//   submit(k)  : (caller) H2D of slot i's ranges + event h2d[i]
 //   pump       : h2d[i] complete -> ready[i] = k + 1 (pinned, mapped word the
 //                kernel watches); done[i] >= k + 1 (mapped word the kernel
-//                publishes) -> D2H of the outputs on slot i's stream + d2h[i]
-//   wait(k)    : pump until d2h[i] of step k has completed
+//                publishes) -> D2H of the outputs on slot i's stream + d2h[i];
+//                d2h[i] complete -> step k is out (atomic counter)
+//   wait(k)    : (caller) spins on that counter -- no CUDA call
+// The pump's API calls run beside the caller's, so a step costs the caller
+// one copy + one event record.
 // No stream memory operations: each costs several microseconds of stream
 // time, and one per step on the H2D stream capped the step rate.
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <new>
+#include <thread>
 
 #include "../../include/fasttrack_b200.h"
 
@@ -53,9 +58,15 @@ struct ft_runner {
     unsigned *flags;  // persistent: [device ready x 8 | - x 8 | arrive x 8] device words
     volatile unsigned *hflags;  // persistent: pinned mapped [ready x 8 | done x 8]
     unsigned *hflags_dev;
-    int64_t last_k;
-    int64_t next_ready;  // oldest step whose ready word is not yet published
-    int64_t next_d2h;    // oldest step whose D2H is not yet issued
+    std::atomic<int64_t> last_k;    // last submitted step (caller -> pump)
+    std::atomic<int64_t> out_k;     // last step whose outputs are on the host (pump -> caller)
+    std::atomic<int> pump_err;      // first error the pump met (FT_OK while healthy)
+    std::atomic<bool> pump_stop;
+    std::thread *pump;
+    int device;
+    int64_t next_ready;  // pump: oldest step whose ready word is not yet published
+    int64_t next_d2h;    // pump: oldest step whose D2H is not yet issued
+    int64_t next_out;    // pump: oldest step whose D2H has not yet completed
     cudaStream_t d2hs[FT_RUNNER_MAX_SLOTS];  // persistent: one D2H stream per slot
     cudaStream_t h2d, comp, d2h;
     cudaEvent_t ev_h2d[FT_RUNNER_MAX_SLOTS], ev_comp[FT_RUNNER_MAX_SLOTS],
@@ -104,6 +115,8 @@ extern "C" int ft_runner_create_n(int32_t n_slots, const void *const *graph_exec
     return FT_OK;
 }
 
+static void persist_pump_loop(ft_runner *r);
+
 extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *plans,
                                            void *const *dev_in, size_t in_bytes,
                                            void *const *dev_out, void *const *host_out,
@@ -117,8 +130,12 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
                                 out);
     if (st != FT_OK) return st;
     ft_runner *r = *out;
-    r->last_k = -1;
-    r->next_ready = r->next_d2h = 0;
+    r->last_k.store(-1);
+    r->out_k.store(-1);
+    r->pump_err.store(FT_OK);
+    r->pump_stop.store(false);
+    r->next_ready = r->next_d2h = r->next_out = 0;
+    cudaGetDevice(&r->device);
     cudaError_t e = cudaMalloc(&r->flags, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned));
     if (e == cudaSuccess)
         e = cudaMemsetAsync(r->flags, 0, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned), r->comp);
@@ -142,6 +159,12 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
             return st;
         }
         r->persistent = true;
+        r->pump = new (std::nothrow) std::thread(persist_pump_loop, r);
+        if (!r->pump) {
+            ft_runner_destroy(r);
+            *out = nullptr;
+            return FT_E_RANGE;
+        }
     }
     if (e != cudaSuccess) {
         ft_runner_destroy(r);
@@ -151,45 +174,76 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
     return FT_OK;
 }
 
-// Persistent mode: publish the ready words of landed inputs and issue the D2H
-// copies of finished steps, oldest first (the H2D stream completes steps in
-// order, the kernel too), so each call checks one event and one flag.
+// Persistent mode: one pass of the pump -- publish the ready words of landed
+// inputs, issue the D2H copies of finished steps, retire completed copies,
+// oldest first (the H2D stream, the kernel and each slot complete steps in
+// order), so a pass checks at most one event / flag per stage.  Returns
+// whether anything moved, or a negative status.
 static int persist_pump(ft_runner *r) {
-    while (r->next_ready <= r->last_k) {
+    int moved = 0;
+    const int64_t last = r->last_k.load(std::memory_order_acquire);
+    if (r->next_ready <= last) {
         const int i = (int)(r->next_ready % r->n);
         const cudaError_t q = cudaEventQuery(r->ev_h2d[i]);
-        if (q == cudaErrorNotReady) break;
-        if (q != cudaSuccess) return (int)q;
-        r->hflags[i] = (unsigned)(r->next_ready + 1);
-        ++r->next_ready;
+        if (q == cudaSuccess) {
+            r->hflags[i] = (unsigned)(r->next_ready + 1);
+            ++r->next_ready;
+            moved = 1;
+        } else if (q != cudaErrorNotReady) {
+            return -(int)q;
+        }
     }
-    while (r->next_d2h < r->next_ready) {
+    if (r->next_d2h < r->next_ready) {
         const int i = (int)(r->next_d2h % r->n);
         const uint32_t want = (uint32_t)(r->next_d2h + 1);
-        if ((int32_t)(r->hflags[PERSIST_MAX_SLOTS + i] - want) < 0) break;
-        cudaError_t e = cudaMemcpyAsync(r->host_out[i], r->dev_out[i], r->out_bytes,
-                                        cudaMemcpyDeviceToHost, r->d2hs[i]);
-        if (e == cudaSuccess) e = cudaEventRecord(r->ev_d2h[i], r->d2hs[i]);
-        if (e != cudaSuccess) return (int)e;
-        ++r->next_d2h;
+        if ((int32_t)(r->hflags[PERSIST_MAX_SLOTS + i] - want) >= 0) {
+            cudaError_t e = cudaMemcpyAsync(r->host_out[i], r->dev_out[i], r->out_bytes,
+                                            cudaMemcpyDeviceToHost, r->d2hs[i]);
+            if (e == cudaSuccess) e = cudaEventRecord(r->ev_d2h[i], r->d2hs[i]);
+            if (e != cudaSuccess) return -(int)e;
+            ++r->next_d2h;
+            moved = 1;
+        }
     }
-    return FT_OK;
+    if (r->next_out < r->next_d2h) {
+        const cudaError_t q = cudaEventQuery(r->ev_d2h[r->next_out % r->n]);
+        if (q == cudaSuccess) {
+            r->out_k.store(r->next_out, std::memory_order_release);
+            ++r->next_out;
+            moved = 1;
+        } else if (q != cudaErrorNotReady) {
+            return -(int)q;
+        }
+    }
+    return moved;
 }
 
-// Persistent mode: pump until step k's outputs are on the host.
+static void persist_pump_loop(ft_runner *r) {
+    cudaSetDevice(r->device);
+    while (!r->pump_stop.load(std::memory_order_acquire)) {
+        const int m = persist_pump(r);
+        if (m < 0) {
+            r->pump_err.store(-m);  // the CUDA error
+            return;
+        }
+        if (!m) {
+#if defined(__x86_64__) || defined(__i386__)
+            __builtin_ia32_pause();
+#endif
+        }
+    }
+}
+
+// Persistent mode: wait until step k's outputs are on the host (the pump
+// thread's counter; no CUDA call on the caller's thread).
 static int persist_wait(ft_runner *r, int64_t k) {
-    const int i = (int)(k % r->n);
-    if (k > r->last_k) return FT_E_RANGE;  // never submitted
+    if (k > r->last_k.load()) return FT_E_RANGE;  // never submitted
     const auto t0 = std::chrono::steady_clock::now();
     for (unsigned it = 1;; ++it) {
-        const int st = persist_pump(r);
-        if (st != FT_OK) return st;
-        if (r->next_d2h > k) {
-            const cudaError_t q = cudaEventQuery(r->ev_d2h[i]);
-            if (q == cudaSuccess) return FT_OK;
-            if (q != cudaErrorNotReady) return (int)q;
-        }
-        if ((it & 1023u) == 0 &&
+        if (r->out_k.load(std::memory_order_acquire) >= k) return FT_OK;
+        const int err = r->pump_err.load();
+        if (err != FT_OK) return err;
+        if ((it & 4095u) == 0 &&
             std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
             return FT_E_TIMEOUT;
 #if defined(__x86_64__) || defined(__i386__)
@@ -212,7 +266,7 @@ extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host
         if (ranges[2 * q] > ranges[2 * q + 1] || ranges[2 * q + 1] > r->in_bytes) return FT_E_RANGE;
     const int i = (int)(k % r->n);
     if (r->persistent) {
-        if (k != r->last_k + 1) return FT_E_RANGE;  // steps are submitted in order
+        if (k != r->last_k.load() + 1) return FT_E_RANGE;  // steps are submitted in order
         // slot i's step k-n must be fully out (outputs on the host, inputs consumed)
         if (k >= r->n) {
             const int st = persist_wait(r, k - r->n);
@@ -228,8 +282,8 @@ extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host
         }
         if (e == cudaSuccess) e = cudaEventRecord(r->ev_h2d[i], r->h2d);
         if (e != cudaSuccess) return (int)e;
-        r->last_k = k;
-        return persist_pump(r);
+        r->last_k.store(k, std::memory_order_release);  // the pump takes it from here
+        return FT_OK;
     }
     cudaError_t e = cudaStreamWaitEvent(r->h2d, r->ev_comp[i], 0);
     for (int q = 0; q < n_ranges && e == cudaSuccess; ++q) {
@@ -278,8 +332,14 @@ extern "C" int ft_runner_destroy(ft_runner *r) {
         // every submitted step completes first, so all blocks are polling the
         // next ready word -- then stop the persistent kernel (a stop seen
         // mid-step by a late block would leave its group at a barrier)
-        for (int64_t k = r->last_k - r->n + 1; k <= r->last_k; ++k)
-            if (k >= 0) persist_wait(r, k);
+        const int64_t last = r->last_k.load();
+        if (last >= 0) persist_wait(r, last);
+        r->pump_stop.store(true);
+        if (r->pump) {
+            r->pump->join();
+            delete r->pump;
+            r->pump = nullptr;
+        }
         for (int i = 0; i < PERSIST_MAX_SLOTS; ++i) r->hflags[i] = PERSIST_STOP;
         cudaStreamSynchronize(r->comp);
         ft_internal_persist_dump();

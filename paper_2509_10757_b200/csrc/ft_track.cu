@@ -866,9 +866,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
             return;
         }
         if (threadIdx.x == 0) {
-            unsigned long long v;
-            while ((uint32_t)(v = ld_acquire_u64(a.tail_s + slot)) != (uint32_t)Gw)
-                __nanosleep(20);
+            while ((uint32_t)ld_acquire_u64(a.tail_s + slot) != (uint32_t)Gw) __nanosleep(20);
             // arrivals back to 0 for the group's next frame (after this one)
             atomicAdd(a.tail_s + slot, (1ull << 32) - (unsigned long long)Gw);
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
