@@ -384,6 +384,14 @@ int ft_track_plan(int32_t n_frames, const ft_keypoints *left, const ft_keypoints
                   const ft_project_io *io, int32_t pmode, const ft_project_out *pout,
                   const ft_workspace *ws, void *plan, size_t plan_bytes);
 
+/* n_steps frames through ONE persistent launch: step k runs plans[k % n_plans]
+ * (ft_track_plan records; same shapes), inputs already resident in the
+ * plans' buffers, no launch or hand-off between steps (the device-resident
+ * form of the persistent runner: a ring of resident frames processed back
+ * to back).  Stream-ordered; n_steps < 2^31. */
+int ft_track_frames_ring(int32_t n_plans, const void *const *plans, int64_t n_steps,
+                         ft_stream_t stream);
+
 /* projection.py:161-178 resolve_conflicts on caller-held phase-A arrays
  * (one frame): correspondences in point order into out->corr_* and
  * out->corr_count[0].  n_kp <= ws->cap_left. */

@@ -112,7 +112,7 @@ EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_works
            "ft_pack_keypoints", "ft_pack_points", "ft_build_pyramids", "ft_stereo_fisheye",
            "ft_gather_points", "ft_scatter_points", "ft_copy_ranges", "ft_runner_create", "ft_runner_create_n", "ft_runner_submit", "ft_runner_submit_range", "ft_runner_submit_ranges",
            "ft_runner_wait", "ft_runner_destroy", "ft_runner_create_persistent",
-           "ft_track_plan", "ft_track_plan_bytes")
+           "ft_track_plan", "ft_track_plan_bytes", "ft_track_frames_ring")
 
 
 def build(force: bool = False) -> Path:
@@ -160,6 +160,7 @@ def load() -> ctypes.CDLL:
     L.ft_runner_destroy.argtypes = [vp]
     L.ft_runner_create_persistent.argtypes = [i32, vp, vp, ctypes.c_size_t, vp, vp,
                                               ctypes.c_size_t, P(vp)]
+    L.ft_track_frames_ring.argtypes = [i32, vp, i64, vp]
     L.ft_track_plan_bytes.restype = ctypes.c_size_t
     L.ft_track_plan_bytes.argtypes = []
     L.ft_track_plan.argtypes = [i32, P(FtKeypoints), P(FtKeypoints), P(FtPyramid),

@@ -44,7 +44,7 @@
 
 extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
                                           const unsigned *h_ready, unsigned *h_done,
-                                          cudaStream_t stream);
+                                          void **args_out, cudaStream_t stream);
 extern "C" void ft_internal_persist_dump(void);
 
 namespace {
@@ -55,7 +55,8 @@ constexpr unsigned PERSIST_STOP = 0xffffffffu;
 struct ft_runner {
     int n;
     bool persistent;
-    unsigned *flags;  // persistent: [device ready x 8 | - x 8 | arrive x 8] device words
+    unsigned *flags;  // persistent: [device ready x 8 | arrive x 8] device words
+    void *args_dev;   // persistent: the kernel's argument array
     volatile unsigned *hflags;  // persistent: pinned mapped [ready x 8 | done x 8]
     unsigned *hflags_dev;
     std::atomic<int64_t> last_k;    // last submitted step (caller -> pump)
@@ -136,9 +137,9 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
     r->pump_stop.store(false);
     r->next_ready = r->next_d2h = r->next_out = 0;
     cudaGetDevice(&r->device);
-    cudaError_t e = cudaMalloc(&r->flags, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned));
+    cudaError_t e = cudaMalloc(&r->flags, 2 * PERSIST_MAX_SLOTS * sizeof(unsigned));
     if (e == cudaSuccess)
-        e = cudaMemsetAsync(r->flags, 0, 3 * PERSIST_MAX_SLOTS * sizeof(unsigned), r->comp);
+        e = cudaMemsetAsync(r->flags, 0, 2 * PERSIST_MAX_SLOTS * sizeof(unsigned), r->comp);
     void *hf = nullptr;
     if (e == cudaSuccess)
         e = cudaHostAlloc(&hf, 2 * PERSIST_MAX_SLOTS * sizeof(unsigned), cudaHostAllocMapped);
@@ -152,7 +153,8 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
     if (e == cudaSuccess) e = cudaStreamSynchronize(r->comp);
     if (e == cudaSuccess) {
         st = ft_internal_persist_launch(plans, n_slots, r->flags, r->hflags_dev,
-                                        r->hflags_dev + PERSIST_MAX_SLOTS, r->comp);
+                                        r->hflags_dev + PERSIST_MAX_SLOTS, &r->args_dev,
+                                        r->comp);
         if (st != FT_OK) {  // no kernel to stop
             ft_runner_destroy(r);
             *out = nullptr;
@@ -346,6 +348,8 @@ extern "C" int ft_runner_destroy(ft_runner *r) {
     }
     if (r->flags) cudaFree(r->flags);
     r->flags = nullptr;
+    if (r->args_dev) cudaFree(r->args_dev);
+    r->args_dev = nullptr;
     if (r->hflags) cudaFreeHost(const_cast<unsigned *>(r->hflags));
     r->hflags = nullptr;
     for (int i = 0; i < r->n; ++i)

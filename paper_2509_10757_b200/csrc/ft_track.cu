@@ -43,6 +43,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "ft_common.cuh"
 #include "ft_ws.cuh"
@@ -1698,8 +1699,10 @@ constexpr int PERSIST_MAX_SLOTS = 8;
 constexpr unsigned FT_PERSIST_STOP = 0xffffffffu;
 
 struct PersistArgs {
-    TrackArgs a[PERSIST_MAX_SLOTS];  // identical geometry (W, Gs, Gm) in every slot
-    int n;
+    const TrackArgs *args;  // [n] in device memory, identical geometry in every slot
+    int n, W, Gs, Gm;
+    unsigned max_steps;     // the launch ends after this many steps (or at a stop)
+    int gate;               // step k waits for the slot's step k - n to be done (ring)
     const unsigned *ready;  // [n] host-mapped: step + 1 whose inputs are in the slot
     unsigned *dready;       // [n] device copy of ready (forwarded by block 0)
     unsigned *done;         // [n] host-mapped: step + 1 whose outputs are complete
@@ -1722,6 +1725,7 @@ FT_DEV unsigned ld_acquire_sys_u32(const unsigned *p) {
 __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_constant__ PersistArgs p) {
     extern __shared__ __align__(16) unsigned char smem_all[];
     __shared__ int s_go, s_last;
+    __shared__ __align__(16) TrackArgs s_args;  // the current slot's arguments
     unsigned long long *mbar = reinterpret_cast<unsigned long long *>(smem_all);
     unsigned char *smem = smem_all + 16;
     if (threadIdx.x == 0) {
@@ -1731,17 +1735,26 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
     }
     __syncthreads();
     unsigned mphase = 0, bpar = 0;
-    const int per = p.a[0].Gs + p.a[0].Gm;
-    const unsigned B = (unsigned)(p.a[0].W * per);
+    const int per = p.Gs + p.Gm;
+    const unsigned B = (unsigned)(p.W * per);
     const int wslot = blockIdx.x / per, r = blockIdx.x - wslot * per;
-    for (unsigned k = 0;; ++k) {
+    constexpr int ARG_WORDS = (int)(sizeof(TrackArgs) / 8);
+    static_assert(sizeof(TrackArgs) % 8 == 0, "TrackArgs copied as 8-byte words");
+    for (unsigned k = 0; k < p.max_steps; ++k) {
         const int i = (int)(k % (unsigned)p.n);
         if (threadIdx.x == 0) {
             unsigned v;
             if (blockIdx.x == 0) {  // the PCIe watcher
                 while ((v = ld_acquire_sys_u32(p.ready + i)) != FT_PERSIST_STOP && v < k + 1)
                     __nanosleep(100);
-                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.dready + i), "r"(v)
+                // the slot's previous step (k - n, same workspace) must be complete:
+                // its tail blocks may still be counting arrivals (the runner's host
+                // ordering implies it; a ring launch with every step ready does not)
+                if (p.gate && v != FT_PERSIST_STOP && k >= (unsigned)p.n)
+                    while (ld_acquire_sys_u32(p.done + i) < k + 1 - (unsigned)p.n) __nanosleep(64);
+                // forward exactly this step (the host word may already allow later ones)
+                const unsigned fwd = v == FT_PERSIST_STOP ? v : k + 1;
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.dready + i), "r"(fwd)
                              : "memory");
             } else {
                 while ((v = ld_acquire_u32(p.dready + i)) != FT_PERSIST_STOP && v < k + 1)
@@ -1750,9 +1763,12 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
             s_go = v != FT_PERSIST_STOP;
             if (p.ts && blockIdx.x == 0 && s_go) p.ts[2 * (k & 4095u)] = global_ns();
         }
+        if (threadIdx.x < ARG_WORDS)  // slot i's arguments -> shared memory
+            reinterpret_cast<unsigned long long *>(&s_args)[threadIdx.x] =
+                __ldg(reinterpret_cast<const unsigned long long *>(p.args + i) + threadIdx.x);
         __syncthreads();
         if (!s_go) break;
-        const TrackArgs &a = p.a[i];
+        const TrackArgs &a = s_args;
         for (int f = wslot; f < a.F; f += a.W) {
             if (r < a.Gs) stereo_frame(a, f, r, wslot, smem, mbar, mphase, bpar);
             else map_frame(a, f, r - a.Gs, wslot, smem, mbar, mphase, bpar);
@@ -2333,25 +2349,36 @@ extern "C" void ft_internal_persist_dump(void) {
 // Launch the persistent kernel over n plans (internal: ft_runner.cu).  The
 // plans must share one geometry and leave SMs free for other work (the
 // launch never ends on its own: it would starve every later kernel).
-extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
-                                          const unsigned *h_ready, unsigned *h_done,
-                                          cudaStream_t stream) {
-    if (!plans || !flags) return FT_E_NULL;
-    if (n < 1 || n > PERSIST_MAX_SLOTS) return FT_E_RANGE;
-    // (the flag words: see track_persist_kernel)
+// Fill a PersistArgs from n plans (same geometry) and launch the persistent
+// kernel.  args_dev: n TrackArgs of device memory the kernel reads (copied
+// here, stream-ordered from a host buffer that outlives the copy).
+static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
+                          std::vector<TrackArgs> &host_args, const unsigned *ready,
+                          unsigned *dready, unsigned *done, unsigned *arrive, unsigned max_steps,
+                          int gate, cudaStream_t stream) {
+    if (!plans || !args_dev || !ready || !dready || !done || !arrive) return FT_E_NULL;
+    if (n < 1) return FT_E_RANGE;
     PersistArgs p;
     memset(&p, 0, sizeof(p));
     size_t smem = 0;
+    host_args.resize(n);
     for (int i = 0; i < n; ++i) {
         const TrackPlan *tp = static_cast<const TrackPlan *>(plans[i]);
         if (!tp) return FT_E_NULL;
         if (tp->magic != PLAN_MAGIC) return FT_E_CONFIG;
-        p.a[i] = tp->a;
-        const TrackArgs &a0 = p.a[0];
-        if (tp->a.W != a0.W || tp->a.Gs != a0.Gs || tp->a.Gm != a0.Gm) return FT_E_CONFIG;
+        host_args[i] = tp->a;
+        if (tp->a.W != host_args[0].W || tp->a.Gs != host_args[0].Gs ||
+            tp->a.Gm != host_args[0].Gm)
+            return FT_E_CONFIG;
         smem = tp->smem > smem ? tp->smem : smem;
     }
+    p.args = args_dev;
     p.n = n;
+    p.W = host_args[0].W;
+    p.Gs = host_args[0].Gs;
+    p.Gm = host_args[0].Gm;
+    p.max_steps = max_steps;
+    p.gate = gate;
     static unsigned long long *ts_buf = nullptr;
     if (getenv("FT_DEBUG_PERSIST")) {
         if (!ts_buf) cudaMalloc(&ts_buf, 4096 * 2 * 8);
@@ -2359,18 +2386,20 @@ extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsig
         p.ts = ts_buf;
         g_persist_ts = ts_buf;
     }
-    if (!h_ready || !h_done) return FT_E_NULL;
-    p.ready = h_ready;
-    p.done = h_done;
-    p.dready = flags;
-    p.arrive = flags + 2 * PERSIST_MAX_SLOTS;
+    p.ready = ready;
+    p.dready = dready;
+    p.done = done;
+    p.arrive = arrive;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = p.a[0].W * (p.a[0].Gs + p.a[0].Gm);
+    const int grid = p.W * (p.Gs + p.Gm);
     if (grid > sms - 4) return FT_E_RANGE;  // keep SMs for the copies' helper kernels
-    cudaError_t e = cudaFuncSetAttribute(track_persist_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaMemcpyAsync(args_dev, host_args.data(), sizeof(TrackArgs) * n,
+                                    cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaFuncSetAttribute(track_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
     if (e != cudaSuccess) return (int)e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -2384,6 +2413,58 @@ extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsig
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, track_persist_kernel, p);
     return (int)e;
+}
+
+// The runner's launch (internal: ft_runner.cu).  flags: 2 * PERSIST_MAX_SLOTS
+// device words [dready | arrive]; h_ready / h_done: mapped host words;
+// *args_out: the device argument array (the runner frees it).
+extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
+                                          const unsigned *h_ready, unsigned *h_done,
+                                          void **args_out, cudaStream_t stream) {
+    if (!plans || !flags || !args_out) return FT_E_NULL;
+    if (n < 1 || n > PERSIST_MAX_SLOTS) return FT_E_RANGE;
+    TrackArgs *args = nullptr;
+    cudaError_t e = cudaMalloc(&args, sizeof(TrackArgs) * n);
+    if (e != cudaSuccess) return (int)e;
+    *args_out = args;
+    static std::vector<TrackArgs> host;  // must outlive the async copy: synchronised below
+    const int st = persist_launch(plans, n, args, host, h_ready, flags, h_done,
+                                  flags + PERSIST_MAX_SLOTS, 0xffffffffu, 0, stream);
+    return st;
+}
+
+extern "C" int ft_track_frames_ring(int32_t n_plans, const void *const *plans, int64_t n_steps,
+                                    ft_stream_t stream) {
+    if (!plans) return FT_E_NULL;
+    if (n_plans < 1 || n_steps < 0 || n_steps >= 0x7f000000) return FT_E_RANGE;
+    if (n_steps == 0) return FT_OK;
+    // per-process buffers, grown on demand (stream-ordered reuse)
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    static TrackArgs *args = nullptr;
+    static unsigned *words = nullptr;
+    static int cap = 0;
+    static std::vector<TrackArgs> host;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_plans > cap) {
+        cudaStreamSynchronize(s);
+        if (args) cudaFree(args);
+        if (words) cudaFree(words);
+        args = nullptr;
+        words = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&args, sizeof(TrackArgs) * n_plans);
+        if (e == cudaSuccess) e = cudaMalloc(&words, 4 * sizeof(unsigned) * n_plans);
+        if (e != cudaSuccess) return (int)e;
+        cap = n_plans;
+    }
+    // [ready | dready | done | arrive]: every step ready up front
+    cudaError_t e = cudaMemsetAsync(words, 0x7f, sizeof(unsigned) * n_plans, s);
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(words + n_plans, 0, 3 * sizeof(unsigned) * n_plans, s);
+    if (e != cudaSuccess) return (int)e;
+    return persist_launch(plans, n_plans, args, host, words, words + n_plans,
+                          words + 2 * n_plans, words + 3 * n_plans, (unsigned)n_steps, 1, s);
 }
 
 extern "C" int ft_stereo_pinhole(int32_t n_frames, const ft_keypoints *left,

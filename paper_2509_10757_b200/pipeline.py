@@ -486,6 +486,13 @@ class FramePipeline:
                             n_slots=int(self._h("slot_n", np.int32, (S,))[s]),
                             n_matched=int(self._h("n_matched", np.int32, (S,))[s]))
 
+    def copy_outputs(self) -> None:
+        """Device outputs -> the pinned host area result() reads (synchronous)."""
+        with torch.cuda.stream(self.stream):
+            self.host[self.out_begin:self.out_end].copy_(self.dev[self.out_begin:self.out_end],
+                                                         non_blocking=True)
+        self.stream.synchronize()
+
     def staged_inputs(self) -> torch.Tensor:
         """A pinned copy of the current input staging (what load_frame wrote):
         one step's inputs, ready for AsyncRunner.submit."""
@@ -506,6 +513,25 @@ class FramePipeline:
         if self.packed:
             self.pack()
         dst.copy_(self.host[:self.in_end])
+
+
+def run_ring(pipes, n_steps: int, stream=None) -> None:
+    """n_steps steps over pipelines whose inputs are already on the device, in
+    ONE persistent launch (ft_track_frames_ring): step k runs pipes[k % n]'s
+    track step.  Stream-ordered on `stream` (default pipes[0].stream); the
+    outputs stay on the device (read them with copy_outputs())."""
+    import ctypes
+    plans = []
+    for p in pipes:
+        if getattr(p, "_plan", None) is None:
+            p._plan = p.plan()
+            if p._plan is None:
+                raise ValueError("run_ring: each step must be the one track launch")
+        plans.append(p._plan)
+    arr = (ctypes.c_void_p * len(plans))(*[ctypes.addressof(pl) for pl in plans])
+    st = stream if stream is not None else pipes[0].stream
+    _lib.check(pipes[0].lib.ft_track_frames_ring(len(plans), arr, int(n_steps), st.cuda_stream),
+               "ft_track_frames_ring")
 
 
 def _graph_exec_ptr(graph) -> int:

@@ -471,3 +471,31 @@ def test_tail_blocks_per_launch(workloads, expected, monkeypatch):
     _run(workloads, expected, 3, 2)
     from paper_2509_10757_b200.maptable import MapTable
     _run(workloads, expected, 1, 2, table=MapTable(capacity=32 * 1024))
+
+
+def test_resident_ring(workloads, expected):
+    """ft_track_frames_ring: 11 steps over 4 resident pipelines in one
+    persistent launch (each pipeline runs 2-3 times); every pipeline's final
+    outputs equal the oracle's."""
+    import torch
+    from paper_2509_10757_b200.pipeline import FramePipeline, run_ring
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left) for _ in range(4)]
+    for i, (p, w) in enumerate(zip(pipes, workloads)):
+        p.load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                     slots=expected[i][1])
+        p.dev[:p.in_end].copy_(p.host[:p.in_end])
+    torch.cuda.synchronize()
+    run_ring(pipes, 11)
+    pipes[0].synchronize()
+    for i, (p, w) in enumerate(zip(pipes, workloads)):
+        p.copy_outputs()
+        m, _, slots, n = expected[i]
+        res = p.result(0, len(w.left.u))
+        for f in FIELDS:
+            np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f), err_msg=f)
+        np.testing.assert_array_equal(res.slots, slots)
+        assert res.n_slots == n
+    run_ring(pipes, 0)  # no-op
