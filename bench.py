@@ -586,12 +586,33 @@ def main() -> None:
         t = json.loads(tf.read_text()).get("ft_track_frames", {})
         if "dram_bytes_read_per_launch" in t:
             traffic = t["dram_bytes_read_per_launch"] + t.get("dram_bytes_write_per_launch", 0)
+    if use_ring:  # the value region's kernel: one persistent launch over K frames
+        ring_traffic = None
+        if tf.exists() and S == 1:
+            t = json.loads(tf.read_text()).get("track_persist_kernel_ring", {})
+            if "dram_bytes_per_frame" in t:
+                ring_traffic = t["dram_bytes_per_frame"] * args.steps
+        ring_bytes = dom_bytes * args.steps
+        ring_ach = ring_bytes / (ring_any / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": "ft_track_frames", "achieved": achieved,
                 "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)", "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
                 "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": track_ms,
                 "note": "one frame per launch is latency-bound (dependent L2/HBM round trips "
                         "and group barriers); see roofline_int and batched"}
+    if use_ring:
+        roofline = {"bound": "hbm", "kernel": "track_persist_kernel (ft_track_frames_ring, "
+                                              f"{args.steps} frames per launch)",
+                    "achieved": ring_ach, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": ring_ach / hbm_peak, "traffic": ring_traffic,
+                    "traffic_source": "profiles/traffic.json (ncu --set full, per frame x K)",
+                    "peak_source": roofline["peak_source"],
+                    "algorithmic_bytes_per_launch": ring_bytes, "launch_ms": ring_any,
+                    "note": "SURVEY 8(d) algorithmic bytes count both whole pyramids (2.2 of "
+                            "the 2.98 MB per frame); phase 2 reads only the levels of the "
+                            "frame's octaves, so DRAM traffic is ~0.37 MB per frame.  A frame "
+                            "is a chain of dependent L2 round trips (latency-bound)",
+                    "per_frame_launch": roofline}
     # PCIe diagnostic: one step's input bytes, pinned H2D alone (events)
     h2d_times = []
     for _ in range(10):
