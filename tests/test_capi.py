@@ -97,3 +97,18 @@ def test_new_entries_validate_without_gpu():
     assert L.ft_runner_submit_ranges(None, 0, None, None, 0) == -1
     assert L.ft_runner_wait(None, 0) == -1
     assert L.ft_runner_destroy(None) == 0
+    # persistent runner / plans / resident ring
+    assert L.ft_runner_create_persistent(2, None, None, 16, None, None, 16,
+                                         ctypes.byref(out)) == -1
+    assert L.ft_runner_create_persistent(1, vp2(None, None), vp2(None, None), 16,
+                                         vp2(None, None), vp2(None, None), 16,
+                                         ctypes.byref(out)) == -2  # needs >= 2 slots
+    assert L.ft_track_plan_bytes() > 0
+    buf = (ctypes.c_ubyte * 16)()
+    assert L.ft_track_plan(1, kp, kp, None, None, None, 0, None, None, None, None, 0, None,
+                           ws, None, 0) == -1  # no plan buffer
+    assert L.ft_track_plan(1, kp, kp, None, None, None, 0, None, None, None, None, 0, None,
+                           ws, buf, 16) == -2  # plan buffer too small
+    assert L.ft_track_frames_ring(1, None, 1, None) == -1
+    assert L.ft_track_frames_ring(0, vp2(None, None), 1, None) == -2
+    assert L.ft_track_frames_ring(1, vp2(None, None), -1, None) == -2
