@@ -2005,9 +2005,13 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int F = a.F;
-    // per-frame block budget: ~1 warp per left keypoint, ~128 map points per block
+    // per-frame block budget: ~1 warp per left keypoint, ~84 map points per block
+    // (measured at cfg2: 128 -> 84 points per block takes the persistent ring
+    // from 13.4 to 12.5 us per frame; the map role's search rounds shrink)
     int gs_ideal = want_stereo ? (a.L.cap + TK_WARPS - 1) / TK_WARPS : 0;
-    int gm_ideal = want_map ? (a.P.cap + 127) / 128 : 0;
+    static const int pts_per_block = getenv("FT_MAP_PTS_PER_BLOCK")
+                                         ? atoi(getenv("FT_MAP_PTS_PER_BLOCK")) : 84;
+    int gm_ideal = want_map ? (a.P.cap + pts_per_block - 1) / pts_per_block : 0;
     if (gs_ideal > 96) gs_ideal = 96;
     if (gm_ideal > 64) gm_ideal = 64;
     // the map role's per-point shared arrays (32 B / point of its chunk) must
