@@ -402,6 +402,7 @@ def test_copy_ranges_alignments():
     assert lib.ft_copy_ranges(None, dd.data_ptr(), 1, None) == -1
 
 
+@pytest.mark.timeout(180)
 @pytest.mark.parametrize("n_streams", [1, 2])
 def test_persistent_runner(workloads, expected, n_streams):
     """Persistent runner: one long-lived track kernel serves 3 slots, steps
@@ -463,6 +464,7 @@ def test_persistent_runner(workloads, expected, n_streams):
     pipes[0].synchronize()
 
 
+@pytest.mark.timeout(180)
 def test_tail_blocks_per_launch(workloads, expected, monkeypatch):
     """The dedicated stereo-tail / map-resolve blocks (persistent plans' mode)
     forced on ordinary launches: same results as the group-barrier path."""
@@ -473,6 +475,7 @@ def test_tail_blocks_per_launch(workloads, expected, monkeypatch):
     _run(workloads, expected, 1, 2, table=MapTable(capacity=32 * 1024))
 
 
+@pytest.mark.timeout(180)
 def test_resident_ring(workloads, expected):
     """ft_track_frames_ring: 11 steps over 4 resident pipelines in one
     persistent launch (each pipeline runs 2-3 times); every pipeline's final
