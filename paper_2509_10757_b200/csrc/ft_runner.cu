@@ -69,6 +69,8 @@ struct ft_runner {
     int64_t next_d2h;    // pump: oldest step whose D2H is not yet issued
     int64_t next_out;    // pump: oldest step whose D2H has not yet completed
     cudaStream_t d2hs[FT_RUNNER_MAX_SLOTS];  // persistent: one D2H stream per slot
+    cudaStream_t h2dx[3];  // persistent: extra H2D streams (steps round robin)
+    int n_h2d;
     cudaStream_t h2d, comp, d2h;
     cudaEvent_t ev_h2d[FT_RUNNER_MAX_SLOTS], ev_comp[FT_RUNNER_MAX_SLOTS],
         ev_d2h[FT_RUNNER_MAX_SLOTS];
@@ -150,6 +152,13 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
     }
     for (int i = 0; i < n_slots && e == cudaSuccess; ++i)
         e = cudaStreamCreateWithFlags(&r->d2hs[i], cudaStreamNonBlocking);
+    {
+        const char *ev = getenv("FT_RUNNER_H2D_STREAMS");
+        const int want = ev ? atoi(ev) : 2;
+        r->n_h2d = want < 1 ? 1 : (want > 4 ? 4 : want);
+    }
+    for (int q = 0; q + 1 < r->n_h2d && e == cudaSuccess; ++q)
+        e = cudaStreamCreateWithFlags(&r->h2dx[q], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamSynchronize(r->comp);
     if (e == cudaSuccess) {
         st = ft_internal_persist_launch(plans, n_slots, r->flags, r->hflags_dev,
@@ -274,15 +283,19 @@ extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host
             const int st = persist_wait(r, k - r->n);
             if (st != FT_OK) return st;
         }
+        // H2D streams round robin (several copy engines): one step's copy
+        // overhead overlaps the other's transfer
+        const int hq = (int)(k % r->n_h2d);
+        cudaStream_t hs = hq == 0 ? r->h2d : r->h2dx[hq - 1];
         cudaError_t e = cudaSuccess;
         for (int q = 0; q < n_ranges && e == cudaSuccess; ++q) {
             const size_t lo = ranges[2 * q], n = ranges[2 * q + 1] - lo;
             if (n)
                 e = cudaMemcpyAsync(static_cast<char *>(r->dev_in[i]) + lo,
                                     static_cast<const char *>(host_in) + lo, n,
-                                    cudaMemcpyHostToDevice, r->h2d);
+                                    cudaMemcpyHostToDevice, hs);
         }
-        if (e == cudaSuccess) e = cudaEventRecord(r->ev_h2d[i], r->h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(r->ev_h2d[i], hs);
         if (e != cudaSuccess) return (int)e;
         r->last_k.store(k, std::memory_order_release);  // the pump takes it from here
         return FT_OK;
@@ -354,6 +367,11 @@ extern "C" int ft_runner_destroy(ft_runner *r) {
     r->hflags = nullptr;
     for (int i = 0; i < r->n; ++i)
         if (r->d2hs[i]) cudaStreamDestroy(r->d2hs[i]);
+    for (int q = 0; q < 3; ++q)
+        if (r->h2dx[q]) {
+            cudaStreamSynchronize(r->h2dx[q]);
+            cudaStreamDestroy(r->h2dx[q]);
+        }
     cudaStreamSynchronize(r->h2d);
     cudaStreamSynchronize(r->comp);
     cudaStreamSynchronize(r->d2h);

@@ -28,7 +28,10 @@ ranges = []
 for k, w in enumerate(ws):
     pipes[0].load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
     pipes[0].stage_into(ring[k])
-    ranges.append(AsyncRunner.ranges_arg(pipes[0].input_ranges()))
+    rr = pipes[0].input_ranges()
+    if os.environ.get("TRUNC_KB"):  # timing experiment: ship only the first TRUNC_KB of each range
+        rr = [(lo, min(hi, lo + 1024 * int(os.environ["TRUNC_KB"]))) for lo, hi in rr]
+    ranges.append(AsyncRunner.ranges_arg(rr))
 for i, p in enumerate(pipes):
     if not os.environ.get("PERSIST_TL_ONLY"):  # (the timeline hook syncs: no capture)
         p.capture()
