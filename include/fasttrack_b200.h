@@ -388,7 +388,9 @@ int ft_track_plan(int32_t n_frames, const ft_keypoints *left, const ft_keypoints
  * (ft_track_plan records; same shapes), inputs already resident in the
  * plans' buffers, no launch or hand-off between steps (the device-resident
  * form of the persistent runner: a ring of resident frames processed back
- * to back).  Stream-ordered; n_steps < 2^31. */
+ * to back).  Stream-ordered; n_steps < 2^31.  Successive calls share the
+ * library's flag / argument buffers and are ordered after one another even
+ * across streams.  Each plan's grid must leave 4 SMs free (FT_E_RANGE). */
 int ft_track_frames_ring(int32_t n_plans, const void *const *plans, int64_t n_steps,
                          ft_stream_t stream);
 

@@ -2462,13 +2462,22 @@ extern "C" int ft_track_frames_ring(int32_t n_plans, const void *const *plans, i
         if (e != cudaSuccess) return (int)e;
         cap = n_plans;
     }
+    // the buffers are shared by every call: order after the previous ring,
+    // whatever stream it ran on
+    static cudaEvent_t prev = nullptr;
+    if (!prev && cudaEventCreateWithFlags(&prev, cudaEventDisableTiming) != cudaSuccess)
+        return FT_E_CONFIG;
+    cudaStreamWaitEvent(s, prev, 0);
     // [ready | dready | done | arrive]: every step ready up front
     cudaError_t e = cudaMemsetAsync(words, 0x7f, sizeof(unsigned) * n_plans, s);
     if (e == cudaSuccess)
         e = cudaMemsetAsync(words + n_plans, 0, 3 * sizeof(unsigned) * n_plans, s);
     if (e != cudaSuccess) return (int)e;
-    return persist_launch(plans, n_plans, args, host, words, words + n_plans,
-                          words + 2 * n_plans, words + 3 * n_plans, (unsigned)n_steps, 1, s);
+    const int st = persist_launch(plans, n_plans, args, host, words, words + n_plans,
+                                  words + 2 * n_plans, words + 3 * n_plans, (unsigned)n_steps,
+                                  1, s);
+    if (st == FT_OK) cudaEventRecord(prev, s);
+    return st;
 }
 
 extern "C" int ft_stereo_pinhole(int32_t n_frames, const ft_keypoints *left,
