@@ -1820,7 +1820,7 @@ namespace {
 // Launch geometry depends only on shapes; cache it so graph capture and
 // steady-state launches make no attribute / occupancy queries.
 struct GeomKey {
-    int dev, F, lcap, rcap, pcap, kcap, H, patch_ints, ncell, hash_bits, ws, wm;
+    int dev, F, lcap, rcap, pcap, kcap, H, patch_ints, ncell, hash_bits, ws, wm, reserve;
     bool operator==(const GeomKey &o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
 };
 struct Geom {
@@ -1835,7 +1835,8 @@ size_t g_attr_smem[64] = {0};  // process-wide, guarded by g_attr_mu
 std::mutex g_attr_mu;
 }  // namespace
 
-static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out);
+static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out,
+                          int reserve);
 
 // The kernel's max-dynamic-smem attribute only ever grows (one attribute per
 // function: lowering it for a small launch would break a cached large one).
@@ -1870,6 +1871,9 @@ static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft
     key.hash_bits = a.hash_bits;
     key.ws = want_stereo;
     key.wm = want_map;
+    // persistent plans (tails) leave SMs for the tail blocks and the copies'
+    // helper kernels: the whole grid must stay <= SMs - 4 with 2 tail blocks
+    key.reserve = tails ? 6 : 0;
     Geom g;
     int hit = -1;
     for (int i = 0; i < g_n; ++i)
@@ -1877,7 +1881,7 @@ static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft
     if (hit >= 0) {
         g = g_vals[hit];
     } else {
-        const int st = track_geometry(a, want_stereo, want_map, g);
+        const int st = track_geometry(a, want_stereo, want_map, g, key.reserve);
         if (st != FT_OK) return st;
         g_keys[g_next] = key;
         g_vals[g_next] = g;
@@ -2000,7 +2004,8 @@ static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_
     return (int)cudaGetLastError();
 }
 
-static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out) {
+static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out,
+                          int reserve) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2040,7 +2045,7 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, track_kernel, TK_THREADS, smem);
         if (occ < 1) return FT_E_RANGE;
-        const int capacity = occ * sms;
+        const int capacity = occ * (sms - reserve);
         const int per_ideal = gs_ideal + gm_ideal;
         int nGs, nGm, nW;
         if ((long long)F * per_ideal <= capacity) {
