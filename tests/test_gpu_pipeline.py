@@ -403,8 +403,8 @@ def test_copy_ranges_alignments():
 
 
 @pytest.mark.timeout(180)
-@pytest.mark.parametrize("n_streams", [1, 2])
-def test_persistent_runner(workloads, expected, n_streams):
+@pytest.mark.parametrize("n_streams,use_table", [(1, False), (2, False), (1, True)])
+def test_persistent_runner(workloads, expected, n_streams, use_table):
     """Persistent runner: one long-lived track kernel serves 3 slots, steps
     handed over by device flags (no launch per step); every step's results
     equal the oracle's, including with level-range shipping (S = 1) and
@@ -414,9 +414,13 @@ def test_persistent_runner(workloads, expected, n_streams):
     w0 = workloads[0]
     S = n_streams
     cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    table = None
+    if use_table:  # map points read in place from the resident table
+        from paper_2509_10757_b200.maptable import MapTable
+        table = MapTable(capacity=32 * 1024)
     pipes = [FramePipeline(w0.cam, n_streams=S, cap_kp=(cap_kp + 31) // 32 * 32,
                            cap_points=5120, pyramid_geometry=w0.pyr_left,
-                           packed_upload=False) for _ in range(3)]
+                           packed_upload=False, map_table=table) for _ in range(3)]
     ring = pipes[0].staging_ring(4)
     ranges = []
     for k in range(4):
@@ -502,3 +506,52 @@ def test_resident_ring(workloads, expected):
         np.testing.assert_array_equal(res.slots, slots)
         assert res.n_slots == n
     run_ring(pipes, 0)  # no-op
+
+
+@pytest.mark.timeout(300)
+def test_persistent_high_load(oracle):
+    """cfg5 shape (~2000 kps, 20k-point maps) through the persistent runner: the
+    plan's geometry leaves SMs for the tail blocks (every SM would be needed
+    otherwise), results equal the oracle's."""
+    from paper_2509_10757_b200.maptable import MapTable
+    from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
+    from paper_2509_10757_b200.synthetic import make_workload
+    from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
+    ws = [make_workload(seed=910 + i, n_landmarks=20000, map_points=20000, images=True,
+                        offset=0.05 * i, id_base=1_000_000 * (i + 1)) for i in range(2)]
+    cap = (max(max(len(w.left.u), len(w.right.u)) for w in ws) + 31) // 32 * 32
+    table = MapTable(capacity=2 * 20480 + 1024)
+    pipes = [FramePipeline(ws[0].cam, n_streams=1, cap_kp=cap, cap_points=20480,
+                           pyramid_geometry=ws[0].pyr_left, map_table=table)
+             for _ in range(4)]
+    ring = pipes[0].staging_ring(2)
+    for k, w in enumerate(ws):
+        pipes[0].load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
+        pipes[0].stage_into(ring[k])
+    want = []
+    for w in ws:
+        m = oracle.stereo_pinhole(w.left, w.right, w.pyr_left, w.pyr_right, w.cam,
+                                  StereoMatchConfig(), w.scale_pow)
+        slots = np.full(len(w.left.u), -1, np.int64)
+        grid = oracle.frame_grid(w.left.u, w.left.v, w.cam.width, w.cam.height, 48) + (48,)
+        n = oracle.search_local_points(w.local.point_ids, w.local.soa, w.left.u, w.left.v,
+                                       w.left.octave, w.left.descriptors, grid, slots, w.pose,
+                                       w.cam, ProjectionSearchConfig(), 1.2, 8)
+        want.append((m, slots, n))
+    runner = AsyncRunner(pipes, persistent=True)
+    try:
+        for k in range(10):
+            if k >= 4:
+                pipe = runner.wait(k - 4)
+                m, slots, n = want[(k - 4) % 2]
+                r = pipe.result(0, len(ws[(k - 4) % 2].left.u))
+                for f in FIELDS:
+                    np.testing.assert_array_equal(getattr(r.matches, f), getattr(m, f),
+                                                  err_msg=f"step {k - 4} {f}")
+                np.testing.assert_array_equal(r.slots, slots)
+                assert r.n_slots == n
+            runner.submit(k, ring[k % 2])
+        for k in range(6, 10):
+            runner.wait(k)
+    finally:
+        runner.close()
