@@ -1703,6 +1703,7 @@ struct PersistArgs {
     int n, W, Gs, Gm;
     unsigned max_steps;     // the launch ends after this many steps (or at a stop)
     int gate;               // step k waits for the slot's step k - n to be done (ring)
+    int red_arrive;         // arrivals by reduction; the last block publishes done
     const unsigned *ready;  // [n] host-mapped: step + 1 whose inputs are in the slot
     unsigned *dready;       // [n] device copy of ready (forwarded by block 0)
     unsigned *done;         // [n] host-mapped: step + 1 whose outputs are complete
@@ -1774,7 +1775,22 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
             else map_frame(a, f, r - a.Gs, wslot, smem, mbar, mphase, bpar);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (p.red_arrive) {
+            // every block but the last one arrives with a release reduction (no
+            // round trip); the last block collects them and publishes the step
+            if (threadIdx.x == 0) {
+                if (blockIdx.x != (int)B - 1) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    atomicAdd(p.arrive + i, 1u);
+                    s_last = 0;
+                } else {
+                    const unsigned want = (k / (unsigned)p.n + 1u) * (B - 1u);
+                    while ((int)(ld_acquire_u32(p.arrive + i) - want) < 0) __nanosleep(32);
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    s_last = 1;
+                }
+            }
+        } else if (threadIdx.x == 0) {
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
             const unsigned old = atomicAdd(p.arrive + i, 1u);
             const bool last = old + 1u == (k / (unsigned)p.n + 1u) * B;  // the step's last block
@@ -2388,6 +2404,7 @@ static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
     p.Gm = host_args[0].Gm;
     p.max_steps = max_steps;
     p.gate = gate;
+    p.red_arrive = getenv("FT_PERSIST_ATOMIC_ARRIVE") ? 0 : 1;
     static unsigned long long *ts_buf = nullptr;
     if (getenv("FT_DEBUG_PERSIST")) {
         if (!ts_buf) cudaMalloc(&ts_buf, 4096 * 2 * 8);
