@@ -933,7 +933,7 @@ def other_configs(args, torch, flush) -> dict:
     for S in (1, 64):
         table = MapTable(capacity=4 * 4096 + 1024)
         pipes = [FisheyePipeline(fw[0].cam, n_streams=S, cap_kp=cap, cap_points=4096,
-                                 map_table=table) for _ in range(4)]
+                                 map_table=table) for _ in range(8 if S == 1 else 4)]
         nst = min(4, S * 4)
         ring = pipes[0].staging_ring(nst)
         for k in range(nst):
