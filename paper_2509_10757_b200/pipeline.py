@@ -578,7 +578,16 @@ class AsyncRunner:
     (ft_runner_create_persistent).  close() ends it after the submitted
     steps; until then the kernel holds its SMs."""
 
-    def __init__(self, pipes, persistent: bool = False):
+    def __init__(self, pipes, persistent=False):
+        """persistent: False (graph launch per step), True (one persistent
+        kernel; raises where the step is not eligible) or "auto" (persistent
+        where eligible, else graph launches; ``self.persistent`` says which)."""
+        if persistent == "auto":
+            try:
+                self.__init__(pipes, persistent=True)
+                return
+            except (ValueError, _lib.FtError):
+                persistent = False
         import ctypes
         if not 2 <= len(pipes) <= 8:
             raise ValueError("AsyncRunner takes 2..8 identically shaped pipelines")

@@ -555,3 +555,34 @@ def test_persistent_high_load(oracle):
             runner.wait(k)
     finally:
         runner.close()
+
+
+@pytest.mark.timeout(180)
+def test_runner_auto_mode(workloads, expected):
+    """persistent="auto": the persistent kernel where the step is one track
+    launch, graph launches otherwise (raw images); both give the oracle's
+    results."""
+    from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    for raw, want in ((False, True), (True, False)):
+        pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=(cap_kp + 31) // 32 * 32,
+                               cap_points=5120, pyramid_geometry=w0.pyr_left, raw_images=raw)
+                 for _ in range(2)]
+        staged = []
+        for k in range(2):
+            w = workloads[k]
+            pipes[0].load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                                slots=expected[k][1])
+            staged.append(pipes[0].staged_inputs())
+        runner = AsyncRunner(pipes, persistent="auto")
+        try:
+            assert runner.persistent == want
+            for k in range(4):
+                if k >= 2:
+                    _check_one(runner.wait(k - 2), workloads, expected, (k - 2) % 2)
+                runner.submit(k, staged[k % 2])
+            for k in (2, 3):
+                _check_one(runner.wait(k), workloads, expected, k % 2)
+        finally:
+            runner.close()
