@@ -176,16 +176,28 @@ __device__ int block_exclusive_scan(int v, int *tmp, int &total) {
 // (callers fold that into an earlier barrier).  Three block barriers: after
 // counting, after the single-warp scan, after the scatter.  Order inside a
 // bin is arbitrary (atomics); every consumer reduces order-independently.
+// With scan_tmp (32 ints) and nbins <= NT the bin counts are scanned by the
+// whole block (one bin per thread) instead of one warp walking nbins/32 bins
+// per lane.
 template <int NT, typename BinFn>
 __device__ void block_csr(int n, int nbins, BinFn bin_of, int *start, int *cursor,
-                          uint16_t *items, uint16_t *binbuf) {
+                          uint16_t *items, uint16_t *binbuf, int *scan_tmp = nullptr) {
     for (int j = threadIdx.x; j < n; j += NT) {
         const int b = bin_of(j);
         binbuf[j] = (uint16_t)b;
         atomicAdd(&cursor[b], 1);
     }
     __syncthreads();
-    if (threadIdx.x < 32) {  // one warp scans the bin counts
+    if (scan_tmp && nbins <= NT) {
+        const int c = threadIdx.x < nbins ? cursor[threadIdx.x] : 0;
+        int total;
+        const int ex = block_exclusive_scan<NT>(c, scan_tmp, total);
+        if (threadIdx.x < nbins) {
+            start[threadIdx.x] = ex;
+            cursor[threadIdx.x] = ex;
+        }
+        if (threadIdx.x == 0) start[nbins] = total;
+    } else if (threadIdx.x < 32) {  // one warp scans the bin counts
         const int lane = threadIdx.x;
         const int per = (nbins + 31) / 32, b0 = lane * per;
         int local = 0;

@@ -834,7 +834,8 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
                     long long r = round_half_even(sm.rtab[j].v);  // np.round: half-even
                     return (int)(r < 0 ? 0 : (r > H - 1 ? H - 1 : r));
                 },
-                sm.row_start, sm.row_cursor, sm.items, sm.binbuf);
+                sm.row_start, sm.row_cursor, sm.items, sm.binbuf,
+                sm.scan_tmp);
         }
         TL_MARK(a, 1);
         if (!do_p1) __syncthreads();  // ticket in misc[6]
@@ -1448,7 +1449,8 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                 cy = cy < 0 ? 0 : (cy > ny - 1 ? ny - 1 : cy);
                 return (int)(cy * nx + cx);
             },
-            sm.cell_start, sm.cell_cursor, sm.items, sm.binbuf);
+            sm.cell_start, sm.cell_cursor, sm.items, sm.binbuf,
+            sm.scan_tmp);
         TL_MARK(a, 1);
         const double *R = sm.pose, *T = sm.pose + 9;
         const double ccx = -(R[0] * T[0] + R[3] * T[1] + R[6] * T[2]);
