@@ -556,3 +556,27 @@ def test_rejection_median_large_sads(oracle):
     got = ft.compute_stereo_matches(w.left, w.right, w.cam, cfg, w.scale_pow, w.pyr_left, pr)
     for f in FIELDS:
         np.testing.assert_array_equal(getattr(got, f), getattr(ref, f), err_msg=f)
+
+
+@pytest.mark.parametrize("tail", [False, True])
+@pytest.mark.parametrize("amp", [60, 70, 75])
+def test_rejection_median_near_histogram_edge(oracle, amp, tail, monkeypatch):
+    """Medians around the group histograms' fine range (4096): right-image
+    noise of +-amp puts the median SAD at ~3.6k / ~4.0k (hundreds of SADs in
+    the overflow bin, median still resolved by the histograms) / above 4096
+    (gather fallback); every case bit-exact with the oracle, with the group
+    barrier path and with the dedicated tail block (persistent plans' mode)."""
+    from copy import deepcopy
+    if tail:
+        monkeypatch.setenv("FT_TAIL_LAUNCH", "1")
+    from paper_2509_10757_b200.synthetic import make_workload
+    w = make_workload(seed=51, n_landmarks=12000, map_points=1000, images=True)
+    pr = deepcopy(w.pyr_right)
+    rng = np.random.default_rng(3)
+    noise = rng.integers(-amp, amp + 1, size=pr.data.shape)
+    pr.data = np.clip(pr.data.astype(np.int32) + noise, 0, 255).astype(np.uint8)
+    cfg = StereoMatchConfig()
+    ref = oracle.stereo_pinhole(w.left, w.right, w.pyr_left, pr, w.cam, cfg, w.scale_pow)
+    got = ft.compute_stereo_matches(w.left, w.right, w.cam, cfg, w.scale_pow, w.pyr_left, pr)
+    for f in FIELDS:
+        np.testing.assert_array_equal(getattr(got, f), getattr(ref, f), err_msg=f)
