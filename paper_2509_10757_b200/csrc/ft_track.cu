@@ -39,6 +39,12 @@
 //   stale claims from earlier launches always lose (no reset pass).  After a
 //   group barrier each block resolves its own points; ordered outputs use
 //   one more barrier for the cross-block prefix.
+// Persistent mode (track_persist_kernel; ft_runner_create_persistent,
+//   ft_track_frames_ring): one launch steps through a ring of frame slots;
+//   its plans add a dedicated tail block to each role (stereo median /
+//   rejection / count, map resolve / slot writes), so the keypoint and point
+//   blocks publish their results with release reductions and move on to the
+//   next frame instead of waiting at group barriers.
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
