@@ -2461,7 +2461,11 @@ extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsig
     cudaError_t e = cudaMalloc(&args, sizeof(TrackArgs) * n);
     if (e != cudaSuccess) return (int)e;
     *args_out = args;
-    static std::vector<TrackArgs> host;  // must outlive the async copy: synchronised below
+    // staging for the argument copy (pageable: the copy is staged before it
+    // returns); one at a time across threads
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    static std::vector<TrackArgs> host;
     const int st = persist_launch(plans, n, args, host, h_ready, flags, h_done,
                                   flags + PERSIST_MAX_SLOTS, 0xffffffffu, 0, stream);
     return st;
