@@ -1950,11 +1950,14 @@ static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft
     // (persistent plans: the keypoint / point blocks go straight on to the
     // next step; a single launch gains nothing from it -- the kernel still
     // ends with the tail -- so per-launch calls keep the group barriers)
+    // grid limit with the tail blocks: persistent plans keep 4 SMs free
+    // (ft_internal_persist_launch / ft_track_frames_ring refuse more)
+    int sms_all = 0;
+    cudaDeviceGetAttribute(&sms_all, cudaDevAttrMultiProcessorCount, dev);
+    const int grid_max = key.reserve ? sms_all - 4 : sms_all;
     tails = tails || getenv("FT_TAIL_LAUNCH");
     if (tails && want_stereo && a.W >= a.F && !getenv("FT_STEREO_BARRIER")) {
-        int sms = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (a.W * (a.Gs + 1 + a.Gm) <= sms) {
+        if (a.W * (a.Gs + 1 + a.Gm) <= grid_max) {
             a.Gs += 1;
             a.stereo_tail = 1;
         }
@@ -1965,9 +1968,7 @@ static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft
     if (tails && want_map && a.W >= a.F && (a.pmode & FT_PROJ_RESOLVE) && !a.po.corr_point &&
         !((a.pmode & FT_PROJ_ROTATION) && a.io.ref_angles) && a.map_chunk_cap > a.Gm + 1 &&
         a.Gm + 1 <= WS_MAX_GROUP && !getenv("FT_MAP_BARRIER")) {
-        int sms = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (a.W * (a.Gs + a.Gm + 1) <= sms) {
+        if (a.W * (a.Gs + a.Gm + 1) <= grid_max) {
             a.Gm += 1;
             a.map_tail = 1;
         }

@@ -586,3 +586,39 @@ def test_runner_auto_mode(workloads, expected):
                 _check_one(runner.wait(k), workloads, expected, k % 2)
         finally:
             runner.close()
+
+
+@pytest.mark.timeout(180)
+def test_resident_ring_multi_stream(workloads, expected):
+    """ft_track_frames_ring over 3 pipelines of 2 streams each (2 frames per
+    step: group barriers inside the persistent kernel, no tail blocks):
+    every pipeline's outputs equal the oracle's."""
+    import torch
+    from paper_2509_10757_b200.pipeline import FramePipeline, run_ring
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    pipes = [FramePipeline(w0.cam, n_streams=2, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left, packed_upload=False)
+             for _ in range(3)]
+    for i, p in enumerate(pipes):
+        for s in range(2):
+            j = (i + s) % 4
+            w = workloads[j]
+            p.load_frame(s, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                         slots=expected[j][1])
+        p.dev[:p.in_end].copy_(p.host[:p.in_end])
+    torch.cuda.synchronize()
+    run_ring(pipes, 7)
+    pipes[0].synchronize()
+    for i, p in enumerate(pipes):
+        p.copy_outputs()
+        for s in range(2):
+            j = (i + s) % 4
+            w = workloads[j]
+            m, _, slots, n = expected[j]
+            res = p.result(s, len(w.left.u))
+            for f in FIELDS:
+                np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f),
+                                              err_msg=f"pipe {i} stream {s} {f}")
+            np.testing.assert_array_equal(res.slots, slots)
+            assert res.n_slots == n
