@@ -32,7 +32,7 @@ from pathlib import Path
 import numpy as np
 
 ROOT = Path(__file__).resolve().parent
-sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
@@ -71,7 +71,7 @@ def parse() -> argparse.Namespace:
 def make_frames(n: int, seed0: int, images: bool):
     """n independent cfg2 frames (distinct worlds: map point ids offset per
     frame so they can share one resident map table)."""
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     return [make_workload(seed=seed0 + i, n_landmarks=12000, map_points=5000, images=images,
                           offset=0.05 * i, id_base=100_000 * (i + 1)) for i in range(n)]
 
@@ -866,7 +866,7 @@ def hamming_roofline(torch, _lib, popc_peak_g) -> dict:
     Hamming, the algorithmic count) over the measured POPC peak -- the north
     star's integer-pipe roofline target for the Hamming kernels."""
     from paper_2509_10757_b200.runtime import fill_kp_records, make_workspace
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     from paper_2509_10757_b200.types import StereoMatchConfig
     w = make_workload(seed=700, n_landmarks=4800, map_points=100, fisheye=True)
     nl, nr = len(w.left.u), len(w.right.u)
@@ -923,7 +923,7 @@ def other_configs(args, torch, flush) -> dict:
     and 64 streams per launch, local maps resident in a MapTable."""
     from paper_2509_10757_b200.maptable import MapTable
     from paper_2509_10757_b200.pipeline import FisheyePipeline, FramePipeline
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     steps = max(10, args.steps // 2)
     out = {}
     fw = [make_workload(seed=700 + i, n_landmarks=4800, map_points=3050, fisheye=True,

@@ -86,7 +86,7 @@ struct TrackArgs {
     // workspace
     unsigned long long *bar_s;   // [W][2]
     unsigned long long *bar_m;   // [W][2]
-    unsigned long long *ep_m;    // [W] map-group instance tickets (group_ticket)
+    unsigned long long *ep_m;    // [F] claim epochs per claims row (group_ticket)
     unsigned long long *ep_s;    // [W] stereo-group instance tickets
     unsigned *med;               // [W][3][MED_WS] SAD-median histograms
     unsigned long long *tail_s;  // [W] stereo-group arrivals (tail mode)
@@ -99,6 +99,13 @@ struct TrackArgs {
     int *blk_counts;             // [F][Gm]
     int *hist;                   // [F][TK_MAX_BINS]
     unsigned long long *tl;      // optional timeline [grid][TL_SLOTS] (FT_DEBUG_TIMELINE)
+    // 1 when the inputs may be rewritten while the kernel is alive (the
+    // persistent runner's H2D copies between steps): per-step inputs are then
+    // read with coherent loads (ld.global.ca, ordered by the step's acquire)
+    // instead of the read-only path (ld.global.nc), which PTX defines only
+    // for data that stays constant for the kernel's lifetime.
+    int32_t coherent;
+    int32_t pad_;
 };
 
 constexpr int TL_SLOTS = 16;
@@ -114,6 +121,12 @@ FT_DEV unsigned long long global_ns() {
     do {                                                                            \
         if ((a).tl && threadIdx.x == 0) (a).tl[blockIdx.x * TL_SLOTS + (k)] = global_ns(); \
     } while (0)
+
+// Per-step input load: read-only path unless the launch is coherent (above).
+template <typename T>
+FT_DEV T ld_in(const TrackArgs &a, const T *p) {
+    return a.coherent ? __ldca(p) : __ldg(p);
+}
 
 // ---------------------------------------------------------------------------
 // group barrier among the G blocks of one role in one slot: one 64-bit
@@ -302,6 +315,17 @@ FT_DEV LeftKp load_left(const TrackArgs &a, int64_t lk) {
     // volatile: issued where written (the prefetch before the TMA wait must
     // not be sunk to the first use by the compiler)
     const ft_kp_record *r = a.L.rec + lk;
+    if (a.coherent) {
+        asm volatile("ld.global.ca.v2.f64 {%0, %1}, [%2];" : "=d"(k.u), "=d"(k.v) : "l"(r));
+        asm volatile("ld.global.ca.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(k.d.lo.x), "=r"(k.d.lo.y), "=r"(k.d.lo.z), "=r"(k.d.lo.w)
+                     : "l"(r->desc));
+        asm volatile("ld.global.ca.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(k.d.hi.x), "=r"(k.d.hi.y), "=r"(k.d.hi.z), "=r"(k.d.hi.w)
+                     : "l"(r->desc + 2));
+        asm volatile("ld.global.ca.s32 %0, [%1];" : "=r"(k.o) : "l"(&r->octave));
+        return k;
+    }
     asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(k.u), "=d"(k.v) : "l"(r));
     asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(k.d.lo.x), "=r"(k.d.lo.y), "=r"(k.d.lo.z), "=r"(k.d.lo.w)
@@ -504,7 +528,7 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
             for (int q = 0; q < LPL; ++q) {
                 const int t = lane + 32 * q;
                 const int dy = t / nw, dx = t - dy * nw;
-                lreg[q] = t < nw * nw ? __ldg(g.lp + (g.yi - hw + dy) * g.wl + (g.xi - hw + dx)) : 0;
+                lreg[q] = t < nw * nw ? ld_in(a, g.lp + (g.yi - hw + dy) * g.wl + (g.xi - hw + dx)) : 0;
             }
         }
     }
@@ -528,7 +552,7 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
     double disp = 0.0, ur = 0.0;
     int sad = 0;
     if (cand >= 0 && cand < n_right) {
-        const double urc = do_p1 ? sm.rtab[cand].u : __ldg(&a.R.rec[rbase + cand].u);
+        const double urc = do_p1 ? sm.rtab[cand].u : ld_in(a, &a.R.rec[rbase + cand].u);
         if (do_ref) {
             if (g.left_ok) {
                 const long long xr0 = round_half_even(urc / g.s);
@@ -543,7 +567,7 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
                             const int t = lane + 32 * q;
                             const int dy = t / nr, dx = t - dy * nr;
                             rreg[q] = t < nw * nr
-                                          ? __ldg(g.rp + (g.yi - hw + dy) * g.wr + (xr0 - hs - hw + dx))
+                                          ? ld_in(a, g.rp + (g.yi - hw + dy) * g.wr + (xr0 - hs - hw + dx))
                                           : 0;
                         }
                         const int c_idx = hw * nw + hw;  // centre pixel of the left patch
@@ -559,14 +583,14 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
                             if (t < nw * nr) pr[t] = rreg[q];
                         }
                     } else {
-                        const int cl = __ldg(g.lp + g.yi * g.wl + g.xi);
+                        const int cl = ld_in(a, g.lp + g.yi * g.wl + g.xi);
                         for (int t = lane; t < nw * nw; t += 32) {
                             const int dy = t / nw, dx = t - dy * nw;
-                            pl[t] = (int)__ldg(g.lp + (g.yi - hw + dy) * g.wl + (g.xi - hw + dx)) - cl;
+                            pl[t] = (int)ld_in(a, g.lp + (g.yi - hw + dy) * g.wl + (g.xi - hw + dx)) - cl;
                         }
                         for (int t = lane; t < nw * nr; t += 32) {
                             const int dy = t / nr, dx = t - dy * nr;
-                            pr[t] = __ldg(g.rp + (g.yi - hw + dy) * g.wr + (xr0 - hs - hw + dx));
+                            pr[t] = ld_in(a, g.rp + (g.yi - hw + dy) * g.wr + (xr0 - hs - hw + dx));
                         }
                     }
                     if (tlw && lane == 0) a.tl[blockIdx.x * TL_SLOTS + 10] = global_ns();
@@ -964,7 +988,12 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
             atomicAdd(&sm.misc[4], cnt);
             atomicMax(reinterpret_cast<unsigned *>(&sm.misc[5]), vmax);
         }
-        __syncthreads();
+        // Every block must have gathered the frame's values before any block
+        // writes its rejections below (a lagging block would otherwise read
+        // right_idx = -1 / sad = 0 of another block's slice and compute a
+        // different median).  Uniform across the group: med_done is decided
+        // from the same histogram in every block.
+        group_barrier(bar, G, bpar);  // includes the block barriers
         TL_MARK(a, 13);
         const int nm = sm.misc[4];
         if (nm > 0) {
@@ -1176,7 +1205,7 @@ FT_DEV void gather_points(const TrackArgs &a, const MapSmem &sm, const int32_t *
     uint4 *dst = reinterpret_cast<uint4 *>(sm.prnd);
     for (int t = threadIdx.x; t < 7 * (q1 - q0); t += TK_THREADS) {
         const int r = t / 7;
-        dst[t] = __ldg(reinterpret_cast<const uint4 *>(a.P.rec + __ldg(pidx + q0 + r)) + (t - 7 * r));
+        dst[t] = ld_in(a, reinterpret_cast<const uint4 *>(a.P.rec + ld_in(a, pidx + q0 + r)) + (t - 7 * r));
     }
 }
 
@@ -1349,7 +1378,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     // critical path (cold HBM), with the other first-touch loads
     if (threadIdx.x >= TK_THREADS - 12) {
         const int t = threadIdx.x - (TK_THREADS - 12);
-        sm.pose[t] = t < 9 ? __ldg(a.io.rot + 9 * (int64_t)f + t) : __ldg(a.io.trans + 3 * (int64_t)f + t - 9);
+        sm.pose[t] = t < 9 ? ld_in(a, a.io.rot + 9 * (int64_t)f + t) : ld_in(a, a.io.trans + 3 * (int64_t)f + t - 9);
     }
 
     TL_MARK(a, 0);
@@ -1373,11 +1402,14 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                 const uint4 *s = src + t;
                 if (pidx) {
                     const int r = t / 7;
-                    s = reinterpret_cast<const uint4 *>(a.P.rec + __ldg(pidx + p0 + r)) + (t - 7 * r);
+                    s = reinterpret_cast<const uint4 *>(a.P.rec + ld_in(a, pidx + p0 + r)) + (t - 7 * r);
                 }
-                asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(pre[q].x), "=r"(pre[q].y), "=r"(pre[q].z), "=r"(pre[q].w)
-                             : "l"(s));
+                if (a.coherent)
+                    pre[q] = __ldca(s);
+                else
+                    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(pre[q].x), "=r"(pre[q].y), "=r"(pre[q].z), "=r"(pre[q].w)
+                                 : "l"(s));
             }
         }
     } else if (pidx && have_pts) {
@@ -1403,9 +1435,12 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
         if (bsl) bulk_g2s(sm.kslots, a.io.slots_in + kbase, bsl, mbar);
         if (!pre_regs && !pidx) stage_points(a, sm, pbase, p0, min(p1, p0 + round_cap), mbar + 1);
     }
-    // launch epoch (same for every block of this slot's frame instance)
+    // claim epoch of this frame instance, the same for every block of the
+    // group.  Keyed by the claims row (frame f), not by the group slot: the
+    // row's epochs then grow monotonically whatever geometry (W) earlier
+    // launches on this workspace used, so stale claims always lose.
     unsigned ticket = 0;
-    if (threadIdx.x == 0 && resolve) ticket = group_ticket(a.ep_m + slot, G);
+    if (threadIdx.x == 0 && resolve) ticket = group_ticket(a.ep_m + f, G);
     if (rank == 0 && threadIdx.x == 0) {
         if (a.po.slot_count) a.po.slot_count[f] = 0;
         if (a.po.corr_count) a.po.corr_count[f] = 0;
@@ -1417,7 +1452,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     if (write_slots) {  // slots_out <- slots_in (this block's share)
         const int sc = (n_kp + G - 1) / G, s0 = rank * sc, s1 = min(n_kp, s0 + sc);
         for (int k = s0 + threadIdx.x; k < s1; k += TK_THREADS) {
-            const long long v = __ldg(a.io.slots_in + kbase + k);
+            const long long v = ld_in(a, a.io.slots_in + kbase + k);
             if (a.io.slots_out != a.io.slots_in) a.io.slots_out[kbase + k] = v;
             prefilled += v != NO_PID;
         }
@@ -1532,7 +1567,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                     sm.res[i - p0] = kp | (d << 16) | (q.lvl << 25);
                     sm.res_pid[i - p0] = qpid;
                     if (write_slots)
-                        sm.res_empty[i - p0] = __ldg(a.io.slots_in + kbase + kp) == NO_PID;
+                        sm.res_empty[i - p0] = ld_in(a, a.io.slots_in + kbase + kp) == NO_PID;
                     if (resolve)
                         atomicMin(a.claims + kbase + kp, ((unsigned long long)epoch_hi << 32) |
                                                              ((unsigned long long)d << 23) |
@@ -2389,7 +2424,7 @@ extern "C" void ft_internal_persist_dump(void) {
 static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
                           std::vector<TrackArgs> &host_args, const unsigned *ready,
                           unsigned *dready, unsigned *done, unsigned *arrive, unsigned max_steps,
-                          int gate, cudaStream_t stream) {
+                          int gate, int coherent, cudaStream_t stream) {
     if (!plans || !args_dev || !ready || !dready || !done || !arrive) return FT_E_NULL;
     if (n < 1) return FT_E_RANGE;
     PersistArgs p;
@@ -2401,6 +2436,7 @@ static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
         if (!tp) return FT_E_NULL;
         if (tp->magic != PLAN_MAGIC) return FT_E_CONFIG;
         host_args[i] = tp->a;
+        host_args[i].coherent = coherent;
         if (tp->a.W != host_args[0].W || tp->a.Gs != host_args[0].Gs ||
             tp->a.Gm != host_args[0].Gm)
             return FT_E_CONFIG;
@@ -2467,8 +2503,9 @@ extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsig
     static std::mutex mu;
     std::lock_guard<std::mutex> lock(mu);
     static std::vector<TrackArgs> host;
+    // the runner rewrites a slot's inputs while the kernel is alive: coherent loads
     const int st = persist_launch(plans, n, args, host, h_ready, flags, h_done,
-                                  flags + PERSIST_MAX_SLOTS, 0xffffffffu, 0, stream);
+                                  flags + PERSIST_MAX_SLOTS, 0xffffffffu, 0, 1, stream);
     return st;
 }
 
@@ -2477,42 +2514,60 @@ extern "C" int ft_track_frames_ring(int32_t n_plans, const void *const *plans, i
     if (!plans) return FT_E_NULL;
     if (n_plans < 1 || n_steps < 0 || n_steps >= 0x7f000000) return FT_E_RANGE;
     if (n_steps == 0) return FT_OK;
-    // per-process buffers, grown on demand (stream-ordered reuse)
+    // per-device buffers, grown on demand (stream-ordered reuse)
+    struct RingState {
+        TrackArgs *args = nullptr;
+        unsigned *words = nullptr;
+        int cap = 0;
+        std::vector<TrackArgs> host;
+        cudaEvent_t prev = nullptr;  // the previous ring on this device
+    };
     static std::mutex mu;
+    static RingState states[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return FT_E_CONFIG;
     std::lock_guard<std::mutex> lock(mu);
-    static TrackArgs *args = nullptr;
-    static unsigned *words = nullptr;
-    static int cap = 0;
-    static std::vector<TrackArgs> host;
+    RingState &rs = states[dev];
     cudaStream_t s = (cudaStream_t)stream;
-    if (n_plans > cap) {
-        cudaStreamSynchronize(s);
-        if (args) cudaFree(args);
-        if (words) cudaFree(words);
-        args = nullptr;
-        words = nullptr;
-        cap = 0;
-        cudaError_t e = cudaMalloc(&args, sizeof(TrackArgs) * n_plans);
-        if (e == cudaSuccess) e = cudaMalloc(&words, 4 * sizeof(unsigned) * n_plans);
-        if (e != cudaSuccess) return (int)e;
-        cap = n_plans;
+    cudaError_t e = cudaSuccess;
+    if (!rs.prev) {
+        e = cudaEventCreateWithFlags(&rs.prev, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            rs.prev = nullptr;
+            return (int)e;
+        }
     }
-    // the buffers are shared by every call: order after the previous ring,
-    // whatever stream it ran on
-    static cudaEvent_t prev = nullptr;
-    if (!prev && cudaEventCreateWithFlags(&prev, cudaEventDisableTiming) != cudaSuccess)
-        return FT_E_CONFIG;
-    cudaStreamWaitEvent(s, prev, 0);
+    if (n_plans > rs.cap) {
+        // the old buffers may still be read by the previous ring
+        e = cudaEventSynchronize(rs.prev);
+        if (e != cudaSuccess) return (int)e;
+        if (rs.args) cudaFree(rs.args);
+        if (rs.words) cudaFree(rs.words);
+        rs.args = nullptr;
+        rs.words = nullptr;
+        rs.cap = 0;
+        e = cudaMalloc(&rs.args, sizeof(TrackArgs) * n_plans);
+        if (e == cudaSuccess) e = cudaMalloc(&rs.words, 4 * sizeof(unsigned) * n_plans);
+        if (e != cudaSuccess) return (int)e;
+        rs.cap = n_plans;
+    }
+    // the buffers are shared by every call on this device: order after the
+    // previous ring, whatever stream it ran on
+    e = cudaStreamWaitEvent(s, rs.prev, 0);
+    if (e != cudaSuccess) return (int)e;
     // [ready | dready | done | arrive]: every step ready up front
-    cudaError_t e = cudaMemsetAsync(words, 0x7f, sizeof(unsigned) * n_plans, s);
+    unsigned *words = rs.words;
+    e = cudaMemsetAsync(words, 0x7f, sizeof(unsigned) * n_plans, s);
     if (e == cudaSuccess)
         e = cudaMemsetAsync(words + n_plans, 0, 3 * sizeof(unsigned) * n_plans, s);
     if (e != cudaSuccess) return (int)e;
-    const int st = persist_launch(plans, n_plans, args, host, words, words + n_plans,
+    // inputs are resident and constant for the launch: read-only loads
+    const int st = persist_launch(plans, n_plans, rs.args, rs.host, words, words + n_plans,
                                   words + 2 * n_plans, words + 3 * n_plans, (unsigned)n_steps,
-                                  1, s);
-    if (st == FT_OK) cudaEventRecord(prev, s);
-    return st;
+                                  1, 0, s);
+    if (st != FT_OK) return st;
+    e = cudaEventRecord(rs.prev, s);
+    return e == cudaSuccess ? FT_OK : (int)e;
 }
 
 extern "C" int ft_stereo_pinhole(int32_t n_frames, const ft_keypoints *left,

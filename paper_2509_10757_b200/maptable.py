@@ -39,8 +39,8 @@ class MapTable:
         self._slot = np.empty(0, dtype=np.int32)   # slot of _ids[k]
         self.size = 0
         self.bytes_uploaded = 0
-        self._h_rec = None
-        self._h_slot = None
+        self._retired: list[int] = []   # slots of rewritten records (in-flight readers)
+        self._free: list[int] = []      # reusable slots (after reclaim())
 
     @property
     def ptr(self) -> int:
@@ -64,40 +64,52 @@ class MapTable:
         return s
 
     def upsert(self, point_ids, soa, only_missing: bool = False) -> int:
-        """Upload the records of the given points (new ids get fresh slots,
-        present ids are overwritten unless only_missing).  Returns the bytes
-        copied host -> device.  Synchronous on the table's stream."""
+        """Upload the records of the given points.  Returns the bytes copied
+        host -> device.  Synchronous on the table's stream.
+
+        New ids get fresh slots.  Present ids (unless only_missing) are
+        rewritten copy-on-write: the new record goes to a fresh slot and the
+        id's old slot is retired, never overwritten in place -- a step that
+        was submitted earlier (its slot list taken before this call) may
+        still be reading the old record on another stream.  Retired slots
+        are reused only after ``reclaim()``, which the caller issues once
+        every step submitted before the upsert has completed (the reference
+        likewise finishes a frame's search before the map changes)."""
         ids = np.asarray(point_ids, dtype=np.int64)
         n = len(ids)
         if n == 0:
             return 0
         slots = self._lookup(ids)
         new = slots < 0
-        if only_missing:
-            keep = np.nonzero(new)[0]
-        else:
-            keep = np.arange(n)
+        keep = np.nonzero(new)[0] if only_missing else np.arange(n)
         if len(keep) == 0:
             return 0
-        n_new = int(new.sum())
-        if n_new:
-            if self.size + n_new > self.capacity:
-                raise _lib.FtError(f"map table full ({self.capacity} points)")
-            new_ids, first = np.unique(ids[new], return_index=True)
-            fresh = np.arange(self.size, self.size + len(new_ids), dtype=np.int32)
-            self.size += len(new_ids)
-            allids = np.concatenate([self._ids, new_ids])
-            allslots = np.concatenate([self._slot, fresh])
-            order = np.argsort(allids, kind="stable")
-            self._ids, self._slot = allids[order], allslots[order]
-            slots = self._lookup(ids)
+        # one record per distinct id (the last occurrence wins, as a serial
+        # overwrite would)
+        kids = ids[keep]
+        _, last_rev = np.unique(kids[::-1], return_index=True)
+        keep = keep[np.sort(len(kids) - 1 - last_rev)]
+        kids = ids[keep]
+        old = self._lookup(kids)
+        fresh = self._alloc(len(kids))
+        if (old >= 0).any():
+            self._retired.extend(int(x) for x in old[old >= 0])
+        # id -> slot map: drop the rewritten ids, add every uploaded id
+        present = old >= 0
+        if present.any():
+            drop = np.isin(self._ids, kids[present])
+            self._ids, self._slot = self._ids[~drop], self._slot[~drop]
+        allids = np.concatenate([self._ids, kids])
+        allslots = np.concatenate([self._slot, fresh])
+        order = np.argsort(allids, kind="stable")
+        self._ids, self._slot = allids[order], allslots[order]
         k = len(keep)
         rec = np.zeros(k, dtype=_lib.POINT_RECORD)
         sub = _SubSoA(soa, keep)
         fill_point_records(rec, sub)
-        rec["id"][:] = ids[keep]
+        rec["id"][:] = kids
         host_rec = torch.from_numpy(rec.view(np.uint8)).pin_memory()
-        host_slot = torch.from_numpy(slots[keep].astype(np.int32)).pin_memory()
+        host_slot = torch.from_numpy(fresh.astype(np.int32)).pin_memory()
         with torch.cuda.stream(self.stream):
             d_rec = host_rec.to(self.device, non_blocking=True)
             d_slot = host_slot.to(self.device, non_blocking=True)
@@ -108,6 +120,27 @@ class MapTable:
         nbytes = host_rec.numel() + host_slot.numel() * 4
         self.bytes_uploaded += nbytes
         return nbytes
+
+    def _alloc(self, k: int) -> np.ndarray:
+        """k slots: recycled ones first, then never-used ones."""
+        take = min(k, len(self._free))
+        out = [self._free.pop() for _ in range(take)]
+        rest = k - take
+        if self.size + rest > self.capacity:
+            self._free.extend(reversed(out))
+            raise _lib.FtError(f"map table full ({self.capacity} points)")
+        out.extend(range(self.size, self.size + rest))
+        self.size += rest
+        return np.asarray(out, dtype=np.int32)
+
+    def reclaim(self) -> int:
+        """Make the slots retired by earlier upserts reusable.  Call only once
+        every step that may read them (submitted before those upserts) has
+        completed.  Returns the number of slots recycled."""
+        n = len(self._retired)
+        self._free.extend(self._retired)
+        self._retired = []
+        return n
 
 
 class _SubSoA:

@@ -320,7 +320,9 @@ def search_prev_frame(prev, cur, pose, world, cam, cfg: ProjectionSearchConfig, 
     slotted points are decomposed on the host (mapping.py:204-235), as in the
     reference; with a resident MapTable only points missing from the table
     are decomposed and uploaded (the map delta) and the search reads the rest
-    in place (SURVEY 8(f) #2)."""
+    in place.  soa_out, when given (the tracker's pooled
+    buffers, tracker.py:304-314), receives the decomposed points as in the
+    reference and the returned point ids are a view of it."""
     from .types import MapPointSoA
     slot_idx = np.nonzero(prev.slots != NO_POINT)[0]
     if len(slot_idx) == 0:
@@ -339,7 +341,17 @@ def search_prev_frame(prev, cur, pose, world, cam, cfg: ProjectionSearchConfig, 
 
     if table is None:
         points = decompose(pids)
+        if soa_out is not None:  # reference: decompose_map_points(mps, out=soa_out)
+            k = len(pids)
+            for name in ("positions", "descriptors", "normals", "min_distances",
+                         "max_distances", "point_ids"):
+                getattr(soa_out, name)[:k] = getattr(points, name)
+            points = MapPointSoA(*(getattr(soa_out, name)[:k] for name in
+                                   ("positions", "descriptors", "normals", "min_distances",
+                                    "max_distances", "point_ids")))
     else:
+        # resident mode: the points are read in place from the table, nothing
+        # is decomposed, soa_out is left untouched
         missing = pids[table._lookup(pids) < 0]
         if len(missing):
             table.upsert(missing, decompose(missing))

@@ -376,14 +376,398 @@ def gen_edge() -> dict:
                      "median_counts": sads}}
 
 
+# Non-default configs (tests/test_gpu_parity.py STEREO_CFGS / PROJ_CFGS).
+STEREO_SWEEP = [
+    dict(t_match=40),
+    dict(band_factor=1.0, half_window=3, half_slide=3),
+    dict(band_factor=3.5, half_window=7, half_slide=8, outlier_multiplier=1.5),
+    dict(min_disparity=2.0, max_disparity=60.0, outlier_multiplier=4.0),
+    dict(t_match=256, half_window=1, half_slide=1, ratio=0.6),
+]
+PROJ_SWEEP = [
+    dict(window_px=2.0, t_proj=50),
+    dict(window_px=12.0, ratio=0.7, view_cos_min=0.9),
+    dict(window_px=30.0, ratio=1.0, view_cos_min=-1.0, t_proj=256),
+    dict(histogram_bins=12, histogram_keep=1),
+]
+SCALES = [(1.2, 8), (1.3, 6), (2.0, 4)]
+
+
+def _load(name):
+    with np.load(OUT / name) as z:
+        return {k: z[k] for k in z.files}
+
+
+def _feats(d, prefix):
+    from trackfront.mapping import FeatureSet
+    return FeatureSet(u=d[f"{prefix}_u"], v=d[f"{prefix}_v"], octave=d[f"{prefix}_octave"],
+                      angle=d[f"{prefix}_angle"], response=d[f"{prefix}_response"],
+                      descriptors=d[f"{prefix}_desc"])
+
+
+def _soa(d, prefix="map"):
+    return MapPointSoA(positions=d[f"{prefix}_positions"], descriptors=d[f"{prefix}_descriptors"],
+                       normals=d[f"{prefix}_normals"], min_distances=d[f"{prefix}_min_d"],
+                       max_distances=d[f"{prefix}_max_d"], point_ids=d[f"{prefix}_ids"])
+
+
+def _pyr(d, side, scale=1.2):
+    from trackfront.extraction import ImagePyramid
+    p = f"pyr_{side}"
+    return ImagePyramid(d[f"{p}_data"], d[f"{p}_offsets"], d[f"{p}_widths"],
+                        d[f"{p}_heights"], scale)
+
+
+def _clip_octaves(f, levels):
+    f.octave = np.minimum(np.asarray(f.octave), levels - 1).astype(np.int32)
+    return f
+
+
+def gen_sweeps() -> dict:
+    """The reference on non-default StereoMatchConfig / ProjectionSearchConfig
+    values and pyramid scales, over the committed cfg1 / cfg2 / cfg3 inputs
+    (no new inputs except the scale-1.3 / 2.0 pyramids)."""
+    d1, d2, d3 = _load("cfg1_stereo.npz"), _load("cfg2_frame_map.npz"), _load("cfg3_fisheye.npz")
+    out, summ = {}, {}
+    cam = default_pinhole()
+    l1, r1 = _feats(d1, "left"), _feats(d1, "right")
+    pl, pr = _pyr(d1, "l"), _pyr(d1, "r")
+    l2, r2 = _feats(d2, "left"), _feats(d2, "right")
+    sp = d1["scale_pow"]
+    for k, kw in enumerate(STEREO_SWEEP):
+        cfg = StereoMatchConfig(**kw)
+        # cfg1: phase 1 -> phase 2 -> reject (rendered ORB frame)
+        idx, dist = match_pinhole_phase1(l1, r1, cam.height, sp, cfg, ENGINE)
+        m = reject_outliers(refine_match_phase2(pl, pr, l1, r1, idx, dist, cam, cfg, ENGINE), cfg)
+        out.update(matches_dict(f"s{k}_cfg1", m))
+        # cfg2: phase 1 -> from candidates -> reject (feature bundle)
+        idx2, dist2 = match_pinhole_phase1(l2, r2, cam.height, sp, cfg, ENGINE)
+        m2 = reject_outliers(matches_from_candidates(idx2, dist2, l2, r2, cam, cfg), cfg)
+        out.update(matches_dict(f"s{k}_cfg2", m2))
+        # cfg3 descriptors: fisheye brute force with this t_match / ratio
+        bi = np.empty(len(d3["left_u"]), dtype=np.int64)
+        bd = np.empty(len(d3["left_u"]), dtype=np.int64)
+        kernels.bruteforce_match_kernel(d3["left_desc"], d3["right_desc"], cfg.t_match, cfg.ratio,
+                                        0, len(bi), bi, bd)
+        out.update({f"s{k}_bf_idx": bi, f"s{k}_bf_dist": bd})
+        summ[f"stereo{k}"] = [int((m.right_idx >= 0).sum()), int((m2.right_idx >= 0).sum()),
+                              int((bi >= 0).sum())]
+    soa = _soa(d2)
+    pose = Pose(d2["pose_rot"], d2["pose_trans"])
+    ref_angles = np.random.default_rng(7).uniform(0, 2 * math.pi, len(soa))
+    out["proj_ref_angles"] = ref_angles
+    for k, kw in enumerate(PROJ_SWEEP):
+        pcfg = ProjectionSearchConfig(**kw)
+        for j, (scale, levels) in enumerate(SCALES):
+            # fewer levels: the bundle's octaves clipped into the pyramid
+            l2 = _clip_octaves(_feats(d2, "left"), levels)
+            frame = make_frame(0, l2, r2, cam, pose)
+            kp, kd, ko = run_phase_a(soa, frame, pose, cam, pcfg, scale, levels, ENGINE)
+            kp, kd, ko = kp.copy(), kd.copy(), ko.copy()
+            c = search_by_projection(soa, frame, pose, cam, pcfg, scale, levels, ENGINE,
+                                     ref_angles=ref_angles, rotation_check=True, u_offset=-1.0)
+            local = LocalMap((0,), soa.point_ids.copy(), soa)
+            fa = make_frame(0, l2, r2, cam, pose)
+            n = search_local_points(local, fa, cam, pcfg, scale, levels, ENGINE)
+            t = f"p{k}_{j}"
+            out.update({f"{t}_kp": kp, f"{t}_dist": kd, f"{t}_oct": ko, f"{t}_slots": fa.slots.copy(),
+                        f"{t}_count": np.int64(n)})
+            out.update(corr_dict(f"{t}_corr", c))
+            summ[t] = [int((kp >= 0).sum()), len(c), int(n)]
+    np.savez_compressed(OUT / "sweeps.npz", **out)
+    return {"sweeps": summ}
+
+
+def gen_scales() -> dict:
+    """cfg1's rendered pair through the reference ORB extraction at pyramid
+    scale 1.3 / 6 levels and 2.0 / 4 levels, then phase 1 -> 2 -> reject."""
+    scfg = SyntheticSceneConfig(landmark_count=8000, n_frames=2, trajectory="line")
+    seq = generate_synthetic(scfg, seed=11)
+    img_l, img_r = seq.render_pair(0)
+    cam = seq.cam
+    out, summ = {}, {}
+    for j, (scale, levels) in enumerate(SCALES[1:], start=1):
+        ecfg = ExtractionConfig(scale=scale, levels=levels)
+        left, pyr_l = extract_features(img_l, ecfg, ENGINE)
+        right, pyr_r = extract_features(img_r, ecfg, ENGINE)
+        cfg = StereoMatchConfig()
+        sp = ecfg.scale_powers()
+        idx, dist = match_pinhole_phase1(left, right, cam.height, sp, cfg, ENGINE)
+        m = reject_outliers(refine_match_phase2(pyr_l, pyr_r, left, right, idx, dist, cam, cfg,
+                                                ENGINE), cfg)
+        t = f"x{j}"
+        out.update(feats_dict(f"{t}_left", left))
+        out.update(feats_dict(f"{t}_right", right))
+        for side, p in (("l", pyr_l), ("r", pyr_r)):
+            out.update({f"{t}_pyr_{side}_data": p.data.copy(), f"{t}_pyr_{side}_offsets": p.offsets.copy(),
+                        f"{t}_pyr_{side}_widths": p.widths.copy(),
+                        f"{t}_pyr_{side}_heights": p.heights.copy()})
+        out.update({f"{t}_scale_pow": sp, f"{t}_p1_idx": idx.copy(), f"{t}_p1_dist": dist.copy()})
+        out.update(matches_dict(f"{t}_final", m))
+        summ[f"scale{scale}"] = {"levels": levels, "n_left": len(left),
+                                 "octaves": np.bincount(left.octave, minlength=levels).tolist(),
+                                 "p1": int((idx >= 0).sum()), "final": int((m.right_idx >= 0).sum())}
+    np.savez_compressed(OUT / "scales.npz", **out)
+    return {"scales": summ}
+
+
+def gen_cfg5() -> dict:
+    """2073-keypoint frame (landmark_count 20000, seed 3),
+    20000-point local map: stereo (phase 1 + from candidates + reject) and
+    search_local_points with 10 % of the keypoints pre-slotted."""
+    scfg = SyntheticSceneConfig(landmark_count=20000, n_frames=2, trajectory="line",
+                                keypoint_noise_px=0.5)
+    seq = generate_synthetic(scfg, seed=3)
+    cam = seq.cam
+    fr = seq.frames[0]
+    left, right = fr.left, fr.right
+    cfg = StereoMatchConfig()
+    sp = scfg.scale ** np.arange(scfg.levels, dtype=np.float64)
+    idx, dist = match_pinhole_phase1(left, right, cam.height, sp, cfg, ENGINE)
+    m = reject_outliers(matches_from_candidates(idx, dist, left, right, cam, cfg), cfg)
+    soa = build_local_map(seq, 0, cam, 20000, np.random.default_rng(13), scfg)
+    pose = perturbed_pose(seq, 0)
+    pcfg = ProjectionSearchConfig()
+    frame = make_frame(0, left, right, cam, pose)
+    kp, kd, ko = run_phase_a(soa, frame, pose, cam, pcfg, scfg.scale, scfg.levels, ENGINE)
+    kp, kd, ko = kp.copy(), kd.copy(), ko.copy()
+    local = LocalMap((0,), soa.point_ids.copy(), soa)
+    fb = make_frame(0, left, right, cam, pose)
+    prng = np.random.default_rng(29)
+    k = prng.choice(len(left), size=len(left) // 10, replace=False)
+    fb.slots[k] = prng.choice(soa.point_ids, size=len(k), replace=False)
+    slots_in = fb.slots.copy()
+    n = search_local_points(local, fb, cam, pcfg, scfg.scale, scfg.levels, ENGINE)
+    d = {}
+    d.update(feats_dict("left", left))
+    d.update(feats_dict("right", right))
+    d.update(soa_dict("map", soa))
+    d.update(pose_dict("pose", pose))
+    d.update(scale_pow=sp, p1_idx=idx.copy(), p1_dist=dist.copy(), pa_kp=kp, pa_dist=kd,
+             pa_oct=ko, slots_in=slots_in, slots=fb.slots.copy(), count=np.int64(n))
+    d.update(matches_dict("final", m))
+    np.savez_compressed(OUT / "cfg5_high_load.npz", **d)
+    return {"cfg5": {"n_left": len(left), "n_right": len(right), "map": len(soa),
+                     "visible_claims": int((kp >= 0).sum()), "count": int(n),
+                     "stereo_matches": int((m.right_idx >= 0).sum())}}
+
+
+def gen_prev() -> dict:
+    """The reference's own search_prev_frame (projection.py:224-253) on cfg2:
+    the previous frame's slots from its search_local_points, a world map of
+    reference MapPoints, the current pose moved forward (u_offset +1), back
+    (-1) and not at all (0); plus SPEC.md:352-353 static and empty cases."""
+    from trackfront.mapping import MapPoint, WorldMap
+    from trackfront.projection import search_prev_frame
+    d2 = _load("cfg2_frame_map.npz")
+    cam = default_pinhole()
+    l2, r2 = _feats(d2, "left"), _feats(d2, "right")
+    soa = _soa(d2)
+    pose = Pose(d2["pose_rot"], d2["pose_trans"])
+    world = WorldMap()
+    for i, pid in enumerate(soa.point_ids):
+        world.add_point(MapPoint(point_id=int(pid), position=soa.positions[i].copy(),
+                                 descriptor=soa.descriptors[i].copy(),
+                                 normal=soa.normals[i].copy(),
+                                 min_distance=float(soa.min_distances[i]),
+                                 max_distance=float(soa.max_distances[i])))
+    pcfg = ProjectionSearchConfig()
+    out, summ = {}, {}
+    prev = make_frame(0, l2, r2, cam, pose)
+    prev.slots[...] = d2["slots_a"]
+    moves = {"fwd": np.array([0.002, -0.001, 0.004]), "back": np.array([-0.001, 0.002, -0.005]),
+             "static": np.zeros(3)}
+    for name, dt in moves.items():
+        cur_pose = Pose(pose.rotation, pose.translation + dt)
+        cur = make_frame(1, l2, r2, cam, cur_pose)
+        corr, pids = search_prev_frame(prev, cur, cur_pose, world, cam, pcfg, 1.2, 8, ENGINE)
+        out.update(corr_dict(f"{name}", corr))
+        out[f"{name}_pids"] = np.asarray(pids).copy()
+        out[f"{name}_trans"] = cur_pose.translation.copy()
+        summ[name] = len(corr)
+    # SPEC.md:352 static case: every slotted point re-matches its own keypoint
+    st_k = out["static_keypoint_idx"]
+    st_p = out["static_pids"][out["static_point_idx"]]
+    summ["static_self_matches"] = int((prev.slots[st_k] == st_p).sum())
+    empty = make_frame(0, l2, r2, cam, pose)
+    corr, pids = search_prev_frame(empty, make_frame(1, l2, r2, cam, pose), pose, world, cam,
+                                   pcfg, 1.2, 8, ENGINE)
+    summ["empty"] = [len(corr), len(pids)]
+    out["prev_slots"] = prev.slots.copy()
+    np.savez_compressed(OUT / "prev_frame.npz", **out)
+    return {"prev_frame": summ}
+
+
+def digest(*arrays) -> np.ndarray:
+    """sha256 over the raw bytes of the arrays (dtype + shape included), as
+    32 uint8 -- a bit-exact check of outputs too large to commit."""
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype.str).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return np.frombuffer(h.digest(), dtype=np.uint8).copy()
+
+
+def gen_cfg4(trajectory: str) -> dict:
+    """BASELINE configs[3] / SURVEY §8(d) cfg4: the reference StereoTracker
+    over a 100-frame feature-bundle sequence (tracker.py:225-393), every call
+    of the hot-path stage functions captured (inputs, outputs).
+
+    Compact form: keypoint descriptors / angles are the landmarks' (asserted
+    below), so frames store landmark ids + u, v, octave; map points are the
+    world's (immutable once created, ids 0..N-1), so a local map is a bitmask
+    over the world table; outputs too large to commit are sha256 digests
+    (golden_io.digest) next to compact copies of the indices."""
+    import time
+    import trackfront.tracker as T
+    from trackfront.tracker import FrameInput, StereoTracker, TrackerConfig
+    scfg = SyntheticSceneConfig(landmark_count=12000, n_frames=100, trajectory=trajectory,
+                                keypoint_noise_px=0.5)
+    seq = generate_synthetic(scfg, seed=4)
+    n_lm = len(seq.landmarks)
+    rec: dict[int, dict] = {}
+    cur = {"f": -1}
+    orig = {k: getattr(T, k) for k in ("match_pinhole_phase1", "matches_from_candidates",
+                                        "reject_outliers", "search_prev_frame",
+                                        "search_local_points")}
+
+    def slot(name):
+        return rec.setdefault(cur["f"], {}).setdefault(name, {})
+
+    def w_phase1(left, right, height, scale_pow, cfg, engine=None, **kw):
+        idx, dist = orig["match_pinhole_phase1"](left, right, height, scale_pow, cfg, engine, **kw)
+        slot("stereo").update(p1=digest(idx, dist))
+        return idx, dist
+
+    def w_fc(idx, dist, left, right, cam, cfg):
+        m = orig["matches_from_candidates"](idx, dist, left, right, cam, cfg)
+        slot("stereo").update(fc=digest(m.right_idx, m.distance, m.disparity, m.refined_u,
+                                        m.depth, m.sad))
+        return m
+
+    def w_rej(m, cfg):
+        out = orig["reject_outliers"](m, cfg)
+        slot("stereo").update(final=digest(out.right_idx, out.distance, out.disparity,
+                                           out.refined_u, out.depth, out.sad),
+                              right_idx=out.right_idx.astype(np.int16),
+                              distance=out.distance.astype(np.int16))
+        return out
+
+    def w_prev(prev, curf, pose, world, cam, cfg, scale, levels, engine=None, soa_out=None,
+               pool=None):
+        slots_in = prev.slots.copy()
+        corr, pids = orig["search_prev_frame"](prev, curf, pose, world, cam, cfg, scale, levels,
+                                               engine, soa_out=soa_out, pool=pool)
+        slot("prev").update(prev_frame=prev.frame_id, prev_slots=slots_in.astype(np.int32),
+                            prev_pose=np.concatenate([prev.pose.rotation.ravel(),
+                                                      prev.pose.translation]),
+                            pose=np.concatenate([pose.rotation.ravel(), pose.translation]),
+                            n_corr=np.int64(len(corr)),
+                            corr_digest=digest(corr.point_idx, corr.keypoint_idx, corr.distance,
+                                               corr.octave),
+                            pids=digest(pids))
+        return corr, pids
+
+    def w_local(local, frame, cam, cfg, scale, levels, engine=None, world=None, pool=None):
+        before = frame.slots.copy()
+        n = orig["search_local_points"](local, frame, cam, cfg, scale, levels, engine,
+                                        world=world, pool=pool)
+        mask = np.zeros(n_lm * 4, dtype=bool)  # world ids < landmarks x keyframes
+        mask[np.asarray(local.point_ids, dtype=np.int64)] = True
+        slot("local").update(slots_in=before.astype(np.int32), local_ids=local.point_ids.copy(),
+                             pose=np.concatenate([frame.pose.rotation.ravel(),
+                                                  frame.pose.translation]),
+                             slots_out=digest(frame.slots),
+                             count=np.int64(n))
+        return n
+
+    for k, fn in (("match_pinhole_phase1", w_phase1), ("matches_from_candidates", w_fc),
+                  ("reject_outliers", w_rej), ("search_prev_frame", w_prev),
+                  ("search_local_points", w_local)):
+        setattr(T, k, fn)
+    try:
+        tr = StereoTracker(seq.cam, tracker=TrackerConfig(max_local_points=40000),
+                           engine=ENGINE, warmup=False)
+        statuses = []
+        for i in range(len(seq)):
+            cur["f"] = i
+            res = tr.track_frame(FrameInput(timestamp=float(seq.timestamps[i]),
+                                            features=seq.frames[i], imu=seq.imu_slice(i)))
+            statuses.append(res.status)
+    finally:
+        for k, fn in orig.items():
+            setattr(T, k, fn)
+    # world table (ids 0..N-1, immutable after creation)
+    n_pts = len(tr.world.points)
+    assert sorted(tr.world.points) == list(range(n_pts))
+    pts = [tr.world.points[i] for i in range(n_pts)]
+    d = {"world_positions": np.array([p.position for p in pts]),
+         "world_descriptors": np.array([p.descriptor for p in pts], dtype=np.uint64),
+         "world_normals": np.array([p.normal for p in pts]),
+         "world_min_d": np.array([p.min_distance for p in pts]),
+         "world_max_d": np.array([p.max_distance for p in pts]),
+         "landmark_desc": seq.landmark_desc.copy(), "landmark_angle": seq.landmark_angle.copy(),
+         "n_frames": np.int64(len(seq)), "status": np.array(statuses)}
+    lens = []
+    for i, fr in enumerate(seq.frames):
+        for side, f, ids in (("l", fr.left, fr.landmark_ids_left),
+                             ("r", fr.right, fr.landmark_ids_right)):
+            assert (f.descriptors == seq.landmark_desc[ids]).all()
+            assert (f.angle == seq.landmark_angle[ids]).all()
+            assert (f.response == 100.0).all()
+            d[f"f{i}_{side}_ids"] = ids.astype(np.uint16)
+            d[f"f{i}_{side}_uv"] = np.stack([f.u, f.v])
+            d[f"f{i}_{side}_octave"] = f.octave.astype(np.int8)
+        r = rec.get(i, {})
+        for stage, fields in r.items():
+            for k, v in fields.items():
+                if stage == "local" and k == "local_ids":
+                    m = np.zeros(n_pts, dtype=bool)
+                    m[v] = True
+                    d[f"f{i}_local_mask"] = np.packbits(m)
+                    continue
+                d[f"f{i}_{stage}_{k}"] = v
+        lens.append(len(fr.left))
+    np.savez_compressed(OUT / f"cfg4_{trajectory}.npz", **d)
+    micros = {s: [rp.micros.get(s, 0) for rp in tr.reports[1:]] for s in
+              ("stereo_match", "initial_pose", "update_local_map", "search_local_points",
+               "total")}
+    return {f"cfg4_{trajectory}": {
+        "frames": len(seq), "status_counts": {s: statuses.count(s) for s in set(statuses)},
+        "world_points": n_pts, "kps_per_frame_median": int(np.median(lens)),
+        "local_map_median": int(np.median([len(r["local"]["local_ids"]) for r in rec.values()
+                                           if "local" in r])),
+        "stage_us_median_seq_engine": {k: float(np.median(v)) for k, v in micros.items()}}}
+
+
 def main() -> None:
     kernels.warmup()
     summary = {}
+    only = sys.argv[1:]
+    if only:
+        old = json.loads((OUT / "summary.json").read_text())
+        summary.update(old)
+        for name in only:
+            summary.update(globals()[f"gen_{name}"]() if "_" not in name
+                           else globals()[f"gen_{name.split('_')[0]}"](name.split("_", 1)[1]))
+        (OUT / "summary.json").write_text(json.dumps(summary, indent=1))
+        print(json.dumps({k: summary[k] for k in summary if any(k.startswith(o) for o in only)},
+                         indent=1))
+        return
     gen_hamming()
     summary.update(gen_edge())
     summary.update(gen_cfg2())
     summary.update(gen_cfg3())
     summary.update(gen_cfg1())
+    summary.update(gen_cfg4("line"))
+    summary.update(gen_cfg4("circle"))
+    summary.update(gen_sweeps())
+    summary.update(gen_scales())
+    summary.update(gen_cfg5())
+    summary.update(gen_prev())
     summary["generator"] = "tests/golden/make_golden.py (reference trackfront, seq engine)"
     (OUT / "summary.json").write_text(json.dumps(summary, indent=1))
     print(json.dumps(summary, indent=1))

@@ -61,3 +61,96 @@ def fisheye() -> FisheyeCamera:
 def grid_tuple(u, v, cam, cell_px: int = 48):
     g = FrameGrid(u, v, cam.width, cam.height, cell_px)
     return g.start, g.indices, g.nx, g.ny, g.cell_px
+
+
+# ---------------------------------------------------------------------------
+# cfg4: the reference StereoTracker's per-frame stage calls (make_golden.gen_cfg4)
+
+def digest(*arrays) -> np.ndarray:
+    """Same sha256 as make_golden.digest (dtype, shape, raw bytes)."""
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype.str).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return np.frombuffer(h.digest(), dtype=np.uint8).copy()
+
+
+class Cfg4:
+    """One captured 100-frame sequence (trajectory "line" or "circle")."""
+
+    def __init__(self, trajectory: str):
+        self.d = load(f"cfg4_{trajectory}.npz")
+        self.n_frames = int(self.d["n_frames"])
+        self.n_points = len(self.d["world_min_d"])
+        self.cam = pinhole()
+        self._feats = {}
+
+    def has(self, i: int, key: str) -> bool:
+        return f"f{i}_{key}" in self.d
+
+    def get(self, i: int, key: str):
+        return self.d[f"f{i}_{key}"]
+
+    def feats(self, i: int, side: str) -> FeatureSet:
+        """Frame i's left ("l") or right ("r") feature bundle, rebuilt exactly:
+        descriptors / angles are the landmarks' (synthetic.py:160-174)."""
+        key = (i, side)
+        if key not in self._feats:
+            ids = self.get(i, f"{side}_ids").astype(np.int64)
+            uv = self.get(i, f"{side}_uv")
+            n = len(ids)
+            self._feats[key] = FeatureSet(
+                u=uv[0].copy(), v=uv[1].copy(), octave=self.get(i, f"{side}_octave").astype(np.int32),
+                angle=self.d["landmark_angle"][ids].copy(),
+                response=np.full(n, 100.0, dtype=np.float32),
+                descriptors=self.d["landmark_desc"][ids].copy())
+        return self._feats[key]
+
+    def pose(self, i: int, key: str) -> Pose:
+        p = self.get(i, key)
+        return Pose(p[:9].reshape(3, 3).copy(), p[9:].copy())
+
+    def world_soa(self, ids) -> MapPointSoA:
+        ids = np.asarray(ids, dtype=np.int64)
+        d = self.d
+        return MapPointSoA(positions=d["world_positions"][ids], descriptors=d["world_descriptors"][ids],
+                           normals=d["world_normals"][ids], min_distances=d["world_min_d"][ids],
+                           max_distances=d["world_max_d"][ids], point_ids=ids.copy())
+
+    def local_ids(self, i: int) -> np.ndarray:
+        m = np.unpackbits(self.get(i, "local_mask"))[:self.n_points].astype(bool)
+        return np.nonzero(m)[0].astype(np.int64)
+
+    def local_map(self, i: int) -> LocalMap:
+        ids = self.local_ids(i)
+        return LocalMap((), ids, self.world_soa(ids))
+
+    def world(self):
+        """Minimal host WorldMap: the MapPoint fields decompose_map_points reads."""
+        from types import SimpleNamespace
+        d = self.d
+
+        class _Pts(dict):
+            def __missing__(s, pid):
+                v = SimpleNamespace(point_id=int(pid), position=d["world_positions"][pid],
+                                    descriptor=d["world_descriptors"][pid],
+                                    normal=d["world_normals"][pid],
+                                    min_distance=float(d["world_min_d"][pid]),
+                                    max_distance=float(d["world_max_d"][pid]))
+                s[pid] = v
+                return v
+
+        pts = _Pts()
+        return SimpleNamespace(points=pts, points_by_ids=lambda ids: [pts[int(i)] for i in ids])
+
+    def frame(self, i: int, pose: Pose, slots=None):
+        """The tracker's Frame for frame i (tracker.py:285-290)."""
+        from paper_2509_10757_b200.types import Frame
+        left, right = self.feats(i, "l"), self.feats(i, "r")
+        g = FrameGrid(left.u, left.v, self.cam.width, self.cam.height, 48)
+        n = len(left.u)
+        s = np.full(n, -1, np.int64) if slots is None else np.asarray(slots, np.int64).copy()
+        return Frame(i, 0.0, left, right, np.full(n, -1.0), s, pose, g)

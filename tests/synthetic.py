@@ -20,7 +20,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .types import (FeatureSet, FisheyeCamera, Frame, FrameGrid, ImagePyramid, LocalMap,
+from paper_2509_10757_b200.types import (FeatureSet, FisheyeCamera, Frame, FrameGrid, ImagePyramid, LocalMap,
                     MapPointSoA, PinholeCamera, Pose, NO_POINT)
 
 EXTENT = 8.0

@@ -1,8 +1,10 @@
 """The reference SPEC's known-answer examples (listed in
 SURVEY.md 8(c)) run through the B200 path; the stereo / fisheye ones also
 through the CPU oracle, so those KATs pin both.  Small hand-built inputs.
-(The SAD-triple parabola example, is a closed form the phase-2
-parity tests cover; the 4.5-px interpolated shift is a tolerance example.)"""
+The SAD-triple parabola, the 4.5-px interpolated shift
+ and the exact ray intersection are in
+test_spec_kat.py; search_prev_frame's static / empty cases
+in test_golden_sweeps.py."""
 
 import numpy as np
 import pytest

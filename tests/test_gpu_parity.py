@@ -216,7 +216,7 @@ def _oracle_local_search(O, w, pcfg, slots):
                                                     (13, 20000, 20000, True),
                                                     (14, 4000, 1000, True)])
 def test_random_pinhole_vs_oracle(oracle, seed, n_lm, m_pts, images):
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     w = make_workload(seed=seed, n_landmarks=n_lm, map_points=m_pts, images=images)
     cfg, pcfg = StereoMatchConfig(), ProjectionSearchConfig()
     ref = oracle.stereo_pinhole(w.left, w.right, w.pyr_left, w.pyr_right, w.cam, cfg,
@@ -240,7 +240,7 @@ def test_random_pinhole_vs_oracle(oracle, seed, n_lm, m_pts, images):
 
 @pytest.mark.parametrize("seed", [21, 22])
 def test_random_fisheye_vs_oracle(oracle, seed):
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     from paper_2509_10757_b200.stereo import fisheye_bruteforce
     w = make_workload(seed=seed, n_landmarks=5000, map_points=5000, fisheye=True, noise_px=0.3)
     cfg, pcfg = StereoMatchConfig(), ProjectionSearchConfig()
@@ -262,7 +262,7 @@ def test_random_fisheye_vs_oracle(oracle, seed):
 def test_projection_fp64_audit_many_points(oracle):
     """Transcendental audit (SURVEY §7 hard part 1): 1e6 random fisheye and
     pinhole map points near frustum edges, device vs oracle phase A."""
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     for fish in (False, True):
         w = make_workload(seed=31, n_landmarks=6000, map_points=2000, fisheye=fish)
         rng = np.random.default_rng(5)
@@ -472,7 +472,7 @@ def test_stereo_config_sweep_vs_oracle(oracle, kw):
     slide sizes incl. the 1x1 and 15x15 extremes, disparity range,
     outlier multiplier) through phase 1 -> phase 2 -> reject and the fisheye
     ratio test, bit-exact with the oracle."""
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     w = make_workload(seed=31, n_landmarks=12000, map_points=2000, images=True)
     cfg = StereoMatchConfig(**kw)
     ref = oracle.stereo_pinhole(w.left, w.right, w.pyr_left, w.pyr_right, w.cam, cfg,
@@ -503,7 +503,7 @@ def test_projection_config_sweep_vs_oracle(oracle, kw, scale, levels):
     """Non-default ProjectionSearchConfig values and pyramid scale / level
     counts (level prediction uses 1 / log(scale)) through phase A, resolve,
     rotation filter and SearchLocalPoints, bit-exact with the oracle."""
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     w = make_workload(seed=41, n_landmarks=12000, map_points=5000)
     pcfg = ProjectionSearchConfig(**kw)
     frame = w.frame()
@@ -540,7 +540,7 @@ def test_rejection_median_large_sads(oracle):
     (>= 4096): a right pyramid of uncorrelated noise makes every SAD large,
     so the gather + radix-select path runs; bit-exact with the oracle."""
     from copy import deepcopy
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     w = make_workload(seed=51, n_landmarks=12000, map_points=1000, images=True)
     pr = deepcopy(w.pyr_right)
     rng = np.random.default_rng(3)
@@ -569,7 +569,7 @@ def test_rejection_median_near_histogram_edge(oracle, amp, tail, monkeypatch):
     from copy import deepcopy
     if tail:
         monkeypatch.setenv("FT_TAIL_LAUNCH", "1")
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     w = make_workload(seed=51, n_landmarks=12000, map_points=1000, images=True)
     pr = deepcopy(w.pyr_right)
     rng = np.random.default_rng(3)

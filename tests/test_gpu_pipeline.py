@@ -16,7 +16,7 @@ def workloads():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     return [make_workload(seed=100 + i, n_landmarks=12000, map_points=5000, images=True,
                           offset=0.05 * i, id_base=100_000 * i) for i in range(4)]
 
@@ -143,18 +143,33 @@ def test_map_table_slots_and_update(workloads):
                                  "max_distances", "point_ids")})
     soa2.positions[3] += 1.0
     t.upsert(w.local.point_ids[3:4], _Rows(soa2, [3]))
-    out = torch.zeros(len(s) * 112, dtype=torch.uint8, device="cuda")
-    idx = torch.from_numpy(s).cuda()
-    cnt = torch.tensor([len(s)], dtype=torch.int32, device="cuda")
-    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s2 = t.slots(w.local.point_ids)
+    # copy-on-write: the rewritten point moved, nothing else did
+    assert s2[3] != s[3] and (np.delete(s2, 3) == np.delete(s, 3)).all()
     L = _lib.load()
-    _lib.check(L.ft_gather_points(1, t.ptr, t.capacity, idx.data_ptr(), cnt.data_ptr(), len(s),
-                                  out.data_ptr(), st.data_ptr(), None), "gather")
-    torch.cuda.synchronize()
-    got = out.cpu().numpy().view(_lib.POINT_RECORD)
+
+    def gather(slots):
+        out = torch.zeros(len(slots) * 112, dtype=torch.uint8, device="cuda")
+        idx = torch.from_numpy(slots).cuda()
+        cnt = torch.tensor([len(slots)], dtype=torch.int32, device="cuda")
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.check(L.ft_gather_points(1, t.ptr, t.capacity, idx.data_ptr(), cnt.data_ptr(),
+                                      len(slots), out.data_ptr(), st.data_ptr(), None), "gather")
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0
+        return out.cpu().numpy().view(_lib.POINT_RECORD)
+
+    got = gather(s2)
     np.testing.assert_array_equal(got["pos"][3], soa2.positions[3])
     np.testing.assert_array_equal(got["pos"][4], w.local.soa.positions[4])
-    assert int(st.item()) == 0
+    # a step that took its slot list before the update still reads the old record
+    old = gather(s)
+    np.testing.assert_array_equal(old["pos"][3], w.local.soa.positions[3])
+    # retired slots are recycled only after reclaim()
+    size = t.size
+    assert t.reclaim() == 1
+    t.upsert(w.local.point_ids[4:5], _Rows(soa2, [4]))
+    assert t.size == size and t.slots(w.local.point_ids[4:5])[0] == s[3]
     with pytest.raises(KeyError):
         t.slots(np.array([10 ** 12]))
 
@@ -214,7 +229,7 @@ def test_fisheye_pipeline(oracle, use_table):
     (reference mode) and search_local_points with the KB projection."""
     from paper_2509_10757_b200.maptable import MapTable
     from paper_2509_10757_b200.pipeline import FisheyePipeline
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
     ws = [make_workload(seed=500 + i, n_landmarks=4800, map_points=3050, fisheye=True,
                         offset=0.05 * i, id_base=100_000 * i) for i in range(3)]
@@ -252,7 +267,7 @@ def test_high_load_batched(oracle):
     launch: the map role must split each frame's 20k points over several
     blocks (per-block shared arrays), results equal the oracle's."""
     from paper_2509_10757_b200.pipeline import FramePipeline
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
     ws = [make_workload(seed=900 + i, n_landmarks=20000, map_points=20000, images=True,
                         offset=0.05 * i) for i in range(2)]
@@ -515,7 +530,7 @@ def test_persistent_high_load(oracle):
     otherwise), results equal the oracle's."""
     from paper_2509_10757_b200.maptable import MapTable
     from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
-    from paper_2509_10757_b200.synthetic import make_workload
+    from synthetic import make_workload
     from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
     ws = [make_workload(seed=910 + i, n_landmarks=20000, map_points=20000, images=True,
                         offset=0.05 * i, id_base=1_000_000 * (i + 1)) for i in range(2)]

@@ -2,7 +2,7 @@ import sys
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 import numpy as np
 import paper_2509_10757_b200 as ft
-from paper_2509_10757_b200.synthetic import make_workload
+from synthetic import make_workload
 from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
 from oracle import oracle as O
 w = make_workload(seed=13, n_landmarks=20000, map_points=20000, images=True)

@@ -3,12 +3,12 @@
 import os
 import sys
 
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 import numpy as np
 import torch
 
 from paper_2509_10757_b200.pipeline import FramePipeline
-from paper_2509_10757_b200.synthetic import make_workload
+from synthetic import make_workload
 
 path = os.environ.get("FT_DEBUG_TIMELINE", "/tmp/tl.txt")
 streams = int(sys.argv[1]) if len(sys.argv) > 1 else 1

@@ -8,7 +8,7 @@ from pathlib import Path
 import numpy as np
 
 ROOT = Path(__file__).resolve().parents[1]
-sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 tl_path = "/tmp/persist_tl.txt"
 os.environ["FT_DEBUG_TIMELINE"] = tl_path
 os.environ["FT_DEBUG_PERSIST"] = "/tmp/persist_ts.txt"

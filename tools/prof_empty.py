@@ -7,9 +7,9 @@ import numpy as np
 import torch
 
 ROOT = Path(__file__).resolve().parents[1]
-sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 from paper_2509_10757_b200.pipeline import FramePipeline  # noqa: E402
-from paper_2509_10757_b200.synthetic import make_workload  # noqa: E402
+from synthetic import make_workload  # noqa: E402
 from paper_2509_10757_b200.types import FeatureSet, LocalMap, MapPointSoA  # noqa: E402
 
 w = make_workload(seed=1000, n_landmarks=12000, map_points=5000, images=True)

@@ -7,10 +7,10 @@ import numpy as np
 import torch
 
 ROOT = Path(__file__).resolve().parents[1]
-sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 from paper_2509_10757_b200 import _lib  # noqa: E402
 from paper_2509_10757_b200.pipeline import FisheyePipeline  # noqa: E402
-from paper_2509_10757_b200.synthetic import make_workload  # noqa: E402
+from synthetic import make_workload  # noqa: E402
 
 w = make_workload(seed=700, n_landmarks=4800, map_points=3050, fisheye=True)
 pipe = FisheyePipeline(w.cam, n_streams=1, cap_kp=1536, cap_points=4096)

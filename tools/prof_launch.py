@@ -8,7 +8,7 @@ import numpy as np
 import torch
 
 ROOT = Path(__file__).resolve().parents[1]
-sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 from paper_2509_10757_b200 import _lib  # noqa: E402
 
 lib = _lib.load()
@@ -41,7 +41,7 @@ for blocks, threads in ((120, 512), (148, 512), (1, 32)):
 
 # empty-frame track kernel, back to back
 from paper_2509_10757_b200.pipeline import FramePipeline  # noqa: E402
-from paper_2509_10757_b200.synthetic import make_workload  # noqa: E402
+from synthetic import make_workload  # noqa: E402
 from paper_2509_10757_b200.types import FeatureSet, LocalMap, MapPointSoA  # noqa: E402
 
 w = make_workload(seed=1000, n_landmarks=12000, map_points=5000, images=True)

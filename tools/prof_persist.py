@@ -8,7 +8,7 @@ from pathlib import Path
 import torch
 
 ROOT = Path(__file__).resolve().parents[1]
-sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 import bench  # noqa: E402
 from paper_2509_10757_b200.maptable import MapTable  # noqa: E402
 from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline  # noqa: E402

@@ -10,10 +10,10 @@ import numpy as np
 import torch
 
 ROOT = Path(__file__).resolve().parents[1]
-sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 from paper_2509_10757_b200.maptable import MapTable  # noqa: E402
 from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline  # noqa: E402
-from paper_2509_10757_b200.synthetic import make_workload  # noqa: E402
+from synthetic import make_workload  # noqa: E402
 
 import os  # noqa: E402
 if os.environ.get("NUMA"):

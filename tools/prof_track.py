@@ -11,9 +11,9 @@ import numpy as np
 import torch
 
 ROOT = Path(__file__).resolve().parents[1]
-sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 from paper_2509_10757_b200.pipeline import FramePipeline  # noqa: E402
-from paper_2509_10757_b200.synthetic import make_workload  # noqa: E402
+from synthetic import make_workload  # noqa: E402
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 S = int(args[0]) if args else 1
