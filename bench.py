@@ -62,7 +62,52 @@ def parse() -> argparse.Namespace:
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--quick", action="store_true", help="skip cpu baseline / batched (profiling)")
     p.add_argument("--no-configs", action="store_true", help="skip the cfg3 / cfg5 measurements")
+    p.add_argument("--dist-selftest", action="store_true", help=argparse.SUPPRESS)
     return p.parse_args()
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int | None:
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one process per
+    GPU) through torch.distributed.run on 127.0.0.1 with the same arguments
+    and relay rank 0's line.  Returns the launcher's exit code, or None when
+    this process is already a rank (or N == 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.run(cmd, env=env).returncode
+
+
+def dist_selftest(args) -> None:
+    """The N-rank plumbing without a GPU (CPU test of the launcher): gloo
+    rendezvous, barrier, max-over-ranks of per-rank times, rank-0 line."""
+    import torch.distributed as dist
+    from paper_2509_10757_b200.sharding import job_frames_per_s, max_over_ranks, streams_of_rank
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    mine = streams_of_rank(args.streams * world, world, rank)
+    ms = 10.0 + rank  # stand-in per-rank time
+    (max_ms,) = max_over_ranks([ms], dist if world > 1 else None)
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"metric": "dist selftest", "n_gpus": world, "ranks_streams": len(mine),
+                          "max_ms": max_ms,
+                          "value": job_frames_per_s(len(mine) * args.steps, world,
+                                                    max_ms * args.steps)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------
@@ -292,12 +337,22 @@ def main() -> None:
     if args.impl == "reference":
         run_reference(args)
         return
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
+    if args.dist_selftest:
+        dist_selftest(args)
+        return
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    args.gpus = world  # n_gpus / config.parallelism follow the ranks actually running
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     n_dev = torch.cuda.device_count()
-    if local_rank >= n_dev and os.environ.get("FT_BENCH_DIST_BACKEND", "nccl") != "nccl":
+    if local_rank >= n_dev:
+        if os.environ.get("FT_BENCH_DIST_BACKEND", "nccl") == "nccl":
+            raise SystemExit(f"bench.py: rank {rank} needs GPU {local_rank} but only {n_dev} "
+                             "are visible (one process per GPU)")
         local_rank = local_rank % n_dev  # rehearsal: several ranks share the visible GPUs
     torch.cuda.set_device(local_rank)
     from paper_2509_10757_b200.runtime import bind_host_to_gpu_numa

@@ -59,3 +59,23 @@ def test_gloo_world2_max_over_ranks():
     for _, _, t in out:
         assert t == [15.0, 5.0]  # every rank sees the slowest rank's time
     assert job_frames_per_s(5, world, 15.0) == pytest.approx(10 / 0.015)
+
+
+def test_bench_self_launch_gloo_world2():
+    """`python bench.py --gpus 2` outside torchrun launches two ranks itself
+    (torch.distributed.run on 127.0.0.1) and rank 0 alone prints one line with
+    n_gpus 2 -- the driver's N-GPU invocation, rehearsed on CPU over gloo."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, FT_BENCH_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--steps", "3",
+                        "--dist-selftest"], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["max_ms"] == 11.0
