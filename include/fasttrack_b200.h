@@ -414,6 +414,103 @@ int ft_rotation_filter(int32_t m, int64_t *corr_point, int64_t *corr_kp, int64_t
 int ft_bench_popc(int32_t blocks, int32_t threads, int32_t iters, uint32_t *sink,
                   ft_stream_t stream);
 
+/* --- host-array drop-in session (csrc/ft_session.cu) ----------------------
+ * The reference stage functions called with HOST arrays -- the fields of the
+ * reference's numpy objects, passed in place -- one C call each: pack into
+ * pinned staging, H2D, the device entry above, D2H of the requested outputs,
+ * synchronise, copy into the caller's arrays.  This is what a ctypes / cffi
+ * binding of the reference binds.  A session owns a stream,
+ * pinned staging, a device arena and a workspace (grown on demand, reused);
+ * one session per tracking thread; calls are synchronous.  n = 0 returns
+ * FT_OK without touching the outputs (the caller returns empty results, as
+ * the reference does). */
+typedef struct ft_session ft_session;
+
+/* reference FeatureSet (mapping.py:18-65) fields; angle may be NULL */
+typedef struct {
+    int64_t n;
+    const double *u, *v;
+    const int32_t *octave;
+    const double *angle;
+    const uint64_t *desc;   /* [n][4] */
+} ft_host_features;
+
+/* reference ImagePyramid (extraction.py:67-94): flat u8 + level table */
+typedef struct {
+    const uint8_t *data;
+    int32_t n_levels;
+    int64_t offsets[FT_MAX_LEVELS + 1];
+    int32_t widths[FT_MAX_LEVELS];
+    int32_t heights[FT_MAX_LEVELS];
+} ft_host_pyramid;
+
+/* reference StereoMatches (stereo.py:45-64), n entries each */
+typedef struct {
+    int64_t *right_idx, *distance;
+    double *disparity, *refined_u, *depth;
+    int64_t *sad;
+} ft_host_matches;
+
+/* reference MapPointSoA (mapping.py:163-201); ids may be NULL */
+typedef struct {
+    int64_t m;
+    const double *positions, *normals;  /* [m][3] */
+    const double *min_dist, *max_dist;
+    const uint64_t *desc;               /* [m][4] */
+    const int64_t *ids;
+} ft_host_points;
+
+/* outputs of ft_session_project; any pointer may be NULL (not copied) */
+typedef struct {
+    int64_t *out_kp, *out_dist, *out_oct;                /* [m] run_phase_a */
+    int64_t *corr_point, *corr_kp, *corr_dist, *corr_oct; /* [m] resolved, point order */
+    int32_t *corr_count;
+    int64_t *slots_out;                                  /* [n_kp] after the slot write */
+    int32_t *slot_count;
+} ft_host_project_out;
+
+/* Host packing of the reference SoA fields into records (the loops the
+ * session runs; exported for callers that stage their own pinned buffers,
+ * e.g. the per-frame pipelines).  Plain C, no CUDA calls. */
+int ft_host_pack_keypoints(const ft_host_features *f, ft_kp_record *out);
+int ft_host_pack_points(const ft_host_points *p, ft_point_record *out);
+
+int ft_session_create(int32_t device, ft_session **out);
+int ft_session_destroy(ft_session *s);
+
+/* stereo.py:77-188 with host arrays; mode bits as ft_stereo_pinhole.
+ *   PHASE1 alone (match_pinhole_phase1): cand_idx / cand_dist [n_left] out.
+ *   REFINE | FROM_CAND without PHASE1 (refine_match_phase2 /
+ *     matches_from_candidates): cand_idx / cand_dist in, matches out.
+ *   PHASE1 | REFINE | FROM_CAND [| REJECT] (fused ComputeStereoMatches):
+ *     matches out (cand_* out too when non-NULL).
+ *   REJECT alone (reject_outliers): matches in and out (in place).
+ * Pyramids (REFINE only): only levels >= the lowest left octave are copied
+ * (phase 2 reads no others, kernels.py:351-428). */
+int ft_session_stereo(ft_session *s, const ft_host_features *left, const ft_host_features *right,
+                      const ft_host_pyramid *left_pyr, const ft_host_pyramid *right_pyr,
+                      const ft_stereo_params *params, int32_t mode, int64_t *cand_idx,
+                      int64_t *cand_dist, const ft_host_matches *matches);
+
+/* projection.py:118-221 / localmap.py:79-122 with host arrays.  Map points
+ * from `points` (packed here), or -- with `table` non-NULL -- read in place
+ * from a resident device table through the host slot list table_index[m]
+ * (points->m gives m).  rot[9] / trans[3] host; skip [m], ref_angles [m],
+ * slots_in [n_kp] host or NULL; mode bits as ft_project_search. */
+int ft_session_project(ft_session *s, const ft_host_points *points, const ft_point_record *table,
+                       int64_t table_size, const int32_t *table_index,
+                       const ft_host_features *frame, const ft_project_params *params,
+                       const double *rot, const double *trans, const uint8_t *skip,
+                       const double *ref_angles, const int64_t *slots_in, int32_t mode,
+                       const ft_host_project_out *out);
+
+/* stereo.py:223-273 with host arrays: brute force + ratio test (tri NULL,
+ * bruteforce_match_kernel) or + triangulation (ft_stereo_fisheye). */
+int ft_session_fisheye(ft_session *s, const ft_host_features *left,
+                       const ft_host_features *right, int32_t t_match, double ratio,
+                       const ft_fisheye_tri *tri, int64_t *out_idx, int64_t *out_dist,
+                       int32_t *out_ok, double *out_points);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2064,6 +2064,18 @@ static int track_launch(TrackArgs &a, bool want_stereo, bool want_map, const ft_
     return (int)cudaGetLastError();
 }
 
+// Keypoint tables staged in shared memory (one TMA copy per block) or read
+// in place from L2; staged unless they would not fit.  FT_STAGE_RDESC /
+// FT_STAGE_KDESC = 0 / 1 override (measurement).
+static void stage_policy(TrackArgs &a, bool want_stereo, bool want_map) {
+    static const char *er = getenv("FT_STAGE_RDESC");
+    static const char *ek = getenv("FT_STAGE_KDESC");
+    a.stage_rdesc = er ? (atoi(er) != 0) : 1;
+    a.stage_kdesc = ek ? (atoi(ek) != 0) : 1;
+    if (want_stereo && stereo_smem(a) > 227 * 1024) a.stage_rdesc = 0;
+    if (want_map && map_smem(a) > 227 * 1024) a.stage_kdesc = 0;
+}
+
 static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out,
                           int reserve) {
     int dev = 0, sms = 148;
@@ -2089,11 +2101,7 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
     a.stage_kdesc = 1;
     for (int iter = 0; iter < 4; ++iter) {
         if (want_map) a.map_chunk_cap = (((a.P.cap + Gm - 1) / Gm) + 1) & ~1;
-        // descriptors stay in L2 when the staged tables would not fit
-        a.stage_rdesc = 1;
-        a.stage_kdesc = 1;
-        if (want_stereo && stereo_smem(a) > 227 * 1024) a.stage_rdesc = 0;
-        if (want_map && map_smem(a) > 227 * 1024) a.stage_kdesc = 0;
+        stage_policy(a, want_stereo, want_map);
         smem = want_stereo ? stereo_smem(a) : 0;
         if (want_map) {
             const size_t m = map_smem(a);
@@ -2163,10 +2171,7 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
         if (same && iter > 0) break;
     }
     if (want_map) a.map_chunk_cap = (((a.P.cap + Gm - 1) / Gm) + 1) & ~1;
-    a.stage_rdesc = 1;
-    a.stage_kdesc = 1;
-    if (want_stereo && stereo_smem(a) > 227 * 1024) a.stage_rdesc = 0;
-    if (want_map && map_smem(a) > 227 * 1024) a.stage_kdesc = 0;
+    stage_policy(a, want_stereo, want_map);
     smem = want_stereo ? stereo_smem(a) : 0;
     if (want_map) {
         const size_t m = map_smem(a);

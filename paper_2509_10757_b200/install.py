@@ -7,6 +7,13 @@ module that imported them; ``uninstall()`` restores the originals.
 
     import trackfront, paper_2509_10757_b200 as ft
     ft.install()                      # StereoTracker now runs on the B200
+
+With ``fuse_stereo=True`` (default) the tracker's pinhole ``_run_stereo``
+(tracker.py:415-427: phase 1 -> phase 2 | from candidates -> reject, three
+calls with host round trips in between) is also replaced, by ONE fused call
+with the same outputs and the same side effects (phase-1 candidates written
+into the pool's stereo_idx / stereo_dist buffers); the fisheye branch keeps
+the reference's method, whose match_fisheye is rebound above.
 """
 
 from __future__ import annotations
@@ -49,9 +56,35 @@ _TARGETS = {
 }
 
 _saved: dict[tuple[str, str], object] = {}
+_saved_method: dict[str, object] = {}
 
 
-def install() -> list[str]:
+def _fused_run_stereo(self, left, right, pyr_l, pyr_r):
+    """StereoTracker._run_stereo (tracker.py:397-427) with the pinhole branch
+    as ONE fused ft_stereo_pinhole call; fisheye -> the reference method."""
+    import numpy as np
+    from . import _lib
+    if hasattr(self.cam, "k1"):  # FisheyeCamera (cameras.py:79-157)
+        return _saved_method["_run_stereo"](self, left, right, pyr_l, pyr_r)
+    scale_pow = self.extraction.scale_powers()
+    n = len(left.u)
+    idx = self.pool.acquire("stereo_idx", (n,), np.int64)
+    dist = self.pool.acquire("stereo_dist", (n,), np.int64)
+    if n == 0:
+        return _stereo.matches_from_candidates(idx, dist, left, right, self.cam, self.stereo)
+    direct = idx.flags.c_contiguous and dist.flags.c_contiguous
+    ci, cd = (idx, dist) if direct else (np.empty(n, np.int64), np.empty(n, np.int64))
+    mode = _lib.FT_STEREO_PHASE1 | _lib.FT_STEREO_REJECT
+    mode |= _lib.FT_STEREO_REFINE if pyr_l is not None else _lib.FT_STEREO_FROM_CAND
+    res, _, _ = _stereo._run_stereo(mode, left, right, self.cam, self.stereo, scale_pow,
+                                    int(self.cam.height), pyr_l, pyr_r, out_cand=(ci, cd))
+    if not direct:
+        idx[...] = ci
+        dist[...] = cd
+    return res
+
+
+def install(fuse_stereo: bool = True) -> list[str]:
     """Rebind the reference's hot-path names; returns the rebound names."""
     done = []
     for modname, names in _TARGETS.items():
@@ -62,6 +95,13 @@ def install() -> list[str]:
             _saved.setdefault((modname, name), getattr(mod, name))
             setattr(mod, name, fn)
             done.append(f"{modname}.{name}")
+    if fuse_stereo:
+        tr = importlib.import_module("trackfront.tracker")
+        cls = tr.StereoTracker
+        if hasattr(cls, "_run_stereo"):
+            _saved_method.setdefault("_run_stereo", cls._run_stereo)
+            cls._run_stereo = _fused_run_stereo
+            done.append("trackfront.tracker.StereoTracker._run_stereo")
     return done
 
 
@@ -69,3 +109,6 @@ def uninstall() -> None:
     for (modname, name), orig in _saved.items():
         setattr(importlib.import_module(modname), name, orig)
     _saved.clear()
+    if "_run_stereo" in _saved_method:
+        tr = importlib.import_module("trackfront.tracker")
+        tr.StereoTracker._run_stereo = _saved_method.pop("_run_stereo")

@@ -74,84 +74,36 @@ def _grid_geometry(frame, cam) -> tuple[int, int, int]:
     return cell, max(1, (int(cam.width) + cell - 1) // cell), max(1, (int(cam.height) + cell - 1) // cell)
 
 
-def _add_points(lay: Layout, cap: int, table=None) -> None:
-    lay.add("P_n", 4)
-    if table is None:
-        lay.add("P_rec", _lib.POINT_RECORD.itemsize * cap)
-    else:
-        lay.add("P_idx", 4 * cap)
-
-
-def _put_points(rt, lay: Layout, pts, table=None) -> int:
-    """Records (reference SoA -> ft_point_record) or, with a resident
-    MapTable, 4-B table slots (points missing from the table are uploaded
-    first: the map delta)."""
-    m = len(pts.point_ids)
-    rt.put(lay, "P_n", np.array([m], dtype=np.int32), np.int32)
-    if m and table is None:
-        fill_point_records(rt.host_view(lay, "P_rec", _lib.POINT_RECORD, (m,)), pts)
-    elif m:
-        if getattr(pts, "positions", None) is not None:
-            table.upsert(pts.point_ids, pts, only_missing=True)
-        rt.put(lay, "P_idx", table.slots(pts.point_ids), np.int32)
-    return m
-
-
-def _points_struct(rt, lay: Layout, cap: int, table=None) -> _lib.FtMapPoints:
-    s = _lib.FtMapPoints()
-    if table is None:
-        s.rec, s.count, s.cap, s.index = rt.ptr(lay, "P_rec"), rt.ptr(lay, "P_n"), cap, None
-    else:
-        s.rec, s.count, s.cap, s.index = table.ptr, rt.ptr(lay, "P_n"), cap, rt.ptr(lay, "P_idx")
-    return s
-
-
-def _out_struct(rt, lay: Layout, phase_a: bool) -> _lib.FtProjectOut:
-    o = _lib.FtProjectOut()
-    if phase_a:
-        o.out_kp, o.out_dist, o.out_oct = (rt.ptr(lay, "out_kp"), rt.ptr(lay, "out_dist"),
-                                           rt.ptr(lay, "out_oct"))
-    o.corr_point, o.corr_kp = rt.ptr(lay, "c_point"), rt.ptr(lay, "c_kp")
-    o.corr_dist, o.corr_oct = rt.ptr(lay, "c_dist"), rt.ptr(lay, "c_oct")
-    o.corr_count, o.slot_count = rt.ptr(lay, "c_n"), rt.ptr(lay, "slot_n")
-    return o
-
-
 def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale: float,
                    levels: int, *, skip_mask=None, ref_angles=None, rotation: bool = False,
                    window_px=None, u_offset: float = 0.0, slots=None, skip_slotted=False,
                    write_slots=False, resolve=True, phase_a_out=False, table=None):
-    """One fused ``ft_project_search`` launch on one frame.
+    """One fused ``ft_project_search`` launch on one frame, through the
+    native session (csrc/ft_session.cu: the reference objects' arrays are
+    packed, shipped, searched and the requested outputs copied back in one
+    C call).  table: a resident MapTable -- the points are read in place
+    through their table slots (points missing from it are uploaded first:
+    the map delta).
 
     Returns a dict with any of: out_kp/out_dist/out_oct (phase A),
     corr (Correspondences), slots (updated copy), count (filled slots)."""
-    rt = runtime()
+    from . import session as S
+    ses = S.session()
     left = frame.left
     n_kp, m = len(left.u), len(points.point_ids)
-    cap_kp, cap_pts = rt.caps(n_kp, m)
     cell, nx, ny = _grid_geometry(frame, cam)
     with_angle = bool(rotation and ref_angles is not None)
-    lay = Layout()
-    add_keypoints(lay, "K", cap_kp, with_angle=with_angle)
-    _add_points(lay, cap_pts, table)
-    lay.add("rot", 72)
-    lay.add("trans", 24)
-    if skip_mask is not None:
-        lay.add("skip", cap_pts)
-    if with_angle:
-        lay.add("ref_ang", 8 * cap_pts)
-    if slots is not None:
-        lay.add("slots", 8 * cap_kp)
-    in_end = lay.total
-    out_begin = lay.total
-    if phase_a_out:
-        lay.add("out_kp", 8 * cap_pts)
-        lay.add("out_dist", 8 * cap_pts)
-        lay.add("out_oct", 8 * cap_pts)
-    for nm_ in ("c_point", "c_kp", "c_dist", "c_oct"):
-        lay.add(nm_, 8 * cap_pts)
-    lay.add("c_n", 4)
-    lay.add("slot_n", 4)
+    keep: list = []
+    kf = S.features(left, with_angle=with_angle, keep=keep)
+    if table is None:
+        pts = S.points(points, keep)
+        tptr, tsize, tidx = None, 0, None
+    else:
+        if m and getattr(points, "positions", None) is not None:
+            table.upsert(points.point_ids, points, only_missing=True)
+        tidx = np.ascontiguousarray(table.slots(points.point_ids), np.int32)
+        pts = S.FtHostPoints(m, None, None, None, None, None, None)
+        tptr, tsize = table.ptr, table.capacity
     mode = 0
     if resolve:
         mode |= _lib.FT_PROJ_RESOLVE
@@ -161,47 +113,43 @@ def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale:
         mode |= _lib.FT_PROJ_SKIP_SLOTS
     if write_slots:
         mode |= _lib.FT_PROJ_WRITE_SLOTS
-    with rt.lock:
-        rt.reserve(lay.total)
-        put_keypoints(rt, lay, "K", left, with_angle=with_angle)
-        _put_points(rt, lay, points, table)
-        rt.put(lay, "rot", np.asarray(pose.rotation, dtype=np.float64).reshape(9), np.float64)
-        rt.put(lay, "trans", np.asarray(pose.translation, dtype=np.float64).reshape(3), np.float64)
-        if skip_mask is not None:
-            rt.put(lay, "skip", np.asarray(skip_mask, dtype=np.uint8), np.uint8)
-        if with_angle:
-            rt.put(lay, "ref_ang", ref_angles, np.float64)
-        if slots is not None:
-            rt.put(lay, "slots", slots, np.int64)
-        rt.h2d(0, in_end)
-        ws = rt.workspace()
-        params = project_params(cam, cfg, scale, levels, cell, nx, ny, window_px, u_offset)
-        io = _lib.FtProjectIO()
-        io.rot, io.trans = rt.ptr(lay, "rot"), rt.ptr(lay, "trans")
-        io.skip = rt.ptr(lay, "skip") if skip_mask is not None else None
-        io.ref_angles = rt.ptr(lay, "ref_ang") if with_angle else None
-        io.slots_in = io.slots_out = rt.ptr(lay, "slots") if slots is not None else None
-        st = rt.lib.ft_project_search(1, _points_struct(rt, lay, cap_pts, table),
-                                      keypoints_struct(rt, lay, "K", cap_kp), params, io, mode,
-                                      _out_struct(rt, lay, phase_a_out), ws,
-                                      rt.stream.cuda_stream)
-        _lib.check(st, "ft_project_search")
-        if slots is not None:
-            rt.d2h(lay.offsets["slots"], lay.offsets["slots"] + 8 * n_kp)
-        rt.d2h(out_begin, lay.total)
-        rt.sync()
-        res = {}
-        if phase_a_out:
-            for k in ("out_kp", "out_dist", "out_oct"):
-                res[k] = rt.host_view(lay, k, np.int64, (m,)).copy()
-        if resolve:
-            c = int(rt.host_view(lay, "c_n", np.int32, (1,))[0])
-            res["corr"] = Correspondences(*(rt.host_view(lay, k, np.int64, (c,)).copy()
-                                            for k in ("c_point", "c_kp", "c_dist", "c_oct")))
-        if slots is not None:
-            res["slots"] = rt.host_view(lay, "slots", np.int64, (n_kp,)).copy()
-        if write_slots:
-            res["count"] = int(rt.host_view(lay, "slot_n", np.int32, (1,))[0])
+    params = S.project_params(cam, cfg, scale, levels, cell, nx, ny, window_px, u_offset)
+    rot = np.ascontiguousarray(pose.rotation, np.float64).reshape(9)
+    trans = np.ascontiguousarray(pose.translation, np.float64).reshape(3)
+    skip = np.ascontiguousarray(skip_mask, np.uint8) if skip_mask is not None else None
+    ref = np.ascontiguousarray(ref_angles, np.float64) if with_angle else None
+    sl = np.ascontiguousarray(slots, np.int64) if slots is not None else None
+    res, out = {}, S.FtHostProjectOut()
+    if phase_a_out:
+        res["out_kp"], res["out_dist"], res["out_oct"] = (np.empty(m, np.int64) for _ in range(3))
+        out.out_kp, out.out_dist, out.out_oct = (res[k].ctypes.data for k in
+                                                 ("out_kp", "out_dist", "out_oct"))
+    cbuf = np.empty((4, max(m, 1)), np.int64) if resolve else None
+    counts = np.zeros(2, np.int32)
+    if resolve:
+        out.corr_point, out.corr_kp, out.corr_dist, out.corr_oct = (cbuf[q].ctypes.data
+                                                                    for q in range(4))
+    out.corr_count = counts.ctypes.data
+    out.slot_count = counts.ctypes.data + 4
+    slots_out = np.empty(n_kp, np.int64) if sl is not None else None
+    if slots_out is not None:
+        out.slots_out = slots_out.ctypes.data
+    with ses.lock:
+        st = ses.lib.ft_session_project(ses.handle, pts, tptr, tsize,
+                                        tidx.ctypes.data if tidx is not None and m else None,
+                                        kf, params, rot.ctypes.data, trans.ctypes.data,
+                                        skip.ctypes.data if skip is not None and m else None,
+                                        ref.ctypes.data if ref is not None and m else None,
+                                        sl.ctypes.data if sl is not None and n_kp else None,
+                                        mode, out)
+    _lib.check(st, "ft_session_project")
+    if resolve:
+        c = int(counts[0])
+        res["corr"] = Correspondences(*(cbuf[q, :c].copy() for q in range(4)))
+    if slots_out is not None:
+        res["slots"] = slots_out
+    if write_slots:
+        res["count"] = int(counts[1])
     return res
 
 

@@ -233,27 +233,29 @@ def add_keypoints(lay: Layout, prefix: str, cap: int, with_angle: bool = False) 
 
 
 def fill_kp_records(rec: np.ndarray, feats, with_angle: bool = False) -> int:
-    """Pack a FeatureSet (reference SoA layout) into ft_kp_record rows."""
+    """Pack a FeatureSet (reference SoA layout) into ft_kp_record rows
+    (ft_host_pack_keypoints: a C loop over the arrays, passed in place)."""
+    from . import session as S
     n = len(feats.u)
     if n:
-        rec["u"][:n] = feats.u
-        rec["v"][:n] = feats.v
-        rec["desc"][:n] = np.asarray(feats.descriptors).reshape(n, 4)
-        rec["octave"][:n] = feats.octave
-        rec["angle"][:n] = feats.angle if with_angle else 0.0
+        if len(rec) < n or not rec.flags.c_contiguous or rec.dtype != _lib.KP_RECORD:
+            raise ValueError("record buffer: contiguous ft_kp_record rows, >= n")
+        keep: list = []
+        _lib.check(S.lib().ft_host_pack_keypoints(S.features(feats, with_angle, keep),
+                                                  rec.ctypes.data), "ft_host_pack_keypoints")
     return n
 
 
 def fill_point_records(rec: np.ndarray, pts) -> int:
-    """Pack a MapPointSoA into ft_point_record rows."""
+    """Pack a MapPointSoA into ft_point_record rows (ft_host_pack_points)."""
+    from . import session as S
     m = len(pts.point_ids)
     if m:
-        rec["desc"][:m] = np.asarray(pts.descriptors).reshape(m, 4)
-        rec["pos"][:m] = np.asarray(pts.positions).reshape(m, 3)
-        rec["nrm"][:m] = np.asarray(pts.normals).reshape(m, 3)
-        rec["min_dist"][:m] = pts.min_distances
-        rec["max_dist"][:m] = pts.max_distances
-        rec["id"][:m] = pts.point_ids
+        if len(rec) < m or not rec.flags.c_contiguous or rec.dtype != _lib.POINT_RECORD:
+            raise ValueError("record buffer: contiguous ft_point_record rows, >= m")
+        keep: list = []
+        _lib.check(S.lib().ft_host_pack_points(S.points(pts, keep), rec.ctypes.data),
+                   "ft_host_pack_points")
     return m
 
 

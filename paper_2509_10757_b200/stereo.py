@@ -19,8 +19,6 @@ from types import SimpleNamespace
 import numpy as np
 
 from . import _lib
-from .runtime import (Layout, add_keypoints, keypoints_struct, put_keypoints, pyramid_struct,
-                      runtime, stereo_params)
 from .types import StereoMatchConfig, StereoMatches
 
 __all__ = ["StereoMatchConfig", "StereoMatches", "build_row_buckets", "match_pinhole_phase1",
@@ -41,79 +39,46 @@ def build_row_buckets(v: np.ndarray, height: int) -> tuple[np.ndarray, np.ndarra
     return start, order.astype(np.int64)
 
 
-def _matches_layout(lay: Layout, cap: int) -> None:
-    for name, nb in (("cand_idx", 8), ("cand_dist", 8), ("right_idx", 8), ("distance", 8),
-                     ("disparity", 8), ("refined_u", 8), ("depth", 8), ("sad", 8)):
-        lay.add(name, nb * cap)
-    lay.add("n_matched", 4)
-
-
-def _out_struct(rt, lay: Layout) -> _lib.FtStereoOut:
-    o = _lib.FtStereoOut()
-    for name in ("cand_idx", "cand_dist", "right_idx", "distance", "disparity", "refined_u",
-                 "depth", "sad", "n_matched"):
-        setattr(o, name, rt.ptr(lay, name))
-    return o
-
-
-def _read_matches(rt, lay: Layout, n: int) -> StereoMatches:
-    g = lambda name, dt: rt.host_view(lay, name, dt, (n,)).copy()  # noqa: E731
-    return StereoMatches(right_idx=g("right_idx", np.int64), distance=g("distance", np.int64),
-                         disparity=g("disparity", np.float64), refined_u=g("refined_u", np.float64),
-                         depth=g("depth", np.float64), sad=g("sad", np.int64))
+def _empty_matches(n: int) -> StereoMatches:
+    return StereoMatches(right_idx=np.empty(n, np.int64), distance=np.empty(n, np.int64),
+                         disparity=np.empty(n), refined_u=np.empty(n), depth=np.empty(n),
+                         sad=np.empty(n, np.int64))
 
 
 def _run_stereo(mode: int, left, right, cam, cfg, scale_pow, height: int,
                 left_pyr=None, right_pyr=None, cand=None, matches=None,
-                out_cand: bool = False):
-    """Pack -> one H2D -> ft_stereo_pinhole -> one D2H."""
-    rt = runtime()
-    n, nr = len(left.u), len(right.u)
-    cap, _ = rt.caps(max(n, nr))
-    lay = Layout()
-    add_keypoints(lay, "L", cap)
-    add_keypoints(lay, "R", cap)
-    use_pyr = bool(mode & _lib.FT_STEREO_REFINE)
-    if use_pyr:
-        lay.add("pyr_l", int(left_pyr.offsets[-1]))
-        lay.add("pyr_r", int(right_pyr.offsets[-1]))
-    in_end = lay.total
-    _matches_layout(lay, cap)
-    with rt.lock:
-        rt.reserve(lay.total)
-        put_keypoints(rt, lay, "L", left)
-        put_keypoints(rt, lay, "R", right)
-        if use_pyr:
-            rt.put(lay, "pyr_l", left_pyr.data, np.uint8)
-            rt.put(lay, "pyr_r", right_pyr.data, np.uint8)
-        upload_end = in_end
-        if cand is not None:
-            rt.put(lay, "cand_idx", cand[0], np.int64)
-            rt.put(lay, "cand_dist", cand[1], np.int64)
-            upload_end = lay.offsets["cand_dist"] + 8 * n
-        if matches is not None:
-            for name, dt in (("right_idx", np.int64), ("distance", np.int64),
-                             ("disparity", np.float64), ("refined_u", np.float64),
-                             ("depth", np.float64), ("sad", np.int64)):
-                rt.put(lay, name, getattr(matches, name), dt)
-            upload_end = lay.total
-        rt.h2d(0, upload_end)
-        ws = rt.workspace()
-        params = stereo_params(cfg, height, scale_pow, getattr(cam, "baseline_times_fx", 1.0))
-        kl = keypoints_struct(rt, lay, "L", cap)
-        kr = keypoints_struct(rt, lay, "R", cap)
-        pl = pyramid_struct(left_pyr, rt.ptr(lay, "pyr_l"), 0) if use_pyr else None
-        pr = pyramid_struct(right_pyr, rt.ptr(lay, "pyr_r"), 0) if use_pyr else None
-        out = _out_struct(rt, lay)
-        st = rt.lib.ft_stereo_pinhole(1, kl, kr, pl, pr, params, mode, out, ws,
-                                      rt.stream.cuda_stream)
-        _lib.check(st, "ft_stereo_pinhole")
-        rt.d2h(lay.offsets["cand_idx"], lay.total)
-        rt.sync()
-        res = _read_matches(rt, lay, n) if mode & ~_lib.FT_STEREO_PHASE1 else None
-        cidx = rt.host_view(lay, "cand_idx", np.int64, (n,)).copy() if out_cand else None
-        cdist = rt.host_view(lay, "cand_dist", np.int64, (n,)).copy() if out_cand else None
-    return res, cidx, cdist
+                out_cand=None):
+    """One ft_session_stereo call: pack -> H2D -> ft_stereo_pinhole -> D2H,
+    with the reference objects' arrays passed in place (csrc/ft_session.cu).
+    Returns (matches or None, cand_idx, cand_dist)."""
+    from . import session as S
+    ses = S.session()
+    n = len(left.u)
+    keep: list = []
+    lf = S.features(left, keep=keep)
+    rf = lf if right is left else S.features(right, keep=keep)
+    pl = pr = None
+    if mode & _lib.FT_STEREO_REFINE:
+        pl, pr = S.pyramid(left_pyr, keep), S.pyramid(right_pyr, keep)
+    params = S.stereo_params(cfg, height, scale_pow, getattr(cam, "baseline_times_fx", 1.0))
+    if cand is not None:
+        ci, cd = np.ascontiguousarray(cand[0], np.int64), np.ascontiguousarray(cand[1], np.int64)
+    elif out_cand is not None:
+        ci, cd = out_cand
+    else:
+        ci = cd = None
+    res = None
+    if matches is not None:
+        res = matches
+    elif mode & ~_lib.FT_STEREO_PHASE1:
+        res = _empty_matches(n)
+    ms = S.matches_struct(res) if res is not None else None
+    with ses.lock:
+        st = ses.lib.ft_session_stereo(ses.handle, lf, rf, pl, pr, params, mode,
+                                       ci.ctypes.data if ci is not None else None,
+                                       cd.ctypes.data if cd is not None else None, ms)
+    _lib.check(st, "ft_session_stereo")
+    return res, ci, cd
 
 
 def match_pinhole_phase1(left, right, height: int, scale_pow: np.ndarray,
@@ -130,10 +95,14 @@ def match_pinhole_phase1(left, right, height: int, scale_pow: np.ndarray,
     dist = out_dist if out_dist is not None else np.empty(n, dtype=np.int64)
     if n == 0:
         return idx, dist
-    _, ci, cd = _run_stereo(_lib.FT_STEREO_PHASE1, left, right, None, cfg, scale_pow, height,
-                            out_cand=True)
-    idx[:n] = ci
-    dist[:n] = cd
+    direct = (idx.dtype == np.int64 and dist.dtype == np.int64 and idx.flags.c_contiguous
+              and dist.flags.c_contiguous and len(idx) >= n and len(dist) >= n)
+    ci, cd = (idx, dist) if direct else (np.empty(n, np.int64), np.empty(n, np.int64))
+    _run_stereo(_lib.FT_STEREO_PHASE1, left, right, None, cfg, scale_pow, height,
+                out_cand=(ci, cd))
+    if not direct:
+        idx[:n] = ci
+        dist[:n] = cd
     return idx, dist
 
 
@@ -177,12 +146,18 @@ def reject_outliers(matches: StereoMatches, cfg: StereoMatchConfig) -> StereoMat
         return matches
 
     n = len(matches.right_idx)
-    left = SimpleNamespace(u=np.zeros(n), v=np.zeros(n), octave=np.zeros(n, dtype=np.int32),
-                           descriptors=np.zeros((n, 4), dtype=np.uint64))
-    res, _, _ = _run_stereo(_lib.FT_STEREO_REJECT, left, left, None, cfg, np.ones(1), 1,
-                            matches=matches)
-    for name in ("right_idx", "distance", "disparity", "refined_u", "depth", "sad"):
-        getattr(matches, name)[...] = getattr(res, name)
+    names = ("right_idx", "distance", "disparity", "refined_u", "depth", "sad")
+    types = (np.int64, np.int64, np.float64, np.float64, np.float64, np.int64)
+    direct = all(getattr(matches, k).dtype == t and getattr(matches, k).flags.c_contiguous and
+                 getattr(matches, k).flags.writeable for k, t in zip(names, types))
+    work = matches if direct else StereoMatches(*(np.ascontiguousarray(getattr(matches, k), t)
+                                                  for k, t in zip(names, types)))
+    counts = SimpleNamespace(u=np.zeros(n), v=np.zeros(n), octave=np.zeros(n, np.int32),
+                             descriptors=np.zeros((0, 4), np.uint64))
+    _run_stereo(_lib.FT_STEREO_REJECT, counts, counts, None, cfg, np.ones(1), 1, matches=work)
+    if not direct:  # in place, as the reference (stereo.py:181-188)
+        for k in names:
+            getattr(matches, k)[...] = getattr(work, k)
     return matches
 
 
@@ -261,45 +236,24 @@ def fisheye_tri_params(cam, cfg: StereoMatchConfig, corrected: bool = False) -> 
 
 
 def _fisheye_device(left, right, cfg: StereoMatchConfig, tri):
-    """One ft_stereo_fisheye_bf (tri None) or ft_stereo_fisheye launch for a
-    frame -> (idx, dist[, ok, points])."""
-    rt = runtime()
-    n, nr = len(left.u), len(right.u)
-    cap, _ = rt.caps(max(n, nr))
-    lay = Layout()
-    add_keypoints(lay, "L", cap)
-    add_keypoints(lay, "R", cap)
-    in_end = lay.total
-    lay.add("idx", 8 * cap)
-    lay.add("dist", 8 * cap)
-    lay.add("ok", 4 * cap)
-    lay.add("pts", 24 * cap)
-    with rt.lock:
-        rt.reserve(lay.total)
-        put_keypoints(rt, lay, "L", left)
-        put_keypoints(rt, lay, "R", right)
-        rt.h2d(0, in_end)
-        ws = rt.workspace()
-        kl = keypoints_struct(rt, lay, "L", cap)
-        kr = keypoints_struct(rt, lay, "R", cap)
-        if tri is None:
-            st = rt.lib.ft_stereo_fisheye_bf(1, kl, kr, int(cfg.t_match), float(cfg.ratio),
-                                             rt.ptr(lay, "idx"), rt.ptr(lay, "dist"), ws,
-                                             rt.stream.cuda_stream)
-        else:
-            st = rt.lib.ft_stereo_fisheye(1, kl, kr, int(cfg.t_match), float(cfg.ratio), tri,
-                                          rt.ptr(lay, "idx"), rt.ptr(lay, "dist"),
-                                          rt.ptr(lay, "ok"), rt.ptr(lay, "pts"), ws,
-                                          rt.stream.cuda_stream)
-        _lib.check(st, "ft_stereo_fisheye_bf" if tri is None else "ft_stereo_fisheye")
-        rt.d2h(lay.offsets["idx"], lay.total)
-        rt.sync()
-        idx = rt.host_view(lay, "idx", np.int64, (n,)).copy()
-        dist = rt.host_view(lay, "dist", np.int64, (n,)).copy()
-        if tri is None:
-            return idx, dist
-        ok = rt.host_view(lay, "ok", np.int32, (n,)).copy()
-        pts = rt.host_view(lay, "pts", np.float64, (n, 3)).copy()
+    """One ft_session_fisheye call (ft_stereo_fisheye_bf when tri is None,
+    else ft_stereo_fisheye) -> (idx, dist[, ok, points])."""
+    from . import session as S
+    ses = S.session()
+    n = len(left.u)
+    keep: list = []
+    lf, rf = S.features(left, keep=keep), S.features(right, keep=keep)
+    idx, dist = np.empty(n, np.int64), np.empty(n, np.int64)
+    ok = np.empty(n, np.int32) if tri is not None else None
+    pts = np.empty((n, 3)) if tri is not None else None
+    with ses.lock:
+        st = ses.lib.ft_session_fisheye(ses.handle, lf, rf, int(cfg.t_match), float(cfg.ratio),
+                                        tri, idx.ctypes.data, dist.ctypes.data,
+                                        ok.ctypes.data if ok is not None else None,
+                                        pts.ctypes.data if pts is not None else None)
+    _lib.check(st, "ft_session_fisheye")
+    if tri is None:
+        return idx, dist
     return idx, dist, ok, pts
 
 

@@ -112,3 +112,45 @@ def test_new_entries_validate_without_gpu():
     assert L.ft_track_frames_ring(1, None, 1, None) == -1
     assert L.ft_track_frames_ring(0, vp2(None, None), 1, None) == -2
     assert L.ft_track_frames_ring(1, vp2(None, None), -1, None) == -2
+
+
+def test_session_entries_validate_without_gpu():
+    """The host-array session entries (csrc/ft_session.cu) reject missing
+    arguments before any CUDA call; creating a session needs a device."""
+    from paper_2509_10757_b200 import session as S
+    L = _lib.load()
+    S._bind(L)
+    f = S.FtHostFeatures()
+    assert L.ft_session_destroy(None) == 0
+    assert L.ft_session_stereo(None, f, f, None, None, _lib.FtStereoParams(), 1, None, None,
+                               None) == -1
+    assert L.ft_session_project(None, S.FtHostPoints(), None, 0, None, f, _lib.FtProjectParams(),
+                                None, None, None, None, None, 1, S.FtHostProjectOut()) == -1
+    assert L.ft_session_fisheye(None, f, f, 100, 0.8, None, None, None, None, None) == -1
+    import torch
+    if not torch.cuda.is_available():
+        h = ctypes.c_void_p()
+        assert L.ft_session_create(0, ctypes.byref(h)) > 0  # a cudaError_t: no device
+
+
+def test_host_packers_match_numpy_layout():
+    """ft_host_pack_keypoints / ft_host_pack_points (C loops, no GPU) write
+    exactly the include/fasttrack_b200.h record layout."""
+    import numpy as np
+    import golden_io as G
+    from paper_2509_10757_b200.runtime import fill_kp_records, fill_point_records
+    d = G.load("cfg2_frame_map.npz")
+    left, pts = G.feats(d, "left"), G.soa(d)
+    n, m = len(left.u), len(pts.point_ids)
+    rec = np.zeros(n + 3, _lib.KP_RECORD)
+    fill_kp_records(rec, left, with_angle=True)
+    want = np.zeros(n, _lib.KP_RECORD)
+    want["u"], want["v"], want["desc"] = left.u, left.v, left.descriptors
+    want["angle"], want["octave"] = left.angle, left.octave
+    assert rec[:n].tobytes() == want.tobytes()
+    prec = np.zeros(m, _lib.POINT_RECORD)
+    fill_point_records(prec, pts)
+    pw = np.zeros(m, _lib.POINT_RECORD)
+    pw["desc"], pw["pos"], pw["nrm"] = pts.descriptors, pts.positions, pts.normals
+    pw["min_dist"], pw["max_dist"], pw["id"] = pts.min_distances, pts.max_distances, pts.point_ids
+    assert prec.tobytes() == pw.tobytes()

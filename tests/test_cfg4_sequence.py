@@ -245,3 +245,35 @@ def _check_step(seq, runner, k):
     _check(_mdig(r.matches), seq.get(i, "stereo_final"), f"frame {i} stereo")
     _check(G.digest(r.slots), seq.get(i, "local_slots_out"), f"frame {i} slots")
     assert r.n_slots == int(seq.get(i, "local_count")), f"frame {i} count"
+
+
+class _Pool:
+    """The reference BufferPool's acquire (buffers.py:38-52): views of
+    pre-reserved storage."""
+
+    def __init__(self):
+        self.buf = {}
+
+    def acquire(self, name, shape, dtype):
+        b = self.buf.get(name)
+        if b is None:
+            b = self.buf[name] = np.empty(4096, dtype)
+        return b[:shape[0]]
+
+
+@pytest.mark.gpu
+def test_cfg4_install_fused_run_stereo(seq):
+    """install()'s replacement of StereoTracker._run_stereo (one fused launch)
+    on every frame: the reference's StereoMatches and its side effect, the
+    phase-1 candidates in the pool's stereo_idx / stereo_dist buffers."""
+    from types import SimpleNamespace
+    from paper_2509_10757_b200.install import _fused_run_stereo
+    tracker = SimpleNamespace(cam=seq.cam, stereo=StereoMatchConfig(), pool=_Pool(),
+                              extraction=SimpleNamespace(scale_powers=lambda: SCALE_POW.copy()))
+    for i in _frames(seq):
+        left, right = seq.feats(i, "l"), seq.feats(i, "r")
+        m = _fused_run_stereo(tracker, left, right, None, None)
+        _check(_mdig(m), seq.get(i, "stereo_final"), f"frame {i} stereo")
+        n = len(left.u)
+        _check(G.digest(tracker.pool.buf["stereo_idx"][:n], tracker.pool.buf["stereo_dist"][:n]),
+               seq.get(i, "stereo_p1"), f"frame {i} pool candidates")

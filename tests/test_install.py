@@ -22,12 +22,22 @@ def test_install_rebinds_reference_names():
         pytest.skip(f"reference not importable: {e}")
     import paper_2509_10757_b200 as ft
     orig = tr.search_local_points
+    orig_run = tr.StereoTracker._run_stereo
     done = ft.install()
     try:
         assert "trackfront.tracker.search_local_points" in done
         assert tr.search_local_points is ft.search_local_points
         assert lm.search_by_projection is ft.search_by_projection
         assert tr.match_pinhole_phase1 is ft.match_pinhole_phase1
+        # the pinhole _run_stereo as one fused call (install(fuse_stereo=True))
+        assert "trackfront.tracker.StereoTracker._run_stereo" in done
+        assert tr.StereoTracker._run_stereo is not orig_run
     finally:
         ft.uninstall()
     assert tr.search_local_points is orig
+    assert tr.StereoTracker._run_stereo is orig_run
+    done = ft.install(fuse_stereo=False)
+    try:
+        assert tr.StereoTracker._run_stereo is orig_run
+    finally:
+        ft.uninstall()
