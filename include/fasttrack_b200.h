@@ -477,6 +477,11 @@ int ft_host_pack_points(const ft_host_points *p, ft_point_record *out);
 
 int ft_session_create(int32_t device, ft_session **out);
 int ft_session_destroy(ft_session *s);
+/* Accumulated host phase times of the session's stereo / project calls (us):
+ * out[0] pack, [1] issue (copies + launch enqueue), [2] kernel (cudaEvents,
+ * only when FT_SESSION_TIMING was set at creation), [3] synchronise, [4]
+ * unpack, [5] calls.  reset != 0 zeroes them. */
+int ft_session_stats(ft_session *s, double *out, int32_t reset);
 
 /* stereo.py:77-188 with host arrays; mode bits as ft_stereo_pinhole.
  *   PHASE1 alone (match_pinhole_phase1): cand_idx / cand_dist [n_left] out.

@@ -113,7 +113,7 @@ EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_works
            "ft_gather_points", "ft_scatter_points", "ft_copy_ranges", "ft_runner_create", "ft_runner_create_n", "ft_runner_submit", "ft_runner_submit_range", "ft_runner_submit_ranges",
            "ft_runner_wait", "ft_runner_destroy", "ft_runner_create_persistent",
            "ft_track_plan", "ft_track_plan_bytes", "ft_track_frames_ring", "ft_session_create",
-           "ft_session_destroy", "ft_session_stereo", "ft_session_project", "ft_session_fisheye",
+           "ft_session_destroy", "ft_session_stats", "ft_session_stereo", "ft_session_project", "ft_session_fisheye",
            "ft_host_pack_keypoints", "ft_host_pack_points")
 
 

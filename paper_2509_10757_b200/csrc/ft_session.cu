@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 
@@ -32,6 +33,12 @@ struct ft_session {
     void *ws_mem = nullptr;
     ft_workspace ws{};
     int cap_kp = 1024, cap_pts = 1024;  // high-water capacities (workspace geometry)
+    // host-side phase timers (us) accumulated over calls: pack, issue (copies +
+    // launch enqueue), device (kernel, cudaEvents, FT_SESSION_TIMING=1 only),
+    // sync (wait for the stream), unpack; [5] = calls
+    double stats[6] = {0, 0, 0, 0, 0, 0};
+    bool timing = getenv("FT_SESSION_TIMING") != nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -161,6 +168,36 @@ ft_pyramid dev_pyramid(const ft_host_pyramid *p, const uint8_t *dev) {
     return q;
 }
 
+using Clock = std::chrono::steady_clock;
+double us_since(Clock::time_point t) {
+    return std::chrono::duration<double, std::micro>(Clock::now() - t).count();
+}
+
+// Phase timer of one session call (host clock; kernel time by events when
+// the session was created with FT_SESSION_TIMING set).
+struct Phases {
+    ft_session *s;
+    Clock::time_point t;
+    explicit Phases(ft_session *s_) : s(s_), t(Clock::now()) {}
+    void mark(int k) {
+        s->stats[k] += us_since(t);
+        t = Clock::now();
+    }
+    void kernel_begin() {
+        if (s->timing) cudaEventRecord(s->ev[0], s->stream);
+    }
+    void kernel_end() {
+        if (s->timing) cudaEventRecord(s->ev[1], s->stream);
+    }
+    void done() {
+        if (s->timing) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]) == cudaSuccess) s->stats[2] += 1e3 * ms;
+        }
+        s->stats[5] += 1;
+    }
+};
+
 #define FT_TRY(x)                     \
     do {                              \
         const int st_ = (x);          \
@@ -192,6 +229,8 @@ extern "C" int ft_session_create(int32_t device, ft_session **out) {
     s->device = device;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess && s->timing) e = cudaEventCreate(&s->ev[0]);
+    if (e == cudaSuccess && s->timing) e = cudaEventCreate(&s->ev[1]);
     if (e != cudaSuccess) {
         delete s;
         return (int)e;
@@ -207,8 +246,19 @@ extern "C" int ft_session_destroy(ft_session *s) {
     if (s->h) cudaFreeHost(s->h);
     if (s->d) cudaFree(s->d);
     if (s->ws_mem) cudaFree(s->ws_mem);
+    if (s->ev[0]) cudaEventDestroy(s->ev[0]);
+    if (s->ev[1]) cudaEventDestroy(s->ev[1]);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;
+    return FT_OK;
+}
+
+extern "C" int ft_session_stats(ft_session *s, double *out, int32_t reset) {
+    if (!s || !out) return FT_E_NULL;
+    for (int k = 0; k < 6; ++k) {
+        out[k] = s->stats[k];
+        if (reset) s->stats[k] = 0;
+    }
     return FT_OK;
 }
 
@@ -254,6 +304,7 @@ extern "C" int ft_session_stereo(ft_session *s, const ft_host_features *left,
     const size_t o_out = L.add(48 * (size_t)cap);  // right_idx distance disparity refined_u depth sad
     const size_t o_nm = L.add(4);
     FT_TRY(reserve(s, L.total));
+    Phases ph(s);
     char *h = s->h;
     *reinterpret_cast<int32_t *>(h + o_ln) = (int32_t)n;
     *reinterpret_cast<int32_t *>(h + o_rn) = (int32_t)nr;
@@ -277,11 +328,15 @@ extern "C" int ft_session_stereo(ft_session *s, const ft_host_features *left,
         memcpy(o + 5 * 8 * (size_t)cap, matches->sad, 8 * n);
         out_in = 48 * (size_t)cap;
     }
-    FT_TRY(h2d(s, 0, rej_only ? o_rn + 4 : small_end));
+    int64_t b0 = 0;
     if (ref) {  // only the levels phase 2 reads, at their own offsets
-        const int64_t b0 = pyr_first_byte(left_pyr, left);
+        b0 = pyr_first_byte(left_pyr, left);
         memcpy(h + o_pl + b0, left_pyr->data + b0, pl_bytes - b0);
         memcpy(h + o_pr + b0, right_pyr->data + b0, pr_bytes - b0);
+    }
+    ph.mark(0);
+    FT_TRY(h2d(s, 0, rej_only ? o_rn + 4 : small_end));
+    if (ref) {
         FT_TRY(h2d(s, o_pl + b0, pl_bytes - b0));
         FT_TRY(h2d(s, o_pr + b0, pr_bytes - b0));
     }
@@ -307,14 +362,18 @@ extern "C" int ft_session_stereo(ft_session *s, const ft_host_features *left,
     so.depth = reinterpret_cast<double *>(dout + 32 * (size_t)cap);
     so.sad = reinterpret_cast<int64_t *>(dout + 40 * (size_t)cap);
     so.n_matched = reinterpret_cast<int32_t *>(s->d + o_nm);
+    ph.kernel_begin();
     FT_TRY(ft_stereo_pinhole(1, &kl, &kr, ref ? &pl : nullptr, ref ? &pr : nullptr, params, mode,
                              &so, &s->ws, s->stream));
+    ph.kernel_end();
     const bool want_cand = p1 && cand_idx && cand_dist;
     const bool want_m = fin || rej_only;
     if (want_cand) FT_TRY(d2h(s, o_cand, 16 * (size_t)cap));
     if (want_m) FT_TRY(d2h(s, o_out, 48 * (size_t)cap));
+    ph.mark(1);
     const cudaError_t e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) return (int)e;
+    ph.mark(3);
     if (want_cand) {
         memcpy(cand_idx, hc, 8 * n);
         memcpy(cand_dist, hc + cap, 8 * n);
@@ -328,6 +387,8 @@ extern "C" int ft_session_stereo(ft_session *s, const ft_host_features *left,
         memcpy(matches->depth, o + 4 * 8 * (size_t)cap, 8 * n);
         memcpy(matches->sad, o + 5 * 8 * (size_t)cap, 8 * n);
     }
+    ph.mark(4);
+    ph.done();
     return FT_OK;
 }
 
@@ -363,6 +424,7 @@ extern "C" int ft_session_project(ft_session *s, const ft_host_points *points,
     const size_t o_c = L.add(32 * (size_t)cp);                     // corr point | kp | dist | oct
     const size_t o_cnt = L.add(8);                                 // corr_count, slot_count
     FT_TRY(reserve(s, L.total));
+    Phases ph(s);
     char *h = s->h;
     *reinterpret_cast<int32_t *>(h + o_kn) = (int32_t)n_kp;
     pack_kp(frame, reinterpret_cast<ft_kp_record *>(h + o_kr));
@@ -377,6 +439,7 @@ extern "C" int ft_session_project(ft_session *s, const ft_host_points *points,
     if (skip) memcpy(h + o_skip, skip, m);
     if (ref_angles) memcpy(h + o_ref, ref_angles, 8 * m);
     if (slots_in) memcpy(h + o_sl, slots_in, 8 * n_kp);
+    ph.mark(0);
     FT_TRY(h2d(s, 0, in_end));
     char *d = s->d;
     ft_keypoints K{reinterpret_cast<const ft_kp_record *>(d + o_kr),
@@ -416,14 +479,18 @@ extern "C" int ft_session_project(ft_session *s, const ft_host_points *points,
         for (int64_t i = 0; i < m; ++i)
             if (table_index[i] < 0 || table_index[i] >= table_size) return FT_E_RANGE;
     }
+    ph.kernel_begin();
     FT_TRY(ft_project_search(1, &P, &K, params, &io, mode, &po, &s->ws, s->stream));
+    ph.kernel_end();
     const bool want_c = (mode & FT_PROJ_RESOLVE) && out->corr_point;
     if (pa) FT_TRY(d2h(s, o_pa, 24 * (size_t)cp));
     if (want_c) FT_TRY(d2h(s, o_c, 32 * (size_t)cp));
     FT_TRY(d2h(s, o_cnt, 8));
     if (slots_in && out->slots_out) FT_TRY(d2h(s, o_sl, 8 * (size_t)n_kp));
+    ph.mark(1);
     const cudaError_t e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) return (int)e;
+    ph.mark(3);
     if (pa) {
         const int64_t *a = reinterpret_cast<const int64_t *>(h + o_pa);
         if (out->out_kp) memcpy(out->out_kp, a, 8 * m);
@@ -442,6 +509,8 @@ extern "C" int ft_session_project(ft_session *s, const ft_host_points *points,
         memcpy(out->corr_oct, c + 3 * (size_t)cp, 8 * (size_t)cc);
     }
     if (slots_in && out->slots_out) memcpy(out->slots_out, h + o_sl, 8 * n_kp);
+    ph.mark(4);
+    ph.done();
     return FT_OK;
 }
 

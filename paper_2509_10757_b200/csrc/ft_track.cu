@@ -1879,7 +1879,7 @@ namespace {
 // Launch geometry depends only on shapes; cache it so graph capture and
 // steady-state launches make no attribute / occupancy queries.
 struct GeomKey {
-    int dev, F, lcap, rcap, pcap, kcap, H, patch_ints, ncell, hash_bits, ws, wm, reserve;
+    int dev, F, lcap, rcap, pcap, kcap, H, patch_ints, ncell, hash_bits, ws, wm, reserve, rej_only;
     bool operator==(const GeomKey &o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
 };
 struct Geom {
@@ -1895,7 +1895,7 @@ std::mutex g_attr_mu;
 }  // namespace
 
 static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out,
-                          int reserve);
+                          int reserve, bool rej_only);
 
 // The kernel's max-dynamic-smem attribute only ever grows (one attribute per
 // function: lowering it for a small launch would break a cached large one).
@@ -1933,6 +1933,10 @@ static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft
     // persistent plans (tails) leave SMs for the tail blocks and the copies'
     // helper kernels: the whole grid must stay <= SMs - 4 with 2 tail blocks
     key.reserve = tails ? 6 : 0;
+    // stereo without any per-keypoint work (reject_outliers alone): one
+    // block per frame gathers, selects the median and rejects
+    key.rej_only = want_stereo && !want_map &&
+                   !(a.smode & (FT_STEREO_PHASE1 | FT_STEREO_REFINE | FT_STEREO_FROM_CAND));
     Geom g;
     int hit = -1;
     for (int i = 0; i < g_n; ++i)
@@ -1940,7 +1944,7 @@ static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft
     if (hit >= 0) {
         g = g_vals[hit];
     } else {
-        const int st = track_geometry(a, want_stereo, want_map, g, key.reserve);
+        const int st = track_geometry(a, want_stereo, want_map, g, key.reserve, key.rej_only);
         if (st != FT_OK) return st;
         g_keys[g_next] = key;
         g_vals[g_next] = g;
@@ -2077,7 +2081,7 @@ static void stage_policy(TrackArgs &a, bool want_stereo, bool want_map) {
 }
 
 static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out,
-                          int reserve) {
+                          int reserve, bool rej_only) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2090,6 +2094,7 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
                                          ? atoi(getenv("FT_MAP_PTS_PER_BLOCK")) : 84;
     int gm_ideal = want_map ? (a.P.cap + pts_per_block - 1) / pts_per_block : 0;
     if (gs_ideal > 96) gs_ideal = 96;
+    if (rej_only) gs_ideal = 1;
     if (gm_ideal > 64) gm_ideal = 64;
     // the map role's per-point shared arrays (32 B / point of its chunk) must
     // fit: at most TK_MAP_CHUNK_MAX points per map block

@@ -58,6 +58,7 @@ def _bind(L) -> None:
     P = ctypes.POINTER
     L.ft_session_create.argtypes = [i32, P(vp)]
     L.ft_session_destroy.argtypes = [vp]
+    L.ft_session_stats.argtypes = [vp, vp, i32]
     L.ft_session_stereo.argtypes = [vp, P(FtHostFeatures), P(FtHostFeatures), P(FtHostPyramid),
                                     P(FtHostPyramid), P(_lib.FtStereoParams), i32, vp, vp,
                                     P(FtHostMatches)]
@@ -89,6 +90,13 @@ class Session:
         _lib.check(self.lib.ft_session_create(int(device), ctypes.byref(h)), "ft_session_create")
         self.handle = h
         self.lock = threading.Lock()
+
+    def stats(self, reset: bool = False) -> dict:
+        """Host phase times (us, summed over calls) of the native calls."""
+        out = np.zeros(6)
+        _lib.check(self.lib.ft_session_stats(self.handle, out.ctypes.data, int(reset)),
+                   "ft_session_stats")
+        return dict(zip(("pack", "issue", "kernel", "sync", "unpack", "calls"), out.tolist()))
 
     def __del__(self):
         h = getattr(self, "handle", None)
