@@ -384,6 +384,19 @@ int ft_track_plan(int32_t n_frames, const ft_keypoints *left, const ft_keypoints
                   const ft_project_io *io, int32_t pmode, const ft_project_out *pout,
                   const ft_workspace *ws, void *plan, size_t plan_bytes);
 
+/* As ft_track_plan, for a persistent launch of `groups` step groups (1..8):
+ * the geometry gets 1 / groups of the SMs and the launch runs `groups`
+ * disjoint block groups, group g taking steps k = g mod groups -- that many
+ * frames in flight at once.  All plans of one launch share `groups`, and the
+ * slot count must be a multiple of it (FT_E_CONFIG). */
+int ft_track_plan_groups(int32_t n_frames, const ft_keypoints *left, const ft_keypoints *right,
+                         const ft_pyramid *left_pyr, const ft_pyramid *right_pyr,
+                         const ft_stereo_params *sparams, int32_t smode,
+                         const ft_stereo_out *sout, const ft_map_points *points,
+                         const ft_project_params *pparams, const ft_project_io *io,
+                         int32_t pmode, const ft_project_out *pout, const ft_workspace *ws,
+                         int32_t groups, void *plan, size_t plan_bytes);
+
 /* n_steps frames through ONE persistent launch: step k runs plans[k % n_plans]
  * (ft_track_plan records; same shapes), inputs already resident in the
  * plans' buffers, no launch or hand-off between steps (the device-resident

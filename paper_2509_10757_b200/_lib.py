@@ -112,7 +112,7 @@ EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_works
            "ft_pack_keypoints", "ft_pack_points", "ft_build_pyramids", "ft_stereo_fisheye",
            "ft_gather_points", "ft_scatter_points", "ft_copy_ranges", "ft_runner_create", "ft_runner_create_n", "ft_runner_submit", "ft_runner_submit_range", "ft_runner_submit_ranges",
            "ft_runner_wait", "ft_runner_destroy", "ft_runner_create_persistent",
-           "ft_track_plan", "ft_track_plan_bytes", "ft_track_frames_ring", "ft_session_create",
+           "ft_track_plan", "ft_track_plan_groups", "ft_track_plan_bytes", "ft_track_frames_ring", "ft_session_create",
            "ft_session_destroy", "ft_session_stats", "ft_session_stereo", "ft_session_project", "ft_session_fisheye",
            "ft_host_pack_keypoints", "ft_host_pack_points")
 
@@ -169,6 +169,10 @@ def load() -> ctypes.CDLL:
                                 P(FtPyramid), P(FtStereoParams), i32, P(FtStereoOut),
                                 P(FtMapPoints), P(FtProjectParams), P(FtProjectIO), i32,
                                 P(FtProjectOut), W, vp, ctypes.c_size_t]
+    L.ft_track_plan_groups.argtypes = [i32, P(FtKeypoints), P(FtKeypoints), P(FtPyramid),
+                                       P(FtPyramid), P(FtStereoParams), i32, P(FtStereoOut),
+                                       P(FtMapPoints), P(FtProjectParams), P(FtProjectIO), i32,
+                                       P(FtProjectOut), W, i32, vp, ctypes.c_size_t]
     L.ft_project_search.argtypes = [i32, P(FtMapPoints), P(FtKeypoints), P(FtProjectParams),
                                     P(FtProjectIO), i32, P(FtProjectOut), W, vp]
     L.ft_track_frames.argtypes = [i32, P(FtKeypoints), P(FtKeypoints), P(FtPyramid),

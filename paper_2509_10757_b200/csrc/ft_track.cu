@@ -1744,6 +1744,7 @@ constexpr unsigned FT_PERSIST_STOP = 0xffffffffu;
 struct PersistArgs {
     const TrackArgs *args;  // [n] in device memory, identical geometry in every slot
     int n, W, Gs, Gm;
+    int Q;                  // step groups: group g = blocks [g B, (g+1) B) runs steps k = g mod Q
     unsigned max_steps;     // the launch ends after this many steps (or at a stop)
     int gate;               // step k waits for the slot's step k - n to be done (ring)
     int red_arrive;         // arrivals by reduction; the last block publishes done
@@ -1780,15 +1781,20 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
     __syncthreads();
     unsigned mphase = 0, bpar = 0;
     const int per = p.Gs + p.Gm;
-    const unsigned B = (unsigned)(p.W * per);
-    const int wslot = blockIdx.x / per, r = blockIdx.x - wslot * per;
+    const unsigned B = (unsigned)(p.W * per);  // blocks per step group
+    const int grp = (int)(blockIdx.x / B), gb = (int)(blockIdx.x - grp * B);
+    const int wslot = gb / per, r = gb - wslot * per;
     constexpr int ARG_WORDS = (int)(sizeof(TrackArgs) / 8);
     static_assert(sizeof(TrackArgs) % 8 == 0, "TrackArgs copied as 8-byte words");
-    for (unsigned k = 0; k < p.max_steps; ++k) {
+    // Step groups: the Q groups take steps round robin, so Q frames are in
+    // flight at once on disjoint blocks.  Slot i = k mod n is only ever run
+    // by group i mod Q (the host requires Q | n), so its arrival counter and
+    // workspace see one group's blocks.
+    for (unsigned k = (unsigned)grp; k < p.max_steps; k += (unsigned)p.Q) {
         const int i = (int)(k % (unsigned)p.n);
         if (threadIdx.x == 0) {
             unsigned v;
-            if (blockIdx.x == 0) {  // the PCIe watcher
+            if (gb == 0) {  // the group's PCIe watcher
                 while ((v = ld_acquire_sys_u32(p.ready + i)) != FT_PERSIST_STOP && v < k + 1)
                     __nanosleep(100);
                 // the slot's previous step (k - n, same workspace) must be complete:
@@ -1805,7 +1811,7 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
                     __nanosleep(64);
             }
             s_go = v != FT_PERSIST_STOP;
-            if (p.ts && blockIdx.x == 0 && s_go) p.ts[2 * (k & 4095u)] = global_ns();
+            if (p.ts && gb == 0 && s_go) p.ts[2 * (k & 4095u)] = global_ns();
         }
         if (threadIdx.x < ARG_WORDS)  // slot i's arguments -> shared memory
             reinterpret_cast<unsigned long long *>(&s_args)[threadIdx.x] =
@@ -1822,7 +1828,7 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
             // every block but the last one arrives with a release reduction (no
             // round trip); the last block collects them and publishes the step
             if (threadIdx.x == 0) {
-                if (blockIdx.x != (int)B - 1) {
+                if (gb != (int)B - 1) {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     atomicAdd(p.arrive + i, 1u);
                     s_last = 0;
@@ -1879,7 +1885,8 @@ namespace {
 // Launch geometry depends only on shapes; cache it so graph capture and
 // steady-state launches make no attribute / occupancy queries.
 struct GeomKey {
-    int dev, F, lcap, rcap, pcap, kcap, H, patch_ints, ncell, hash_bits, ws, wm, reserve, rej_only;
+    int dev, F, lcap, rcap, pcap, kcap, H, patch_ints, ncell, hash_bits, ws, wm, reserve, rej_only,
+        groups;
     bool operator==(const GeomKey &o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
 };
 struct Geom {
@@ -1895,7 +1902,7 @@ std::mutex g_attr_mu;
 }  // namespace
 
 static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out,
-                          int reserve, bool rej_only);
+                          int reserve, bool rej_only, int groups);
 
 // The kernel's max-dynamic-smem attribute only ever grows (one attribute per
 // function: lowering it for a small launch would break a cached large one).
@@ -1913,7 +1920,7 @@ static int raise_smem_attr(int dev, size_t smem) {
 // Geometry, kernel attribute and workspace pointers of a launch (shared by
 // the per-launch path and the persistent plans).
 static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft_workspace *ws,
-                         Geom &g_out, bool tails) {
+                         Geom &g_out, bool tails, int groups = 1) {
     int dev = 0;
     cudaGetDevice(&dev);
     GeomKey key;
@@ -1937,6 +1944,8 @@ static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft
     // block per frame gathers, selects the median and rejects
     key.rej_only = want_stereo && !want_map &&
                    !(a.smode & (FT_STEREO_PHASE1 | FT_STEREO_REFINE | FT_STEREO_FROM_CAND));
+    // persistent step groups: each group gets 1 / groups of the SMs
+    key.groups = groups < 1 ? 1 : groups;
     Geom g;
     int hit = -1;
     for (int i = 0; i < g_n; ++i)
@@ -1944,7 +1953,8 @@ static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft
     if (hit >= 0) {
         g = g_vals[hit];
     } else {
-        const int st = track_geometry(a, want_stereo, want_map, g, key.reserve, key.rej_only);
+        const int st = track_geometry(a, want_stereo, want_map, g, key.reserve, key.rej_only,
+                                      key.groups);
         if (st != FT_OK) return st;
         g_keys[g_next] = key;
         g_vals[g_next] = g;
@@ -1993,7 +2003,7 @@ static int track_prepare(TrackArgs &a, bool want_stereo, bool want_map, const ft
     // (ft_internal_persist_launch / ft_track_frames_ring refuse more)
     int sms_all = 0;
     cudaDeviceGetAttribute(&sms_all, cudaDevAttrMultiProcessorCount, dev);
-    const int grid_max = key.reserve ? sms_all - 4 : sms_all;
+    const int grid_max = (key.reserve ? sms_all - 4 : sms_all) / key.groups;
     tails = tails || getenv("FT_TAIL_LAUNCH");
     if (tails && want_stereo && a.W >= a.F && !getenv("FT_STEREO_BARRIER")) {
         if (a.W * (a.Gs + 1 + a.Gm) <= grid_max) {
@@ -2081,7 +2091,7 @@ static void stage_policy(TrackArgs &a, bool want_stereo, bool want_map) {
 }
 
 static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &out,
-                          int reserve, bool rej_only) {
+                          int reserve, bool rej_only, int groups) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2118,7 +2128,7 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, track_kernel, TK_THREADS, smem);
         if (occ < 1) return FT_E_RANGE;
-        const int capacity = occ * (sms - reserve);
+        const int capacity = occ * (sms - reserve) / groups;
         const int per_ideal = gs_ideal + gm_ideal;
         int nGs, nGm, nW;
         if ((long long)F * per_ideal <= capacity) {
@@ -2186,8 +2196,9 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
     if (raise_smem_attr(dev, smem) != FT_OK) return FT_E_RANGE;
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, track_kernel, TK_THREADS, smem);
-    while (W > 1 && (long long)W * (Gs + Gm) > (long long)occ * sms) --W;
-    if ((long long)W * (Gs + Gm) > (long long)occ * sms) return FT_E_RANGE;
+    const long long cap_all = (long long)occ * (sms - reserve) / groups;
+    while (W > 1 && (long long)W * (Gs + Gm) > cap_all) --W;
+    if ((long long)W * (Gs + Gm) > cap_all) return FT_E_RANGE;
     out.Gs = Gs;
     out.Gm = Gm;
     out.W = W;
@@ -2345,6 +2356,7 @@ struct TrackPlan {
     uint32_t magic, version;
     TrackArgs a;
     size_t smem;
+    int32_t groups;  // persistent step groups the geometry was sized for
 };
 constexpr uint32_t PLAN_MAGIC = 0x46545450u;  // "FTTP"
 }  // namespace
@@ -2355,6 +2367,16 @@ static int g_plan_tl_hdr[4];
 
 extern "C" size_t ft_track_plan_bytes(void) { return sizeof(TrackPlan); }
 
+extern "C" int ft_track_plan_groups(int32_t n_frames, const ft_keypoints *left,
+                                    const ft_keypoints *right, const ft_pyramid *left_pyr,
+                                    const ft_pyramid *right_pyr, const ft_stereo_params *sparams,
+                                    int32_t smode, const ft_stereo_out *sout,
+                                    const ft_map_points *points,
+                                    const ft_project_params *pparams, const ft_project_io *io,
+                                    int32_t pmode, const ft_project_out *pout,
+                                    const ft_workspace *ws, int32_t groups, void *plan,
+                                    size_t plan_bytes);
+
 extern "C" int ft_track_plan(int32_t n_frames, const ft_keypoints *left,
                              const ft_keypoints *right, const ft_pyramid *left_pyr,
                              const ft_pyramid *right_pyr, const ft_stereo_params *sparams,
@@ -2362,7 +2384,21 @@ extern "C" int ft_track_plan(int32_t n_frames, const ft_keypoints *left,
                              const ft_map_points *points, const ft_project_params *pparams,
                              const ft_project_io *io, int32_t pmode, const ft_project_out *pout,
                              const ft_workspace *ws, void *plan, size_t plan_bytes) {
+    return ft_track_plan_groups(n_frames, left, right, left_pyr, right_pyr, sparams, smode, sout,
+                                points, pparams, io, pmode, pout, ws, 1, plan, plan_bytes);
+}
+
+extern "C" int ft_track_plan_groups(int32_t n_frames, const ft_keypoints *left,
+                                    const ft_keypoints *right, const ft_pyramid *left_pyr,
+                                    const ft_pyramid *right_pyr, const ft_stereo_params *sparams,
+                                    int32_t smode, const ft_stereo_out *sout,
+                                    const ft_map_points *points,
+                                    const ft_project_params *pparams, const ft_project_io *io,
+                                    int32_t pmode, const ft_project_out *pout,
+                                    const ft_workspace *ws, int32_t groups, void *plan,
+                                    size_t plan_bytes) {
     if (!plan) return FT_E_NULL;
+    if (groups < 1 || groups > 8) return FT_E_RANGE;
     if (plan_bytes < sizeof(TrackPlan)) return FT_E_RANGE;
     TrackPlan *tp = static_cast<TrackPlan *>(plan);
     memset(tp, 0, sizeof(*tp));
@@ -2376,7 +2412,7 @@ extern "C" int ft_track_plan(int32_t n_frames, const ft_keypoints *left,
     st = ws_check(ws, n_frames, capl, points->cap);
     if (st != FT_OK) return st;
     Geom g;
-    st = track_prepare(a, true, true, ws, g, true);
+    st = track_prepare(a, true, true, ws, g, true, groups);
     if (st != FT_OK) return st;
     if (getenv("FT_DEBUG_TIMELINE")) {  // debug: every step overwrites one timeline
         const size_t n = (size_t)a.W * (a.Gs + a.Gm) * TL_SLOTS;
@@ -2391,6 +2427,7 @@ extern "C" int ft_track_plan(int32_t n_frames, const ft_keypoints *left,
         }
     }
     tp->smem = g.smem;
+    tp->groups = groups;
     tp->magic = PLAN_MAGIC;
     tp->version = 1;
     return FT_OK;
@@ -2447,13 +2484,17 @@ static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
         if (tp->magic != PLAN_MAGIC) return FT_E_CONFIG;
         host_args[i] = tp->a;
         host_args[i].coherent = coherent;
+        const TrackPlan *t0 = static_cast<const TrackPlan *>(plans[0]);
         if (tp->a.W != host_args[0].W || tp->a.Gs != host_args[0].Gs ||
-            tp->a.Gm != host_args[0].Gm)
+            tp->a.Gm != host_args[0].Gm || tp->groups != t0->groups)
             return FT_E_CONFIG;
         smem = tp->smem > smem ? tp->smem : smem;
     }
     p.args = args_dev;
     p.n = n;
+    p.Q = static_cast<const TrackPlan *>(plans[0])->groups;
+    if (p.Q < 1) p.Q = 1;
+    if (n % p.Q) return FT_E_CONFIG;  // slot i must always run in group i mod Q
     p.W = host_args[0].W;
     p.Gs = host_args[0].Gs;
     p.Gm = host_args[0].Gm;
@@ -2474,7 +2515,7 @@ static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = p.W * (p.Gs + p.Gm);
+    const int grid = p.Q * p.W * (p.Gs + p.Gm);
     if (grid > sms - 4) return FT_E_RANGE;  // keep SMs for the copies' helper kernels
     cudaError_t e = cudaMemcpyAsync(args_dev, host_args.data(), sizeof(TrackArgs) * n,
                                     cudaMemcpyHostToDevice, stream);

@@ -388,18 +388,21 @@ class FramePipeline:
                                             self.pparams, self.pio, self.pmode, self.pout,
                                             self.ws, stream.cuda_stream), "ft_track_frames")
 
-    def plan(self):
+    def plan(self, groups: int = 1):
         """The track launch of this pipeline's step recorded as an
         ft_track_plan (input of the persistent runner); None when the step is
-        more than that one launch (device pyramid build / packed upload)."""
+        more than that one launch (device pyramid build / packed upload).
+        groups > 1: sized for a persistent launch of that many step groups
+        (ft_track_plan_groups: that many frames in flight)."""
         import ctypes
         if self.raw or self.packed:
             return None
         buf = (ctypes.c_ubyte * int(self.lib.ft_track_plan_bytes()))()
-        _lib.check(self.lib.ft_track_plan(self.S, self.kl, self.kr, self.pl, self.pr,
-                                          self.sparams, self.smode, self.sout, self.points,
-                                          self.pparams, self.pio, self.pmode, self.pout,
-                                          self.ws, buf, len(buf)), "ft_track_plan")
+        _lib.check(self.lib.ft_track_plan_groups(self.S, self.kl, self.kr, self.pl, self.pr,
+                                                 self.sparams, self.smode, self.sout,
+                                                 self.points, self.pparams, self.pio,
+                                                 self.pmode, self.pout, self.ws, int(groups),
+                                                 buf, len(buf)), "ft_track_plan_groups")
         return buf
 
     def launch_pyramids(self, stream) -> None:
@@ -515,19 +518,24 @@ class FramePipeline:
         dst.copy_(self.host[:self.in_end])
 
 
-def run_ring(pipes, n_steps: int, stream=None) -> None:
+def run_ring(pipes, n_steps: int, stream=None, groups: int = 1) -> None:
     """n_steps steps over pipelines whose inputs are already on the device, in
     ONE persistent launch (ft_track_frames_ring): step k runs pipes[k % n]'s
-    track step.  Stream-ordered on `stream` (default pipes[0].stream); the
-    outputs stay on the device (read them with copy_outputs())."""
+    track step.  groups > 1: that many disjoint block groups take the steps
+    round robin (that many frames in flight; len(pipes) must be a multiple).
+    Stream-ordered on `stream` (default pipes[0].stream); the outputs stay on
+    the device (read them with copy_outputs())."""
     import ctypes
+    if len(pipes) % groups:
+        raise ValueError("run_ring: the pipeline count must be a multiple of groups")
     plans = []
     for p in pipes:
-        if getattr(p, "_plan", None) is None:
-            p._plan = p.plan()
-            if p._plan is None:
+        cache = p.__dict__.setdefault("_plans", {})
+        if groups not in cache:
+            cache[groups] = p.plan(groups)
+            if cache[groups] is None:
                 raise ValueError("run_ring: each step must be the one track launch")
-        plans.append(p._plan)
+        plans.append(cache[groups])
     arr = (ctypes.c_void_p * len(plans))(*[ctypes.addressof(pl) for pl in plans])
     st = stream if stream is not None else pipes[0].stream
     _lib.check(pipes[0].lib.ft_track_frames_ring(len(plans), arr, int(n_steps), st.cuda_stream),
@@ -578,13 +586,16 @@ class AsyncRunner:
     (ft_runner_create_persistent).  close() ends it after the submitted
     steps; until then the kernel holds its SMs."""
 
-    def __init__(self, pipes, persistent=False):
+    def __init__(self, pipes, persistent=False, groups: int = 1):
         """persistent: False (graph launch per step), True (one persistent
         kernel; raises where the step is not eligible) or "auto" (persistent
-        where eligible, else graph launches; ``self.persistent`` says which)."""
+        where eligible, else graph launches; ``self.persistent`` says which).
+        groups (persistent only): step groups of the persistent kernel --
+        that many steps computed at once on disjoint SMs (len(pipes) must be a
+        multiple)."""
         if persistent == "auto":
             try:
-                self.__init__(pipes, persistent=True)
+                self.__init__(pipes, persistent=True, groups=groups)
                 return
             except (ValueError, _lib.FtError):
                 persistent = False
@@ -602,7 +613,9 @@ class AsyncRunner:
         self.persistent = bool(persistent)
         vpn = ctypes.c_void_p * self.n
         if self.persistent:
-            plans = [p.plan() for p in pipes]
+            if len(pipes) % groups:
+                raise ValueError("persistent runner: slots must be a multiple of groups")
+            plans = [p.plan(groups) for p in pipes]
             if any(pl is None for pl in plans):
                 raise ValueError("persistent runner: each step must be the one track launch "
                                  "(no raw images / packed upload)")

@@ -484,6 +484,52 @@ def test_persistent_runner(workloads, expected, n_streams, use_table):
 
 
 @pytest.mark.timeout(180)
+@pytest.mark.parametrize("groups", [2, 4])
+def test_persistent_runner_groups(workloads, expected, groups):
+    """Persistent runner with step groups: 4 slots, `groups` steps computed at
+    once on disjoint SMs; every step equals the oracle."""
+    from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left) for _ in range(4)]
+    ring = pipes[0].staging_ring(4)
+    ranges = []
+    for k in range(4):
+        w = workloads[k]
+        pipes[0].load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                            slots=expected[k][1])
+        pipes[0].stage_into(ring[k])
+        ranges.append(pipes[0].input_ranges())
+    for p in pipes:
+        p.dev.fill_(0xAB)
+    runner = AsyncRunner(pipes, persistent=True, groups=groups)
+
+    def check(pipe, k):
+        w = workloads[k % 4]
+        m, _, slots, n = expected[k % 4]
+        res = pipe.result(0, len(w.left.u))
+        for f in FIELDS:
+            np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f),
+                                          err_msg=f"step {k} {f}")
+        np.testing.assert_array_equal(res.slots, slots, err_msg=f"step {k}")
+        assert res.n_slots == n
+
+    try:
+        n_steps = 41
+        for k in range(n_steps):
+            if k >= 4:
+                check(runner.wait(k - 4), k - 4)
+            runner.submit(k, ring[k % 4], ranges[k % 4])
+        for k in range(n_steps - 4, n_steps):
+            check(runner.wait(k), k)
+    finally:
+        runner.close()
+    with pytest.raises(ValueError):
+        AsyncRunner(pipes[:3], persistent=True, groups=2)
+
+
+@pytest.mark.timeout(180)
 def test_tail_blocks_per_launch(workloads, expected, monkeypatch):
     """The dedicated stereo-tail / map-resolve blocks (persistent plans' mode)
     forced on ordinary launches: same results as the group-barrier path."""
@@ -495,10 +541,12 @@ def test_tail_blocks_per_launch(workloads, expected, monkeypatch):
 
 
 @pytest.mark.timeout(180)
-def test_resident_ring(workloads, expected):
+@pytest.mark.parametrize("groups", [1, 2, 4])
+def test_resident_ring(workloads, expected, groups):
     """ft_track_frames_ring: 11 steps over 4 resident pipelines in one
-    persistent launch (each pipeline runs 2-3 times); every pipeline's final
-    outputs equal the oracle's."""
+    persistent launch (each pipeline runs 2-3 times), with 1 / 2 / 4 step
+    groups (that many frames in flight on disjoint SMs); every pipeline's
+    final outputs equal the oracle's."""
     import torch
     from paper_2509_10757_b200.pipeline import FramePipeline, run_ring
     w0 = workloads[0]
@@ -509,8 +557,9 @@ def test_resident_ring(workloads, expected):
         p.load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
                      slots=expected[i][1])
         p.dev[:p.in_end].copy_(p.host[:p.in_end])
+        p.dev[p.out_begin:p.out_end].fill_(0x5A)  # nothing stale can pass
     torch.cuda.synchronize()
-    run_ring(pipes, 11)
+    run_ring(pipes, 11, groups=groups)
     pipes[0].synchronize()
     for i, (p, w) in enumerate(zip(pipes, workloads)):
         p.copy_outputs()
@@ -520,7 +569,9 @@ def test_resident_ring(workloads, expected):
             np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f), err_msg=f)
         np.testing.assert_array_equal(res.slots, slots)
         assert res.n_slots == n
-    run_ring(pipes, 0)  # no-op
+    run_ring(pipes, 0, groups=groups)  # no-op
+    with pytest.raises(ValueError):
+        run_ring(pipes[:3], 4, groups=2)  # slots must be a multiple of the groups
 
 
 @pytest.mark.timeout(300)
