@@ -35,6 +35,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+RING_GROUPS = (1, 2, 4, 8)  # persistent step-group counts tried (ft_track_plan_groups)
+PERSIST_GROUPS = (1, 2, 4)  # ... for the 8-slot persistent runner (e2e)
 FALLBACK_HBM = 6650.0
 
 
@@ -430,6 +432,7 @@ def main() -> None:
     # frame's inputs in HBM, together > 2x L2, so back-to-back steps read
     # their inputs cold without a flush between them
     n_res = max(2, min(160, -(-(256 << 20) // pipe.in_end)))
+    n_res = (n_res + 7) // 8 * 8  # a multiple of every step-group count tried
     res_pipes = []
     for i in range(n_res):
         rp = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,
@@ -481,21 +484,42 @@ def main() -> None:
             dist.barrier()
         # ---- value, persistent: the same resident ring through ONE persistent
         # launch (ft_track_frames_ring: no launch or hand-off between steps)
-        ring_ms = None
+        ring_ms, ring_groups, ring_group_ms = None, 1, None
         if not raw:
             try:
                 from paper_2509_10757_b200.pipeline import run_ring
-                run_ring(res_pipes, max(args.warmup, n_res), res_stream)  # plans + warm
+                # step groups (G frames in flight on disjoint SMs): picked in
+                # the warm-up by timing K-step rings at each G, then ONE timed
+                # run at the chosen G
+                g_try = {}
+                for G in RING_GROUPS:
+                    run_ring(res_pipes, max(args.warmup, n_res), res_stream, groups=G)
+                    ts = []
+                    for _ in range(2):
+                        ra, rb = ev(), ev()
+                        ra.record(res_stream)
+                        run_ring(res_pipes, args.steps, res_stream, groups=G)
+                        rb.record(res_stream)
+                        torch.cuda.synchronize()
+                        ts.append(ra.elapsed_time(rb))
+                    g_try[G] = min(ts)
+                ring_groups = min(g_try, key=g_try.get)
+                if dist:  # every rank runs the same G (rank 0's pick)
+                    gt = torch.tensor([ring_groups], device="cuda")
+                    dist.broadcast(gt, 0)
+                    ring_groups = int(gt.item())
+                run_ring(res_pipes, max(args.warmup, n_res), res_stream, groups=ring_groups)
                 torch.cuda.synchronize()
                 if dist:
                     dist.barrier()
                 torch.cuda.synchronize()
                 ra, rb = ev(), ev()
                 ra.record(res_stream)
-                run_ring(res_pipes, args.steps, res_stream)
+                run_ring(res_pipes, args.steps, res_stream, groups=ring_groups)
                 rb.record(res_stream)
                 torch.cuda.synchronize()
                 ring_ms = ra.elapsed_time(rb)
+                ring_group_ms = {str(G): v for G, v in g_try.items()}
             except Exception as exc:  # noqa: BLE001  (reported; graph value stands)
                 print(f"[bench] ring value: {type(exc).__name__}: {exc}", file=sys.stderr)
             if dist:
@@ -574,6 +598,7 @@ def main() -> None:
     # ---- e2e, persistent runner: the same steps through ONE long-lived track
     # kernel (no launch per step; ft_runner_create_persistent)
     persist_ms = persist_lat_ms = None
+    persist_groups, persist_by_g = 1, {}
     if not raw and os.environ.get("FT_BENCH_PERSIST", "1") != "0":
         try:
             from paper_2509_10757_b200.pipeline import AsyncRunner
@@ -585,38 +610,45 @@ def main() -> None:
                 FramePipeline(pipe.cam, n_streams=pipe.S, cap_kp=pipe.cap_kp,
                               cap_points=pipe.cap_pts, pyramid_geometry=pipe.pyr,
                               map_table=table) for _ in range(n_p - len(runner.pipes))]
-            pr = AsyncRunner(ppipes, persistent=True)
-            try:
-                k, tw = 0, time.perf_counter()
-                while k < max(args.warmup, 4 * len(staged) + 2) or time.perf_counter() - tw < 0.3:
-                    if k >= pr.n:
-                        pr.wait(k - pr.n)
-                    pr.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
-                    k += 1
-                for j in range(max(0, k - pr.n), k):
-                    pr.wait(j)
-                k0 = k
-                t0 = time.perf_counter()
-                for k in range(k0, k0 + args.steps):
-                    if k - k0 >= pr.n:
-                        pr.wait(k - pr.n)
-                    pr.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
-                for k in range(max(k0, k0 + args.steps - pr.n), k0 + args.steps):
-                    pr.wait(k)
-                persist_ms = 1e3 * (time.perf_counter() - t0)
-                # per-frame latency: one frame in flight at a time (H2D -> kernel
-                # -> D2H -> host), the real-time tracker's frame-to-result delay
-                lat = []
-                k1 = k0 + args.steps
-                for j in range(min(args.steps, 200)):
-                    k = k1 + j
-                    a = time.perf_counter()
-                    pr.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
-                    pr.wait(k)
-                    lat.append(1e3 * (time.perf_counter() - a))
-                persist_lat_ms = float(np.median(lat)) if lat else None
-            finally:
-                pr.close()
+            persist_by_g = {}
+            for G in PERSIST_GROUPS:
+                pr = AsyncRunner(ppipes, persistent=True, groups=G)
+                try:
+                    k, tw = 0, time.perf_counter()
+                    while (k < max(args.warmup, 4 * len(staged) + 2) or
+                           time.perf_counter() - tw < 0.3):
+                        if k >= pr.n:
+                            pr.wait(k - pr.n)
+                        pr.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
+                        k += 1
+                    for j in range(max(0, k - pr.n), k):
+                        pr.wait(j)
+                    k0 = k
+                    t0 = time.perf_counter()
+                    for k in range(k0, k0 + args.steps):
+                        if k - k0 >= pr.n:
+                            pr.wait(k - pr.n)
+                        pr.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
+                    for k in range(max(k0, k0 + args.steps - pr.n), k0 + args.steps):
+                        pr.wait(k)
+                    persist_by_g[G] = 1e3 * (time.perf_counter() - t0)
+                    if G == 1:
+                        # per-frame latency: one frame in flight at a time (H2D ->
+                        # kernel -> D2H -> host), the real-time tracker's
+                        # frame-to-result delay
+                        lat = []
+                        k1 = k0 + args.steps
+                        for j in range(min(args.steps, 200)):
+                            k = k1 + j
+                            a = time.perf_counter()
+                            pr.submit(k, staged[k % len(staged)], ranges[k % len(staged)])
+                            pr.wait(k)
+                            lat.append(1e3 * (time.perf_counter() - a))
+                        persist_lat_ms = float(np.median(lat)) if lat else None
+                finally:
+                    pr.close()
+            persist_groups = min(persist_by_g, key=persist_by_g.get)
+            persist_ms = persist_by_g[persist_groups]
         except Exception as exc:  # noqa: BLE001  (reported, never fatal)
             print(f"[bench] persistent runner: {type(exc).__name__}: {exc}", file=sys.stderr)
 
@@ -698,7 +730,8 @@ def main() -> None:
                         "and group barriers); see roofline_int and batched"}
     if use_ring:
         roofline = {"bound": "hbm", "kernel": "track_persist_kernel (ft_track_frames_ring, "
-                                              f"{args.steps} frames per launch)",
+                                              f"{args.steps} frames per launch, "
+                                              f"{ring_groups} step groups)",
                     "achieved": ring_ach, "peak": hbm_peak, "unit": "GB/s",
                     "frac": ring_ach / hbm_peak, "traffic": ring_traffic,
                     "traffic_source": "profiles/traffic.json (ncu --set full, per frame x K)",
@@ -724,7 +757,10 @@ def main() -> None:
             "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": value_ms / args.steps,
             "value_method": (f"ONE persistent track launch (ft_track_frames_ring) running the "
-                             f"K steps over {n_res} resident pipelines"
+                             f"K steps over {n_res} resident pipelines in {ring_groups} step "
+                             f"group(s) ({ring_groups} frames in flight on disjoint SMs; G "
+                             "picked in the warm-up from "
+                             f"{list(RING_GROUPS)}, ring ms per G: {ring_group_ms})"
                              if use_ring else
                              f"compute graphs replayed back to back on one stream over {n_res} "
                              "resident pipelines") +
@@ -733,6 +769,7 @@ def main() -> None:
                             "CUDA events around all K steps",
             "value_graph_replays": value_graph,
             "value_persistent_ring": value_ring,
+            "value_ring_groups": ring_groups,
             "latency_ms_per_frame": tot_comp / args.steps,
             "isolated_step": {"value": isolated_value, "unit": "frames/s",
                               "method": "one step at a time: L2 flushed, events, synchronise"},
@@ -749,11 +786,14 @@ def main() -> None:
                                 "persistent": "AsyncRunner(persistent=True), 8 slots: the "
                                               "async schedule with ONE long-lived track "
                                               "kernel handed each step through mapped "
-                                              "host flags (no launch per step); host wall "
-                                              "clock"},
+                                              "host flags (no launch per step), G step "
+                                              "groups (G steps computed at once; best of "
+                                              f"{list(PERSIST_GROUPS)}); host wall clock"},
                     "async_value": e2e_async,
                     "serial_value": e2e_serial,
                     "persistent_value": e2e_persist,
+                    "persistent_groups": persist_groups,
+                    "persistent_ms_by_groups": {str(g): v for g, v in persist_by_g.items()},
                     "latency_ms_per_frame_e2e": persist_lat_ms,
                     "latency_method": "persistent runner, one frame in flight: submit (448 KB "
                                       "H2D) -> kernel -> D2H -> result on the host, median, "
