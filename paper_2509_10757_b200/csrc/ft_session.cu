@@ -64,6 +64,7 @@ int reserve(ft_session *s, size_t bytes) {
         s->h_cap = 0;
         e = cudaHostAlloc((void **)&s->h, cap, cudaHostAllocDefault);
         if (e != cudaSuccess) return (int)e;
+        memset(s->h, 0, cap);  // capacity-strided layouts ship bytes past the counts
         s->h_cap = cap;
     }
     if (bytes > s->d_cap) {
@@ -72,6 +73,7 @@ int reserve(ft_session *s, size_t bytes) {
         s->d = nullptr;
         s->d_cap = 0;
         e = cudaMalloc((void **)&s->d, cap);
+        if (e == cudaSuccess) e = cudaMemsetAsync(s->d, 0, cap, s->stream);
         if (e != cudaSuccess) return (int)e;
         s->d_cap = cap;
     }

@@ -593,6 +593,10 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
                             pr[t] = ld_in(a, g.rp + (g.yi - hw + dy) * g.wr + (xr0 - hs - hw + dx));
                         }
                     }
+                    // every lane's patch elements are stored before any lane
+                    // reads its neighbours' (independent thread scheduling;
+                    // found by compute-sanitizer racecheck)
+                    __syncwarp();
                     if (tlw && lane == 0) a.tl[blockIdx.x * TL_SLOTS + 10] = global_ns();
                     if constexpr (FIXED)
                         ok = p2_sweep_fixed<HW, HS>(a, patch, kp, g, xr0, lane, disp, ur, sad);

@@ -70,10 +70,10 @@ class Runtime:
     def reserve(self, nbytes: int) -> None:
         if nbytes > self._dev.numel():
             cap = _align(max(nbytes, 2 * self._dev.numel(), 1 << 20))
-            self._dev = torch.empty(cap, dtype=torch.uint8, device=self.device)
+            self._dev = torch.zeros(cap, dtype=torch.uint8, device=self.device)
         if nbytes > self._host.numel():
             cap = _align(max(nbytes, 2 * self._host.numel(), 1 << 20))
-            self._host = torch.empty(cap, dtype=torch.uint8).pin_memory()
+            self._host = torch.zeros(cap, dtype=torch.uint8).pin_memory()
             self._hnp = self._host.numpy()
 
     @property
