@@ -441,6 +441,9 @@ class FramePipeline:
                     self.dev[self.out_begin:self.out_end], non_blocking=True)
 
     def run_eager(self, copies: bool = True) -> None:
+        from . import _guard
+        _guard.check(self.device.index if self.device.index is not None else 0,
+                     "FramePipeline.run_eager")
         if copies and self.packed:
             self.pack()
         self._step(copies)
@@ -465,6 +468,9 @@ class FramePipeline:
         self.stream.synchronize()
 
     def replay(self, copies: bool = True) -> None:
+        from . import _guard
+        _guard.check(self.device.index if self.device.index is not None else 0,
+                     "FramePipeline.replay")
         if self.graph is None:
             self.capture()
         if copies and self.packed:
@@ -526,6 +532,8 @@ def run_ring(pipes, n_steps: int, stream=None, groups: int = 1) -> None:
     Stream-ordered on `stream` (default pipes[0].stream); the outputs stay on
     the device (read them with copy_outputs())."""
     import ctypes
+    from . import _guard
+    _guard.check(pipes[0].device.index if pipes[0].device.index is not None else 0, "run_ring")
     if len(pipes) % groups:
         raise ValueError("run_ring: the pipeline count must be a multiple of groups")
     plans = []
@@ -612,6 +620,7 @@ class AsyncRunner:
         self.lib = a.lib
         self.persistent = bool(persistent)
         vpn = ctypes.c_void_p * self.n
+        self._guard_dev = None
         if self.persistent:
             if len(pipes) % groups:
                 raise ValueError("persistent runner: slots must be a multiple of groups")
@@ -633,8 +642,19 @@ class AsyncRunner:
         torch.cuda.synchronize(a.device)
         create = (self.lib.ft_runner_create_persistent if self.persistent
                   else self.lib.ft_runner_create_n)
-        _lib.check(create(self.n, execs, dev_in, a.in_end, dev_out, host_out,
-                          a.out_end - a.out_begin, ctypes.byref(self._r)), "ft_runner_create")
+        from . import _guard
+        dev = a.device.index if a.device.index is not None else torch.cuda.current_device()
+        if self.persistent:
+            _guard.acquire(dev)  # one persistent kernel per GPU
+            self._guard_dev = dev
+        else:
+            _guard.check(dev, "AsyncRunner")
+        try:
+            _lib.check(create(self.n, execs, dev_in, a.in_end, dev_out, host_out,
+                              a.out_end - a.out_begin, ctypes.byref(self._r)), "ft_runner_create")
+        except Exception:
+            self.close()
+            raise
         self._keep = (execs, dev_in, dev_out, host_out, plans)
         self._submit_ranges = self.lib.ft_runner_submit_ranges
         self._wait = self.lib.ft_runner_wait
@@ -687,9 +707,13 @@ class AsyncRunner:
         torch.cuda.synchronize(self.pipes[0].device)
 
     def close(self) -> None:
-        if self._r:
+        if getattr(self, "_r", None):
             self.lib.ft_runner_destroy(self._r)
             self._r = None
+        if getattr(self, "_guard_dev", None) is not None:
+            from . import _guard
+            _guard.release(self._guard_dev)
+            self._guard_dev = None
 
     def __del__(self):
         try:

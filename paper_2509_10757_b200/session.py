@@ -115,6 +115,8 @@ def session() -> Session:
     if not torch.cuda.is_available():
         raise _lib.FtError("no CUDA device: the B200 path has no CPU fallback")
     dev = torch.cuda.current_device()
+    from . import _guard
+    _guard.check(dev, "drop-in call")
     s = _SESSIONS.get(dev)
     if s is None:
         s = _SESSIONS[dev] = Session(dev)

@@ -688,3 +688,35 @@ def test_resident_ring_multi_stream(workloads, expected):
                                               err_msg=f"pipe {i} stream {s} {f}")
             np.testing.assert_array_equal(res.slots, slots)
             assert res.n_slots == n
+
+
+@pytest.mark.timeout(120)
+def test_persistent_runner_guard(workloads, expected):
+    """While a persistent runner holds the GPU's SMs, calls that would need a
+    cooperative track launch raise instead of hanging; after close() they run."""
+    from paper_2509_10757_b200 import _lib
+    from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline, run_ring
+    import paper_2509_10757_b200 as ft
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left) for _ in range(2)]
+    w = workloads[0]
+    pipes[0].load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right)
+    r = AsyncRunner(pipes, persistent=True)
+    try:
+        with pytest.raises(_lib.FtError):
+            ft.compute_stereo_matches(w.left, w.right, w.cam)
+        with pytest.raises(_lib.FtError):
+            pipes[1].replay()
+        with pytest.raises(_lib.FtError):
+            run_ring(pipes, 2)
+        with pytest.raises(_lib.FtError):
+            AsyncRunner(pipes, persistent=True)
+        r.submit(0)
+        r.wait(0)
+    finally:
+        r.close()
+    m = ft.compute_stereo_matches(w.left, w.right, w.cam, scale_pow=w.scale_pow,
+                                  left_pyr=w.pyr_left, right_pyr=w.pyr_right)
+    np.testing.assert_array_equal(m.right_idx, expected[0][0].right_idx)
