@@ -522,6 +522,37 @@ int ft_session_project(ft_session *s, const ft_host_points *points, const ft_poi
                        const double *ref_angles, const int64_t *slots_in, int32_t mode,
                        const ft_host_project_out *out);
 
+/* Device-resident world for update_local_map (localmap.py:42-76, SURVEY
+ * 8(f)-4): keyframe k's observed point ids (KeyFrame.observed_point_ids,
+ * mapping.py:142-145) at kf_obs[kf_off[k] .. kf_off[k+1]), point id p's slot
+ * in the map table at id_slot[p] (-1 absent), ids in [0, id_cap).  All
+ * DEVICE pointers. */
+typedef struct {
+    const int32_t *kf_obs;
+    const int64_t *kf_off;   /* [n_kf + 1] */
+    int32_t n_kf;
+    const int32_t *id_slot;  /* [id_cap] */
+    int64_t id_cap;
+} ft_world_dev;
+
+/* localmap.py:42-76 on the device: seeds = the frame's slotted ids (DEVICE
+ * slots[n_slots], -1 empty); keyframes = those observing any seed; points =
+ * every id they observe.  Outputs (DEVICE): kf_out ascending keyframe
+ * indices, point_out ascending point ids, slot_out (may be NULL) their table
+ * slots, counts[3] = (keyframes, points, 1 if a slot held an id outside
+ * [0, id_cap)).  One block, bitmaps in shared memory: id_cap <= ~0.9M. */
+int ft_update_local_map(const int64_t *slots, int32_t n_slots, const int32_t *kf_obs,
+                        const int64_t *kf_off, int32_t n_kf, const int32_t *id_slot,
+                        int64_t id_cap, int32_t *kf_out, int64_t *point_out, int32_t *slot_out,
+                        int32_t *counts, ft_stream_t stream);
+
+/* ft_update_local_map with the frame's HOST slots and host outputs (up to
+ * out_cap entries each; FT_E_RANGE with counts set when more -- retry with
+ * bigger buffers, or when a slot held an id outside the world). */
+int ft_session_update_local_map(ft_session *s, const int64_t *slots, int64_t n_slots,
+                                const ft_world_dev *world, int64_t out_cap, int32_t *kf_out,
+                                int64_t *point_out, int32_t *slot_out, int32_t *counts);
+
 /* stereo.py:223-273 with host arrays: brute force + ratio test (tri NULL,
  * bruteforce_match_kernel) or + triangulation (ft_stereo_fisheye). */
 int ft_session_fisheye(ft_session *s, const ft_host_features *left,

@@ -506,3 +506,29 @@ def _env_threads() -> int:
         return max(1, int(os.environ.get("FT_ORACLE_THREADS", "1")))
     except ValueError:
         return 1
+
+
+# ---------------------------------------------------------------------------
+# local map gathering
+
+def update_local_map(slots, kf_obs, kf_off, n_kf: int):
+    """localmap.py:42-76 update_local_map over a world given as keyframe
+    observation lists (keyframe k observes kf_obs[kf_off[k]:kf_off[k+1]],
+    KeyFrame.observed_point_ids, mapping.py:142-145): seeds = the frame's
+    slotted ids; keyframes = those observing any seed (a point's
+    observations are exactly the (keyframe, slot) pairs whose keyframe holds
+    it, mapping.py:262-266); points = every id those keyframes observe.
+    Returns (keyframe indices ascending, point ids ascending); empty seeds ->
+    both empty (LocalMap.empty())."""
+    slots = np.asarray(slots, dtype=np.int64)
+    seeds = np.unique(slots[slots != -1])
+    if len(seeds) == 0:
+        return np.empty(0, np.int64), np.empty(0, np.int64)
+    kf_off = np.asarray(kf_off, dtype=np.int64)
+    kf_obs = np.asarray(kf_obs, dtype=np.int64)
+    kfs = [k for k in range(int(n_kf))
+           if np.isin(kf_obs[kf_off[k]:kf_off[k + 1]], seeds, assume_unique=False).any()]
+    if not kfs:
+        return np.empty(0, np.int64), np.empty(0, np.int64)
+    pts = np.unique(np.concatenate([kf_obs[kf_off[k]:kf_off[k + 1]] for k in kfs]))
+    return np.asarray(kfs, dtype=np.int64), pts.astype(np.int64)

@@ -16,7 +16,7 @@ from .stereo import (build_row_buckets, compute_stereo_fisheye_matches, compute_
 from .projection import (frustum_and_cone_check, predict_scale, resolve_conflicts,
                          rotation_consistency_filter, run_phase_a, search_by_projection,
                          search_prev_frame)
-from .localmap import search_local_points
+from .localmap import search_local_points, update_local_map
 from .install import install, uninstall
 
 # ORB-SLAM-style names (BASELINE.json north star)
@@ -33,7 +33,8 @@ __all__ = [
     "match_pinhole_phase1", "matches_from_candidates", "matches_to_csv_rows",
     "refine_match_phase2", "reject_outliers", "triangulate_rays", "frustum_and_cone_check",
     "predict_scale", "resolve_conflicts", "rotation_consistency_filter", "run_phase_a",
-    "search_by_projection", "search_prev_frame", "search_local_points", "SearchByProjection",
+    "search_by_projection", "search_prev_frame", "search_local_points", "update_local_map",
+    "SearchByProjection",
     "SearchLocalPoints", "ComputeStereoMatches", "ComputeStereoFishEyeMatches", "install",
     "uninstall",
 ]

@@ -114,7 +114,8 @@ EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_works
            "ft_runner_wait", "ft_runner_destroy", "ft_runner_create_persistent",
            "ft_track_plan", "ft_track_plan_groups", "ft_track_plan_bytes", "ft_track_frames_ring", "ft_session_create",
            "ft_session_destroy", "ft_session_stats", "ft_session_stereo", "ft_session_project", "ft_session_fisheye",
-           "ft_host_pack_keypoints", "ft_host_pack_points")
+           "ft_host_pack_keypoints", "ft_host_pack_points", "ft_update_local_map",
+           "ft_session_update_local_map")
 
 
 def build(force: bool = False) -> Path:

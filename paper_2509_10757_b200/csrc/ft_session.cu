@@ -567,3 +567,57 @@ extern "C" int ft_session_fisheye(ft_session *s, const ft_host_features *left,
     }
     return FT_OK;
 }
+
+extern "C" int ft_session_update_local_map(ft_session *s, const int64_t *slots, int64_t n_slots,
+                                           const ft_world_dev *world, int64_t out_cap,
+                                           int32_t *kf_out, int64_t *point_out,
+                                           int32_t *slot_out, int32_t *counts) {
+    if (!s || !world || !counts || !kf_out || !point_out || (n_slots > 0 && !slots))
+        return FT_E_NULL;
+    if (n_slots < 0 || out_cap < 0 || world->n_kf < 0) return FT_E_RANGE;
+    cudaSetDevice(s->device);
+    Lay L;
+    const size_t o_sl = L.add(8 * (size_t)n_slots);
+    const size_t o_cnt = L.add(16);
+    const size_t o_kf = L.add(4 * (size_t)std::max<int64_t>(world->n_kf, 1));
+    const size_t o_pt = L.add(8 * (size_t)std::max<int64_t>(world->id_cap, 1));
+    const size_t o_ps = L.add(4 * (size_t)std::max<int64_t>(world->id_cap, 1));
+    FT_TRY(reserve(s, L.total));
+    Phases ph(s);
+    if (n_slots) memcpy(s->h + o_sl, slots, 8 * n_slots);
+    ph.mark(0);
+    FT_TRY(h2d(s, o_sl, 8 * (size_t)n_slots));
+    char *d = s->d;
+    ph.kernel_begin();
+    FT_TRY(ft_update_local_map(reinterpret_cast<const int64_t *>(d + o_sl), (int32_t)n_slots,
+                               world->kf_obs, world->kf_off, world->n_kf, world->id_slot,
+                               world->id_cap, reinterpret_cast<int32_t *>(d + o_kf),
+                               reinterpret_cast<int64_t *>(d + o_pt),
+                               slot_out ? reinterpret_cast<int32_t *>(d + o_ps) : nullptr,
+                               reinterpret_cast<int32_t *>(d + o_cnt), s->stream));
+    ph.kernel_end();
+    // outputs up to out_cap entries in the same round trip; more -> FT_E_RANGE
+    // with the counts set (the caller retries with bigger buffers)
+    const size_t np = (size_t)std::min<int64_t>(out_cap, world->id_cap);
+    const size_t nk = (size_t)std::min<int64_t>(out_cap, world->n_kf);
+    FT_TRY(d2h(s, o_cnt, 16));
+    FT_TRY(d2h(s, o_kf, 4 * nk));
+    FT_TRY(d2h(s, o_pt, 8 * np));
+    if (slot_out) FT_TRY(d2h(s, o_ps, 4 * np));
+    ph.mark(1);
+    const cudaError_t e = cudaStreamSynchronize(s->stream);
+    if (e != cudaSuccess) return (int)e;
+    ph.mark(3);
+    const int32_t *c = reinterpret_cast<const int32_t *>(s->h + o_cnt);
+    counts[0] = c[0];
+    counts[1] = c[1];
+    counts[2] = c[2];
+    if (c[2]) return FT_E_RANGE;  // a slotted id outside the world
+    if ((size_t)c[0] > nk || (size_t)c[1] > np) return FT_E_RANGE;
+    memcpy(kf_out, s->h + o_kf, 4 * (size_t)c[0]);
+    memcpy(point_out, s->h + o_pt, 8 * (size_t)c[1]);
+    if (slot_out) memcpy(slot_out, s->h + o_ps, 4 * (size_t)c[1]);
+    ph.mark(4);
+    ph.done();
+    return FT_OK;
+}

@@ -43,6 +43,7 @@ _TARGETS = {
     "trackfront.localmap": {
         "search_by_projection": _projection.search_by_projection,
         "search_local_points": _localmap.search_local_points,
+        "update_local_map": _localmap.update_local_map,
     },
     "trackfront.tracker": {
         "match_pinhole_phase1": _stereo.match_pinhole_phase1,
@@ -52,6 +53,7 @@ _TARGETS = {
         "match_fisheye": _stereo.match_fisheye,
         "search_prev_frame": _projection.search_prev_frame,
         "search_local_points": _localmap.search_local_points,
+        "update_local_map": _localmap.update_local_map,
     },
 }
 

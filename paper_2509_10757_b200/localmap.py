@@ -16,7 +16,9 @@ import numpy as np
 from .projection import project_search
 from .types import LocalMap, NO_POINT
 
-__all__ = ["LocalMap", "search_local_points"]
+from .worldmap import update_local_map  # noqa: E402,F401  (device update_local_map)
+
+__all__ = ["LocalMap", "search_local_points", "update_local_map"]
 
 
 def search_local_points(local, frame, cam, cfg, scale: float, levels: int, engine=None,
@@ -39,9 +41,17 @@ def search_local_points(local, frame, cam, cfg, scale: float, levels: int, engin
     elif rotation_check:
         rotation_check = False
     before = np.asarray(frame.slots).copy()
-    r = project_search(local.soa, frame, frame.pose, cam, cfg, scale, levels,
-                       ref_angles=ref_angles, rotation=rotation_check, slots=before,
-                       skip_slotted=True, write_slots=True, table=table)
+    tslots = getattr(local, "table_slots", None)
+    if tslots is not None:  # a ResidentLocalMap (worldmap.update_local_map): read in place
+        from .projection import _IdsOnly
+        r = project_search(_IdsOnly(local.point_ids), frame, frame.pose, cam, cfg, scale,
+                           levels, ref_angles=ref_angles, rotation=rotation_check, slots=before,
+                           skip_slotted=True, write_slots=True, table=local.table,
+                           table_slots=tslots)
+    else:
+        r = project_search(local.soa, frame, frame.pose, cam, cfg, scale, levels,
+                           ref_angles=ref_angles, rotation=rotation_check, slots=before,
+                           skip_slotted=True, write_slots=True, table=table)
     after = r["slots"]
     frame.slots[...] = after
     if world is not None:

@@ -143,6 +143,64 @@ class MapTable:
         return n
 
 
+    def gather_soa(self, slots, pool=None) -> "MapPointSoA":
+        """Decompose the records at table ``slots`` into a MapPointSoA (the
+        reference's decompose_map_points, mapping.py:204-235), gathered on the
+        device (ft_gather_points) and copied back once; into the pool's
+        soa_* buffers when a pool is given (localmap.py:67-75)."""
+        from .types import MapPointSoA
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        m = len(slots)
+        if m == 0:
+            return MapPointSoA.empty()
+        with torch.cuda.stream(self.stream):
+            idx = torch.from_numpy(slots).pin_memory().to(self.device, non_blocking=True)
+            cnt = torch.tensor([m], dtype=torch.int32).pin_memory().to(self.device,
+                                                                        non_blocking=True)
+            out = torch.empty(m * _lib.POINT_RECORD.itemsize, dtype=torch.uint8,
+                              device=self.device)
+            st = torch.zeros(1, dtype=torch.int32, device=self.device)
+            _lib.check(self.lib.ft_gather_points(1, self.ptr, self.capacity, idx.data_ptr(),
+                                                 cnt.data_ptr(), m, out.data_ptr(),
+                                                 st.data_ptr(), self.stream.cuda_stream),
+                       "ft_gather_points")
+            host = out.to("cpu", non_blocking=True)
+            hst = st.to("cpu", non_blocking=True)
+        self.stream.synchronize()
+        if int(hst.item()) != 0:
+            raise _lib.FtError("map table gather: slot out of range")
+        rec = host.numpy().view(_lib.POINT_RECORD)
+        fields = (("positions", "pos", (m, 3), np.float64), ("descriptors", "desc", (m, 4), np.uint64),
+                  ("normals", "nrm", (m, 3), np.float64), ("min_distances", "min_dist", (m,),
+                                                            np.float64),
+                  ("max_distances", "max_dist", (m,), np.float64), ("point_ids", "id", (m,),
+                                                                  np.int64))
+        pool_names = {"positions": "soa_positions", "descriptors": "soa_descriptors",
+                      "normals": "soa_normals", "min_distances": "soa_min_d",
+                      "max_distances": "soa_max_d", "point_ids": "soa_ids"}
+        arrs = {}
+        for name, f, shape, dt in fields:
+            dst = pool.acquire(pool_names[name], shape, dt) if pool is not None else \
+                np.empty(shape, dt)
+            dst[...] = rec[f]
+            arrs[name] = dst
+        return MapPointSoA(**arrs)
+
+
+def decompose_points(mps) -> "MapPointSoA":
+    """decompose_map_points (reference mapping.py:204-235) of MapPoint-like
+    objects (point_id, position, descriptor, normal, min_distance,
+    max_distance), host side."""
+    from .types import MapPointSoA
+    return MapPointSoA(
+        positions=np.array([p.position for p in mps], dtype=np.float64).reshape(-1, 3),
+        descriptors=np.array([p.descriptor for p in mps], dtype=np.uint64).reshape(-1, 4),
+        normals=np.array([p.normal for p in mps], dtype=np.float64).reshape(-1, 3),
+        min_distances=np.array([p.min_distance for p in mps], dtype=np.float64),
+        max_distances=np.array([p.max_distance for p in mps], dtype=np.float64),
+        point_ids=np.array([p.point_id for p in mps], dtype=np.int64))
+
+
 class _SubSoA:
     """Row subset of a MapPointSoA-like object (reference field names)."""
 

@@ -621,6 +621,25 @@ class AsyncRunner:
         self.persistent = bool(persistent)
         vpn = ctypes.c_void_p * self.n
         self._guard_dev = None
+        self._r = ctypes.c_void_p()
+        # before anything waits on the device: while a persistent kernel lives,
+        # a device-wide synchronise (below) would never return
+        from . import _guard
+        dev = a.device.index if a.device.index is not None else torch.cuda.current_device()
+        if self.persistent:
+            _guard.acquire(dev)  # one persistent kernel per GPU
+            self._guard_dev = dev
+        else:
+            _guard.check(dev, "AsyncRunner")
+        try:
+            self._setup(pipes, groups, vpn)
+        except Exception:
+            self.close()
+            raise
+
+    def _setup(self, pipes, groups, vpn) -> None:
+        import ctypes
+        a = pipes[0]
         if self.persistent:
             if len(pipes) % groups:
                 raise ValueError("persistent runner: slots must be a multiple of groups")
@@ -638,23 +657,11 @@ class AsyncRunner:
         dev_in = vpn(*[p.dev.data_ptr() for p in pipes])
         dev_out = vpn(*[p.dev.data_ptr() + p.out_begin for p in pipes])
         host_out = vpn(*[p.host.data_ptr() + p.out_begin for p in pipes])
-        self._r = ctypes.c_void_p()
         torch.cuda.synchronize(a.device)
         create = (self.lib.ft_runner_create_persistent if self.persistent
                   else self.lib.ft_runner_create_n)
-        from . import _guard
-        dev = a.device.index if a.device.index is not None else torch.cuda.current_device()
-        if self.persistent:
-            _guard.acquire(dev)  # one persistent kernel per GPU
-            self._guard_dev = dev
-        else:
-            _guard.check(dev, "AsyncRunner")
-        try:
-            _lib.check(create(self.n, execs, dev_in, a.in_end, dev_out, host_out,
-                              a.out_end - a.out_begin, ctypes.byref(self._r)), "ft_runner_create")
-        except Exception:
-            self.close()
-            raise
+        _lib.check(create(self.n, execs, dev_in, a.in_end, dev_out, host_out,
+                          a.out_end - a.out_begin, ctypes.byref(self._r)), "ft_runner_create")
         self._keep = (execs, dev_in, dev_out, host_out, plans)
         self._submit_ranges = self.lib.ft_runner_submit_ranges
         self._wait = self.lib.ft_runner_wait

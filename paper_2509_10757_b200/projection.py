@@ -77,7 +77,8 @@ def _grid_geometry(frame, cam) -> tuple[int, int, int]:
 def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale: float,
                    levels: int, *, skip_mask=None, ref_angles=None, rotation: bool = False,
                    window_px=None, u_offset: float = 0.0, slots=None, skip_slotted=False,
-                   write_slots=False, resolve=True, phase_a_out=False, table=None):
+                   write_slots=False, resolve=True, phase_a_out=False, table=None,
+                   table_slots=None):
     """One fused ``ft_project_search`` launch on one frame, through the
     native session (csrc/ft_session.cu: the reference objects' arrays are
     packed, shipped, searched and the requested outputs copied back in one
@@ -99,9 +100,12 @@ def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale:
         pts = S.points(points, keep)
         tptr, tsize, tidx = None, 0, None
     else:
-        if m and getattr(points, "positions", None) is not None:
-            table.upsert(points.point_ids, points, only_missing=True)
-        tidx = np.ascontiguousarray(table.slots(points.point_ids), np.int32)
+        if table_slots is not None:  # resident local map: slots already known
+            tidx = np.ascontiguousarray(table_slots, np.int32)
+        else:
+            if m and getattr(points, "positions", None) is not None:
+                table.upsert(points.point_ids, points, only_missing=True)
+            tidx = np.ascontiguousarray(table.slots(points.point_ids), np.int32)
         pts = S.FtHostPoints(m, None, None, None, None, None, None)
         tptr, tsize = table.ptr, table.capacity
     mode = 0
@@ -278,14 +282,8 @@ def search_prev_frame(prev, cur, pose, world, cam, cfg: ProjectionSearchConfig, 
     pids = np.asarray(prev.slots[slot_idx], dtype=np.int64)
 
     def decompose(ids):
-        mps = [world.points[int(p)] for p in ids]
-        return MapPointSoA(
-            positions=np.array([p.position for p in mps], dtype=np.float64).reshape(-1, 3),
-            descriptors=np.array([p.descriptor for p in mps], dtype=np.uint64).reshape(-1, 4),
-            normals=np.array([p.normal for p in mps], dtype=np.float64).reshape(-1, 3),
-            min_distances=np.array([p.min_distance for p in mps], dtype=np.float64),
-            max_distances=np.array([p.max_distance for p in mps], dtype=np.float64),
-            point_ids=np.array([p.point_id for p in mps], dtype=np.int64))
+        from .maptable import decompose_points
+        return decompose_points([world.points[int(p)] for p in ids])
 
     if table is None:
         points = decompose(pids)

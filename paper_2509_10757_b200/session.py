@@ -48,6 +48,10 @@ class FtHostProjectOut(ctypes.Structure):
                 ("slots_out", vp), ("slot_count", vp)]
 
 
+class FtWorldDev(ctypes.Structure):
+    _fields_ = [("kf_obs", vp), ("kf_off", vp), ("n_kf", i32), ("id_slot", vp), ("id_cap", i64)]
+
+
 _bound = False
 
 
@@ -67,6 +71,8 @@ def _bind(L) -> None:
                                      P(FtHostProjectOut)]
     L.ft_session_fisheye.argtypes = [vp, P(FtHostFeatures), P(FtHostFeatures), i32,
                                      ctypes.c_double, P(_lib.FtFisheyeTri), vp, vp, vp, vp]
+    L.ft_session_update_local_map.argtypes = [vp, vp, i64, P(FtWorldDev), i64, vp, vp, vp, vp]
+    L.ft_update_local_map.argtypes = [vp, i32, vp, vp, i32, vp, i64, vp, vp, vp, vp, vp]
     L.ft_host_pack_keypoints.argtypes = [P(FtHostFeatures), vp]
     L.ft_host_pack_points.argtypes = [P(FtHostPoints), vp]
     _bound = True

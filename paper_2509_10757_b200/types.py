@@ -302,6 +302,10 @@ class LocalMap:
     def __len__(self) -> int:
         return len(self.point_ids)
 
+    @staticmethod
+    def empty() -> "LocalMap":
+        return LocalMap((), np.empty(0, dtype=np.int64), MapPointSoA.empty())
+
 
 class ImagePyramid:
     """Flat u8 multi-level image: level l at data[offsets[l]:offsets[l+1]],

@@ -632,7 +632,7 @@ def gen_cfg4(trajectory: str) -> dict:
     cur = {"f": -1}
     orig = {k: getattr(T, k) for k in ("match_pinhole_phase1", "matches_from_candidates",
                                         "reject_outliers", "search_prev_frame",
-                                        "search_local_points")}
+                                        "search_local_points", "update_local_map")}
 
     def slot(name):
         return rec.setdefault(cur["f"], {}).setdefault(name, {})
@@ -684,9 +684,23 @@ def gen_cfg4(trajectory: str) -> dict:
                              count=np.int64(n))
         return n
 
+    def w_update(frame, world, pool=None):
+        slots_in = frame.slots.copy()
+        local = orig["update_local_map"](frame, world, pool)
+        soa = local.soa
+        slot("update").update(slots_in=slots_in.astype(np.int32),
+                              n_keyframes=np.int64(len(world.keyframes)),
+                              n_points=np.int64(len(world.points)),
+                              kf_ids=np.asarray(local.keyframe_ids, dtype=np.int32),
+                              ids_digest=digest(np.asarray(local.point_ids, np.int64)),
+                              soa_digest=digest(soa.positions, soa.descriptors, soa.normals,
+                                                soa.min_distances, soa.max_distances,
+                                                soa.point_ids))
+        return local
+
     for k, fn in (("match_pinhole_phase1", w_phase1), ("matches_from_candidates", w_fc),
                   ("reject_outliers", w_rej), ("search_prev_frame", w_prev),
-                  ("search_local_points", w_local)):
+                  ("search_local_points", w_local), ("update_local_map", w_update)):
         setattr(T, k, fn)
     try:
         tr = StereoTracker(seq.cam, tracker=TrackerConfig(max_local_points=40000),
@@ -711,6 +725,14 @@ def gen_cfg4(trajectory: str) -> dict:
          "world_max_d": np.array([p.max_distance for p in pts]),
          "landmark_desc": seq.landmark_desc.copy(), "landmark_angle": seq.landmark_angle.copy(),
          "n_frames": np.int64(len(seq)), "status": np.array(statuses)}
+    # keyframe observation lists (KeyFrame.observed_point_ids, mapping.py:142-145),
+    # immutable once the keyframe exists: kf k's ids at kf_obs[kf_off[k]:kf_off[k+1]]
+    kfs = [tr.world.keyframes[k] for k in sorted(tr.world.keyframes)]
+    assert [kf.kf_id for kf in kfs] == list(range(len(kfs)))
+    obs = [np.asarray(kf.observed_point_ids(), dtype=np.int32) for kf in kfs]
+    d["kf_off"] = np.concatenate([[0], np.cumsum([len(o) for o in obs])]).astype(np.int64)
+    d["kf_obs"] = np.concatenate(obs).astype(np.int32) if obs else np.zeros(0, np.int32)
+    d["kf_frame"] = np.array([kf.frame_id for kf in kfs], dtype=np.int32)
     lens = []
     for i, fr in enumerate(seq.frames):
         for side, f, ids in (("l", fr.left, fr.landmark_ids_left),
@@ -724,6 +746,8 @@ def gen_cfg4(trajectory: str) -> dict:
         r = rec.get(i, {})
         for stage, fields in r.items():
             for k, v in fields.items():
+                if stage == "update" and k == "slots_in":
+                    continue  # == local_slots_in (same frame.slots, tracker.py:345-357)
                 if stage == "local" and k == "local_ids":
                     m = np.zeros(n_pts, dtype=bool)
                     m[v] = True
@@ -737,7 +761,8 @@ def gen_cfg4(trajectory: str) -> dict:
                "total")}
     return {f"cfg4_{trajectory}": {
         "frames": len(seq), "status_counts": {s: statuses.count(s) for s in set(statuses)},
-        "world_points": n_pts, "kps_per_frame_median": int(np.median(lens)),
+        "world_points": n_pts, "keyframes": len(kfs),
+        "kps_per_frame_median": int(np.median(lens)),
         "local_map_median": int(np.median([len(r["local"]["local_ids"]) for r in rec.values()
                                            if "local" in r])),
         "stage_us_median_seq_engine": {k: float(np.median(v)) for k, v in micros.items()}}}

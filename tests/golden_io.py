@@ -154,3 +154,38 @@ class Cfg4:
         n = len(left.u)
         s = np.full(n, -1, np.int64) if slots is None else np.asarray(slots, np.int64).copy()
         return Frame(i, 0.0, left, right, np.full(n, -1.0), s, pose, g)
+
+    def growing_world(self):
+        """The reference WorldMap as the tracker grew it (advance(n_kf, n_pts)
+        before frame i with its update_n_keyframes / update_n_points)."""
+        return _GrowingWorld(self)
+
+
+class _KF:
+    """KeyFrame.observed_point_ids (mapping.py:142-145) of a captured keyframe."""
+
+    def __init__(self, ids):
+        self._ids = ids
+
+    def observed_point_ids(self):
+        return self._ids
+
+
+class _GrowingWorld:
+    """Keyframes and map points appear in creation order (ids sequential);
+    both are immutable once created (the reference tracker only appends)."""
+
+    def __init__(self, seq):
+        self.seq, self.points, self.keyframes = seq, {}, {}
+
+    def advance(self, n_kf, n_pts):
+        from types import SimpleNamespace
+        d = self.seq.d
+        for k in range(len(self.keyframes), n_kf):
+            self.keyframes[k] = _KF(d["kf_obs"][d["kf_off"][k]:d["kf_off"][k + 1]].astype(np.int64))
+        for p in range(len(self.points), n_pts):
+            self.points[p] = SimpleNamespace(point_id=p, position=d["world_positions"][p],
+                                             descriptor=d["world_descriptors"][p],
+                                             normal=d["world_normals"][p],
+                                             min_distance=float(d["world_min_d"][p]),
+                                             max_distance=float(d["world_max_d"][p]))

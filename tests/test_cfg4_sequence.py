@@ -277,3 +277,50 @@ def test_cfg4_install_fused_run_stereo(seq):
         n = len(left.u)
         _check(G.digest(tracker.pool.buf["stereo_idx"][:n], tracker.pool.buf["stereo_dist"][:n]),
                seq.get(i, "stereo_p1"), f"frame {i} pool candidates")
+
+
+def test_cfg4_oracle_update_local_map(oracle, seq):
+    """localmap.py:42-76 (the reference keeps it on the host):
+    the oracle's set restatement over the keyframe observation lists gives the
+    reference tracker's keyframes and ascending point ids on every frame."""
+    for i in range(1, seq.n_frames):
+        kfs, ids = oracle.update_local_map(seq.get(i, "local_slots_in"), seq.d["kf_obs"],
+                                           seq.d["kf_off"], int(seq.get(i, "update_n_keyframes")))
+        _check(kfs.astype(np.int32), seq.get(i, "update_kf_ids"), f"frame {i} keyframes")
+        _check(G.digest(ids), seq.get(i, "update_ids_digest"), f"frame {i} point ids")
+        _check(ids, seq.local_ids(i), f"frame {i} ids == the searched local map")
+
+
+@pytest.mark.gpu
+def test_cfg4_update_local_map_device(seq):
+    """update_local_map on the device (reference
+    localmap.py:42-76) over the growing world of the reference run: keyframe
+    ids and ascending point ids equal the reference's on every frame; the
+    resident local map feeds search_local_points in place (slots equal the
+    reference's); its lazily gathered SoA equals the reference's SoA; only
+    new keyframes / points cross PCIe."""
+    import paper_2509_10757_b200 as ft
+    pcfg, cam = ProjectionSearchConfig(), seq.cam
+    world = seq.growing_world()
+    shipped = []
+    from paper_2509_10757_b200.worldmap import world_table
+    for i in range(1, seq.n_frames):
+        world.advance(int(seq.get(i, "update_n_keyframes")), int(seq.get(i, "update_n_points")))
+        frame = seq.frame(i, seq.pose(i, "local_pose"), seq.get(i, "local_slots_in"))
+        before = world_table(world).bytes_uploaded if i > 1 else 0
+        local = ft.update_local_map(frame, world)
+        shipped.append(world_table(world).bytes_uploaded - before)
+        _check(np.asarray(local.keyframe_ids, np.int32), seq.get(i, "update_kf_ids"),
+               f"frame {i} keyframes")
+        _check(G.digest(np.asarray(local.point_ids, np.int64)), seq.get(i, "update_ids_digest"),
+               f"frame {i} point ids")
+        n = ft.search_local_points(local, frame, cam, pcfg, SCALE, LEVELS)
+        assert n == int(seq.get(i, "local_count")), f"frame {i} count"
+        _check(G.digest(frame.slots), seq.get(i, "local_slots_out"), f"frame {i} slots")
+        if i % 17 == 1:  # the lazily gathered SoA (decompose_map_points order)
+            s = local.soa
+            _check(G.digest(s.positions, s.descriptors, s.normals, s.min_distances,
+                            s.max_distances, s.point_ids), seq.get(i, "update_soa_digest"),
+                   f"frame {i} soa")
+    # the world is mirrored once: per frame only the keyframes / points added since
+    assert max(shipped[1:]) < 0.5 * world_table(world).bytes_uploaded

@@ -29,6 +29,8 @@ def test_install_rebinds_reference_names():
         assert tr.search_local_points is ft.search_local_points
         assert lm.search_by_projection is ft.search_by_projection
         assert tr.match_pinhole_phase1 is ft.match_pinhole_phase1
+        assert tr.update_local_map is ft.update_local_map  # SURVEY 8(f)-4, on the device
+        assert lm.update_local_map is ft.update_local_map
         # the pinhole _run_stereo as one fused call (install(fuse_stereo=True))
         assert "trackfront.tracker.StereoTracker._run_stereo" in done
         assert tr.StereoTracker._run_stereo is not orig_run
