@@ -1219,25 +1219,33 @@ def api_e2e_run(frames, steps: int) -> dict:
 
 def cfg4_sequence_run(steps_cap: int) -> dict:
     """BASELINE configs[3] (cfg4): the reference tracker's 100-frame line
-    sequence (tests/golden/cfg4_line.npz, captured stage inputs) replayed as a
-    DEPENDENT sequence -- one frame at a time, each frame's results back on
-    the host before the next frame starts (the tracker's host logic runs in
-    between) -- ms/frame of the hot-path work per frame:
-    (a) the drop-in seam the tracker calls under install(): _run_stereo as
-        one fused call, search_prev_frame, search_local_points;
-    (b) resident: map points in a MapTable (only new points cross PCIe),
-        search_prev_frame reading the table in place, then stereo + the local
-        search in ONE graph-captured launch (FramePipeline).
-    Every frame's outputs are checked against the reference's digests."""
+    sequence (tests/golden/cfg4_line.npz: every stage call's inputs, the world
+    as it grew) replayed as a DEPENDENT sequence -- one frame at a time, each
+    frame's results back on the host before the next (the tracker's host
+    logic -- pose prediction / refinement, keyframe decisions -- runs in
+    between) -- ms/frame of the hot-path work per frame, through the
+    reference's signatures as install() serves the tracker:
+    (a) dropin: _run_stereo as one fused call, search_prev_frame (prev-frame
+        points decomposed on the host, as the reference), update_local_map on
+        the device (the world mirrored in HBM, only new keyframes / points
+        shipped), search_local_points reading the resident local map in place;
+    (b) dropin_resident_world: (a) with install(resident_world=True):
+        search_prev_frame reads the mirrored world in place;
+    (c) resident: (b), with stereo + the local search as ONE graph-captured
+        launch (FramePipeline on the world table).
+    Every frame's outputs are checked against the reference's digests
+    (outside the timed region); the reference's own per-stage host times for
+    the same sequence are in tests/golden/summary.json."""
     import golden_io as G
     import paper_2509_10757_b200 as ft
-    from paper_2509_10757_b200.maptable import MapTable
     from paper_2509_10757_b200.pipeline import FramePipeline
     from paper_2509_10757_b200.types import ProjectionSearchConfig, StereoMatchConfig
+    from paper_2509_10757_b200.worldmap import world_table
+    from types import SimpleNamespace
+    from paper_2509_10757_b200.install import _fused_run_stereo
     seq = G.Cfg4("line")
     cfg, pcfg, cam = StereoMatchConfig(), ProjectionSearchConfig(), seq.cam
     sp = 1.2 ** np.arange(8, dtype=np.float64)
-    world = seq.world()
     frames = list(range(1, min(seq.n_frames, steps_cap + 1)))
     inputs = {}
     for i in frames:  # host objects built before timing (the tracker has them)
@@ -1246,16 +1254,16 @@ def cfg4_sequence_run(steps_cap: int) -> dict:
                          prev=seq.frame(pf, seq.pose(i, "prev_prev_pose"),
                                         seq.get(i, "prev_prev_slots")),
                          ppose=seq.pose(i, "prev_pose"), cur=seq.frame(i, seq.pose(i, "prev_pose")),
-                         local=seq.local_map(i), lpose=seq.pose(i, "local_pose"),
-                         slots=seq.get(i, "local_slots_in").astype(np.int64))
+                         lpose=seq.pose(i, "local_pose"),
+                         slots=seq.get(i, "local_slots_in").astype(np.int64),
+                         world=(int(seq.get(i, "update_n_keyframes")),
+                                int(seq.get(i, "update_n_points"))))
+        inputs[i]["frame"] = seq.frame(i, inputs[i]["lpose"], inputs[i]["slots"])
     mdig = lambda m: G.digest(*(np.asarray(getattr(m, f), t) for f, t in (  # noqa: E731
         ("right_idx", np.int64), ("distance", np.int64), ("disparity", np.float64),
         ("refined_u", np.float64), ("depth", np.float64), ("sad", np.int64))))
     cdig = lambda c: G.digest(*(np.asarray(getattr(c, f), np.int64) for f in (  # noqa: E731
         "point_idx", "keypoint_idx", "distance", "octave")))
-
-    from types import SimpleNamespace
-    from paper_2509_10757_b200.install import _fused_run_stereo
 
     class _Pool:  # reference BufferPool.acquire (buffers.py:38-52)
         def __init__(self):
@@ -1269,57 +1277,84 @@ def cfg4_sequence_run(steps_cap: int) -> dict:
     tracker = SimpleNamespace(cam=cam, stereo=cfg, pool=_Pool(),
                               extraction=SimpleNamespace(scale_powers=lambda: sp))
 
-    frames_obj = {i: seq.frame(i, inputs[i]["lpose"], inputs[i]["slots"]) for i in frames}
-
-    def seam(i, x):  # the tracker's calls as install() (default) serves them
+    def dropin(i, x, world, pipe=None):
         m = _fused_run_stereo(tracker, x["left"], x["right"], None, None)
         corr, _ = ft.search_prev_frame(x["prev"], x["cur"], x["ppose"], world, cam, pcfg, 1.2, 8)
-        fr = frames_obj[i]
+        fr = x["frame"]
         fr.slots[...] = x["slots"]
-        n = ft.search_local_points(x["local"], fr, cam, pcfg, 1.2, 8)
-        return m, corr, fr.slots, n
+        local = ft.update_local_map(fr, world)
+        n = ft.search_local_points(local, fr, cam, pcfg, 1.2, 8)
+        return m, corr, fr.slots, n, local
 
-    table = MapTable(capacity=32768)
-    pipe = FramePipeline(cam, n_streams=1, cap_kp=2048, cap_points=8192, map_table=table)
-    pipe.capture()
-
-    def resident(i, x):
+    def resident(i, x, world, pipe):
+        table = world_table(world).table
         corr, _ = ft.search_prev_frame(x["prev"], x["cur"], x["ppose"], world, cam, pcfg, 1.2,
                                        8, table=table)
-        pipe.load_frame(0, x["left"], x["right"], x["local"], x["lpose"], slots=x["slots"])
+        fr = x["frame"]
+        fr.slots[...] = x["slots"]
+        local = ft.update_local_map(fr, world)
+        pipe.load_frame(0, x["left"], x["right"], local, x["lpose"], slots=x["slots"])
         pipe.replay()
         pipe.synchronize()
         r = pipe.result(0, len(x["left"].u))
-        return r.matches, corr, r.slots, r.n_slots
+        return r.matches, corr, r.slots, r.n_slots, local
 
     out = {"workload": "cfg4: reference StereoTracker line sequence (12000 landmarks, 0.5 px "
                        f"noise, seed 4), frames 1..{frames[-1]}, ~1200 kps / image, local maps "
-                       f"of ~2100 points; one frame in flight (dependent sequence)"}
-    for name, fn in (("dropin_seam", seam), ("resident_pipeline", resident)):
-        ok, ts, delta0 = True, [], table.bytes_uploaded
-        for rep in range(2):  # pass 0 warms (and fills the table), pass 1 is timed
-            ts = []
+                       "of ~2100 points from the growing world (21 keyframes); one frame in "
+                       "flight (dependent sequence)",
+           "reference_host_us_per_frame_median": None}
+    try:
+        import json as _json
+        summ = _json.loads((ROOT / "tests" / "golden" / "summary.json").read_text())
+        out["reference_host_us_per_frame_median"] = summ["cfg4_line"]["stage_us_median_seq_engine"]
+    except (OSError, KeyError, ValueError):
+        pass
+    from paper_2509_10757_b200 import projection as _proj
+
+    def dropin_rw(i, x, world, pipe=None):  # install(resident_world=True)
+        _proj._RESIDENT_WORLD = True
+        try:
+            return dropin(i, x, world, pipe)
+        finally:
+            _proj._RESIDENT_WORLD = False
+
+    for name, fn in (("dropin", dropin), ("dropin_resident_world", dropin_rw),
+                     ("resident", resident)):
+        best = None
+        for rep in range(2):  # pass 0 warms up (a fresh world: the first frames sync it)
+            world = seq.growing_world()
+            pipe = None
+            if name == "resident":
+                world.advance(*inputs[frames[0]]["world"])
+                pipe = FramePipeline(cam, n_streams=1, cap_kp=2048, cap_points=8192,
+                                     map_table=world_table(world).table)
+                pipe.capture()
+            ts, ok = [], True
             for i in frames:
+                x = inputs[i]
+                world.advance(*x["world"])
                 t0 = time.perf_counter()
-                m, corr, slots, n = fn(i, inputs[i])
+                m, corr, slots, n, local = fn(i, x, world, pipe)
                 ts.append(time.perf_counter() - t0)
                 # checked outside the timed region
                 ok &= (np.array_equal(mdig(m), seq.get(i, "stereo_final")) and
                        np.array_equal(cdig(corr), seq.get(i, "prev_corr_digest")) and
+                       np.array_equal(G.digest(np.asarray(local.point_ids, np.int64)),
+                                      seq.get(i, "update_ids_digest")) and
                        np.array_equal(G.digest(np.asarray(slots, np.int64)),
                                       seq.get(i, "local_slots_out")) and
                        n == int(seq.get(i, "local_count")))
-            if rep == 0:
-                delta0 = table.bytes_uploaded
+            best = (ts, ok, world_table(world).bytes_uploaded)
+        ts, ok, shipped = best
         out[name] = {"ms_per_frame_median": 1e3 * float(np.median(ts)),
                      "ms_per_frame_p90": 1e3 * float(np.percentile(ts, 90)),
                      "frames_per_s": len(ts) / sum(ts), "frames": len(ts),
-                     "bit_exact_vs_reference": bool(ok)}
-        if name == "resident_pipeline":
-            out[name]["map_bytes_uploaded_first_pass"] = int(delta0)
-            out[name]["launches_per_frame"] = 2
-        else:
-            out[name]["launches_per_frame"] = 3
+                     "bit_exact_vs_reference": bool(ok),
+                     "world_bytes_shipped_total": int(shipped),
+                     "stages": "stereo, search_prev_frame, update_local_map, "
+                               "search_local_points",
+                     "launches_per_frame": 3 if name == "resident" else 4}
     return out
 
 

@@ -86,9 +86,16 @@ def _fused_run_stereo(self, left, right, pyr_l, pyr_r):
     return res
 
 
-def install(fuse_stereo: bool = True) -> list[str]:
-    """Rebind the reference's hot-path names; returns the rebound names."""
+def install(fuse_stereo: bool = True, resident_world: bool = False) -> list[str]:
+    """Rebind the reference's hot-path names; returns the rebound names.
+
+    resident_world=True: search_prev_frame reads the previous frame's map
+    points in place from the world mirror that update_local_map keeps in HBM
+    (only new points are uploaded) instead of decomposing them on the host;
+    the tracker's pooled ``soa_out`` is then not filled (the tracker never
+    reads it, tracker.py:304-316)."""
     done = []
+    _projection._RESIDENT_WORLD = bool(resident_world)
     for modname, names in _TARGETS.items():
         mod = importlib.import_module(modname)
         for name, fn in names.items():
@@ -108,6 +115,7 @@ def install(fuse_stereo: bool = True) -> list[str]:
 
 
 def uninstall() -> None:
+    _projection._RESIDENT_WORLD = False
     for (modname, name), orig in _saved.items():
         setattr(importlib.import_module(modname), name, orig)
     _saved.clear()

@@ -233,12 +233,17 @@ class FramePipeline:
                 pyrs = self._h("pyrs", np.uint8, (2, S, pb))
                 pyrs[0, s, :self.pyr_total] = pyr_left.data
                 pyrs[1, s, :self.pyr_total] = pyr_right.data
-        soa = local.soa
         m = len(local.point_ids)
+        soa = local.soa if (self.table is None or getattr(local, "table", None) is not self.table
+                            ) else None
         if m > cp:
             raise ValueError(f"{m} map points exceed capacity {cp}")
         self._h("P_n", np.int32, (S,))[s] = m
-        if self.table is None:
+        if self.table is not None and getattr(local, "table", None) is self.table and \
+                getattr(local, "table_slots", None) is not None:
+            # a ResidentLocalMap of this table (worldmap.update_local_map): slots known
+            self._h("P_idx", np.int32, (S, cp))[s, :m] = local.table_slots
+        elif self.table is None:
             fill_point_records(self._h("P_rec", _lib.POINT_RECORD, (S, cp))[s], soa)
         else:
             # points new to the table are the frame's map delta (uploaded now)

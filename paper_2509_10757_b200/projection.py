@@ -265,6 +265,9 @@ def search_by_projection(points, frame, pose, cam, cfg: ProjectionSearchConfig, 
     return r["corr"]
 
 
+_RESIDENT_WORLD = False  # set by install(resident_world=True)
+
+
 def search_prev_frame(prev, cur, pose, world, cam, cfg: ProjectionSearchConfig, scale: float,
                       levels: int, engine=None, soa_out=None, pool=None, table=None):
     """Match the previous frame's map points into the current frame
@@ -280,6 +283,13 @@ def search_prev_frame(prev, cur, pose, world, cam, cfg: ProjectionSearchConfig, 
     if len(slot_idx) == 0:
         return Correspondences.empty(), np.empty(0, dtype=np.int64)
     pids = np.asarray(prev.slots[slot_idx], dtype=np.int64)
+    if table is None and _RESIDENT_WORLD and world is not None:
+        # install(resident_world=True): the world update_local_map mirrors in
+        # HBM serves the previous frame's points in place (soa_out untouched)
+        from .worldmap import world_table
+        wt = world_table(world)
+        wt.sync(world)
+        table = wt.table
 
     def decompose(ids):
         from .maptable import decompose_points

@@ -74,10 +74,19 @@ class WorldTable:
         shipped = 0
         if len(world.points) != self._n_pts:
             ids = np.fromiter(world.points.keys(), dtype=np.int64, count=len(world.points))
-            missing = np.sort(ids[self.table._lookup(ids) < 0])
+            if len(ids) and int(ids.min()) < 0:
+                raise KeyError("negative map point id")
+            known = np.zeros(len(ids), bool)
+            inside = ids < len(self._h_id_slot)
+            known[inside] = self._h_id_slot[ids[inside]] >= 0
+            missing = np.sort(ids[~known])  # not yet in the id -> slot map
             if len(missing):
-                shipped += self.table.upsert(missing, decompose_points(
-                    [world.points[int(p)] for p in missing]), only_missing=True)
+                # records the table does not hold yet (another caller -- e.g.
+                # search_prev_frame(table=) -- may have uploaded some already)
+                absent = missing[self.table._lookup(missing) < 0]
+                if len(absent):
+                    shipped += self.table.upsert(absent, decompose_points(
+                        [world.points[int(p)] for p in absent]), only_missing=True)
                 hi = int(missing.max()) + 1
                 if hi > len(self._h_id_slot):
                     grow = np.full(max(hi, 2 * len(self._h_id_slot)), -1, np.int32)

@@ -324,3 +324,28 @@ def test_cfg4_update_local_map_device(seq):
                    f"frame {i} soa")
     # the world is mirrored once: per frame only the keyframes / points added since
     assert max(shipped[1:]) < 0.5 * world_table(world).bytes_uploaded
+
+
+@pytest.mark.gpu
+def test_cfg4_prev_frame_resident_world(seq):
+    """install(resident_world=True): search_prev_frame reads the previous
+    frame's points from the world mirror update_local_map keeps in HBM;
+    correspondences and point ids equal the reference's on every frame."""
+    import paper_2509_10757_b200 as ft
+    from paper_2509_10757_b200 import projection as P
+    pcfg, cam = ProjectionSearchConfig(), seq.cam
+    world = seq.growing_world()
+    P._RESIDENT_WORLD = True
+    try:
+        for i in range(1, seq.n_frames):
+            world.advance(int(seq.get(i, "update_n_keyframes")),
+                          int(seq.get(i, "update_n_points")))
+            pf = int(seq.get(i, "prev_prev_frame"))
+            prev = seq.frame(pf, seq.pose(i, "prev_prev_pose"), seq.get(i, "prev_prev_slots"))
+            pose = seq.pose(i, "prev_pose")
+            corr, pids = ft.search_prev_frame(prev, seq.frame(i, pose), pose, world, cam, pcfg,
+                                              SCALE, LEVELS)
+            _check(_cdig(corr), seq.get(i, "prev_corr_digest"), f"frame {i} search_prev_frame")
+            _check(G.digest(np.asarray(pids, np.int64)), seq.get(i, "prev_pids"), f"frame {i}")
+    finally:
+        P._RESIDENT_WORLD = False
