@@ -717,7 +717,13 @@ def main() -> None:
     if use_ring:  # the value region's kernel: one persistent launch over K frames
         ring_traffic = None
         if tf.exists() and S == 1:
-            t = json.loads(tf.read_text()).get("track_persist_kernel_ring", {})
+            tj = json.loads(tf.read_text())
+            # the capture of this launch shape: step groups G, K steps (else the
+            # nearest K of the same G)
+            cands = [v for k, v in tj.items()
+                     if k.startswith(f"track_persist_kernel_ring_g{ring_groups}_k")]
+            t = (min(cands, key=lambda v: abs(v["steps_per_launch"] - args.steps)) if cands
+                 else tj.get("track_persist_kernel_ring", {}) if ring_groups == 1 else {})
             if "dram_bytes_per_frame" in t:
                 ring_traffic = t["dram_bytes_per_frame"] * args.steps
         ring_bytes = dom_bytes * args.steps
