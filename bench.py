@@ -1010,7 +1010,7 @@ def hamming_roofline(torch, _lib, popc_peak_g) -> dict:
     out = {"bound": "popc (XU pipe)", "unit": "G popc/s", "peak": popc_peak_g,
            "peak_source": "ft_bench_popc (measured, same run)",
            "work": f"{nl} x {nr} Hamming per frame, 8 POPC each"}
-    for F in (1, 64):
+    for F in (1, 2, 4, 64):
         recs = np.zeros((2, F, cap), dtype=_lib.KP_RECORD)
         for f in range(F):
             fill_kp_records(recs[0, f], w.left)

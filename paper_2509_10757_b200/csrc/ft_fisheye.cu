@@ -13,10 +13,15 @@
 //   associative and commutative, so the result is the reference's
 //   ascending-j scan -- and applies the ratio test.  On rejection dist = best
 //   (kernels.py:462-464).
+#include <cooperative_groups.h>
+
+#include <cstdlib>
 #include <cstring>
 
 #include "ft_common.cuh"
 #include "ft_ws.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ft {
 
@@ -105,6 +110,71 @@ FT_DEV bool fisheye_triangulate(const ft_fisheye_tri &c, double ul, double vl, d
     return zr > 0;
 }
 
+__device__ void bf_finish(const BfArgs &a, const Best2 &m, int f, int k, int64_t lbase,
+                          int64_t rbase);
+
+// One (left tile, right split) block's scan: best / second over right
+// descriptors [j0, j1) for its BF_TL left keypoints, right descriptors
+// streamed through shared memory (broadcast LDS.128).
+__device__ __forceinline__ void bf_scan(const BfArgs &a, uint4 (*rdesc)[2], int k, int n_left,
+                                        int64_t lbase, int64_t rbase, int j0, int j1, Best2 &b) {
+    Desc ld;
+    if (k < n_left) ld = load_desc(a.L.rec[lbase + k].desc, 0);
+    else ld = Desc{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+    for (int c0 = j0; c0 < j1; c0 += BF_CHUNK) {
+        const int cn = min(BF_CHUNK, j1 - c0);
+        __syncthreads();
+        // descriptor = 2nd and 3rd uint4 of each 64-B record
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.R.rec + rbase + c0);
+        for (int t = threadIdx.x; t < 2 * cn; t += BF_TL)
+            (&rdesc[0][0])[t] = __ldg(src + 4 * (t >> 1) + 1 + (t & 1));
+        __syncthreads();
+#pragma unroll 4
+        for (int jj = 0; jj < cn; ++jj) {
+            Desc rd;
+            rd.lo = rdesc[jj][0];
+            rd.hi = rdesc[jj][1];
+            best2_push(b, hamming(ld, rd), (uint32_t)(c0 + jj));
+        }
+    }
+}
+
+// Latency path (few frames): the right splits of a left tile form ONE thread
+// block cluster; each block leaves its partial (key, second) states in its
+// own shared memory and the cluster's rank-0 block merges them through
+// distributed shared memory -- no global partials, no atomic ticket, no
+// second L2 round trip.  gridDim.y == cluster size == splits.
+__global__ void __launch_bounds__(BF_TL) fisheye_bf_cluster_kernel(const BfArgs a) {
+    __shared__ uint4 rdesc[BF_CHUNK][2];
+    __shared__ uint2 part[BF_TL];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int f = blockIdx.z;
+    const int tile = blockIdx.x, split = blockIdx.y;
+    const int n_left = min(a.L.count[f], a.L.cap);
+    const int n_right = min(a.R.count[f], a.R.cap);
+    if (tile * BF_TL >= n_left) return;  // uniform across the cluster (same tile)
+    const int k = tile * BF_TL + threadIdx.x;
+    const int64_t lbase = (int64_t)f * a.L.cap, rbase = (int64_t)f * a.R.cap;
+    const int j0 = split * a.split_len;
+    const int j1 = min(n_right, j0 + a.split_len);
+    Best2 b;
+    best2_init(b);
+    if (j0 < j1) bf_scan(a, rdesc, k, n_left, lbase, rbase, j0, j1, b);
+    part[threadIdx.x] = make_uint2(b.key, b.second);
+    cluster.sync();  // every block's partials visible cluster-wide
+    if (cluster.block_rank() == 0 && k < n_left) {
+        Best2 m;
+        best2_init(m);
+        const int cs = (int)cluster.num_blocks();
+        for (int r = 0; r < cs; ++r) {
+            const uint2 p = cluster.map_shared_rank(part, r)[threadIdx.x];
+            best2_merge(m, p.x, p.y);
+        }
+        bf_finish(a, m, f, k, lbase, rbase);
+    }
+    cluster.sync();  // keep every block's shared memory alive until rank 0 is done
+}
+
 __global__ void __launch_bounds__(BF_TL) fisheye_bf_kernel(const BfArgs a) {
     __shared__ uint4 rdesc[BF_CHUNK][2];
     __shared__ int flag;
@@ -120,27 +190,7 @@ __global__ void __launch_bounds__(BF_TL) fisheye_bf_kernel(const BfArgs a) {
 
     Best2 b;
     best2_init(b);
-    if (tile_live && j0 < j1) {
-        Desc ld;
-        if (k < n_left) ld = load_desc(a.L.rec[lbase + k].desc, 0);
-        else ld = Desc{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-        for (int c0 = j0; c0 < j1; c0 += BF_CHUNK) {
-            const int cn = min(BF_CHUNK, j1 - c0);
-            __syncthreads();
-            // descriptor = 2nd and 3rd uint4 of each 64-B record
-            const uint4 *src = reinterpret_cast<const uint4 *>(a.R.rec + rbase + c0);
-            for (int t = threadIdx.x; t < 2 * cn; t += BF_TL)
-                (&rdesc[0][0])[t] = __ldg(src + 4 * (t >> 1) + 1 + (t & 1));
-            __syncthreads();
-#pragma unroll 4
-            for (int jj = 0; jj < cn; ++jj) {
-                Desc rd;
-                rd.lo = rdesc[jj][0];
-                rd.hi = rdesc[jj][1];
-                best2_push(b, hamming(ld, rd), (uint32_t)(c0 + jj));
-            }
-        }
-    }
+    if (tile_live && j0 < j1) bf_scan(a, rdesc, k, n_left, lbase, rbase, j0, j1, b);
     if (!tile_live) return;  // whole tile beyond the frame's keypoints
     if (k < n_left)
         a.partials[((int64_t)f * a.splits + split) * a.L.cap + k] = make_uint2(b.key, b.second);
@@ -161,6 +211,14 @@ __global__ void __launch_bounds__(BF_TL) fisheye_bf_kernel(const BfArgs a) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) best2_merge(m, p[u].x, p[u].y);
     }
+    bf_finish(a, m, f, k, lbase, rbase);
+}
+
+// Ratio test + outputs (+ triangulation) of left keypoint k from its merged
+// (key, second) state (kernels.py:459-464; stereo.py:245-268).
+__device__ void bf_finish(const BfArgs &a, const Best2 &m, int f, int k, int64_t lbase,
+                          int64_t rbase) {
+    (void)f;
     const int64_t lk = lbase + k;
     const bool acc = ratio_accept(m, a.t_match, a.ratio);
     if (acc) {
@@ -188,6 +246,20 @@ __global__ void __launch_bounds__(BF_TL) fisheye_bf_kernel(const BfArgs a) {
 }  // namespace ft
 
 using namespace ft;
+
+// Cluster size of the latency path, or 0 for the split-K path: used while the
+// clusters alone fill the GPU with few frames (tiles x CS x F blocks within
+// ~1.5 waves), CS = 16 (non-portable) or 8, at least 32 right keypoints per
+// split.
+static int cluster_splits(int n_frames, int tiles, int cap_right, int only) {
+    for (int cs : {16, 8}) {
+        if (only && cs != only) continue;
+        if (cap_right < 32 * cs) continue;
+        const long long blocks = (long long)tiles * cs * n_frames;
+        if (blocks <= 2 * 148) return cs;
+    }
+    return 0;
+}
 
 static int fisheye_launch(int32_t n_frames, const ft_keypoints *left, const ft_keypoints *right,
                           int32_t t_match, double ratio, const ft_fisheye_tri *tri,
@@ -223,6 +295,35 @@ static int fisheye_launch(int32_t n_frames, const ft_keypoints *left, const ft_k
     a.split_len = (right->cap + a.splits - 1) / a.splits;
     a.counters = ws_ptr<unsigned>(ws, wl.fisheye_counters);
     a.partials = ws_ptr<uint2>(ws, wl.fisheye_partials);
+    // Opt-in (FT_FISHEYE_CLUSTER=8 or 16): one cluster of CS right splits per
+    // left tile, merged through DSMEM.  Measured slower than the split-K path
+    // at 1-2 frames (r2u: 15.8 vs 14.4 us at 1 frame, 22.7 vs 19.4 at 2, equal
+    // at 4), so the split-K path is the default.
+    static const char *ce = getenv("FT_FISHEYE_CLUSTER");
+    const int cs = ce ? cluster_splits(n_frames, tiles, right->cap, atoi(ce)) : 0;
+    if (cs > 0) {
+        static bool attr_done = false;
+        if (!attr_done) {
+            const cudaError_t e = cudaFuncSetAttribute(
+                fisheye_bf_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return (int)e;
+            attr_done = true;
+        }
+        a.splits = cs;
+        a.split_len = (right->cap + cs - 1) / cs;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(tiles, cs, n_frames);
+        cfg.blockDim = dim3(BF_TL);
+        cfg.stream = (cudaStream_t)stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = cs;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return (int)cudaLaunchKernelEx(&cfg, fisheye_bf_cluster_kernel, a);
+    }
     dim3 grid(tiles, a.splits, n_frames);
     fisheye_bf_kernel<<<grid, BF_TL, 0, (cudaStream_t)stream>>>(a);
     return (int)cudaGetLastError();
