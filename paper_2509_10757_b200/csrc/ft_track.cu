@@ -627,6 +627,241 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Software-pipelined per-warp stereo loop for the default 11x11 window /
+// +-5 slide with phase 1 and phase 2 in the launch: the global loads of
+// keypoint j (its record, its left patch, its right strip) are issued as
+// cp.async copies into a per-warp double buffer while keypoint j-1's SAD
+// sweep runs, so a warp's chain per keypoint is ~ max(load latency, compute)
+// instead of their sum.  Per iteration j:
+//   wait record j -> geometry -> cp.async record j+1 -> cp.async left patch j
+//   -> phase 1 (shared memory) -> cp.async right strip j -> wait j-1's
+//   patches -> SAD sweep + parabola of j-1 -> outputs of j-1.
+// Patch rows are copied as whole 16-B chunks (2 per left row, 3 per right
+// row; the bytes of a row start at (row address & 15) inside its chunks);
+// a chunk reaching outside the level's bytes is copied byte by byte (only
+// the in-level bytes).
+// Results are those of stereo_kp<5, 5> (same predicates, same order).
+constexpr int PIPE_LROW = 32, PIPE_RROW = 48;           // bytes per staged row
+constexpr int PIPE_SLOT = 11 * PIPE_LROW + 11 * PIPE_RROW;  // 880 B per keypoint
+struct PipeKp {  // a keypoint between its loads and its SAD (per-warp smem)
+    double u, s;
+    long long xr0, lk;
+    int cand, cdist, state;   // state: 0 no refinement, 1 SAD pending
+    int loff, lw, roff, rw;   // low 4 bits of row 0's address, row pitch (left, right)
+    int pad_;
+};
+constexpr int PIPE_PART = 2 * PIPE_SLOT;                  // SAD partials [121] int
+constexpr int PIPE_STATE = PIPE_PART + 496;               // PipeKp x 2
+constexpr int PIPE_REC = PIPE_STATE + 2 * (int)sizeof(PipeKp);  // ft_kp_record x 2
+constexpr int PIPE_BYTES = PIPE_REC + 2 * 64;
+static_assert(sizeof(PipeKp) == 64, "PipeKp is 64 B");
+static_assert(PIPE_STATE % 16 == 0 && PIPE_REC % 16 == 0, "16-B aligned regions");
+
+FT_DEV void cp_async16(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+                 "l"(gsrc)
+                 : "memory");
+}
+FT_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+FT_DEV void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// One 16-B chunk of pyramid bytes at gsrc (16-B aligned) into shared memory;
+// bytes outside [beg, end) are not read (and left as they are).
+FT_DEV void pipe_chunk(unsigned char *dst, const unsigned char *gsrc, const unsigned char *beg,
+                       const unsigned char *end, bool coherent) {
+    if (gsrc >= beg && gsrc + 16 <= end) {
+        cp_async16(dst, gsrc);
+        return;
+    }
+    for (int b = 0; b < 16; ++b)
+        if (gsrc + b >= beg && gsrc + b < end) dst[b] = coherent ? __ldca(gsrc + b) : __ldg(gsrc + b);
+}
+
+__device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, unsigned char *wb,
+                                   int f, int64_t lbase, int kf, int k1, int64_t rbase,
+                                   int n_right, int lane, unsigned *medh) {
+    constexpr int HW = 5, HS = 5, NW = 11, NR = 21, NOFF = 11, NJOB = NOFF * NW;
+    constexpr int QJ = (NJOB + 31) / 32;
+    const int n = k1 > kf ? (k1 - kf + TK_WARPS - 1) / TK_WARPS : 0;
+    PipeKp *st = reinterpret_cast<PipeKp *>(wb + PIPE_STATE);
+    ft_kp_record *rec = reinterpret_cast<ft_kp_record *>(wb + PIPE_REC);
+    int *part = reinterpret_cast<int *>(wb + PIPE_PART);
+    const bool coh = a.coherent;
+    // prologue: record 0, then two empty groups (every iteration commits 3)
+    if (n > 0 && lane < 4) cp_async16(reinterpret_cast<char *>(rec) + 16 * lane,
+                                      reinterpret_cast<const char *>(a.L.rec + lbase + kf) + 16 * lane);
+    cp_async_commit();
+    cp_async_commit();
+    cp_async_commit();
+    for (int j = 0; j <= n; ++j) {
+        const int sl = j & 1;
+        if (j < n) {
+            const int64_t lk = lbase + kf + (int64_t)j * TK_WARPS;
+            cp_async_wait<2>();  // record j (committed three groups ago)
+            __syncwarp();
+            LeftKp kp;
+            {
+                const ft_kp_record &r = rec[sl];
+                kp.u = r.u;
+                kp.v = r.v;
+                kp.o = r.octave;
+                kp.d = rec_desc(r);
+            }
+            __syncwarp();  // record slot sl is refilled two iterations on
+            if (j + 1 < n && lane < 4)
+                cp_async16(reinterpret_cast<char *>(rec + (sl ^ 1)) + 16 * lane,
+                           reinterpret_cast<const char *>(a.L.rec + lk + TK_WARPS) + 16 * lane);
+            cp_async_commit();
+            // left patch of keypoint j (kernels.py:371-387)
+            const P2Geom g = p2_geom(a, f, kp);
+            unsigned char *lb = wb + sl * PIPE_SLOT;
+            unsigned char *rb = lb + 11 * PIPE_LROW;
+            const unsigned char *lrow0 = g.lp + (g.yi - HW) * g.wl + (g.xi - HW);
+            if (g.left_ok && lane < 2 * NW) {  // chunks bounded by the level's own bytes
+                const unsigned char *row = lrow0 + (lane >> 1) * g.wl;
+                const unsigned char *c0 =
+                    reinterpret_cast<const unsigned char *>((uintptr_t)row & ~(uintptr_t)15);
+                pipe_chunk(lb + (lane >> 1) * PIPE_LROW + 16 * (lane & 1), c0 + 16 * (lane & 1),
+                           g.lp, g.lp + g.wl * a.PL.heights[g.o], coh);
+            }
+            cp_async_commit();
+            int cdist;
+            const int cand = phase1(a, sm, kp, lane, cdist);
+            if (lane == 0 && a.so.cand_idx) {
+                a.so.cand_idx[lk] = cand;
+                a.so.cand_dist[lk] = cdist;
+            }
+            // right strip of the candidate (kernels.py:388-397)
+            int state = 0;
+            long long xr0 = 0;
+            const unsigned char *rrow0 = nullptr;
+            if (cand >= 0 && cand < n_right && g.left_ok) {
+                const double urc = sm.rtab[cand].u;
+                xr0 = round_half_even(urc / g.s);
+                const long long hr = a.PR.heights[g.o];
+                if (!(xr0 - HS - HW < 0 || xr0 + HS + HW >= g.wr || g.yi - HW < 0 ||
+                      g.yi + HW >= hr)) {
+                    state = 1;
+                    rrow0 = g.rp + (g.yi - HW) * g.wr + (xr0 - HS - HW);
+                    for (int c = lane; c < 3 * NW; c += 32) {
+                        const int r = c / 3, q = c - 3 * r;
+                        const unsigned char *row = rrow0 + r * g.wr;
+                        const unsigned char *c0 =
+                            reinterpret_cast<const unsigned char *>((uintptr_t)row & ~(uintptr_t)15);
+                        pipe_chunk(rb + r * PIPE_RROW + 16 * q, c0 + 16 * q, g.rp, g.rp + g.wr * hr,
+                                   coh);
+                    }
+                }
+            }
+            cp_async_commit();
+            if (lane == 0) {
+                PipeKp &q = st[sl];
+                q.u = kp.u;
+                q.s = g.s;
+                q.xr0 = xr0;
+                q.lk = lk;
+                q.cand = cand;
+                q.cdist = cdist;
+                q.state = state;
+                q.loff = (int)((uintptr_t)lrow0 & 15);
+                q.lw = (int)(g.wl & 15);
+                q.roff = (int)((uintptr_t)rrow0 & 15);
+                q.rw = (int)(g.wr & 15);
+            }
+        } else {
+            cp_async_commit();  // keep three groups per iteration
+            cp_async_commit();
+            cp_async_commit();
+        }
+        if (j == 0) continue;
+        // ---- keypoint j - 1: its patches were committed 3-5 groups ago
+        cp_async_wait<3>();
+        __syncwarp();
+        const int ps = sl ^ 1;
+        const PipeKp q = st[ps];
+        bool ok = false;
+        double disp = 0.0, ur = 0.0;
+        int sad = 0;
+        if (q.state) {
+            const unsigned char *lb = wb + ps * PIPE_SLOT;
+            const unsigned char *rb = lb + 11 * PIPE_LROW;
+            // centre pixels: cl = L[yi, xi], cr(oi) = R[yi, xr0 + oi - HS]
+            const int lo5 = (q.loff + HW * q.lw) & 15, ro5 = (q.roff + HW * q.rw) & 15;
+            const int cl = lb[HW * PIPE_LROW + lo5 + HW];
+            int acc[QJ];
+#pragma unroll
+            for (int t = 0; t < QJ; ++t) {
+                const int job = lane + 32 * t;
+                acc[t] = 0;
+                if (job < NJOB) {
+                    const int oi = job / NW, dy = job - oi * NW;
+                    const int lo = (q.loff + dy * q.lw) & 15, ro = (q.roff + dy * q.rw) & 15;
+                    const unsigned char *lr = lb + dy * PIPE_LROW + lo;
+                    const unsigned char *rr = rb + dy * PIPE_RROW + ro + oi;
+                    const int c = (int)rb[HW * PIPE_RROW + ro5 + oi + HW] - cl;  // cr - cl
+#pragma unroll
+                    for (int dx = 0; dx < NW; ++dx) acc[t] += abs((int)lr[dx] + c - (int)rr[dx]);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < QJ; ++t) {
+                const int job = lane + 32 * t;
+                if (job < NJOB) part[job] = acc[t];
+            }
+            __syncwarp();
+            int sv = 0x7fffffff;
+            if (lane < NOFF) {
+                sv = 0;
+#pragma unroll
+                for (int dy = 0; dy < NW; ++dy) sv += part[lane * NW + dy];
+            }
+            const unsigned key = lane < NOFF ? ((unsigned)sv << 5) | (unsigned)lane : 0xffffffffu;
+            const unsigned best = __reduce_min_sync(FULL, key);
+            const int best_oi = (int)(best & 31u), best_sad = (int)(best >> 5);
+            const int s_m = __shfl_sync(FULL, sv, best_oi > 0 ? best_oi - 1 : 0);
+            const int s_p = __shfl_sync(FULL, sv, best_oi < NOFF - 1 ? best_oi + 1 : 0);
+            if (best_oi > 0 && best_oi < NOFF - 1) {  // kernels.py:410-428
+                const double d_m = (double)s_m, d_0 = (double)best_sad, d_p = (double)s_p;
+                const double denom = d_m + d_p - 2.0 * d_0;
+                if (denom > 0.0) {
+                    const double delta = (d_m - d_p) / (2.0 * denom);
+                    if (!(delta < -1.0 || delta > 1.0)) {
+                        const double ur_ref = ((double)(q.xr0 + (best_oi - HS)) + delta) * q.s;
+                        const double dsp = q.u - ur_ref;
+                        if (!(dsp < a.sp.min_disparity || dsp > a.sp.max_disparity)) {
+                            ok = true;
+                            disp = dsp;
+                            ur = ur_ref;
+                            sad = best_sad;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();  // slot ps (patches, partials, state) is refilled next iteration
+        if (lane == 0) {
+            if (ok && medh) {  // SAD-median histogram of the frame (fire-and-forget reds)
+                const uint32_t x = (uint32_t)sad;
+                atomicAdd(medh + (x < MED_FINE ? x / MED_CW : MED_NC), 1u);
+                if (x < MED_FINE) atomicAdd(medh + 128 + x, 1u);
+            }
+            const int64_t lk = q.lk;
+            a.so.right_idx[lk] = ok ? q.cand : -1;
+            a.so.distance[lk] = ok ? q.cdist : 10000;
+            a.so.disparity[lk] = ok ? disp : 0.0;
+            a.so.refined_u[lk] = ok ? ur : 0.0;
+            a.so.depth[lk] = ok ? a.sp.baseline_times_fx / disp : 0.0;
+            a.so.sad[lk] = ok ? sad : 0;
+        }
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+}
+
 // np.median (stereo.py:180) of a group's accepted SADs from its histograms
 // (warp 0): coarse bins locate the bins of ranks (n-1)/2 and n/2, one fine
 // read resolves them.  misc[4] = n, misc[7] = resolved (0: the median lies
@@ -821,6 +1056,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
     p += (size_t)4 * (H + 1);
     sm.row_cursor = reinterpret_cast<int *>(p);
     p += (size_t)4 * H;
+    p = reinterpret_cast<unsigned char *>(((uintptr_t)p + 15) & ~(uintptr_t)15);  // cp.async dst
     sm.patch = reinterpret_cast<int *>(p);
     p += (size_t)4 * TK_WARPS * a.patch_ints;
     sm.items = reinterpret_cast<uint16_t *>(p);
@@ -877,6 +1113,13 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
                                : nullptr;
         int *patch = sm.patch + wid * a.patch_ints;
         const bool fixed55 = a.sp.half_window == 5 && a.sp.half_slide == 5;
+        // default window with both phases here: the software-pipelined loop
+        // (the per-warp timeline debug marks live in stereo_kp only)
+        const bool pipe = fixed55 && do_p1 && do_ref && a.patch_ints * 4 >= PIPE_BYTES;
+        if (pipe) {
+            stereo_warp_pipe55(a, sm, reinterpret_cast<unsigned char *>(patch), f, lbase, kf, k1,
+                               rbase, n_right, lane, medh);
+        } else
         for (int k = kf; k < k1; k += TK_WARPS) {
             const LeftKp kp = k == kf ? kp_first : load_left(a, lbase + k);
             if (fixed55)
@@ -1872,7 +2115,7 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
 
 size_t stereo_smem(const TrackArgs &a) {
     const int cap = a.R.cap, H = a.sp.height;
-    return 16 + stereo_table_bytes(a) + 4 * (32 + 16 + 512) + 4 * (size_t)(2 * H + 1) +
+    return 16 + stereo_table_bytes(a) + 4 * (32 + 16 + 512) + 4 * (size_t)(2 * H + 1) + 16 +
            4 * (size_t)TK_WARPS * a.patch_ints + 4 * (size_t)cap + 64;
 }
 
@@ -2148,12 +2391,18 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
         } else {
             // more frames than one resident wave holds: pick slots W and the
             // stereo / map split minimising the modelled job time
-            //   waves(W) * (c0 + max(stereo rounds * cs, map rounds * cm)),
-            // a stereo round = one keypoint per warp, a map round = one
-            // 512-point staging round (c0, cs, cm: measured us, round 1)
+            //   waves(W) * (c0 + max(cs * keypoints per warp, cm * points per block))
+            // (us; fitted to the persistent ring at 8 step groups, r2j: the
+            // pipelined stereo loop costs ~3.8 us per keypoint per warp at 16
+            // warps / SM, the map role ~15.6 us per 512 points per block;
+            // 17 blocks per frame -> 11 stereo + 6 map, measured best of 4..8
+            // map blocks, 206k vs 167k frames/s for the old 13 + 4)
             const int min_per = (want_stereo ? 1 : 0) + (want_map ? gm_min : 0);
             if (min_per > capacity) return FT_E_RANGE;
-            const double c0 = 8.0, cs = 3.6, cm = 8.0;
+            static const double cs_env = getenv("FT_COST_CS") ? atof(getenv("FT_COST_CS")) : 3.8;
+            static const double cm_env =
+                getenv("FT_COST_CM") ? atof(getenv("FT_COST_CM")) : 15.6 / 512.0;
+            const double c0 = 9.0, cs = cs_env, cm = cm_env;
             double best = 1e30;
             nW = 1;
             nGs = want_stereo ? 1 : 0;
@@ -2164,19 +2413,19 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
                 const int waves = (F + w - 1) / w;
                 const int g_lo = want_map ? gm_min : 0;
                 const int g_hi = want_map ? (want_stereo ? per - 1 : per) : 0;
+                static const int gm_force = getenv("FT_GEOM_GM") ? atoi(getenv("FT_GEOM_GM")) : 0;
                 for (int gm = g_lo; gm <= g_hi; ++gm) {
+                    if (gm_force > 0 && want_stereo && want_map && gm != gm_force) continue;
                     const int gs = want_stereo ? (want_map ? per - gm : per) : 0;
                     if (want_stereo && gs < 1) continue;
                     double t = 0.0;
                     if (want_stereo) {
-                        const int kw = gs * TK_WARPS;
-                        const double r = (double)((a.L.cap + kw - 1) / kw);
-                        t = r * cs;
+                        const double kpw = (double)a.L.cap / (double)(gs * TK_WARPS);
+                        t = (kpw > 1.0 ? kpw : 1.0) * cs;
                     }
                     if (want_map) {
                         const int chunk = (a.P.cap + gm - 1) / gm;
-                        const double r = (double)((chunk + TK_THREADS - 1) / TK_THREADS);
-                        t = t > r * cm ? t : r * cm;
+                        t = t > chunk * cm ? t : chunk * cm;
                     }
                     const double total = waves * (c0 + t);
                     if (total < best * 0.999) {
@@ -2285,6 +2534,12 @@ static bool fill_stereo(TrackArgs &a, int32_t n_frames, const ft_keypoints *left
     a.patch_ints = (mode & FT_STEREO_REFINE)
                        ? nw * nw + nw * nr + (2 * params->half_slide + 1) * nw
                        : 0;
+    // the default window's pipelined loop (stereo_warp_pipe55): its double
+    // buffers, in 16-B units per warp
+    if ((mode & FT_STEREO_REFINE) && params->half_window == 5 && params->half_slide == 5 &&
+        !getenv("FT_STEREO_NOPIPE"))
+        a.patch_ints = a.patch_ints > PIPE_BYTES / 4 ? a.patch_ints : PIPE_BYTES / 4;
+    a.patch_ints = (a.patch_ints + 3) & ~3;
     return true;
 }
 
