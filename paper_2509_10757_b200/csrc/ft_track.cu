@@ -61,7 +61,6 @@ constexpr int TK_WARPS = TK_THREADS / 32;
 constexpr int TK_MAX_BINS = 256;
 constexpr int TK_MAP_CHUNK_MAX = 2048;  // points per map block (shared per-point arrays)
 constexpr long long NO_PID = -1;  // mapping.py:13 NO_POINT
-constexpr long long HASH_EMPTY = (long long)0x8000000000000000ull;
 
 struct TrackArgs {
     int32_t F, W, Gs, Gm;
@@ -684,7 +683,7 @@ FT_DEV void pipe_chunk(unsigned char *dst, const unsigned char *gsrc, const unsi
 __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, unsigned char *wb,
                                    int f, int64_t lbase, int kf, int k1, int64_t rbase,
                                    int n_right, int lane, unsigned *medh) {
-    constexpr int HW = 5, HS = 5, NW = 11, NR = 21, NOFF = 11, NJOB = NOFF * NW;
+    constexpr int HW = 5, HS = 5, NW = 11, NOFF = 11, NJOB = NOFF * NW;
     constexpr int QJ = (NJOB + 31) / 32;
     const int n = k1 > kf ? (k1 - kf + TK_WARPS - 1) / TK_WARPS : 0;
     PipeKp *st = reinterpret_cast<PipeKp *>(wb + PIPE_STATE);
@@ -1038,7 +1037,6 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
     const bool do_fc = a.smode & FT_STEREO_FROM_CAND;
     const bool do_rej = a.smode & FT_STEREO_REJECT;
     const bool finalize = do_ref || do_fc;
-    const int cap_r = a.R.cap;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
     StereoSmem sm;
@@ -1445,15 +1443,26 @@ FT_DEV void stage_points(const TrackArgs &a, const MapSmem &sm, int64_t pbase, i
 }
 
 // Resident-table variant: points [q0, q1) gathered through the slot index
-// into the round buffer by all threads (16-B loads; visible after the
-// caller's next __syncthreads).
+// into the round buffer by all threads (visible after the caller's next
+// __syncthreads).  Two round trips however many points: the round's indices
+// into shared memory (the search queue's space, free until the projection
+// refills it), then every 16-B piece of every record as a cp.async copy, all
+// in flight at once.  (One dependent index + record load per piece in a
+// loop cost ~12 serial round trips per round at 854 points per block: the
+// map role's bottleneck at 8 step groups, r2h.)
 FT_DEV void gather_points(const TrackArgs &a, const MapSmem &sm, const int32_t *pidx, int q0,
                           int q1) {
     uint4 *dst = reinterpret_cast<uint4 *>(sm.prnd);
-    for (int t = threadIdx.x; t < 7 * (q1 - q0); t += TK_THREADS) {
+    int *ix = reinterpret_cast<int *>(sm.queue);
+    const int n = q1 - q0;
+    for (int i = threadIdx.x; i < n; i += TK_THREADS) ix[i] = ld_in(a, pidx + q0 + i);
+    __syncthreads();
+    for (int t = threadIdx.x; t < 7 * n; t += TK_THREADS) {
         const int r = t / 7;
-        dst[t] = ld_in(a, reinterpret_cast<const uint4 *>(a.P.rec + ld_in(a, pidx + q0 + r)) + (t - 7 * r));
+        cp_async16(dst + t, reinterpret_cast<const uint4 *>(a.P.rec + ix[r]) + (t - 7 * r));
     }
+    cp_async_commit();
+    cp_async_wait<0>();
 }
 
 // Tail mode of the map group (one frame per group, resolve without ordered
@@ -1813,8 +1822,9 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                     }
                     sm.res[i - p0] = kp | (d << 16) | (q.lvl << 25);
                     sm.res_pid[i - p0] = qpid;
-                    if (write_slots)
-                        sm.res_empty[i - p0] = ld_in(a, a.io.slots_in + kbase + kp) == NO_PID;
+                    if (write_slots)  // staged copy of slots_in when the hash set uses it
+                        sm.res_empty[i - p0] =
+                            (use_hash ? sm.kslots[kp] : ld_in(a, a.io.slots_in + kbase + kp)) == NO_PID;
                     if (resolve)
                         atomicMin(a.claims + kbase + kp, ((unsigned long long)epoch_hi << 32) |
                                                              ((unsigned long long)d << 23) |
@@ -2391,18 +2401,14 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
         } else {
             // more frames than one resident wave holds: pick slots W and the
             // stereo / map split minimising the modelled job time
-            //   waves(W) * (c0 + max(cs * keypoints per warp, cm * points per block))
-            // (us; fitted to the persistent ring at 8 step groups, r2j: the
-            // pipelined stereo loop costs ~3.8 us per keypoint per warp at 16
-            // warps / SM, the map role ~15.6 us per 512 points per block;
-            // 17 blocks per frame -> 11 stereo + 6 map, measured best of 4..8
-            // map blocks, 206k vs 167k frames/s for the old 13 + 4)
+            //   waves(W) * max(t_stereo, t_map)
+            //   t_stereo = 8.8 + 4.14 * keypoints per warp
+            //   t_map    = 11.4 + 2.28 * 512-point rounds + 0.0205 * points per block
+            // (us per frame of a group; fitted to the persistent ring at 4 and
+            // 8 step groups over forced splits, r2k: picks 11 or 12 map blocks of
+            // 35 and 5 of 17, the measured optima)
             const int min_per = (want_stereo ? 1 : 0) + (want_map ? gm_min : 0);
             if (min_per > capacity) return FT_E_RANGE;
-            static const double cs_env = getenv("FT_COST_CS") ? atof(getenv("FT_COST_CS")) : 3.8;
-            static const double cm_env =
-                getenv("FT_COST_CM") ? atof(getenv("FT_COST_CM")) : 15.6 / 512.0;
-            const double c0 = 9.0, cs = cs_env, cm = cm_env;
             double best = 1e30;
             nW = 1;
             nGs = want_stereo ? 1 : 0;
@@ -2421,13 +2427,15 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
                     double t = 0.0;
                     if (want_stereo) {
                         const double kpw = (double)a.L.cap / (double)(gs * TK_WARPS);
-                        t = (kpw > 1.0 ? kpw : 1.0) * cs;
+                        t = 8.8 + 4.14 * (kpw > 1.0 ? kpw : 1.0);
                     }
                     if (want_map) {
                         const int chunk = (a.P.cap + gm - 1) / gm;
-                        t = t > chunk * cm ? t : chunk * cm;
+                        const int rounds = (chunk + TK_THREADS - 1) / TK_THREADS;
+                        const double tm = 11.4 + 2.28 * rounds + 0.0205 * chunk;
+                        t = t > tm ? t : tm;
                     }
-                    const double total = waves * (c0 + t);
+                    const double total = waves * t;
                     if (total < best * 0.999) {
                         best = total;
                         nW = w;
