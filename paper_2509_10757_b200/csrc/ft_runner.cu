@@ -28,7 +28,10 @@
 //                d2h[i] complete -> step k is out (atomic counter)
 //   wait(k)    : (caller) spins on that counter -- no CUDA call
 // The pump's API calls run beside the caller's, so a step costs the caller
-// one copy + one event record.
+// one copy + one event record.  Push mode (default when host_out is pinned
+// and device-mapped): the kernel's last block writes the outputs into
+// host_out itself before publishing done, so the pump only watches done --
+// no D2H copy, stream or event per step.
 // No stream memory operations: each costs several microseconds of stream
 // time, and one per step on the H2D stream capped the step rate.
 #include <cuda_runtime.h>
@@ -44,7 +47,9 @@
 
 extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
                                           const unsigned *h_ready, unsigned *h_done,
-                                          void **args_out, cudaStream_t stream);
+                                          void **args_out, cudaStream_t stream,
+                                          void *const *push_dev, void *const *push_host,
+                                          size_t push_bytes);
 extern "C" void ft_internal_persist_dump(void);
 
 namespace {
@@ -79,6 +84,7 @@ struct ft_runner {
     void *dev_out[FT_RUNNER_MAX_SLOTS];
     void *host_out[FT_RUNNER_MAX_SLOTS];
     size_t in_bytes, out_bytes;
+    bool push;  // persistent: the kernel writes the outputs to host_out itself
 };
 
 extern "C" int ft_runner_create_n(int32_t n_slots, const void *const *graph_exec,
@@ -160,10 +166,30 @@ extern "C" int ft_runner_create_persistent(int32_t n_slots, const void *const *p
     for (int q = 0; q + 1 < r->n_h2d && e == cudaSuccess; ++q)
         e = cudaStreamCreateWithFlags(&r->h2dx[q], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamSynchronize(r->comp);
+    // push mode: the kernel's last block of a step writes the outputs into
+    // host_out (pinned, device-mapped) with its own stores -- no D2H copy,
+    // event or pump call per step (FT_RUNNER_PUSH=0 turns it off)
+    void *hout_dev[PERSIST_MAX_SLOTS] = {nullptr};
+    {
+        const char *ev = getenv("FT_RUNNER_PUSH");
+        r->push = !(ev && atoi(ev) == 0);
+        for (int i = 0; i < n_slots && r->push; ++i) {
+            cudaPointerAttributes at;
+            if (cudaPointerGetAttributes(&at, host_out[i]) != cudaSuccess ||
+                at.type != cudaMemoryTypeHost || !at.devicePointer ||
+                (((uintptr_t)at.devicePointer | (uintptr_t)dev_out[i]) & 15u)) {
+                cudaGetLastError();
+                r->push = false;  // not device-mapped / aligned: the copy engine moves them
+            } else {
+                hout_dev[i] = at.devicePointer;
+            }
+        }
+    }
     if (e == cudaSuccess) {
         st = ft_internal_persist_launch(plans, n_slots, r->flags, r->hflags_dev,
                                         r->hflags_dev + PERSIST_MAX_SLOTS, &r->args_dev,
-                                        r->comp);
+                                        r->comp, r->push ? dev_out : nullptr,
+                                        r->push ? hout_dev : nullptr, out_bytes);
         if (st != FT_OK) {  // no kernel to stop
             ft_runner_destroy(r);
             *out = nullptr;
@@ -203,6 +229,18 @@ static int persist_pump(ft_runner *r) {
         } else if (q != cudaErrorNotReady) {
             return -(int)q;
         }
+    }
+    if (r->push && r->next_d2h < r->next_ready) {  // outputs written by the kernel
+        const int i = (int)(r->next_d2h % r->n);
+        const uint32_t want = (uint32_t)(r->next_d2h + 1);
+        if ((int32_t)(r->hflags[PERSIST_MAX_SLOTS + i] - want) >= 0) {
+            std::atomic_thread_fence(std::memory_order_acquire);
+            r->out_k.store(r->next_d2h, std::memory_order_release);
+            ++r->next_d2h;
+            r->next_out = r->next_d2h;
+            moved = 1;
+        }
+        return moved;
     }
     if (r->next_d2h < r->next_ready) {
         const int i = (int)(r->next_d2h % r->n);

@@ -2010,7 +2010,39 @@ struct PersistArgs {
     unsigned *done;         // [n] host-mapped: step + 1 whose outputs are complete
     unsigned *arrive;       // [n] block arrivals (monotonic)
     unsigned long long *ts;  // debug (FT_DEBUG_PERSIST): [4096][2] step start / done (ns)
+    // push mode (runner): the step's last block writes the slot's outputs
+    // into its pinned host range itself (no D2H copy / event per step)
+    unsigned long long out_bytes;
+    unsigned long long out_dev[PERSIST_MAX_SLOTS];   // slot output ranges (device)
+    unsigned long long out_host[PERSIST_MAX_SLOTS];  // ... their pinned host ranges
 };
+
+// Push mode, step end (the step's last block, after every arrival): the
+// slot's outputs -> its pinned host range with 16-B stores over PCIe (posted
+// writes), ordered before done for the host: the block's stores are
+// performed relative to thread 0 at the barrier, and thread 0's release
+// store of done at system scope is cumulative over them.  (A fence.sc.sys
+// per thread serialises, ~0.5 us each.)
+__device__ void push_outputs(const PersistArgs &p, int i) {
+    constexpr int U = 8;  // 16-B loads in flight per thread
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(p.out_dev[i]);
+    uint4 *d4 = reinterpret_cast<uint4 *>(p.out_host[i]);
+    const unsigned long long nv = p.out_bytes >> 4;
+    for (unsigned long long t = threadIdx.x; t < nv; t += U * TK_THREADS) {
+        uint4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (t + u * TK_THREADS < nv) x[u] = __ldcg(s4 + t + u * TK_THREADS);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (t + u * TK_THREADS < nv) d4[t + u * TK_THREADS] = x[u];
+    }
+    const char *sb = reinterpret_cast<const char *>(p.out_dev[i]);
+    char *db = reinterpret_cast<char *>(p.out_host[i]);
+    for (unsigned long long x = (nv << 4) + threadIdx.x; x < p.out_bytes; x += TK_THREADS)
+        db[x] = __ldcg(sb + x);
+    __syncthreads();
+}
 
 FT_DEV unsigned ld_acquire_u32(const unsigned *p) {
     unsigned v;
@@ -2030,6 +2062,9 @@ FT_DEV unsigned ld_acquire_sys_u32(const unsigned *p) {
 // 48-108 B inside the callees) but the resident ring measured 3 % slower
 // (r2o: 12.48 vs 12.07 us per frame at G = 1, 6.95 vs 6.75 at G = 4); the
 // spill slots stay in L1.)
+// PUSH: the push-mode instantiation (the default one carries none of its
+// code, so its register allocation is unchanged)
+template <bool PUSH>
 __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_constant__ PersistArgs p) {
     extern __shared__ __align__(16) unsigned char smem_all[];
     __shared__ int s_go, s_last;
@@ -2111,6 +2146,7 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
         }
         __syncthreads();
         if (s_last) {
+            if (PUSH) push_outputs(p, i);
             if (threadIdx.x == 0) {
                 asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done + i), "r"(k + 1u)
                              : "memory");
@@ -2744,11 +2780,24 @@ extern "C" void ft_internal_persist_dump(void) {
 static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
                           std::vector<TrackArgs> &host_args, const unsigned *ready,
                           unsigned *dready, unsigned *done, unsigned *arrive, unsigned max_steps,
-                          int gate, int coherent, cudaStream_t stream) {
+                          int gate, int coherent, cudaStream_t stream,
+                          void *const *push_dev = nullptr, void *const *push_host = nullptr,
+                          size_t push_bytes = 0) {
     if (!plans || !args_dev || !ready || !dready || !done || !arrive) return FT_E_NULL;
     if (n < 1) return FT_E_RANGE;
     PersistArgs p;
     memset(&p, 0, sizeof(p));
+    const bool push = push_dev && push_host;
+    if (push) {
+        if (n > PERSIST_MAX_SLOTS) return FT_E_RANGE;
+        p.out_bytes = push_bytes;
+        for (int i = 0; i < n; ++i) {
+            p.out_dev[i] = (unsigned long long)(uintptr_t)push_dev[i];
+            p.out_host[i] = (unsigned long long)(uintptr_t)push_host[i];
+            if (!p.out_dev[i] || !p.out_host[i]) return FT_E_NULL;
+            if ((p.out_dev[i] | p.out_host[i]) & 15ull) return FT_E_CONFIG;  // 16-B vectors
+        }
+    }
     size_t smem = 0;
     host_args.resize(n);
     for (int i = 0; i < n; ++i) {
@@ -2793,7 +2842,8 @@ static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
     cudaError_t e = cudaMemcpyAsync(args_dev, host_args.data(), sizeof(TrackArgs) * n,
                                     cudaMemcpyHostToDevice, stream);
     if (e != cudaSuccess) return (int)e;
-    e = cudaFuncSetAttribute(track_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    void (*kern)(PersistArgs) = push ? track_persist_kernel<true> : track_persist_kernel<false>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess) return (int)e;
     cudaLaunchConfig_t cfg = {};
@@ -2806,7 +2856,7 @@ static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, track_persist_kernel, p);
+    e = cudaLaunchKernelEx(&cfg, kern, p);
     return (int)e;
 }
 
@@ -2815,7 +2865,9 @@ static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
 // *args_out: the device argument array (the runner frees it).
 extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsigned *flags,
                                           const unsigned *h_ready, unsigned *h_done,
-                                          void **args_out, cudaStream_t stream) {
+                                          void **args_out, cudaStream_t stream,
+                                          void *const *push_dev, void *const *push_host,
+                                          size_t push_bytes) {
     if (!plans || !flags || !args_out) return FT_E_NULL;
     if (n < 1 || n > PERSIST_MAX_SLOTS) return FT_E_RANGE;
     TrackArgs *args = nullptr;
@@ -2829,7 +2881,8 @@ extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsig
     static std::vector<TrackArgs> host;
     // the runner rewrites a slot's inputs while the kernel is alive: coherent loads
     const int st = persist_launch(plans, n, args, host, h_ready, flags, h_done,
-                                  flags + PERSIST_MAX_SLOTS, 0xffffffffu, 0, 1, stream);
+                                  flags + PERSIST_MAX_SLOTS, 0xffffffffu, 0, 1, stream, push_dev,
+                                  push_host, push_bytes);
     return st;
 }
 
