@@ -457,6 +457,14 @@ def main() -> None:
     check = spot_check(pipe, frames[0]) if rank == 0 else None
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def preroll(stream):
+        # ~100 us of device spin ahead of the start event: the host enqueues
+        # the timed launch (and its argument staging) while the device is
+        # still busy, so the events bracket device work only, not the host's
+        # enqueue latency on an idle device
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(200_000)
     # ---- value: inputs resident in HBM, compute graph only -----------------
     for k in range(args.warmup):
         load(k)
@@ -473,6 +481,7 @@ def main() -> None:
             dist.barrier()
         torch.cuda.synchronize()
         ra, rb = ev(), ev()
+        preroll(res_stream)
         with torch.cuda.stream(res_stream):
             ra.record(res_stream)
             for k in range(args.steps):
@@ -497,6 +506,7 @@ def main() -> None:
                     ts = []
                     for _ in range(2):
                         ra, rb = ev(), ev()
+                        preroll(res_stream)
                         ra.record(res_stream)
                         run_ring(res_pipes, args.steps, res_stream, groups=G)
                         rb.record(res_stream)
@@ -514,6 +524,7 @@ def main() -> None:
                     dist.barrier()
                 torch.cuda.synchronize()
                 ra, rb = ev(), ev()
+                preroll(res_stream)
                 ra.record(res_stream)
                 run_ring(res_pipes, args.steps, res_stream, groups=ring_groups)
                 rb.record(res_stream)
