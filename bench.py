@@ -35,7 +35,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
-RING_GROUPS = (1, 2, 4, 8, 14)  # persistent step-group counts tried (ft_track_plan_groups)
+RING_GROUPS = (1, 2, 4, 10, 14)  # persistent step-group counts tried (ft_track_plan_groups)
 PERSIST_GROUPS = (1, 2, 4)  # ... for the 8-slot persistent runner (e2e)
 FALLBACK_HBM = 6650.0
 
@@ -432,7 +432,7 @@ def main() -> None:
     # frame's inputs in HBM, together > 2x L2, so back-to-back steps read
     # their inputs cold without a flush between them
     n_res = max(2, min(160, -(-(256 << 20) // pipe.in_end)))
-    n_res = (n_res + 55) // 56 * 56  # a multiple of every step-group count tried
+    n_res = (n_res + 139) // 140 * 140  # a multiple of every step-group count tried
     res_pipes = []
     for i in range(n_res):
         rp = FramePipeline(w0.cam, n_streams=S, cap_kp=cap_kp, cap_points=cap_pts,

@@ -23,7 +23,8 @@ table, _ = bench.make_table(args, frames, cp)
 w0 = frames[0]
 probe = FramePipeline(w0.cam, 1, ck, cp, pyramid_geometry=w0.pyr_left, map_table=table)
 R = -(-(256 << 20) // probe.in_end)
-R = (R + 111) // 112 * 112  # a multiple of every group count tried (1..8, 14, 16)
+RM = int(os.environ.get("RING_R_MULT", "112"))  # R: a multiple of every group count tried
+R = (R + RM - 1) // RM * RM
 pipes = []
 for i in range(R):
     p = FramePipeline(w0.cam, 1, ck, cp, pyramid_geometry=w0.pyr_left, map_table=table)
