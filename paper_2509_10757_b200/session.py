@@ -173,10 +173,30 @@ def _pyr_geometry(offsets: tuple, widths: tuple, heights: tuple) -> FtHostPyrami
     return p
 
 
+_PYR_BY_BYTES: dict = {}
+
+
+def _geometry_of(pyr) -> FtHostPyramid:
+    # keyed by the level table's raw bytes (a new ImagePyramid per frame, the
+    # same geometry): ~1 us instead of converting 25 numpy scalars per call
+    try:
+        key = (pyr.offsets.tobytes(), pyr.widths.tobytes(), pyr.heights.tobytes())
+    except AttributeError:  # plain sequences
+        key = None
+    g = _PYR_BY_BYTES.get(key) if key is not None else None
+    if g is None:
+        g = _pyr_geometry(tuple(int(x) for x in pyr.offsets), tuple(int(x) for x in pyr.widths),
+                          tuple(int(x) for x in pyr.heights))
+        if key is not None:
+            if len(_PYR_BY_BYTES) > 64:
+                _PYR_BY_BYTES.clear()
+            _PYR_BY_BYTES[key] = g
+    return g
+
+
 def pyramid(pyr, keep: list) -> FtHostPyramid:
     """ImagePyramid -> ft_host_pyramid (level table cached per geometry)."""
-    g = _pyr_geometry(tuple(int(x) for x in pyr.offsets), tuple(int(x) for x in pyr.widths),
-                      tuple(int(x) for x in pyr.heights))
+    g = _geometry_of(pyr)
     data = _c(pyr.data, np.uint8)
     if len(data) < g.offsets[g.n_levels]:
         raise ValueError("pyramid data shorter than its level table")
@@ -186,9 +206,33 @@ def pyramid(pyr, keep: list) -> FtHostPyramid:
     return p
 
 
+_MFIELDS = ("right_idx", "distance", "disparity", "refined_u", "depth", "sad")
+
+
 def matches_struct(m) -> FtHostMatches:
-    return FtHostMatches(*(getattr(m, k).ctypes.data for k in
-                           ("right_idx", "distance", "disparity", "refined_u", "depth", "sad")))
+    one = getattr(m, "_ft_rows", None)
+    if one is not None and all(getattr(m, k) is r for k, r in zip(_MFIELDS, one[1])):
+        # one allocation (empty_matches), fields not rebound: six rows of 8 * n bytes
+        base, n = one[0], len(m.right_idx)
+        return FtHostMatches(base, base + 8 * n, base + 16 * n, base + 24 * n, base + 32 * n,
+                             base + 40 * n)
+    return FtHostMatches(*(getattr(m, k).ctypes.data for k in _MFIELDS))
+
+
+def empty_matches(n: int):
+    """A StereoMatches whose six arrays are rows of ONE (6, n) allocation
+    (int64 rows, the three fp64 fields as float64 views): one allocation and
+    one pointer lookup per call instead of six."""
+    from .types import StereoMatches
+    buf = np.empty((6, n), np.int64)
+    m = StereoMatches(right_idx=buf[0], distance=buf[1], disparity=buf[2].view(np.float64),
+                      refined_u=buf[3].view(np.float64), depth=buf[4].view(np.float64),
+                      sad=buf[5])
+    try:
+        m._ft_rows = (buf.ctypes.data, tuple(getattr(m, k) for k in _MFIELDS))
+    except AttributeError:  # slotted / frozen result type: the generic path
+        pass
+    return m
 
 
 def check(status: int, what: str) -> None:
@@ -225,10 +269,26 @@ def _cam_key(cam) -> tuple:
         hasattr(cam, "k1"),)
 
 
+_CAM_KEYS: dict = {}
+
+
+def _cam_key_cached(cam) -> tuple:
+    # the tracker's camera lives as long as the tracker: key it by identity,
+    # keeping the object alive in the cache so its id is never reused
+    hit = _CAM_KEYS.get(id(cam))
+    if hit is not None and hit[0] is cam:
+        return hit[1]
+    k = _cam_key(cam)
+    if len(_CAM_KEYS) > 64:
+        _CAM_KEYS.clear()
+    _CAM_KEYS[id(cam)] = (cam, k)
+    return k
+
+
 def project_params(cam, cfg, scale, levels, cell, nx, ny, window_px, u_offset):
     from .runtime import project_params as build
     try:
-        key = (_cam_key(cam), cfg, float(scale), int(levels), int(cell), int(nx), int(ny),
+        key = (_cam_key_cached(cam), cfg, float(scale), int(levels), int(cell), int(nx), int(ny),
                None if window_px is None else float(window_px), float(u_offset))
         hash(key)
     except TypeError:

@@ -71,7 +71,7 @@ def _run_stereo(mode: int, left, right, cam, cfg, scale_pow, height: int,
     if matches is not None:
         res = matches
     elif mode & ~_lib.FT_STEREO_PHASE1:
-        res = _empty_matches(n)
+        res = S.empty_matches(n)
     ms = S.matches_struct(res) if res is not None else None
     with ses.lock:
         st = ses.lib.ft_session_stereo(ses.handle, lf, rf, pl, pr, params, mode,

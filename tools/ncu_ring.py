@@ -20,7 +20,7 @@ cp = int(max(len(f.local.point_ids) for f in frames) + 255) // 256 * 256
 table, _ = bench.make_table(type("A", (), {"no_map_table": False})(), frames, cp)
 w0 = frames[0]
 probe = FramePipeline(w0.cam, 1, ck, cp, pyramid_geometry=w0.pyr_left, map_table=table)
-R = (-(-(256 << 20) // probe.in_end) + 7) // 8 * 8
+R = (-(-(256 << 20) // probe.in_end) + 139) // 140 * 140  # a multiple of 1, 2, 4, 10, 14 (bench)
 pipes = []
 for i in range(R):
     p = FramePipeline(w0.cam, 1, ck, cp, pyramid_geometry=w0.pyr_left, map_table=table)

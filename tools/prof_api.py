@@ -55,3 +55,17 @@ for k in range(100):
     seam(ws[k % 4])
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+
+
+def fused_frame(w):
+    ft.compute_stereo_matches(w.left, w.right, w.cam, cfg, w.scale_pow, w.pyr_left, w.pyr_right)
+    return ft.search_local_points(w.local, w.frame(), w.cam, pcfg, 1.2, 8)
+
+
+timeit("fused_frame", fused_frame)
+pr = cProfile.Profile()
+pr.enable()
+for k in range(200):
+    fused_frame(ws[k % 4])
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(30)
