@@ -681,25 +681,36 @@ FT_DEV void pipe_chunk(unsigned char *dst, const unsigned char *gsrc, const unsi
 }
 
 __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, unsigned char *wb,
-                                   int f, int64_t lbase, int kf, int k1, int64_t rbase,
+                                   int f, int64_t lbase, int k0, int nk, int *ctr, int64_t rbase,
                                    int n_right, int lane, unsigned *medh) {
     constexpr int HW = 5, HS = 5, NW = 11, NOFF = 11, NJOB = NOFF * NW;
     constexpr int QJ = (NJOB + 31) / 32;
-    const int n = k1 > kf ? (k1 - kf + TK_WARPS - 1) / TK_WARPS : 0;
     PipeKp *st = reinterpret_cast<PipeKp *>(wb + PIPE_STATE);
     ft_kp_record *rec = reinterpret_cast<ft_kp_record *>(wb + PIPE_REC);
     int *part = reinterpret_cast<int *>(wb + PIPE_PART);
     const bool coh = a.coherent;
+    // dynamic assignment: the block's keypoints k0 + [0, nk) are claimed one
+    // at a time from a shared counter (claimed one keypoint ahead, so the
+    // next record's copy is issued early), so warps finish together
+    auto claim = [&]() {
+        int v = 0;
+        if (lane == 0) v = atomicAdd(ctr, 1);
+        return __shfl_sync(FULL, v, 0);
+    };
+    int cur = claim();
     // prologue: record 0, then two empty groups (every iteration commits 3)
-    if (n > 0 && lane < 4) cp_async16(reinterpret_cast<char *>(rec) + 16 * lane,
-                                      reinterpret_cast<const char *>(a.L.rec + lbase + kf) + 16 * lane);
+    if (cur < nk && lane < 4)
+        cp_async16(reinterpret_cast<char *>(rec) + 16 * lane,
+                   reinterpret_cast<const char *>(a.L.rec + lbase + k0 + cur) + 16 * lane);
     cp_async_commit();
     cp_async_commit();
     cp_async_commit();
-    for (int j = 0; j <= n; ++j) {
+    for (int j = 0;; ++j) {
         const int sl = j & 1;
-        if (j < n) {
-            const int64_t lk = lbase + kf + (int64_t)j * TK_WARPS;
+        const bool have = cur < nk;
+        int nxt = nk;
+        if (have) {
+            const int64_t lk = lbase + k0 + cur;
             cp_async_wait<2>();  // record j (committed three groups ago)
             __syncwarp();
             LeftKp kp;
@@ -711,9 +722,10 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
                 kp.d = rec_desc(r);
             }
             __syncwarp();  // record slot sl is refilled two iterations on
-            if (j + 1 < n && lane < 4)
+            nxt = claim();
+            if (nxt < nk && lane < 4)
                 cp_async16(reinterpret_cast<char *>(rec + (sl ^ 1)) + 16 * lane,
-                           reinterpret_cast<const char *>(a.L.rec + lk + TK_WARPS) + 16 * lane);
+                           reinterpret_cast<const char *>(a.L.rec + lbase + k0 + nxt) + 16 * lane);
             cp_async_commit();
             // left patch of keypoint j (kernels.py:371-387)
             const P2Geom g = p2_geom(a, f, kp);
@@ -776,7 +788,11 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
             cp_async_commit();
             cp_async_commit();
         }
-        if (j == 0) continue;
+        if (j == 0) {
+            if (!have) break;
+            cur = nxt;
+            continue;
+        }
         // ---- keypoint j - 1: its patches were committed 3-5 groups ago
         cp_async_wait<3>();
         __syncwarp();
@@ -856,6 +872,8 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
             a.so.depth[lk] = ok ? a.sp.baseline_times_fx / disp : 0.0;
             a.so.sad[lk] = ok ? sad : 0;
         }
+        if (!have) break;
+        cur = nxt;
     }
     cp_async_wait<0>();
     __syncwarp();
@@ -1092,6 +1110,7 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
                 if (bytes) bulk_g2s(sm.rtab_s, a.R.rec + rbase, bytes, mbar);
             }
             for (int b = threadIdx.x; b < H; b += TK_THREADS) sm.row_cursor[b] = 0;
+            if (threadIdx.x == 0) sm.misc[14] = 0;  // keypoint work counter (pipelined loop)
             mbar_wait(mbar, mphase & 1u);  // bit 0: phase of mbar[0]
             mphase ^= 1u;
             __syncthreads();  // cursor zeroed, ticket in misc[6]
@@ -1115,8 +1134,8 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
         // (the per-warp timeline debug marks live in stereo_kp only)
         const bool pipe = fixed55 && do_p1 && do_ref && a.patch_ints * 4 >= PIPE_BYTES;
         if (pipe) {
-            stereo_warp_pipe55(a, sm, reinterpret_cast<unsigned char *>(patch), f, lbase, kf, k1,
-                               rbase, n_right, lane, medh);
+            stereo_warp_pipe55(a, sm, reinterpret_cast<unsigned char *>(patch), f, lbase, k0,
+                               k1 - k0, &sm.misc[14], rbase, n_right, lane, medh);
         } else
         for (int k = kf; k < k1; k += TK_WARPS) {
             const LeftKp kp = k == kf ? kp_first : load_left(a, lbase + k);
