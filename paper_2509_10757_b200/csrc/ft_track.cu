@@ -2111,14 +2111,22 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
         const int i = (int)(k % (unsigned)p.n);
         if (threadIdx.x == 0) {
             unsigned v;
-            if (gb == 0) {  // the group's PCIe watcher
+            if (p.gate) {
+                // ring (ft_track_frames_ring): the ready / done words live in
+                // device memory, so every block checks them itself -- no
+                // forward through block 0, whose own previous step would
+                // otherwise gate every block's next one
+                while ((v = ld_acquire_u32(p.ready + i)) != FT_PERSIST_STOP && v < k + 1)
+                    __nanosleep(64);
+                // the slot's previous step (k - n, same workspace) must be
+                // complete: its tail blocks may still be counting arrivals
+                if (v != FT_PERSIST_STOP && k >= (unsigned)p.n)
+                    while (ld_acquire_u32(p.done + i) < k + 1 - (unsigned)p.n) __nanosleep(64);
+            } else if (gb == 0) {  // the group's PCIe watcher
+                // (the runner's host ordering already implies that the slot's
+                // previous step k - n is complete)
                 while ((v = ld_acquire_sys_u32(p.ready + i)) != FT_PERSIST_STOP && v < k + 1)
                     __nanosleep(100);
-                // the slot's previous step (k - n, same workspace) must be complete:
-                // its tail blocks may still be counting arrivals (the runner's host
-                // ordering implies it; a ring launch with every step ready does not)
-                if (p.gate && v != FT_PERSIST_STOP && k >= (unsigned)p.n)
-                    while (ld_acquire_sys_u32(p.done + i) < k + 1 - (unsigned)p.n) __nanosleep(64);
                 // forward exactly this step (the host word may already allow later ones)
                 const unsigned fwd = v == FT_PERSIST_STOP ? v : k + 1;
                 asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.dready + i), "r"(fwd)
