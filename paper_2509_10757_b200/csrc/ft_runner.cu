@@ -39,6 +39,8 @@
 #include <cstdio>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cstdlib>
 #include <new>
 #include <thread>
@@ -68,6 +70,8 @@ struct ft_runner {
     std::atomic<int64_t> out_k;     // last step whose outputs are on the host (pump -> caller)
     std::atomic<int> pump_err;      // first error the pump met (FT_OK while healthy)
     std::atomic<bool> pump_stop;
+    std::mutex pump_mu;               // idle pump: sleeps until a submit (or stop)
+    std::condition_variable pump_cv;
     std::thread *pump;
     int device;
     int64_t next_ready;  // pump: oldest step whose ready word is not yet published
@@ -269,6 +273,8 @@ static int persist_pump(ft_runner *r) {
 
 static void persist_pump_loop(ft_runner *r) {
     cudaSetDevice(r->device);
+    auto idle_since = std::chrono::steady_clock::now();
+    bool idle = false;
     while (!r->pump_stop.load(std::memory_order_acquire)) {
         const int m = persist_pump(r);
         if (m < 0) {
@@ -276,6 +282,28 @@ static void persist_pump_loop(ft_runner *r) {
             return;
         }
         if (!m) {
+            // nothing in flight (every submitted step is out) for 200 us: sleep
+            // until the next submit instead of spinning a host core between
+            // frames (a real-time tracker submits every ~50 ms).  While steps
+            // are in flight, and briefly after, the pump spins -- its latency
+            // is on every step's path.
+            const bool none = r->next_out > r->last_k.load(std::memory_order_acquire);
+            if (none && !idle) {
+                idle = true;
+                idle_since = std::chrono::steady_clock::now();
+            } else if (!none) {
+                idle = false;
+            }
+            if (idle && std::chrono::steady_clock::now() - idle_since >
+                            std::chrono::microseconds(200)) {
+                std::unique_lock<std::mutex> lk(r->pump_mu);
+                r->pump_cv.wait_for(lk, std::chrono::milliseconds(5), [r] {
+                    return r->pump_stop.load(std::memory_order_acquire) ||
+                           r->next_out <= r->last_k.load(std::memory_order_acquire);
+                });
+                idle = false;
+                continue;
+            }
 #if defined(__x86_64__) || defined(__i386__)
             __builtin_ia32_pause();
 #endif
@@ -335,7 +363,11 @@ extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host
         }
         if (e == cudaSuccess) e = cudaEventRecord(r->ev_h2d[i], hs);
         if (e != cudaSuccess) return (int)e;
-        r->last_k.store(k, std::memory_order_release);  // the pump takes it from here
+        {
+            std::lock_guard<std::mutex> lk(r->pump_mu);  // (pairs with the idle pump's wait)
+            r->last_k.store(k, std::memory_order_release);  // the pump takes it from here
+        }
+        r->pump_cv.notify_one();
         return FT_OK;
     }
     cudaError_t e = cudaStreamWaitEvent(r->h2d, r->ev_comp[i], 0);
@@ -387,7 +419,11 @@ extern "C" int ft_runner_destroy(ft_runner *r) {
         // mid-step by a late block would leave its group at a barrier)
         const int64_t last = r->last_k.load();
         if (last >= 0) persist_wait(r, last);
-        r->pump_stop.store(true);
+        {
+            std::lock_guard<std::mutex> lk(r->pump_mu);
+            r->pump_stop.store(true);
+        }
+        r->pump_cv.notify_one();
         if (r->pump) {
             r->pump->join();
             delete r->pump;
