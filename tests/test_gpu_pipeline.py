@@ -720,3 +720,39 @@ def test_persistent_runner_guard(workloads, expected):
     m = ft.compute_stereo_matches(w.left, w.right, w.cam, scale_pow=w.scale_pow,
                                   left_pyr=w.pyr_left, right_pyr=w.pyr_right)
     np.testing.assert_array_equal(m.right_idx, expected[0][0].right_idx)
+
+
+@pytest.mark.timeout(120)
+def test_persistent_runner_idle_gaps(workloads, expected):
+    """Real-time cadence: steps submitted with idle gaps (the pump sleeps on
+    its condition variable once nothing is in flight) still complete, in
+    order, with the oracle's results, and promptly after each submit."""
+    import time
+    from paper_2509_10757_b200.pipeline import AsyncRunner, FramePipeline
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left) for _ in range(2)]
+    ring = pipes[0].staging_ring(2)
+    ranges = []
+    for k in range(2):
+        w = workloads[k]
+        pipes[0].load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                            slots=expected[k][1])
+        pipes[0].stage_into(ring[k])
+        ranges.append(pipes[0].input_ranges())
+    runner = AsyncRunner(pipes, persistent=True)
+    try:
+        for k in range(6):
+            time.sleep(0.01)  # 10 ms with nothing in flight: the pump is asleep
+            t0 = time.perf_counter()
+            runner.submit(k, ring[k % 2], ranges[k % 2])
+            res = runner.wait(k).result(0, len(workloads[k % 2].left.u))
+            assert time.perf_counter() - t0 < 0.5
+            m, _, slots, n = expected[k % 2]
+            for f in FIELDS:
+                np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f),
+                                              err_msg=f"step {k} {f}")
+            np.testing.assert_array_equal(res.slots, slots)
+    finally:
+        runner.close()
