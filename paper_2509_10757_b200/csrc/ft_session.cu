@@ -146,16 +146,6 @@ int d2h(ft_session *s, size_t off, size_t bytes) {
     return (int)cudaMemcpyAsync(s->h + off, s->d + off, bytes, cudaMemcpyDeviceToHost, s->stream);
 }
 
-// The pyramid levels phase 2 reads: level o of both images for a left
-// keypoint of octave o (kernels.py:351-428), so levels >= the lowest left
-// octave (clamped) -- one contiguous byte range of each flat pyramid.
-int64_t pyr_first_byte(const ft_host_pyramid *p, const ft_host_features *left) {
-    int32_t m = p->n_levels - 1;
-    for (int64_t i = 0; i < left->n && m > 0; ++i)
-        m = std::min(m, std::max(0, std::min(left->octave[i], p->n_levels - 1)));
-    return p->offsets[m];
-}
-
 ft_pyramid dev_pyramid(const ft_host_pyramid *p, const uint8_t *dev) {
     ft_pyramid q;
     memset(&q, 0, sizeof(q));
@@ -291,18 +281,25 @@ extern "C" int ft_session_stereo(ft_session *s, const ft_host_features *left,
     cudaSetDevice(s->device);
     FT_TRY(caps(s, std::max(n, nr), 0));
     const int cap = s->cap_kp;
+    // Layout [right pyramid | small inputs | left pyramid, levels L-1..0]:
+    // phase 2 reads levels >= the lowest left octave m of both images, so
+    // the bytes a call needs -- the right pyramid's tail, the small inputs,
+    // the left pyramid's first levels (reversed) -- are ONE contiguous H2D
+    // (each copy costs ~3.6 us of fixed DMA setup; r2d_pcie_copies).
     Lay L;
-    const size_t o_ln = L.add(4), o_lr = L.add(64 * (size_t)cap);
-    const size_t o_rn = L.add(4), o_rr = L.add(64 * (size_t)cap);
-    const size_t o_cand = L.add(16 * (size_t)cap);  // cand_idx | cand_dist
-    const size_t small_end = L.total;
     size_t o_pl = 0, o_pr = 0, pl_bytes = 0, pr_bytes = 0;
     if (ref) {
         pl_bytes = (size_t)left_pyr->offsets[left_pyr->n_levels];
         pr_bytes = (size_t)right_pyr->offsets[right_pyr->n_levels];
-        o_pl = L.add(pl_bytes);
-        o_pr = L.add(pr_bytes);
+        // the right region ends exactly where the small inputs start
+        const size_t pad = (SALIGN - pr_bytes % SALIGN) % SALIGN;
+        o_pr = L.add(pr_bytes + pad) + pad;
     }
+    const size_t o_ln = L.add(4), o_lr = L.add(64 * (size_t)cap);
+    const size_t o_rn = L.add(4), o_rr = L.add(64 * (size_t)cap);
+    const size_t o_cand = L.add(16 * (size_t)cap);  // cand_idx | cand_dist
+    const size_t small_end = L.total;
+    if (ref) o_pl = L.add(pl_bytes);
     const size_t o_out = L.add(48 * (size_t)cap);  // right_idx distance disparity refined_u depth sad
     const size_t o_nm = L.add(4);
     FT_TRY(reserve(s, L.total));
@@ -330,18 +327,31 @@ extern "C" int ft_session_stereo(ft_session *s, const ft_host_features *left,
         memcpy(o + 5 * 8 * (size_t)cap, matches->sad, 8 * n);
         out_in = 48 * (size_t)cap;
     }
-    int64_t b0 = 0;
-    if (ref) {  // only the levels phase 2 reads, at their own offsets
-        b0 = pyr_first_byte(left_pyr, left);
-        memcpy(h + o_pl + b0, left_pyr->data + b0, pl_bytes - b0);
-        memcpy(h + o_pr + b0, right_pyr->data + b0, pr_bytes - b0);
+    int64_t b0r = 0;
+    size_t left_tail = 0;
+    int64_t lrev[FT_MAX_LEVELS + 1] = {0};  // left level l at o_pl + lrev[l]
+    if (ref) {  // only the levels phase 2 reads (>= m)
+        const int nl = left_pyr->n_levels;
+        int m = nl - 1;
+        for (int64_t i = 0; i < n && m > 0; ++i)
+            m = std::min(m, std::max(0, std::min(left->octave[i], nl - 1)));
+        int64_t acc = 0;
+        for (int l = nl - 1; l >= 0; --l) {
+            lrev[l] = acc;
+            acc += left_pyr->offsets[l + 1] - left_pyr->offsets[l];
+        }
+        for (int l = m; l < nl; ++l)
+            memcpy(h + o_pl + lrev[l], left_pyr->data + left_pyr->offsets[l],
+                   left_pyr->offsets[l + 1] - left_pyr->offsets[l]);
+        left_tail = (size_t)(lrev[m] + left_pyr->offsets[m + 1] - left_pyr->offsets[m]);
+        b0r = right_pyr->offsets[std::min(m, right_pyr->n_levels - 1)];
+        memcpy(h + o_pr + b0r, right_pyr->data + b0r, pr_bytes - b0r);
     }
     ph.mark(0);
-    FT_TRY(h2d(s, 0, rej_only ? o_rn + 4 : small_end));
-    if (ref) {
-        FT_TRY(h2d(s, o_pl + b0, pl_bytes - b0));
-        FT_TRY(h2d(s, o_pr + b0, pr_bytes - b0));
-    }
+    if (ref)  // right tail | small | left head: one copy
+        FT_TRY(h2d(s, o_pr + b0r, o_pl + left_tail - (o_pr + b0r)));
+    else
+        FT_TRY(h2d(s, o_ln, (rej_only ? o_rn + 4 : small_end) - o_ln));
     if (out_in) FT_TRY(h2d(s, o_out, out_in));
     ft_keypoints kl{reinterpret_cast<const ft_kp_record *>(s->d + o_lr),
                     reinterpret_cast<const int32_t *>(s->d + o_ln), cap};
@@ -350,6 +360,7 @@ extern "C" int ft_session_stereo(ft_session *s, const ft_host_features *left,
     ft_pyramid pl, pr;
     if (ref) {
         pl = dev_pyramid(left_pyr, reinterpret_cast<const uint8_t *>(s->d + o_pl));
+        for (int l = 0; l < left_pyr->n_levels; ++l) pl.offsets[l] = lrev[l];  // reversed levels
         pr = dev_pyramid(right_pyr, reinterpret_cast<const uint8_t *>(s->d + o_pr));
     }
     int64_t *dc = reinterpret_cast<int64_t *>(s->d + o_cand);
@@ -419,12 +430,14 @@ extern "C" int ft_session_project(ft_session *s, const ft_host_points *points,
     const size_t o_rot = L.add(96);  // rot[9] | trans[3]
     const size_t o_skip = skip ? L.add((size_t)cp) : 0;
     const size_t o_ref = ref_angles ? L.add(8 * (size_t)cp) : 0;
+    // the counts sit right before the slots, so the slot read-back and the
+    // counts are ONE D2H (the kernel zeroes the counts itself)
+    const size_t o_cnt = L.add(8);                                 // corr_count, slot_count
     const size_t o_sl = slots_in ? L.add(8 * (size_t)ck) : 0;
     const size_t in_end = L.total;
     const bool pa = out->out_kp || out->out_dist || out->out_oct;
     const size_t o_pa = pa ? L.add(24 * (size_t)cp) : 0;           // out_kp | dist | oct
     const size_t o_c = L.add(32 * (size_t)cp);                     // corr point | kp | dist | oct
-    const size_t o_cnt = L.add(8);                                 // corr_count, slot_count
     FT_TRY(reserve(s, L.total));
     Phases ph(s);
     char *h = s->h;
@@ -470,11 +483,16 @@ extern "C" int ft_session_project(ft_session *s, const ft_host_points *points,
         po.out_dist = po.out_kp + cp;
         po.out_oct = po.out_kp + 2 * (size_t)cp;
     }
+    // ordered correspondences only when the caller wants them (search_local_points
+    // needs the slots and the count: the kernel then skips the ordered-output pass)
+    const bool want_c = (mode & FT_PROJ_RESOLVE) && out->corr_point;
     int64_t *dc = reinterpret_cast<int64_t *>(d + o_c);
-    po.corr_point = dc;
-    po.corr_kp = dc + cp;
-    po.corr_dist = dc + 2 * (size_t)cp;
-    po.corr_oct = dc + 3 * (size_t)cp;
+    if (want_c) {
+        po.corr_point = dc;
+        po.corr_kp = dc + cp;
+        po.corr_dist = dc + 2 * (size_t)cp;
+        po.corr_oct = dc + 3 * (size_t)cp;
+    }
     po.corr_count = reinterpret_cast<int32_t *>(d + o_cnt);
     po.slot_count = reinterpret_cast<int32_t *>(d + o_cnt + 4);
     if (table) {  // slot range check is the gather's; here the kernel reads in place
@@ -484,11 +502,12 @@ extern "C" int ft_session_project(ft_session *s, const ft_host_points *points,
     ph.kernel_begin();
     FT_TRY(ft_project_search(1, &P, &K, params, &io, mode, &po, &s->ws, s->stream));
     ph.kernel_end();
-    const bool want_c = (mode & FT_PROJ_RESOLVE) && out->corr_point;
     if (pa) FT_TRY(d2h(s, o_pa, 24 * (size_t)cp));
     if (want_c) FT_TRY(d2h(s, o_c, 32 * (size_t)cp));
-    FT_TRY(d2h(s, o_cnt, 8));
-    if (slots_in && out->slots_out) FT_TRY(d2h(s, o_sl, 8 * (size_t)n_kp));
+    if (slots_in && out->slots_out)  // counts + slots
+        FT_TRY(d2h(s, o_cnt, o_sl + 8 * (size_t)n_kp - o_cnt));
+    else
+        FT_TRY(d2h(s, o_cnt, 8));
     ph.mark(1);
     const cudaError_t e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) return (int)e;

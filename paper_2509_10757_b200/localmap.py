@@ -47,11 +47,11 @@ def search_local_points(local, frame, cam, cfg, scale: float, levels: int, engin
         r = project_search(_IdsOnly(local.point_ids), frame, frame.pose, cam, cfg, scale,
                            levels, ref_angles=ref_angles, rotation=rotation_check, slots=before,
                            skip_slotted=True, write_slots=True, table=local.table,
-                           table_slots=tslots)
+                           table_slots=tslots, want_corr=False)
     else:
         r = project_search(local.soa, frame, frame.pose, cam, cfg, scale, levels,
                            ref_angles=ref_angles, rotation=rotation_check, slots=before,
-                           skip_slotted=True, write_slots=True, table=table)
+                           skip_slotted=True, write_slots=True, table=table, want_corr=False)
     after = r["slots"]
     frame.slots[...] = after
     if world is not None:

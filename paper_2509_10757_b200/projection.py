@@ -78,7 +78,7 @@ def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale:
                    levels: int, *, skip_mask=None, ref_angles=None, rotation: bool = False,
                    window_px=None, u_offset: float = 0.0, slots=None, skip_slotted=False,
                    write_slots=False, resolve=True, phase_a_out=False, table=None,
-                   table_slots=None):
+                   table_slots=None, want_corr=True):
     """One fused ``ft_project_search`` launch on one frame, through the
     native session (csrc/ft_session.cu: the reference objects' arrays are
     packed, shipped, searched and the requested outputs copied back in one
@@ -128,9 +128,10 @@ def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale:
         res["out_kp"], res["out_dist"], res["out_oct"] = (np.empty(m, np.int64) for _ in range(3))
         out.out_kp, out.out_dist, out.out_oct = (res[k].ctypes.data for k in
                                                  ("out_kp", "out_dist", "out_oct"))
-    cbuf = np.empty((4, max(m, 1)), np.int64) if resolve else None
+    want_corr = want_corr and resolve
+    cbuf = np.empty((4, max(m, 1)), np.int64) if want_corr else None
     counts = np.zeros(2, np.int32)
-    if resolve:
+    if want_corr:  # (search_local_points needs only the slots and the count)
         out.corr_point, out.corr_kp, out.corr_dist, out.corr_oct = (cbuf[q].ctypes.data
                                                                     for q in range(4))
     out.corr_count = counts.ctypes.data
@@ -147,7 +148,7 @@ def project_search(points, frame, pose, cam, cfg: ProjectionSearchConfig, scale:
                                         sl.ctypes.data if sl is not None and n_kp else None,
                                         mode, out)
     _lib.check(st, "ft_session_project")
-    if resolve:
+    if want_corr:
         c = int(counts[0])
         res["corr"] = Correspondences(*(cbuf[q, :c].copy() for q in range(4)))
     if slots_out is not None:
