@@ -756,8 +756,9 @@ def main() -> None:
                     "algorithmic_bytes_per_launch": ring_bytes, "launch_ms": ring_any,
                     "note": "SURVEY 8(d) algorithmic bytes count both whole pyramids (2.2 of "
                             "the 2.98 MB per frame); phase 2 reads only the levels of the "
-                            "frame's octaves, so DRAM traffic is ~0.37 MB per frame.  A frame "
-                            "is a chain of dependent L2 round trips (latency-bound)",
+                            "frame's octaves, so ncu DRAM traffic is ~0.64 MB per frame "
+                            "(traffic).  A frame is a chain of dependent L2 round trips "
+                            "(latency-bound)",
                     "per_frame_launch": roofline}
     # PCIe diagnostic: one step's input bytes, pinned H2D alone (events)
     h2d_times = []
