@@ -1,4 +1,2 @@
-timeout 200 python tools/debug_pipe.py
-RING_R_MULT=140 RING_GROUPS=1,2,10,14 timeout 600 python tools/ring_groups.py 2>&1 | grep "us/frame\|PARITY"
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-timeout 300 python bench.py --quick --no-configs --steps 200 --warmup 5 > gpurun_out/r2z_b200.json 2>/dev/null
+FT_DEBUG_GEOMETRY=1 RING_R_MULT=140 RING_GROUPS=10,14,20,28,35 timeout 900 python tools/ring_groups.py > /tmp/rs.txt 2>&1
+grep "us/frame\|PARITY\|Error" /tmp/rs.txt; grep -o "W=[0-9]* Gs=[0-9]* Gm=[0-9]* smem=[0-9]* grid=[0-9]*" /tmp/rs.txt | sort | uniq -c | grep -v "Gs=80"
