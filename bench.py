@@ -863,7 +863,7 @@ def main() -> None:
 
         if args.batched_streams > 0 and world == 1:
             extra("batched", lambda: batched_run(args, frames, torch, FramePipeline, cap_kp,
-                                                 cap_pts, images, flush))
+                                                 cap_pts, images, flush, popc=popc))
             if images:  # the other pyramid input mode at batch
                 other_raw = not raw
                 extra("batched_hybrid_pyramids" if other_raw else "batched_pyramids_shipped",
@@ -1418,7 +1418,7 @@ def raw_mode_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, flush) -> 
 
 
 def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flush,
-                raw: bool | None = None) -> dict:
+                raw: bool | None = None, popc: float | None = None) -> dict:
     """S frame streams per launch on this GPU (one frame of every stream per
     step): device-resident throughput, and e2e through AsyncRunner."""
     from paper_2509_10757_b200.pipeline import AsyncRunner
@@ -1485,13 +1485,15 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
     # HBM roofline of the batched launch: SURVEY 8(d) algorithmic bytes of the
     # S frames over the launch time (inputs > L2 at this S)
     per = {}
-    tot_bytes = 0
+    tot_bytes = tot_ham = 0
     for s_ in range(S):
         i = s_ % len(frames)
         if i not in per:
             u = algorithmic_units(frames[i])
-            per[i] = u["stereo_bytes"] + u["map_bytes"]
-        tot_bytes += per[i]
+            per[i] = (u["stereo_bytes"] + u["map_bytes"],
+                      u["hamming_phase1"] + u["hamming_projection"])
+        tot_bytes += per[i][0]
+        tot_ham += per[i][1]
     peaks = json.loads(PEAKS_FILE.read_text()) if PEAKS_FILE.exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM))
     med_ms = float(np.median(comp))
@@ -1503,6 +1505,14 @@ def batched_run(args, frames, torch, FramePipeline, cap_kp, cap_pts, images, flu
                          "frac": ach / hbm_peak,
                          "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback"}
             if not raw else None,
+            # integer pipe: the phase-1 + projection Hamming evaluations of the S
+            # frames (8 POPC each) over the launch time, vs the POPC peak
+            # measured in this run (ft_bench_popc)
+            "roofline_int": {"bound": "popc", "kernel": "ft_track_frames (S frames per launch)",
+                             "hamming_per_launch": tot_ham, "popc_per_launch": 8 * tot_ham,
+                             "achieved_gpopc_s": 8 * tot_ham / (med_ms / 1e3) / 1e9,
+                             "peak_gpopc_s": popc,
+                             "frac": (8 * tot_ham / (med_ms / 1e3) / 1e9) / popc if popc else None},
             "build_levels": (pipe.build_levels if raw else None),
             "ms_per_step": float(np.mean(comp)),
             "frames_per_s": S * steps / (sum(comp) / 1e3),
