@@ -1810,27 +1810,42 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             __syncthreads();
             TL_MARK(a, 2);
             const int nq = sm.misc[1];
-            for (int qi = wid; qi < nq; qi += TK_WARPS) {  // warp per visible point
-                const QItem &q = sm.queue[qi];
-                const long long qpid = sm.prnd[q.li].id;
-                if (use_hash && hash_contains(sm.htab, a.hash_bits, sm.kslots, qpid)) continue;
-                const Desc pd = rec_desc(sm.prnd[q.li]);
+            // two visible points per warp (half-warps: lanes 0-15 and 16-31): a
+            // point's window holds ~10-20 candidates, so 16 lanes cover it in
+            // one pass and the Best2 reduction (4 xor-shuffle levels) serves
+            // two points
+            const int hl = lane & 15, hh = lane >> 4;
+            for (int qb = 2 * wid; qb < nq; qb += 2 * TK_WARPS) {
+                const int qi = qb + hh;
+                bool live = qi < nq;
+                const QItem &q = sm.queue[live ? qi : 0];
+                const long long qpid = live ? sm.prnd[q.li].id : 0;
+                if (live && use_hash && hash_contains(sm.htab, a.hash_bits, sm.kslots, qpid))
+                    live = false;
                 Best2 b;
                 best2_init(b);
-                for (int gy = q.cy0; gy <= q.cy1; ++gy) {
-                    const int beg = sm.cell_start[gy * nx + q.cx0];
-                    const int end = sm.cell_start[gy * nx + q.cx1 + 1];
-                    for (int ii = beg + lane; ii < end; ii += 32) {
-                        const int j = sm.items[ii];
-                        const ft_kp_record &kr = sm.ktab[j];
-                        if (fabs(kr.u - q.ucen) > q.r || fabs(kr.v - q.v) > q.r) continue;
-                        const int ko = kr.octave;
-                        if (ko < q.lvl - 1 || ko > q.lvl + 1) continue;
-                        best2_push(b, hamming(pd, rec_desc(kr)), (uint32_t)j);
+                if (live) {
+                    const Desc pd = rec_desc(sm.prnd[q.li]);
+                    for (int gy = q.cy0; gy <= q.cy1; ++gy) {
+                        const int beg = sm.cell_start[gy * nx + q.cx0];
+                        const int end = sm.cell_start[gy * nx + q.cx1 + 1];
+                        for (int ii = beg + hl; ii < end; ii += 16) {
+                            const int j = sm.items[ii];
+                            const ft_kp_record &kr = sm.ktab[j];
+                            if (fabs(kr.u - q.ucen) > q.r || fabs(kr.v - q.v) > q.r) continue;
+                            const int ko = kr.octave;
+                            if (ko < q.lvl - 1 || ko > q.lvl + 1) continue;
+                            best2_push(b, hamming(pd, rec_desc(kr)), (uint32_t)j);
+                        }
                     }
                 }
-                best2_warp_reduce(b);
-                if (lane == 0 && ratio_accept(b, pp.t_proj, pp.ratio)) {
+#pragma unroll
+                for (int sh = 8; sh > 0; sh >>= 1) {  // within the half (order-independent)
+                    const uint32_t ok = __shfl_xor_sync(FULL, b.key, sh);
+                    const uint32_t os = __shfl_xor_sync(FULL, b.second, sh);
+                    best2_merge(b, ok, os);
+                }
+                if (live && hl == 0 && ratio_accept(b, pp.t_proj, pp.ratio)) {
                     const int kp = (int)(b.key & 0xffffu), d = (int)(b.key >> 16);
                     const int i = r0 + q.li;
                     const int64_t gi = pbase + i;
