@@ -54,6 +54,10 @@
 #include "ft_common.cuh"
 #include "ft_ws.cuh"
 
+#ifndef FT_MAP_LANES_PER_POINT
+#define FT_MAP_LANES_PER_POINT 16
+#endif
+
 namespace ft {
 
 constexpr int TK_THREADS = 512;
@@ -1814,8 +1818,9 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             // point's window holds ~10-20 candidates, so 16 lanes cover it in
             // one pass and the Best2 reduction (4 xor-shuffle levels) serves
             // two points
-            const int hl = lane & 15, hh = lane >> 4;
-            for (int qb = 2 * wid; qb < nq; qb += 2 * TK_WARPS) {
+            constexpr int LPP = FT_MAP_LANES_PER_POINT;  // lanes per visible point
+            const int hl = lane & (LPP - 1), hh = lane / LPP;
+            for (int qb = (32 / LPP) * wid; qb < nq; qb += (32 / LPP) * TK_WARPS) {
                 const int qi = qb + hh;
                 bool live = qi < nq;
                 const QItem &q = sm.queue[live ? qi : 0];
@@ -1829,7 +1834,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                     for (int gy = q.cy0; gy <= q.cy1; ++gy) {
                         const int beg = sm.cell_start[gy * nx + q.cx0];
                         const int end = sm.cell_start[gy * nx + q.cx1 + 1];
-                        for (int ii = beg + hl; ii < end; ii += 16) {
+                        for (int ii = beg + hl; ii < end; ii += LPP) {
                             const int j = sm.items[ii];
                             const ft_kp_record &kr = sm.ktab[j];
                             if (fabs(kr.u - q.ucen) > q.r || fabs(kr.v - q.v) > q.r) continue;
@@ -1840,7 +1845,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                     }
                 }
 #pragma unroll
-                for (int sh = 8; sh > 0; sh >>= 1) {  // within the half (order-independent)
+                for (int sh = LPP / 2; sh > 0; sh >>= 1) {  // within the point's lanes
                     const uint32_t ok = __shfl_xor_sync(FULL, b.key, sh);
                     const uint32_t os = __shfl_xor_sync(FULL, b.second, sh);
                     best2_merge(b, ok, os);
