@@ -822,8 +822,14 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
                     const unsigned char *lr = lb + dy * PIPE_LROW + lo;
                     const unsigned char *rr = rb + dy * PIPE_RROW + ro + oi;
                     const int c = (int)rb[HW * PIPE_RROW + ro5 + oi + HW] - cl;  // cr - cl
+                    // two partial sums (even / odd dx): half the dependent-add depth
+                    int ae = 0, ao = 0;
 #pragma unroll
-                    for (int dx = 0; dx < NW; ++dx) acc[t] += abs((int)lr[dx] + c - (int)rr[dx]);
+                    for (int dx = 0; dx < NW; dx += 2) {
+                        ae += abs((int)lr[dx] + c - (int)rr[dx]);
+                        if (dx + 1 < NW) ao += abs((int)lr[dx + 1] + c - (int)rr[dx + 1]);
+                    }
+                    acc[t] = ae + ao;
                 }
             }
 #pragma unroll
