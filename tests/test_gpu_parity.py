@@ -580,3 +580,47 @@ def test_rejection_median_near_histogram_edge(oracle, amp, tail, monkeypatch):
     got = ft.compute_stereo_matches(w.left, w.right, w.cam, cfg, w.scale_pow, w.pyr_left, pr)
     for f in FIELDS:
         np.testing.assert_array_equal(getattr(got, f), getattr(ref, f), err_msg=f)
+
+
+@pytest.mark.parametrize("seed", [31, 32])
+def test_pipelined_patch_edges_vs_oracle(oracle, seed):
+    """The pipelined stereo loop stages patch rows as 16-B chunks, falling back
+    to byte loads where a chunk would reach outside its level (first / last
+    rows and columns of a level, the end of the last level).  Keypoints placed
+    on every level right at the patch borders, through the fused call (the
+    pipelined loop; the session's pyramid base is not 16-B aligned), must
+    equal the oracle."""
+    from synthetic import make_workload
+    from paper_2509_10757_b200.types import FeatureSet
+    w = make_workload(seed=seed, n_landmarks=2000, map_points=500, images=True)
+    pyr, scale_pow = w.pyr_left, w.scale_pow
+    rng = np.random.default_rng(seed)
+    lu, lv, lo, ru, rv, ro, desc_l, desc_r = [], [], [], [], [], [], [], []
+    for o in range(len(pyr.widths)):
+        wd, ht, s = int(pyr.widths[o]), int(pyr.heights[o]), float(scale_pow[o])
+        for x in (5, 6, 7, 15, 16, 17, wd - 18, wd - 17, wd - 8, wd - 7, wd - 6):
+            for y in (5, 6, ht // 2, ht - 7, ht - 6):
+                d = rng.integers(0, 2**63, 4, dtype=np.uint64)
+                disp = 2.0 + rng.integers(0, 6)  # level-o pixels
+                lu.append(x * s + rng.uniform(-0.3, 0.3) * s)
+                lv.append(y * s)
+                lo.append(o)
+                ru.append((x - disp) * s)
+                rv.append(y * s)
+                ro.append(o)
+                desc_l.append(d)
+                d2 = d.copy()
+                d2[0] ^= np.uint64(1 << int(rng.integers(0, 8)))  # a few bits apart
+                desc_r.append(d2)
+
+    def fs(u, v, o, d):
+        n = len(u)
+        return FeatureSet(np.array(u), np.array(v), np.array(o, np.int32), np.zeros(n),
+                          np.zeros(n, np.float32), np.array(d, np.uint64).reshape(n, 4))
+    left, right = fs(lu, lv, lo, desc_l), fs(ru, rv, ro, desc_r)
+    cfg = StereoMatchConfig()
+    ref = oracle.stereo_pinhole(left, right, w.pyr_left, w.pyr_right, w.cam, cfg, scale_pow)
+    got = ft.compute_stereo_matches(left, right, w.cam, cfg, scale_pow, w.pyr_left, w.pyr_right)
+    for f in FIELDS:
+        np.testing.assert_array_equal(getattr(got, f), getattr(ref, f), err_msg=f)
+    assert (ref.right_idx >= 0).sum() > 20  # the edge patches were refined, not all rejected
