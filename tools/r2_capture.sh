@@ -1,5 +1,5 @@
 # final round-2 evidence: ncu of the ring at the bench's picks, sanitizers,
-# full bench lines (driver command, default) and the reference arm
+# GPU tests, smoke, full bench lines (driver command, default), reference arm
 P=${1:-r2fin}
 for gk in "10 20" "14 200"; do
   set -- $gk
@@ -7,4 +7,6 @@ for gk in "10 20" "14 200"; do
       -o gpurun_out/${P}_ring_g$1_k$2 python tools/ncu_ring.py $1 $2 > gpurun_out/${P}_ncu_g$1_k$2.log 2>&1
 done
 bash tools/run_sanitizers.sh > gpurun_out/${P}_sanitizers.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/${P}_gputest.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${P}_smoke.log 2>&1
 bash tools/r2_final.sh ${P}
