@@ -35,6 +35,7 @@
 // No stream memory operations: each costs several microseconds of stream
 // time, and one per step on the H2D stream capped the step rate.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdio>
 #include <atomic>
@@ -337,9 +338,17 @@ extern "C" int ft_runner_create(const void *const graph_exec[2], void *const dev
     return ft_runner_create_n(2, graph_exec, dev_in, in_bytes, dev_out, host_out, out_bytes, out);
 }
 
+namespace {
+struct NvtxRange {  // NVTX range for nsys / ncu timelines (a few ns without a tool)
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host_in,
                                        const uint64_t *ranges, int32_t n_ranges) {
     if (!r || !host_in || (!ranges && n_ranges > 0)) return FT_E_NULL;
+    NvtxRange nv("ft_runner_submit");
     if (k < 0 || n_ranges < 0) return FT_E_RANGE;
     for (int q = 0; q < n_ranges; ++q)
         if (ranges[2 * q] > ranges[2 * q + 1] || ranges[2 * q + 1] > r->in_bytes) return FT_E_RANGE;
@@ -408,6 +417,7 @@ extern "C" int ft_runner_submit(ft_runner *r, int64_t k, const void *host_in) {
 
 extern "C" int ft_runner_wait(ft_runner *r, int64_t k) {
     if (!r) return FT_E_NULL;
+    NvtxRange nv("ft_runner_wait");
     if (k < 0) return FT_E_RANGE;
     if (r->persistent) return persist_wait(r, k);
     return (int)cudaEventSynchronize(r->ev_d2h[k % r->n]);

@@ -15,6 +15,7 @@
 // A session serves one tracking thread (the reference's single-writer rule,
 // tracker.py:1-7); calls are synchronous like the reference's.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -167,13 +168,27 @@ double us_since(Clock::time_point t) {
 
 // Phase timer of one session call (host clock; kernel time by events when
 // the session was created with FT_SESSION_TIMING set).
+// NVTX: one range per session call ("ft_session_<stage>"), with nested
+// phase ranges (pack, issue, sync, unpack) -- visible in nsys / ncu
+// timelines; a few ns per call without a tool attached (tracing).
+const char *const PHASE_NAMES[5] = {"pack", "issue", "kernel", "sync", "unpack"};
+
 struct Phases {
     ft_session *s;
     Clock::time_point t;
-    explicit Phases(ft_session *s_) : s(s_), t(Clock::now()) {}
+    explicit Phases(ft_session *s_, const char *name = "ft_session") : s(s_), t(Clock::now()) {
+        nvtxRangePushA(name);
+        nvtxRangePushA(PHASE_NAMES[0]);
+    }
+    ~Phases() {
+        nvtxRangePop();  // phase
+        nvtxRangePop();  // call
+    }
     void mark(int k) {
         s->stats[k] += us_since(t);
         t = Clock::now();
+        nvtxRangePop();
+        nvtxRangePushA(k == 0 ? PHASE_NAMES[1] : k == 1 ? PHASE_NAMES[3] : PHASE_NAMES[4]);
     }
     void kernel_begin() {
         if (s->timing) cudaEventRecord(s->ev[0], s->stream);
@@ -303,7 +318,7 @@ extern "C" int ft_session_stereo(ft_session *s, const ft_host_features *left,
     const size_t o_out = L.add(48 * (size_t)cap);  // right_idx distance disparity refined_u depth sad
     const size_t o_nm = L.add(4);
     FT_TRY(reserve(s, L.total));
-    Phases ph(s);
+    Phases ph(s, "ft_session_stereo");
     char *h = s->h;
     *reinterpret_cast<int32_t *>(h + o_ln) = (int32_t)n;
     *reinterpret_cast<int32_t *>(h + o_rn) = (int32_t)nr;
@@ -439,7 +454,7 @@ extern "C" int ft_session_project(ft_session *s, const ft_host_points *points,
     const size_t o_pa = pa ? L.add(24 * (size_t)cp) : 0;           // out_kp | dist | oct
     const size_t o_c = L.add(32 * (size_t)cp);                     // corr point | kp | dist | oct
     FT_TRY(reserve(s, L.total));
-    Phases ph(s);
+    Phases ph(s, "ft_session_project");
     char *h = s->h;
     *reinterpret_cast<int32_t *>(h + o_kn) = (int32_t)n_kp;
     pack_kp(frame, reinterpret_cast<ft_kp_record *>(h + o_kr));
@@ -602,7 +617,7 @@ extern "C" int ft_session_update_local_map(ft_session *s, const int64_t *slots, 
     const size_t o_pt = L.add(8 * (size_t)std::max<int64_t>(world->id_cap, 1));
     const size_t o_ps = L.add(4 * (size_t)std::max<int64_t>(world->id_cap, 1));
     FT_TRY(reserve(s, L.total));
-    Phases ph(s);
+    Phases ph(s, "ft_session_update_local_map");
     if (n_slots) memcpy(s->h + o_sl, slots, 8 * n_slots);
     ph.mark(0);
     FT_TRY(h2d(s, o_sl, 8 * (size_t)n_slots));

@@ -46,6 +46,7 @@
 //   blocks publish their results with release reductions and move on to the
 //   next frame instead of waiting at group barriers.
 #include <cstdio>
+#include <nvtx3/nvToolsExt.h>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -2942,6 +2943,10 @@ extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsig
 extern "C" int ft_track_frames_ring(int32_t n_plans, const void *const *plans, int64_t n_steps,
                                     ft_stream_t stream) {
     if (!plans) return FT_E_NULL;
+    nvtxRangePushA("ft_track_frames_ring");  // host side of the launch (NVTX timelines)
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop_;
     if (n_plans < 1 || n_steps < 0 || n_steps >= 0x7f000000) return FT_E_RANGE;
     if (n_steps == 0) return FT_OK;
     // per-device buffers, grown on demand (stream-ordered reuse)
