@@ -876,11 +876,13 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
                 if (x < MED_FINE) atomicAdd(medh + 128 + x, 1u);
             }
             const int64_t lk = q.lk;
+            double depth = 0.0;
+            if (ok) depth = a.sp.baseline_times_fx / disp;  // (only for accepted matches)
             a.so.right_idx[lk] = ok ? q.cand : -1;
             a.so.distance[lk] = ok ? q.cdist : 10000;
             a.so.disparity[lk] = ok ? disp : 0.0;
             a.so.refined_u[lk] = ok ? ur : 0.0;
-            a.so.depth[lk] = ok ? a.sp.baseline_times_fx / disp : 0.0;
+            a.so.depth[lk] = depth;
             a.so.sad[lk] = ok ? sad : 0;
         }
         if (!have) break;
