@@ -10,9 +10,14 @@ plus a 5000-point local map; a step is one frame per stream through
     map:     skip slotted -> project -> window search -> resolve -> slot write
                                                                (ft_project_search)
 
-Default: 1 stream per GPU (single-stream latency = ms_per_step).  Under
-torchrun each rank drives its own GPU with independent streams (weak scaling,
-no collective on the data path; NCCL only for the barrier and max-time).
+Default: 1 stream per GPU.  `value` = frames/s of ONE persistent ring launch
+over K resident frames (> 2x L2) with G step groups (G frames in flight on
+disjoint SMs, picked in the warm-up); `e2e` = the same frames through the
+persistent runner with every step's inputs copied from pinned host memory and
+its outputs back (host wall clock).  `--gpus N` launches N ranks itself (one
+per GPU, torch.distributed.run on 127.0.0.1); each rank drives its own GPU with
+independent streams (weak scaling, no collective on the data path; NCCL only
+for the barrier, the G broadcast and the max over ranks).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--streams S]
     python bench.py --impl reference ...    # CPU oracle arm (host cores)
