@@ -61,7 +61,10 @@
 
 namespace ft {
 
-constexpr int TK_THREADS = 512;
+#ifndef FT_TK_THREADS
+#define FT_TK_THREADS 512
+#endif
+constexpr int TK_THREADS = FT_TK_THREADS;  // threads per block (one block per SM)
 constexpr int TK_WARPS = TK_THREADS / 32;
 constexpr int TK_MAX_BINS = 256;
 constexpr int TK_MAP_CHUNK_MAX = 2048;  // points per map block (shared per-point arrays)
@@ -198,7 +201,7 @@ FT_DEV void warp_find_rank(const int *hist, int k, int *out_digit, int *out_k) {
 // value histogram in shared memory, one block scan, both ranks (n-1)/2 and
 // n/2 located in the same pass.  Same result as block_median_pair.
 constexpr int MED_SMALL_BINS = 4096;
-constexpr int MED_PER_THREAD = MED_SMALL_BINS / TK_THREADS;
+constexpr int MED_PER_THREAD = (MED_SMALL_BINS + TK_THREADS - 1) / TK_THREADS;
 
 __device__ void block_median_pair_small(const uint32_t *vals, int n, int nm, int *hist,
                                         int *scan_tmp, int *misc, uint32_t &v_lo,
@@ -217,7 +220,7 @@ __device__ void block_median_pair_small(const uint32_t *vals, int n, int nm, int
     int sum = 0;
 #pragma unroll
     for (int j = 0; j < MED_PER_THREAD; ++j) {
-        local[j] = hist[b0 + j];
+        local[j] = b0 + j < MED_SMALL_BINS ? hist[b0 + j] : 0;
         sum += local[j];
     }
     int total;
@@ -343,6 +346,12 @@ FT_DEV LeftKp load_left(const TrackArgs &a, int64_t lk) {
 
 // Phase 1 (kernels.py:312-345) over the contiguous CSR range of rows
 // [floor(v - band), ceil(v + band)] held in shared memory.
+static_assert(offsetof(ft_kp_record, v) == 8 && offsetof(ft_kp_record, desc) == 16 &&
+                  offsetof(ft_kp_record, octave) == 56 && sizeof(ft_kp_record) == 64,
+              "ft_kp_record field offsets used by the shared-memory readers");
+// SH: the right table is staged in shared memory (read with 32-bit LDS
+// addressing; the generic path serves a table left in global memory).
+template <bool SH = false>
 FT_DEV int phase1(const TrackArgs &a, const StereoSmem &sm, const LeftKp &kp, int lane,
                   int &cdist) {
     const double band = a.sp.band_factor * a.sp.scale_pow[clampi(kp.o, 0, FT_MAX_LEVELS - 1)];
@@ -352,7 +361,24 @@ FT_DEV int phase1(const TrackArgs &a, const StereoSmem &sm, const LeftKp &kp, in
     if (r0 < 0) r0 = 0;
     if (r1 > H - 1) r1 = H - 1;
     uint32_t best = NO_KEY;
-    if (r0 <= r1) {
+    if (SH && r0 <= r1) {
+        const unsigned rs = smem_u32(sm.row_start), it = smem_u32(sm.items),
+                       tb = smem_u32(sm.rtab_s);
+        const int beg = lds_s32(rs + 4 * (unsigned)r0), end = lds_s32(rs + 4 * (unsigned)(r1 + 1));
+        for (int ii = beg + lane; ii < end; ii += 32) {
+            const int j = lds_u16(it + 2 * ii);
+            const unsigned rec = tb + 64u * (unsigned)j;  // ft_kp_record
+            const int ro = lds_s32(rec + 56);
+            if (ro < kp.o - 1 || ro > kp.o + 1) continue;
+            if (fabs(lds_f64(rec + 8) - kp.v) > band) continue;
+            const double disp = kp.u - lds_f64(rec);
+            if (disp < a.sp.min_disparity || disp > a.sp.max_disparity) continue;
+            Desc rd;
+            rd.lo = lds_v4(rec + 16);
+            rd.hi = lds_v4(rec + 32);
+            best = min(best, (hamming(kp.d, rd) << 16) | (uint32_t)j);
+        }
+    } else if (r0 <= r1) {
         const int beg = sm.row_start[r0], end = sm.row_start[r1 + 1];
         for (int ii = beg + lane; ii < end; ii += 32) {
             const int j = sm.items[ii];
@@ -690,9 +716,12 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
                                    int n_right, int lane, unsigned *medh) {
     constexpr int HW = 5, HS = 5, NW = 11, NOFF = 11, NJOB = NOFF * NW;
     constexpr int QJ = (NJOB + 31) / 32;
+    // the per-warp buffer is shared memory: the SAD sweep reads it with
+    // 32-bit LDS addressing (lds_*) instead of generic 64-bit loads (the
+    // pointer reaches here through StereoSmem, where its space is lost)
+    const unsigned wbs = smem_u32(wb);
     PipeKp *st = reinterpret_cast<PipeKp *>(wb + PIPE_STATE);
     ft_kp_record *rec = reinterpret_cast<ft_kp_record *>(wb + PIPE_REC);
-    int *part = reinterpret_cast<int *>(wb + PIPE_PART);
     const bool coh = a.coherent;
     // dynamic assignment: the block's keypoints k0 + [0, nk) are claimed one
     // at a time from a shared counter (claimed one keypoint ahead, so the
@@ -746,7 +775,8 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
             }
             cp_async_commit();
             int cdist;
-            const int cand = phase1(a, sm, kp, lane, cdist);
+            const int cand = a.stage_rdesc ? phase1<true>(a, sm, kp, lane, cdist)
+                                           : phase1<false>(a, sm, kp, lane, cdist);
             if (lane == 0 && a.so.cand_idx) {
                 a.so.cand_idx[lk] = cand;
                 a.so.cand_dist[lk] = cdist;
@@ -756,7 +786,8 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
             long long xr0 = 0;
             const unsigned char *rrow0 = nullptr;
             if (cand >= 0 && cand < n_right && g.left_ok) {
-                const double urc = sm.rtab[cand].u;
+                const double urc = a.stage_rdesc ? lds_f64(smem_u32(sm.rtab_s) + 64u * (unsigned)cand)
+                                                 : sm.rtab[cand].u;
                 xr0 = round_half_even(urc / g.s);
                 const long long hr = a.PR.heights[g.o];
                 if (!(xr0 - HS - HW < 0 || xr0 + HS + HW >= g.wr || g.yi - HW < 0 ||
@@ -807,11 +838,12 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
         double disp = 0.0, ur = 0.0;
         int sad = 0;
         if (q.state) {
-            const unsigned char *lb = wb + ps * PIPE_SLOT;
-            const unsigned char *rb = lb + 11 * PIPE_LROW;
+            const unsigned lb = wbs + ps * PIPE_SLOT;  // shared addresses
+            const unsigned rb = lb + 11 * PIPE_LROW;
+            const unsigned pt = wbs + PIPE_PART;
             // centre pixels: cl = L[yi, xi], cr(oi) = R[yi, xr0 + oi - HS]
             const int lo5 = (q.loff + HW * q.lw) & 15, ro5 = (q.roff + HW * q.rw) & 15;
-            const int cl = lb[HW * PIPE_LROW + lo5 + HW];
+            const int cl = lds_u8(lb + HW * PIPE_LROW + lo5 + HW);
             int acc[QJ];
 #pragma unroll
             for (int t = 0; t < QJ; ++t) {
@@ -820,15 +852,17 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
                 if (job < NJOB) {
                     const int oi = job / NW, dy = job - oi * NW;
                     const int lo = (q.loff + dy * q.lw) & 15, ro = (q.roff + dy * q.rw) & 15;
-                    const unsigned char *lr = lb + dy * PIPE_LROW + lo;
-                    const unsigned char *rr = rb + dy * PIPE_RROW + ro + oi;
-                    const int c = (int)rb[HW * PIPE_RROW + ro5 + oi + HW] - cl;  // cr - cl
+                    const unsigned lr = lb + dy * PIPE_LROW + lo;
+                    const unsigned rr = rb + dy * PIPE_RROW + ro + oi;
+                    const int c = lds_u8(rb + HW * PIPE_RROW + ro5 + oi + HW) - cl;  // cr - cl
                     // two partial sums (even / odd dx): half the dependent-add depth
                     int ae = 0, ao = 0;
 #pragma unroll
                     for (int dx = 0; dx < NW; dx += 2) {
-                        ae += abs((int)lr[dx] + c - (int)rr[dx]);
-                        if (dx + 1 < NW) ao += abs((int)lr[dx + 1] + c - (int)rr[dx + 1]);
+                        // |x - y| + acc: one VABSDIFF per pixel
+                        ae = (int)__sad(lds_u8(lr + dx) + c, lds_u8(rr + dx), (unsigned)ae);
+                        if (dx + 1 < NW)
+                            ao = (int)__sad(lds_u8(lr + dx + 1) + c, lds_u8(rr + dx + 1), (unsigned)ao);
                     }
                     acc[t] = ae + ao;
                 }
@@ -836,14 +870,14 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
 #pragma unroll
             for (int t = 0; t < QJ; ++t) {
                 const int job = lane + 32 * t;
-                if (job < NJOB) part[job] = acc[t];
+                if (job < NJOB) sts_s32(pt + 4 * job, acc[t]);
             }
             __syncwarp();
             int sv = 0x7fffffff;
             if (lane < NOFF) {
                 sv = 0;
 #pragma unroll
-                for (int dy = 0; dy < NW; ++dy) sv += part[lane * NW + dy];
+                for (int dy = 0; dy < NW; ++dy) sv += lds_s32(pt + 4 * (lane * NW + dy));
             }
             const unsigned key = lane < NOFF ? ((unsigned)sv << 5) | (unsigned)lane : 0xffffffffu;
             const unsigned best = __reduce_min_sync(FULL, key);
