@@ -658,35 +658,50 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
 }
 
 // ---------------------------------------------------------------------------
-// Software-pipelined per-warp stereo loop for the default 11x11 window /
-// +-5 slide with phase 1 and phase 2 in the launch: the global loads of
-// keypoint j (its record, its left patch, its right strip) are issued as
-// cp.async copies into a per-warp double buffer while keypoint j-1's SAD
-// sweep runs, so a warp's chain per keypoint is ~ max(load latency, compute)
-// instead of their sum.  Per iteration j:
-//   wait record j -> geometry -> cp.async record j+1 -> cp.async left patch j
-//   -> phase 1 (shared memory) -> cp.async right strip j -> wait j-1's
-//   patches -> SAD sweep + parabola of j-1 -> outputs of j-1.
+// Block-batched stereo for the default 11x11 window / +-5 slide with phase 1
+// and phase 2 in the launch.  The per-keypoint scalar work -- level
+// geometry with its fp64 divisions, the parabola, depth and the six output
+// stores -- runs one THREAD per keypoint instead of once per warp per
+// keypoint, and the warps' SAD loop only streams patches.  Per batch of up
+// to KB_N keypoints of the block's range:
+//   records -> shared memory (one TMA bulk copy; the first batch's copy is
+//     issued before the right table's CSR is built)
+//   B  warp per keypoint: phase 1 over the shared row band -> cand, cdist
+//   G  thread per keypoint: level geometry, the right strip's column and
+//      bounds -> patch row addresses; the keypoints with a SAD sweep to run
+//      are compacted into a list (block scan)
+//   C  warp per listed keypoint, one item ahead: cp.async of item j+1's
+//      left patch and right strip while item j's SAD sweep runs -> the best
+//      offset and its neighbours' SADs
+//   D  thread per keypoint: parabola, disparity range, depth, outputs
+//      (coalesced), SAD-median histogram
+// Results are those of stereo_kp<5, 5> (same predicates, same order).
 // Patch rows are copied as whole 16-B chunks (2 per left row, 3 per right
 // row; the bytes of a row start at (row address & 15) inside its chunks);
 // a chunk reaching outside the level's bytes is copied byte by byte (only
 // the in-level bytes).
-// Results are those of stereo_kp<5, 5> (same predicates, same order).
-constexpr int PIPE_LROW = 32, PIPE_RROW = 48;           // bytes per staged row
+constexpr int PIPE_LROW = 32, PIPE_RROW = 48;               // bytes per staged row
 constexpr int PIPE_SLOT = 11 * PIPE_LROW + 11 * PIPE_RROW;  // 880 B per keypoint
-struct PipeKp {  // a keypoint between its loads and its SAD (per-warp smem)
-    double u, s;
-    long long xr0, lk;
-    int cand, cdist, state;   // state: 0 no refinement, 1 SAD pending
-    int loff, lw, roff, rw;   // low 4 bits of row 0's address, row pitch (left, right)
-    int pad_;
+constexpr int PIPE_PART = 2 * PIPE_SLOT;                    // SAD partials [121] int
+constexpr int PIPE_WARP = PIPE_PART + 496;                  // per-warp buffer
+constexpr int KB_N = 256;                                   // keypoints per batch
+struct KbMeta {  // one keypoint between the passes (32 B)
+    unsigned long long lrow0, rrow0;  // patch row 0 (left) / strip row 0 (right)
+    int xr0, cand;
+    short cdist;
+    unsigned char o, state;        // state 1: SAD sweep to run
+    unsigned char loff, lw, roff, rw;  // row 0 address & 15, row pitch & 15
 };
-constexpr int PIPE_PART = 2 * PIPE_SLOT;                  // SAD partials [121] int
-constexpr int PIPE_STATE = PIPE_PART + 496;               // PipeKp x 2
-constexpr int PIPE_REC = PIPE_STATE + 2 * (int)sizeof(PipeKp);  // ft_kp_record x 2
-constexpr int PIPE_BYTES = PIPE_REC + 2 * 64;
-static_assert(sizeof(PipeKp) == 64, "PipeKp is 64 B");
-static_assert(PIPE_STATE % 16 == 0 && PIPE_REC % 16 == 0, "16-B aligned regions");
+static_assert(sizeof(KbMeta) == 32, "KbMeta is 32 B");
+// byte offsets inside the stereo patch region (16-B aligned)
+constexpr int KB_REC = TK_WARPS * PIPE_WARP;  // ft_kp_record [KB_N]
+constexpr int KB_META = KB_REC + KB_N * 64;   // KbMeta [KB_N]
+constexpr int KB_SAD = KB_META + KB_N * 32;   // int4 (best offset, s-, s0, s+) [KB_N]
+constexpr int KB_LIST = KB_SAD + KB_N * 16;   // uint16 [KB_N]
+constexpr int KB_END = KB_LIST + KB_N * 2;
+// per-warp share of the region (the host sizes patch_ints from it)
+constexpr int PIPE_BYTES = ((KB_END + TK_WARPS - 1) / TK_WARPS + 15) & ~15;
+static_assert(KB_REC % 16 == 0 && KB_META % 16 == 0 && KB_SAD % 16 == 0, "16-B aligned");
 
 FT_DEV void cp_async16(void *smem_dst, const void *gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
@@ -711,166 +726,170 @@ FT_DEV void pipe_chunk(unsigned char *dst, const unsigned char *gsrc, const unsi
         if (gsrc + b >= beg && gsrc + b < end) dst[b] = coherent ? __ldca(gsrc + b) : __ldg(gsrc + b);
 }
 
-__device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, unsigned char *wb,
-                                   int f, int64_t lbase, int k0, int nk, int *ctr, int64_t rbase,
-                                   int n_right, int lane, unsigned *medh) {
+FT_DEV unsigned long long lds_u64(unsigned a) {
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+
+// Records of keypoints [kb, kb + nb) -> the batch area (thread 0).
+FT_DEV void kb_issue_records(const TrackArgs &a, const StereoSmem &sm, int64_t lbase, int kb,
+                             int nb, unsigned long long *mbar1) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(mbar1, 64u * (unsigned)nb);
+    bulk_g2s(reinterpret_cast<unsigned char *>(sm.patch) + KB_REC, a.L.rec + lbase + kb,
+             64u * (unsigned)nb, mbar1);
+}
+
+__device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, int f, int64_t lbase,
+                                    int k0, int k1, int n_right, unsigned *medh,
+                                    unsigned long long *mbar1, unsigned &mphase) {
     constexpr int HW = 5, HS = 5, NW = 11, NOFF = 11, NJOB = NOFF * NW;
     constexpr int QJ = (NJOB + 31) / 32;
-    // the per-warp buffer is shared memory: the SAD sweep reads it with
-    // 32-bit LDS addressing (lds_*) instead of generic 64-bit loads (the
-    // pointer reaches here through StereoSmem, where its space is lost)
-    const unsigned wbs = smem_u32(wb);
-    PipeKp *st = reinterpret_cast<PipeKp *>(wb + PIPE_STATE);
-    ft_kp_record *rec = reinterpret_cast<ft_kp_record *>(wb + PIPE_REC);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const bool coh = a.coherent;
-    // dynamic assignment: the block's keypoints k0 + [0, nk) are claimed one
-    // at a time from a shared counter (claimed one keypoint ahead, so the
-    // next record's copy is issued early), so warps finish together
-    auto claim = [&]() {
-        int v = 0;
-        if (lane == 0) v = atomicAdd(ctr, 1);
-        return __shfl_sync(FULL, v, 0);
-    };
-    int cur = claim();
-    // prologue: record 0, then two empty groups (every iteration commits 3)
-    if (cur < nk && lane < 4)
-        cp_async16(reinterpret_cast<char *>(rec) + 16 * lane,
-                   reinterpret_cast<const char *>(a.L.rec + lbase + k0 + cur) + 16 * lane);
-    cp_async_commit();
-    cp_async_commit();
-    cp_async_commit();
-    for (int j = 0;; ++j) {
-        const int sl = j & 1;
-        const bool have = cur < nk;
-        int nxt = nk;
-        if (have) {
-            const int64_t lk = lbase + k0 + cur;
-            cp_async_wait<2>();  // record j (committed three groups ago)
-            __syncwarp();
+    unsigned char *pb = reinterpret_cast<unsigned char *>(sm.patch);
+    const unsigned base = smem_u32(pb);  // shared addresses for the warp loops
+    const unsigned wbs = base + wid * PIPE_WARP, pt = wbs + PIPE_PART;
+    const ft_kp_record *krec = reinterpret_cast<const ft_kp_record *>(pb + KB_REC);
+    KbMeta *km = reinterpret_cast<KbMeta *>(pb + KB_META);
+    int4 *ks = reinterpret_cast<int4 *>(pb + KB_SAD);
+    uint16_t *list = reinterpret_cast<uint16_t *>(pb + KB_LIST);
+    const uint8_t *lframe = a.PL.data + (int64_t)f * a.PL.frame_bytes;
+    const uint8_t *rframe = a.PR.data + (int64_t)f * a.PR.frame_bytes;
+    for (int kb = k0, bt = 0; kb < k1; kb += KB_N, ++bt) {
+        const int nb = min(KB_N, k1 - kb);
+        if (bt > 0 && threadIdx.x == 0) kb_issue_records(a, sm, lbase, kb, nb, mbar1);
+        mbar_wait(mbar1, (mphase >> 1) & 1u);  // bit 1: phase of mbar[1]
+        mphase ^= 2u;
+        // ---- B: phase 1, warp per keypoint (kernels.py:312-345)
+        for (int i = wid; i < nb; i += TK_WARPS) {
+            const unsigned r = base + KB_REC + 64u * (unsigned)i;
             LeftKp kp;
-            {
-                const ft_kp_record &r = rec[sl];
-                kp.u = r.u;
-                kp.v = r.v;
-                kp.o = r.octave;
-                kp.d = rec_desc(r);
-            }
-            __syncwarp();  // record slot sl is refilled two iterations on
-            nxt = claim();
-            if (nxt < nk && lane < 4)
-                cp_async16(reinterpret_cast<char *>(rec + (sl ^ 1)) + 16 * lane,
-                           reinterpret_cast<const char *>(a.L.rec + lbase + k0 + nxt) + 16 * lane);
-            cp_async_commit();
-            // left patch of keypoint j (kernels.py:371-387)
-            const P2Geom g = p2_geom(a, f, kp);
-            unsigned char *lb = wb + sl * PIPE_SLOT;
-            unsigned char *rb = lb + 11 * PIPE_LROW;
-            const unsigned char *lrow0 = g.lp + (g.yi - HW) * g.wl + (g.xi - HW);
-            if (g.left_ok && lane < 2 * NW) {  // chunks bounded by the level's own bytes
-                const unsigned char *row = lrow0 + (lane >> 1) * g.wl;
-                const unsigned char *c0 =
-                    reinterpret_cast<const unsigned char *>((uintptr_t)row & ~(uintptr_t)15);
-                pipe_chunk(lb + (lane >> 1) * PIPE_LROW + 16 * (lane & 1), c0 + 16 * (lane & 1),
-                           g.lp, g.lp + g.wl * a.PL.heights[g.o], coh);
-            }
-            cp_async_commit();
+            kp.u = lds_f64(r);
+            kp.v = lds_f64(r + 8);
+            kp.d.lo = lds_v4(r + 16);
+            kp.d.hi = lds_v4(r + 32);
+            kp.o = lds_s32(r + 56);
             int cdist;
             const int cand = a.stage_rdesc ? phase1<true>(a, sm, kp, lane, cdist)
                                            : phase1<false>(a, sm, kp, lane, cdist);
-            if (lane == 0 && a.so.cand_idx) {
-                a.so.cand_idx[lk] = cand;
-                a.so.cand_dist[lk] = cdist;
+            if (lane == 0) {
+                km[i].cand = cand;
+                km[i].cdist = (short)cdist;
             }
-            // right strip of the candidate (kernels.py:388-397)
-            int state = 0;
+        }
+        __syncthreads();
+        // ---- G: geometry, thread per keypoint (kernels.py:371-397)
+        int need = 0;
+        const int i = threadIdx.x;
+        if (i < nb) {
+            LeftKp kp;
+            kp.u = krec[i].u;
+            kp.v = krec[i].v;
+            kp.o = krec[i].octave;
+            const P2Geom g = p2_geom(a, f, kp);
+            KbMeta m = km[i];
+            const int64_t lk = lbase + kb + i;
+            if (a.so.cand_idx) {
+                a.so.cand_idx[lk] = m.cand;
+                a.so.cand_dist[lk] = m.cdist;
+            }
             long long xr0 = 0;
-            const unsigned char *rrow0 = nullptr;
-            if (cand >= 0 && cand < n_right && g.left_ok) {
-                const double urc = a.stage_rdesc ? lds_f64(smem_u32(sm.rtab_s) + 64u * (unsigned)cand)
-                                                 : sm.rtab[cand].u;
-                xr0 = round_half_even(urc / g.s);
+            const uint8_t *rrow0 = nullptr;
+            m.state = 0;
+            if (m.cand >= 0 && m.cand < n_right && g.left_ok) {
+                xr0 = round_half_even(sm.rtab[m.cand].u / g.s);
                 const long long hr = a.PR.heights[g.o];
                 if (!(xr0 - HS - HW < 0 || xr0 + HS + HW >= g.wr || g.yi - HW < 0 ||
                       g.yi + HW >= hr)) {
-                    state = 1;
+                    m.state = 1;
                     rrow0 = g.rp + (g.yi - HW) * g.wr + (xr0 - HS - HW);
-                    for (int c = lane; c < 3 * NW; c += 32) {
-                        const int r = c / 3, q = c - 3 * r;
-                        const unsigned char *row = rrow0 + r * g.wr;
-                        const unsigned char *c0 =
-                            reinterpret_cast<const unsigned char *>((uintptr_t)row & ~(uintptr_t)15);
-                        pipe_chunk(rb + r * PIPE_RROW + 16 * q, c0 + 16 * q, g.rp, g.rp + g.wr * hr,
-                                   coh);
-                    }
                 }
             }
-            cp_async_commit();
-            if (lane == 0) {
-                PipeKp &q = st[sl];
-                q.u = kp.u;
-                q.s = g.s;
-                q.xr0 = xr0;
-                q.lk = lk;
-                q.cand = cand;
-                q.cdist = cdist;
-                q.state = state;
-                q.loff = (int)((uintptr_t)lrow0 & 15);
-                q.lw = (int)(g.wl & 15);
-                q.roff = (int)((uintptr_t)rrow0 & 15);
-                q.rw = (int)(g.wr & 15);
+            const uint8_t *lrow0 = g.lp + (g.yi - HW) * g.wl + (g.xi - HW);
+            m.lrow0 = (unsigned long long)lrow0;
+            m.rrow0 = (unsigned long long)rrow0;
+            m.xr0 = (int)xr0;
+            m.o = (unsigned char)g.o;
+            m.loff = (unsigned char)((uintptr_t)lrow0 & 15);
+            m.lw = (unsigned char)(g.wl & 15);
+            m.roff = (unsigned char)((uintptr_t)rrow0 & 15);
+            m.rw = (unsigned char)(g.wr & 15);
+            km[i] = m;
+            need = m.state;
+        }
+        int nl;
+        const int pos = block_exclusive_scan<TK_THREADS>(need, sm.scan_tmp, nl);
+        if (need) list[pos] = (uint16_t)i;
+        __syncthreads();
+        // ---- C: SAD sweeps (kernels.py:388-409), warp per listed keypoint
+        auto issue = [&](int j, int sl) {  // item j's patches -> slot sl
+            const unsigned mr = base + KB_META + 32u * (unsigned)lds_u16(base + KB_LIST + 2u * j);
+            const uint8_t *lrow0 = reinterpret_cast<const uint8_t *>(lds_u64(mr));
+            const uint8_t *rrow0 = reinterpret_cast<const uint8_t *>(lds_u64(mr + 8));
+            const int o = lds_u8(mr + 26);
+            const long long wl = a.PL.widths[o], wr = a.PR.widths[o];
+            const uint8_t *lp = lframe + a.PL.offsets[o], *rp = rframe + a.PR.offsets[o];
+            unsigned char *lb = pb + wid * PIPE_WARP + sl * PIPE_SLOT;
+            unsigned char *rb = lb + 11 * PIPE_LROW;
+            if (lane < 2 * NW) {  // chunks bounded by the level's own bytes
+                const uint8_t *row = lrow0 + (lane >> 1) * wl;
+                const uint8_t *c0 = reinterpret_cast<const uint8_t *>((uintptr_t)row & ~(uintptr_t)15);
+                pipe_chunk(lb + (lane >> 1) * PIPE_LROW + 16 * (lane & 1), c0 + 16 * (lane & 1), lp,
+                           lp + wl * a.PL.heights[o], coh);
             }
-        } else {
-            cp_async_commit();  // keep three groups per iteration
+            for (int c = lane; c < 3 * NW; c += 32) {
+                const int r = c / 3, q = c - 3 * r;
+                const uint8_t *row = rrow0 + r * wr;
+                const uint8_t *c0 = reinterpret_cast<const uint8_t *>((uintptr_t)row & ~(uintptr_t)15);
+                pipe_chunk(rb + r * PIPE_RROW + 16 * q, c0 + 16 * q, rp, rp + wr * a.PR.heights[o], coh);
+            }
+        };
+        int j = wid;
+        if (j < nl) issue(j, 0);
+        cp_async_commit();
+        for (int t = 0; j < nl; j += TK_WARPS, ++t) {
+            const int sl = t & 1;
+            if (j + TK_WARPS < nl) issue(j + TK_WARPS, sl ^ 1);
             cp_async_commit();
-            cp_async_commit();
-        }
-        if (j == 0) {
-            if (!have) break;
-            cur = nxt;
-            continue;
-        }
-        // ---- keypoint j - 1: its patches were committed 3-5 groups ago
-        cp_async_wait<3>();
-        __syncwarp();
-        const int ps = sl ^ 1;
-        const PipeKp q = st[ps];
-        bool ok = false;
-        double disp = 0.0, ur = 0.0;
-        int sad = 0;
-        if (q.state) {
-            const unsigned lb = wbs + ps * PIPE_SLOT;  // shared addresses
-            const unsigned rb = lb + 11 * PIPE_LROW;
-            const unsigned pt = wbs + PIPE_PART;
+            cp_async_wait<1>();  // item j's patches
+            __syncwarp();
+            const int idx = lds_u16(base + KB_LIST + 2u * j);
+            const unsigned mr = base + KB_META + 32u * (unsigned)idx;
+            const int pk = lds_s32(mr + 28);  // loff, lw, roff, rw
+            const int loff = pk & 255, lw = (pk >> 8) & 255, roff = (pk >> 16) & 255,
+                      rw = (pk >> 24) & 255;
+            const unsigned lb = wbs + sl * PIPE_SLOT, rb = lb + 11 * PIPE_LROW;
             // centre pixels: cl = L[yi, xi], cr(oi) = R[yi, xr0 + oi - HS]
-            const int lo5 = (q.loff + HW * q.lw) & 15, ro5 = (q.roff + HW * q.rw) & 15;
+            const int lo5 = (loff + HW * lw) & 15, ro5 = (roff + HW * rw) & 15;
             const int cl = lds_u8(lb + HW * PIPE_LROW + lo5 + HW);
             int acc[QJ];
 #pragma unroll
-            for (int t = 0; t < QJ; ++t) {
-                const int job = lane + 32 * t;
-                acc[t] = 0;
+            for (int t2 = 0; t2 < QJ; ++t2) {
+                const int job = lane + 32 * t2;
+                acc[t2] = 0;
                 if (job < NJOB) {
                     const int oi = job / NW, dy = job - oi * NW;
-                    const int lo = (q.loff + dy * q.lw) & 15, ro = (q.roff + dy * q.rw) & 15;
+                    const int lo = (loff + dy * lw) & 15, ro = (roff + dy * rw) & 15;
                     const unsigned lr = lb + dy * PIPE_LROW + lo;
                     const unsigned rr = rb + dy * PIPE_RROW + ro + oi;
                     const int c = lds_u8(rb + HW * PIPE_RROW + ro5 + oi + HW) - cl;  // cr - cl
-                    // two partial sums (even / odd dx): half the dependent-add depth
+                    // two partial sums (even / odd dx), |x - y| + acc in one VABSDIFF
                     int ae = 0, ao = 0;
 #pragma unroll
                     for (int dx = 0; dx < NW; dx += 2) {
-                        // |x - y| + acc: one VABSDIFF per pixel
                         ae = (int)__sad(lds_u8(lr + dx) + c, lds_u8(rr + dx), (unsigned)ae);
                         if (dx + 1 < NW)
                             ao = (int)__sad(lds_u8(lr + dx + 1) + c, lds_u8(rr + dx + 1), (unsigned)ao);
                     }
-                    acc[t] = ae + ao;
+                    acc[t2] = ae + ao;
                 }
             }
 #pragma unroll
-            for (int t = 0; t < QJ; ++t) {
-                const int job = lane + 32 * t;
-                if (job < NJOB) sts_s32(pt + 4 * job, acc[t]);
+            for (int t2 = 0; t2 < QJ; ++t2) {
+                const int job = lane + 32 * t2;
+                if (job < NJOB) sts_s32(pt + 4 * job, acc[t2]);
             }
             __syncwarp();
             int sv = 0x7fffffff;
@@ -884,46 +903,54 @@ __device__ void stereo_warp_pipe55(const TrackArgs &a, const StereoSmem &sm, uns
             const int best_oi = (int)(best & 31u), best_sad = (int)(best >> 5);
             const int s_m = __shfl_sync(FULL, sv, best_oi > 0 ? best_oi - 1 : 0);
             const int s_p = __shfl_sync(FULL, sv, best_oi < NOFF - 1 ? best_oi + 1 : 0);
-            if (best_oi > 0 && best_oi < NOFF - 1) {  // kernels.py:410-428
-                const double d_m = (double)s_m, d_0 = (double)best_sad, d_p = (double)s_p;
-                const double denom = d_m + d_p - 2.0 * d_0;
-                if (denom > 0.0) {
-                    const double delta = (d_m - d_p) / (2.0 * denom);
-                    if (!(delta < -1.0 || delta > 1.0)) {
-                        const double ur_ref = ((double)(q.xr0 + (best_oi - HS)) + delta) * q.s;
-                        const double dsp = q.u - ur_ref;
-                        if (!(dsp < a.sp.min_disparity || dsp > a.sp.max_disparity)) {
-                            ok = true;
-                            disp = dsp;
-                            ur = ur_ref;
-                            sad = best_sad;
+            if (lane == 0) ks[idx] = make_int4(best_oi, s_m, best_sad, s_p);
+            __syncwarp();  // slot sl and the partials are refilled next iteration
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+        // ---- D: parabola + outputs, thread per keypoint (kernels.py:410-428)
+        if (i < nb) {
+            const KbMeta m = km[i];
+            const int64_t lk = lbase + kb + i;
+            bool ok = false;
+            double disp = 0.0, ur = 0.0;
+            int sad = 0;
+            if (m.state) {
+                const int4 r = ks[i];
+                const int best_oi = r.x, best_sad = r.z;
+                if (best_oi > 0 && best_oi < NOFF - 1) {
+                    const double d_m = (double)r.y, d_0 = (double)best_sad, d_p = (double)r.w;
+                    const double denom = d_m + d_p - 2.0 * d_0;
+                    if (denom > 0.0) {
+                        const double delta = (d_m - d_p) / (2.0 * denom);
+                        if (!(delta < -1.0 || delta > 1.0)) {
+                            const double s = a.sp.scale_pow[m.o];
+                            const double ur_ref = ((double)((long long)m.xr0 + (best_oi - HS)) + delta) * s;
+                            const double dsp = krec[i].u - ur_ref;
+                            if (!(dsp < a.sp.min_disparity || dsp > a.sp.max_disparity)) {
+                                ok = true;
+                                disp = dsp;
+                                ur = ur_ref;
+                                sad = best_sad;
+                            }
                         }
                     }
                 }
             }
-        }
-        __syncwarp();  // slot ps (patches, partials, state) is refilled next iteration
-        if (lane == 0) {
             if (ok && medh) {  // SAD-median histogram of the frame (fire-and-forget reds)
                 const uint32_t x = (uint32_t)sad;
                 atomicAdd(medh + (x < MED_FINE ? x / MED_CW : MED_NC), 1u);
                 if (x < MED_FINE) atomicAdd(medh + 128 + x, 1u);
             }
-            const int64_t lk = q.lk;
-            double depth = 0.0;
-            if (ok) depth = a.sp.baseline_times_fx / disp;  // (only for accepted matches)
-            a.so.right_idx[lk] = ok ? q.cand : -1;
-            a.so.distance[lk] = ok ? q.cdist : 10000;
+            a.so.right_idx[lk] = ok ? m.cand : -1;
+            a.so.distance[lk] = ok ? (int)m.cdist : 10000;
             a.so.disparity[lk] = ok ? disp : 0.0;
             a.so.refined_u[lk] = ok ? ur : 0.0;
-            a.so.depth[lk] = depth;
+            a.so.depth[lk] = ok ? a.sp.baseline_times_fx / disp : 0.0;
             a.so.sad[lk] = ok ? sad : 0;
         }
-        if (!have) break;
-        cur = nxt;
+        __syncthreads();  // the batch area is refilled by the next batch
     }
-    cp_async_wait<0>();
-    __syncwarp();
 }
 
 // np.median (stereo.py:180) of a group's accepted SADs from its histograms
@@ -1144,20 +1171,26 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
             prefetch_l2(a.PR.data + (int64_t)f * a.PR.frame_bytes + a.PR.offsets[l - 16]);
     }
 
+    // default window with both phases here: the block-batched passes
+    // (stereo_block_pipe55; the per-warp timeline debug marks live in
+    // stereo_kp only)
+    const bool fixed55 = a.sp.half_window == 5 && a.sp.half_slide == 5;
+    const bool pipe = fixed55 && do_p1 && do_ref && a.patch_ints * 4 >= PIPE_BYTES;
     if (k0 < k1 && (do_p1 || finalize)) {
         const int kf = k0 + wid;
         LeftKp kp_first;  // issued now: lands while the right table streams in
-        if (kf < k1) kp_first = load_left(a, lbase + kf);
+        if (!pipe && kf < k1) kp_first = load_left(a, lbase + kf);
         if (do_p1) {
             // right keypoint table -> shared memory with TMA bulk copies
+            // (pipe: the first batch of left records too, on mbar[1])
             if (threadIdx.x == 0) {
                 fence_proxy_async_smem();
+                if (pipe) kb_issue_records(a, sm, lbase, k0, min(KB_N, k1 - k0), mbar + 1);
                 const unsigned bytes = a.stage_rdesc ? 64u * n_right : 0u;
                 mbar_arrive_expect_tx(mbar, bytes);
                 if (bytes) bulk_g2s(sm.rtab_s, a.R.rec + rbase, bytes, mbar);
             }
             for (int b = threadIdx.x; b < H; b += TK_THREADS) sm.row_cursor[b] = 0;
-            if (threadIdx.x == 0) sm.misc[14] = 0;  // keypoint work counter (pipelined loop)
             mbar_wait(mbar, mphase & 1u);  // bit 0: phase of mbar[0]
             mphase ^= 1u;
             __syncthreads();  // cursor zeroed, ticket in misc[6]
@@ -1176,13 +1209,8 @@ __device__ void stereo_frame(const TrackArgs &a, int f, int rank, int slot,
         unsigned *medh = med_h ? a.med + ((size_t)slot * 3 + (unsigned)sm.misc[6] % 3u) * MED_WS
                                : nullptr;
         int *patch = sm.patch + wid * a.patch_ints;
-        const bool fixed55 = a.sp.half_window == 5 && a.sp.half_slide == 5;
-        // default window with both phases here: the software-pipelined loop
-        // (the per-warp timeline debug marks live in stereo_kp only)
-        const bool pipe = fixed55 && do_p1 && do_ref && a.patch_ints * 4 >= PIPE_BYTES;
         if (pipe) {
-            stereo_warp_pipe55(a, sm, reinterpret_cast<unsigned char *>(patch), f, lbase, k0,
-                               k1 - k0, &sm.misc[14], rbase, n_right, lane, medh);
+            stereo_block_pipe55(a, sm, f, lbase, k0, k1, n_right, medh, mbar + 1, mphase);
         } else
         for (int k = kf; k < k1; k += TK_WARPS) {
             const LeftKp kp = k == kf ? kp_first : load_left(a, lbase + k);
@@ -2526,11 +2554,13 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
             // more frames than one resident wave holds: pick slots W and the
             // stereo / map split minimising the modelled job time
             //   waves(W) * max(t_stereo, t_map)
-            //   t_stereo = 8.8 + 4.14 * keypoints per warp
+            //   t_stereo = 8.8 + 3.1 * keypoints per warp
             //   t_map    = 11.4 + 2.28 * 512-point rounds + 0.0205 * points per block
             // (us per frame of a group; fitted to the persistent ring at 4 and
             // 8 step groups over forced splits, r2k: picks 11 or 12 map blocks of
-            // 35 and 5 of 17, the measured optima)
+            // 35 and 5 of 17, the measured optima; the stereo slope refit after
+            // the block-batched stereo passes, s1: 5 map blocks of 14 and 4 of
+            // 10, the measured optima at cfg2)
             const int min_per = (want_stereo ? 1 : 0) + (want_map ? gm_min : 0);
             if (min_per > capacity) return FT_E_RANGE;
             double best = 1e30;
@@ -2551,7 +2581,7 @@ static int track_geometry(TrackArgs &a, bool want_stereo, bool want_map, Geom &o
                     double t = 0.0;
                     if (want_stereo) {
                         const double kpw = (double)a.L.cap / (double)(gs * TK_WARPS);
-                        t = 8.8 + 4.14 * (kpw > 1.0 ? kpw : 1.0);
+                        t = 8.8 + 3.1 * (kpw > 1.0 ? kpw : 1.0);
                     }
                     if (want_map) {
                         const int chunk = (a.P.cap + gm - 1) / gm;
@@ -2666,8 +2696,8 @@ static bool fill_stereo(TrackArgs &a, int32_t n_frames, const ft_keypoints *left
     a.patch_ints = (mode & FT_STEREO_REFINE)
                        ? nw * nw + nw * nr + (2 * params->half_slide + 1) * nw
                        : 0;
-    // the default window's pipelined loop (stereo_warp_pipe55): its double
-    // buffers, in 16-B units per warp
+    // the default window's block-batched passes (stereo_block_pipe55): the
+    // warps' double buffers and the batch area, per-warp share
     if ((mode & FT_STEREO_REFINE) && params->half_window == 5 && params->half_slide == 5 &&
         !getenv("FT_STEREO_NOPIPE"))
         a.patch_ints = a.patch_ints > PIPE_BYTES / 4 ? a.patch_ints : PIPE_BYTES / 4;
