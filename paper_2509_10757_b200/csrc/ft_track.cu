@@ -680,8 +680,8 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
 // row; the bytes of a row start at (row address & 15) inside its chunks);
 // a chunk reaching outside the level's bytes is copied byte by byte (only
 // the in-level bytes).
-constexpr int PIPE_LROW = 32, PIPE_RROW = 48;               // bytes per staged row
-constexpr int PIPE_SLOT = 11 * PIPE_LROW + 11 * PIPE_RROW;  // 880 B per keypoint
+constexpr int PIPE_LROW = 48, PIPE_RROW = 48;  // bytes per staged row (2-way banks)
+constexpr int PIPE_SLOT = 11 * PIPE_LROW + 11 * PIPE_RROW;  // 1056 B per keypoint
 constexpr int PIPE_PART = 2 * PIPE_SLOT;                    // SAD partials [121] int
 constexpr int PIPE_WARP = PIPE_PART + 496;                  // per-warp buffer
 constexpr int KB_N = 256;                                   // keypoints per batch
@@ -744,8 +744,7 @@ FT_DEV void kb_issue_records(const TrackArgs &a, const StereoSmem &sm, int64_t l
 __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, int f, int64_t lbase,
                                     int k0, int k1, int n_right, unsigned *medh,
                                     unsigned long long *mbar1, unsigned &mphase) {
-    constexpr int HW = 5, HS = 5, NW = 11, NOFF = 11, NJOB = NOFF * NW;
-    constexpr int QJ = (NJOB + 31) / 32;
+    constexpr int HW = 5, HS = 5, NW = 11, NOFF = 11;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const bool coh = a.coherent;
     unsigned char *pb = reinterpret_cast<unsigned char *>(sm.patch);
@@ -780,9 +779,10 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
             }
         }
         __syncthreads();
+        if (bt == 0) TL_MARK(a, 8);
         // ---- G: geometry, thread per keypoint (kernels.py:371-397)
-        int need = 0;
         const int i = threadIdx.x;
+        int need = 0;
         if (i < nb) {
             LeftKp kp;
             kp.u = krec[i].u;
@@ -823,6 +823,7 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
         const int pos = block_exclusive_scan<TK_THREADS>(need, sm.scan_tmp, nl);
         if (need) list[pos] = (uint16_t)i;
         __syncthreads();
+        if (bt == 0) TL_MARK(a, 9);
         // ---- C: SAD sweeps (kernels.py:388-409), warp per listed keypoint
         auto issue = [&](int j, int sl) {  // item j's patches -> slot sl
             const unsigned mr = base + KB_META + 32u * (unsigned)lds_u16(base + KB_LIST + 2u * j);
@@ -864,39 +865,41 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
             // centre pixels: cl = L[yi, xi], cr(oi) = R[yi, xr0 + oi - HS]
             const int lo5 = (loff + HW * lw) & 15, ro5 = (roff + HW * rw) & 15;
             const int cl = lds_u8(lb + HW * PIPE_LROW + lo5 + HW);
-            int acc[QJ];
+            // lane (g, dy), 22 lanes: row dy, offsets 6g .. 6g + 5 (g = 1: .. 10).
+            // A lane reads its left row once (11 B) and the 16 right bytes its
+            // offsets cover, then runs 6 independent VABSDIFF chains (|x - y| +
+            // acc): 33 LDS per lane instead of 22 per (offset, row) job.
+            const int g = lane < 11 ? 0 : (lane < 22 ? 1 : 2), dy = lane - 11 * g;
+            if (g < 2) {
+                const int o0 = 6 * g;
+                const int lo = (loff + dy * lw) & 15, ro = (roff + dy * rw) & 15;
+                const unsigned lr = lb + dy * PIPE_LROW + lo;
+                const unsigned rr = rb + dy * PIPE_RROW + ro + o0;  // + 15 stays in the row
+                const unsigned rc = rb + HW * PIPE_RROW + ro5 + HW + o0;
+                int L[NW], Rv[16], cc[6], acc[6];
 #pragma unroll
-            for (int t2 = 0; t2 < QJ; ++t2) {
-                const int job = lane + 32 * t2;
-                acc[t2] = 0;
-                if (job < NJOB) {
-                    const int oi = job / NW, dy = job - oi * NW;
-                    const int lo = (loff + dy * lw) & 15, ro = (roff + dy * rw) & 15;
-                    const unsigned lr = lb + dy * PIPE_LROW + lo;
-                    const unsigned rr = rb + dy * PIPE_RROW + ro + oi;
-                    const int c = lds_u8(rb + HW * PIPE_RROW + ro5 + oi + HW) - cl;  // cr - cl
-                    // two partial sums (even / odd dx), |x - y| + acc in one VABSDIFF
-                    int ae = 0, ao = 0;
+                for (int dx = 0; dx < NW; ++dx) L[dx] = lds_u8(lr + dx);
 #pragma unroll
-                    for (int dx = 0; dx < NW; dx += 2) {
-                        ae = (int)__sad(lds_u8(lr + dx) + c, lds_u8(rr + dx), (unsigned)ae);
-                        if (dx + 1 < NW)
-                            ao = (int)__sad(lds_u8(lr + dx + 1) + c, lds_u8(rr + dx + 1), (unsigned)ao);
-                    }
-                    acc[t2] = ae + ao;
-                }
-            }
+                for (int x = 0; x < 16; ++x) Rv[x] = lds_u8(rr + x);
 #pragma unroll
-            for (int t2 = 0; t2 < QJ; ++t2) {
-                const int job = lane + 32 * t2;
-                if (job < NJOB) sts_s32(pt + 4 * job, acc[t2]);
+                for (int k = 0; k < 6; ++k) cc[k] = lds_u8(rc + k) - cl;  // cr - cl
+#pragma unroll
+                for (int k = 0; k < 6; ++k) acc[k] = 0;
+#pragma unroll
+                for (int dx = 0; dx < NW; ++dx)
+#pragma unroll
+                    for (int k = 0; k < 6; ++k)
+                        acc[k] = (int)__sad(L[dx] + cc[k], Rv[k + dx], (unsigned)acc[k]);
+#pragma unroll
+                for (int k = 0; k < 6; ++k)
+                    if (o0 + k < NOFF) sts_s32(pt + 4 * ((o0 + k) * NW + dy), acc[k]);
             }
             __syncwarp();
             int sv = 0x7fffffff;
             if (lane < NOFF) {
                 sv = 0;
 #pragma unroll
-                for (int dy = 0; dy < NW; ++dy) sv += lds_s32(pt + 4 * (lane * NW + dy));
+                for (int d = 0; d < NW; ++d) sv += lds_s32(pt + 4 * (lane * NW + d));
             }
             const unsigned key = lane < NOFF ? ((unsigned)sv << 5) | (unsigned)lane : 0xffffffffu;
             const unsigned best = __reduce_min_sync(FULL, key);
@@ -908,6 +911,7 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
         }
         cp_async_wait<0>();
         __syncthreads();
+        if (bt == 0) TL_MARK(a, 10);
         // ---- D: parabola + outputs, thread per keypoint (kernels.py:410-428)
         if (i < nb) {
             const KbMeta m = km[i];

@@ -49,7 +49,7 @@ Gm = int(hdr.split("Gm=")[1].split()[0])
 per = Gs + Gm
 t0 = T[:, 0][T[:, 0] > 0].min()
 names = {"stereo": ["start", "staged+csr", "phase1/2 done", "barrier", "end", "-", "table landed",
-                    "-", "-", "-", "-", "-", "-", "gathered", "median"],
+                    "-", "B phase 1", "G geometry", "C SAD sweeps", "-", "-", "gathered", "median"],
          "map": ["start", "staged+csr+hash", "projected (round 1)", "searched", "barrier", "end",
                  "table landed", "points landed"]}
 for role, sel in (("stereo", [i for i in range(len(T)) if i % per < Gs]),
