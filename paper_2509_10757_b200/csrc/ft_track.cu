@@ -351,9 +351,12 @@ static_assert(offsetof(ft_kp_record, v) == 8 && offsetof(ft_kp_record, desc) == 
               "ft_kp_record field offsets used by the shared-memory readers");
 // SH: the right table is staged in shared memory (read with 32-bit LDS
 // addressing; the generic path serves a table left in global memory).
-template <bool SH = false>
+// LPP: lanes per keypoint (32, or 16 for two keypoints per warp: `lane` is
+// then the lane within the keypoint's half and the arg-min stays in it);
+// live = false runs no candidates (the idle half of a warp's last pair).
+template <bool SH = false, int LPP = 32>
 FT_DEV int phase1(const TrackArgs &a, const StereoSmem &sm, const LeftKp &kp, int lane,
-                  int &cdist) {
+                  int &cdist, bool live = true) {
     const double band = a.sp.band_factor * a.sp.scale_pow[clampi(kp.o, 0, FT_MAX_LEVELS - 1)];
     long long r0 = (long long)floor(kp.v - band);
     long long r1 = (long long)ceil(kp.v + band);
@@ -361,26 +364,29 @@ FT_DEV int phase1(const TrackArgs &a, const StereoSmem &sm, const LeftKp &kp, in
     if (r0 < 0) r0 = 0;
     if (r1 > H - 1) r1 = H - 1;
     uint32_t best = NO_KEY;
+    if (!live) r1 = r0 - 1;
     if (SH && r0 <= r1) {
         const unsigned rs = smem_u32(sm.row_start), it = smem_u32(sm.items),
                        tb = smem_u32(sm.rtab_s);
         const int beg = lds_s32(rs + 4 * (unsigned)r0), end = lds_s32(rs + 4 * (unsigned)(r1 + 1));
-        for (int ii = beg + lane; ii < end; ii += 32) {
+        for (int ii = beg + lane; ii < end; ii += LPP) {
             const int j = lds_u16(it + 2 * ii);
             const unsigned rec = tb + 64u * (unsigned)j;  // ft_kp_record
+            // every field in one round trip, then the predicates
             const int ro = lds_s32(rec + 56);
-            if (ro < kp.o - 1 || ro > kp.o + 1) continue;
-            if (fabs(lds_f64(rec + 8) - kp.v) > band) continue;
-            const double disp = kp.u - lds_f64(rec);
-            if (disp < a.sp.min_disparity || disp > a.sp.max_disparity) continue;
+            const double rv = lds_f64(rec + 8), ru = lds_f64(rec);
             Desc rd;
             rd.lo = lds_v4(rec + 16);
             rd.hi = lds_v4(rec + 32);
+            if (ro < kp.o - 1 || ro > kp.o + 1) continue;
+            if (fabs(rv - kp.v) > band) continue;
+            const double disp = kp.u - ru;
+            if (disp < a.sp.min_disparity || disp > a.sp.max_disparity) continue;
             best = min(best, (hamming(kp.d, rd) << 16) | (uint32_t)j);
         }
     } else if (r0 <= r1) {
         const int beg = sm.row_start[r0], end = sm.row_start[r1 + 1];
-        for (int ii = beg + lane; ii < end; ii += 32) {
+        for (int ii = beg + lane; ii < end; ii += LPP) {
             const int j = sm.items[ii];
             const ft_kp_record &rr = sm.rtab[j];
             const int ro = rr.octave;
@@ -391,7 +397,12 @@ FT_DEV int phase1(const TrackArgs &a, const StereoSmem &sm, const LeftKp &kp, in
             best = min(best, (hamming(kp.d, rec_desc(rr)) << 16) | (uint32_t)j);
         }
     }
-    best = __reduce_min_sync(FULL, best);
+    if (LPP == 32) {
+        best = __reduce_min_sync(FULL, best);
+    } else {
+#pragma unroll
+        for (int sh = LPP / 2; sh > 0; sh >>= 1) best = min(best, __shfl_xor_sync(FULL, best, sh));
+    }
     if (best != NO_KEY && (int)(best >> 16) <= a.sp.t_match) {
         cdist = (int)(best >> 16);
         return (int)(best & 0xffffu);
@@ -684,6 +695,9 @@ constexpr int PIPE_LROW = 48, PIPE_RROW = 48;  // bytes per staged row (2-way ba
 constexpr int PIPE_SLOT = 11 * PIPE_LROW + 11 * PIPE_RROW;  // 1056 B per keypoint
 constexpr int PIPE_PART = 2 * PIPE_SLOT;                    // SAD partials [121] int
 constexpr int PIPE_WARP = PIPE_PART + 496;                  // per-warp buffer
+#ifndef FT_P1_PAIRS
+#define FT_P1_PAIRS 1  // two keypoints per warp in phase 1 (+2-3 % ring, ab4)
+#endif
 constexpr int KB_N = 256;                                   // keypoints per batch
 struct KbMeta {  // one keypoint between the passes (32 B)
     unsigned long long lrow0, rrow0;  // patch row 0 (left) / strip row 0 (right)
@@ -762,8 +776,17 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
         mbar_wait(mbar1, (mphase >> 1) & 1u);  // bit 1: phase of mbar[1]
         mphase ^= 2u;
         // ---- B: phase 1, warp per keypoint (kernels.py:312-345)
+#if FT_P1_PAIRS  // two keypoints per warp, 16 lanes each
+        for (int i2 = 2 * wid; i2 < nb; i2 += 2 * TK_WARPS) {
+            const int h = lane >> 4, hl = lane & 15, i = i2 + h;
+            const bool live = i < nb;
+            const unsigned r = base + KB_REC + 64u * (unsigned)(live ? i : i2);
+#else
         for (int i = wid; i < nb; i += TK_WARPS) {
+            constexpr bool live = true;
+            const int hl = lane;
             const unsigned r = base + KB_REC + 64u * (unsigned)i;
+#endif
             LeftKp kp;
             kp.u = lds_f64(r);
             kp.v = lds_f64(r + 8);
@@ -771,9 +794,10 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
             kp.d.hi = lds_v4(r + 32);
             kp.o = lds_s32(r + 56);
             int cdist;
-            const int cand = a.stage_rdesc ? phase1<true>(a, sm, kp, lane, cdist)
-                                           : phase1<false>(a, sm, kp, lane, cdist);
-            if (lane == 0) {
+            constexpr int LPP = FT_P1_PAIRS ? 16 : 32;
+            const int cand = a.stage_rdesc ? phase1<true, LPP>(a, sm, kp, hl, cdist, live)
+                                           : phase1<false, LPP>(a, sm, kp, hl, cdist, live);
+            if (live && hl == 0) {
                 km[i].cand = cand;
                 km[i].cdist = (short)cdist;
             }
