@@ -693,7 +693,11 @@ FT_DEV void stereo_kp(const TrackArgs &a, const StereoSmem &sm, int *patch, int 
 // the in-level bytes).
 constexpr int PIPE_LROW = 48, PIPE_RROW = 48;  // bytes per staged row (2-way banks)
 constexpr int PIPE_SLOT = 11 * PIPE_LROW + 11 * PIPE_RROW;  // 1056 B per keypoint
-constexpr int PIPE_PART = 2 * PIPE_SLOT;                    // SAD partials [121] int
+#ifndef FT_PIPE_NS
+#define FT_PIPE_NS 3
+#endif
+constexpr int PIPE_NS = FT_PIPE_NS;                         // patch slots per warp
+constexpr int PIPE_PART = PIPE_NS * PIPE_SLOT;              // SAD partials [121] int
 constexpr int PIPE_WARP = PIPE_PART + 496;                  // per-warp buffer
 #ifndef FT_P1_PAIRS
 #define FT_P1_PAIRS 1  // two keypoints per warp in phase 1 (+2-3 % ring, ab4)
@@ -871,14 +875,19 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
                 pipe_chunk(rb + r * PIPE_RROW + 16 * q, c0 + 16 * q, rp, rp + wr * a.PR.heights[o], coh);
             }
         };
+        // PIPE_NS slots per warp: items PIPE_NS - 1 ahead are in flight
         int j = wid;
-        if (j < nl) issue(j, 0);
-        cp_async_commit();
-        for (int t = 0; j < nl; j += TK_WARPS, ++t) {
-            const int sl = t & 1;
-            if (j + TK_WARPS < nl) issue(j + TK_WARPS, sl ^ 1);
+#pragma unroll
+        for (int q = 0; q < PIPE_NS - 1; ++q) {
+            if (j + q * TK_WARPS < nl) issue(j + q * TK_WARPS, q);
             cp_async_commit();
-            cp_async_wait<1>();  // item j's patches
+        }
+        for (int t = 0; j < nl; j += TK_WARPS, ++t) {
+            const int sl = t % PIPE_NS;
+            const int ja = j + (PIPE_NS - 1) * TK_WARPS;
+            if (ja < nl) issue(ja, (t + PIPE_NS - 1) % PIPE_NS);
+            cp_async_commit();
+            cp_async_wait<PIPE_NS - 1>();  // item j's patches
             __syncwarp();
             const int idx = lds_u16(base + KB_LIST + 2u * j);
             const unsigned mr = base + KB_META + 32u * (unsigned)idx;
