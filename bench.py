@@ -40,7 +40,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
-RING_GROUPS = (1, 2, 4, 10, 14)  # persistent step-group counts tried (ft_track_plan_groups)
+RING_GROUPS = (1, 2, 4, 10, 14, 20)  # persistent step-group counts tried (ft_track_plan_groups)
 PERSIST_GROUPS = (1, 2, 4)  # ... for the 8-slot persistent runner (e2e)
 FALLBACK_HBM = 6650.0
 

@@ -389,7 +389,7 @@ int ft_track_plan(int32_t n_frames, const ft_keypoints *left, const ft_keypoints
                   const ft_project_io *io, int32_t pmode, const ft_project_out *pout,
                   const ft_workspace *ws, void *plan, size_t plan_bytes);
 
-/* As ft_track_plan, for a persistent launch of `groups` step groups (1..16):
+/* As ft_track_plan, for a persistent launch of `groups` step groups (1..36):
  * the geometry gets 1 / groups of the SMs and the launch runs `groups`
  * disjoint block groups, group g taking steps k = g mod groups -- that many
  * frames in flight at once.  All plans of one launch share `groups`, and the

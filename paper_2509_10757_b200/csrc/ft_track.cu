@@ -2862,7 +2862,7 @@ extern "C" int ft_track_plan_groups(int32_t n_frames, const ft_keypoints *left,
                                     const ft_workspace *ws, int32_t groups, void *plan,
                                     size_t plan_bytes) {
     if (!plan) return FT_E_NULL;
-    if (groups < 1 || groups > 16) return FT_E_RANGE;
+    if (groups < 1 || groups > 36) return FT_E_RANGE;
     if (plan_bytes < sizeof(TrackPlan)) return FT_E_RANGE;
     TrackPlan *tp = static_cast<TrackPlan *>(plan);
     memset(tp, 0, sizeof(*tp));

@@ -655,6 +655,38 @@ def test_runner_auto_mode(workloads, expected):
 
 
 @pytest.mark.timeout(180)
+@pytest.mark.timeout(180)
+def test_resident_ring_20_groups(workloads, expected):
+    """ft_track_frames_ring at the bench's step-group pick: 20 groups of 7
+    blocks (4 stereo + 3 map each) over 20 resident pipelines, 45 steps
+    (every pipeline runs 2-3 times): every pipeline's outputs equal the
+    oracle's."""
+    import torch
+    from paper_2509_10757_b200.pipeline import FramePipeline, run_ring
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left) for _ in range(20)]
+    for i, p in enumerate(pipes):
+        w = workloads[i % 4]
+        p.load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                     slots=expected[i % 4][1])
+        p.dev[:p.in_end].copy_(p.host[:p.in_end])
+        p.dev[p.out_begin:p.out_end].fill_(0x5A)
+    torch.cuda.synchronize()
+    run_ring(pipes, 45, groups=20)
+    pipes[0].synchronize()
+    for i, p in enumerate(pipes):
+        w = workloads[i % 4]
+        p.copy_outputs()
+        m, _, slots, n = expected[i % 4]
+        res = p.result(0, len(w.left.u))
+        for f in FIELDS:
+            np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f), err_msg=f)
+        np.testing.assert_array_equal(res.slots, slots)
+        assert res.n_slots == n
+
+
 def test_resident_ring_multi_stream(workloads, expected):
     """ft_track_frames_ring over 3 pipelines of 2 streams each (2 frames per
     step: group barriers inside the persistent kernel, no tail blocks):

@@ -1,7 +1,7 @@
 # final round-2 evidence: ncu of the ring at the bench's picks, sanitizers,
 # GPU tests, smoke, full bench lines (driver command, default), reference arm
 P=${1:-r2fin}
-for gk in "10 20" "14 200"; do
+for gk in "20 20" "20 200"; do
   set -- $gk
   ncu --set full --import-source on --clock-control none -k regex:track_persist_kernel -s 1 -c 1 \
       -o gpurun_out/${P}_ring_g$1_k$2 python tools/ncu_ring.py $1 $2 > gpurun_out/${P}_ncu_g$1_k$2.log 2>&1
