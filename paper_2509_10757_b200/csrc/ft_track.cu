@@ -702,7 +702,11 @@ constexpr int PIPE_WARP = PIPE_PART + 496;                  // per-warp buffer
 #ifndef FT_P1_PAIRS
 #define FT_P1_PAIRS 1  // two keypoints per warp in phase 1 (+2-3 % ring, ab4)
 #endif
-constexpr int KB_N = 256;                                   // keypoints per batch
+#ifndef FT_KB_N
+#define FT_KB_N 384  // one batch per stereo block at 20 step groups (320 keypoints); 256: +6 % slower there
+#endif
+constexpr int KB_N = FT_KB_N;  // keypoints per batch (<= TK_THREADS: G and D run a thread each)
+static_assert(KB_N <= TK_THREADS, "one thread per batch keypoint");                                   // keypoints per batch
 struct KbMeta {  // one keypoint between the passes (32 B)
     unsigned long long lrow0, rrow0;  // patch row 0 (left) / strip row 0 (right)
     int xr0, cand;
