@@ -707,18 +707,20 @@ constexpr int PIPE_WARP = PIPE_PART + 496;                  // per-warp buffer
 #endif
 constexpr int KB_N = FT_KB_N;  // keypoints per batch (<= TK_THREADS: G and D run a thread each)
 static_assert(KB_N <= TK_THREADS, "one thread per batch keypoint");                                   // keypoints per batch
-struct KbMeta {  // one keypoint between the passes (32 B)
+struct KbMeta {  // one keypoint between the passes (40 B)
     unsigned long long lrow0, rrow0;  // patch row 0 (left) / strip row 0 (right)
     int xr0, cand;
     short cdist;
     unsigned char o, state;        // state 1: SAD sweep to run
     unsigned char loff, lw, roff, rw;  // row 0 address & 15, row pitch & 15
+    unsigned short wl, wr;         // row pitches (level widths)
+    unsigned char inside, pad_[3];  // 1: every 16-B chunk of both patches is in its level
 };
-static_assert(sizeof(KbMeta) == 32, "KbMeta is 32 B");
+static_assert(sizeof(KbMeta) == 40, "KbMeta is 40 B");
 // byte offsets inside the stereo patch region (16-B aligned)
 constexpr int KB_REC = TK_WARPS * PIPE_WARP;  // ft_kp_record [KB_N]
 constexpr int KB_META = KB_REC + KB_N * 64;   // KbMeta [KB_N]
-constexpr int KB_SAD = KB_META + KB_N * 32;   // int4 (best offset, s-, s0, s+) [KB_N]
+constexpr int KB_SAD = KB_META + KB_N * 40;   // int4 (best offset, s-, s0, s+) [KB_N]
 constexpr int KB_LIST = KB_SAD + KB_N * 16;   // uint16 [KB_N]
 constexpr int KB_END = KB_LIST + KB_N * 2;
 // per-warp share of the region (the host sizes patch_ints from it)
@@ -848,6 +850,18 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
             m.lw = (unsigned char)(g.wl & 15);
             m.roff = (unsigned char)((uintptr_t)rrow0 & 15);
             m.rw = (unsigned char)(g.wr & 15);
+            m.wl = (unsigned short)g.wl;
+            m.wr = (unsigned short)g.wr;
+            m.inside = 0;
+            if (m.state) {  // all chunks of both patches inside their levels: no per-chunk checks
+                const uintptr_t l0 = (uintptr_t)lrow0 & ~(uintptr_t)15,
+                                l1 = (((uintptr_t)lrow0 + 10 * g.wl) & ~(uintptr_t)15) + 32,
+                                r0 = (uintptr_t)rrow0 & ~(uintptr_t)15,
+                                r1 = (((uintptr_t)rrow0 + 10 * g.wr) & ~(uintptr_t)15) + 48;
+                const uintptr_t lb0 = (uintptr_t)g.lp, lb1 = lb0 + g.wl * a.PL.heights[g.o];
+                const uintptr_t rb0 = (uintptr_t)g.rp, rb1 = rb0 + g.wr * a.PR.heights[g.o];
+                m.inside = l0 >= lb0 && l1 <= lb1 && r0 >= rb0 && r1 <= rb1;
+            }
             km[i] = m;
             need = m.state;
         }
@@ -857,15 +871,38 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
         __syncthreads();
         if (bt == 0) TL_MARK(a, 9);
         // ---- C: SAD sweeps (kernels.py:388-409), warp per listed keypoint
+        // per-lane chunk of the copies: left (row lane / 2, chunk lane & 1)
+        // for lanes < 22, right (row lane / 3, chunk lane % 3) and, lane 0,
+        // the right strip's 33rd chunk (row 10, chunk 2)
+        const int lcr = lane >> 1, lcq = lane & 1, rcr = lane / 3, rcq = lane - 3 * (lane / 3);
         auto issue = [&](int j, int sl) {  // item j's patches -> slot sl
-            const unsigned mr = base + KB_META + 32u * (unsigned)lds_u16(base + KB_LIST + 2u * j);
+            const unsigned mr = base + KB_META + 40u * (unsigned)lds_u16(base + KB_LIST + 2u * j);
             const uint8_t *lrow0 = reinterpret_cast<const uint8_t *>(lds_u64(mr));
             const uint8_t *rrow0 = reinterpret_cast<const uint8_t *>(lds_u64(mr + 8));
+            const int wlr = lds_s32(mr + 32);
+            unsigned char *lb = pb + wid * PIPE_WARP + sl * PIPE_SLOT;
+            unsigned char *rb = lb + 11 * PIPE_LROW;
+            if (lds_u8(mr + 36)) {  // interior: plain 16-B copies
+                const int wl = wlr & 0xffff, wr = (wlr >> 16) & 0xffff;
+                if (lane < 2 * NW) {
+                    const uintptr_t c0 = ((uintptr_t)lrow0 + lcr * wl) & ~(uintptr_t)15;
+                    cp_async16(lb + lcr * PIPE_LROW + 16 * lcq,
+                               reinterpret_cast<const void *>(c0 + 16 * lcq));
+                }
+                {
+                    const uintptr_t c0 = ((uintptr_t)rrow0 + rcr * wr) & ~(uintptr_t)15;
+                    cp_async16(rb + rcr * PIPE_RROW + 16 * rcq,
+                               reinterpret_cast<const void *>(c0 + 16 * rcq));
+                }
+                if (lane == 0) {
+                    const uintptr_t c0 = ((uintptr_t)rrow0 + 10 * wr) & ~(uintptr_t)15;
+                    cp_async16(rb + 10 * PIPE_RROW + 32, reinterpret_cast<const void *>(c0 + 32));
+                }
+                return;
+            }
             const int o = lds_u8(mr + 26);
             const long long wl = a.PL.widths[o], wr = a.PR.widths[o];
             const uint8_t *lp = lframe + a.PL.offsets[o], *rp = rframe + a.PR.offsets[o];
-            unsigned char *lb = pb + wid * PIPE_WARP + sl * PIPE_SLOT;
-            unsigned char *rb = lb + 11 * PIPE_LROW;
             if (lane < 2 * NW) {  // chunks bounded by the level's own bytes
                 const uint8_t *row = lrow0 + (lane >> 1) * wl;
                 const uint8_t *c0 = reinterpret_cast<const uint8_t *>((uintptr_t)row & ~(uintptr_t)15);
@@ -894,7 +931,7 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
             cp_async_wait<PIPE_NS - 1>();  // item j's patches
             __syncwarp();
             const int idx = lds_u16(base + KB_LIST + 2u * j);
-            const unsigned mr = base + KB_META + 32u * (unsigned)idx;
+            const unsigned mr = base + KB_META + 40u * (unsigned)idx;
             const int pk = lds_s32(mr + 28);  // loff, lw, roff, rw
             const int loff = pk & 255, lw = (pk >> 8) & 255, roff = (pk >> 16) & 255,
                       rw = (pk >> 24) & 255;
