@@ -1943,6 +1943,8 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
             }
             if (r0 == p0) TL_MARK(a, 7);
             __syncthreads();
+            const int rr = (r0 - p0) / round_cap;  // round (debug marks 8..15: rounds 0-3)
+            if (rr < 4) TL_MARK(a, 8 + 2 * rr);
             const int li = threadIdx.x;
             const int i = r0 + li;
             if (i < r1) {
@@ -2020,6 +2022,7 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
                 }
             }
             __syncthreads();
+            if (rr < 4) TL_MARK(a, 9 + 2 * rr);
         }
     }
     TL_MARK(a, 3);

@@ -51,7 +51,9 @@ t0 = T[:, 0][T[:, 0] > 0].min()
 names = {"stereo": ["start", "staged+csr", "phase1/2 done", "barrier", "end", "-", "table landed",
                     "-", "B phase 1", "G geometry", "C SAD sweeps", "-", "-", "gathered", "median"],
          "map": ["start", "staged+csr+hash", "projected (last round)", "searched", "barrier", "end",
-                 "table landed", "points landed", "-", "-", "-", "project start", "thread 0 projected"]}
+                 "table landed", "points landed", "round 0 projecting", "round 0 done",
+                 "round 1 projecting", "round 1 done", "round 2 projecting", "round 2 done",
+                 "round 3 projecting", "round 3 done"]}
 for role, sel in (("stereo", [i for i in range(len(T)) if i % per < Gs]),
                   ("map", [i for i in range(len(T)) if i % per >= Gs])):
     Rr = T[sel]
