@@ -786,9 +786,10 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
         mbar_wait(mbar1, (mphase >> 1) & 1u);  // bit 1: phase of mbar[1]
         mphase ^= 2u;
         // ---- B: phase 1, warp per keypoint (kernels.py:312-345)
-#if FT_P1_PAIRS  // two keypoints per warp, 16 lanes each
-        for (int i2 = 2 * wid; i2 < nb; i2 += 2 * TK_WARPS) {
-            const int h = lane >> 4, hl = lane & 15, i = i2 + h;
+#if FT_P1_PAIRS  // FT_P1_PAIRS keypoints per warp (2 or 4), 32 / that lanes each
+        constexpr int KPW = FT_P1_PAIRS >= 4 ? 4 : 2, LW = 32 / KPW;
+        for (int i2 = KPW * wid; i2 < nb; i2 += KPW * TK_WARPS) {
+            const int h = lane / LW, hl = lane % LW, i = i2 + h;
             const bool live = i < nb;
             const unsigned r = base + KB_REC + 64u * (unsigned)(live ? i : i2);
 #else
@@ -804,7 +805,7 @@ __device__ void stereo_block_pipe55(const TrackArgs &a, const StereoSmem &sm, in
             kp.d.hi = lds_v4(r + 32);
             kp.o = lds_s32(r + 56);
             int cdist;
-            constexpr int LPP = FT_P1_PAIRS ? 16 : 32;
+            constexpr int LPP = FT_P1_PAIRS ? (FT_P1_PAIRS >= 4 ? 8 : 16) : 32;
             const int cand = a.stage_rdesc ? phase1<true, LPP>(a, sm, kp, hl, cdist, live)
                                            : phase1<false, LPP>(a, sm, kp, hl, cdist, live);
             if (live && hl == 0) {
