@@ -584,11 +584,11 @@ def test_rejection_median_near_histogram_edge(oracle, amp, tail, monkeypatch):
 
 @pytest.mark.parametrize("seed", [31, 32])
 def test_pipelined_patch_edges_vs_oracle(oracle, seed):
-    """The pipelined stereo loop stages patch rows as 16-B chunks, falling back
+    """The block-batched SAD pass stages patch rows as 16-B chunks, falling back
     to byte loads where a chunk would reach outside its level (first / last
     rows and columns of a level, the end of the last level).  Keypoints placed
     on every level right at the patch borders, through the fused call (the
-    pipelined loop; the session's pyramid base is not 16-B aligned), must
+    block-batched passes; the session's pyramid base is not 16-B aligned), must
     equal the oracle."""
     from synthetic import make_workload
     from paper_2509_10757_b200.types import FeatureSet

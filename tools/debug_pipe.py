@@ -1,4 +1,4 @@
-"""Debug: the pipelined stereo loop vs the per-keypoint loop on the cfg1
+"""Debug: the block-batched stereo passes vs the per-keypoint loop on the cfg1
 golden frame (phase 1 + phase 2, no rejection), per keypoint."""
 import os
 import subprocess
