@@ -687,6 +687,39 @@ def test_resident_ring_20_groups(workloads, expected):
         assert res.n_slots == n
 
 
+@pytest.mark.timeout(240)
+def test_resident_ring_35_groups_multi_batch(workloads, expected):
+    """ft_track_frames_ring at 35 step groups: 4 blocks per group, so a frame
+    has ONE stereo block holding every left keypoint -- the block-batched
+    stereo passes then run several 384-keypoint batches (records re-staged
+    per batch on mbar[1]).  Every pipeline's outputs equal the oracle's."""
+    import torch
+    from paper_2509_10757_b200.pipeline import FramePipeline, run_ring
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    assert max(len(w.left.u) for w in workloads) > 384  # more than one batch per block
+    pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left) for _ in range(35)]
+    for i, p in enumerate(pipes):
+        w = workloads[i % 4]
+        p.load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                     slots=expected[i % 4][1])
+        p.dev[:p.in_end].copy_(p.host[:p.in_end])
+        p.dev[p.out_begin:p.out_end].fill_(0x5A)
+    torch.cuda.synchronize()
+    run_ring(pipes, 70, groups=35)
+    pipes[0].synchronize()
+    for i, p in enumerate(pipes):
+        w = workloads[i % 4]
+        p.copy_outputs()
+        m, _, slots, n = expected[i % 4]
+        res = p.result(0, len(w.left.u))
+        for f in FIELDS:
+            np.testing.assert_array_equal(getattr(res.matches, f), getattr(m, f), err_msg=f)
+        np.testing.assert_array_equal(res.slots, slots)
+        assert res.n_slots == n
+
+
 def test_resident_ring_multi_stream(workloads, expected):
     """ft_track_frames_ring over 3 pipelines of 2 streams each (2 frames per
     step: group barriers inside the persistent kernel, no tail blocks):
