@@ -2036,21 +2036,36 @@ __device__ void map_frame(const TrackArgs &a, int f, int rank, int slot, unsigne
     group_barrier(bar, G, bpar);
     TL_MARK(a, 4);
 
-    // phase B on this block's points: winner iff its claim is the minimum
+    // phase B on this block's points: winner iff its claim is the minimum.
+    // The block's claim words are loaded in one round trip (a chunk is at
+    // most TK_MAP_CHUNK_MAX points), then compared.
     int n_win = 0;
-    for (int i = p0 + threadIdx.x; i < p1; i += TK_THREADS) {
-        const int r = sm.res[i - p0];
-        if (r < 0) continue;
-        const int kp = r & 0xffff, d = (r >> 16) & 0x1ff;
-        const unsigned long long key = ((unsigned long long)epoch_hi << 32) |
-                                       ((unsigned long long)d << 23) | (unsigned)i;
-        if (__ldcg(a.claims + kbase + kp) != key) {
-            sm.res[i - p0] = -1;
-            continue;
+    {
+        constexpr int MAXI = (TK_MAP_CHUNK_MAX + TK_THREADS - 1) / TK_THREADS;
+        int rr[MAXI];
+        unsigned long long cl[MAXI];
+#pragma unroll
+        for (int u = 0; u < MAXI; ++u) {
+            const int i = p0 + (int)threadIdx.x + u * TK_THREADS;
+            rr[u] = i < p1 ? sm.res[i - p0] : -1;
+            cl[u] = rr[u] >= 0 ? __ldcg(a.claims + kbase + (rr[u] & 0xffff)) : 0ull;
         }
-        ++n_win;
-        if (rotation)
-            atomicAdd(a.hist + (int64_t)f * TK_MAX_BINS + rotation_bin(a, kbase, pbase, kp, i), 1);
+#pragma unroll
+        for (int u = 0; u < MAXI; ++u) {
+            const int i = p0 + (int)threadIdx.x + u * TK_THREADS;
+            const int r = rr[u];
+            if (r < 0) continue;
+            const int kp = r & 0xffff, d = (r >> 16) & 0x1ff;
+            const unsigned long long key = ((unsigned long long)epoch_hi << 32) |
+                                           ((unsigned long long)d << 23) | (unsigned)i;
+            if (cl[u] != key) {
+                sm.res[i - p0] = -1;
+                continue;
+            }
+            ++n_win;
+            if (rotation)
+                atomicAdd(a.hist + (int64_t)f * TK_MAX_BINS + rotation_bin(a, kbase, pbase, kp, i), 1);
+        }
     }
     if (rotation) {
         group_barrier(bar, G, bpar);
