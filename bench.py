@@ -578,6 +578,7 @@ def main() -> None:
     # is noise at ~50 us per step.
     runner, staged, ranges = make_runner(args, frames, pipe, table, load)
     shipped = float(np.mean([hi - lo for lo, hi in ranges]))
+    same_ranges = all(tuple(r) == tuple(ranges[0]) for r in ranges)
     from paper_2509_10757_b200.pipeline import AsyncRunner
     ranges = [AsyncRunner.ranges_arg(r) for r in ranges]  # marshalled once, not per step
     staged_keep = staged  # the pinned ring rows (kept alive: only pointers go to submit)
@@ -668,6 +669,57 @@ def main() -> None:
         except Exception as exc:  # noqa: BLE001  (reported, never fatal)
             print(f"[bench] persistent runner: {type(exc).__name__}: {exc}", file=sys.stderr)
 
+    # ---- e2e, persistent runner with batched submits: m consecutive steps'
+    # inputs (rows of the pinned staging ring) go up as ONE strided copy per
+    # range into slots that share a DeviceArena (ft_runner_submit_batch): the
+    # copy engine's ~3.6 us fixed cost per copy is paid once per m steps.
+    # Every step is still its own frame: H2D, track, results back to the host.
+    # Measured slower than one submit per step (62-66k vs 71k frames/s at
+    # K = 200, profiles/r3_batched_submit_negative.txt): opt-in, FT_BENCH_BATCH=1.
+    batch_by = {}
+    ring_rows = getattr(runner, "staging", None)
+    if (not raw and same_ranges and ring_rows is not None and persist_ms
+            and os.environ.get("FT_BENCH_BATCH", "0") != "0"):
+        try:
+            from paper_2509_10757_b200.pipeline import AsyncRunner, DeviceArena
+            n_max = 16
+            arena = DeviceArena(n_max)
+            apipes = [FramePipeline(pipe.cam, n_streams=pipe.S, cap_kp=pipe.cap_kp,
+                                    cap_points=pipe.cap_pts, pyramid_geometry=pipe.pyr,
+                                    map_table=table, arena=arena) for _ in range(n_max)]
+            nr = len(staged)
+            for n_p, m, G in ((8, 2, 2), (8, 4, 2), (16, 1, 2), (16, 2, 2), (16, 4, 2),
+                              (16, 4, 1), (16, 8, 2)):
+                if nr % m or n_p % m:
+                    continue
+                if True:
+                    pr = AsyncRunner(apipes[:n_p], persistent=True, groups=G)
+                    try:
+                        def run(k, n_steps):
+                            end = k + n_steps
+                            while k < end:
+                                mm = min(m, end - k)
+                                j = k % nr
+                                pr.submit_batch(k, ring_rows[j:j + mm], ranges[0])
+                                k += mm
+                            return k
+                        k, tw = 0, time.perf_counter()
+                        while k < max(args.warmup, 4 * nr + 2) or time.perf_counter() - tw < 0.3:
+                            k = run(k, m)
+                        pr.wait(k - 1)
+                        t0 = time.perf_counter()
+                        k = run(k, args.steps)
+                        pr.wait(k - 1)
+                        batch_by[f"n{n_p}_m{m}_g{G}"] = 1e3 * (time.perf_counter() - t0)
+                    finally:
+                        pr.close()
+            del apipes, arena
+        except Exception as exc:  # noqa: BLE001  (reported, never fatal)
+            print(f"[bench] batched persistent runner: {type(exc).__name__}: {exc}",
+                  file=sys.stderr)
+    batch_ms = min(batch_by.values()) if batch_by else None
+    batch_pick = min(batch_by, key=batch_by.get) if batch_by else None
+
     # ---- per-kernel timing for the roofline (eager, on the launching stream)
     kern = {"pyramids": [], "track": [], "stereo_only": [], "map_only": []}
     for k in range(max(10, args.steps // 2)):
@@ -688,9 +740,9 @@ def main() -> None:
     tot_comp = sum(comp_ms)
     tot_e2e = sum(e2e_ms)
     from paper_2509_10757_b200.sharding import job_frames_per_s, max_over_ranks
-    tot_comp, tot_e2e, async_ms, stream_ms, persist_any, ring_any = max_over_ranks(
+    tot_comp, tot_e2e, async_ms, stream_ms, persist_any, ring_any, batch_any = max_over_ranks(
         [tot_comp, tot_e2e, async_ms, stream_ms, persist_ms if persist_ms else 0.0,
-         ring_ms if ring_ms else 0.0], dist, device="cuda")
+         ring_ms if ring_ms else 0.0, batch_ms if batch_ms else 0.0], dist, device="cuda")
     value_graph = job_frames_per_s(S * args.steps, world, stream_ms)
     value_ring = (job_frames_per_s(S * args.steps, world, ring_any)
                   if ring_ms and ring_any > 0 else None)
@@ -709,6 +761,10 @@ def main() -> None:
     cands = {"async": e2e_async, "serial": e2e_serial}
     if e2e_persist:
         cands["persistent"] = e2e_persist
+    e2e_batch = (job_frames_per_s(S * args.steps, world, batch_any)
+                 if batch_ms and batch_any > 0 else None)
+    if e2e_batch:
+        cands["persistent_batched"] = e2e_batch
     e2e_method = max(cands, key=cands.get)
     e2e_value = cands[e2e_method]
 
@@ -811,10 +867,20 @@ def main() -> None:
                                               "kernel handed each step through mapped "
                                               "host flags (no launch per step), G step "
                                               "groups (G steps computed at once; best of "
-                                              f"{list(PERSIST_GROUPS)}); host wall clock"},
+                                              f"{list(PERSIST_GROUPS)}); host wall clock",
+                                "persistent_batched": "the persistent runner over 8 slots in "
+                                                      "one DeviceArena: m consecutive steps' "
+                                                      "inputs (pinned ring rows) go up as ONE "
+                                                      "strided 2D copy (ft_runner_submit_batch), "
+                                                      "each step still its own frame with its "
+                                                      "results pushed to the host; best of "
+                                                      "m in (2, 4) x G in (1, 2); host wall clock"},
                     "async_value": e2e_async,
                     "serial_value": e2e_serial,
                     "persistent_value": e2e_persist,
+                    "persistent_batched_value": e2e_batch,
+                    "persistent_batched_pick": batch_pick,
+                    "persistent_batched_ms": batch_by,
                     "persistent_groups": persist_groups,
                     "persistent_ms_by_groups": {str(g): v for g, v in persist_by_g.items()},
                     "latency_ms_per_frame_e2e": persist_lat_ms,
@@ -946,7 +1012,9 @@ def make_runner(args, frames, pipe, table, load):
         ranges.append(pipe.input_range())
     for t in twins:
         t.capture()
-    return AsyncRunner([pipe] + twins), [ring[k] for k in range(n)], ranges
+    r = AsyncRunner([pipe] + twins)
+    r.staging = ring  # [n, in_end] rows at one pitch (batched submits)
+    return r, [ring[k] for k in range(n)], ranges
 
 
 def _pipe_rates(torch, pipes, staged, steps, flush, S, ranges=None) -> dict:

@@ -274,7 +274,7 @@ int ft_scatter_points(int32_t n, const ft_point_record *recs, const int32_t *slo
  * ft_runner_wait(k) blocks until step k's outputs are on the host.  Slot
  * buffers are reused n steps later (the runner orders that itself). */
 typedef struct ft_runner ft_runner;
-#define FT_RUNNER_MAX_SLOTS 8
+#define FT_RUNNER_MAX_SLOTS 16
 int ft_runner_create(const void *const graph_exec[2], void *const dev_in[2], size_t in_bytes,
                      void *const dev_out[2], void *const host_out[2], size_t out_bytes,
                      ft_runner **out);
@@ -292,11 +292,21 @@ int ft_runner_submit_range(ft_runner *r, int64_t k, const void *host_in, size_t 
  * levels). */
 int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host_in,
                             const uint64_t *ranges, int32_t n_ranges);
+/* Steps k .. k+m-1 (1 <= m <= n_slots) at once: step k+j's inputs are at
+ * host_in + j * host_pitch (host_pitch >= the slot input size when m > 1),
+ * the same byte ranges for every step.  When the m slots do not wrap and
+ * their device inputs sit at one pitch (one arena), each range goes up as ONE
+ * strided 2D copy of m rows: the copy engine's fixed cost per copy (~3.6 us,
+ * profiles/r3_h2d2d_probe.txt) is paid once per m steps instead of per step
+ * (448 KB ranges: 84k -> 99k / 109k per s at m = 2 / 4).  Otherwise it issues
+ * the m steps' copies one by one -- same results either way. */
+int ft_runner_submit_batch(ft_runner *r, int64_t k, int32_t m, const void *host_in,
+                           size_t host_pitch, const uint64_t *ranges, int32_t n_ranges);
 int ft_runner_wait(ft_runner *r, int64_t k);
 int ft_runner_destroy(ft_runner *r);
 
 /* Persistent runner: instead of a graph launch per step, ONE long-lived
- * ft_track_frames kernel serves the n slots (2..8).  plans[i] holds slot i's
+ * ft_track_frames kernel serves the n slots (2..16).  plans[i] holds slot i's
  * launch (ft_track_plan over that slot's device buffers; all slots the same
  * shapes).  The runner's host thread hands a step to the kernel through a
  * pinned, mapped flag once the step's inputs have landed, and issues the

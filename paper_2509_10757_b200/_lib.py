@@ -110,7 +110,7 @@ EXPORTS = ("ft_abi_version", "ft_status_string", "ft_workspace_bytes", "ft_works
            "ft_hamming_pairs", "ft_stereo_pinhole", "ft_stereo_fisheye_bf", "ft_project_search",
            "ft_track_frames", "ft_resolve_conflicts", "ft_rotation_filter", "ft_bench_popc",
            "ft_pack_keypoints", "ft_pack_points", "ft_build_pyramids", "ft_stereo_fisheye",
-           "ft_gather_points", "ft_scatter_points", "ft_copy_ranges", "ft_runner_create", "ft_runner_create_n", "ft_runner_submit", "ft_runner_submit_range", "ft_runner_submit_ranges",
+           "ft_gather_points", "ft_scatter_points", "ft_copy_ranges", "ft_runner_create", "ft_runner_create_n", "ft_runner_submit", "ft_runner_submit_range", "ft_runner_submit_ranges", "ft_runner_submit_batch",
            "ft_runner_wait", "ft_runner_destroy", "ft_runner_create_persistent",
            "ft_track_plan", "ft_track_plan_groups", "ft_track_plan_bytes", "ft_track_frames_ring", "ft_session_create",
            "ft_session_destroy", "ft_session_stats", "ft_session_stereo", "ft_session_project", "ft_session_fisheye",
@@ -159,6 +159,7 @@ def load() -> ctypes.CDLL:
     L.ft_runner_submit.argtypes = [vp, i64, vp]
     L.ft_runner_submit_range.argtypes = [vp, i64, vp, ctypes.c_size_t, ctypes.c_size_t]
     L.ft_runner_submit_ranges.argtypes = [vp, i64, vp, vp, i32]
+    L.ft_runner_submit_batch.argtypes = [vp, i64, i32, vp, ctypes.c_size_t, vp, i32]
     L.ft_runner_wait.argtypes = [vp, i64]
     L.ft_runner_destroy.argtypes = [vp]
     L.ft_runner_create_persistent.argtypes = [i32, vp, vp, ctypes.c_size_t, vp, vp,

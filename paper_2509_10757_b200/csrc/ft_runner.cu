@@ -56,7 +56,7 @@ extern "C" int ft_internal_persist_launch(const void *const *plans, int n, unsig
 extern "C" void ft_internal_persist_dump(void);
 
 namespace {
-constexpr int PERSIST_MAX_SLOTS = 8;  // == ft_track.cu
+constexpr int PERSIST_MAX_SLOTS = 16;  // == ft_track.cu
 constexpr unsigned PERSIST_STOP = 0xffffffffu;
 }  // namespace
 
@@ -400,6 +400,60 @@ extern "C" int ft_runner_submit_ranges(ft_runner *r, int64_t k, const void *host
                             r->d2h);
     if (e == cudaSuccess) e = cudaEventRecord(r->ev_d2h[i], r->d2h);
     return (int)e;
+}
+
+extern "C" int ft_runner_submit_batch(ft_runner *r, int64_t k, int32_t m, const void *host_in,
+                                      size_t host_pitch, const uint64_t *ranges,
+                                      int32_t n_ranges) {
+    if (!r || !host_in || (!ranges && n_ranges > 0)) return FT_E_NULL;
+    if (k < 0 || n_ranges < 0 || m < 1 || m > r->n) return FT_E_RANGE;
+    if (m > 1 && host_pitch < r->in_bytes) return FT_E_RANGE;
+    for (int q = 0; q < n_ranges; ++q)
+        if (ranges[2 * q] > ranges[2 * q + 1] || ranges[2 * q + 1] > r->in_bytes) return FT_E_RANGE;
+    const int i0 = (int)(k % r->n);
+    // one strided copy per range needs the m slots' device inputs at one pitch
+    size_t dpitch = 0;
+    bool strided = r->persistent && m > 1 && i0 + m <= r->n;
+    if (strided) {
+        const char *b0 = static_cast<const char *>(r->dev_in[i0]);
+        const char *b1 = static_cast<const char *>(r->dev_in[i0 + 1]);
+        strided = b1 > b0 && (size_t)(b1 - b0) >= r->in_bytes;
+        dpitch = strided ? (size_t)(b1 - b0) : 0;
+        for (int j = 2; j < m && strided; ++j)
+            strided = static_cast<const char *>(r->dev_in[i0 + j]) == b0 + j * dpitch;
+    }
+    if (!strided) {  // step by step (graph mode, wrapped slots, scattered buffers)
+        for (int j = 0; j < m; ++j) {
+            const int st = ft_runner_submit_ranges(
+                r, k + j, static_cast<const char *>(host_in) + j * host_pitch, ranges, n_ranges);
+            if (st != FT_OK) return st;
+        }
+        return FT_OK;
+    }
+    NvtxRange nv("ft_runner_submit_batch");
+    if (k != r->last_k.load() + 1) return FT_E_RANGE;  // steps are submitted in order
+    // slots i0 .. i0+m-1: their steps k-n .. k+m-1-n must be fully out
+    if (k + m - 1 >= r->n) {
+        const int st = persist_wait(r, k + m - 1 - r->n);
+        if (st != FT_OK) return st;
+    }
+    cudaStream_t hs = r->h2d;
+    cudaError_t e = cudaSuccess;
+    for (int q = 0; q < n_ranges && e == cudaSuccess; ++q) {
+        const size_t lo = ranges[2 * q], w = ranges[2 * q + 1] - lo;
+        if (w)
+            e = cudaMemcpy2DAsync(static_cast<char *>(r->dev_in[i0]) + lo, dpitch,
+                                  static_cast<const char *>(host_in) + lo, host_pitch, w, m,
+                                  cudaMemcpyHostToDevice, hs);
+    }
+    for (int j = 0; j < m && e == cudaSuccess; ++j) e = cudaEventRecord(r->ev_h2d[i0 + j], hs);
+    if (e != cudaSuccess) return (int)e;
+    {
+        std::lock_guard<std::mutex> lk(r->pump_mu);
+        r->last_k.store(k + m - 1, std::memory_order_release);
+    }
+    r->pump_cv.notify_one();
+    return FT_OK;
 }
 
 extern "C" int ft_runner_submit_range(ft_runner *r, int64_t k, const void *host_in,

@@ -2202,7 +2202,7 @@ __global__ void __launch_bounds__(TK_THREADS) track_kernel(const TrackArgs a) {
 // step k + 1 while others finish k (each slot has its own workspace, so the
 // groups' barrier words and tickets never mix).  ready[] == FT_PERSIST_STOP
 // ends the launch.
-constexpr int PERSIST_MAX_SLOTS = 8;
+constexpr int PERSIST_MAX_SLOTS = 16;
 constexpr unsigned FT_PERSIST_STOP = 0xffffffffu;
 
 struct PersistArgs {

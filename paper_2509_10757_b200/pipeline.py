@@ -39,13 +39,36 @@ class StreamResult:
     n_matched: int
 
 
+class DeviceArena:
+    """One device allocation holding n pipelines' buffers at ONE pitch (a
+    2 MB multiple, 2 MB aligned).  AsyncRunner(persistent=True) over such
+    pipelines can then ship m consecutive steps' inputs as one strided copy
+    per range (submit_batch; ft_runner_submit_batch)."""
+
+    def __init__(self, n: int):
+        self.n, self.used, self.pitch, self.buf = int(n), 0, None, None
+
+    def take(self, nbytes: int, device) -> torch.Tensor:
+        pitch = (int(nbytes) + (2 << 20) - 1) // (2 << 20) * (2 << 20)
+        if self.buf is None:
+            self._raw = torch.zeros(self.n * pitch + (2 << 20), dtype=torch.uint8, device=device)
+            off = (-self._raw.data_ptr()) % (2 << 20)
+            self.buf, self.pitch = self._raw[off:off + self.n * pitch], pitch
+        if pitch != self.pitch or self.used >= self.n:
+            raise ValueError(f"DeviceArena: {self.used}/{self.n} rows of {self.pitch} B taken; "
+                             f"cannot place {nbytes} B")
+        row = self.buf[self.used * pitch:self.used * pitch + int(nbytes)]
+        self.used += 1
+        return row
+
+
 class FramePipeline:
     def __init__(self, cam, n_streams: int = 1, cap_kp: int = 2048, cap_points: int = 8192,
                  pyramid_geometry=None, stereo_cfg: StereoMatchConfig | None = None,
                  proj_cfg: ProjectionSearchConfig | None = None, scale: float = 1.2,
                  levels: int = 8, grid_cell_px: int = 48, device: int | None = None,
                  raw_images: bool = False, map_table=None, build_levels: int | None = None,
-                 packed_upload: bool | None = None):
+                 packed_upload: bool | None = None, arena: "DeviceArena | None" = None):
         if not torch.cuda.is_available():
             raise _lib.FtError("FramePipeline needs a CUDA device (no CPU fallback)")
         self.lib = _lib.load()
@@ -160,10 +183,16 @@ class FramePipeline:
         for name in ("c_point", "c_kp", "c_dist", "c_oct"):
             lay.add(name, 8 * S * cp)
         self.lay = lay
-        # 2 MB-aligned arena (GPU large pages): fewest pages per frame
-        self._dev_raw = torch.zeros(lay.total + (2 << 20), dtype=torch.uint8, device=self.device)
-        off = (-self._dev_raw.data_ptr()) % (2 << 20)
-        self.dev = self._dev_raw[off:off + lay.total]
+        # 2 MB-aligned arena (GPU large pages): fewest pages per frame; or a
+        # row of a shared DeviceArena (slots at one pitch: batched submits)
+        if arena is not None:
+            self._dev_raw = arena
+            self.dev = arena.take(lay.total, self.device)
+        else:
+            self._dev_raw = torch.zeros(lay.total + (2 << 20), dtype=torch.uint8,
+                                        device=self.device)
+            off = (-self._dev_raw.data_ptr()) % (2 << 20)
+            self.dev = self._dev_raw[off:off + lay.total]
         self.host = torch.zeros(lay.total, dtype=torch.uint8).pin_memory()
         self.hnp = self.host.numpy()
         self.stream = torch.cuda.Stream(self.device)
@@ -613,8 +642,8 @@ class AsyncRunner:
             except (ValueError, _lib.FtError):
                 persistent = False
         import ctypes
-        if not 2 <= len(pipes) <= 8:
-            raise ValueError("AsyncRunner takes 2..8 identically shaped pipelines")
+        if not 2 <= len(pipes) <= 16:
+            raise ValueError("AsyncRunner takes 2..16 identically shaped pipelines")
         a = pipes[0]
         for b in pipes[1:]:
             if (a.S, a.cap_kp, a.cap_pts, a.in_end, a.out_begin, a.out_end) != \
@@ -700,6 +729,21 @@ class AsyncRunner:
             lo, hi = int(rng[0]), int(rng[1])
             st = self.lib.ft_runner_submit_range(self._r, k, src, lo, hi - lo)
         _lib.check(st, "ft_runner_submit")
+
+    def submit_batch(self, k: int, rows: torch.Tensor, rng) -> None:
+        """Enqueue steps k .. k+m-1 whose inputs are the m rows of one pinned
+        [m, >= in_end] tensor view (e.g. staging_ring(n)[j:j+m]), the same
+        ranges (ranges_arg()) for each.  On persistent pipelines that share a
+        DeviceArena each range goes up as one strided copy for all m steps
+        (ft_runner_submit_batch); otherwise step by step."""
+        m = int(rows.shape[0])
+        pitch = int(rows.stride(0)) if m > 1 else 0
+        if not isinstance(rng, _Ranges):
+            rng = _Ranges(rng)
+        st = self.lib.ft_runner_submit_batch(self._r, k, m, rows.data_ptr(), pitch,
+                                             rng.flat, rng.n)
+        if st:
+            _lib.check(st, "ft_runner_submit_batch")
 
     @staticmethod
     def ranges_arg(rng) -> "_Ranges":

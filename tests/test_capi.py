@@ -95,6 +95,7 @@ def test_new_entries_validate_without_gpu():
     assert L.ft_runner_submit(None, 0, None) == -1
     assert L.ft_runner_submit_range(None, 0, None, 0, 0) == -1
     assert L.ft_runner_submit_ranges(None, 0, None, None, 0) == -1
+    assert L.ft_runner_submit_batch(None, 0, 2, None, 0, None, 0) == -1
     assert L.ft_runner_wait(None, 0) == -1
     assert L.ft_runner_destroy(None) == 0
     # persistent runner / plans / resident ring

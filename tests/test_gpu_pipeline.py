@@ -530,6 +530,60 @@ def test_persistent_runner_groups(workloads, expected, groups):
 
 
 @pytest.mark.timeout(180)
+@pytest.mark.parametrize("arena,m,groups", [(True, 2, 1), (True, 4, 2), (True, 4, 1),
+                                            (False, 2, 1)])
+def test_persistent_runner_batched_submit(workloads, expected, arena, m, groups):
+    """submit_batch: m consecutive steps per call.  With the slots in one
+    DeviceArena each range is one strided 2D copy for all m steps
+    (ft_runner_submit_batch); without it, step-by-step copies.  Every step
+    equals the oracle either way (each step is still its own frame)."""
+    from paper_2509_10757_b200.pipeline import AsyncRunner, DeviceArena, FramePipeline
+    w0 = workloads[0]
+    cap_kp = max(max(len(w.left.u), len(w.right.u)) for w in workloads)
+    ar = DeviceArena(4) if arena else None
+    pipes = [FramePipeline(w0.cam, n_streams=1, cap_kp=(cap_kp + 31) // 32 * 32,
+                           cap_points=5120, pyramid_geometry=w0.pyr_left, arena=ar)
+             for _ in range(4)]
+    if arena:
+        pitch = pipes[1].dev.data_ptr() - pipes[0].dev.data_ptr()
+        assert pitch > 0 and all(p.dev.data_ptr() == pipes[0].dev.data_ptr() + j * pitch
+                                 for j, p in enumerate(pipes))
+    ring = pipes[0].staging_ring(4)
+    for k in range(4):
+        w = workloads[k]
+        pipes[0].load_frame(0, w.left, w.right, w.local, w.pose, w.pyr_left, w.pyr_right,
+                            slots=expected[k][1])
+        pipes[0].stage_into(ring[k])
+    full = [(0, pipes[0].in_end)]  # one range for every step of a batch
+    for p in pipes:
+        p.dev.fill_(0xAB)
+    runner = AsyncRunner(pipes, persistent=True, groups=groups)
+
+    def check(pipe, k):
+        w = workloads[k % 4]
+        mt, _, slots, n = expected[k % 4]
+        res = pipe.result(0, len(w.left.u))
+        for f in FIELDS:
+            np.testing.assert_array_equal(getattr(res.matches, f), getattr(mt, f),
+                                          err_msg=f"step {k} {f}")
+        np.testing.assert_array_equal(res.slots, slots, err_msg=f"step {k}")
+        assert res.n_slots == n
+
+    try:
+        n_steps, k = 40, 0
+        while k < n_steps:
+            for j in range(k - 4, k + m - 4):  # results about to be overwritten
+                if j >= 0:
+                    check(runner.wait(j), j)
+            runner.submit_batch(k, ring[k % 4:k % 4 + m], full)
+            k += m
+        for j in range(n_steps - 4, n_steps):
+            check(runner.wait(j), j)
+    finally:
+        runner.close()
+
+
+@pytest.mark.timeout(180)
 def test_tail_blocks_per_launch(workloads, expected, monkeypatch):
     """The dedicated stereo-tail / map-resolve blocks (persistent plans' mode)
     forced on ordinary launches: same results as the group-barrier path."""
