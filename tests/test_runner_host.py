@@ -34,3 +34,30 @@ def test_runner_submit_checks_without_gpu():
     flat = (ctypes.c_uint64 * 2)(8, 4)
     assert L.ft_runner_submit_ranges(None, 0, ctypes.c_void_p(16), flat, 1) == -1
     assert L.ft_runner_wait(None, -1) == -1
+
+
+def test_device_arena_rows_at_one_pitch():
+    """DeviceArena (batched submits' slot layout): rows 2 MB aligned at one
+    2 MB-multiple pitch; a different size or one row too many is refused.
+    Host tensors stand in for device memory (the layout logic is the same)."""
+    from paper_2509_10757_b200.pipeline import DeviceArena
+    a = DeviceArena(3)
+    rows = [a.take(3_000_000, "cpu") for _ in range(3)]
+    assert a.pitch == 4 << 20
+    base = rows[0].data_ptr()
+    assert base % (2 << 20) == 0
+    assert [r.data_ptr() - base for r in rows] == [0, a.pitch, 2 * a.pitch]
+    assert all(r.numel() == 3_000_000 for r in rows)
+    with pytest.raises(ValueError):
+        a.take(3_000_000, "cpu")  # all rows taken
+    b = DeviceArena(2)
+    b.take(100, "cpu")
+    with pytest.raises(ValueError):
+        b.take(5 << 20, "cpu")  # another pitch
+
+
+def test_runner_submit_batch_checks_without_gpu():
+    L = _lib.load()
+    flat = (ctypes.c_uint64 * 2)(0, 16)
+    assert L.ft_runner_submit_batch(None, 0, 2, ctypes.c_void_p(16), 64, flat, 1) == -1
+    assert L.ft_runner_submit_batch(None, 0, 2, None, 64, flat, 1) == -1
