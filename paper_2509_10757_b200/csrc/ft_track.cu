@@ -2212,6 +2212,7 @@ struct PersistArgs {
     unsigned max_steps;     // the launch ends after this many steps (or at a stop)
     int gate;               // step k waits for the slot's step k - n to be done (ring)
     int red_arrive;         // arrivals by reduction; the last block publishes done
+    unsigned poll_ns;       // PCIe watcher: sleep between polls of the host-mapped ready word
     const unsigned *ready;  // [n] host-mapped: step + 1 whose inputs are in the slot
     unsigned *dready;       // [n] device copy of ready (forwarded by block 0)
     unsigned *done;         // [n] host-mapped: step + 1 whose outputs are complete
@@ -2312,7 +2313,7 @@ __global__ void __launch_bounds__(TK_THREADS) track_persist_kernel(const __grid_
                 // (the runner's host ordering already implies that the slot's
                 // previous step k - n is complete)
                 while ((v = ld_acquire_sys_u32(p.ready + i)) != FT_PERSIST_STOP && v < k + 1)
-                    __nanosleep(100);
+                    __nanosleep(p.poll_ns);
                 // forward exactly this step (the host word may already allow later ones)
                 const unsigned fwd = v == FT_PERSIST_STOP ? v : k + 1;
                 asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.dready + i), "r"(fwd)
@@ -3038,6 +3039,10 @@ static int persist_launch(const void *const *plans, int n, TrackArgs *args_dev,
     p.max_steps = max_steps;
     p.gate = gate;
     p.red_arrive = getenv("FT_PERSIST_ATOMIC_ARRIVE") ? 0 : 1;
+    {
+        const char *ev = getenv("FT_PERSIST_POLL_NS");
+        p.poll_ns = ev ? (unsigned)atoi(ev) : 100u;
+    }
     static unsigned long long *ts_buf = nullptr;
     if (getenv("FT_DEBUG_PERSIST")) {
         if (!ts_buf) cudaMalloc(&ts_buf, 4096 * 2 * 8);
